@@ -1,0 +1,96 @@
+"""Generates the golden fixtures in tests/golden/ from the UNMODIFIED reference.
+
+Run here (where /root/reference exists):  python tests/golden/make_golden.py
+It builds oracle/_ref/ref_tool (oracle/Makefile `ref`: reference sources compiled where they lie,
+plus the builder env synth17x6 registered by link-time wrapping) and records, per case:
+  trace_<case>.npz : Interp::whole phase-by-phase tensors (the DP-D k=1 unit)
+  run_<case>.npz   : run_plan_local under dp-d with k replicas (episode rewards, final params)
+The fixtures are small enough to commit; the GPU box never needs /root/reference.
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+from oracle import pyoracle  # noqa: E402
+
+# name -> (algo config, seed)
+TRACE_CASES = {
+    "ppo_gridline": ({"algorithm": "ppo", "env": {"type": "gridline", "num": 6, "params": {"length": 8}},
+                      "policy_net": {"hidden": [8, 8]}, "loop": {"episodes": 3, "steps_per_episode": 8}}, 5),
+    "ppo_gridline_relu": ({"algorithm": "ppo", "env": {"type": "gridline", "num": 5, "params": {"length": 6}},
+                           "learner": {"params": {"normalize_adv": False, "lr": 0.01}},
+                           "policy_net": {"hidden": [8], "activation": "relu"},
+                           "loop": {"episodes": 2, "steps_per_episode": 7}}, 11),
+    "ppo_synth7": ({"algorithm": "ppo", "env": {"type": "synth17x6", "num": 8},
+                    "policy_net": {"hidden": [16, 16, 16, 16, 16, 16]},
+                    "loop": {"episodes": 2, "steps_per_episode": 8}}, 7),
+    "ppo_synth_maxsteps": ({"algorithm": "ppo", "env": {"type": "synth17x6", "num": 6, "params": {"max_steps": 5}},
+                            "learner": {"params": {"gamma": 0.99, "lam": 0.9, "clip_eps": 0.1, "train_iters": 3}},
+                            "policy_net": {"hidden": [12, 12]}, "loop": {"episodes": 2, "steps_per_episode": 8}}, 3),
+    "a3c_gridline": ({"algorithm": "a3c", "actor": {"num": 4}, "env": {"type": "gridline", "num": 4},
+                      "policy_net": {"hidden": [8, 8]}, "loop": {"episodes": 2, "steps_per_episode": 8}}, 9),
+    "mappo_spread3": ({"algorithm": "mappo", "agent": {"num": 3}, "env": {"type": "spread_lite", "num": 4,
+                                                                          "params": {"accel": 1}},
+                       "policy_net": {"hidden": [8, 8]}, "loop": {"episodes": 2, "steps_per_episode": 6}}, 13),
+}
+
+# name -> (algo config, seed, dp-d replicas k)
+RUN_CASES = {
+    "dpd_k1_synth": (TRACE_CASES["ppo_synth7"][0] | {"loop": {"episodes": 3, "steps_per_episode": 8}}, 7, 1),
+    "dpd_k2_synth": ({"algorithm": "ppo", "actor": {"num": 2}, "env": {"type": "synth17x6", "num": 10},
+                      "policy_net": {"hidden": [16, 16]}, "loop": {"episodes": 3, "steps_per_episode": 8}}, 21, 2),
+    "dpd_k3_gridline": ({"algorithm": "ppo", "actor": {"num": 3}, "env": {"type": "gridline", "num": 10},
+                         "policy_net": {"hidden": [8, 8]}, "loop": {"episodes": 3, "steps_per_episode": 8}}, 4, 3),
+    "dpd_a3c_k4": ({"algorithm": "a3c", "actor": {"num": 4}, "env": {"type": "gridline", "num": 4},
+                    "policy_net": {"hidden": [8, 8]}, "loop": {"episodes": 3, "steps_per_episode": 8}}, 2, 4),
+}
+
+
+def build_ref():
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
+
+
+def main():
+    build_ref()
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, (algo, seed) in TRACE_CASES.items():
+            ap = os.path.join(tmp, name + ".json")
+            json.dump(algo, open(ap, "w"))
+            prefix = os.path.join(tmp, name)
+            subprocess.run([pyoracle.REF_TOOL, "trace", ap, str(seed), prefix], check=True)
+            tr = pyoracle.load_trace(prefix)
+            np.savez_compressed(os.path.join(HERE, f"trace_{name}.npz"),
+                                __algo__=np.array(json.dumps(algo)), __seed__=np.array(seed),
+                                **{k.replace("/", "__"): v for k, v in tr.items()})
+            print("trace", name, len(tr), "tensors")
+        for name, (algo, seed, k) in RUN_CASES.items():
+            algo = dict(algo)
+            algo["actor"] = {"num": k}
+            ap = os.path.join(tmp, name + ".json")
+            dp = os.path.join(tmp, name + "_deploy.json")
+            json.dump(algo, open(ap, "w"))
+            json.dump({"workers": ["local"], "slots_per_worker": {"cpu": 16, "accel": 16},
+                       "distribution_policy": "dp-d"}, open(dp, "w"))
+            out = subprocess.run([pyoracle.REF_TOOL, "run", ap, dp, str(seed), "--params"], check=True,
+                                 capture_output=True, text=True).stdout
+            r = json.loads(out)
+            np.savez_compressed(os.path.join(HERE, f"run_{name}.npz"),
+                                __algo__=np.array(json.dumps(algo)), __seed__=np.array(seed), k=np.array(k),
+                                rewards=np.array([e["reward"] for e in r["episodes"]]),
+                                final_params=np.array(r["final_params"]), steps=np.array(r["steps"]),
+                                grad_messages=np.array(r["grad_messages"]),
+                                bytes_total=np.array([e["bytes_total"] for e in r["episodes"]]))
+            print("run", name, r["units"], "units", r["steps"], "steps")
+
+
+if __name__ == "__main__":
+    main()

@@ -22,6 +22,7 @@
 #include <thread>
 #include <vector>
 
+#include "../include/fraglow.h"
 #include "config.hpp"
 #include "fdgc/fdg.hpp"
 #include "plan/plan.hpp"
@@ -183,10 +184,40 @@ int run_cmd(const std::string& algo_path, const std::string& deploy_path, uint64
     return 0;
 }
 
+// ref_tool plan <algo.json> <deploy.json>: the reference C API's view of a program
+// (flw_program_create / flw_program_dump(PLAN) / flw_validate_plan, capi.cpp:207-247).
+int plan_cmd(const std::string& algo_path, const std::string& deploy_path) {
+    std::string a = slurp(algo_path), d = slurp(deploy_path);
+    flw_program* p = nullptr;
+    int rc = flw_program_create(a.c_str(), d.c_str(), &p);
+    std::cout << "{\"rc\": " << rc;
+    if (rc != 0) {
+        std::string err = flw_last_error();
+        std::string esc;
+        for (char c : err) {
+            if (c == '"' || c == '\\') esc += '\\';
+            esc += c;
+        }
+        std::cout << ", \"error\": \"" << esc << "\"}\n";
+        return 0;
+    }
+    char* plan = nullptr;
+    char* report = nullptr;
+    int nv = 0;
+    flw_program_dump(p, FLW_DUMP_PLAN, &plan);
+    flw_validate_plan(p, &report, &nv);
+    std::cout << ", \"plan\": " << plan << ", \"violations\": " << report << "}\n";
+    flw_string_free(plan);
+    flw_string_free(report);
+    flw_program_destroy(p);
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     try {
+        if (argc >= 4 && std::string(argv[1]) == "plan") return plan_cmd(argv[2], argv[3]);
         if (argc >= 5 && std::string(argv[1]) == "trace")
             return trace(argv[2], std::stoull(argv[3]), argv[4]);
         if (argc >= 5 && std::string(argv[1]) == "run") {

@@ -1,0 +1,437 @@
+// C-ABI of libfraglow_b200.so (include/fraglow_b200.h): the reference's public API for the
+// DP-D path plus the per-unit engine seam. Conventions follow /root/reference/proj/src/capi.cpp:
+// guarded() maps exceptions to codes, thread-local last error, malloc'd out strings.
+#include <cuda_runtime.h>
+
+#include <barrier>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <thread>
+
+#include "../../include/fraglow_b200.h"
+#include "comm.hpp"
+#include "common.cuh"
+#include "config.hpp"
+#include "engine.hpp"
+#include "nlohmann/json.hpp"
+
+using namespace flw;
+
+struct flw_program {
+    AlgoConfig algo;
+    DeployConfig deploy;
+    Plan plan;
+    Numerics numerics = Numerics::Exact;
+    // Engines persist across flw_run_local calls on the same program (re-initialised per run):
+    // device buffers and the captured episode graph are set up once.
+    std::vector<std::unique_ptr<Engine>> engines;
+    bool unpartitioned_engines = false;
+    std::mutex mu;
+};
+
+struct flw_dpd {
+    std::unique_ptr<Engine> engine;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const Error& e) {
+        g_last_error = std::string(errc_name(e.code())) + ": " + e.what();
+        return c_code(e.code());
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FLW_ERR_RUNTIME;
+    }
+}
+
+char* dup_string(const std::string& s) {
+    char* out = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return out;
+}
+
+Numerics numerics_from(const std::string& s) {
+    if (s == "exact") return Numerics::Exact;
+    if (s == "fast") return Numerics::Fast;
+    fail(Errc::Config, "numerics must be 'exact' or 'fast'");
+}
+
+struct EpisodeMetrics {
+    double wall_ms = 0.0, reward = 0.0;
+    int64_t bytes_total = 0;
+};
+
+// capi.cpp:74-113 summary schema.
+std::string summarize(const std::vector<EpisodeMetrics>& eps, int64_t steps, const std::vector<double>& params,
+                      int64_t grad_bytes_total, const flw_run_options* opts) {
+    nlohmann::ordered_json j;
+    j["episodes"] = eps.size();
+    j["steps"] = steps;
+    j["grad_messages"] = 0;  // DP-D has no async gradient pushes (local_run.cpp:447-456)
+    j["final_reward"] = eps.empty() ? 0.0 : eps.back().reward;
+    double total_ms = 0.0;
+    for (const auto& e : eps) total_ms += e.wall_ms;
+    j["total_wall_ms"] = total_ms;
+    j["bytes_total"] = grad_bytes_total;
+    nlohmann::ordered_json per = nlohmann::ordered_json::object();
+    if (grad_bytes_total > 0) per["0"] = grad_bytes_total;
+    j["bytes_per_channel"] = per;
+    double sum = 0.0, sumsq = 0.0;
+    for (double v : params) {
+        sum += v;
+        sumsq += v * v;
+    }
+    j["param_count"] = params.size();
+    j["param_checksum"] = sum;
+    j["param_l2"] = std::sqrt(sumsq);
+    if (opts && opts->reward_threshold >= 0.0) {
+        double t = -1.0, acc = 0.0;
+        for (const auto& e : eps) {
+            acc += e.wall_ms;
+            if (e.reward >= opts->reward_threshold) {
+                t = acc;
+                break;
+            }
+        }
+        j["reward_threshold"] = opts->reward_threshold;
+        j["time_to_threshold_ms"] = t;
+    }
+    return j.dump(2);
+}
+
+std::string to_csv(const std::vector<EpisodeMetrics>& eps) {  // local_run.cpp:503-510
+    std::ostringstream os;
+    os << "episode,wall_ms,reward,bytes_total\n";
+    for (size_t i = 0; i < eps.size(); ++i)
+        os << i << "," << eps[i].wall_ms << "," << eps[i].reward << "," << eps[i].bytes_total << "\n";
+    return os.str();
+}
+
+// run_plan_local (local_run.cpp:512-581) for a DP-D plan: one host thread per unit, each unit
+// on its own GPU, an episode lockstep gate driven by this thread, wall_ms per episode.
+void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeMetrics>& eps, int64_t& steps,
+               std::vector<double>& final_params, int64_t& grad_bytes) {
+    std::lock_guard<std::mutex> lk(p.mu);
+    const uint64_t seed = opts ? opts->seed : 0;
+    const int64_t episodes = opts && opts->episodes > 0 ? opts->episodes : p.algo.episodes;
+    const bool unpart = opts && opts->unpartitioned;
+    std::vector<Unit> units = p.plan.units;
+    if (unpart) units = {Unit{0, 0, 0, 0, p.algo.envs}};
+    const int k = static_cast<int>(units.size());
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+        fail(Errc::Runtime, "no CUDA device visible: the DP-D engine has no CPU fallback");
+    if (k > ndev)
+        fail(Errc::InsufficientSlots, "dp-d plan has " + std::to_string(k) + " units but only " +
+                                          std::to_string(ndev) + " GPUs are visible (one accel slot = one GPU)");
+    bool reuse = static_cast<int>(p.engines.size()) == k && p.unpartitioned_engines == unpart;
+    if (!reuse) {
+        p.engines.clear();
+        for (const Unit& u : units)
+            p.engines.push_back(std::make_unique<Engine>(p.algo, u.id, seed, u.env_lo, u.env_hi, p.algo.envs,
+                                                         p.numerics));
+        p.unpartitioned_engines = unpart;
+        if (k > 1) {
+            std::vector<int> devs;
+            for (const Unit& u : units) devs.push_back(u.id);
+            auto comms = Comm::init_all(devs);
+            for (int r = 0; r < k; ++r) p.engines[r]->set_comm(std::make_unique<Comm>(comms[r], r, k));
+        }
+    } else {
+        for (auto& e : p.engines) e->reinit(seed);
+    }
+    eps.assign(static_cast<size_t>(episodes), {});
+    std::vector<std::vector<double>> rsum(static_cast<size_t>(k), std::vector<double>(episodes, 0.0));
+    const ProgramShape& s = p.engines[0]->shape();
+    // Reference byte accounting of the GradSync channel: k(k-1) legs x learn iters x (14 + 8P).
+    const int64_t per_ep_bytes = k > 1 ? static_cast<int64_t>(k) * (k - 1) * s.learn_iters * (14 + 8 * s.P) : 0;
+    std::mutex err_mu;
+    std::string first_error;
+    if (k == 1) {
+        for (int64_t ep = 0; ep < episodes; ++ep) {
+            auto t0 = std::chrono::steady_clock::now();
+            rsum[0][static_cast<size_t>(ep)] = p.engines[0]->run_episode(ep);
+            auto t1 = std::chrono::steady_clock::now();
+            eps[static_cast<size_t>(ep)].wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        }
+    } else {
+        std::barrier gate(k + 1);
+        std::vector<std::thread> threads;
+        for (int r = 0; r < k; ++r)
+            threads.emplace_back([&, r] {
+                for (int64_t ep = 0; ep < episodes; ++ep) {
+                    gate.arrive_and_wait();  // raise_gate(ep)
+                    try {
+                        if (first_error.empty()) rsum[r][static_cast<size_t>(ep)] = p.engines[r]->run_episode(ep);
+                    } catch (const std::exception& e) {
+                        std::lock_guard<std::mutex> g(err_mu);
+                        if (first_error.empty()) first_error = "unit " + std::to_string(r) + ": " + e.what();
+                    }
+                    gate.arrive_and_wait();  // on_episode_done
+                }
+            });
+        for (int64_t ep = 0; ep < episodes; ++ep) {
+            auto t0 = std::chrono::steady_clock::now();
+            gate.arrive_and_wait();
+            gate.arrive_and_wait();
+            auto t1 = std::chrono::steady_clock::now();
+            eps[static_cast<size_t>(ep)].wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        }
+        for (auto& t : threads) t.join();
+        if (!first_error.empty()) fail(Errc::Runtime, first_error);
+    }
+    for (int64_t ep = 0; ep < episodes; ++ep) {  // local_run.cpp:560-570
+        double sum = 0.0;
+        for (int r = 0; r < k; ++r) sum += rsum[r][static_cast<size_t>(ep)];
+        eps[static_cast<size_t>(ep)].reward = sum / static_cast<double>(p.algo.envs);
+        eps[static_cast<size_t>(ep)].bytes_total = per_ep_bytes;
+    }
+    steps = 0;
+    for (auto& e : p.engines) steps += e->steps_executed();
+    final_params.assign(static_cast<size_t>(s.P), 0.0);
+    p.engines[0]->get_params(final_params.data());
+    grad_bytes = per_ep_bytes * episodes;
+}
+
+Engine& eng(flw_dpd* e) {
+    if (!e || !e->engine) fail(Errc::Config, "null engine handle");
+    return *e->engine;
+}
+
+}  // namespace
+
+extern "C" {
+
+int flw_program_create(const char* algo_json, const char* deploy_json, flw_program** out) {
+    return guarded([&] {
+        auto p = std::make_unique<flw_program>();
+        p->algo = parse_algo_config(algo_json ? algo_json : "{}");
+        if (deploy_json && *deploy_json) {
+            p->deploy = parse_deploy_config(deploy_json);
+            auto j = nlohmann::json::parse(deploy_json);
+            if (j.contains("numerics")) p->numerics = numerics_from(j["numerics"].get<std::string>());
+        } else {
+            p->deploy = DeployConfig{{"local"}, 8, 8, Policy::DpA};  // capi.cpp:211-212 default
+        }
+        if (const char* env = std::getenv("FLW_NUMERICS")) p->numerics = numerics_from(env);
+        p->plan = make_dpd_plan(p->algo, p->deploy);
+        *out = p.release();
+        return FLW_OK;
+    });
+}
+
+void flw_program_destroy(flw_program* p) { delete p; }
+
+int flw_program_dump(const flw_program* p, int what, char** out_text) {
+    return guarded([&] {
+        if (what != FLW_DUMP_PLAN)
+            fail(Errc::Config, "the DP-D engine serves FLW_DUMP_PLAN only (the DFG/FDG are the reference's)");
+        *out_text = dup_string(p->plan.to_json());
+        return FLW_OK;
+    });
+}
+
+int flw_validate_plan(const flw_program* p, char** out_report, int* n_violations) {
+    return guarded([&] {
+        auto v = p->plan.violations();
+        nlohmann::ordered_json j = nlohmann::ordered_json::array();
+        for (const auto& [code, msg] : v) j.push_back({{"code", code}, {"message", msg}});
+        if (out_report) *out_report = dup_string(j.dump(2));
+        if (n_violations) *n_violations = static_cast<int>(v.size());
+        return FLW_OK;
+    });
+}
+
+int flw_run_local(const flw_program* p, const flw_run_options* opts, char** metrics_csv, char** summary_json) {
+    return guarded([&] {
+        std::vector<EpisodeMetrics> eps;
+        int64_t steps = 0, bytes = 0;
+        std::vector<double> params;
+        run_local(*const_cast<flw_program*>(p), opts, eps, steps, params, bytes);
+        if (metrics_csv) *metrics_csv = dup_string(to_csv(eps));
+        if (summary_json) *summary_json = dup_string(summarize(eps, steps, params, bytes, opts));
+        return FLW_OK;
+    });
+}
+
+void flw_string_free(char* s) { std::free(s); }
+
+const char* flw_last_error(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------------------ engine seam
+int flw_dpd_create(const char* algo_json, int device, uint64_t seed, int64_t env_lo, int64_t env_hi,
+                   int64_t env_total, int numerics, flw_dpd** out) {
+    return guarded([&] {
+        AlgoConfig a = parse_algo_config(algo_json ? algo_json : "{}");
+        if (numerics != FLW_NUMERICS_EXACT && numerics != FLW_NUMERICS_FAST) fail(Errc::Config, "bad numerics");
+        auto h = std::make_unique<flw_dpd>();
+        h->engine = std::make_unique<Engine>(a, device, seed, env_lo, env_hi, env_total, static_cast<Numerics>(numerics));
+        *out = h.release();
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_destroy(flw_dpd* e) {
+    return guarded([&] {
+        delete e;
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_comm_unique_id(char* out_id, int64_t cap) {
+    return guarded([&] {
+        std::string id = Comm::new_unique_id();
+        if (cap < static_cast<int64_t>(id.size())) fail(Errc::Config, "unique id buffer too small");
+        std::memcpy(out_id, id.data(), id.size());
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_comm_init(flw_dpd* e, const char* id, int64_t id_len, int rank, int nranks) {
+    return guarded([&] {
+        Engine& en = eng(e);
+        en.set_comm(std::make_unique<Comm>(std::string(id, static_cast<size_t>(id_len)), rank, nranks, en.device()));
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_run_episode(flw_dpd* e, int64_t episode, double* reward_sum, float* device_ms) {
+    return guarded([&] {
+        double r = eng(e).run_episode(episode, device_ms);
+        if (reward_sum) *reward_sum = r;
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_run_episodes(flw_dpd* e, int64_t first_episode, int64_t count, float* device_ms) {
+    return guarded([&] {
+        Engine& en = eng(e);
+        cudaEvent_t a, b;
+        FLW_CUDA(cudaSetDevice(en.device()));
+        FLW_CUDA(cudaEventCreate(&a));
+        FLW_CUDA(cudaEventCreate(&b));
+        FLW_CUDA(cudaEventRecord(a, en.stream()));
+        en.enqueue_episodes(first_episode, count);
+        FLW_CUDA(cudaEventRecord(b, en.stream()));
+        FLW_CUDA(cudaEventSynchronize(b));
+        float ms = 0.0f;
+        FLW_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        if (device_ms) *device_ms = ms;
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_reinit(flw_dpd* e, uint64_t seed) {
+    return guarded([&] {
+        eng(e).reinit(seed);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_param_count(const flw_dpd* e, int64_t* n) {
+    return guarded([&] {
+        *n = eng(const_cast<flw_dpd*>(e)).param_count();
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_get_params(flw_dpd* e, double* out, int64_t n) {
+    return guarded([&] {
+        if (n != eng(e).param_count()) fail(Errc::Shape, "param count mismatch");
+        eng(e).get_params(out);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_set_params(flw_dpd* e, const double* in, int64_t n) {
+    return guarded([&] {
+        if (n != eng(e).param_count()) fail(Errc::Shape, "param count mismatch");
+        eng(e).set_params(in);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_stats(const flw_dpd* e, int64_t* steps, int64_t* env_count, int64_t* learn_iters, int64_t* graph_kernels) {
+    return guarded([&] {
+        Engine& en = eng(const_cast<flw_dpd*>(e));
+        if (steps) *steps = en.steps_executed();
+        if (env_count) *env_count = en.env_count();
+        if (learn_iters) *learn_iters = en.learn_iters();
+        if (graph_kernels) *graph_kernels = en.graph_kernel_nodes();
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_reset(flw_dpd* e, int64_t episode) {
+    return guarded([&] {
+        eng(e).reset(episode);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_step(flw_dpd* e, int64_t episode, int64_t step) {
+    return guarded([&] {
+        eng(e).step(episode, step);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_learn(flw_dpd* e, int64_t episode, int64_t iter) {
+    return guarded([&] {
+        eng(e).learn(episode, iter);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_learn_grads(flw_dpd* e, int64_t episode, int64_t iter) {
+    return guarded([&] {
+        eng(e).learn_grads(episode, iter);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_apply_grads(flw_dpd* e, const double* grads, int64_t n) {
+    return guarded([&] {
+        if (grads && n != eng(e).param_count()) fail(Errc::Shape, "gradient length mismatch");
+        eng(e).apply_grads(grads);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_tensor_size(const flw_dpd* e, const char* name, int64_t* n) {
+    return guarded([&] {
+        *n = eng(const_cast<flw_dpd*>(e)).tensor_size(name);
+        if (*n < 0) fail(Errc::Config, std::string("unknown tensor '") + name + "'");
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_read(flw_dpd* e, const char* name, double* out, int64_t n) {
+    return guarded([&] {
+        if (n != eng(e).tensor_size(name)) fail(Errc::Shape, std::string("size mismatch for '") + name + "'");
+        eng(e).read_tensor(name, out);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_write(flw_dpd* e, const char* name, const double* in, int64_t n) {
+    return guarded([&] {
+        eng(e).write_tensor(name, in, n);
+        return FLW_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,622 @@
+// DP-D unit engine: buffer layout, phase sequencing and per-episode CUDA graph.
+//
+// HBM layout for one unit with E envs, T steps, obs width S (PPO/A3C):
+//   states  f32 [(T+1), E, S]   block t = policy input of step t (== trajectory state column);
+//                               block T = the last step's next obs (last_next, programs.cpp:240)
+//   actions i32 [T, E], logp/reward/done f32 [T, E], reward_d f64 [T, E]  (t-major == the
+//                               reference's BufferSample row order t*E + e, interp.cpp:297-301)
+//   est     f64 [sw, E]         env state, structure-of-arrays
+//   H/DZ    f32 [T*E, width]    learn-phase activations / adjoints per layer and net
+//   params  f32 [P], m/v f64 [P], grads f32 [P]   flat, reference parameter order
+#include "engine.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "comm.hpp"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace flw {
+
+struct Engine::Bufs {
+    DeviceCtx* ctx = nullptr;
+    double2* bc_table = nullptr;
+    int64_t bc_len = 0;
+    float* params = nullptr;
+    double *m = nullptr, *v = nullptr;
+    float* grads = nullptr;
+    float* gather = nullptr;
+    double* gmean = nullptr;
+    double* est = nullptr;
+    uint8_t* done = nullptr;
+    int32_t* stepc = nullptr;
+    float* states = nullptr;
+    float *act0 = nullptr, *act1 = nullptr, *logits = nullptr;
+    int32_t* actions = nullptr;
+    float *logp = nullptr, *rew = nullptr, *done_f = nullptr;
+    double* rew_d = nullptr;
+    std::vector<float*> Hp, Hc, Hl, DZp, DZc;
+    double* adv_d = nullptr;
+    float *adv = nullptr, *ret = nullptr;
+    double* terms = nullptr;
+    double* stats = nullptr;
+    float* loss = nullptr;
+    double* rsum = nullptr;
+    double* synth_b = nullptr;
+    DwTile* tiles = nullptr;
+    int ntiles = 0;
+    std::vector<void*> owned;
+
+    template <typename T>
+    T* alloc(int64_t n) {
+        void* p = nullptr;
+        FLW_CUDA(cudaMalloc(&p, static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T)));
+        FLW_CUDA(cudaMemset(p, 0, static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T)));
+        owned.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~Bufs() {
+        for (void* p : owned) cudaFree(p);
+    }
+};
+
+namespace {
+
+EnvParams env_params(const AlgoConfig& c, const ProgramShape& s, const double* synth_b) {
+    EnvParams p{};
+    p.synth_b = synth_b;
+    p.kind = static_cast<int>(s.env);
+    p.n_agents = s.n_agents;
+    p.max_steps = static_cast<int64_t>(c.env_param("max_steps", 0));
+    p.length = static_cast<int64_t>(c.env_param("length", 8));  // envs.cpp:24,27
+    return p;
+}
+
+int act_of(const AlgoConfig& c) { return c.activation == "relu" ? kRelu : kTanh; }
+
+}  // namespace
+
+Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo, int64_t env_hi, int64_t env_total,
+               Numerics numerics)
+    : cfg_(cfg), device_(device), seed_(seed), lo_(env_lo), hi_(env_hi), etot_(env_total), numerics_(numerics) {
+    cfg_.validate();
+    shape_ = program_shape(cfg_);
+    if (!shape_.accel_capable)
+        fail(Errc::PolicyInapplicable, "dp-d requires an accelerator-capable environment implementation");
+    if (shape_.algo == Algo::Mappo)
+        fail(Errc::PolicyInapplicable, "MAPPO is not served by this engine build (PPO and A3C are)");
+    if (env_hi <= env_lo || env_lo < 0 || env_hi > env_total) fail(Errc::Config, "bad env range");
+    if (shape_.n_actions > 16) fail(Errc::Config, "at most 16 discrete actions are supported");
+    E_ = env_hi - env_lo;
+    R_ = static_cast<int64_t>(shape_.n_agents) * E_;
+    T_ = cfg_.steps_per_episode;
+    TR_ = T_ * R_;
+    FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    FLW_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    FLW_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    FLW_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    FLW_CUDA(cudaEventCreate(&ev_t0_));
+    FLW_CUDA(cudaEventCreate(&ev_t1_));
+    alloc();
+    init_params();
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    if (graph_) cudaGraphExecDestroy(graph_);
+    comm_.reset();
+    b_.reset();
+    for (cudaEvent_t e : {ev_fork_, ev_join_, ev_t0_, ev_t1_})
+        if (e) cudaEventDestroy(e);
+    if (side_) cudaStreamDestroy(side_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::set_comm(std::unique_ptr<Comm> comm) {
+    if (graph_) {
+        cudaGraphExecDestroy(graph_);
+        graph_ = nullptr;
+    }
+    comm_ = std::move(comm);
+    if (comm_ && numerics_ == Numerics::Exact && !b_->gather) {
+        b_->gather = b_->alloc<float>(static_cast<int64_t>(comm_->nranks()) * shape_.P);
+    }
+}
+
+void Engine::alloc() {
+    b_ = std::make_unique<Bufs>();
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    const int S = s.obs_dim, A = s.n_actions, L = s.L;
+    b.ctx = b.alloc<DeviceCtx>(1);
+    // Adam bias-correction table 1 - beta^t computed with the host libm pow, the reference's
+    // arithmetic (mlp.cpp:485-486), for every step this run can take (+ slack).
+    b.bc_len = std::max<int64_t>(4096, (cfg_.episodes + 16) * s.learn_iters);
+    {
+        std::vector<double2> tab(static_cast<size_t>(b.bc_len));
+        for (int64_t t = 1; t <= b.bc_len; ++t) {
+            tab[static_cast<size_t>(t - 1)].x = 1.0 - std::pow(0.9, static_cast<double>(t));
+            tab[static_cast<size_t>(t - 1)].y = 1.0 - std::pow(0.999, static_cast<double>(t));
+        }
+        b.bc_table = b.alloc<double2>(b.bc_len);
+        FLW_CUDA(cudaMemcpy(b.bc_table, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    }
+    if (s.env == EnvKind::Synth17x6) {
+        double tab[kSynthAct * kSynthObs];
+        for (int a = 0; a < kSynthAct; ++a)
+            for (int i = 0; i < kSynthObs; ++i)
+                tab[a * kSynthObs + i] = rng_uniform_range(
+                    rng_key(kSynthTableSeed, static_cast<uint64_t>(a), static_cast<uint64_t>(i)), -1.0, 1.0);
+        b.synth_b = b.alloc<double>(kSynthAct * kSynthObs);
+        FLW_CUDA(cudaMemcpy(b.synth_b, tab, sizeof(tab), cudaMemcpyHostToDevice));
+    }
+    b.params = b.alloc<float>(s.P);
+    b.m = b.alloc<double>(s.P);
+    b.v = b.alloc<double>(s.P);
+    b.grads = b.alloc<float>(s.P);
+    b.gmean = b.alloc<double>(s.P);
+    b.est = b.alloc<double>(static_cast<int64_t>(s.env_state_w) * E_);
+    b.done = b.alloc<uint8_t>(E_);
+    b.stepc = b.alloc<int32_t>(E_);
+    b.states = b.alloc<float>((T_ + 1) * E_ * S);
+    int maxw = 0;
+    for (int d : s.pdims) maxw = std::max(maxw, d);
+    for (int d : s.cdims) maxw = std::max(maxw, d);
+    b.act0 = b.alloc<float>(E_ * maxw);
+    b.act1 = b.alloc<float>(E_ * maxw);
+    b.logits = b.alloc<float>(E_ * A);
+    b.actions = b.alloc<int32_t>(T_ * E_);
+    b.logp = b.alloc<float>(T_ * E_);
+    b.rew = b.alloc<float>(T_ * E_);
+    b.done_f = b.alloc<float>(T_ * E_);
+    b.rew_d = b.alloc<double>(T_ * E_);
+    for (int l = 0; l < L; ++l) {
+        b.Hp.push_back(b.alloc<float>(TR_ * s.pdims[l + 1]));
+        b.DZp.push_back(b.alloc<float>(TR_ * s.pdims[l + 1]));
+        b.Hc.push_back(b.alloc<float>(TR_ * s.cdims[l + 1]));
+        b.DZc.push_back(b.alloc<float>(TR_ * s.cdims[l + 1]));
+        b.Hl.push_back(b.alloc<float>(R_ * s.cdims[l + 1]));
+    }
+    b.adv_d = b.alloc<double>(TR_);
+    b.adv = b.alloc<float>(TR_);
+    b.ret = b.alloc<float>(TR_);
+    b.terms = b.alloc<double>(3 * TR_);
+    b.stats = b.alloc<double>(2);
+    b.loss = b.alloc<float>(1);
+    b.rsum = b.alloc<double>(1);
+    // dW tile table: every (net, layer) as 32(t, incl. the bias row t == K) x 32(j) tiles.
+    std::vector<DwTile> tiles;
+    for (int net = 0; net < 2; ++net) {
+        const auto& d = net == 0 ? s.pdims : s.cdims;
+        const auto& H = net == 0 ? b.Hp : b.Hc;
+        const auto& DZ = net == 0 ? b.DZp : b.DZc;
+        for (int l = 0; l < L; ++l) {
+            int K = d[l], N = d[l + 1];
+            for (int t0 = 0; t0 <= K; t0 += 32)
+                for (int j0 = 0; j0 < N; j0 += 32) {
+                    DwTile t{};
+                    t.H = l == 0 ? b.states : H[l - 1];
+                    t.DZ = DZ[l];
+                    t.gW = b.grads + s.woff[net][l];
+                    t.gB = b.grads + s.boff[net][l];
+                    t.K = K, t.N = N, t.t0 = t0, t.j0 = j0;
+                    tiles.push_back(t);
+                }
+        }
+    }
+    b.ntiles = static_cast<int>(tiles.size());
+    b.tiles = b.alloc<DwTile>(b.ntiles);
+    FLW_CUDA(cudaMemcpy(b.tiles, tiles.data(), tiles.size() * sizeof(DwTile), cudaMemcpyHostToDevice));
+}
+
+// Xavier-uniform weights keyed by (seed, param stream, node id, i), zero biases, rounded to
+// f32 (interp.cpp:71-85); node ids follow make_mlp_params order (programs.cpp:42-54).
+void Engine::init_params() {
+    const ProgramShape& s = shape_;
+    std::vector<float> p(static_cast<size_t>(s.P), 0.0f);
+    for (int net = 0; net < 2; ++net) {
+        const auto& d = net == 0 ? s.pdims : s.cdims;
+        for (int l = 0; l < s.L; ++l) {
+            uint64_t node = static_cast<uint64_t>(net * 2 * s.L + 2 * l);
+            double a = std::sqrt(6.0 / (static_cast<double>(d[l]) + static_cast<double>(d[l + 1])));
+            int64_t n = static_cast<int64_t>(d[l]) * d[l + 1];
+            for (int64_t i = 0; i < n; ++i)
+                p[static_cast<size_t>(s.woff[net][l] + i)] = static_cast<float>(
+                    rng_uniform_range(rng_key(seed_, kParamStream, node, static_cast<uint64_t>(i)), -a, a));
+        }
+    }
+    FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaMemcpy(b_->params, p.data(), p.size() * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+void Engine::reinit(uint64_t seed) {
+    FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+    if (seed != seed_ && graph_) {  // the seed is baked into the captured kernel arguments
+        FLW_CUDA(cudaGraphExecDestroy(graph_));
+        graph_ = nullptr;
+    }
+    seed_ = seed;
+    init_params();
+    FLW_CUDA(cudaMemset(b_->m, 0, static_cast<size_t>(shape_.P) * sizeof(double)));
+    FLW_CUDA(cudaMemset(b_->v, 0, static_cast<size_t>(shape_.P) * sizeof(double)));
+    FLW_CUDA(cudaMemset(b_->ctx, 0, sizeof(DeviceCtx)));
+    steps_ = 0;
+    cur_step_ = 0;
+}
+
+// Pageable H2D copies are staged before cudaMemcpyAsync returns, so `ep` may live on the stack.
+void Engine::set_episode(int64_t ep) {
+    FLW_CUDA(cudaMemcpyAsync(&b_->ctx->episode, &ep, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+}
+
+// ----------------------------------------------------------------------------- phases
+void Engine::enq_reset() {
+    Bufs& b = *b_;
+    exact_reset(stream_, b.ctx, env_params(cfg_, shape_, b_->synth_b), b.est, b.done, b.stepc, b.states, E_, lo_,
+                shape_.obs_dim, seed_);
+}
+
+void Engine::enq_mlp_forward(int net, const float* X, int64_t M, float* const* H) {
+    const ProgramShape& s = shape_;
+    const auto& d = net == 0 ? s.pdims : s.cdims;
+    const float* in = X;
+    for (int l = 0; l < s.L; ++l) {
+        exact_layer_fwd(stream_, in, b_->params + s.woff[net][l], b_->params + s.boff[net][l], H[l], M, d[l], d[l + 1],
+                        l + 1 < s.L ? act_of(cfg_) : kNone);
+        in = H[l];
+    }
+}
+
+void Engine::enq_step(int64_t st) {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    const int S = s.obs_dim, A = s.n_actions;
+    const float* in = b.states + st * E_ * S;
+    float* bufs[2] = {b.act0, b.act1};
+    for (int l = 0; l < s.L; ++l) {
+        float* out = l + 1 == s.L ? b.logits : bufs[l & 1];
+        exact_layer_fwd(stream_, in, b.params + s.woff[0][l], b.params + s.boff[0][l], out, E_, s.pdims[l],
+                        s.pdims[l + 1], l + 1 < s.L ? act_of(cfg_) : kNone);
+        in = out;
+    }
+    RolloutArgs a{};
+    a.logits = b.logits;
+    a.est = b.est;
+    a.done = b.done;
+    a.stepc = b.stepc;
+    a.actions = b.actions + st * E_;
+    a.logp = b.logp + st * E_;
+    a.reward = b.rew + st * E_;
+    a.reward_d = b.rew_d + st * E_;
+    a.done_f = b.done_f + st * E_;
+    a.next_obs = b.states + (st + 1) * E_ * S;
+    a.E = E_;
+    a.env_lo = lo_;
+    a.S = S;
+    a.A = A;
+    a.seed = seed_;
+    a.step = st;
+    a.env = env_params(cfg_, shape_, b_->synth_b);
+    exact_rollout(stream_, b.ctx, a);
+}
+
+void Engine::enq_learn_grads() {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    const int S = s.obs_dim, A = s.n_actions, L = s.L;
+    const float* X = b.states;                        // [T*E, S] t-major
+    const float* last_next = b.states + T_ * E_ * S;  // [E, S]
+    enq_mlp_forward(1, X, TR_, b.Hc.data());          // values = critic(states)
+    enq_mlp_forward(1, last_next, R_, b.Hl.data());   // last_value = critic(last_next)
+    const bool ppo = s.algo != Algo::A3c;
+    exact_gae(stream_, b.rew, b.Hc[L - 1], b.done_f, b.Hl[L - 1], TR_, R_, cfg_.gamma, cfg_.lam, b.adv_d, b.ret, ppo);
+    if (ppo) exact_normalize(stream_, b.adv_d, TR_, cfg_.normalize_adv, b.stats, b.adv);
+    enq_mlp_forward(0, X, TR_, b.Hp.data());          // logits_new = policy(states)
+    exact_loss_rows(stream_, ppo ? 0 : 1, b.Hp[L - 1], b.Hc[L - 1], b.actions, b.logp, b.adv, b.ret, TR_, A,
+                    cfg_.clip_eps, cfg_.value_coef, cfg_.entropy_coef, b.DZp[L - 1], b.DZc[L - 1], b.terms);
+    // Adjoint chains (row-parallel), then every dW/db chain of both nets in one launch.
+    for (int net = 0; net < 2; ++net) {
+        const auto& d = net == 0 ? s.pdims : s.cdims;
+        const auto& H = net == 0 ? b.Hp : b.Hc;
+        const auto& DZ = net == 0 ? b.DZp : b.DZc;
+        for (int l = L - 1; l >= 1; --l)
+            exact_layer_dh(stream_, DZ[l], b.params + s.woff[net][l], H[l - 1], DZ[l - 1], TR_, d[l], d[l + 1],
+                           act_of(cfg_));
+    }
+    exact_dw(stream_, b.tiles, b.ntiles, TR_);
+}
+
+void Engine::enq_grad_sync_and_adam() {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    adam_tick(stream_, b.ctx, b.bc_table, b.bc_len);
+    const double* g64 = nullptr;
+    if (comm_ && comm_->nranks() > 1) {
+        // GradSync (local_run.cpp:379-414): AllGather then the mean in unit-id (= rank) order.
+        comm_->all_gather(b.grads, b.gather, s.P, stream_);
+        exact_grad_mean(stream_, b.gather, comm_->nranks(), s.P, b.gmean);
+        g64 = b.gmean;
+    }
+    exact_adam(stream_, b.ctx, b.params, b.grads, g64, b.m, b.v, s.P, cfg_.lr, 0.9, 0.999, 1e-8);
+}
+
+void Engine::enq_reward_sum() {
+    // Episode reward sum in the reference's order: steps outer, envs inner (interp.cpp:257).
+    exact_seq_sum(side_, b_->rew_d, T_ * E_, b_->rsum);
+}
+
+// ------------------------------------------------------------------- phase-level API
+void Engine::reset(int64_t ep) {
+    FLW_CUDA(cudaSetDevice(device_));
+    set_episode(ep);
+    enq_reset();
+    FLW_CUDA(cudaMemsetAsync(b_->rew_d, 0, static_cast<size_t>(T_ * E_) * sizeof(double), stream_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+    cur_step_ = 0;
+}
+
+void Engine::step(int64_t ep, int64_t st) {
+    FLW_CUDA(cudaSetDevice(device_));
+    if (st < 0 || st >= T_) fail(Errc::Config, "step index outside the episode");
+    set_episode(ep);
+    enq_step(st);
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+    cur_step_ = st + 1;
+    steps_ += 1;
+}
+
+void Engine::learn_grads(int64_t ep, int64_t k) {
+    (void)k;
+    FLW_CUDA(cudaSetDevice(device_));
+    set_episode(ep);
+    enq_learn_grads();
+    exact_loss_reduce(stream_, b_->terms, TR_, cfg_.entropy_coef, b_->loss);
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::apply_grads(const double* host_grads) {
+    FLW_CUDA(cudaSetDevice(device_));
+    Bufs& b = *b_;
+    adam_tick(stream_, b.ctx, b.bc_table, b.bc_len);
+    const double* g64 = nullptr;
+    if (host_grads) {
+        FLW_CUDA(cudaMemcpyAsync(b.gmean, host_grads, static_cast<size_t>(shape_.P) * sizeof(double),
+                                 cudaMemcpyHostToDevice, stream_));
+        g64 = b.gmean;
+    }
+    exact_adam(stream_, b.ctx, b.params, b.grads, g64, b.m, b.v, shape_.P, cfg_.lr, 0.9, 0.999, 1e-8);
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::learn(int64_t ep, int64_t k) {
+    (void)k;
+    FLW_CUDA(cudaSetDevice(device_));
+    set_episode(ep);
+    enq_learn_grads();
+    exact_loss_reduce(stream_, b_->terms, TR_, cfg_.entropy_coef, b_->loss);
+    enq_grad_sync_and_adam();
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// ------------------------------------------------------------------------ episode graph
+void Engine::build_graph() {
+    FLW_CUDA(cudaSetDevice(device_));
+    cudaGraph_t g;
+    FLW_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    begin_episode(stream_, b_->ctx);
+    enq_reset();
+    for (int64_t st = 0; st < T_; ++st) enq_step(st);
+    FLW_CUDA(cudaEventRecord(ev_fork_, stream_));
+    FLW_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+    enq_reward_sum();
+    FLW_CUDA(cudaEventRecord(ev_join_, side_));
+    for (int64_t k = 0; k < shape_.learn_iters; ++k) {
+        enq_learn_grads();
+        enq_grad_sync_and_adam();
+    }
+    FLW_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+    FLW_CUDA(cudaStreamEndCapture(stream_, &g));
+    size_t n = 0;
+    FLW_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    FLW_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+    graph_kernels_ = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        FLW_CUDA(cudaGraphNodeGetType(nd, &ty));
+        if (ty == cudaGraphNodeTypeKernel) ++graph_kernels_;
+    }
+    FLW_CUDA(cudaGraphInstantiate(&graph_, g, 0));
+    FLW_CUDA(cudaGraphDestroy(g));
+}
+
+void Engine::enqueue_episodes(int64_t first, int64_t count) {
+    FLW_CUDA(cudaSetDevice(device_));
+    if (!graph_) build_graph();
+    FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, &first, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+    for (int64_t i = 0; i < count; ++i) FLW_CUDA(cudaGraphLaunch(graph_, stream_));
+    steps_ += T_ * count;
+    cur_step_ = T_;
+}
+
+double Engine::last_reward_sum() {
+    double r = 0.0;
+    FLW_CUDA(cudaMemcpy(&r, b_->rsum, sizeof(double), cudaMemcpyDeviceToHost));
+    return r;
+}
+
+void Engine::sync() {
+    FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+}
+
+double Engine::run_episode(int64_t ep, float* device_ms) {
+    FLW_CUDA(cudaSetDevice(device_));
+    if (!graph_) build_graph();
+    FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, &ep, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+    FLW_CUDA(cudaEventRecord(ev_t0_, stream_));
+    FLW_CUDA(cudaGraphLaunch(graph_, stream_));
+    FLW_CUDA(cudaEventRecord(ev_t1_, stream_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+    steps_ += T_;
+    cur_step_ = T_;
+    if (device_ms) FLW_CUDA(cudaEventElapsedTime(device_ms, ev_t0_, ev_t1_));
+    return last_reward_sum();
+}
+
+// --------------------------------------------------------------------------- params
+void Engine::get_params(double* out) {
+    FLW_CUDA(cudaSetDevice(device_));
+    std::vector<float> p(static_cast<size_t>(shape_.P));
+    FLW_CUDA(cudaMemcpy(p.data(), b_->params, p.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < p.size(); ++i) out[i] = static_cast<double>(p[i]);
+}
+
+void Engine::set_params(const double* in) {
+    FLW_CUDA(cudaSetDevice(device_));
+    std::vector<float> p(static_cast<size_t>(shape_.P));
+    for (size_t i = 0; i < p.size(); ++i) p[i] = static_cast<float>(in[i]);
+    FLW_CUDA(cudaMemcpy(b_->params, p.data(), p.size() * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+// ----------------------------------------------------------------- named tensors (tests)
+namespace {
+template <typename T>
+std::vector<T> d2h(const T* p, int64_t n) {
+    std::vector<T> v(static_cast<size_t>(n));
+    if (n) FLW_CUDA(cudaMemcpy(v.data(), p, static_cast<size_t>(n) * sizeof(T), cudaMemcpyDeviceToHost));
+    return v;
+}
+template <typename T>
+void h2d(T* p, const std::vector<T>& v) {
+    if (!v.empty()) FLW_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+}  // namespace
+
+int64_t Engine::tensor_size(const std::string& n) const {
+    const int64_t S = shape_.obs_dim, A = shape_.n_actions;
+    if (n == "reset_obs" || n == "state_in") return E_ * S;
+    if (n == "logits") return E_ * A;
+    if (n == "pa") return E_ * 2;
+    if (n == "envstep") return E_ * (S + 2);
+    if (n == "sample") return TR_ * (2 * S + 4);
+    if (n == "values" || n == "adv" || n == "ret") return TR_;
+    if (n == "last_value") return R_;
+    if (n == "logits_new" || n == "dlogits") return TR_ * A;
+    if (n == "loss") return 1;
+    if (n == "grads") return shape_.P;
+    if (n == "env_state") return E_ * shape_.env_state_w;
+    return -1;
+}
+
+void Engine::read_tensor(const std::string& n, double* out) {
+    FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+    Bufs& b = *b_;
+    const int64_t S = shape_.obs_dim, A = shape_.n_actions, L = shape_.L;
+    auto put = [&](const auto& v) {
+        for (size_t i = 0; i < v.size(); ++i) out[i] = static_cast<double>(v[i]);
+    };
+    const int64_t last = std::max<int64_t>(cur_step_ - 1, 0);
+    if (n == "reset_obs") return put(d2h(b.states, E_ * S));
+    if (n == "state_in") return put(d2h(b.states + cur_step_ * E_ * S, E_ * S));
+    if (n == "logits") return put(d2h(b.logits, E_ * A));
+    if (n == "values") return put(d2h(b.Hc[L - 1], TR_));
+    if (n == "last_value") return put(d2h(b.Hl[L - 1], R_));
+    if (n == "adv") return put(d2h(b.adv, TR_));
+    if (n == "ret") return put(d2h(b.ret, TR_));
+    if (n == "logits_new") return put(d2h(b.Hp[L - 1], TR_ * A));
+    if (n == "dlogits") return put(d2h(b.DZp[L - 1], TR_ * A));
+    if (n == "loss") return put(d2h(b.loss, 1));
+    if (n == "grads") return put(d2h(b.grads, shape_.P));
+    if (n == "pa" || n == "envstep") {
+        auto act = d2h(b.actions + last * E_, E_);
+        auto lp = d2h(b.logp + last * E_, E_);
+        if (n == "pa") {
+            for (int64_t e = 0; e < E_; ++e) {
+                out[2 * e] = act[static_cast<size_t>(e)];
+                out[2 * e + 1] = lp[static_cast<size_t>(e)];
+            }
+            return;
+        }
+        auto obs = d2h(b.states + (last + 1) * E_ * S, E_ * S);
+        auto rw = d2h(b.rew + last * E_, E_);
+        auto dn = d2h(b.done_f + last * E_, E_);
+        for (int64_t e = 0; e < E_; ++e) {
+            for (int64_t j = 0; j < S; ++j) out[e * (S + 2) + j] = obs[static_cast<size_t>(e * S + j)];
+            out[e * (S + 2) + S] = rw[static_cast<size_t>(e)];
+            out[e * (S + 2) + S + 1] = dn[static_cast<size_t>(e)];
+        }
+        return;
+    }
+    if (n == "sample") {  // [T*E, 2S+4] = state | action | reward | next | done | logp (programs.cpp:229-230)
+        auto st = d2h(b.states, (T_ + 1) * E_ * S);
+        auto act = d2h(b.actions, TR_);
+        auto rw = d2h(b.rew, TR_);
+        auto dn = d2h(b.done_f, TR_);
+        auto lp = d2h(b.logp, TR_);
+        const int64_t W = 2 * S + 4;
+        for (int64_t i = 0; i < TR_; ++i) {
+            double* row = out + i * W;
+            for (int64_t j = 0; j < S; ++j) row[j] = st[static_cast<size_t>(i * S + j)];
+            row[S] = act[static_cast<size_t>(i)];
+            row[S + 1] = rw[static_cast<size_t>(i)];
+            for (int64_t j = 0; j < S; ++j) row[S + 2 + j] = st[static_cast<size_t>((i + E_) * S + j)];
+            row[2 * S + 2] = dn[static_cast<size_t>(i)];
+            row[2 * S + 3] = lp[static_cast<size_t>(i)];
+        }
+        return;
+    }
+    if (n == "env_state") {
+        auto est = d2h(b.est, E_ * shape_.env_state_w);
+        for (int64_t e = 0; e < E_; ++e)
+            for (int64_t j = 0; j < shape_.env_state_w; ++j)
+                out[e * shape_.env_state_w + j] = est[static_cast<size_t>(j * E_ + e)];
+        return;
+    }
+    fail(Errc::Config, "unknown tensor '" + n + "'");
+}
+
+void Engine::write_tensor(const std::string& n, const double* in, int64_t cnt) {
+    FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+    if (cnt != tensor_size(n)) fail(Errc::Shape, "tensor '" + n + "' expects " + std::to_string(tensor_size(n)));
+    Bufs& b = *b_;
+    const int64_t S = shape_.obs_dim;
+    auto f = [&](int64_t off, int64_t len, int64_t stride = 1) {
+        std::vector<float> v(static_cast<size_t>(len));
+        for (int64_t i = 0; i < len; ++i) v[static_cast<size_t>(i)] = static_cast<float>(in[off + i * stride]);
+        return v;
+    };
+    if (n == "state_in") return h2d(b.states + cur_step_ * E_ * S, f(0, E_ * S));
+    if (n == "sample") {  // teacher forcing of the learn batch
+        const int64_t W = 2 * S + 4;
+        std::vector<float> st(static_cast<size_t>((T_ + 1) * E_ * S)), rw(TR_), dn(TR_), lp(TR_);
+        std::vector<int32_t> act(static_cast<size_t>(TR_));
+        for (int64_t i = 0; i < TR_; ++i) {
+            const double* row = in + i * W;
+            for (int64_t j = 0; j < S; ++j) st[static_cast<size_t>(i * S + j)] = static_cast<float>(row[j]);
+            act[static_cast<size_t>(i)] = static_cast<int32_t>(row[S] + 0.5);
+            rw[static_cast<size_t>(i)] = static_cast<float>(row[S + 1]);
+            dn[static_cast<size_t>(i)] = static_cast<float>(row[2 * S + 2]);
+            lp[static_cast<size_t>(i)] = static_cast<float>(row[2 * S + 3]);
+        }
+        for (int64_t e = 0; e < E_; ++e)  // last_next = next-state column of the last E rows
+            for (int64_t j = 0; j < S; ++j)
+                st[static_cast<size_t>((TR_ + e) * S + j)] = static_cast<float>(in[(TR_ - E_ + e) * W + S + 2 + j]);
+        h2d(b.states, st);
+        h2d(b.actions, act);
+        h2d(b.rew, rw);
+        h2d(b.done_f, dn);
+        h2d(b.logp, lp);
+        return;
+    }
+    fail(Errc::Config, "tensor '" + n + "' is not writable");
+}
+
+}  // namespace flw

@@ -1,0 +1,112 @@
+// The B200 DP-D unit engine: one instance owns one fused-loop replica (the reference's
+// run_unit + Interp over the fused fragment, local_run.cpp:367-501 / interp.hpp:34-115) with
+// ALL of its state resident in HBM: parameters, Adam moments, env state (SoA), trajectory,
+// activations. The host only drives phases (or replays a captured CUDA graph per episode) and
+// reads back per-episode scalars.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "config.hpp"
+
+namespace flw {
+
+enum class Numerics : int {
+    Exact = 0,  // FP64-accumulate CUDA-core path, bit-exact with the reference's per-op f32 rounding
+    Fast = 1,   // tensor-core (tcgen05) path, fp32 accumulate, tolerance-checked
+};
+
+struct DeviceCtx {      // device-resident episode context (read by kernels inside captured graphs)
+    int64_t episode;
+    int64_t next_episode;  // consumed by the graph's first node, so replays can be queued back to back
+    int64_t adam_t;
+    double bc1, bc2;    // Adam bias corrections 1 - beta^t, from a host-computed table
+};
+
+class Comm;  // NCCL gradient group (comm.hpp)
+
+class Engine {
+  public:
+    Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo, int64_t env_hi, int64_t env_total,
+           Numerics numerics);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // Gradient group (GradSync): rank = unit id, nranks = k. Takes ownership.
+    void set_comm(std::unique_ptr<Comm> comm);
+
+    // Phase-level API (each enqueues on the engine stream and synchronises before returning).
+    void reset(int64_t ep);
+    void step(int64_t ep, int64_t st);
+    void learn_grads(int64_t ep, int64_t k);       // up to GradCompute (flat f32 gradient)
+    void apply_grads(const double* host_grads);     // OptimStep on given (already synced) grads
+    void learn(int64_t ep, int64_t k);              // grads + GradSync + Adam
+
+    // Whole episode: Reset, T x Step, I x Learn as one captured CUDA graph. Returns the
+    // episode reward sum (sum over this unit's envs, interp.cpp:257) and the device time.
+    double run_episode(int64_t ep, float* device_ms = nullptr);
+    // Enqueue `count` episodes starting at `first` back to back (no host sync in between).
+    void enqueue_episodes(int64_t first, int64_t count);
+    double last_reward_sum();
+    void sync();
+    cudaStream_t stream() const { return stream_; }
+
+    int64_t param_count() const { return shape_.P; }
+    // Fresh run on the same buffers: re-initialised params (new seed), Adam state and counters.
+    void reinit(uint64_t seed);
+    void get_params(double* out);
+    void set_params(const double* in);
+    int64_t steps_executed() const { return steps_; }
+    int64_t env_count() const { return E_; }
+    int64_t learn_iters() const { return shape_.learn_iters; }
+    const ProgramShape& shape() const { return shape_; }
+    Numerics numerics() const { return numerics_; }
+    int device() const { return device_; }
+
+    // Named tensors for parity tests (same names as the oracle): reset_obs, state_in, logits,
+    // pa, envstep, sample, values, last_value, adv, ret, logits_new, loss, grads, dlogits,
+    // env_state. Values are returned as doubles in the reference's row-major layouts.
+    int64_t tensor_size(const std::string& name) const;
+    void read_tensor(const std::string& name, double* out);
+    void write_tensor(const std::string& name, const double* in, int64_t n);
+
+    // Launch statistics of the last captured episode graph (kernel nodes).
+    int64_t graph_kernel_nodes() const { return graph_kernels_; }
+
+  private:
+    struct Bufs;
+    void alloc();
+    void init_params();
+    void set_episode(int64_t ep);
+    void enq_reset();
+    void enq_step(int64_t st);
+    void enq_learn_grads();
+    void enq_grad_sync_and_adam();
+    void enq_reward_sum();
+    void enq_mlp_forward(int net, const float* X, int64_t M, float* const* H);
+    void build_graph();
+
+    AlgoConfig cfg_;
+    ProgramShape shape_;
+    int device_;
+    uint64_t seed_;
+    int64_t lo_, hi_, etot_, E_, R_, T_, TR_;
+    Numerics numerics_;
+    cudaStream_t stream_ = nullptr, side_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_t0_ = nullptr, ev_t1_ = nullptr;
+    std::unique_ptr<Bufs> b_;
+    std::unique_ptr<Comm> comm_;
+    cudaGraphExec_t graph_ = nullptr;
+    int64_t graph_kernels_ = 0;
+    int64_t steps_ = 0;
+    int64_t cur_step_ = 0;      // index of the trajectory block holding the current policy input
+};
+
+}  // namespace flw

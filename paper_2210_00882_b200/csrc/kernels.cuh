@@ -1,0 +1,66 @@
+// Launchers for the DP-D kernels. Every launcher enqueues on the given stream and returns
+// immediately; shapes are in rows (M), reduction width (K) and output width (N).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "envs.cuh"
+
+namespace flw {
+
+struct DeviceCtx;
+
+// Activation of a hidden layer (programs.cpp:67-68): 0 tanh, 1 relu; 2 = none (last layer).
+enum Act : int { kTanh = 0, kRelu = 1, kNone = 2 };
+
+struct RolloutArgs {      // one rollout step over E envs (single-agent PPO/A3C)
+    const float* logits;  // [E, A]
+    double* est;          // env state SoA [sw, E]
+    uint8_t* done;        // [E]
+    int32_t* stepc;       // [E]
+    int32_t* actions;     // [E]   (this step's slice of the trajectory)
+    float* logp;          // [E]
+    float* reward;        // [E]
+    double* reward_d;     // [E]   unrounded env reward (episode reward sum)
+    float* done_f;        // [E]   0/1
+    float* next_obs;      // [E, S] next step's policy input (or last_next)
+    int64_t E, env_lo;
+    int S, A;
+    uint64_t seed;
+    int64_t step;
+    EnvParams env;
+};
+
+struct DwTile {           // one 32(t) x 32(j) block of dW_l = H_{l-1}^T dZ_l (+ bias row t == K)
+    const float* H;       // [M, K]
+    const float* DZ;      // [M, N]
+    float* gW;            // [K, N] slice of the flat gradient
+    float* gB;            // [N]
+    int K, N, t0, j0;
+};
+
+// ---------------------------------------------------------------- exact (FP64-accumulate) path
+void exact_reset(cudaStream_t s, const DeviceCtx* ctx, const EnvParams& env, double* est, uint8_t* done,
+                 int32_t* stepc, float* obs0, int64_t E, int64_t env_lo, int S, uint64_t seed);
+void exact_layer_fwd(cudaStream_t s, const float* in, const float* W, const float* b, float* out, int64_t M, int K,
+                     int N, int act);
+void exact_layer_dh(cudaStream_t s, const float* dz, const float* W, const float* hprev, float* dzprev, int64_t M,
+                    int K, int N, int act);
+void exact_rollout(cudaStream_t s, const DeviceCtx* ctx, const RolloutArgs& a);
+void exact_seq_sum(cudaStream_t s, const double* x, int64_t n, double* out);
+void exact_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
+               int64_t TR, int64_t R, double gamma, double lam, double* adv_d, float* ret, bool with_adv);
+void exact_normalize(cudaStream_t s, const double* adv_d, int64_t n, bool normalize, double* stats, float* adv);
+void exact_loss_rows(cudaStream_t s, int algo, const float* logits, const float* values, const int32_t* actions,
+                     const float* logp_old, const float* adv, const float* ret, int64_t n, int A, double clip_eps,
+                     double value_coef, double entropy_coef, float* dlogits, float* dvalues, double* terms);
+void exact_loss_reduce(cudaStream_t s, const double* terms, int64_t n, double entropy_coef, float* loss);
+void exact_dw(cudaStream_t s, const DwTile* tiles, int ntiles, int64_t M);
+void exact_grad_mean(cudaStream_t s, const float* gathered, int k, int64_t P, double* mean);
+void begin_episode(cudaStream_t s, DeviceCtx* ctx);  // ctx->episode = ctx->next_episode++
+void adam_tick(cudaStream_t s, DeviceCtx* ctx, const double2* bc_table, int64_t table_len);
+void exact_adam(cudaStream_t s, const DeviceCtx* ctx, float* params, const float* g32, const double* g64, double* m,
+                double* v, int64_t P, double lr, double b1, double b2, double eps);
+
+}  // namespace flw

@@ -55,6 +55,32 @@ RUN_CASES = {
 }
 
 
+# (algo, deploy) pairs for the control-plane parity: DP-D plans and the errors the reference raises.
+_G = {"algorithm": "ppo", "env": {"type": "gridline", "num": 10}}
+PLAN_CASES = [
+    (_G, {"distribution_policy": "dp-d"}),
+    (_G | {"actor": {"num": 3}}, {"workers": ["a", "b"], "slots_per_worker": {"cpu": 2, "accel": 2},
+                                  "distribution_policy": "GPU_only"}),
+    (_G | {"actor": {"num": 4}}, {"workers": ["local"], "slots_per_worker": {"cpu": 1, "accel": 4},
+                                  "distribution_policy": "dp-d"}),
+    (_G | {"actor": {"num": 5}}, {"workers": ["w0", "w1"], "slots_per_worker": {"cpu": 1, "accel": 2},
+                                  "distribution_policy": "dp-d"}),
+    ({"algorithm": "ppo", "env": {"type": "cartpole_lite", "num": 4}}, {"distribution_policy": "dp-d"}),
+    ({"algorithm": "ppo", "env": {"type": "nope", "num": 4}}, {"distribution_policy": "dp-d"}),
+    ({"algorithm": "a3c", "actor": {"num": 2}, "env": {"type": "gridline", "num": 4}}, {"distribution_policy": "dp-d"}),
+    ({"algorithm": "a3c", "actor": {"num": 4}, "env": {"type": "gridline", "num": 4}},
+     {"slots_per_worker": {"cpu": 1, "accel": 4}, "distribution_policy": "dp-d"}),
+    (_G | {"learner": {"params": {"gamma": 1.5}}}, {"distribution_policy": "dp-d"}),
+    (_G | {"policy_net": {"hidden": []}}, {"distribution_policy": "dp-d"}),
+    (_G, {"distribution_policy": "dp-z"}),
+    (_G, {"workers": [], "distribution_policy": "dp-d"}),
+    (_G | {"actor": {"num": 11}}, {"distribution_policy": "dp-d"}),
+    ({"algorithm": "ppo", "env": {"type": "synth17x6", "num": 4096}, "actor": {"num": 8},
+      "policy_net": {"hidden": [64, 64, 64, 64, 64, 64]}}, {"slots_per_worker": {"cpu": 8, "accel": 8},
+                                                            "distribution_policy": "dp-d"}),
+]
+
+
 def build_ref():
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
 
@@ -62,6 +88,16 @@ def build_ref():
 def main():
     build_ref()
     with tempfile.TemporaryDirectory() as tmp:
+        plans = []
+        for i, (algo, deploy) in enumerate(PLAN_CASES):
+            ap, dp = os.path.join(tmp, f"pa{i}.json"), os.path.join(tmp, f"pd{i}.json")
+            json.dump(algo, open(ap, "w"))
+            json.dump(deploy, open(dp, "w"))
+            out = subprocess.run([pyoracle.REF_TOOL, "plan", ap, dp], check=True, capture_output=True,
+                                 text=True).stdout
+            plans.append({"algo": algo, "deploy": deploy, **json.loads(out)})
+        json.dump(plans, open(os.path.join(HERE, "plans.json"), "w"), indent=1)
+        print("plans", len(plans))
         for name, (algo, seed) in TRACE_CASES.items():
             ap = os.path.join(tmp, name + ".json")
             json.dump(algo, open(ap, "w"))

@@ -1,0 +1,76 @@
+"""CPU-side checks of the C-ABI boundary (no GPU needed): the library loads, exports every
+symbol include/fraglow_b200.h declares, and its control plane (config parsing/validation, the
+DP-D placement, plan dump, error codes and messages) matches the reference's own C API on the
+same documents (tests/golden/plans.json, produced by the unmodified reference)."""
+import json
+import os
+
+import pytest
+
+from paper_2210_00882_b200 import FlwError, Program
+from paper_2210_00882_b200 import _native as N
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+PLANS = json.load(open(os.path.join(GOLDEN, "plans.json")))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.lib()
+    syms = N.header_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+@pytest.mark.parametrize("case", PLANS, ids=[f"plan{i}" for i in range(len(PLANS))])
+def test_program_matches_reference_c_api(case):
+    if case["rc"] == 0:
+        p = Program(case["algo"], case["deploy"])
+        assert json.loads(p.dump()) == case["plan"]
+        viol, n = p.validate_plan()
+        assert n == len(case["violations"]) and viol == case["violations"]
+    else:
+        with pytest.raises(FlwError) as ei:
+            Program(case["algo"], case["deploy"])
+        assert ei.value.code == case["rc"]
+        assert ei.value.message == case["error"]
+
+
+def test_non_dpd_policies_are_refused_loudly():
+    for pol in ("dp-a", "single_learner_fine", "dp-c", "dp-e", "central"):
+        with pytest.raises(FlwError) as ei:
+            Program({"algorithm": "ppo", "env": {"type": "gridline", "num": 4}}, {"distribution_policy": pol})
+        assert ei.value.code == N.FLW_ERR_CONFIG and ei.value.message.startswith("PolicyInapplicable")
+    with pytest.raises(FlwError):  # default deploy (capi.cpp:211-212) is dp-a
+        Program({"algorithm": "ppo", "env": {"type": "gridline", "num": 4}}, None)
+
+
+def test_only_plan_dump_is_served():
+    p = Program({"algorithm": "ppo", "env": {"type": "gridline", "num": 4}}, {"distribution_policy": "dp-d"})
+    for what in (N.FLW_DUMP_DFG, N.FLW_DUMP_FDG, N.FLW_DUMP_DOT):
+        with pytest.raises(FlwError) as ei:
+            p.dump(what)
+        assert ei.value.code == N.FLW_ERR_CONFIG
+
+
+def test_numerics_selection_is_validated():
+    with pytest.raises(FlwError):
+        Program({"algorithm": "ppo", "env": {"type": "gridline", "num": 4}},
+                {"distribution_policy": "dp-d", "numerics": "approximate"})
+
+
+def test_last_error_is_thread_local():
+    import threading
+
+    errs = {}
+
+    def bad(tag, algo):
+        try:
+            Program(algo, {"distribution_policy": "dp-d"})
+        except FlwError as e:
+            errs[tag] = e.message
+
+    t1 = threading.Thread(target=bad, args=("a", {"algorithm": "xx"}))
+    t2 = threading.Thread(target=bad, args=("b", {"algorithm": "ppo", "env": {"type": "nope"}}))
+    t1.start(), t2.start(), t1.join(), t2.join()
+    assert errs["a"].startswith("ConfigError") and errs["b"].startswith("UnknownEnv")

@@ -110,6 +110,11 @@ int flw_dpd_tensor_size(const flw_dpd* e, const char* name, int64_t* n);
 int flw_dpd_read(flw_dpd* e, const char* name, double* out, int64_t n);
 int flw_dpd_write(flw_dpd* e, const char* name, const double* in, int64_t n);
 
+/* Diagnostic (tests only): one tcgen05.mma GEMM D[M,N] = op(A) op(B) through the engine's
+ * shared-memory operand convention. a_mn=0: A is [M,K] row-major; a_mn=1: A is stored [K,M].
+ * b_mn=0: B is stored [N,K]; b_mn=1: B is [K,N]. lane_off = TMEM lane offset of D (M=64 only). */
+int flw_selftest_umma(int M, int N, int K, int a_mn, int b_mn, int lane_off, const float* A, const float* B, float* D);
+
 #ifdef __cplusplus
 }
 #endif

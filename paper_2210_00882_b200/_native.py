@@ -74,6 +74,7 @@ def lib():
         "flw_dpd_tensor_size": (ci, [vp, cs, P(i64)]),
         "flw_dpd_read": (ci, [vp, cs, P(d), i64]),
         "flw_dpd_write": (ci, [vp, cs, P(d), i64]),
+        "flw_selftest_umma": (ci, [ci, ci, ci, ci, ci, ci, P(C.c_float), P(C.c_float), P(C.c_float)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -22,6 +22,10 @@
 
 using namespace flw;
 
+namespace flw {
+int umma_selftest(int M, int N, int K, int a_mn, int b_mn, int lane_off, const float* A, const float* B, float* D);
+}
+
 struct flw_program {
     AlgoConfig algo;
     DeployConfig deploy;
@@ -431,6 +435,15 @@ int flw_dpd_write(flw_dpd* e, const char* name, const double* in, int64_t n) {
     return guarded([&] {
         eng(e).write_tensor(name, in, n);
         return FLW_OK;
+    });
+}
+
+int flw_selftest_umma(int M, int N, int K, int a_mn, int b_mn, int lane_off, const float* A, const float* B,
+                      float* D) {
+    return guarded([&] {
+        if (!((M == 64 || M == 128) && N % 16 == 0 && N >= 16 && N <= 256 && K % 16 == 0 && K > 0))
+            fail(Errc::Config, "unsupported selftest shape");
+        return umma_selftest(M, N, K, a_mn, b_mn, lane_off, A, B, D);
     });
 }
 

@@ -16,6 +16,7 @@
 
 #include "comm.hpp"
 #include "common.cuh"
+#include "fast.cuh"
 #include "kernels.cuh"
 
 namespace flw {
@@ -47,6 +48,13 @@ struct Engine::Bufs {
     double* synth_b = nullptr;
     DwTile* tiles = nullptr;
     int ntiles = 0;
+    // both modes: critic outputs consumed by GAE and the loss
+    float *values = nullptr, *last_value = nullptr;
+    // fast numerics
+    FastNet pol{}, crit{};
+    int grid = 0;                       // persistent CTAs of the fused learn kernel
+    float *part_p = nullptr, *part_c = nullptr, *loss_parts = nullptr;
+    double *block_sums = nullptr, *rsum_scratch = nullptr;
     std::vector<void*> owned;
 
     template <typename T>
@@ -174,6 +182,44 @@ void Engine::alloc() {
     b.rew = b.alloc<float>(T_ * E_);
     b.done_f = b.alloc<float>(T_ * E_);
     b.rew_d = b.alloc<double>(T_ * E_);
+    b.adv = b.alloc<float>(TR_);
+    b.ret = b.alloc<float>(TR_);
+    b.stats = b.alloc<double>(2);
+    b.loss = b.alloc<float>(1);
+    b.rsum = b.alloc<double>(1);
+    if (numerics_ == Numerics::Fast) {
+        // Fused tensor-core learn kernels: per-CTA dW partials replace the per-layer activations.
+        auto make_net = [&](int net) {
+            const auto& d = net == 0 ? s.pdims : s.cdims;
+            FastNet n{};
+            n.L = L;
+            for (int l = 0; l < L; ++l) {
+                n.rin[l] = d[l];
+                n.rout[l] = d[l + 1];
+                n.din[l] = (d[l] + 15) / 16 * 16;
+                n.dout[l] = (d[l + 1] + 15) / 16 * 16;
+                n.woff[l] = s.woff[net][l];
+                n.boff[l] = s.boff[net][l];
+                if (n.din[l] > 64 || n.dout[l] > 64)
+                    fail(Errc::Config, "fast numerics supports MLP widths up to 64 (use numerics=exact)");
+            }
+            return n;
+        };
+        if (L > kMaxLayers) fail(Errc::Config, "fast numerics supports at most 8 layers");
+        b.pol = make_net(0);
+        b.crit = make_net(1);
+        int sms = 0;
+        FLW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+        b.grid = static_cast<int>(std::min<int64_t>(sms, (TR_ + 127) / 128));
+        b.part_p = b.alloc<float>(static_cast<int64_t>(b.grid) * s.P_policy);
+        b.part_c = b.alloc<float>(static_cast<int64_t>(b.grid) * (s.P - s.P_policy));
+        b.loss_parts = b.alloc<float>(2 * 3 * b.grid);
+        b.block_sums = b.alloc<double>(2 * ((R_ + 255) / 256));
+        b.rsum_scratch = b.alloc<double>(256);
+        b.values = b.alloc<float>(TR_);
+        b.last_value = b.alloc<float>(R_);
+        return;
+    }
     for (int l = 0; l < L; ++l) {
         b.Hp.push_back(b.alloc<float>(TR_ * s.pdims[l + 1]));
         b.DZp.push_back(b.alloc<float>(TR_ * s.pdims[l + 1]));
@@ -181,13 +227,10 @@ void Engine::alloc() {
         b.DZc.push_back(b.alloc<float>(TR_ * s.cdims[l + 1]));
         b.Hl.push_back(b.alloc<float>(R_ * s.cdims[l + 1]));
     }
+    b.values = b.Hc[L - 1];
+    b.last_value = b.Hl[L - 1];
     b.adv_d = b.alloc<double>(TR_);
-    b.adv = b.alloc<float>(TR_);
-    b.ret = b.alloc<float>(TR_);
     b.terms = b.alloc<double>(3 * TR_);
-    b.stats = b.alloc<double>(2);
-    b.loss = b.alloc<float>(1);
-    b.rsum = b.alloc<double>(1);
     // dW tile table: every (net, layer) as 32(t, incl. the bias row t == K) x 32(j) tiles.
     std::vector<DwTile> tiles;
     for (int net = 0; net < 2; ++net) {
@@ -272,7 +315,40 @@ void Engine::enq_mlp_forward(int net, const float* X, int64_t M, float* const* H
     }
 }
 
+void Engine::enq_rollout_fast(int64_t step0, int64_t nsteps) {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    FastRolloutArgs a{};
+    a.params = b.params;
+    a.L = s.L;
+    for (int l = 0; l <= s.L; ++l) a.dims[l] = s.pdims[l];
+    for (int l = 0; l < s.L; ++l) {
+        a.woff[l] = s.woff[0][l];
+        a.boff[l] = s.boff[0][l];
+    }
+    a.act = act_of(cfg_);
+    a.est = b.est;
+    a.done = b.done;
+    a.stepc = b.stepc;
+    a.states = b.states;
+    a.actions = b.actions;
+    a.logp = b.logp;
+    a.reward = b.rew;
+    a.done_f = b.done_f;
+    a.reward_d = b.rew_d;
+    a.E = E_;
+    a.env_lo = lo_;
+    a.step0 = step0;
+    a.nsteps = nsteps;
+    a.S = s.obs_dim;
+    a.A = s.n_actions;
+    a.seed = seed_;
+    a.env = env_params(cfg_, shape_, b.synth_b);
+    fast_rollout(stream_, b.ctx, a);
+}
+
 void Engine::enq_step(int64_t st) {
+    if (numerics_ == Numerics::Fast) return enq_rollout_fast(st, 1);
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions;
@@ -305,7 +381,64 @@ void Engine::enq_step(int64_t st) {
     exact_rollout(stream_, b.ctx, a);
 }
 
+// Fast numerics: critic forward (tensor cores) -> GAE + advantage stats -> fused policy and
+// critic learn kernels (forward, loss, backward, TMEM-resident dW) -> deterministic reduction.
+void Engine::enq_learn_fast() {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    const int S = s.obs_dim;
+    const bool ppo = s.algo != Algo::A3c;
+    FastLearnArgs f{};
+    f.act = act_of(cfg_);
+    f.params = b.params;
+    f.in_cols = S;
+    f.inv_n = 1.0 / static_cast<double>(TR_);
+    f.value_coef = cfg_.value_coef;
+    f.entropy_coef = cfg_.entropy_coef;
+    f.clip_eps = static_cast<float>(cfg_.clip_eps);
+    // values = critic(states), last_value = critic(last_next)
+    f.net = b.crit;
+    f.kind = kNetCritic;
+    f.mode = 0;
+    f.X = b.states;
+    f.rows = TR_;
+    f.values_out = b.values;
+    fast_mlp(stream_, f, b.grid);
+    f.X = b.states + T_ * E_ * S;
+    f.rows = R_;
+    f.values_out = b.last_value;
+    fast_mlp(stream_, f, static_cast<int>(std::min<int64_t>(b.grid, (R_ + 127) / 128)));
+    fast_gae(stream_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
+             b.block_sums, b.stats);
+    // learn: policy then critic, each a persistent fused kernel
+    f.mode = 1;
+    f.X = b.states;
+    f.rows = TR_;
+    f.actions = b.actions;
+    f.logp_old = b.logp;
+    f.adv = b.adv;
+    f.adv_stats = (ppo && cfg_.normalize_adv) ? b.stats : nullptr;
+    f.ret = b.ret;
+    f.values_in = b.values;
+    f.net = b.pol;
+    f.kind = ppo ? kNetPolicyPpo : kNetPolicyA3c;
+    f.partials = b.part_p;
+    f.part_stride = s.P_policy;
+    f.loss_partials = b.loss_parts;
+    fast_mlp(stream_, f, b.grid);
+    f.net = b.crit;
+    f.kind = kNetCritic;
+    f.partials = b.part_c;
+    f.part_stride = s.P - s.P_policy;
+    f.loss_partials = b.loss_parts + 3 * b.grid;
+    fast_mlp(stream_, f, b.grid);
+    fast_reduce_partials(stream_, b.part_p, b.grid, s.P_policy, b.grads);
+    fast_reduce_partials(stream_, b.part_c, b.grid, s.P - s.P_policy, b.grads + s.P_policy);
+    fast_reduce_loss(stream_, b.loss_parts, b.grid, 2, cfg_.entropy_coef, b.loss);
+}
+
 void Engine::enq_learn_grads() {
+    if (numerics_ == Numerics::Fast) return enq_learn_fast();
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions, L = s.L;
@@ -336,18 +469,28 @@ void Engine::enq_grad_sync_and_adam() {
     const ProgramShape& s = shape_;
     adam_tick(stream_, b.ctx, b.bc_table, b.bc_len);
     const double* g64 = nullptr;
+    double gscale = 1.0;
     if (comm_ && comm_->nranks() > 1) {
-        // GradSync (local_run.cpp:379-414): AllGather then the mean in unit-id (= rank) order.
-        comm_->all_gather(b.grads, b.gather, s.P, stream_);
-        exact_grad_mean(stream_, b.gather, comm_->nranks(), s.P, b.gmean);
-        g64 = b.gmean;
+        if (numerics_ == Numerics::Exact) {
+            // GradSync (local_run.cpp:379-414): AllGather then the mean in unit-id (= rank) order.
+            comm_->all_gather(b.grads, b.gather, s.P, stream_);
+            exact_grad_mean(stream_, b.gather, comm_->nranks(), s.P, b.gmean);
+            g64 = b.gmean;
+        } else {
+            // Fast: in-place NCCL sum over NVLink, the 1/k of the mean folded into Adam.
+            comm_->all_reduce_sum(b.grads, b.grads, s.P, stream_);
+            gscale = 1.0 / static_cast<double>(comm_->nranks());
+        }
     }
-    exact_adam(stream_, b.ctx, b.params, b.grads, g64, b.m, b.v, s.P, cfg_.lr, 0.9, 0.999, 1e-8);
+    exact_adam(stream_, b.ctx, b.params, b.grads, g64, b.m, b.v, s.P, cfg_.lr, 0.9, 0.999, 1e-8, gscale);
 }
 
 void Engine::enq_reward_sum() {
     // Episode reward sum in the reference's order: steps outer, envs inner (interp.cpp:257).
-    exact_seq_sum(side_, b_->rew_d, T_ * E_, b_->rsum);
+    if (numerics_ == Numerics::Fast)
+        fast_sum(side_, b_->rew_d, T_ * E_, b_->rsum_scratch, b_->rsum);
+    else
+        exact_seq_sum(side_, b_->rew_d, T_ * E_, b_->rsum);
 }
 
 // ------------------------------------------------------------------- phase-level API
@@ -375,7 +518,7 @@ void Engine::learn_grads(int64_t ep, int64_t k) {
     FLW_CUDA(cudaSetDevice(device_));
     set_episode(ep);
     enq_learn_grads();
-    exact_loss_reduce(stream_, b_->terms, TR_, cfg_.entropy_coef, b_->loss);
+    if (numerics_ == Numerics::Exact) exact_loss_reduce(stream_, b_->terms, TR_, cfg_.entropy_coef, b_->loss);
     FLW_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -398,7 +541,7 @@ void Engine::learn(int64_t ep, int64_t k) {
     FLW_CUDA(cudaSetDevice(device_));
     set_episode(ep);
     enq_learn_grads();
-    exact_loss_reduce(stream_, b_->terms, TR_, cfg_.entropy_coef, b_->loss);
+    if (numerics_ == Numerics::Exact) exact_loss_reduce(stream_, b_->terms, TR_, cfg_.entropy_coef, b_->loss);
     enq_grad_sync_and_adam();
     FLW_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -410,7 +553,10 @@ void Engine::build_graph() {
     FLW_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     begin_episode(stream_, b_->ctx);
     enq_reset();
-    for (int64_t st = 0; st < T_; ++st) enq_step(st);
+    if (numerics_ == Numerics::Fast)
+        enq_rollout_fast(0, T_);
+    else
+        for (int64_t st = 0; st < T_; ++st) enq_step(st);
     FLW_CUDA(cudaEventRecord(ev_fork_, stream_));
     FLW_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
     enq_reward_sum();
@@ -525,9 +671,21 @@ void Engine::read_tensor(const std::string& n, double* out) {
     const int64_t last = std::max<int64_t>(cur_step_ - 1, 0);
     if (n == "reset_obs") return put(d2h(b.states, E_ * S));
     if (n == "state_in") return put(d2h(b.states + cur_step_ * E_ * S, E_ * S));
+    const bool fast = numerics_ == Numerics::Fast;
+    if (fast && (n == "logits" || n == "logits_new" || n == "dlogits"))
+        fail(Errc::Config, "tensor '" + n + "' is only materialised by numerics=exact (fused away in fast)");
     if (n == "logits") return put(d2h(b.logits, E_ * A));
-    if (n == "values") return put(d2h(b.Hc[L - 1], TR_));
-    if (n == "last_value") return put(d2h(b.Hl[L - 1], R_));
+    if (n == "values") return put(d2h(b.values, TR_));
+    if (n == "last_value") return put(d2h(b.last_value, R_));
+    if (n == "adv" && fast) {  // fast keeps raw GAE advantages; normalised on the fly by the loss
+        auto raw = d2h(b.adv, TR_);
+        auto st = d2h(b.stats, 2);
+        const bool norm = cfg_.normalize_adv && !(st[1] < 1e-8);
+        for (int64_t i = 0; i < TR_; ++i)
+            out[i] = norm ? static_cast<float>((raw[static_cast<size_t>(i)] - st[0]) / (st[1] + 1e-8))
+                          : raw[static_cast<size_t>(i)];
+        return;
+    }
     if (n == "adv") return put(d2h(b.adv, TR_));
     if (n == "ret") return put(d2h(b.ret, TR_));
     if (n == "logits_new") return put(d2h(b.Hp[L - 1], TR_ * A));

@@ -87,6 +87,8 @@ class Engine {
     void set_episode(int64_t ep);
     void enq_reset();
     void enq_step(int64_t st);
+    void enq_rollout_fast(int64_t step0, int64_t nsteps);
+    void enq_learn_fast();
     void enq_learn_grads();
     void enq_grad_sync_and_adam();
     void enq_reward_sum();

@@ -1,0 +1,79 @@
+// Fast-numerics (tensor-core learn phase, f32 rollout) kernel interfaces.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "envs.cuh"
+
+namespace flw {
+
+constexpr int kMaxLayers = 8;
+
+enum NetKind : int { kNetPolicyPpo = 0, kNetPolicyA3c = 1, kNetCritic = 2 };
+
+struct FastNet {                       // one MLP, dims padded to multiples of 16 (<= 64)
+    int L;
+    int din[kMaxLayers], dout[kMaxLayers];   // padded
+    int rin[kMaxLayers], rout[kMaxLayers];   // real
+    int64_t woff[kMaxLayers], boff[kMaxLayers];  // offsets in the flat parameter vector
+};
+
+struct FastLearnArgs {
+    FastNet net;
+    int kind;            // NetKind
+    int mode;            // 0: forward only (values_out), 1: learn (partials)
+    int act;             // 0 tanh, 1 relu
+    const float* params; // flat f32 parameters
+    const float* X;      // input rows [rows, in_cols]
+    int in_cols;
+    int64_t rows;
+    // per-row learn inputs
+    const int32_t* actions;
+    const float* logp_old;
+    const float* adv;          // raw GAE advantages (normalised on the fly with adv_stats)
+    const double* adv_stats;   // {mean, sd} or null (no normalisation)
+    const float* ret;
+    const float* values_in;    // critic values (A3C advantage)
+    float* values_out;         // mode 0
+    double inv_n, value_coef, entropy_coef;
+    float clip_eps;
+    float* partials;           // [grid, part_stride]
+    int64_t part_stride;       // = parameter count of this net
+    float* loss_partials;      // [grid, 3]
+};
+
+size_t fast_mlp_smem_bytes(const FastNet& n);
+void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid);
+void fast_reduce_partials(cudaStream_t s, const float* part, int nparts, int64_t stride, float* grads);
+void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int nparts, int nsets, double entropy_coef, float* loss);
+void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
+              int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
+              double* block_sums, double* stats);
+void fast_sum(cudaStream_t s, const double* x, int64_t n, double* scratch, double* out);
+
+struct FastRolloutArgs {     // whole-episode rollout, all T steps in one launch
+    const float* params;     // policy params (flat, reference layout)
+    int L;
+    int dims[kMaxLayers + 1];
+    int64_t woff[kMaxLayers], boff[kMaxLayers];
+    int act;
+    double* est;
+    uint8_t* done;
+    int32_t* stepc;
+    float* states;           // [(T+1), E, S]
+    int32_t* actions;        // [T, E]
+    float *logp, *reward, *done_f;
+    double* reward_d;
+    int64_t E, env_lo;
+    int64_t step0, nsteps;   // steps [step0, step0 + nsteps) of the episode
+    int S, A;
+    uint64_t seed;
+    EnvParams env;
+};
+
+struct DeviceCtx;
+size_t fast_rollout_smem_bytes(const FastRolloutArgs& a);
+void fast_rollout(cudaStream_t s, const DeviceCtx* ctx, const FastRolloutArgs& a);
+
+}  // namespace flw

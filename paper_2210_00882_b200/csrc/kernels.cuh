@@ -61,6 +61,6 @@ void exact_grad_mean(cudaStream_t s, const float* gathered, int k, int64_t P, do
 void begin_episode(cudaStream_t s, DeviceCtx* ctx);  // ctx->episode = ctx->next_episode++
 void adam_tick(cudaStream_t s, DeviceCtx* ctx, const double2* bc_table, int64_t table_len);
 void exact_adam(cudaStream_t s, const DeviceCtx* ctx, float* params, const float* g32, const double* g64, double* m,
-                double* v, int64_t P, double lr, double b1, double b2, double eps);
+                double* v, int64_t P, double lr, double b1, double b2, double eps, double gscale = 1.0);
 
 }  // namespace flw

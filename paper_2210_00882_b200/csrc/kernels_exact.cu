@@ -183,19 +183,46 @@ __global__ void k_rollout(const DeviceCtx* __restrict__ ctx, RolloutArgs a) {
 }
 
 // --------------------------------------------------------------------- sequential sums
-// One chain, loads batched ahead of the dependent adds.
-__global__ void k_seq_sum(const double* __restrict__ x, int64_t n, double* out) {
+// A left-to-right double sum has to be ONE dependent chain. The block stages the stream through
+// double-buffered shared memory (all 256 threads load chunk c+1 while thread 0 adds chunk c), so
+// the chain runs at DADD latency instead of global-load latency.
+constexpr int kSeqThreads = 256;
+constexpr int kSeqChunk = 2048;
+
+// mode 0: sum x; mode 1: sum (x - center)^2, each term individually rounded.
+__device__ double seq_chain(const double* __restrict__ x, int64_t n, int mode, double center, double (*buf)[kSeqChunk]) {
+    const int t = threadIdx.x;
+    auto load = [&](int64_t c, int slot) {
+        const int64_t base = c * kSeqChunk;
+        for (int i = t; i < kSeqChunk; i += kSeqThreads) buf[slot][i] = base + i < n ? x[base + i] : 0.0;
+    };
+    const int64_t nchunks = (n + kSeqChunk - 1) / kSeqChunk;
     double acc = 0.0;
-    int64_t i = 0;
-    for (; i + 8 <= n; i += 8) {
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = x[i + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
+    load(0, 0);
+    __syncthreads();
+    for (int64_t c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) load(c + 1, (c + 1) & 1);
+        if (t == 0) {
+            const double* b = buf[c & 1];
+            const int m = static_cast<int>(min(static_cast<int64_t>(kSeqChunk), n - c * kSeqChunk));
+            if (mode == 0) {
+                for (int i = 0; i < m; ++i) acc = __dadd_rn(acc, b[i]);
+            } else {
+                for (int i = 0; i < m; ++i) {
+                    double d = __dsub_rn(b[i], center);
+                    acc = __dadd_rn(acc, __dmul_rn(d, d));
+                }
+            }
+        }
+        __syncthreads();
     }
-    for (; i < n; ++i) acc = __dadd_rn(acc, x[i]);
-    *out = acc;
+    return acc;
+}
+
+__global__ void __launch_bounds__(kSeqThreads) k_seq_sum(const double* __restrict__ x, int64_t n, double* out) {
+    __shared__ double buf[2][kSeqChunk];
+    double acc = seq_chain(x, n, 0, 0.0, buf);
+    if (threadIdx.x == 0) *out = acc;
 }
 
 // -------------------------------------------------------------------------- GAE/returns
@@ -230,32 +257,18 @@ __global__ void k_gae(const float* __restrict__ rew, const float* __restrict__ v
 }
 
 // normalize_advantages (rl.cpp:97-107): sequential mean, then sequential variance.
-__global__ void k_norm_stats(const double* __restrict__ a, int64_t n, double* stats) {
-    double mean = 0.0;
-    int64_t i = 0;
-    for (; i + 8 <= n; i += 8) {
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = a[i + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mean = __dadd_rn(mean, v[q]);
+__global__ void __launch_bounds__(kSeqThreads) k_norm_stats(const double* __restrict__ a, int64_t n, double* stats) {
+    __shared__ double buf[2][kSeqChunk];
+    __shared__ double mean_s;
+    double s = seq_chain(a, n, 0, 0.0, buf);
+    if (threadIdx.x == 0) mean_s = __ddiv_rn(s, static_cast<double>(n));
+    __syncthreads();
+    const double mean = mean_s;
+    double var = seq_chain(a, n, 1, mean, buf);
+    if (threadIdx.x == 0) {
+        stats[0] = mean;
+        stats[1] = __dsqrt_rn(__ddiv_rn(var, static_cast<double>(n)));
     }
-    for (; i < n; ++i) mean = __dadd_rn(mean, a[i]);
-    mean = __ddiv_rn(mean, static_cast<double>(n));
-    double var = 0.0;
-    for (i = 0; i + 8 <= n; i += 8) {
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = __dsub_rn(a[i + q], mean);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) var = __dadd_rn(var, __dmul_rn(v[q], v[q]));
-    }
-    for (; i < n; ++i) {
-        double d = __dsub_rn(a[i], mean);
-        var = __dadd_rn(var, __dmul_rn(d, d));
-    }
-    stats[0] = mean;
-    stats[1] = __dsqrt_rn(__ddiv_rn(var, static_cast<double>(n)));
 }
 
 __global__ void k_norm_apply(const double* __restrict__ a, int64_t n, const double* __restrict__ stats, bool normalize,
@@ -340,18 +353,23 @@ __global__ void k_loss_reduce(const double* __restrict__ terms, int64_t n, doubl
 // matmul_grad_rhs (ops.cpp:228-240) and reduce_to_shape (ops.cpp:267-277): one sequential
 // chain over ALL rows per weight (bit-exactness forbids split-K). Tile = 32 t x 32 j; a thread
 // owns 4 t's x 1 j. The bias is the extra row t == K with h == 1 (1*dz is exact). The next
-// 32-row chunk is prefetched into registers while the current one is consumed from smem.
+// 128-row chunk is prefetched into registers while the current one is consumed from smem, so
+// the chains run at DFMA latency rather than global-load latency.
+constexpr int kDwRows = 128;
+constexpr int kDwPer = kDwRows / 8;  // rows per thread per chunk (8 warps)
+
 __global__ void __launch_bounds__(256) k_dw(const DwTile* __restrict__ tiles, int64_t M) {
-    __shared__ double Hs[2][32][33];
-    __shared__ double Ds[2][32][33];
+    extern __shared__ double dw_smem[];
+    double(*Hs)[kDwRows][33] = reinterpret_cast<double(*)[kDwRows][33]>(dw_smem);
+    double(*Ds)[kDwRows][33] = reinterpret_cast<double(*)[kDwRows][33]>(dw_smem + 2 * kDwRows * 33);
     const DwTile tl = tiles[blockIdx.x];
     const int tx = threadIdx.x & 31, tg = threadIdx.x >> 5;
     const int K = tl.K, N = tl.N;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    float hreg[4], dreg[4];
+    float hreg[kDwPer], dreg[kDwPer];
     auto fetch = [&](int64_t i0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kDwPer; ++q) {
             int rr = tg + 8 * q;
             int64_t row = i0 + rr;
             int t = tl.t0 + tx, j = tl.j0 + tx;
@@ -361,7 +379,7 @@ __global__ void __launch_bounds__(256) k_dw(const DwTile* __restrict__ tiles, in
     };
     auto stash = [&](int buf) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kDwPer; ++q) {
             Hs[buf][tg + 8 * q][tx] = static_cast<double>(hreg[q]);
             Ds[buf][tg + 8 * q][tx] = static_cast<double>(dreg[q]);
         }
@@ -370,10 +388,10 @@ __global__ void __launch_bounds__(256) k_dw(const DwTile* __restrict__ tiles, in
     stash(0);
     __syncthreads();
     int buf = 0;
-    for (int64_t i0 = 0; i0 < M; i0 += 32) {
-        const bool more = i0 + 32 < M;
-        if (more) fetch(i0 + 32);
-        const int rows = M - i0 < 32 ? static_cast<int>(M - i0) : 32;
+    for (int64_t i0 = 0; i0 < M; i0 += kDwRows) {
+        const bool more = i0 + kDwRows < M;
+        if (more) fetch(i0 + kDwRows);
+        const int rows = M - i0 < kDwRows ? static_cast<int>(M - i0) : kDwRows;
         for (int r = 0; r < rows; ++r) {
             double d = Ds[buf][r][tx];
 #pragma unroll
@@ -421,11 +439,11 @@ __global__ void k_adam_tick(DeviceCtx* ctx, const double2* __restrict__ table, i
 // adam_step (mlp.cpp:480-495): double moments, f32 params.
 __global__ void k_adam(const DeviceCtx* __restrict__ ctx, float* params, const float* __restrict__ g32,
                        const double* __restrict__ g64, double* m, double* v, int64_t P, double lr, double b1,
-                       double b2, double eps) {
+                       double b2, double eps, double gscale) {
     int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= P) return;
     const double bc1 = ctx->bc1, bc2 = ctx->bc2;
-    double g = g64 ? g64[i] : static_cast<double>(g32[i]);
+    double g = g64 ? g64[i] : __dmul_rn(static_cast<double>(g32[i]), gscale);
     double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(__dsub_rn(1.0, b1), g));
     double vi = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, b2), g), g));
     m[i] = mi;
@@ -470,7 +488,9 @@ void exact_rollout(cudaStream_t s, const DeviceCtx* ctx, const RolloutArgs& a) {
     k_rollout<<<blocks_for(a.E, 128), 128, 0, s>>>(ctx, a);
 }
 
-void exact_seq_sum(cudaStream_t s, const double* x, int64_t n, double* out) { k_seq_sum<<<1, 1, 0, s>>>(x, n, out); }
+void exact_seq_sum(cudaStream_t s, const double* x, int64_t n, double* out) {
+    k_seq_sum<<<1, kSeqThreads, 0, s>>>(x, n, out);
+}
 
 void exact_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
                int64_t TR, int64_t R, double gamma, double lam, double* adv_d, float* ret, bool with_adv) {
@@ -479,7 +499,7 @@ void exact_gae(cudaStream_t s, const float* rew, const float* values, const floa
 }
 
 void exact_normalize(cudaStream_t s, const double* adv_d, int64_t n, bool normalize, double* stats, float* adv) {
-    if (normalize) k_norm_stats<<<1, 1, 0, s>>>(adv_d, n, stats);
+    if (normalize) k_norm_stats<<<1, kSeqThreads, 0, s>>>(adv_d, n, stats);
     k_norm_apply<<<blocks_for(n, 256), 256, 0, s>>>(adv_d, n, stats, normalize, adv);
 }
 
@@ -495,7 +515,13 @@ void exact_loss_reduce(cudaStream_t s, const double* terms, int64_t n, double en
 }
 
 void exact_dw(cudaStream_t s, const DwTile* tiles, int ntiles, int64_t M) {
-    if (ntiles > 0) k_dw<<<ntiles, 256, 0, s>>>(tiles, M);
+    const size_t smem = 4 * kDwRows * 33 * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+        FLW_CUDA(cudaFuncSetAttribute(k_dw, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured = true;
+    }
+    if (ntiles > 0) k_dw<<<ntiles, 256, smem, s>>>(tiles, M);
 }
 
 void exact_grad_mean(cudaStream_t s, const float* gathered, int k, int64_t P, double* mean) {
@@ -509,8 +535,8 @@ void adam_tick(cudaStream_t s, DeviceCtx* ctx, const double2* bc_table, int64_t 
 }
 
 void exact_adam(cudaStream_t s, const DeviceCtx* ctx, float* params, const float* g32, const double* g64, double* m,
-                double* v, int64_t P, double lr, double b1, double b2, double eps) {
-    k_adam<<<blocks_for(P, 256), 256, 0, s>>>(ctx, params, g32, g64, m, v, P, lr, b1, b2, eps);
+                double* v, int64_t P, double lr, double b1, double b2, double eps, double gscale) {
+    k_adam<<<blocks_for(P, 256), 256, 0, s>>>(ctx, params, g32, g64, m, v, P, lr, b1, b2, eps, gscale);
 }
 
 }  // namespace flw

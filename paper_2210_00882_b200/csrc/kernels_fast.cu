@@ -1,0 +1,472 @@
+// Fast-numerics learn phase: the whole PPO/A3C train iteration of one MLP fused per 128-row
+// tile on the 5th-gen tensor cores.
+//
+//   critic forward  (mode 0): values / last_value for GAE
+//   learn           (mode 1): forward (L layers) -> loss epilogue -> backward (L layers), with
+//                             dW_l += H_{l-1}^T dZ_l accumulated in TMEM across all tiles a CTA
+//                             owns, db_l by column sums, per-CTA partials written once at the end.
+//
+// One CTA per SM (persistent, grid = #SMs), 128 threads: thread r owns tile row r == TMEM lane r
+// for every M=128 accumulator; thread 0 issues tcgen05.mma. Operands are bf16 in shared memory
+// in the core-matrix layout of umma.cuh; activations H_l written once serve as the K-major A of
+// the next forward GEMM and the MN-major A of the dW GEMM. Accumulation is f32 (TMEM).
+// TMEM map (512 columns): [0,64) = Z (M=128 forward / dH accumulator); layer pair (2j, 2j+1)
+// dW accumulators (M=64, "half sub-partition" layout) share columns [64+64j, 128+64j) at
+// lane offsets 0 and 16.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "fast.cuh"
+#include "umma.cuh"
+
+namespace flw {
+
+namespace {
+
+constexpr int kRows = 128;
+constexpr int kMaxW = 64;
+
+struct Smem {  // carve-up of dynamic shared memory (byte offsets)
+    uint32_t wt[kMaxLayers], x, h[kMaxLayers], dz[2], bias, dbacc, loss, total;
+};
+
+__host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline Smem carve(const FastNet& n) {
+    Smem s{};
+    uint32_t off = 0;
+    for (int l = 0; l < n.L; ++l) {
+        s.wt[l] = off;
+        off = align_up(off + static_cast<uint32_t>(n.dout[l] * n.din[l] * 2), 128);
+    }
+    s.x = off;
+    off = align_up(off + kRows * n.din[0] * 2, 128);
+    for (int l = 0; l + 1 < n.L; ++l) {
+        s.h[l] = off;
+        off = align_up(off + static_cast<uint32_t>(kRows * n.dout[l] * 2), 128);
+    }
+    for (int i = 0; i < 2; ++i) {
+        s.dz[i] = off;
+        off = align_up(off + kRows * kMaxW * 2, 128);
+    }
+    s.bias = off;
+    off += kMaxLayers * kMaxW * 4;
+    s.dbacc = off;
+    off += kMaxLayers * kMaxW * 4;
+    s.loss = off;
+    off += 4 * 4 * 4;
+    // slack: M=64 MN-major reads of narrow tiles run past their end (rows >= din are ignored)
+    s.total = off + 2048;
+    return s;
+}
+
+__device__ __forceinline__ float act_fwd(float z, int act) {
+    return act == 0 ? tanhf(z) : (z > 0.0f ? z : 0.0f);
+}
+
+__global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const FastNet& n = a.net;
+    const Smem S = carve(n);
+    const int t = threadIdx.x, w = t >> 5;
+    const int L = n.L;
+    float* bias = reinterpret_cast<float*>(smem + S.bias);
+    float* dbacc = reinterpret_cast<float*>(smem + S.dbacc);
+
+    // ---- weights (once per CTA): W_l^T as [dout x din] K-major B tiles, zero padded
+    for (int l = 0; l < L; ++l) {
+        const int di = n.din[l], dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
+        const float* W = a.params + n.woff[l];
+        for (int i = t; i < dout * di; i += 128) {
+            int o = i / di, c = i % di;
+            float v = (o < ro && c < ri) ? W[c * ro + o] : 0.0f;
+            *reinterpret_cast<__nv_bfloat16*>(smem + S.wt[l] + umma::tile_offset(o, c, di)) = __float2bfloat16(v);
+        }
+        for (int o = t; o < kMaxW; o += 128) {
+            bias[l * kMaxW + o] = o < ro ? a.params[n.boff[l] + o] : 0.0f;
+            dbacc[l * kMaxW + o] = 0.0f;
+        }
+    }
+    if (t < 16) reinterpret_cast<float*>(smem + S.loss)[t] = 0.0f;
+    umma::fence_async_smem();
+    if (w == 0) umma::tmem_alloc<512>(&tslot);
+    if (t == 0) {
+        umma::mbar_init(&bar, 1);
+        umma::fence_barrier_init();
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = tslot;
+    const uint32_t lane_base = static_cast<uint32_t>(32 * w) << 16;
+    const uint32_t sbase = umma::smem_u32(smem);
+    uint32_t phase = 0;
+    float pl_acc = 0.0f, vl_acc = 0.0f, en_acc = 0.0f;
+    bool first = true;
+    const int64_t ntiles = (a.rows + kRows - 1) / kRows;
+
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row = tile * kRows + t;
+        const bool valid = row < a.rows;
+        // ---- input tile (f32 -> bf16), zero padded columns and rows
+        {
+            float v[8];
+            for (int c0 = 0; c0 < n.din[0]; c0 += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    int c = c0 + j;
+                    v[j] = (valid && c < a.in_cols) ? a.X[row * a.in_cols + c] : 0.0f;
+                }
+                umma::st_row8(smem + S.x, n.din[0], t, c0, v);
+            }
+        }
+        umma::fence_async_smem();
+        umma::fence_before_sync();
+        __syncthreads();
+        // ---- forward
+        float out[16];
+        for (int l = 0; l < L; ++l) {
+            const int di = n.din[l], dout = n.dout[l];
+            const uint32_t in_tile = l == 0 ? sbase + S.x : sbase + S.h[l - 1];
+            if (t == 0) {
+                umma::fence_after_sync();
+                const uint32_t idesc = umma::idesc_bf16(128, dout, false, false);
+                for (int kb = 0; kb < di / 16; ++kb)
+                    umma::mma_bf16(tmem, umma::desc_kmajor(in_tile, di, kb),
+                                   umma::desc_kmajor(sbase + S.wt[l], di, kb), idesc, kb > 0);
+                umma::commit(&bar);
+            }
+            umma::mbar_wait(&bar, phase);
+            phase ^= 1;
+            umma::fence_after_sync();
+            const bool last = l + 1 == L;
+            for (int c0 = 0; c0 < dout; c0 += 16) {
+                float z[16];
+                umma::tmem_ld16(tmem + lane_base + c0, z);
+                umma::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 16; ++j) z[j] += bias[l * kMaxW + c0 + j];
+                if (!last) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) z[j] = act_fwd(z[j], a.act);
+                    umma::st_row8(smem + S.h[l], dout, t, c0, z);
+                    umma::st_row8(smem + S.h[l], dout, t, c0 + 8, z + 8);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) out[j] = z[j];
+                }
+            }
+            umma::fence_async_smem();
+            umma::fence_before_sync();
+            __syncthreads();
+        }
+        // ---- loss epilogue (rl.cpp:137-202 semantics, f32) -> dZ_{L-1}
+        float dz[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dz[j] = 0.0f;
+        if (a.mode == 0) {
+            if (valid) a.values_out[row] = out[0];
+        } else if (valid) {
+            if (a.kind == kNetCritic) {  // value MSE: dV = 2 c_v (V - R) / N
+                float verr = out[0] - a.ret[row];
+                dz[0] = static_cast<float>(2.0 * a.value_coef * a.inv_n) * verr;
+                vl_acc += static_cast<float>(a.value_coef * a.inv_n) * verr * verr;
+            } else {  // policy: clipped surrogate (PPO) or A3C policy gradient, + entropy bonus
+                const int A = n.rout[L - 1];
+                float mx = out[0];
+                for (int j = 1; j < A; ++j) mx = fmaxf(mx, out[j]);
+                float den = 0.0f;
+                for (int j = 0; j < A; ++j) den += expf(out[j] - mx);
+                const float lden = logf(den);
+                float p[16], lp[16], H = 0.0f;
+                for (int j = 0; j < A; ++j) {
+                    lp[j] = out[j] - mx - lden;
+                    p[j] = expf(lp[j]);
+                    H -= p[j] * lp[j];
+                }
+                const int act = a.actions[row];
+                const float inv_n = static_cast<float>(a.inv_n);
+                float coef;
+                if (a.kind == kNetPolicyPpo) {
+                    float adv = a.adv[row];
+                    if (a.adv_stats) {
+                        const double sd = a.adv_stats[1];
+                        if (!(sd < 1e-8)) adv = static_cast<float>((adv - a.adv_stats[0]) / (sd + 1e-8));
+                    }
+                    const float ratio = expf(lp[act] - a.logp_old[row]);
+                    const float clipped = fminf(fmaxf(ratio, 1.0f - a.clip_eps), 1.0f + a.clip_eps);
+                    const float s1 = ratio * adv, s2 = clipped * adv;
+                    pl_acc -= fminf(s1, s2) * inv_n;
+                    coef = s1 <= s2 ? -inv_n * ratio * adv : 0.0f;
+                } else {  // A3C: advantage R - V (rl.cpp:188)
+                    const float adv = a.ret[row] - a.values_in[row];
+                    pl_acc -= lp[act] * adv * inv_n;
+                    coef = -inv_n * adv;
+                }
+                en_acc += H * inv_n;
+                const float eci = static_cast<float>(a.entropy_coef) * inv_n;
+                for (int j = 0; j < A; ++j) dz[j] = coef * ((j == act ? 1.0f : 0.0f) - p[j]) + eci * p[j] * (lp[j] + H);
+            }
+        }
+        if (a.mode == 0) continue;  // forward only: the next tile reuses the same buffers safely
+        int cur = 0;
+        umma::st_row8(smem + S.dz[cur], n.dout[L - 1], t, 0, dz);
+        umma::st_row8(smem + S.dz[cur], n.dout[L - 1], t, 8, dz + 8);
+        umma::fence_async_smem();
+        umma::fence_before_sync();
+        __syncthreads();
+        // ---- backward
+        for (int l = L - 1; l >= 0; --l) {
+            const int di = n.din[l], dout = n.dout[l];
+            const uint32_t hin = l == 0 ? sbase + S.x : sbase + S.h[l - 1];
+            const uint32_t dzt = sbase + S.dz[cur];
+            const uint32_t dw_tmem = tmem + 64u + 64u * static_cast<uint32_t>(l >> 1) + ((l & 1) ? (16u << 16) : 0u);
+            if (t == 0) {
+                umma::fence_after_sync();
+                const uint32_t id_dw = umma::idesc_bf16(64, dout, true, true);
+                for (int kb = 0; kb < kRows / 16; ++kb)
+                    umma::mma_bf16(dw_tmem, umma::desc_mnmajor(hin, di, kb), umma::desc_mnmajor(dzt, dout, kb), id_dw,
+                                   !(first && kb == 0));
+                if (l > 0) {
+                    const uint32_t id_dh = umma::idesc_bf16(128, di, false, true);
+                    for (int kb = 0; kb < dout / 16; ++kb)
+                        umma::mma_bf16(tmem, umma::desc_kmajor(dzt, dout, kb),
+                                       umma::desc_mnmajor(sbase + S.wt[l], di, kb), id_dh, kb > 0);
+                }
+                umma::commit(&bar);
+            }
+            // db_l: column sums of dZ_l (overlaps the MMAs; both only read the tile)
+            if (t < dout) {
+                float s = 0.0f;
+                for (int r8 = 0; r8 < kRows; r8 += 8) {
+#pragma unroll
+                    for (int rr = 0; rr < 8; ++rr)
+                        s += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+                            smem + S.dz[cur] + umma::tile_offset(r8 + rr, t, dout)));
+                }
+                dbacc[l * kMaxW + t] += s;
+            }
+            umma::mbar_wait(&bar, phase);
+            phase ^= 1;
+            umma::fence_after_sync();
+            if (l > 0) {
+                const int pw = di;  // width of dZ_{l-1}
+                for (int c0 = 0; c0 < pw; c0 += 16) {
+                    float g[16], y[16];
+                    umma::tmem_ld16(tmem + lane_base + c0, g);
+                    umma::ld_row8(smem + S.h[l - 1], pw, t, c0, y);
+                    umma::ld_row8(smem + S.h[l - 1], pw, t, c0 + 8, y + 8);
+                    umma::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) g[j] = a.act == 0 ? g[j] * (1.0f - y[j] * y[j]) : (y[j] > 0.0f ? g[j] : 0.0f);
+                    umma::st_row8(smem + S.dz[cur ^ 1], pw, t, c0, g);
+                    umma::st_row8(smem + S.dz[cur ^ 1], pw, t, c0 + 8, g + 8);
+                }
+                umma::fence_async_smem();
+                umma::fence_before_sync();
+                __syncthreads();
+                cur ^= 1;
+            }
+        }
+        first = false;
+        umma::fence_before_sync();
+        __syncthreads();
+    }
+
+    // ---- per-CTA partials: dW from TMEM, db from smem, loss terms
+    if (a.mode == 1) {
+        umma::fence_after_sync();
+        float* part = a.partials + static_cast<int64_t>(blockIdx.x) * a.part_stride;
+        const int lane = t & 31;
+        for (int l = 0; l < L; ++l) {
+            const int dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
+            const int lo = (l & 1) ? 16 : 0;
+            const uint32_t col = 64u + 64u * static_cast<uint32_t>(l >> 1);
+            for (int c0 = 0; c0 < dout; c0 += 16) {
+                float v[16];
+                umma::tmem_ld16(tmem + lane_base + col + c0, v);
+                umma::tmem_ld_wait();
+                const int m = lane - lo;  // dW row (input index) held by this lane
+                if (!first && m >= 0 && m < 16) {
+                    const int i = m + 16 * w;
+                    if (i < ri)
+                        for (int j = 0; j < 16; ++j)
+                            if (c0 + j < ro) part[n.woff[l] - n.woff[0] + i * ro + c0 + j] = v[j];
+                }
+            }
+            for (int o = t; o < ro; o += 128) part[n.boff[l] - n.woff[0] + o] = dbacc[l * kMaxW + o];
+        }
+        // loss partials: warp reduce then one atomic per warp into smem (fixed-order sum below)
+        float* ls = reinterpret_cast<float*>(smem + S.loss);
+        for (int off = 16; off > 0; off >>= 1) {
+            pl_acc += __shfl_xor_sync(0xffffffffu, pl_acc, off);
+            vl_acc += __shfl_xor_sync(0xffffffffu, vl_acc, off);
+            en_acc += __shfl_xor_sync(0xffffffffu, en_acc, off);
+        }
+        if (lane == 0) {
+            ls[w * 3 + 0] = pl_acc;
+            ls[w * 3 + 1] = vl_acc;
+            ls[w * 3 + 2] = en_acc;
+        }
+        __syncthreads();
+        if (t < 3) a.loss_partials[blockIdx.x * 3 + t] = ls[t] + ls[3 + t] + ls[6 + t] + ls[9 + t];
+        if (first) {  // CTA owned no tile: zero its partial slot
+            for (int64_t i = t; i < a.part_stride; i += 128) part[i] = 0.0f;
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (w == 0) umma::tmem_free<512>(tmem);
+}
+
+// ------------------------------------------------------------------ partial reduction
+// grads[p] = sum over CTA partials in CTA order (deterministic), written into the flat f32
+// gradient at the net's offset.
+__global__ void k_reduce_partials(const float* __restrict__ part, int nparts, int64_t stride, float* grads) {
+    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= stride) return;
+    float s = 0.0f;
+    for (int p = 0; p < nparts; ++p) s += part[p * stride + i];
+    grads[i] = s;
+}
+
+__global__ void k_reduce_loss(const float* __restrict__ lp, int nparts, int nsets, double ec, float* loss) {
+    if (threadIdx.x != 0) return;
+    double pl = 0, vl = 0, en = 0;
+    for (int s = 0; s < nsets; ++s)
+        for (int p = 0; p < nparts; ++p) {
+            const float* q = lp + (s * nparts + p) * 3;
+            pl += q[0];
+            vl += q[1];
+            en += q[2];
+        }
+    *loss = static_cast<float>(pl + vl - ec * en);
+}
+
+// --------------------------------------------------------------------- GAE (parallel)
+// Thread per stream (rl.cpp:28-95 recurrences in double); per-block sums of adv and adv^2 for
+// the normalisation statistics, combined in fixed block order by k_adv_stats.
+__global__ void __launch_bounds__(256) k_fast_gae(const float* __restrict__ rew, const float* __restrict__ values,
+                                                  const float* __restrict__ done_f,
+                                                  const float* __restrict__ last_value, int64_t T, int64_t R,
+                                                  double gamma, double lam, float* adv, float* ret, bool with_adv,
+                                                  double* block_sums) {
+    __shared__ double s1[256], s2[256];
+    int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    double a1 = 0.0, a2 = 0.0;
+    if (s < R) {
+        const double gl = gamma * lam;
+        const double lv = last_value[s];
+        double acc = 0.0, running = lv;
+        for (int64_t t = T - 1; t >= 0; --t) {
+            int64_t i = t * R + s;
+            bool done = done_f[i] > 0.5f;
+            double r = rew[i];
+            if (with_adv) {
+                double next_v = t + 1 < T ? static_cast<double>(values[i + R]) : lv;
+                if (done) {
+                    next_v = 0.0;
+                    acc = 0.0;
+                }
+                acc = (r + gamma * next_v - static_cast<double>(values[i])) + gl * acc;
+                adv[i] = static_cast<float>(acc);
+                a1 += acc;
+                a2 += acc * acc;
+            }
+            if (done) running = 0.0;
+            running = r + gamma * running;
+            ret[i] = static_cast<float>(running);
+        }
+    }
+    s1[threadIdx.x] = a1;
+    s2[threadIdx.x] = a2;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+        if (threadIdx.x < off) {
+            s1[threadIdx.x] += s1[threadIdx.x + off];
+            s2[threadIdx.x] += s2[threadIdx.x + off];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        block_sums[2 * blockIdx.x] = s1[0];
+        block_sums[2 * blockIdx.x + 1] = s2[0];
+    }
+}
+
+__global__ void k_adv_stats(const double* __restrict__ block_sums, int nblocks, int64_t n, double* stats) {
+    if (threadIdx.x != 0) return;
+    double a1 = 0.0, a2 = 0.0;
+    for (int b = 0; b < nblocks; ++b) {
+        a1 += block_sums[2 * b];
+        a2 += block_sums[2 * b + 1];
+    }
+    double mean = a1 / static_cast<double>(n);
+    double var = a2 / static_cast<double>(n) - mean * mean;
+    stats[0] = mean;
+    stats[1] = sqrt(var > 0.0 ? var : 0.0);
+}
+
+// Parallel episode reward sum (fast numerics): block tree sums in double, fixed block order.
+__global__ void __launch_bounds__(256) k_block_sum(const double* __restrict__ x, int64_t n, double* block_out) {
+    __shared__ double s[256];
+    double a = 0.0;
+    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += static_cast<int64_t>(gridDim.x) * 256) a += x[i];
+    s[threadIdx.x] = a;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+        if (threadIdx.x < off) s[threadIdx.x] += s[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) block_out[blockIdx.x] = s[0];
+}
+
+__global__ void k_sum_blocks(const double* __restrict__ b, int n, double* out) {
+    if (threadIdx.x != 0) return;
+    double a = 0.0;
+    for (int i = 0; i < n; ++i) a += b[i];
+    *out = a;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ launchers
+size_t fast_mlp_smem_bytes(const FastNet& n) { return carve(n).total; }
+
+void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid) {
+    const size_t smem = carve(a.net).total;
+    static size_t configured = 0;
+    if (smem > configured) {
+        FLW_CUDA(cudaFuncSetAttribute(k_fast_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured = smem;
+    }
+    k_fast_mlp<<<grid, 128, smem, s>>>(a);
+}
+
+void fast_reduce_partials(cudaStream_t s, const float* part, int nparts, int64_t stride, float* grads) {
+    k_reduce_partials<<<static_cast<unsigned>((stride + 255) / 256), 256, 0, s>>>(part, nparts, stride, grads);
+}
+
+void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int nparts, int nsets, double entropy_coef,
+                      float* loss) {
+    k_reduce_loss<<<1, 32, 0, s>>>(loss_parts, nparts, nsets, entropy_coef, loss);
+}
+
+void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
+              int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
+              double* block_sums, double* stats) {
+    const int nb = static_cast<int>((R + 255) / 256);
+    k_fast_gae<<<nb, 256, 0, s>>>(rew, values, done_f, last_value, TR / R, R, gamma, lam, adv, ret, with_adv,
+                                  block_sums);
+    if (with_adv) k_adv_stats<<<1, 32, 0, s>>>(block_sums, nb, TR, stats);
+}
+
+void fast_sum(cudaStream_t s, const double* x, int64_t n, double* scratch, double* out) {
+    const int nb = static_cast<int>(std::min<int64_t>(148, (n + 255) / 256));
+    k_block_sum<<<nb, 256, 0, s>>>(x, n, scratch);
+    k_sum_blocks<<<1, 32, 0, s>>>(scratch, nb, out);
+}
+
+}  // namespace flw

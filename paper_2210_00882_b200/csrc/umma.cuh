@@ -1,0 +1,152 @@
+// Minimal sm_100a tensor-core toolkit (tcgen05 / TMEM / mbarrier) written as inline PTX.
+//
+// Operand layout convention used by every fused kernel of this engine: a logical row-major
+// matrix [R x C] of bf16 (C a multiple of 8) lives in shared memory as 8x8 "core matrices"
+// (8 rows x 16 bytes, 128 contiguous bytes), no swizzle:
+//     offset(r, c) = (r / 8) * (C * 16) + (c / 8) * 128 + (r % 8) * 16 + (c % 8) * 2
+// The same bytes serve as
+//     K-major  operand with (MN = r, K = c):  LBO = 128,     SBO = C * 16
+//     MN-major operand with (MN = c, K = r):  LBO = C * 16,  SBO = 128
+// (CUTLASS canonical INTERLEAVE layouts, cute/atom/mma_traits_sm100.hpp make_umma_desc), so an
+// activation tile written once is the A operand of the next forward GEMM (K-major) and the
+// transposed A operand of the weight-gradient GEMM (MN-major) without any data movement.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace flw {
+namespace umma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t tile_offset(int r, int c, int C) {
+    return static_cast<uint32_t>((r >> 3) * (C * 16) + (c >> 3) * 128 + (r & 7) * 16 + (c & 7) * 2);
+}
+
+// Shared-memory matrix descriptor (SmemDescriptor, mma_sm100_desc.hpp): start >> 4 [0,14),
+// LBO >> 4 [16,30), SBO >> 4 [32,46), version 1 [46,48), layout SWIZZLE_NONE (0) [61,64).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    return d;
+}
+
+// Descriptors for k-block `kb` (16 elements of K) of a core-matrix tiled [R x C] matrix.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int C, int kb) {  // MN = rows, K = cols
+    return make_desc(base + static_cast<uint32_t>(kb) * 256u, 128u, static_cast<uint32_t>(C) * 16u);
+}
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int C, int kb) {  // MN = cols, K = rows
+    return make_desc(base + static_cast<uint32_t>(kb) * 2u * static_cast<uint32_t>(C) * 16u,
+                     static_cast<uint32_t>(C) * 16u, 128u);
+}
+
+// Instruction descriptor, kind::f16 with BF16 A/B and F32 accumulate (InstrDescriptor):
+// c_format [4,6)=1, a_format [7,10)=1, b_format [10,13)=1, a_major bit 15, b_major bit 16,
+// N >> 3 at [17,23), M >> 4 at [24,29).
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u) |
+           (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// D[tmem] (+)= A[smem] * B[smem], issued by one thread for the whole CTA.
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         bool accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate ? 1u : 0u));
+}
+
+// Arrive on an mbarrier once every previously issued tcgen05.mma of this thread completed.
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+// Generic-proxy shared-memory writes -> visible to the tensor core's async proxy.
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// TMEM allocation by one full warp; the base address is written to shared memory.
+template <int COLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)),
+                 "n"(COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+
+template <int COLS>
+__device__ __forceinline__ void tmem_free(uint32_t base) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(base), "n"(COLS) : "memory");
+}
+
+// Warp-collective TMEM -> registers: lane i of warp w reads TMEM lane 32*(w%4)+i, 16 / 32
+// consecutive 32-bit columns starting at `taddr` (lane field of taddr = 32*(w%4)).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Writes 8 consecutive columns [c0, c0+8) of row r (one 16-byte core-matrix row).
+__device__ __forceinline__ void st_row8(uint8_t* tile, int C, int r, int c0, const float* v) {
+    uint4 w;
+    w.x = pack_bf16x2(v[0], v[1]);
+    w.y = pack_bf16x2(v[2], v[3]);
+    w.z = pack_bf16x2(v[4], v[5]);
+    w.w = pack_bf16x2(v[6], v[7]);
+    *reinterpret_cast<uint4*>(tile + tile_offset(r, c0, C)) = w;
+}
+
+__device__ __forceinline__ void ld_row8(const uint8_t* tile, int C, int r, int c0, float* v) {
+    uint4 w = *reinterpret_cast<const uint4*>(tile + tile_offset(r, c0, C));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 f = __bfloat1622float2(h[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+    }
+}
+
+}  // namespace umma
+}  // namespace flw

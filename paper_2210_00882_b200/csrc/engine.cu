@@ -432,8 +432,7 @@ void Engine::enq_learn_fast() {
     f.part_stride = s.P - s.P_policy;
     f.loss_partials = b.loss_parts + 3 * b.grid;
     fast_mlp(stream_, f, b.grid);
-    fast_reduce_partials(stream_, b.part_p, b.grid, s.P_policy, b.grads);
-    fast_reduce_partials(stream_, b.part_c, b.grid, s.P - s.P_policy, b.grads + s.P_policy);
+    fast_reduce_partials(stream_, b.part_p, b.part_c, b.grid, s.P_policy, s.P - s.P_policy, b.grads);
     fast_reduce_loss(stream_, b.loss_parts, b.grid, 2, cfg_.entropy_coef, b.loss);
 }
 

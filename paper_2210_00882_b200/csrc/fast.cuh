@@ -45,7 +45,8 @@ struct FastLearnArgs {
 
 size_t fast_mlp_smem_bytes(const FastNet& n);
 void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid);
-void fast_reduce_partials(cudaStream_t s, const float* part, int nparts, int64_t stride, float* grads);
+void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int nparts, int64_t Pp, int64_t Pc,
+                          float* grads);
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int nparts, int nsets, double entropy_coef, float* loss);
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,

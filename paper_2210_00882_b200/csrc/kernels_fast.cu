@@ -6,10 +6,12 @@
 //                             dW_l += H_{l-1}^T dZ_l accumulated in TMEM across all tiles a CTA
 //                             owns, db_l by column sums, per-CTA partials written once at the end.
 //
-// One CTA per SM (persistent, grid = #SMs), 128 threads: thread r owns tile row r == TMEM lane r
-// for every M=128 accumulator; thread 0 issues tcgen05.mma. Operands are bf16 in shared memory
-// in the core-matrix layout of umma.cuh; activations H_l written once serve as the K-major A of
-// the next forward GEMM and the MN-major A of the dW GEMM. Accumulation is f32 (TMEM).
+// One CTA per SM (persistent, grid = #SMs), 256 threads: warp w reads TMEM lane quadrant w%4,
+// so rows r = 32*(w%4) + lane are shared by warps w and w+4, which split each row's columns
+// (16-column chunks alternate between the two halves). Thread 0 issues tcgen05.mma. Operands are
+// bf16 in shared memory in the core-matrix layout of umma.cuh; activations H_l written once
+// serve as the K-major A of the next forward GEMM and as the MN-major A of the dW GEMM.
+// Accumulation is f32 (TMEM).
 // TMEM map (512 columns): [0,64) = Z (M=128 forward / dH accumulator); layer pair (2j, 2j+1)
 // dW accumulators (M=64, "half sub-partition" layout) share columns [64+64j, 128+64j) at
 // lane offsets 0 and 16.
@@ -25,6 +27,7 @@ namespace {
 
 constexpr int kRows = 128;
 constexpr int kMaxW = 64;
+constexpr int kThreads = 256;
 
 struct Smem {  // carve-up of dynamic shared memory (byte offsets)
     uint32_t wt[kMaxLayers], x, h[kMaxLayers], dz[2], bias, dbacc, loss, total;
@@ -52,25 +55,32 @@ __host__ __device__ inline Smem carve(const FastNet& n) {
     s.bias = off;
     off += kMaxLayers * kMaxW * 4;
     s.dbacc = off;
-    off += kMaxLayers * kMaxW * 4;
+    off += 2 * kMaxLayers * kMaxW * 4;  // two row halves
     s.loss = off;
-    off += 4 * 4 * 4;
+    off += 8 * 3 * 4;
     // slack: M=64 MN-major reads of narrow tiles run past their end (rows >= din are ignored)
     s.total = off + 2048;
     return s;
 }
 
-__device__ __forceinline__ float act_fwd(float z, int act) {
-    return act == 0 ? tanhf(z) : (z > 0.0f ? z : 0.0f);
+// MUFU tanh (max rel. error ~2^-11): the activation is rounded to bf16 (2^-8) right after.
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
-__global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
+__device__ __forceinline__ float act_fwd(float z, int act) { return act == 0 ? tanh_fast(z) : (z > 0.0f ? z : 0.0f); }
+
+__global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tslot;
     const FastNet& n = a.net;
     const Smem S = carve(n);
-    const int t = threadIdx.x, w = t >> 5;
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    const int quad = w & 3, half = w >> 2;
+    const int r = 32 * quad + lane;  // tile row == TMEM lane
     const int L = n.L;
     float* bias = reinterpret_cast<float*>(smem + S.bias);
     float* dbacc = reinterpret_cast<float*>(smem + S.dbacc);
@@ -79,17 +89,14 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
     for (int l = 0; l < L; ++l) {
         const int di = n.din[l], dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
         const float* W = a.params + n.woff[l];
-        for (int i = t; i < dout * di; i += 128) {
+        for (int i = t; i < dout * di; i += kThreads) {
             int o = i / di, c = i % di;
             float v = (o < ro && c < ri) ? W[c * ro + o] : 0.0f;
             *reinterpret_cast<__nv_bfloat16*>(smem + S.wt[l] + umma::tile_offset(o, c, di)) = __float2bfloat16(v);
         }
-        for (int o = t; o < kMaxW; o += 128) {
-            bias[l * kMaxW + o] = o < ro ? a.params[n.boff[l] + o] : 0.0f;
-            dbacc[l * kMaxW + o] = 0.0f;
-        }
+        for (int o = t; o < kMaxW; o += kThreads) bias[l * kMaxW + o] = o < ro ? a.params[n.boff[l] + o] : 0.0f;
     }
-    if (t < 16) reinterpret_cast<float*>(smem + S.loss)[t] = 0.0f;
+    for (int i = t; i < 2 * kMaxLayers * kMaxW; i += kThreads) dbacc[i] = 0.0f;
     umma::fence_async_smem();
     if (w == 0) umma::tmem_alloc<512>(&tslot);
     if (t == 0) {
@@ -100,7 +107,7 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
     __syncthreads();
     umma::fence_after_sync();
     const uint32_t tmem = tslot;
-    const uint32_t lane_base = static_cast<uint32_t>(32 * w) << 16;
+    const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
     const uint32_t sbase = umma::smem_u32(smem);
     uint32_t phase = 0;
     float pl_acc = 0.0f, vl_acc = 0.0f, en_acc = 0.0f;
@@ -108,19 +115,17 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
     const int64_t ntiles = (a.rows + kRows - 1) / kRows;
 
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t row = tile * kRows + t;
+        const int64_t row = tile * kRows + r;
         const bool valid = row < a.rows;
-        // ---- input tile (f32 -> bf16), zero padded columns and rows
-        {
+        // ---- input tile (f32 -> bf16), zero padded columns and rows; halves split 8-col chunks
+        for (int c0 = 8 * half; c0 < n.din[0]; c0 += 16) {
             float v[8];
-            for (int c0 = 0; c0 < n.din[0]; c0 += 8) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    int c = c0 + j;
-                    v[j] = (valid && c < a.in_cols) ? a.X[row * a.in_cols + c] : 0.0f;
-                }
-                umma::st_row8(smem + S.x, n.din[0], t, c0, v);
+            for (int j = 0; j < 8; ++j) {
+                int c = c0 + j;
+                v[j] = (valid && c < a.in_cols) ? a.X[row * a.in_cols + c] : 0.0f;
             }
+            umma::st_row8(smem + S.x, n.din[0], r, c0, v);
         }
         umma::fence_async_smem();
         umma::fence_before_sync();
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
             phase ^= 1;
             umma::fence_after_sync();
             const bool last = l + 1 == L;
-            for (int c0 = 0; c0 < dout; c0 += 16) {
+            for (int c0 = 16 * half; c0 < dout; c0 += 32) {
                 float z[16];
                 umma::tmem_ld16(tmem + lane_base + c0, z);
                 umma::tmem_ld_wait();
@@ -151,8 +156,8 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
                 if (!last) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) z[j] = act_fwd(z[j], a.act);
-                    umma::st_row8(smem + S.h[l], dout, t, c0, z);
-                    umma::st_row8(smem + S.h[l], dout, t, c0 + 8, z + 8);
+                    umma::st_row8(smem + S.h[l], dout, r, c0, z);
+                    umma::st_row8(smem + S.h[l], dout, r, c0 + 8, z + 8);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) out[j] = z[j];
@@ -162,58 +167,64 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
             umma::fence_before_sync();
             __syncthreads();
         }
-        // ---- loss epilogue (rl.cpp:137-202 semantics, f32) -> dZ_{L-1}
-        float dz[16];
+        // ---- loss epilogue (rl.cpp:137-202 semantics, f32) -> dZ_{L-1}; the output layer is one
+        // 16-column chunk, owned by the half-0 warps.
+        if (half == 0) {
+            float dz[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) dz[j] = 0.0f;
-        if (a.mode == 0) {
-            if (valid) a.values_out[row] = out[0];
-        } else if (valid) {
-            if (a.kind == kNetCritic) {  // value MSE: dV = 2 c_v (V - R) / N
-                float verr = out[0] - a.ret[row];
-                dz[0] = static_cast<float>(2.0 * a.value_coef * a.inv_n) * verr;
-                vl_acc += static_cast<float>(a.value_coef * a.inv_n) * verr * verr;
-            } else {  // policy: clipped surrogate (PPO) or A3C policy gradient, + entropy bonus
-                const int A = n.rout[L - 1];
-                float mx = out[0];
-                for (int j = 1; j < A; ++j) mx = fmaxf(mx, out[j]);
-                float den = 0.0f;
-                for (int j = 0; j < A; ++j) den += expf(out[j] - mx);
-                const float lden = logf(den);
-                float p[16], lp[16], H = 0.0f;
-                for (int j = 0; j < A; ++j) {
-                    lp[j] = out[j] - mx - lden;
-                    p[j] = expf(lp[j]);
-                    H -= p[j] * lp[j];
-                }
-                const int act = a.actions[row];
-                const float inv_n = static_cast<float>(a.inv_n);
-                float coef;
-                if (a.kind == kNetPolicyPpo) {
-                    float adv = a.adv[row];
-                    if (a.adv_stats) {
-                        const double sd = a.adv_stats[1];
-                        if (!(sd < 1e-8)) adv = static_cast<float>((adv - a.adv_stats[0]) / (sd + 1e-8));
+            for (int j = 0; j < 16; ++j) dz[j] = 0.0f;
+            if (a.mode == 0) {
+                if (valid) a.values_out[row] = out[0];
+            } else if (valid) {
+                if (a.kind == kNetCritic) {  // value MSE: dV = 2 c_v (V - R) / N
+                    float verr = out[0] - a.ret[row];
+                    dz[0] = static_cast<float>(2.0 * a.value_coef * a.inv_n) * verr;
+                    vl_acc += static_cast<float>(a.value_coef * a.inv_n) * verr * verr;
+                } else {  // policy: clipped surrogate (PPO) or A3C policy gradient, + entropy bonus
+                    const int A = n.rout[L - 1];
+                    float mx = out[0];
+                    for (int j = 1; j < A; ++j) mx = fmaxf(mx, out[j]);
+                    float den = 0.0f;
+                    for (int j = 0; j < A; ++j) den += expf(out[j] - mx);
+                    const float lden = logf(den);
+                    float p[16], lp[16], H = 0.0f;
+                    for (int j = 0; j < A; ++j) {
+                        lp[j] = out[j] - mx - lden;
+                        p[j] = expf(lp[j]);
+                        H -= p[j] * lp[j];
                     }
-                    const float ratio = expf(lp[act] - a.logp_old[row]);
-                    const float clipped = fminf(fmaxf(ratio, 1.0f - a.clip_eps), 1.0f + a.clip_eps);
-                    const float s1 = ratio * adv, s2 = clipped * adv;
-                    pl_acc -= fminf(s1, s2) * inv_n;
-                    coef = s1 <= s2 ? -inv_n * ratio * adv : 0.0f;
-                } else {  // A3C: advantage R - V (rl.cpp:188)
-                    const float adv = a.ret[row] - a.values_in[row];
-                    pl_acc -= lp[act] * adv * inv_n;
-                    coef = -inv_n * adv;
+                    const int act = a.actions[row];
+                    const float inv_n = static_cast<float>(a.inv_n);
+                    float coef;
+                    if (a.kind == kNetPolicyPpo) {
+                        float adv = a.adv[row];
+                        if (a.adv_stats) {
+                            const double sd = a.adv_stats[1];
+                            if (!(sd < 1e-8)) adv = static_cast<float>((adv - a.adv_stats[0]) / (sd + 1e-8));
+                        }
+                        const float ratio = expf(lp[act] - a.logp_old[row]);
+                        const float clipped = fminf(fmaxf(ratio, 1.0f - a.clip_eps), 1.0f + a.clip_eps);
+                        const float s1 = ratio * adv, s2 = clipped * adv;
+                        pl_acc -= fminf(s1, s2) * inv_n;
+                        coef = s1 <= s2 ? -inv_n * ratio * adv : 0.0f;
+                    } else {  // A3C: advantage R - V (rl.cpp:188)
+                        const float adv = a.ret[row] - a.values_in[row];
+                        pl_acc -= lp[act] * adv * inv_n;
+                        coef = -inv_n * adv;
+                    }
+                    en_acc += H * inv_n;
+                    const float eci = static_cast<float>(a.entropy_coef) * inv_n;
+                    for (int j = 0; j < A; ++j)
+                        dz[j] = coef * ((j == act ? 1.0f : 0.0f) - p[j]) + eci * p[j] * (lp[j] + H);
                 }
-                en_acc += H * inv_n;
-                const float eci = static_cast<float>(a.entropy_coef) * inv_n;
-                for (int j = 0; j < A; ++j) dz[j] = coef * ((j == act ? 1.0f : 0.0f) - p[j]) + eci * p[j] * (lp[j] + H);
+            }
+            if (a.mode == 1) {
+                umma::st_row8(smem + S.dz[0], n.dout[L - 1], r, 0, dz);
+                umma::st_row8(smem + S.dz[0], n.dout[L - 1], r, 8, dz + 8);
             }
         }
         if (a.mode == 0) continue;  // forward only: the next tile reuses the same buffers safely
         int cur = 0;
-        umma::st_row8(smem + S.dz[cur], n.dout[L - 1], t, 0, dz);
-        umma::st_row8(smem + S.dz[cur], n.dout[L - 1], t, 8, dz + 8);
         umma::fence_async_smem();
         umma::fence_before_sync();
         __syncthreads();
@@ -237,32 +248,30 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
                 }
                 umma::commit(&bar);
             }
-            // db_l: column sums of dZ_l (overlaps the MMAs; both only read the tile)
-            if (t < dout) {
+            // db_l: column sums of dZ_l, two row halves (overlaps the MMAs; both only read the tile)
+            if (t < 2 * dout) {
+                const int c = t % dout, h2 = t / dout;
                 float s = 0.0f;
-                for (int r8 = 0; r8 < kRows; r8 += 8) {
-#pragma unroll
-                    for (int rr = 0; rr < 8; ++rr)
-                        s += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
-                            smem + S.dz[cur] + umma::tile_offset(r8 + rr, t, dout)));
-                }
-                dbacc[l * kMaxW + t] += s;
+                for (int rr = 64 * h2; rr < 64 * h2 + 64; ++rr)
+                    s += __bfloat162float(
+                        *reinterpret_cast<const __nv_bfloat16*>(smem + S.dz[cur] + umma::tile_offset(rr, c, dout)));
+                dbacc[(h2 * kMaxLayers + l) * kMaxW + c] += s;
             }
             umma::mbar_wait(&bar, phase);
             phase ^= 1;
             umma::fence_after_sync();
             if (l > 0) {
                 const int pw = di;  // width of dZ_{l-1}
-                for (int c0 = 0; c0 < pw; c0 += 16) {
+                for (int c0 = 16 * half; c0 < pw; c0 += 32) {
                     float g[16], y[16];
                     umma::tmem_ld16(tmem + lane_base + c0, g);
-                    umma::ld_row8(smem + S.h[l - 1], pw, t, c0, y);
-                    umma::ld_row8(smem + S.h[l - 1], pw, t, c0 + 8, y + 8);
+                    umma::ld_row8(smem + S.h[l - 1], pw, r, c0, y);
+                    umma::ld_row8(smem + S.h[l - 1], pw, r, c0 + 8, y + 8);
                     umma::tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 16; ++j) g[j] = a.act == 0 ? g[j] * (1.0f - y[j] * y[j]) : (y[j] > 0.0f ? g[j] : 0.0f);
-                    umma::st_row8(smem + S.dz[cur ^ 1], pw, t, c0, g);
-                    umma::st_row8(smem + S.dz[cur ^ 1], pw, t, c0 + 8, g + 8);
+                    umma::st_row8(smem + S.dz[cur ^ 1], pw, r, c0, g);
+                    umma::st_row8(smem + S.dz[cur ^ 1], pw, r, c0 + 8, g + 8);
                 }
                 umma::fence_async_smem();
                 umma::fence_before_sync();
@@ -279,26 +288,25 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
     if (a.mode == 1) {
         umma::fence_after_sync();
         float* part = a.partials + static_cast<int64_t>(blockIdx.x) * a.part_stride;
-        const int lane = t & 31;
         for (int l = 0; l < L; ++l) {
             const int dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
             const int lo = (l & 1) ? 16 : 0;
             const uint32_t col = 64u + 64u * static_cast<uint32_t>(l >> 1);
-            for (int c0 = 0; c0 < dout; c0 += 16) {
+            for (int c0 = 16 * half; c0 < dout; c0 += 32) {
                 float v[16];
                 umma::tmem_ld16(tmem + lane_base + col + c0, v);
                 umma::tmem_ld_wait();
                 const int m = lane - lo;  // dW row (input index) held by this lane
                 if (!first && m >= 0 && m < 16) {
-                    const int i = m + 16 * w;
+                    const int i = m + 16 * quad;
                     if (i < ri)
                         for (int j = 0; j < 16; ++j)
                             if (c0 + j < ro) part[n.woff[l] - n.woff[0] + i * ro + c0 + j] = v[j];
                 }
             }
-            for (int o = t; o < ro; o += 128) part[n.boff[l] - n.woff[0] + o] = dbacc[l * kMaxW + o];
+            for (int o = t; o < ro; o += kThreads)
+                part[n.boff[l] - n.woff[0] + o] = dbacc[l * kMaxW + o] + dbacc[(kMaxLayers + l) * kMaxW + o];
         }
-        // loss partials: warp reduce then one atomic per warp into smem (fixed-order sum below)
         float* ls = reinterpret_cast<float*>(smem + S.loss);
         for (int off = 16; off > 0; off >>= 1) {
             pl_acc += __shfl_xor_sync(0xffffffffu, pl_acc, off);
@@ -311,9 +319,13 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
             ls[w * 3 + 2] = en_acc;
         }
         __syncthreads();
-        if (t < 3) a.loss_partials[blockIdx.x * 3 + t] = ls[t] + ls[3 + t] + ls[6 + t] + ls[9 + t];
+        if (t < 3) {
+            float s = 0.0f;
+            for (int k = 0; k < 8; ++k) s += ls[k * 3 + t];
+            a.loss_partials[blockIdx.x * 3 + t] = s;
+        }
         if (first) {  // CTA owned no tile: zero its partial slot
-            for (int64_t i = t; i < a.part_stride; i += 128) part[i] = 0.0f;
+            for (int64_t i = t; i < a.part_stride; i += kThreads) part[i] = 0.0f;
         }
     }
     umma::fence_before_sync();
@@ -322,32 +334,42 @@ __global__ void __launch_bounds__(128, 1) k_fast_mlp(FastLearnArgs a) {
 }
 
 // ------------------------------------------------------------------ partial reduction
-// grads[p] = sum over CTA partials in CTA order (deterministic), written into the flat f32
-// gradient at the net's offset.
-__global__ void k_reduce_partials(const float* __restrict__ part, int nparts, int64_t stride, float* grads) {
+// grads[p] = sum over CTA partials in CTA order (deterministic); both nets in one launch, the
+// critic's partials following the policy's in the flat gradient.
+__global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict__ pp, const float* __restrict__ pc,
+                                                         int nparts, int64_t Pp, int64_t Pc, float* grads) {
     int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= stride) return;
+    if (i >= Pp + Pc) return;
+    const float* src = i < Pp ? pp + i : pc + (i - Pp);
+    const int64_t stride = i < Pp ? Pp : Pc;
     float s = 0.0f;
-    for (int p = 0; p < nparts; ++p) s += part[p * stride + i];
+#pragma unroll 8
+    for (int p = 0; p < nparts; ++p) s += src[p * stride];
     grads[i] = s;
 }
 
 __global__ void k_reduce_loss(const float* __restrict__ lp, int nparts, int nsets, double ec, float* loss) {
-    if (threadIdx.x != 0) return;
+    const int lane = threadIdx.x;
     double pl = 0, vl = 0, en = 0;
     for (int s = 0; s < nsets; ++s)
-        for (int p = 0; p < nparts; ++p) {
+        for (int p = lane; p < nparts; p += 32) {
             const float* q = lp + (s * nparts + p) * 3;
             pl += q[0];
             vl += q[1];
             en += q[2];
         }
-    *loss = static_cast<float>(pl + vl - ec * en);
+    for (int off = 16; off > 0; off >>= 1) {
+        pl += __shfl_xor_sync(0xffffffffu, pl, off);
+        vl += __shfl_xor_sync(0xffffffffu, vl, off);
+        en += __shfl_xor_sync(0xffffffffu, en, off);
+    }
+    if (lane == 0) *loss = static_cast<float>(pl + vl - ec * en);
 }
 
 // --------------------------------------------------------------------- GAE (parallel)
-// Thread per stream (rl.cpp:28-95 recurrences in double); per-block sums of adv and adv^2 for
-// the normalisation statistics, combined in fixed block order by k_adv_stats.
+// Thread per stream (rl.cpp:28-95 recurrences in double); the T-loop is processed in chunks of 8
+// steps whose loads are issued together. Per-block sums of adv and adv^2 feed the normalisation
+// statistics, combined in fixed block order by k_adv_stats.
 __global__ void __launch_bounds__(256) k_fast_gae(const float* __restrict__ rew, const float* __restrict__ values,
                                                   const float* __restrict__ done_f,
                                                   const float* __restrict__ last_value, int64_t T, int64_t R,
@@ -359,25 +381,39 @@ __global__ void __launch_bounds__(256) k_fast_gae(const float* __restrict__ rew,
     if (s < R) {
         const double gl = gamma * lam;
         const double lv = last_value[s];
-        double acc = 0.0, running = lv;
-        for (int64_t t = T - 1; t >= 0; --t) {
-            int64_t i = t * R + s;
-            bool done = done_f[i] > 0.5f;
-            double r = rew[i];
-            if (with_adv) {
-                double next_v = t + 1 < T ? static_cast<double>(values[i + R]) : lv;
-                if (done) {
-                    next_v = 0.0;
-                    acc = 0.0;
+        double acc = 0.0, running = lv, next_v = lv;
+        for (int64_t hi = T - 1; hi >= 0; hi -= 8) {
+            float rr[8], vv[8], dd[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int64_t tt = hi - j;
+                if (tt >= 0) {
+                    int64_t i = tt * R + s;
+                    rr[j] = rew[i];
+                    vv[j] = values[i];
+                    dd[j] = done_f[i];
                 }
-                acc = (r + gamma * next_v - static_cast<double>(values[i])) + gl * acc;
-                adv[i] = static_cast<float>(acc);
-                a1 += acc;
-                a2 += acc * acc;
             }
-            if (done) running = 0.0;
-            running = r + gamma * running;
-            ret[i] = static_cast<float>(running);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int64_t tt = hi - j;
+                if (tt < 0) break;
+                int64_t i = tt * R + s;
+                const bool done = dd[j] > 0.5f;
+                const double r = rr[j], v = vv[j];
+                if (with_adv) {
+                    double nv = done ? 0.0 : next_v;
+                    if (done) acc = 0.0;
+                    acc = (r + gamma * nv - v) + gl * acc;
+                    adv[i] = static_cast<float>(acc);
+                    a1 += acc;
+                    a2 += acc * acc;
+                }
+                next_v = v;
+                if (done) running = 0.0;
+                running = r + gamma * running;
+                ret[i] = static_cast<float>(running);
+            }
         }
     }
     s1[threadIdx.x] = a1;
@@ -442,11 +478,13 @@ void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid) {
         FLW_CUDA(cudaFuncSetAttribute(k_fast_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         configured = smem;
     }
-    k_fast_mlp<<<grid, 128, smem, s>>>(a);
+    k_fast_mlp<<<grid, kThreads, smem, s>>>(a);
 }
 
-void fast_reduce_partials(cudaStream_t s, const float* part, int nparts, int64_t stride, float* grads) {
-    k_reduce_partials<<<static_cast<unsigned>((stride + 255) / 256), 256, 0, s>>>(part, nparts, stride, grads);
+void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int nparts, int64_t Pp, int64_t Pc,
+                          float* grads) {
+    k_reduce_partials<<<static_cast<unsigned>((Pp + Pc + 255) / 256), 256, 0, s>>>(part_p, part_c, nparts, Pp, Pc,
+                                                                                   grads);
 }
 
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int nparts, int nsets, double entropy_coef,

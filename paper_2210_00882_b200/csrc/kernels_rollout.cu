@@ -15,7 +15,8 @@ namespace flw {
 namespace {
 
 constexpr int kEnvsPerCta = 32;
-constexpr int kThreads = 128;  // 4 threads (a quad) per env
+constexpr int kPerEnv = 8;                        // threads per env: each owns 8 of <= 64 outputs
+constexpr int kThreads = kEnvsPerCta * kPerEnv;   // 256
 constexpr int kHStride = 68;   // activation row stride (floats): 16B aligned, spreads banks
 
 __host__ __device__ inline int pad4(int x) { return (x + 3) & ~3; }
@@ -47,7 +48,7 @@ template <int ENV>
 __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* __restrict__ ctx, FastRolloutArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const RolloutSmem S = rollout_carve(a);
-    const int t = threadIdx.x, q = t & 3, r = t >> 2;
+    const int t = threadIdx.x, q = t & (kPerEnv - 1), r = t / kPerEnv;
     const int64_t e = static_cast<int64_t>(blockIdx.x) * kEnvsPerCta + r;
     const bool live = e < a.E;
     const int S_ = a.S, A = a.A;
@@ -89,23 +90,42 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             const float* hin = reinterpret_cast<const float*>(smem + S.h[cur]) + r * kHStride;
             float* hout = reinterpret_cast<float*>(smem + S.h[cur ^ 1]) + r * kHStride;
             const bool last = l + 1 == a.L;
-            // thread q computes output groups of 4 starting at 4q, stride 16
-            for (int o0 = 4 * q; o0 < op; o0 += 16) {
-                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            // thread q owns output groups [4q, 4q+4) and [32+4q, 36+4q): two float4 accumulators,
+            // one h load per input feeds 8 FMAs (in-order f32 accumulation over the inputs)
+            const int o0 = 4 * q, o1 = 32 + 4 * q;
+            const bool has0 = o0 < op, has1 = o1 < op;
+            if (has0) {
+                float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+                const float4* W4 = reinterpret_cast<const float4*>(W);
+                const int op4 = op / 4;
+#pragma unroll 4
                 for (int i = 0; i < in; ++i) {
                     const float x = hin[i];
-                    const float4 w = *reinterpret_cast<const float4*>(W + i * op + o0);
-                    acc.x = fmaf(x, w.x, acc.x);
-                    acc.y = fmaf(x, w.y, acc.y);
-                    acc.z = fmaf(x, w.z, acc.z);
-                    acc.w = fmaf(x, w.w, acc.w);
+                    const float4 w0 = W4[i * op4 + q];
+                    acc0.x = fmaf(x, w0.x, acc0.x);
+                    acc0.y = fmaf(x, w0.y, acc0.y);
+                    acc0.z = fmaf(x, w0.z, acc0.z);
+                    acc0.w = fmaf(x, w0.w, acc0.w);
+                    if (has1) {
+                        const float4 w1 = W4[i * op4 + 8 + q];
+                        acc1.x = fmaf(x, w1.x, acc1.x);
+                        acc1.y = fmaf(x, w1.y, acc1.y);
+                        acc1.z = fmaf(x, w1.z, acc1.z);
+                        acc1.w = fmaf(x, w1.w, acc1.w);
+                    }
                 }
-                float v[4] = {acc.x + B[o0], acc.y + B[o0 + 1], acc.z + B[o0 + 2], acc.w + B[o0 + 3]};
+                float v[8] = {acc0.x + B[o0], acc0.y + B[o0 + 1], acc0.z + B[o0 + 2], acc0.w + B[o0 + 3],
+                              acc1.x, acc1.y, acc1.z, acc1.w};
+                if (has1) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[4 + j] += B[o1 + j];
+                }
                 if (!last) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) v[j] = a.act == 0 ? tanhf(v[j]) : fmaxf(v[j], 0.0f);
+                    for (int j = 0; j < 8; ++j) v[j] = a.act == 0 ? tanhf(v[j]) : fmaxf(v[j], 0.0f);
                 }
                 *reinterpret_cast<float4*>(hout + o0) = make_float4(v[0], v[1], v[2], v[3]);
+                if (has1) *reinterpret_cast<float4*>(hout + o1) = make_float4(v[4], v[5], v[6], v[7]);
             }
             __syncthreads();
             cur ^= 1;
@@ -121,8 +141,11 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                 mx = dmaxd(mx, l[c]);
             }
             double den = 0.0;
-            for (int c = 0; c < A; ++c) den = __dadd_rn(den, exp(__dsub_rn(l[c], mx)));
-            for (int c = 0; c < A; ++c) p[c] = f32r(__ddiv_rn(exp(__dsub_rn(l[c], mx)), den));
+            for (int c = 0; c < A; ++c) {
+                p[c] = exp(__dsub_rn(l[c], mx));  // the same value the reference computes twice
+                den = __dadd_rn(den, p[c]);
+            }
+            for (int c = 0; c < A; ++c) p[c] = f32r(__ddiv_rn(p[c], den));
             const double u = rng_uniform(rng_key(a.seed, kActionStream, ep, static_cast<uint64_t>(step),
                                                  static_cast<uint64_t>(a.env_lo + e)));
             double cum = 0.0;
@@ -190,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
         // the next step's input must sit in buffer 0: copy if the layer count left it in 1
         if ((cur ^ 1) != 0) {
             float* h0w = reinterpret_cast<float*>(smem + S.h[0]) + r * kHStride;
-            for (int j = q; j < S_; j += 4) h0w[j] = next[j];
+            for (int j = q; j < S_; j += kPerEnv) h0w[j] = next[j];
             __syncthreads();
         }
     }

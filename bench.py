@@ -144,11 +144,70 @@ def run_reference(envs: int, replicas: int, episodes: int, seed: int = 7) -> dic
 
 
 def reference_sample(cores: int, target_s: float) -> tuple[int, int]:
-    """Bounded sample: envs so that one episode is ~target_s on `cores` threads (C2 costs
-    ~0.16 s of one core per env per episode), one replica per core."""
-    envs = int(max(cores, min(ENVS_PER_GPU, round(target_s * cores / 0.16))))
+    """Bounded sample: envs so that one episode is ~target_s on `cores` threads (C2 cost measured
+    on the GPU box host: ~0.023 s of one core per env per episode), one replica per core."""
+    envs = int(max(cores, min(ENVS_PER_GPU, round(target_s * cores / 0.023))))
     envs -= envs % cores
     return max(envs, cores), cores
+
+
+def mlp_macs(dims) -> tuple[int, int]:
+    """(sum in*out over layers, same without the first layer) for one MLP."""
+    macs = [dims[i] * dims[i + 1] for i in range(len(dims) - 1)]
+    return sum(macs), sum(macs[1:])
+
+
+def load_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+def ncu_traffic(tag: str):
+    """dram read+write bytes per launch of kernel `tag` from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get(tag)
+    return None
+
+
+def roofline_for(tag: str, ms: float, envs: int, peaks: dict) -> dict:
+    """Dominant-kernel roofline. Learn kernels are tensor-core GEMM chains: algorithmic FLOPs =
+    2 * rows * (forward + dW + dH) MACs of that net (real, unpadded dims)."""
+    pol = [17] + HIDDEN + [6]
+    cri = [17] + HIDDEN + [1]
+    rows = envs * T_STEPS
+    if tag in ("learn_policy", "learn_critic", "critic_fwd"):
+        dims = pol if tag == "learn_policy" else cri
+        fwd, dh = mlp_macs(dims)
+        flops = 2.0 * rows * (fwd if tag == "critic_fwd" else fwd + fwd + dh)
+        ach = flops / (ms * 1e-3) / 1e12
+        return {"kernel": tag, "bound": "tensor", "achieved": ach, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": ach / peaks["bf16_tflops"], "traffic": ncu_traffic(tag), "peak_source": peaks["source"],
+                "work_per_launch": f"{flops:.4g} FLOP ({rows} rows x 2 x MACs)", "launch_ms": ms}
+    if tag == "rollout":
+        # per env-step: (8S+9) B trajectory/env bytes (SURVEY §8d) + policy MLP FLOPs on CUDA cores
+        nbytes = envs * T_STEPS * (8 * 17 + 9)
+        ach = nbytes / (ms * 1e-3) / 1e9
+        return {"kernel": tag, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": ncu_traffic(tag), "peak_source": peaks["source"],
+                "work_per_launch": f"{nbytes} B ((8S+9) B x {envs * T_STEPS} env-steps)", "launch_ms": ms}
+    return {"kernel": tag, "bound": "hbm", "achieved": None, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": None,
+            "traffic": None}
+
+
+def hbm_microbenchmarks(peaks: dict) -> dict:
+    """Env step / GAE / Adam at scaled sizes (inputs >> 126 MB L2), SURVEY §8(d)."""
+    from paper_2210_00882_b200.api import microbench
+
+    out = {}
+    for name, n in (("env_step", 1 << 21), ("gae", 1 << 26), ("adam", 1 << 27)):
+        ms, nbytes = microbench(name, n, 10)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"n": n, "ms": ms, "bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peaks["hbm_gbs"]}
+    return out
 
 
 def cpu_baseline(target_s: float = 12.0) -> dict:
@@ -205,7 +264,8 @@ def bench_ours(args, world, rank, local):
         obj = [DpdEngine.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         eng.comm_init(obj[0], rank, world)
-    # warm-up (also captures the episode graph)
+    # warm-up (also captures the episode graph, with CUDA-event probes around the main kernels)
+    eng.enable_probes(True)
     eng.run_episodes(0, args.warmup)
     barrier(world)
     torch.cuda.synchronize()
@@ -213,6 +273,7 @@ def bench_ours(args, world, rank, local):
         dev_ms = eng.run_episodes(args.warmup, args.steps)
     torch.cuda.synchronize()
     barrier(world)
+    probes = eng.probe_times()  # per-kernel ms of the last timed episode
     dev_ms = max_over_ranks(dev_ms, world)
     value = total * T_STEPS * args.steps / (dev_ms / 1e3)
     stats = eng.stats()
@@ -229,6 +290,11 @@ def bench_ours(args, world, rank, local):
 
     if rank != 0:
         return
+    peaks = load_peaks()
+    episode_ms = dev_ms / args.steps
+    shares = {k: {"ms_per_episode": sum(v), "launches": len(v), "share": sum(v) / episode_ms} for k, v in probes.items()}
+    dom = max(shares, key=lambda k: shares[k]["ms_per_episode"]) if shares else None
+    roofline = roofline_for(dom, sum(probes[dom]) / len(probes[dom]), ENVS_PER_GPU, peaks) if dom else None
     line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
@@ -238,8 +304,9 @@ def bench_ours(args, world, rank, local):
                                    "train_iters=4, dp-d fused loop", "envs_total": total, "envs_per_gpu":
                        ENVS_PER_GPU, "numerics": args.numerics, "parallelism": f"dp{world}",
                        "l2": "per-episode working set (activations, ~0.9 GB) exceeds the 126 MB L2"},
-            "episode_ms": dev_ms / args.steps, "gpu_launches": stats["graph_kernels"] * args.steps,
-            "clocks": clk.summary(), "e2e": e2e}
+            "episode_ms": episode_ms, "gpu_launches": stats["graph_kernels"] * args.steps,
+            "clocks": clk.summary(), "e2e": e2e, "roofline": roofline, "kernel_shares": shares}
+    line["hbm_kernels"] = hbm_microbenchmarks(peaks)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)

@@ -110,6 +110,18 @@ int flw_dpd_tensor_size(const flw_dpd* e, const char* name, int64_t* n);
 int flw_dpd_read(flw_dpd* e, const char* name, double* out, int64_t n);
 int flw_dpd_write(flw_dpd* e, const char* name, const double* in, int64_t n);
 
+/* Scaled-size HBM microbenchmark of one element-wise DP-D kernel on the current device:
+ * which = "env_step" (n envs), "gae" (n = T*E rows, T=32) or "adam" (n params). Returns the
+ * mean ms per launch (CUDA events, after warm-up) and the algorithmic bytes per launch. */
+int flw_microbench(const char* which, int64_t n, int iters, double* ms_per_launch, double* bytes_per_launch);
+
+/* Per-kernel device times (ms) of the most recent episode replay, measured by CUDA events
+ * captured inside the episode graph; probes are enabled by this call (the graph is rebuilt).
+ * JSON object: {"rollout": x, "critic_fwd": [..], "learn_policy": [..], "learn_critic": [..],
+ * "gae": [..], "reduce": [..], "adam": [..]}; malloc'd, release with flw_string_free. */
+int flw_dpd_enable_probes(flw_dpd* e, int on);
+int flw_dpd_probe_times(flw_dpd* e, char** json);
+
 /* Diagnostic (tests only): one tcgen05.mma GEMM D[M,N] = op(A) op(B) through the engine's
  * shared-memory operand convention. a_mn=0: A is [M,K] row-major; a_mn=1: A is stored [K,M].
  * b_mn=0: B is stored [N,K]; b_mn=1: B is [K,N]. lane_off = TMEM lane offset of D (M=64 only). */

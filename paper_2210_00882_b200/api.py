@@ -58,6 +58,13 @@ class Program:
         return N.take_string(csv), json.loads(N.take_string(summ))
 
 
+def microbench(which: str, n: int, iters: int = 10) -> tuple[float, float]:
+    """flw_microbench: (ms per launch, algorithmic bytes per launch) of an element-wise kernel."""
+    ms, nbytes = C.c_double(), C.c_double()
+    N.check(N.lib().flw_microbench(which.encode(), n, iters, C.byref(ms), C.byref(nbytes)))
+    return ms.value, nbytes.value
+
+
 def _dp(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
@@ -108,6 +115,16 @@ class DpdEngine:
 
     def reinit(self, seed: int):
         N.check(N.lib().flw_dpd_reinit(self._h, seed))
+
+    def enable_probes(self, on: bool = True):
+        """CUDA-event probes around the main kernels inside the episode graph."""
+        N.check(N.lib().flw_dpd_enable_probes(self._h, int(on)))
+
+    def probe_times(self) -> dict:
+        """Per-kernel device ms of the most recent episode replay."""
+        out = C.c_void_p()
+        N.check(N.lib().flw_dpd_probe_times(self._h, C.byref(out)))
+        return json.loads(N.take_string(out))
 
     # -- params / stats
     @property

@@ -448,3 +448,34 @@ int flw_selftest_umma(int M, int N, int K, int a_mn, int b_mn, int lane_off, con
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ profiling helpers
+namespace flw {
+void microbench(const std::string& which, int64_t n, int iters, double* ms, double* bytes);
+}
+
+extern "C" {
+
+int flw_microbench(const char* which, int64_t n, int iters, double* ms_per_launch, double* bytes_per_launch) {
+    return guarded([&] {
+        if (n < 1 || iters < 1) fail(Errc::Config, "microbench needs n >= 1 and iters >= 1");
+        microbench(which ? which : "", n, iters, ms_per_launch, bytes_per_launch);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_enable_probes(flw_dpd* e, int on) {
+    return guarded([&] {
+        eng(e).enable_probes(on != 0);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_probe_times(flw_dpd* e, char** json) {
+    return guarded([&] {
+        *json = dup_string(eng(e).probe_times_json());
+        return FLW_OK;
+    });
+}
+
+}  // extern "C"

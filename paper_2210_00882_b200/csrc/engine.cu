@@ -54,6 +54,7 @@ struct Engine::Bufs {
     FastNet pol{}, crit{};
     int grid = 0;                       // persistent CTAs of the fused learn kernel
     float *part_p = nullptr, *part_c = nullptr, *loss_parts = nullptr;
+    __nv_bfloat16 *wimg_p = nullptr, *wimg_c = nullptr;
     double *block_sums = nullptr, *rsum_scratch = nullptr;
     std::vector<void*> owned;
 
@@ -214,6 +215,8 @@ void Engine::alloc() {
         b.part_p = b.alloc<float>(static_cast<int64_t>(b.grid) * s.P_policy);
         b.part_c = b.alloc<float>(static_cast<int64_t>(b.grid) * (s.P - s.P_policy));
         b.loss_parts = b.alloc<float>(2 * 3 * b.grid);
+        b.wimg_p = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.pol) / 2));
+        b.wimg_c = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.crit) / 2));
         b.block_sums = b.alloc<double>(2 * ((R_ + 255) / 256));
         b.rsum_scratch = b.alloc<double>(256);
         b.values = b.alloc<float>(TR_);
@@ -290,6 +293,66 @@ void Engine::reinit(uint64_t seed) {
     FLW_CUDA(cudaMemset(b_->ctx, 0, sizeof(DeviceCtx)));
     steps_ = 0;
     cur_step_ = 0;
+}
+
+// ------------------------------------------------------------------------------ probes
+void Engine::probe_begin(const char* tag) {
+    if (!probes_on_ || !capturing_) return;
+    Probe p{tag, nullptr, nullptr};
+    FLW_CUDA(cudaEventCreate(&p.a));
+    FLW_CUDA(cudaEventCreate(&p.b));
+    // External: a real event-record node in the captured graph (a plain record during capture
+    // only expresses an intra-graph dependency and cannot be timed).
+    FLW_CUDA(cudaEventRecordWithFlags(p.a, stream_, cudaEventRecordExternal));
+    probes_.push_back(p);
+    open_probe_ = static_cast<int>(probes_.size()) - 1;
+}
+
+void Engine::probe_end() {
+    if (open_probe_ < 0) return;
+    FLW_CUDA(cudaEventRecordWithFlags(probes_[static_cast<size_t>(open_probe_)].b, stream_, cudaEventRecordExternal));
+    open_probe_ = -1;
+}
+
+void Engine::clear_probes() {
+    for (auto& p : probes_) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    probes_.clear();
+    open_probe_ = -1;
+}
+
+void Engine::enable_probes(bool on) {
+    FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+    probes_on_ = on;
+    if (graph_) {
+        FLW_CUDA(cudaGraphExecDestroy(graph_));
+        graph_ = nullptr;
+    }
+    clear_probes();
+}
+
+std::string Engine::probe_times_json() {
+    FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));
+    std::map<std::string, std::vector<float>> by;
+    std::vector<std::string> order;
+    for (auto& p : probes_) {
+        float ms = 0.0f;
+        FLW_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        if (!by.count(p.tag)) order.push_back(p.tag);
+        by[p.tag].push_back(ms);
+    }
+    std::string s = "{";
+    for (size_t i = 0; i < order.size(); ++i) {
+        s += (i ? ", \"" : "\"") + order[i] + "\": [";
+        const auto& v = by[order[i]];
+        for (size_t j = 0; j < v.size(); ++j) s += (j ? ", " : "") + std::to_string(v[j]);
+        s += "]";
+    }
+    return s + "}";
 }
 
 // Pageable H2D copies are staged before cudaMemcpyAsync returns, so `ep` may live on the stack.
@@ -396,20 +459,30 @@ void Engine::enq_learn_fast() {
     f.value_coef = cfg_.value_coef;
     f.entropy_coef = cfg_.entropy_coef;
     f.clip_eps = static_cast<float>(cfg_.clip_eps);
+    f.split_rows = -1;
+    fast_build_wimg(stream_, b.params, b.crit, b.wimg_c);
+    fast_build_wimg(stream_, b.params, b.pol, b.wimg_p);
     // values = critic(states), last_value = critic(last_next)
     f.net = b.crit;
+    f.wimg = b.wimg_c;
     f.kind = kNetCritic;
     f.mode = 0;
     f.X = b.states;
     f.rows = TR_;
+    // states block T (= last_next) directly follows the T*E trajectory rows, so ONE launch over
+    // T*E + E rows yields values and last_value (values_out rows >= T*E go to last_value).
+    f.rows = TR_ + R_;
+    f.split_rows = TR_;
     f.values_out = b.values;
-    fast_mlp(stream_, f, b.grid);
-    f.X = b.states + T_ * E_ * S;
-    f.rows = R_;
-    f.values_out = b.last_value;
-    fast_mlp(stream_, f, static_cast<int>(std::min<int64_t>(b.grid, (R_ + 127) / 128)));
+    f.values_out2 = b.last_value;
+    probe_begin("critic_fwd");
+    fast_mlp(stream_, f, static_cast<int>(std::min<int64_t>(b.grid, (f.rows + 127) / 128)));
+    probe_end();
+    f.split_rows = -1;
+    probe_begin("gae");
     fast_gae(stream_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
              b.block_sums, b.stats);
+    probe_end();
     // learn: policy then critic, each a persistent fused kernel
     f.mode = 1;
     f.X = b.states;
@@ -421,18 +494,26 @@ void Engine::enq_learn_fast() {
     f.ret = b.ret;
     f.values_in = b.values;
     f.net = b.pol;
+    f.wimg = b.wimg_p;
     f.kind = ppo ? kNetPolicyPpo : kNetPolicyA3c;
     f.partials = b.part_p;
     f.part_stride = s.P_policy;
     f.loss_partials = b.loss_parts;
+    probe_begin("learn_policy");
     fast_mlp(stream_, f, b.grid);
+    probe_end();
     f.net = b.crit;
+    f.wimg = b.wimg_c;
     f.kind = kNetCritic;
     f.partials = b.part_c;
     f.part_stride = s.P - s.P_policy;
     f.loss_partials = b.loss_parts + 3 * b.grid;
+    probe_begin("learn_critic");
     fast_mlp(stream_, f, b.grid);
+    probe_end();
+    probe_begin("reduce");
     fast_reduce_partials(stream_, b.part_p, b.part_c, b.grid, s.P_policy, s.P - s.P_policy, b.grads);
+    probe_end();
     fast_reduce_loss(stream_, b.loss_parts, b.grid, 2, cfg_.entropy_coef, b.loss);
 }
 
@@ -481,7 +562,9 @@ void Engine::enq_grad_sync_and_adam() {
             gscale = 1.0 / static_cast<double>(comm_->nranks());
         }
     }
+    probe_begin("adam");
     exact_adam(stream_, b.ctx, b.params, b.grads, g64, b.m, b.v, s.P, cfg_.lr, 0.9, 0.999, 1e-8, gscale);
+    probe_end();
 }
 
 void Engine::enq_reward_sum() {
@@ -549,22 +632,29 @@ void Engine::learn(int64_t ep, int64_t k) {
 void Engine::build_graph() {
     FLW_CUDA(cudaSetDevice(device_));
     cudaGraph_t g;
+    clear_probes();
     FLW_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    capturing_ = true;
     begin_episode(stream_, b_->ctx);
     enq_reset();
+    probe_begin("rollout");
     if (numerics_ == Numerics::Fast)
         enq_rollout_fast(0, T_);
     else
         for (int64_t st = 0; st < T_; ++st) enq_step(st);
+    probe_end();
     FLW_CUDA(cudaEventRecord(ev_fork_, stream_));
     FLW_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
     enq_reward_sum();
     FLW_CUDA(cudaEventRecord(ev_join_, side_));
     for (int64_t k = 0; k < shape_.learn_iters; ++k) {
+        if (numerics_ == Numerics::Exact) probe_begin("learn_grads");
         enq_learn_grads();
+        if (numerics_ == Numerics::Exact) probe_end();
         enq_grad_sync_and_adam();
     }
     FLW_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+    capturing_ = false;
     FLW_CUDA(cudaStreamEndCapture(stream_, &g));
     size_t n = 0;
     FLW_CUDA(cudaGraphGetNodes(g, nullptr, &n));

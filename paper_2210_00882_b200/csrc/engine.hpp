@@ -80,6 +80,10 @@ class Engine {
     // Launch statistics of the last captured episode graph (kernel nodes).
     int64_t graph_kernel_nodes() const { return graph_kernels_; }
 
+    // CUDA-event probes around the main kernels, recorded inside the episode graph.
+    void enable_probes(bool on);
+    std::string probe_times_json();
+
   private:
     struct Bufs;
     void alloc();
@@ -109,6 +113,18 @@ class Engine {
     int64_t graph_kernels_ = 0;
     int64_t steps_ = 0;
     int64_t cur_step_ = 0;      // index of the trajectory block holding the current policy input
+
+    struct Probe {
+        std::string tag;
+        cudaEvent_t a, b;
+    };
+    bool probes_on_ = false;
+    bool capturing_ = false;
+    std::vector<Probe> probes_;
+    int open_probe_ = -1;
+    void probe_begin(const char* tag);
+    void probe_end();
+    void clear_probes();
 };
 
 }  // namespace flw

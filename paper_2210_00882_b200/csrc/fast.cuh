@@ -1,6 +1,7 @@
 // Fast-numerics (tensor-core learn phase, f32 rollout) kernel interfaces.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -35,7 +36,10 @@ struct FastLearnArgs {
     const double* adv_stats;   // {mean, sd} or null (no normalisation)
     const float* ret;
     const float* values_in;    // critic values (A3C advantage)
-    float* values_out;         // mode 0
+    float* values_out;         // mode 0: rows [0, split_rows)
+    float* values_out2;        // mode 0: rows [split_rows, rows) (when split_rows >= 0)
+    int64_t split_rows;
+    const __nv_bfloat16* wimg; // pre-built shared-memory image of the weight tiles (bf16)
     double inv_n, value_coef, entropy_coef;
     float clip_eps;
     float* partials;           // [grid, part_stride]
@@ -44,6 +48,10 @@ struct FastLearnArgs {
 };
 
 size_t fast_mlp_smem_bytes(const FastNet& n);
+size_t fast_wimg_bytes(const FastNet& n);  // bytes of the weight-tile image (smem prefix)
+// Builds the bf16 W^T tile image of one net from the f32 params (once per train iteration,
+// shared by every CTA of the critic-forward / learn kernels that follow).
+void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv_bfloat16* img);
 void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid);
 void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int nparts, int64_t Pp, int64_t Pc,
                           float* grads);

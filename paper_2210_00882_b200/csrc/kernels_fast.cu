@@ -28,6 +28,7 @@ namespace {
 constexpr int kRows = 128;
 constexpr int kMaxW = 64;
 constexpr int kThreads = 256;
+constexpr int kDbSlices = 4;  // db column sums: 4 threads per column, 32 rows each
 
 struct Smem {  // carve-up of dynamic shared memory (byte offsets)
     uint32_t wt[kMaxLayers], x, h[kMaxLayers], dz[2], bias, dbacc, loss, total;
@@ -55,7 +56,7 @@ __host__ __device__ inline Smem carve(const FastNet& n) {
     s.bias = off;
     off += kMaxLayers * kMaxW * 4;
     s.dbacc = off;
-    off += 2 * kMaxLayers * kMaxW * 4;  // two row halves
+    off += kDbSlices * kMaxLayers * kMaxW * 4;  // one slice per row quarter
     s.loss = off;
     off += 8 * 3 * 4;
     // slack: M=64 MN-major reads of narrow tiles run past their end (rows >= din are ignored)
@@ -85,18 +86,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
     float* bias = reinterpret_cast<float*>(smem + S.bias);
     float* dbacc = reinterpret_cast<float*>(smem + S.dbacc);
 
-    // ---- weights (once per CTA): W_l^T as [dout x din] K-major B tiles, zero padded
+    // ---- weights (once per CTA): W_l^T as [dout x din] K-major B tiles, zero padded; copied
+    // with 16-byte loads from the pre-built image (k_build_wimg) that every CTA shares via L2
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.wimg);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (uint32_t i = t; i < S.x / 16; i += kThreads) dst[i] = src[i];
+    }
     for (int l = 0; l < L; ++l) {
-        const int di = n.din[l], dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
-        const float* W = a.params + n.woff[l];
-        for (int i = t; i < dout * di; i += kThreads) {
-            int o = i / di, c = i % di;
-            float v = (o < ro && c < ri) ? W[c * ro + o] : 0.0f;
-            *reinterpret_cast<__nv_bfloat16*>(smem + S.wt[l] + umma::tile_offset(o, c, di)) = __float2bfloat16(v);
-        }
+        const int ro = n.rout[l];
         for (int o = t; o < kMaxW; o += kThreads) bias[l * kMaxW + o] = o < ro ? a.params[n.boff[l] + o] : 0.0f;
     }
-    for (int i = t; i < 2 * kMaxLayers * kMaxW; i += kThreads) dbacc[i] = 0.0f;
+    for (int i = t; i < kDbSlices * kMaxLayers * kMaxW; i += kThreads) dbacc[i] = 0.0f;
     umma::fence_async_smem();
     if (w == 0) umma::tmem_alloc<512>(&tslot);
     if (t == 0) {
@@ -114,18 +115,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
     bool first = true;
     const int64_t ntiles = (a.rows + kRows - 1) / kRows;
 
+    // Input rows are fetched one tile ahead into registers (this thread's 8-column chunks of
+    // its row), so the HBM latency of tile i+1 hides behind tile i's 2L GEMM stages.
+    constexpr int kXRegs = kMaxW / 2;
+    float xnext[kXRegs];
+    auto fetch_x = [&](int64_t tl) {
+        const int64_t rw = tl * kRows + r;
+        const bool ok = tl < ntiles && rw < a.rows;
+#pragma unroll
+        for (int k = 0; k < kXRegs / 8; ++k) {
+            const int c0 = 8 * half + 16 * k;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = c0 + j;
+                xnext[8 * k + j] = (ok && c < a.in_cols) ? a.X[rw * a.in_cols + c] : 0.0f;
+            }
+        }
+    };
+    fetch_x(blockIdx.x);
+
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t row = tile * kRows + r;
         const bool valid = row < a.rows;
         // ---- input tile (f32 -> bf16), zero padded columns and rows; halves split 8-col chunks
-        for (int c0 = 8 * half; c0 < n.din[0]; c0 += 16) {
+#pragma unroll
+        for (int k = 0; k < kXRegs / 8; ++k) {
+            const int c0 = 8 * half + 16 * k;
             float v[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                int c = c0 + j;
-                v[j] = (valid && c < a.in_cols) ? a.X[row * a.in_cols + c] : 0.0f;
+            for (int j = 0; j < 8; ++j) v[j] = xnext[8 * k + j];
+            if (c0 < n.din[0]) umma::st_row8(smem + S.x, n.din[0], r, c0, v);
+        }
+        fetch_x(tile + gridDim.x);
+        // per-row learn inputs, issued now and consumed by the loss epilogue after the forward
+        int act_r = 0;
+        float lpo_r = 0.0f, adv_r = 0.0f, ret_r = 0.0f, val_r = 0.0f;
+        if (a.mode == 1 && half == 0 && valid) {
+            ret_r = a.kind == kNetPolicyPpo ? 0.0f : a.ret[row];
+            if (a.kind != kNetCritic) act_r = a.actions[row];
+            if (a.kind == kNetPolicyPpo) {
+                lpo_r = a.logp_old[row];
+                adv_r = a.adv[row];
             }
-            umma::st_row8(smem + S.x, n.din[0], r, c0, v);
+            if (a.kind == kNetPolicyA3c) val_r = a.values_in[row];
         }
         umma::fence_async_smem();
         umma::fence_before_sync();
@@ -174,10 +206,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) dz[j] = 0.0f;
             if (a.mode == 0) {
-                if (valid) a.values_out[row] = out[0];
+                if (valid) {
+                    if (a.split_rows >= 0 && row >= a.split_rows)
+                        a.values_out2[row - a.split_rows] = out[0];
+                    else
+                        a.values_out[row] = out[0];
+                }
             } else if (valid) {
                 if (a.kind == kNetCritic) {  // value MSE: dV = 2 c_v (V - R) / N
-                    float verr = out[0] - a.ret[row];
+                    float verr = out[0] - ret_r;
                     dz[0] = static_cast<float>(2.0 * a.value_coef * a.inv_n) * verr;
                     vl_acc += static_cast<float>(a.value_coef * a.inv_n) * verr * verr;
                 } else {  // policy: clipped surrogate (PPO) or A3C policy gradient, + entropy bonus
@@ -193,22 +230,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
                         p[j] = expf(lp[j]);
                         H -= p[j] * lp[j];
                     }
-                    const int act = a.actions[row];
+                    const int act = act_r;
                     const float inv_n = static_cast<float>(a.inv_n);
                     float coef;
                     if (a.kind == kNetPolicyPpo) {
-                        float adv = a.adv[row];
+                        float adv = adv_r;
                         if (a.adv_stats) {
                             const double sd = a.adv_stats[1];
                             if (!(sd < 1e-8)) adv = static_cast<float>((adv - a.adv_stats[0]) / (sd + 1e-8));
                         }
-                        const float ratio = expf(lp[act] - a.logp_old[row]);
+                        const float ratio = expf(lp[act] - lpo_r);
                         const float clipped = fminf(fmaxf(ratio, 1.0f - a.clip_eps), 1.0f + a.clip_eps);
                         const float s1 = ratio * adv, s2 = clipped * adv;
                         pl_acc -= fminf(s1, s2) * inv_n;
                         coef = s1 <= s2 ? -inv_n * ratio * adv : 0.0f;
                     } else {  // A3C: advantage R - V (rl.cpp:188)
-                        const float adv = a.ret[row] - a.values_in[row];
+                        const float adv = ret_r - val_r;
                         pl_acc -= lp[act] * adv * inv_n;
                         coef = -inv_n * adv;
                     }
@@ -248,14 +285,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
                 }
                 umma::commit(&bar);
             }
-            // db_l: column sums of dZ_l, two row halves (overlaps the MMAs; both only read the tile)
-            if (t < 2 * dout) {
-                const int c = t % dout, h2 = t / dout;
+            // db_l: column sums of dZ_l, 4 row quarters per column, each thread accumulating its
+            // own slice across tiles (fixed order; overlaps the MMAs, which only read the tile)
+            if (t < kDbSlices * dout) {
+                const int c = t % dout, q4 = t / dout;
+                const uint8_t* col = smem + S.dz[cur] + umma::tile_offset(0, c, dout);
                 float s = 0.0f;
-                for (int rr = 64 * h2; rr < 64 * h2 + 64; ++rr)
-                    s += __bfloat162float(
-                        *reinterpret_cast<const __nv_bfloat16*>(smem + S.dz[cur] + umma::tile_offset(rr, c, dout)));
-                dbacc[(h2 * kMaxLayers + l) * kMaxW + c] += s;
+#pragma unroll 8
+                for (int rr = 32 * q4; rr < 32 * q4 + 32; ++rr)
+                    s += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+                        col + (rr >> 3) * (dout * 16) + (rr & 7) * 16));
+                dbacc[(q4 * kMaxLayers + l) * kMaxW + c] += s;
             }
             umma::mbar_wait(&bar, phase);
             phase ^= 1;
@@ -304,8 +344,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
                             if (c0 + j < ro) part[n.woff[l] - n.woff[0] + i * ro + c0 + j] = v[j];
                 }
             }
-            for (int o = t; o < ro; o += kThreads)
-                part[n.boff[l] - n.woff[0] + o] = dbacc[l * kMaxW + o] + dbacc[(kMaxLayers + l) * kMaxW + o];
+            for (int o = t; o < ro; o += kThreads) {
+                float s = 0.0f;
+                for (int q4 = 0; q4 < kDbSlices; ++q4) s += dbacc[(q4 * kMaxLayers + l) * kMaxW + o];
+                part[n.boff[l] - n.woff[0] + o] = s;
+            }
         }
         float* ls = reinterpret_cast<float*>(smem + S.loss);
         for (int off = 16; off > 0; off >>= 1) {
@@ -331,6 +374,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
     umma::fence_before_sync();
     __syncthreads();
     if (w == 0) umma::tmem_free<512>(tmem);
+}
+
+// Weight-tile image: exactly the bytes [0, S.x) of k_fast_mlp's shared memory.
+__global__ void __launch_bounds__(256) k_build_wimg(const float* __restrict__ params, FastNet n,
+                                                    __nv_bfloat16* __restrict__ img) {
+    const Smem S = carve(n);
+    for (int l = 0; l < n.L; ++l) {
+        const int di = n.din[l], dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
+        const float* W = params + n.woff[l];
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < dout * di; i += gridDim.x * blockDim.x) {
+            const int o = i / di, c = i % di;
+            const float v = (o < ro && c < ri) ? W[c * ro + o] : 0.0f;
+            img[(S.wt[l] + umma::tile_offset(o, c, di)) / 2] = __float2bfloat16(v);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ partial reduction
@@ -432,17 +490,32 @@ __global__ void __launch_bounds__(256) k_fast_gae(const float* __restrict__ rew,
     }
 }
 
-__global__ void k_adv_stats(const double* __restrict__ block_sums, int nblocks, int64_t n, double* stats) {
-    if (threadIdx.x != 0) return;
+// Fixed-order (deterministic) parallel combine of the per-block sums: strided partials per
+// thread, then a shared-memory tree.
+__global__ void __launch_bounds__(256) k_adv_stats(const double* __restrict__ block_sums, int nblocks, int64_t n,
+                                                   double* stats) {
+    __shared__ double s1[256], s2[256];
     double a1 = 0.0, a2 = 0.0;
-    for (int b = 0; b < nblocks; ++b) {
+    for (int b = threadIdx.x; b < nblocks; b += 256) {
         a1 += block_sums[2 * b];
         a2 += block_sums[2 * b + 1];
     }
-    double mean = a1 / static_cast<double>(n);
-    double var = a2 / static_cast<double>(n) - mean * mean;
-    stats[0] = mean;
-    stats[1] = sqrt(var > 0.0 ? var : 0.0);
+    s1[threadIdx.x] = a1;
+    s2[threadIdx.x] = a2;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+        if (threadIdx.x < off) {
+            s1[threadIdx.x] += s1[threadIdx.x + off];
+            s2[threadIdx.x] += s2[threadIdx.x + off];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double mean = s1[0] / static_cast<double>(n);
+        const double var = s2[0] / static_cast<double>(n) - mean * mean;
+        stats[0] = mean;
+        stats[1] = sqrt(var > 0.0 ? var : 0.0);
+    }
 }
 
 // Parallel episode reward sum (fast numerics): block tree sums in double, fixed block order.
@@ -470,6 +543,11 @@ __global__ void k_sum_blocks(const double* __restrict__ b, int n, double* out) {
 
 // ------------------------------------------------------------------------------ launchers
 size_t fast_mlp_smem_bytes(const FastNet& n) { return carve(n).total; }
+size_t fast_wimg_bytes(const FastNet& n) { return carve(n).x; }
+
+void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv_bfloat16* img) {
+    k_build_wimg<<<16, 256, 0, s>>>(params, n, img);
+}
 
 void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid) {
     const size_t smem = carve(a.net).total;
@@ -498,7 +576,7 @@ void fast_gae(cudaStream_t s, const float* rew, const float* values, const float
     const int nb = static_cast<int>((R + 255) / 256);
     k_fast_gae<<<nb, 256, 0, s>>>(rew, values, done_f, last_value, TR / R, R, gamma, lam, adv, ret, with_adv,
                                   block_sums);
-    if (with_adv) k_adv_stats<<<1, 32, 0, s>>>(block_sums, nb, TR, stats);
+    if (with_adv) k_adv_stats<<<1, 256, 0, s>>>(block_sums, nb, TR, stats);
 }
 
 void fast_sum(cudaStream_t s, const double* x, int64_t n, double* scratch, double* out) {

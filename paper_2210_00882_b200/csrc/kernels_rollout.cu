@@ -14,9 +14,9 @@ namespace flw {
 
 namespace {
 
-constexpr int kEnvsPerCta = 32;
-constexpr int kPerEnv = 8;                        // threads per env: each owns 8 of <= 64 outputs
-constexpr int kThreads = kEnvsPerCta * kPerEnv;   // 256
+constexpr int kEnvsPerCta = 16;
+constexpr int kPerEnv = 16;                       // threads per env: each owns 4 of <= 64 outputs
+constexpr int kThreads = kEnvsPerCta * kPerEnv;   // 256 (2 CTAs per SM at the C2 shape)
 constexpr int kHStride = 68;   // activation row stride (floats): 16B aligned, spreads banks
 
 __host__ __device__ inline int pad4(int x) { return (x + 3) & ~3; }
@@ -25,12 +25,13 @@ struct RolloutSmem {
     uint32_t w[kMaxLayers], b[kMaxLayers], h[2], total;
 };
 
+// W_l stored [pad4(in) x pad4(out)] row-major (zero padded) so the input loop runs in float4 steps.
 __host__ __device__ inline RolloutSmem rollout_carve(const FastRolloutArgs& a) {
     RolloutSmem s{};
     uint32_t off = 0;
     for (int l = 0; l < a.L; ++l) {
         s.w[l] = off;
-        off += static_cast<uint32_t>(a.dims[l] * pad4(a.dims[l + 1]) * 4);
+        off += static_cast<uint32_t>(pad4(a.dims[l]) * pad4(a.dims[l + 1]) * 4);
         s.b[l] = off;
         off += static_cast<uint32_t>(pad4(a.dims[l + 1]) * 4);
     }
@@ -52,17 +53,20 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     const int64_t e = static_cast<int64_t>(blockIdx.x) * kEnvsPerCta + r;
     const bool live = e < a.E;
     const int S_ = a.S, A = a.A;
-    // weights: W_l [in x out] row-major, out padded to a multiple of 4 (zeros)
+    // weights: W_l [in x out] row-major, in and out padded to multiples of 4 (zeros)
     for (int l = 0; l < a.L; ++l) {
-        const int in = a.dims[l], out = a.dims[l + 1], op = pad4(out);
+        const int in = a.dims[l], out = a.dims[l + 1], op = pad4(out), ip = pad4(in);
         float* W = reinterpret_cast<float*>(smem + S.w[l]);
         float* B = reinterpret_cast<float*>(smem + S.b[l]);
-        for (int i = t; i < in * op; i += kThreads) {
+        for (int i = t; i < ip * op; i += kThreads) {
             int ii = i / op, o = i % op;
-            W[i] = o < out ? a.params[a.woff[l] + ii * out + o] : 0.0f;
+            W[i] = (o < out && ii < in) ? a.params[a.woff[l] + ii * out + o] : 0.0f;
         }
         for (int o = t; o < op; o += kThreads) B[o] = o < out ? a.params[a.boff[l] + o] : 0.0f;
     }
+    // zero both activation buffers once: padded input columns must read as 0
+    for (int i = t; i < 2 * kEnvsPerCta * kHStride; i += kThreads) reinterpret_cast<float*>(smem + S.h[0])[i] = 0.0f;
+    __syncthreads();
     // env state -> registers of the quad leader
     constexpr int SW = ENV == 0 ? 2 : kSynthObs;
     double st[SW];
@@ -90,42 +94,32 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             const float* hin = reinterpret_cast<const float*>(smem + S.h[cur]) + r * kHStride;
             float* hout = reinterpret_cast<float*>(smem + S.h[cur ^ 1]) + r * kHStride;
             const bool last = l + 1 == a.L;
-            // thread q owns output groups [4q, 4q+4) and [32+4q, 36+4q): two float4 accumulators,
-            // one h load per input feeds 8 FMAs (in-order f32 accumulation over the inputs)
-            const int o0 = 4 * q, o1 = 32 + 4 * q;
-            const bool has0 = o0 < op, has1 = o1 < op;
-            if (has0) {
-                float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
-                const float4* W4 = reinterpret_cast<const float4*>(W);
-                const int op4 = op / 4;
-#pragma unroll 4
-                for (int i = 0; i < in; ++i) {
-                    const float x = hin[i];
-                    const float4 w0 = W4[i * op4 + q];
-                    acc0.x = fmaf(x, w0.x, acc0.x);
-                    acc0.y = fmaf(x, w0.y, acc0.y);
-                    acc0.z = fmaf(x, w0.z, acc0.z);
-                    acc0.w = fmaf(x, w0.w, acc0.w);
-                    if (has1) {
-                        const float4 w1 = W4[i * op4 + 8 + q];
-                        acc1.x = fmaf(x, w1.x, acc1.x);
-                        acc1.y = fmaf(x, w1.y, acc1.y);
-                        acc1.z = fmaf(x, w1.z, acc1.z);
-                        acc1.w = fmaf(x, w1.w, acc1.w);
+            // thread q owns outputs [4q, 4q+4): one float4 of inputs (LDS.128, broadcast to the
+            // env's 16 threads) feeds 16 FMAs issued as 8 packed FFMA2; in-order f32 accumulation
+            const int o0 = 4 * q;
+            if (o0 < op) {
+                float2 lo = make_float2(0.f, 0.f), hi = lo;
+                const float4* W4 = reinterpret_cast<const float4*>(W) + q;
+                const float4* X4 = reinterpret_cast<const float4*>(hin);
+                const int op4 = op / 4, ip4 = pad4(in) / 4;
+#pragma unroll 2
+                for (int i4 = 0; i4 < ip4; ++i4) {
+                    const float4 x = X4[i4];
+                    const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float4 w = W4[(4 * i4 + u) * op4];
+                        const float2 xx = make_float2(xs[u], xs[u]);
+                        lo = __ffma2_rn(xx, make_float2(w.x, w.y), lo);
+                        hi = __ffma2_rn(xx, make_float2(w.z, w.w), hi);
                     }
                 }
-                float v[8] = {acc0.x + B[o0], acc0.y + B[o0 + 1], acc0.z + B[o0 + 2], acc0.w + B[o0 + 3],
-                              acc1.x, acc1.y, acc1.z, acc1.w};
-                if (has1) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) v[4 + j] += B[o1 + j];
-                }
+                float v[4] = {lo.x + B[o0], lo.y + B[o0 + 1], hi.x + B[o0 + 2], hi.y + B[o0 + 3]};
                 if (!last) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) v[j] = a.act == 0 ? tanhf(v[j]) : fmaxf(v[j], 0.0f);
+                    for (int j = 0; j < 4; ++j) v[j] = a.act == 0 ? tanhf(v[j]) : fmaxf(v[j], 0.0f);
                 }
                 *reinterpret_cast<float4*>(hout + o0) = make_float4(v[0], v[1], v[2], v[3]);
-                if (has1) *reinterpret_cast<float4*>(hout + o1) = make_float4(v[4], v[5], v[6], v[7]);
             }
             __syncthreads();
             cur ^= 1;
@@ -206,14 +200,15 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                 next[j] = o;
                 nxt_traj[j] = o;
             }
+            for (int j = S_; j < pad4(S_); ++j) next[j] = 0.0f;  // float4 input padding reads zeros
         } else if (q == 0) {
-            for (int j = 0; j < S_; ++j) next[j] = 0.0f;
+            for (int j = 0; j < pad4(S_); ++j) next[j] = 0.0f;
         }
         __syncthreads();
         // the next step's input must sit in buffer 0: copy if the layer count left it in 1
         if ((cur ^ 1) != 0) {
             float* h0w = reinterpret_cast<float*>(smem + S.h[0]) + r * kHStride;
-            for (int j = q; j < S_; j += kPerEnv) h0w[j] = next[j];
+            for (int j = q; j < pad4(S_); j += kPerEnv) h0w[j] = next[j];
             __syncthreads();
         }
     }

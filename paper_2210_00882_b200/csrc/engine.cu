@@ -50,6 +50,8 @@ struct Engine::Bufs {
     int ntiles = 0;
     // both modes: critic outputs consumed by GAE and the loss
     float *values = nullptr, *last_value = nullptr;
+    // MAPPO: joint observation blocks [(T+1), E, W] and critic input rows [(T+1), n*E, W+n]
+    float *joint = nullptr, *cin = nullptr;
     // fast numerics
     FastNet pol{}, crit{};
     int grid = 0;                       // persistent CTAs of the fused learn kernel
@@ -94,8 +96,14 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     shape_ = program_shape(cfg_);
     if (!shape_.accel_capable)
         fail(Errc::PolicyInapplicable, "dp-d requires an accelerator-capable environment implementation");
-    if (shape_.algo == Algo::Mappo)
-        fail(Errc::PolicyInapplicable, "MAPPO is not served by this engine build (PPO and A3C are)");
+    mappo_ = shape_.algo == Algo::Mappo;
+    if (mappo_ && shape_.env != EnvKind::SpreadLite)
+        fail(Errc::PolicyInapplicable, "MAPPO runs on spread_lite (the reference's multi-agent env)");
+    if (mappo_ && numerics == Numerics::Fast)
+        fail(Errc::Config, "MAPPO is served with numerics=exact in this build");
+    if (mappo_ && shape_.n_agents > 64) fail(Errc::Config, "at most 64 agents");
+    if (!mappo_ && shape_.env == EnvKind::SpreadLite)
+        fail(Errc::PolicyInapplicable, "PPO/A3C need a single-agent env (spread_lite is multi-agent)");
     if (env_hi <= env_lo || env_lo < 0 || env_hi > env_total) fail(Errc::Config, "bad env range");
     if (shape_.n_actions > 16) fail(Errc::Config, "at most 16 discrete actions are supported");
     E_ = env_hi - env_lo;
@@ -171,18 +179,23 @@ void Engine::alloc() {
     b.est = b.alloc<double>(static_cast<int64_t>(s.env_state_w) * E_);
     b.done = b.alloc<uint8_t>(E_);
     b.stepc = b.alloc<int32_t>(E_);
-    b.states = b.alloc<float>((T_ + 1) * E_ * S);
+    // policy rows per step: R = E (PPO/A3C) or n*E agent-major (MAPPO)
+    b.states = b.alloc<float>((T_ + 1) * R_ * S);
     int maxw = 0;
     for (int d : s.pdims) maxw = std::max(maxw, d);
     for (int d : s.cdims) maxw = std::max(maxw, d);
-    b.act0 = b.alloc<float>(E_ * maxw);
-    b.act1 = b.alloc<float>(E_ * maxw);
-    b.logits = b.alloc<float>(E_ * A);
-    b.actions = b.alloc<int32_t>(T_ * E_);
-    b.logp = b.alloc<float>(T_ * E_);
-    b.rew = b.alloc<float>(T_ * E_);
-    b.done_f = b.alloc<float>(T_ * E_);
+    b.act0 = b.alloc<float>(R_ * maxw);
+    b.act1 = b.alloc<float>(R_ * maxw);
+    b.logits = b.alloc<float>(R_ * A);
+    b.actions = b.alloc<int32_t>(T_ * R_);
+    b.logp = b.alloc<float>(T_ * R_);
+    b.rew = b.alloc<float>(T_ * R_);
+    b.done_f = b.alloc<float>(T_ * R_);
     b.rew_d = b.alloc<double>(T_ * E_);
+    if (mappo_) {  // joint obs per env and the critic rows [joint | one-hot] per (agent, env)
+        b.joint = b.alloc<float>((T_ + 1) * E_ * s.state_w);
+        b.cin = b.alloc<float>((T_ + 1) * R_ * s.crit_in);
+    }
     b.adv = b.alloc<float>(TR_);
     b.ret = b.alloc<float>(TR_);
     b.stats = b.alloc<double>(2);
@@ -245,7 +258,7 @@ void Engine::alloc() {
             for (int t0 = 0; t0 <= K; t0 += 32)
                 for (int j0 = 0; j0 < N; j0 += 32) {
                     DwTile t{};
-                    t.H = l == 0 ? b.states : H[l - 1];
+                    t.H = l == 0 ? ((net == 1 && mappo_) ? b.cin : b.states) : H[l - 1];
                     t.DZ = DZ[l];
                     t.gW = b.grads + s.woff[net][l];
                     t.gB = b.grads + s.boff[net][l];
@@ -363,8 +376,11 @@ void Engine::set_episode(int64_t ep) {
 // ----------------------------------------------------------------------------- phases
 void Engine::enq_reset() {
     Bufs& b = *b_;
-    exact_reset(stream_, b.ctx, env_params(cfg_, shape_, b_->synth_b), b.est, b.done, b.stepc, b.states, E_, lo_,
-                shape_.obs_dim, seed_);
+    if (mappo_)
+        mappo_reset(stream_, b.ctx, shape_.n_agents, b.est, b.done, b.stepc, b.joint, b.states, b.cin, E_, lo_, seed_);
+    else
+        exact_reset(stream_, b.ctx, env_params(cfg_, shape_, b_->synth_b), b.est, b.done, b.stepc, b.states, E_, lo_,
+                    shape_.obs_dim, seed_);
 }
 
 void Engine::enq_mlp_forward(int net, const float* X, int64_t M, float* const* H) {
@@ -415,13 +431,38 @@ void Engine::enq_step(int64_t st) {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions;
-    const float* in = b.states + st * E_ * S;
+    const float* in = b.states + st * R_ * S;
     float* bufs[2] = {b.act0, b.act1};
     for (int l = 0; l < s.L; ++l) {
         float* out = l + 1 == s.L ? b.logits : bufs[l & 1];
-        exact_layer_fwd(stream_, in, b.params + s.woff[0][l], b.params + s.boff[0][l], out, E_, s.pdims[l],
+        exact_layer_fwd(stream_, in, b.params + s.woff[0][l], b.params + s.boff[0][l], out, R_, s.pdims[l],
                         s.pdims[l + 1], l + 1 < s.L ? act_of(cfg_) : kNone);
         in = out;
+    }
+    if (mappo_) {
+        MappoStepArgs m{};
+        m.logits = b.logits;
+        m.est = b.est;
+        m.done = b.done;
+        m.stepc = b.stepc;
+        m.actions = b.actions;
+        m.logp = b.logp;
+        m.reward = b.rew;
+        m.done_f = b.done_f;
+        m.reward_d = b.rew_d;
+        m.joint = b.joint;
+        m.prows = b.states;
+        m.cin = b.cin;
+        m.E = E_;
+        m.env_lo = lo_;
+        m.env_total = etot_;
+        m.step = st;
+        m.max_steps = static_cast<int64_t>(cfg_.env_param("max_steps", 0));
+        m.n = s.n_agents;
+        m.A = A;
+        m.seed = seed_;
+        mappo_rollout(stream_, b.ctx, m);
+        return;
     }
     RolloutArgs a{};
     a.logits = b.logits;
@@ -522,10 +563,13 @@ void Engine::enq_learn_grads() {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions, L = s.L;
-    const float* X = b.states;                        // [T*E, S] t-major
-    const float* last_next = b.states + T_ * E_ * S;  // [E, S]
-    enq_mlp_forward(1, X, TR_, b.Hc.data());          // values = critic(states)
-    enq_mlp_forward(1, last_next, R_, b.Hl.data());   // last_value = critic(last_next)
+    const float* X = b.states;  // [T*R, S] t-major policy rows
+    // critic rows: the states themselves (PPO/A3C) or [joint | one-hot] (MAPPO); block T holds
+    // the last step's next rows (last_next / last nci, programs.cpp:240-245, 422-427)
+    const float* Xc = mappo_ ? b.cin : b.states;
+    const float* last_next = Xc + T_ * R_ * s.crit_in;
+    enq_mlp_forward(1, Xc, TR_, b.Hc.data());         // values = critic(states | ci)
+    enq_mlp_forward(1, last_next, R_, b.Hl.data());   // last_value = critic(last_next | last nci)
     const bool ppo = s.algo != Algo::A3c;
     exact_gae(stream_, b.rew, b.Hc[L - 1], b.done_f, b.Hl[L - 1], TR_, R_, cfg_.gamma, cfg_.lam, b.adv_d, b.ret, ppo);
     if (ppo) exact_normalize(stream_, b.adv_d, TR_, cfg_.normalize_adv, b.stats, b.adv);
@@ -735,6 +779,14 @@ void h2d(T* p, const std::vector<T>& v) {
 
 int64_t Engine::tensor_size(const std::string& n) const {
     const int64_t S = shape_.obs_dim, A = shape_.n_actions;
+    if (mappo_) {  // MAPPO layouts (programs.cpp:349-454)
+        const int64_t W = shape_.state_w, C = shape_.crit_in, na = shape_.n_agents;
+        if (n == "reset_obs" || n == "state_in") return E_ * W;
+        if (n == "logits") return R_ * A;
+        if (n == "pa") return R_ * 2;
+        if (n == "envstep") return E_ * (W + na + 1);
+        if (n == "sample") return TR_ * (S + 4 + 2 * C);
+    }
     if (n == "reset_obs" || n == "state_in") return E_ * S;
     if (n == "logits") return E_ * A;
     if (n == "pa") return E_ * 2;
@@ -758,6 +810,54 @@ void Engine::read_tensor(const std::string& n, double* out) {
         for (size_t i = 0; i < v.size(); ++i) out[i] = static_cast<double>(v[i]);
     };
     const int64_t last = std::max<int64_t>(cur_step_ - 1, 0);
+    if (mappo_) {
+        const int64_t W = shape_.state_w, C = shape_.crit_in, na = shape_.n_agents;
+        if (n == "reset_obs") return put(d2h(b.joint, E_ * W));
+        if (n == "state_in") return put(d2h(b.joint + cur_step_ * E_ * W, E_ * W));
+        if (n == "logits") return put(d2h(b.logits, R_ * A));
+        if (n == "pa") {
+            auto act = d2h(b.actions + last * R_, R_);
+            auto lp = d2h(b.logp + last * R_, R_);
+            for (int64_t r = 0; r < R_; ++r) {
+                out[2 * r] = act[static_cast<size_t>(r)];
+                out[2 * r + 1] = lp[static_cast<size_t>(r)];
+            }
+            return;
+        }
+        if (n == "envstep") {  // [joint | per-agent rewards | done] (programs.cpp:366-367)
+            auto obs = d2h(b.joint + (last + 1) * E_ * W, E_ * W);
+            auto rw = d2h(b.rew + last * R_, R_);
+            auto dn = d2h(b.done_f + last * R_, R_);
+            const int64_t ow = W + na + 1;
+            for (int64_t e = 0; e < E_; ++e) {
+                for (int64_t j = 0; j < W; ++j) out[e * ow + j] = obs[static_cast<size_t>(e * W + j)];
+                for (int64_t a = 0; a < na; ++a) out[e * ow + W + a] = rw[static_cast<size_t>(a * E_ + e)];
+                out[e * ow + W + na] = dn[static_cast<size_t>(e)];
+            }
+            return;
+        }
+        if (n == "sample") {  // rows_state | action | reward | ci | nci | done | logp (programs.cpp:410-411)
+            auto st = d2h(b.states, TR_ * S);
+            auto ci = d2h(b.cin, (T_ + 1) * R_ * C);
+            auto act = d2h(b.actions, TR_);
+            auto rw = d2h(b.rew, TR_);
+            auto dn = d2h(b.done_f, TR_);
+            auto lp = d2h(b.logp, TR_);
+            const int64_t wd = S + 4 + 2 * C;
+            for (int64_t i = 0; i < TR_; ++i) {
+                double* row = out + i * wd;
+                int64_t c = 0;
+                for (int64_t j = 0; j < S; ++j) row[c++] = st[static_cast<size_t>(i * S + j)];
+                row[c++] = act[static_cast<size_t>(i)];
+                row[c++] = rw[static_cast<size_t>(i)];
+                for (int64_t j = 0; j < C; ++j) row[c++] = ci[static_cast<size_t>(i * C + j)];
+                for (int64_t j = 0; j < C; ++j) row[c++] = ci[static_cast<size_t>((i + R_) * C + j)];
+                row[c++] = dn[static_cast<size_t>(i)];
+                row[c++] = lp[static_cast<size_t>(i)];
+            }
+            return;
+        }
+    }
     if (n == "reset_obs") return put(d2h(b.states, E_ * S));
     if (n == "state_in") return put(d2h(b.states + cur_step_ * E_ * S, E_ * S));
     const bool fast = numerics_ == Numerics::Fast;
@@ -833,6 +933,7 @@ void Engine::write_tensor(const std::string& n, const double* in, int64_t cnt) {
     FLW_CUDA(cudaSetDevice(device_));
     FLW_CUDA(cudaStreamSynchronize(stream_));
     if (cnt != tensor_size(n)) fail(Errc::Shape, "tensor '" + n + "' expects " + std::to_string(tensor_size(n)));
+    if (mappo_) fail(Errc::Config, "teacher forcing is not implemented for MAPPO layouts");
     Bufs& b = *b_;
     const int64_t S = shape_.obs_dim;
     auto f = [&](int64_t off, int64_t len, int64_t stride = 1) {

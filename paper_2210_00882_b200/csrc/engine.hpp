@@ -104,6 +104,7 @@ class Engine {
     int device_;
     uint64_t seed_;
     int64_t lo_, hi_, etot_, E_, R_, T_, TR_;
+    bool mappo_ = false;   // agent-major rows R = n*E, critic on [joint obs | agent one-hot]
     Numerics numerics_;
     cudaStream_t stream_ = nullptr, side_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_t0_ = nullptr, ev_t1_ = nullptr;

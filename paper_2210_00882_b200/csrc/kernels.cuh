@@ -32,6 +32,24 @@ struct RolloutArgs {      // one rollout step over E envs (single-agent PPO/A3C)
     EnvParams env;
 };
 
+struct MappoStepArgs {    // one MAPPO rollout step over E envs x n agents (spread_lite)
+    const float* logits;  // [n*E, A] agent-major
+    double* est;          // [4n, E]
+    uint8_t* done;
+    int32_t* stepc;
+    int32_t* actions;     // [T, n*E]
+    float *logp, *reward, *done_f;  // [T, n*E]
+    double* reward_d;     // [T, E] env total reward
+    float *joint, *prows, *cin;     // step-block layouts (see kernels_mappo.cu)
+    int64_t E, env_lo, env_total, step, max_steps;
+    int n, A;
+    uint64_t seed;
+};
+
+void mappo_reset(cudaStream_t s, const DeviceCtx* ctx, int n, double* est, uint8_t* done, int32_t* stepc, float* joint,
+                 float* prows, float* cin, int64_t E, int64_t env_lo, uint64_t seed);
+void mappo_rollout(cudaStream_t s, const DeviceCtx* ctx, const MappoStepArgs& a);
+
 struct DwTile {           // one 32(t) x 32(j) block of dW_l = H_{l-1}^T dZ_l (+ bias row t == K)
     const float* H;       // [M, K]
     const float* DZ;      // [M, N]

@@ -1,9 +1,11 @@
-// Fast-numerics rollout: the whole episode's T steps in ONE launch. Each CTA owns 32 envs for
-// the episode: env state lives in registers, the policy weights are staged in shared memory
-// once, and every step runs policy MLP (f32 FMA, 4 threads per env) -> PolicyApply (the
-// reference's double-precision inverse-CDF sampling on the f32 logits, interp.cpp:175-203) ->
-// EnvStep (bit-exact double dynamics, envs.cuh) -> trajectory write, with no HBM round trip of
-// the env state or activations between steps.
+// Fast-numerics rollout: the whole episode's T steps in ONE launch. Each CTA owns 16 envs for
+// the episode, 16 threads per env (a "group" = half a warp). Env state lives in registers
+// spread over the group, the policy weights are staged in shared memory once, and every step
+// runs policy MLP (f32 packed FFMA2, each thread 4 outputs) -> PolicyApply (the reference's
+// double-precision softmax / inverse-CDF sampling on the f32 logits, interp.cpp:175-203, the
+// per-action exps spread over the group, the order-sensitive sums gathered to the leader) ->
+// EnvStep (bit-exact double dynamics; synth17x6 state component q on lane q) -> trajectory
+// write, with no HBM round trip of env state or activations between steps.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -18,6 +20,7 @@ constexpr int kEnvsPerCta = 16;
 constexpr int kPerEnv = 16;                       // threads per env: each owns 4 of <= 64 outputs
 constexpr int kThreads = kEnvsPerCta * kPerEnv;   // 256 (2 CTAs per SM at the C2 shape)
 constexpr int kHStride = 68;   // activation row stride (floats): 16B aligned, spreads banks
+constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ inline int pad4(int x) { return (x + 3) & ~3; }
 
@@ -44,6 +47,9 @@ __host__ __device__ inline RolloutSmem rollout_carve(const FastRolloutArgs& a) {
 }
 
 __device__ __forceinline__ double dmaxd(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double gshfl(double v, int src) { return __shfl_sync(kFull, v, src, kPerEnv); }
+__device__ __forceinline__ float gshflf(float v, int src) { return __shfl_sync(kFull, v, src, kPerEnv); }
+__device__ __forceinline__ int gshfli(int v, int src) { return __shfl_sync(kFull, v, src, kPerEnv); }
 
 template <int ENV>
 __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* __restrict__ ctx, FastRolloutArgs a) {
@@ -52,6 +58,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     const int t = threadIdx.x, q = t & (kPerEnv - 1), r = t / kPerEnv;
     const int64_t e = static_cast<int64_t>(blockIdx.x) * kEnvsPerCta + r;
     const bool live = e < a.E;
+    const int64_t E = a.E;
     const int S_ = a.S, A = a.A;
     // weights: W_l [in x out] row-major, in and out padded to multiples of 4 (zeros)
     for (int l = 0; l < a.L; ++l) {
@@ -67,21 +74,25 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     // zero both activation buffers once: padded input columns must read as 0
     for (int i = t; i < 2 * kEnvsPerCta * kHStride; i += kThreads) reinterpret_cast<float*>(smem + S.h[0])[i] = 0.0f;
     __syncthreads();
-    // env state -> registers of the quad leader
-    constexpr int SW = ENV == 0 ? 2 : kSynthObs;
-    double st[SW];
+    // env state -> registers. gridline: (x, len) on the leader. synth17x6: component q on lane q,
+    // component 16 also on lane 0 (s16).
+    double sq_own = 0.0, s16 = 0.0, gx = 0.0, glen = 0.0;
     bool done = false;
     int32_t stepc = 0;
-    if (live && q == 0) {
-#pragma unroll
-        for (int j = 0; j < SW; ++j) st[j] = a.est[j * a.E + e];
+    if (live) {
+        if (ENV == 0) {
+            gx = a.est[e];
+            glen = a.est[E + e];
+        } else {
+            sq_own = a.est[q * E + e];
+            if (q == 0) s16 = a.est[16 * E + e];
+        }
         done = a.done[e] != 0;
         stepc = a.stepc[e];
     }
-    // step-0 policy input: the reset observation (trajectory block 0)
+    // step-0 policy input: the observation in trajectory block step0
     float* h0 = reinterpret_cast<float*>(smem + S.h[0]);
-    if (q == 0)
-        for (int j = 0; j < S_; ++j) h0[r * kHStride + j] = live ? a.states[(a.step0 * a.E + e) * S_ + j] : 0.0f;
+    for (int j = q; j < S_; j += kPerEnv) h0[r * kHStride + j] = live ? a.states[(a.step0 * E + e) * S_ + j] : 0.0f;
     __syncthreads();
     const uint64_t ep = static_cast<uint64_t>(ctx->episode);
 
@@ -95,26 +106,40 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             float* hout = reinterpret_cast<float*>(smem + S.h[cur ^ 1]) + r * kHStride;
             const bool last = l + 1 == a.L;
             // thread q owns outputs [4q, 4q+4): one float4 of inputs (LDS.128, broadcast to the
-            // env's 16 threads) feeds 16 FMAs issued as 8 packed FFMA2; in-order f32 accumulation
+            // env's 16 threads) feeds 16 FMAs as packed FFMA2 over two partial sums (even/odd
+            // input quads) for instruction-level parallelism
             const int o0 = 4 * q;
             if (o0 < op) {
-                float2 lo = make_float2(0.f, 0.f), hi = lo;
+                float2 lo0 = make_float2(0.f, 0.f), hi0 = lo0, lo1 = lo0, hi1 = lo0;
                 const float4* W4 = reinterpret_cast<const float4*>(W) + q;
                 const float4* X4 = reinterpret_cast<const float4*>(hin);
                 const int op4 = op / 4, ip4 = pad4(in) / 4;
-#pragma unroll 2
-                for (int i4 = 0; i4 < ip4; ++i4) {
-                    const float4 x = X4[i4];
-                    const float xs[4] = {x.x, x.y, x.z, x.w};
+                int i4 = 0;
+                for (; i4 + 1 < ip4; i4 += 2) {
+                    const float4 x0 = X4[i4], x1 = X4[i4 + 1];
+                    const float xs0[4] = {x0.x, x0.y, x0.z, x0.w}, xs1[4] = {x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const float4 w = W4[(4 * i4 + u) * op4];
-                        const float2 xx = make_float2(xs[u], xs[u]);
-                        lo = __ffma2_rn(xx, make_float2(w.x, w.y), lo);
-                        hi = __ffma2_rn(xx, make_float2(w.z, w.w), hi);
+                        const float4 w0 = W4[(4 * i4 + u) * op4];
+                        const float4 w1 = W4[(4 * i4 + 4 + u) * op4];
+                        lo0 = __ffma2_rn(make_float2(xs0[u], xs0[u]), make_float2(w0.x, w0.y), lo0);
+                        hi0 = __ffma2_rn(make_float2(xs0[u], xs0[u]), make_float2(w0.z, w0.w), hi0);
+                        lo1 = __ffma2_rn(make_float2(xs1[u], xs1[u]), make_float2(w1.x, w1.y), lo1);
+                        hi1 = __ffma2_rn(make_float2(xs1[u], xs1[u]), make_float2(w1.z, w1.w), hi1);
                     }
                 }
-                float v[4] = {lo.x + B[o0], lo.y + B[o0 + 1], hi.x + B[o0 + 2], hi.y + B[o0 + 3]};
+                if (i4 < ip4) {
+                    const float4 x0 = X4[i4];
+                    const float xs0[4] = {x0.x, x0.y, x0.z, x0.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float4 w0 = W4[(4 * i4 + u) * op4];
+                        lo0 = __ffma2_rn(make_float2(xs0[u], xs0[u]), make_float2(w0.x, w0.y), lo0);
+                        hi0 = __ffma2_rn(make_float2(xs0[u], xs0[u]), make_float2(w0.z, w0.w), hi0);
+                    }
+                }
+                float v[4] = {(lo0.x + lo1.x) + B[o0], (lo0.y + lo1.y) + B[o0 + 1], (hi0.x + hi1.x) + B[o0 + 2],
+                              (hi0.y + hi1.y) + B[o0 + 3]};
                 if (!last) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) v[j] = a.act == 0 ? tanhf(v[j]) : fmaxf(v[j], 0.0f);
@@ -124,86 +149,107 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             __syncthreads();
             cur ^= 1;
         }
-        // PolicyApply + EnvStep by the quad leader
         const float* logits = reinterpret_cast<const float*>(smem + S.h[cur]) + r * kHStride;
         float* next = reinterpret_cast<float*>(smem + S.h[cur ^ 1]) + r * kHStride;  // next step's layer-0 input
-        if (live && q == 0) {
-            double l[16], p[16];
-            double mx = logits[0];
-            for (int c = 0; c < A; ++c) {
-                l[c] = logits[c];
-                mx = dmaxd(mx, l[c]);
-            }
-            double den = 0.0;
-            for (int c = 0; c < A; ++c) {
-                p[c] = exp(__dsub_rn(l[c], mx));  // the same value the reference computes twice
-                den = __dadd_rn(den, p[c]);
-            }
-            for (int c = 0; c < A; ++c) p[c] = f32r(__ddiv_rn(p[c], den));
+        // ---- PolicyApply over the group: lane c < A owns action c
+        double lq = q < A ? static_cast<double>(logits[q]) : -1e300;
+        double mx = lq;
+#pragma unroll
+        for (int off = 8; off > 0; off >>= 1) mx = dmaxd(mx, __shfl_xor_sync(kFull, mx, off, kPerEnv));
+        const double eq = q < A ? exp(__dsub_rn(lq, mx)) : 0.0;
+        double den = 0.0;  // ordered sum, as ops.cpp:117-118
+        for (int c = 0; c < A; ++c) den = __dadd_rn(den, gshfl(eq, c));
+        const double pq = q < A ? f32r(__ddiv_rn(eq, den)) : 0.0;
+        int chosen = A - 1;
+        {
             const double u = rng_uniform(rng_key(a.seed, kActionStream, ep, static_cast<uint64_t>(step),
                                                  static_cast<uint64_t>(a.env_lo + e)));
             double cum = 0.0;
-            int chosen = A - 1;
+            bool found = false;
             for (int c = 0; c < A; ++c) {
-                cum = __dadd_rn(cum, p[c]);
-                if (u < cum) {
+                cum = __dadd_rn(cum, gshfl(pq, c));
+                if (!found && u < cum) {
                     chosen = c;
-                    break;
+                    found = true;
                 }
             }
-            const int64_t ti = step * a.E + e;
-            a.actions[ti] = chosen;
-            a.logp[ti] = static_cast<float>(log(dmaxd(p[chosen], 1e-30)));
-            double rew = 0.0;
-            if (!done) {
-                bool d = false;
-                if (ENV == 0) {  // gridline, envs.cpp:38-53
-                    int64_t len = static_cast<int64_t>(st[1]), x = static_cast<int64_t>(st[0]);
-                    x += chosen == 1 ? 1 : -1;
-                    if (x < 0) x = 0;
-                    if (x > len - 1) x = len - 1;
-                    st[0] = static_cast<double>(x);
-                    if (x == len - 1) {
-                        rew = 1.0;
-                        d = true;
-                    }
-                } else {  // synth17x6
-                    double old[kSynthObs], sq = 0.0, m = 0.0;
-#pragma unroll
-                    for (int i = 0; i < kSynthObs; ++i) old[i] = st[i];
-#pragma unroll
-                    for (int i = 0; i < kSynthObs; ++i) {
-                        double t4 = __dadd_rn(__dsub_rn(__dmul_rn(0.3, old[(i + 1) % kSynthObs]), __dmul_rn(0.5, old[i])),
-                                              a.env.synth_b[chosen * kSynthObs + i]);
-                        double nv = __dadd_rn(old[i], __dmul_rn(0.05, t4));
-                        st[i] = nv;
-                        sq = __dadd_rn(sq, __dmul_rn(nv, nv));
-                        double av = nv < 0.0 ? -nv : nv;
-                        m = av > m ? av : m;
-                    }
-                    rew = __dsub_rn(1.0, __ddiv_rn(sq, static_cast<double>(kSynthObs)));
-                    d = m > 2.0;
-                }
-                if (a.env.max_steps > 0 && stepc + 1 >= a.env.max_steps) d = true;
-                stepc += 1;
-                done = d;
-                a.reward[ti] = static_cast<float>(rew);
-                a.done_f[ti] = d ? 1.0f : 0.0f;
-            } else {
-                a.reward[ti] = 0.0f;
-                a.done_f[ti] = 1.0f;
-            }
-            a.reward_d[ti] = rew;
-            float* nxt_traj = a.states + ((step + 1) * a.E + e) * S_;
-            for (int j = 0; j < S_; ++j) {
-                float o = ENV == 0 ? static_cast<float>(__ddiv_rn(st[0], __dsub_rn(st[1], 1.0))) : static_cast<float>(st[j]);
-                next[j] = o;
-                nxt_traj[j] = o;
-            }
-            for (int j = S_; j < pad4(S_); ++j) next[j] = 0.0f;  // float4 input padding reads zeros
-        } else if (q == 0) {
-            for (int j = 0; j < pad4(S_); ++j) next[j] = 0.0f;
         }
+        const double pch = gshfl(pq, chosen);
+        const int64_t ti = step * E + e;
+        if (live && q == 0) {
+            a.actions[ti] = chosen;
+            a.logp[ti] = static_cast<float>(log(dmaxd(pch, 1e-30)));
+        }
+        // ---- EnvStep (absorbing after done, interp.cpp:239-245)
+        double rew = 0.0;
+        bool d = done;
+        if (ENV == 0) {
+            if (!done) {  // gridline, envs.cpp:38-53 (uniform across the group)
+                int64_t len = static_cast<int64_t>(glen), x = static_cast<int64_t>(gx);
+                x += chosen == 1 ? 1 : -1;
+                if (x < 0) x = 0;
+                if (x > len - 1) x = len - 1;
+                gx = static_cast<double>(x);
+                d = false;
+                if (x == len - 1) {
+                    rew = 1.0;
+                    d = true;
+                }
+            }
+            const float o = static_cast<float>(__ddiv_rn(gx, __dsub_rn(glen, 1.0)));
+            if (q == 0) {
+                next[0] = o;
+                for (int j = 1; j < pad4(S_); ++j) next[j] = 0.0f;
+                if (live) a.states[((step + 1) * E + e) * S_] = o;
+            }
+        } else {
+            if (!done) {  // synth17x6: component q on lane q (and 16 on lane 0)
+                const double* tb = a.env.synth_b + chosen * kSynthObs;
+                const double nb_a = gshfl(sq_own, (q + 1) & 15);
+                const double nb_b = gshfl(s16, 0);
+                const double nb = q == 15 ? nb_b : nb_a;
+                const double s0 = gshfl(sq_own, 0);  // neighbour of component 16
+                const double n_own = __dadd_rn(
+                    sq_own, __dmul_rn(0.05, __dadd_rn(__dsub_rn(__dmul_rn(0.3, nb), __dmul_rn(0.5, sq_own)), tb[q])));
+                double n16 = 0.0;
+                if (q == 0)
+                    n16 = __dadd_rn(s16, __dmul_rn(0.05, __dadd_rn(__dsub_rn(__dmul_rn(0.3, s0), __dmul_rn(0.5, s16)),
+                                                                   tb[16])));
+                const double sq2 = __dmul_rn(n_own, n_own);
+                double sum = 0.0;  // sequential in component order (bit-exact reward)
+                for (int c = 0; c < 16; ++c) sum = __dadd_rn(sum, gshfl(sq2, c));
+                sum = __dadd_rn(sum, gshfl(__dmul_rn(n16, n16), 0));
+                double m = n_own < 0.0 ? -n_own : n_own;
+                if (q == 0) m = dmaxd(m, n16 < 0.0 ? -n16 : n16);
+#pragma unroll
+                for (int off = 8; off > 0; off >>= 1) m = dmaxd(m, __shfl_xor_sync(kFull, m, off, kPerEnv));
+                sq_own = n_own;
+                s16 = n16;
+                rew = __dsub_rn(1.0, __ddiv_rn(sum, static_cast<double>(kSynthObs)));
+                d = m > 2.0;
+            }
+            const float o = static_cast<float>(sq_own);
+            next[q] = o;
+            if (q == 0) {
+                next[16] = static_cast<float>(s16);
+                for (int j = 17; j < pad4(S_); ++j) next[j] = 0.0f;
+            }
+            if (live) {
+                float* nt = a.states + ((step + 1) * E + e) * S_;
+                nt[q] = o;
+                if (q == 0) nt[16] = static_cast<float>(s16);
+            }
+        }
+        if (!done) {
+            if (a.env.max_steps > 0 && stepc + 1 >= a.env.max_steps) d = true;
+            stepc += 1;
+        }
+        if (live && q == 0) {
+            a.reward[ti] = done ? 0.0f : static_cast<float>(rew);
+            a.done_f[ti] = (done || d) ? 1.0f : 0.0f;
+            a.reward_d[ti] = done ? 0.0 : rew;
+        }
+        done = done || d;
         __syncthreads();
         // the next step's input must sit in buffer 0: copy if the layer count left it in 1
         if ((cur ^ 1) != 0) {
@@ -212,11 +258,20 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             __syncthreads();
         }
     }
-    if (live && q == 0) {
-#pragma unroll
-        for (int j = 0; j < SW; ++j) a.est[j * a.E + e] = st[j];
-        a.done[e] = done ? 1 : 0;
-        a.stepc[e] = stepc;
+    if (live) {
+        if (ENV == 0) {
+            if (q == 0) {
+                a.est[e] = gx;
+                a.est[E + e] = glen;
+            }
+        } else {
+            a.est[q * E + e] = sq_own;
+            if (q == 0) a.est[16 * E + e] = s16;
+        }
+        if (q == 0) {
+            a.done[e] = done ? 1 : 0;
+            a.stepc[e] = stepc;
+        }
     }
 }
 

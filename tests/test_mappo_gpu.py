@@ -1,0 +1,75 @@
+"""MAPPO on spread_lite (exact numerics) against the unmodified reference's trace
+(tests/golden/trace_mappo_spread3.npz): agent-major policy rows, joint-observation critic with
+agent one-hot, per-agent rewards, GAE over n*E streams (programs.cpp:349-454)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _close(name, got, want, exact=False):
+    got, want = np.asarray(got, float).ravel(), np.asarray(want, float).ravel()
+    assert got.shape == want.shape, name
+    diff = got != want
+    if not diff.any():
+        return
+    assert not exact, f"{name}: {diff.sum()} integer mismatches"
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+    assert rel[diff].max() <= 2.5e-7 and diff.mean() <= 1e-3, f"{name}: {diff.sum()} differ, max rel {rel.max():.3g}"
+
+
+def test_mappo_matches_reference_trace():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2210_00882_b200 import DpdEngine
+
+    z = np.load(os.path.join(GOLDEN, "trace_mappo_spread3.npz"))
+    tr = {k.replace("__", "/"): z[k] for k in z.files if not k.startswith("__")}
+    algo, seed = json.loads(str(z["__algo__"])), int(z["__seed__"])
+    a = pyoracle.parse_algo(algo)
+    eng = DpdEngine(algo, seed=seed, numerics="exact")
+    _close("params0", eng.params(), tr["params0"])
+    for ep in range(2):
+        eng.reset(ep)
+        _close("reset_obs", eng.get("reset_obs"), tr[f"ep{ep}/reset_obs"])
+        for st in range(a["steps_per_episode"]):
+            p = f"ep{ep}/st{st}/"
+            _close(p + "state_in", eng.get("state_in"), tr[p + "state_in"])
+            eng.step(ep, st)
+            _close(p + "logits", eng.get("logits"), tr[p + "logits"])
+            pa, want = eng.get("pa").reshape(-1, 2), tr[p + "pa"].reshape(-1, 2)
+            _close(p + "action", pa[:, 0], want[:, 0], exact=True)
+            _close(p + "logp", pa[:, 1], want[:, 1])
+            _close(p + "envstep", eng.get("envstep"), tr[p + "envstep"])
+        for k in range(eng.stats()["learn_iters"]):
+            p = f"ep{ep}/it{k}/"
+            eng.learn(ep, k)
+            if k == 0:
+                _close(f"ep{ep}/sample", eng.get("sample"), tr[f"ep{ep}/sample"])
+            for n in ("values", "last_value", "adv", "ret", "logits_new", "loss", "grads"):
+                _close(p + n, eng.get(n), tr[p + n])
+            _close(p + "params", eng.params(), tr[p + "params"])
+
+
+@pytest.mark.parametrize("n_agents", [2, 4])
+def test_mappo_episodes_match_oracle(n_agents):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2210_00882_b200 import DpdEngine
+
+    algo = {"algorithm": "mappo", "agent": {"num": n_agents},
+            "env": {"type": "spread_lite", "num": 16, "params": {"accel": 1, "max_steps": 10}},
+            "policy_net": {"hidden": [16, 16]}, "loop": {"episodes": 3, "steps_per_episode": 12}}
+    rew, par, _ = pyoracle.run(algo, 3, 1)
+    eng = DpdEngine(algo, seed=3, numerics="exact")
+    got = [eng.run_episode(ep)[0] / 16 for ep in range(3)]
+    _close("rewards", got, rew)
+    _close("params", eng.params(), par)

@@ -318,7 +318,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--numerics", choices=["exact", "fast"], default="exact")
+    ap.add_argument("--numerics", choices=["exact", "fast"], default="fast")
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -271,19 +271,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
             const uint32_t hin = l == 0 ? sbase + S.x : sbase + S.h[l - 1];
             const uint32_t dzt = sbase + S.dz[cur];
             const uint32_t dw_tmem = tmem + 64u + 64u * static_cast<uint32_t>(l >> 1) + ((l & 1) ? (16u << 16) : 0u);
+            // Issue order: dH_l first, then its commit, then dW_l. tcgen05.mma from one thread
+            // completes in issue order and a commit covers every earlier MMA, so the epilogue
+            // (which needs dH_l) waits on a barrier that does not include dW_l: dW_l runs under
+            // this layer's epilogue and is covered by the next layer's commit.
             if (t == 0) {
                 umma::fence_after_sync();
-                const uint32_t id_dw = umma::idesc_bf16(64, dout, true, true);
-                for (int kb = 0; kb < kRows / 16; ++kb)
-                    umma::mma_bf16(dw_tmem, umma::desc_mnmajor(hin, di, kb), umma::desc_mnmajor(dzt, dout, kb), id_dw,
-                                   !(first && kb == 0));
                 if (l > 0) {
                     const uint32_t id_dh = umma::idesc_bf16(128, di, false, true);
                     for (int kb = 0; kb < dout / 16; ++kb)
                         umma::mma_bf16(tmem, umma::desc_kmajor(dzt, dout, kb),
                                        umma::desc_mnmajor(sbase + S.wt[l], di, kb), id_dh, kb > 0);
+                    umma::commit(&bar);
                 }
-                umma::commit(&bar);
+                const uint32_t id_dw = umma::idesc_bf16(64, dout, true, true);
+                for (int kb = 0; kb < kRows / 16; ++kb)
+                    umma::mma_bf16(dw_tmem, umma::desc_mnmajor(hin, di, kb), umma::desc_mnmajor(dzt, dout, kb), id_dw,
+                                   !(first && kb == 0));
+                if (l == 0) umma::commit(&bar);  // the tile's last MMAs: wait before the buffers are reused
             }
             // db_l: column sums of dZ_l, 4 row quarters per column, each thread accumulating its
             // own slice across tiles (fixed order; overlaps the MMAs, which only read the tile)

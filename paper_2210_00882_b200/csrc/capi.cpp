@@ -150,7 +150,14 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
             std::vector<int> devs;
             for (const Unit& u : units) devs.push_back(u.id);
             auto comms = Comm::init_all(devs);
-            for (int r = 0; r < k; ++r) p.engines[r]->set_comm(std::make_unique<Comm>(comms[r], r, k));
+            std::vector<Comm*> cs;
+            for (int r = 0; r < k; ++r) {
+                auto c = std::make_unique<Comm>(comms[r], r, k);
+                cs.push_back(c.get());
+                p.engines[r]->set_eager_collectives(true);
+                p.engines[r]->set_comm(std::move(c));
+            }
+            Comm::connect_all(cs, devs, p.engines[0]->shape().P);
         }
     } else {
         for (auto& e : p.engines) e->reinit(seed);
@@ -170,6 +177,8 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
             eps[static_cast<size_t>(ep)].wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         }
     } else {
+        // Every unit's episode graph segments are captured before any unit launches.
+        for (auto& e : p.engines) e->prepare();
         std::barrier gate(k + 1);
         std::vector<std::thread> threads;
         for (int r = 0; r < k; ++r)
@@ -177,10 +186,14 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
                 for (int64_t ep = 0; ep < episodes; ++ep) {
                     gate.arrive_and_wait();  // raise_gate(ep)
                     try {
+                        flw_trace(("unit " + std::to_string(r) + " episode " + std::to_string(ep)).c_str());
                         if (first_error.empty()) rsum[r][static_cast<size_t>(ep)] = p.engines[r]->run_episode(ep);
                     } catch (const std::exception& e) {
                         std::lock_guard<std::mutex> g(err_mu);
                         if (first_error.empty()) first_error = "unit " + std::to_string(r) + ": " + e.what();
+                        // peers may be blocked inside a collective waiting for this unit
+                        for (auto& en : p.engines)
+                            if (en->comm()) en->comm()->abort();
                     }
                     gate.arrive_and_wait();  // on_episode_done
                 }
@@ -193,7 +206,10 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
             eps[static_cast<size_t>(ep)].wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         }
         for (auto& t : threads) t.join();
-        if (!first_error.empty()) fail(Errc::Runtime, first_error);
+        if (!first_error.empty()) {
+            p.engines.clear();  // aborted communicators: rebuild on the next run
+            fail(Errc::PeerFailure, first_error);
+        }
     }
     for (int64_t ep = 0; ep < episodes; ++ep) {  // local_run.cpp:560-570
         double sum = 0.0;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -33,14 +34,17 @@ class Comm {
 
     static std::string new_unique_id();  // NCCL_UNIQUE_ID_BYTES raw bytes
     static std::vector<ncclComm_t> init_all(const std::vector<int>& devices);
+    static void connect_all(const std::vector<Comm*>& comms, const std::vector<int>& devices, int64_t count);
 
     void all_gather(const float* send, float* recv, int64_t count, cudaStream_t s);
     void all_reduce_sum(const float* send, float* recv, int64_t count, cudaStream_t s);
+    void abort();
     int rank() const { return rank_; }
     int nranks() const { return nranks_; }
 
   private:
     ncclComm_t comm_ = nullptr;
+    std::atomic<bool> aborted_{false};
     int rank_ = 0, nranks_ = 1;
 };
 

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -23,6 +25,12 @@ namespace flw {
 // ------------------------------------------------------------------ counter RNG
 // splitmix64 keyed counter generator; same arithmetic as the reference
 // (/root/reference/proj/src/core/rng.hpp:12-38), so draws are placement- and device-invariant.
+// Host-side progress trace to stderr when FLW_TRACE is set (diagnosing multi-GPU stalls).
+inline void flw_trace(const char* what) {
+    static const bool on = std::getenv("FLW_TRACE") != nullptr;
+    if (on) std::fprintf(stderr, "[flw] %s\n", what);
+}
+
 __host__ __device__ __forceinline__ uint64_t rng_mix(uint64_t x) {
     x += 0x9e3779b97f4a7c15ULL;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;

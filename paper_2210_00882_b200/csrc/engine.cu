@@ -14,6 +14,8 @@
 #include <cstring>
 #include <vector>
 
+#include <mutex>
+
 #include "comm.hpp"
 #include "common.cuh"
 #include "fast.cuh"
@@ -57,6 +59,7 @@ struct Engine::Bufs {
     int grid = 0;                       // persistent CTAs of the fused learn kernel
     float *part_p = nullptr, *part_c = nullptr, *loss_parts = nullptr;
     __nv_bfloat16 *wimg_p = nullptr, *wimg_c = nullptr;
+    uint8_t* hsave = nullptr;           // critic hidden activations of the values pass (bf16 tiles)
     double *block_sums = nullptr, *rsum_scratch = nullptr;
     std::vector<void*> owned;
 
@@ -124,7 +127,7 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
 Engine::~Engine() {
     cudaSetDevice(device_);
     if (stream_) cudaStreamSynchronize(stream_);
-    if (graph_) cudaGraphExecDestroy(graph_);
+    destroy_graph();
     comm_.reset();
     b_.reset();
     for (cudaEvent_t e : {ev_fork_, ev_join_, ev_t0_, ev_t1_})
@@ -133,12 +136,22 @@ Engine::~Engine() {
     if (stream_) cudaStreamDestroy(stream_);
 }
 
+void Engine::destroy_graph() {
+    for (cudaGraphExec_t g : segs_) cudaGraphExecDestroy(g);
+    segs_.clear();
+    between_.clear();
+    graph_ = nullptr;
+}
+
+void Engine::set_eager_collectives(bool on) {
+    if (on != eager_coll_) destroy_graph();
+    eager_coll_ = on;
+}
+
 void Engine::set_comm(std::unique_ptr<Comm> comm) {
-    if (graph_) {
-        cudaGraphExecDestroy(graph_);
-        graph_ = nullptr;
-    }
+    if (graph_) destroy_graph();
     comm_ = std::move(comm);
+    FLW_CUDA(cudaSetDevice(device_));  // the gather buffer must live on this engine's GPU
     if (comm_ && numerics_ == Numerics::Exact && !b_->gather) {
         b_->gather = b_->alloc<float>(static_cast<int64_t>(comm_->nranks()) * shape_.P);
     }
@@ -230,6 +243,7 @@ void Engine::alloc() {
         b.loss_parts = b.alloc<float>(2 * 3 * b.grid);
         b.wimg_p = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.pol) / 2));
         b.wimg_c = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.crit) / 2));
+        b.hsave = b.alloc<uint8_t>(static_cast<int64_t>(fast_hsave_bytes(b.crit)) * ((TR_ + 127) / 128));
         b.block_sums = b.alloc<double>(2 * ((R_ + 255) / 256));
         b.rsum_scratch = b.alloc<double>(256);
         b.values = b.alloc<float>(TR_);
@@ -295,10 +309,7 @@ void Engine::init_params() {
 void Engine::reinit(uint64_t seed) {
     FLW_CUDA(cudaSetDevice(device_));
     FLW_CUDA(cudaStreamSynchronize(stream_));
-    if (seed != seed_ && graph_) {  // the seed is baked into the captured kernel arguments
-        FLW_CUDA(cudaGraphExecDestroy(graph_));
-        graph_ = nullptr;
-    }
+    if (seed != seed_ && graph_) destroy_graph();  // the seed is baked into the captured kernel arguments
     seed_ = seed;
     init_params();
     FLW_CUDA(cudaMemset(b_->m, 0, static_cast<size_t>(shape_.P) * sizeof(double)));
@@ -340,10 +351,7 @@ void Engine::enable_probes(bool on) {
     FLW_CUDA(cudaSetDevice(device_));
     FLW_CUDA(cudaStreamSynchronize(stream_));
     probes_on_ = on;
-    if (graph_) {
-        FLW_CUDA(cudaGraphExecDestroy(graph_));
-        graph_ = nullptr;
-    }
+    if (graph_) destroy_graph();
     clear_probes();
 }
 
@@ -516,6 +524,11 @@ void Engine::enq_learn_fast() {
     f.split_rows = TR_;
     f.values_out = b.values;
     f.values_out2 = b.last_value;
+    // Keep the trajectory tiles' hidden activations for the critic learn pass (FLW_NO_HREUSE
+    // disables the reuse, for A/B measurement only).
+    static const bool hreuse = std::getenv("FLW_NO_HREUSE") == nullptr;
+    f.hsave = hreuse ? b.hsave : nullptr;
+    f.save_tiles = hreuse ? (TR_ + 127) / 128 : 0;
     probe_begin("critic_fwd");
     fast_mlp(stream_, f, static_cast<int>(std::min<int64_t>(b.grid, (f.rows + 127) / 128)));
     probe_end();
@@ -536,6 +549,8 @@ void Engine::enq_learn_fast() {
     f.values_in = b.values;
     f.net = b.pol;
     f.wimg = b.wimg_p;
+    f.hsave = nullptr;
+    f.hload = 0;
     f.kind = ppo ? kNetPolicyPpo : kNetPolicyA3c;
     f.partials = b.part_p;
     f.part_stride = s.P_policy;
@@ -545,6 +560,8 @@ void Engine::enq_learn_fast() {
     probe_end();
     f.net = b.crit;
     f.wimg = b.wimg_c;
+    f.hsave = hreuse ? b.hsave : nullptr;  // same params as the values pass: same activations
+    f.hload = hreuse ? 1 : 0;
     f.kind = kNetCritic;
     f.partials = b.part_c;
     f.part_stride = s.P - s.P_policy;
@@ -597,12 +614,20 @@ void Engine::enq_grad_sync_and_adam() {
     if (comm_ && comm_->nranks() > 1) {
         if (numerics_ == Numerics::Exact) {
             // GradSync (local_run.cpp:379-414): AllGather then the mean in unit-id (= rank) order.
-            comm_->all_gather(b.grads, b.gather, s.P, stream_);
+            auto op = [this, &b, P = s.P] { comm_->all_gather(b.grads, b.gather, P, stream_); };
+            if (eager_coll_ && capturing_)
+                segment_break(op);
+            else
+                op();
             exact_grad_mean(stream_, b.gather, comm_->nranks(), s.P, b.gmean);
             g64 = b.gmean;
         } else {
             // Fast: in-place NCCL sum over NVLink, the 1/k of the mean folded into Adam.
-            comm_->all_reduce_sum(b.grads, b.grads, s.P, stream_);
+            auto op = [this, &b, P = s.P] { comm_->all_reduce_sum(b.grads, b.grads, P, stream_); };
+            if (eager_coll_ && capturing_)
+                segment_break(op);
+            else
+                op();
             gscale = 1.0 / static_cast<double>(comm_->nranks());
         }
     }
@@ -675,12 +700,16 @@ void Engine::learn(int64_t ep, int64_t k) {
 // ------------------------------------------------------------------------ episode graph
 void Engine::build_graph() {
     FLW_CUDA(cudaSetDevice(device_));
-    cudaGraph_t g;
+    flw_trace("build_graph: capture");
+    destroy_graph();
+    graph_kernels_ = 0;
     clear_probes();
     FLW_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     capturing_ = true;
     begin_episode(stream_, b_->ctx);
+    trace_capture("begin");
     enq_reset();
+    trace_capture("reset");
     probe_begin("rollout");
     if (numerics_ == Numerics::Fast)
         enq_rollout_fast(0, T_);
@@ -691,34 +720,77 @@ void Engine::build_graph() {
     FLW_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
     enq_reward_sum();
     FLW_CUDA(cudaEventRecord(ev_join_, side_));
+    // a capture segment cannot end with the side stream still forked
+    if (eager_coll_) FLW_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+    trace_capture("rollout+reward");
     for (int64_t k = 0; k < shape_.learn_iters; ++k) {
         if (numerics_ == Numerics::Exact) probe_begin("learn_grads");
         enq_learn_grads();
+        trace_capture("learn_grads");
         if (numerics_ == Numerics::Exact) probe_end();
         enq_grad_sync_and_adam();
+        trace_capture("sync+adam");
     }
-    FLW_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+    if (!eager_coll_) FLW_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+    end_segment();
+    graph_ = segs_.front();
+    flw_trace("build_graph: done");
+}
+
+void Engine::trace_capture(const char* where) {
+    static const bool on = std::getenv("FLW_TRACE") != nullptr;
+    if (!on) return;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(stream_, &st);
+    std::fprintf(stderr, "[flw] dev %d %s: capture status %d (%s)\n", device_, where, static_cast<int>(st),
+                 cudaGetErrorString(e));
+}
+
+void Engine::end_segment() {
+    trace_capture("end_segment");
+    cudaGraph_t g;
     capturing_ = false;
     FLW_CUDA(cudaStreamEndCapture(stream_, &g));
     size_t n = 0;
     FLW_CUDA(cudaGraphGetNodes(g, nullptr, &n));
     std::vector<cudaGraphNode_t> nodes(n);
     FLW_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
-    graph_kernels_ = 0;
     for (auto nd : nodes) {
         cudaGraphNodeType ty;
         FLW_CUDA(cudaGraphNodeGetType(nd, &ty));
         if (ty == cudaGraphNodeTypeKernel) ++graph_kernels_;
     }
-    FLW_CUDA(cudaGraphInstantiate(&graph_, g, 0));
+    cudaGraphExec_t exec = nullptr;
+    FLW_CUDA(cudaGraphInstantiate(&exec, g, 0));
     FLW_CUDA(cudaGraphDestroy(g));
+    segs_.push_back(exec);
+}
+
+void Engine::segment_break(std::function<void()> op) {
+    end_segment();
+    between_.push_back(std::move(op));
+    FLW_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    capturing_ = true;
+}
+
+void Engine::launch_graph() {
+    for (size_t i = 0; i < segs_.size(); ++i) {
+        FLW_CUDA(cudaGraphLaunch(segs_[i], stream_));
+        if (i < between_.size()) between_[i]();
+    }
+}
+
+void Engine::prepare() {
+    FLW_CUDA(cudaSetDevice(device_));
+    if (!graph_) build_graph();
+    FLW_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void Engine::enqueue_episodes(int64_t first, int64_t count) {
     FLW_CUDA(cudaSetDevice(device_));
     if (!graph_) build_graph();
     FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, &first, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
-    for (int64_t i = 0; i < count; ++i) FLW_CUDA(cudaGraphLaunch(graph_, stream_));
+    for (int64_t i = 0; i < count; ++i) launch_graph();
     steps_ += T_ * count;
     cur_step_ = T_;
 }
@@ -739,9 +811,11 @@ double Engine::run_episode(int64_t ep, float* device_ms) {
     if (!graph_) build_graph();
     FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, &ep, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
     FLW_CUDA(cudaEventRecord(ev_t0_, stream_));
-    FLW_CUDA(cudaGraphLaunch(graph_, stream_));
+    launch_graph();
     FLW_CUDA(cudaEventRecord(ev_t1_, stream_));
+    flw_trace("run_episode: launched");
     FLW_CUDA(cudaStreamSynchronize(stream_));
+    flw_trace("run_episode: synced");
     steps_ += T_;
     cur_step_ = T_;
     if (device_ms) FLW_CUDA(cudaEventElapsedTime(device_ms, ev_t0_, ev_t1_));

@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <map>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -41,6 +42,9 @@ class Engine {
 
     // Gradient group (GradSync): rank = unit id, nranks = k. Takes ownership.
     void set_comm(std::unique_ptr<Comm> comm);
+    Comm* comm() { return comm_.get(); }
+    void set_eager_collectives(bool on);
+    void prepare();  // captures the episode graph now (before any peer launches its own)
 
     // Phase-level API (each enqueues on the engine stream and synchronises before returning).
     void reset(int64_t ep);
@@ -110,8 +114,18 @@ class Engine {
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_t0_ = nullptr, ev_t1_ = nullptr;
     std::unique_ptr<Bufs> b_;
     std::unique_ptr<Comm> comm_;
-    cudaGraphExec_t graph_ = nullptr;
+    cudaGraphExec_t graph_ = nullptr;  // == segs_[0]
+    // Single-process multi-GPU: the collectives are issued eagerly between graph segments
+    // (NCCL >= 2.28 cannot capture collectives of several communicators of one process).
+    bool eager_coll_ = false;
+    std::vector<cudaGraphExec_t> segs_;
+    std::vector<std::function<void()>> between_;
     int64_t graph_kernels_ = 0;
+    void destroy_graph();
+    void segment_break(std::function<void()> op);
+    void end_segment();
+    void trace_capture(const char* where);
+    void launch_graph();
     int64_t steps_ = 0;
     int64_t cur_step_ = 0;      // index of the trajectory block holding the current policy input
 

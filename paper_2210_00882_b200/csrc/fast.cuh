@@ -40,6 +40,12 @@ struct FastLearnArgs {
     float* values_out2;        // mode 0: rows [split_rows, rows) (when split_rows >= 0)
     int64_t split_rows;
     const __nv_bfloat16* wimg; // pre-built shared-memory image of the weight tiles (bf16)
+    // Critic activation reuse: mode 0 stores each tile's hidden-activation tiles (the exact
+    // shared-memory bytes, bf16) for tiles < save_tiles; mode 1 with hload set skips the
+    // forward pass and bulk-copies them back (values come from values_in).
+    uint8_t* hsave;
+    int64_t save_tiles;
+    int hload;
     double inv_n, value_coef, entropy_coef;
     float clip_eps;
     float* partials;           // [grid, part_stride]
@@ -49,6 +55,7 @@ struct FastLearnArgs {
 
 size_t fast_mlp_smem_bytes(const FastNet& n);
 size_t fast_wimg_bytes(const FastNet& n);  // bytes of the weight-tile image (smem prefix)
+size_t fast_hsave_bytes(const FastNet& n); // bytes of one tile's hidden-activation tiles
 // Builds the bf16 W^T tile image of one net from the f32 params (once per train iteration,
 // shared by every CTA of the critic-forward / learn kernels that follow).
 void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv_bfloat16* img);

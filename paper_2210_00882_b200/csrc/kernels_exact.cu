@@ -516,11 +516,8 @@ void exact_loss_reduce(cudaStream_t s, const double* terms, int64_t n, double en
 
 void exact_dw(cudaStream_t s, const DwTile* tiles, int ntiles, int64_t M) {
     const size_t smem = 4 * kDwRows * 33 * sizeof(double);
-    static bool configured = false;
-    if (!configured) {
-        FLW_CUDA(cudaFuncSetAttribute(k_dw, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured = true;
-    }
+    // per-device attribute: set on every launch (cheap, and legal inside stream capture)
+    FLW_CUDA(cudaFuncSetAttribute(k_dw, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (ntiles > 0) k_dw<<<ntiles, 256, smem, s>>>(tiles, M);
 }
 

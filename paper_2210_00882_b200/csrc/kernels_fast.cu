@@ -75,8 +75,9 @@ __device__ __forceinline__ float act_fwd(float z, int act) { return act == 0 ? t
 
 __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, hbar;
     __shared__ uint32_t tslot;
+    uint32_t hphase = 0;
     const FastNet& n = a.net;
     const Smem S = carve(n);
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
     if (w == 0) umma::tmem_alloc<512>(&tslot);
     if (t == 0) {
         umma::mbar_init(&bar, 1);
+        umma::mbar_init(&hbar, 1);
         umma::fence_barrier_init();
     }
     umma::fence_before_sync();
@@ -159,12 +161,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
             }
             if (a.kind == kNetPolicyA3c) val_r = a.values_in[row];
         }
+        // hidden-activation region [S.h[0], S.h[L-2] + size): contiguous in shared memory
+        const uint32_t hbytes = L > 1 ? S.dz[0] - S.h[0] : 0u;
+        const bool reuse = a.hload && a.mode == 1 && hbytes > 0;
+        if (t == 0 && hbytes > 0) {
+            if (a.mode == 0) umma::bulk_wait_read();  // previous tile's save has read the region
+            if (reuse) {  // saved tile -> shared memory via the TMA engine (arrives on hbar)
+                umma::mbar_expect_tx(&hbar, hbytes);
+                const uint8_t* src = a.hsave + static_cast<size_t>(tile) * hbytes;
+                for (uint32_t o = 0; o < hbytes; o += 16384u)
+                    umma::bulk_g2s(smem + S.h[0] + o, src + o, min(16384u, hbytes - o), &hbar);
+            }
+        }
         umma::fence_async_smem();
         umma::fence_before_sync();
         __syncthreads();
-        // ---- forward
+        // ---- forward (skipped when the critic's activations are reused from the values pass)
         float out[16];
-        for (int l = 0; l < L; ++l) {
+        if (reuse) {
+            umma::mbar_wait(&hbar, hphase);
+            hphase ^= 1;
+            out[0] = valid ? a.values_in[row] : 0.0f;
+        }
+        for (int l = 0; l < (reuse ? 0 : L); ++l) {
             const int di = n.din[l], dout = n.dout[l];
             const uint32_t in_tile = l == 0 ? sbase + S.x : sbase + S.h[l - 1];
             if (t == 0) {
@@ -198,6 +217,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
             umma::fence_async_smem();
             umma::fence_before_sync();
             __syncthreads();
+        }
+        // values pass: hand this tile's hidden activations to the learn kernel (async bulk store)
+        if (a.mode == 0 && a.hsave && t == 0 && hbytes > 0 && tile < a.save_tiles) {
+            uint8_t* dst = a.hsave + static_cast<size_t>(tile) * hbytes;
+            for (uint32_t o = 0; o < hbytes; o += 16384u)
+                umma::bulk_s2g(dst + o, smem + S.h[0] + o, min(16384u, hbytes - o));
+            umma::bulk_commit();
         }
         // ---- loss epilogue (rl.cpp:137-202 semantics, f32) -> dZ_{L-1}; the output layer is one
         // 16-column chunk, owned by the half-0 warps.
@@ -376,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_mlp(FastLearnArgs a) {
             for (int64_t i = t; i < a.part_stride; i += kThreads) part[i] = 0.0f;
         }
     }
+    if (t == 0 && a.mode == 0 && a.hsave) umma::bulk_wait_all();  // saved tiles landed in HBM
     umma::fence_before_sync();
     __syncthreads();
     if (w == 0) umma::tmem_free<512>(tmem);
@@ -549,6 +576,10 @@ __global__ void k_sum_blocks(const double* __restrict__ b, int n, double* out) {
 // ------------------------------------------------------------------------------ launchers
 size_t fast_mlp_smem_bytes(const FastNet& n) { return carve(n).total; }
 size_t fast_wimg_bytes(const FastNet& n) { return carve(n).x; }
+size_t fast_hsave_bytes(const FastNet& n) {
+    const Smem s = carve(n);
+    return n.L > 1 ? s.dz[0] - s.h[0] : 0;
+}
 
 void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv_bfloat16* img) {
     k_build_wimg<<<16, 256, 0, s>>>(params, n, img);
@@ -556,11 +587,8 @@ void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv
 
 void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid) {
     const size_t smem = carve(a.net).total;
-    static size_t configured = 0;
-    if (smem > configured) {
-        FLW_CUDA(cudaFuncSetAttribute(k_fast_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured = smem;
-    }
+    // per-device attribute: set on every launch (cheap, and legal inside stream capture)
+    FLW_CUDA(cudaFuncSetAttribute(k_fast_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     k_fast_mlp<<<grid, kThreads, smem, s>>>(a);
 }
 

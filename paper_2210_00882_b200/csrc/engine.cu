@@ -60,6 +60,8 @@ struct Engine::Bufs {
     float *part_p = nullptr, *part_c = nullptr, *loss_parts = nullptr;
     __nv_bfloat16 *wimg_p = nullptr, *wimg_c = nullptr;
     uint8_t* hsave = nullptr;           // critic hidden activations of the values pass (bf16 tiles)
+    uint8_t* hscratch = nullptr;        // k_learn per-(CTA, group) activation scratch
+    int grid2 = 0;                      // k_learn grid (two tiles per CTA in flight)
     double *block_sums = nullptr, *rsum_scratch = nullptr;
     std::vector<void*> owned;
 
@@ -244,6 +246,9 @@ void Engine::alloc() {
         b.wimg_p = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.pol) / 2));
         b.wimg_c = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.crit) / 2));
         b.hsave = b.alloc<uint8_t>(static_cast<int64_t>(fast_hsave_bytes(b.crit)) * ((TR_ + 127) / 128));
+        b.grid2 = static_cast<int>(std::min<int64_t>(sms, ((TR_ + 127) / 128 + 1) / 2));
+        b.hscratch = b.alloc<uint8_t>(static_cast<int64_t>(
+            std::max(fast_learn_scratch_bytes(b.pol), fast_learn_scratch_bytes(b.crit)) * 2 * b.grid2));
         b.block_sums = b.alloc<double>(2 * ((R_ + 255) / 256));
         b.rsum_scratch = b.alloc<double>(256);
         b.values = b.alloc<float>(TR_);
@@ -529,8 +534,20 @@ void Engine::enq_learn_fast() {
     static const bool hreuse = std::getenv("FLW_NO_HREUSE") == nullptr;
     f.hsave = hreuse ? b.hsave : nullptr;
     f.save_tiles = hreuse ? (TR_ + 127) / 128 : 0;
+    // k_learn (warp-specialised, two tiles per SM) unless FLW_LEARN_V1 selects the
+    // single-tile kernel (A/B measurement only)
+    static const bool v1 = std::getenv("FLW_LEARN_V1") != nullptr;
+    const int lgrid = v1 ? b.grid : b.grid2;
+    auto launch = [&](int grid) {
+        if (v1)
+            fast_mlp(stream_, f, grid);
+        else
+            fast_learn(stream_, f, grid);
+    };
+    f.hscratch = b.hscratch;
     probe_begin("critic_fwd");
-    fast_mlp(stream_, f, static_cast<int>(std::min<int64_t>(b.grid, (f.rows + 127) / 128)));
+    launch(static_cast<int>(std::min<int64_t>(
+        lgrid, v1 ? (f.rows + 127) / 128 : ((f.rows + 127) / 128 + 1) / 2)));
     probe_end();
     f.split_rows = -1;
     probe_begin("gae");
@@ -556,7 +573,7 @@ void Engine::enq_learn_fast() {
     f.part_stride = s.P_policy;
     f.loss_partials = b.loss_parts;
     probe_begin("learn_policy");
-    fast_mlp(stream_, f, b.grid);
+    launch(lgrid);
     probe_end();
     f.net = b.crit;
     f.wimg = b.wimg_c;
@@ -565,14 +582,14 @@ void Engine::enq_learn_fast() {
     f.kind = kNetCritic;
     f.partials = b.part_c;
     f.part_stride = s.P - s.P_policy;
-    f.loss_partials = b.loss_parts + 3 * b.grid;
+    f.loss_partials = b.loss_parts + 3 * lgrid;
     probe_begin("learn_critic");
-    fast_mlp(stream_, f, b.grid);
+    launch(lgrid);
     probe_end();
     probe_begin("reduce");
-    fast_reduce_partials(stream_, b.part_p, b.part_c, b.grid, s.P_policy, s.P - s.P_policy, b.grads);
+    fast_reduce_partials(stream_, b.part_p, b.part_c, lgrid, s.P_policy, s.P - s.P_policy, b.grads);
     probe_end();
-    fast_reduce_loss(stream_, b.loss_parts, b.grid, 2, cfg_.entropy_coef, b.loss);
+    fast_reduce_loss(stream_, b.loss_parts, lgrid, 2, cfg_.entropy_coef, b.loss);
 }
 
 void Engine::enq_learn_grads() {

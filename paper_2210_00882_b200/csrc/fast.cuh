@@ -46,6 +46,7 @@ struct FastLearnArgs {
     uint8_t* hsave;
     int64_t save_tiles;
     int hload;
+    uint8_t* hscratch;         // k_learn: per (CTA, group) hidden-activation scratch [grid*2][hbytes]
     double inv_n, value_coef, entropy_coef;
     float clip_eps;
     float* partials;           // [grid, part_stride]
@@ -60,6 +61,10 @@ size_t fast_hsave_bytes(const FastNet& n); // bytes of one tile's hidden-activat
 // shared by every CTA of the critic-forward / learn kernels that follow).
 void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv_bfloat16* img);
 void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid);
+// Warp-specialised two-tiles-per-SM learn kernel (kernels_learn.cu); same arguments.
+void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid);
+size_t fast_learn_smem_bytes(const FastNet& n);
+size_t fast_learn_scratch_bytes(const FastNet& n);  // hidden bytes of one 128-row tile
 void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int nparts, int64_t Pp, int64_t Pc,
                           float* grads);
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int nparts, int nsets, double entropy_coef, float* loss);

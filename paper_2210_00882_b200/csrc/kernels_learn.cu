@@ -1,0 +1,663 @@
+// Fast-numerics learn phase, warp-specialised: one PPO/A3C train iteration of one MLP, fused
+// per 128-row tile on the 5th-gen tensor cores (forward -> loss -> backward -> dW in TMEM).
+//
+// Every stage of a tile is a dependency chain (MMA -> TMEM load -> activation -> shared store ->
+// next MMA), so a single tile per SM leaves the tensor pipe idle most of the time. Here each CTA
+// (one per SM) runs TWO tiles at once, ping-ponging on the tensor core:
+//
+//   warps 0-3  epilogue group 0   (tile rows = TMEM lanes, one full row per thread)
+//   warps 4-7  epilogue group 1
+//   warp  8    producer: lane 0 issues every tcgen05.mma / commit and every TMA bulk copy, in a
+//              FIXED alternating order (group 0 job j, group 1 job j, ...), so the dW
+//              accumulation order - and therefore the result - is deterministic.
+//
+// Shared memory holds, per group, the input tile, a 2-slot ring for hidden activations and a
+// 2-slot dZ ring; the forward streams every hidden tile H_l out to global scratch (L2-resident,
+// cp.async.bulk) and the backward streams H_{l-1} back in one stage ahead, so two tiles fit in
+// the 227 KB of one SM. The critic learn pass skips its forward entirely: its activations were
+// saved by the values pass (same parameters) and are streamed from there.
+//
+// TMEM (512 columns): Z/dH accumulator of group g at columns [64g, 64g+64) (M=128); dW_l
+// accumulators (M=64, half-sub-partition layout) for the layer pair (2j, 2j+1) at columns
+// [128+64j, 192+64j), lane offsets 0 / 16 - shared by both groups, accumulated across all tiles.
+//
+// Stage protocol per group: the producer waits epi_done[g] (all 4 epilogue warps stored their
+// operand tile and fenced it to the async proxy), issues the stage's MMAs and commits to
+// mma_done[g]; the epilogue waits mma_done[g], reads the accumulator, writes the next operand.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "fast.cuh"
+#include "umma.cuh"
+
+namespace flw {
+
+namespace {
+
+constexpr int kRows = 128;
+constexpr int kMaxW = 64;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 32 * (kEpiWarps + 1);
+constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
+constexpr int kXPre = 32;                      // input columns prefetched in registers
+
+struct Carve {
+    uint32_t wt[kMaxLayers], wbytes;
+    uint32_t x[2], ring[2][2], dz[2][2];
+    uint32_t bias, dbacc, loss, total;
+    uint32_t hoff[kMaxLayers], hbytes;  // hidden tile offsets inside one tile's saved activations
+};
+
+__host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline Carve carve_learn(const FastNet& n) {
+    Carve c{};
+    uint32_t off = 0;
+    for (int l = 0; l < n.L; ++l) {  // identical to the weight image built by k_build_wimg
+        c.wt[l] = off;
+        off = align_up(off + static_cast<uint32_t>(n.dout[l] * n.din[l] * 2), 128);
+    }
+    c.wbytes = off;
+    off = align_up(off, 1024);
+    for (int g = 0; g < 2; ++g) {
+        c.x[g] = off;
+        off = align_up(off + kRows * n.din[0] * 2, 1024);
+        for (int s = 0; s < 2; ++s) {
+            c.ring[g][s] = off;
+            off += kSlot;
+        }
+        for (int s = 0; s < 2; ++s) {
+            c.dz[g][s] = off;
+            off += kSlot;
+        }
+    }
+    c.bias = off;
+    off += kMaxLayers * kMaxW * 4;
+    c.dbacc = off;
+    off += kEpiWarps * kMaxLayers * kMaxW * 4;
+    c.loss = off;
+    off += kEpiWarps * 3 * 4;
+    c.total = off + 2048;  // slack: M=64 MN-major reads of narrow tiles run past their end
+    uint32_t h = 0;
+    for (int l = 0; l + 1 < n.L; ++l) {
+        c.hoff[l] = h;
+        h += static_cast<uint32_t>(kRows * n.dout[l] * 2);
+    }
+    c.hbytes = h;
+    return c;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+}
+
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// bf16x2 MUFU tanh: two activations per SFU op; the result is already the packed bf16 operand.
+__device__ __forceinline__ uint32_t tanh_bf16x2(uint32_t x) {
+    uint32_t y;
+    asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
+__device__ __forceinline__ void bulk_load(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint64_t* bar) {
+    umma::mbar_expect_tx(bar, bytes);
+    for (uint32_t o = 0; o < bytes; o += 16384u) umma::bulk_g2s(dst + o, src + o, min(16384u, bytes - o), bar);
+}
+
+__device__ __forceinline__ void bulk_store(uint8_t* dst, const uint8_t* src, uint32_t bytes) {
+    for (uint32_t o = 0; o < bytes; o += 16384u) umma::bulk_s2g(dst + o, src + o, min(16384u, bytes - o));
+    umma::bulk_commit();
+}
+
+// Column sums over the warp's 32 rows of a 32-wide row slice held one row per lane: a
+// reduce-scatter butterfly (31 shuffles); lane l ends with the sum of column l.
+__device__ __forceinline__ float warp_colsum32(float* v, int lane) {
+#pragma unroll
+    for (int w = 16, off = 16; off > 0; w >>= 1, off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (i < w) {
+                const float keep = up ? v[i + w] : v[i];
+                const float send = up ? v[i] : v[i + w];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        }
+    }
+    return v[0];
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t mma_done[2], epi_done[2], ldbar[2][2], wbar;
+    __shared__ uint32_t tslot;
+    __shared__ Carve C;  // offsets live in shared memory, not in 40 registers per thread
+#ifdef FLW_LEARN_TRACE
+    __shared__ long long tr_p[4][64], tr_e[3][64], tr_f[5][16];
+    int np_ev = 0, ne_ev = 0;
+#endif
+    const FastNet& n = a.net;
+    if (threadIdx.x == 0) C = carve_learn(n);
+    __syncthreads();
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    const int L = n.L;
+    const int64_t ntiles = (a.rows + kRows - 1) / kRows;
+    const int G = gridDim.x;
+    const bool learn = a.mode == 1;
+    const bool reuse = learn && a.hload && L > 1;  // critic: forward skipped, activations streamed in
+    const bool fwd = !reuse;
+    const int nfwd = fwd ? L : 0;
+    const int njobs = learn ? nfwd + L : L;
+    float* bias = reinterpret_cast<float*>(smem + C.bias);
+    float* dbacc = reinterpret_cast<float*>(smem + C.dbacc);
+    // hidden H_k is resident in the ring from the forward (never reloaded) for the last two
+    auto resident = [&](int k) { return fwd && (k == L - 2 || k == L - 3); };
+    auto dzslot = [&](int k) { return (L - 1 - k) & 1; };
+
+    // ---- setup
+    if (t == 0) {
+        for (int g = 0; g < 2; ++g) {
+            umma::mbar_init(&mma_done[g], 1);
+            umma::mbar_init(&epi_done[g], 4);
+            umma::mbar_init(&ldbar[g][0], 1);
+            umma::mbar_init(&ldbar[g][1], 1);
+        }
+        umma::mbar_init(&wbar, 1);
+        umma::fence_barrier_init();
+    }
+    for (int l = 0; l < L; ++l)
+        for (int o = t; o < kMaxW; o += kThreads) bias[l * kMaxW + o] = o < n.rout[l] ? a.params[n.boff[l] + o] : 0.0f;
+    for (int i = t; i < kEpiWarps * kMaxLayers * kMaxW; i += kThreads) dbacc[i] = 0.0f;
+    if (w == 0) umma::tmem_alloc<512>(&tslot);
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = tslot;
+    const uint32_t sbase = umma::smem_u32(smem);
+
+    if (w == kEpiWarps) {
+        // ================================================================ producer (one lane)
+        if (lane == 0) {
+            bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
+            umma::mbar_wait(&wbar, 0);
+            uint32_t ph_epi[2] = {0, 0}, ph_ld[2][2] = {{0, 0}, {0, 0}};
+            bool dw_init[kMaxLayers];
+            for (int l = 0; l < kMaxLayers; ++l) dw_init[l] = false;
+            auto dw_tmem = [&](int l) {
+                return tmem + 128u + 64u * static_cast<uint32_t>(l >> 1) + ((l & 1) ? (16u << 16) : 0u);
+            };
+            auto hsrc = [&](int g, int64_t tile) -> uint8_t* {
+                return reuse ? a.hsave + static_cast<size_t>(tile) * C.hbytes
+                             : a.hscratch + static_cast<size_t>(2 * blockIdx.x + g) * C.hbytes;
+            };
+            auto issue_dw = [&](int g, int l, uint32_t hin) {  // dW_l += H_{l-1}^T dZ_l  (M = din_l)
+                const int di = n.din[l], dout = n.dout[l];
+                const uint32_t dzt = sbase + C.dz[g][dzslot(l)];
+                const uint32_t id = umma::idesc_bf16(64, dout, true, true);
+                for (int kb = 0; kb < kRows / 16; ++kb) {
+                    umma::mma_bf16(dw_tmem(l), umma::desc_mnmajor(hin, di, kb), umma::desc_mnmajor(dzt, dout, kb), id,
+                                   dw_init[l] || kb > 0);
+                }
+                dw_init[l] = true;
+            };
+            for (int64_t it = 0;; ++it) {
+                int64_t tl[2];
+                bool has[2];
+                for (int g = 0; g < 2; ++g) {
+                    tl[g] = it * 2 * G + 2 * static_cast<int64_t>(blockIdx.x) + g;
+                    has[g] = tl[g] < ntiles;
+                }
+                if (!has[0] && !has[1]) break;
+                for (int j = 0; j < njobs; ++j) {
+                    for (int g = 0; g < 2; ++g) {
+                        if (!has[g]) continue;
+                        umma::mbar_wait(&epi_done[g], ph_epi[g]);
+                        ph_epi[g] ^= 1;
+#ifdef FLW_LEARN_TRACE
+                        if (g == 0 && np_ev < 64) tr_p[0][np_ev] = clock64();
+#endif
+                        umma::fence_after_sync();
+                        const uint32_t zt = tmem + 64u * static_cast<uint32_t>(g);
+                        if (j < nfwd) {  // ---- forward layer l: Z = In_l W_l^T
+                            const int l = j, di = n.din[l], dout = n.dout[l];
+                            // stream H_{l-1} out: to this group's scratch (learn: reloaded by the
+                            // backward) or to the values pass's save area (the critic learn's input)
+                            bool stored = false;
+                            if (l >= 1) {
+                                uint8_t* dst = nullptr;
+                                if (learn) {
+                                    if (!resident(l - 1))
+                                        dst = a.hscratch + static_cast<size_t>(2 * blockIdx.x + g) * C.hbytes;
+                                } else if (a.hsave && tl[g] < a.save_tiles) {
+                                    dst = a.hsave + static_cast<size_t>(tl[g]) * C.hbytes;
+                                }
+                                if (dst) {
+                                    bulk_store(dst + C.hoff[l - 1], smem + C.ring[g][(l - 1) & 1],
+                                               kRows * n.dout[l - 1] * 2);
+                                    stored = true;
+                                }
+                            }
+#ifdef FLW_LEARN_TRACE
+                            if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
+#endif
+                            const uint32_t in = l == 0 ? sbase + C.x[g] : sbase + C.ring[g][(l - 1) & 1];
+                            const uint32_t id = umma::idesc_bf16(128, dout, false, false);
+                            for (int kb = 0; kb < di / 16; ++kb)
+                                umma::mma_bf16(zt, umma::desc_kmajor(in, di, kb),
+                                               umma::desc_kmajor(sbase + C.wt[l], di, kb), id, kb > 0);
+#ifdef FLW_LEARN_TRACE
+                            if (g == 0 && np_ev < 64) tr_p[3][np_ev] = clock64();
+#endif
+                            // the epilogue of this stage overwrites the ring slot of H_{l-2}
+                            if (stored)
+                                bulk_wait_read1();
+                            else
+                                umma::bulk_wait_read();
+                            umma::commit(&mma_done[g]);
+#ifdef FLW_LEARN_TRACE
+                            if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
+#endif
+                        } else {  // ---- backward layer m
+                            const int m = L - 1 - (j - nfwd);
+                            if (m == L - 1) umma::bulk_wait_all();  // saved activations landed
+                            if (m >= 1 && !resident(m - 1)) {       // stream H_{m-1} in, one stage ahead
+                                const int s = (m - 1) & 1;
+                                bulk_load(smem + C.ring[g][s], hsrc(g, tl[g]) + C.hoff[m - 1],
+                                          kRows * n.dout[m - 1] * 2, &ldbar[g][s]);
+                            }
+#ifdef FLW_LEARN_TRACE
+                            if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
+#endif
+                            if (m + 1 <= L - 1) {  // deferred dW_{m+1} (needs H_m)
+                                if (!resident(m)) {
+                                    umma::mbar_wait(&ldbar[g][m & 1], ph_ld[g][m & 1]);
+                                    ph_ld[g][m & 1] ^= 1;
+                                }
+                                issue_dw(g, m + 1, sbase + C.ring[g][m & 1]);
+                            }
+#ifdef FLW_LEARN_TRACE
+                            if (g == 0 && np_ev < 64) tr_p[3][np_ev] = clock64();
+#endif
+                            if (m >= 1) {  // dH_m = dZ_m W_m  (N = din_m)
+                                const int di = n.din[m], dout = n.dout[m];
+                                const uint32_t id = umma::idesc_bf16(128, di, false, true);
+                                const uint32_t dzt = sbase + C.dz[g][dzslot(m)];
+                                for (int kb = 0; kb < dout / 16; ++kb)
+                                    umma::mma_bf16(zt, umma::desc_kmajor(dzt, dout, kb),
+                                                   umma::desc_mnmajor(sbase + C.wt[m], di, kb), id, kb > 0);
+                            } else {
+                                issue_dw(g, 0, sbase + C.x[g]);
+                            }
+                            umma::commit(&mma_done[g]);
+#ifdef FLW_LEARN_TRACE
+                            if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
+#endif
+                        }
+                    }
+                }
+            }
+            umma::bulk_wait_all();
+        }
+    } else {
+        // ================================================================ epilogue groups
+        const int g = w >> 2, q = w & 3;
+        const int r = 32 * q + lane;  // tile row == TMEM lane
+        const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
+        const uint32_t zt = tmem + lane_base + 64u * static_cast<uint32_t>(g);
+        uint32_t ph_mma = 0, ph_ld[2] = {0, 0};
+        float pl_acc = 0.0f, vl_acc = 0.0f, en_acc = 0.0f;
+        float* mydb = dbacc + w * kMaxLayers * kMaxW;
+        const int din0 = n.din[0];
+        const bool xpre = a.in_cols <= kXPre;
+        uint32_t xnext[kXPre / 2];  // next tile's input row, already packed to bf16 pairs
+        auto fetch_x = [&](int64_t tile) {
+            const int64_t rw = tile * kRows + r;
+            const bool ok = tile < ntiles && rw < a.rows;
+#pragma unroll
+            for (int c = 0; c < kXPre; c += 2) {
+                const float x0 = (ok && c < a.in_cols) ? a.X[rw * a.in_cols + c] : 0.0f;
+                const float x1 = (ok && c + 1 < a.in_cols) ? a.X[rw * a.in_cols + c + 1] : 0.0f;
+                xnext[c / 2] = umma::pack_bf16x2(x0, x1);
+            }
+        };
+        auto signal = [&]() {  // operand tile stored: hand it to the producer
+            umma::fence_async_smem();
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&epi_done[g]);
+#ifdef FLW_LEARN_TRACE
+            if (t == 0 && ne_ev > 0 && ne_ev <= 64) tr_e[2][ne_ev - 1] = clock64();
+#endif
+        };
+        auto wait_mma = [&]() {
+#ifdef FLW_LEARN_TRACE
+            if (t == 0 && ne_ev < 64) tr_e[0][ne_ev] = clock64();
+#endif
+            umma::mbar_wait(&mma_done[g], ph_mma);
+            ph_mma ^= 1;
+            umma::fence_after_sync();
+#ifdef FLW_LEARN_TRACE
+            if (t == 0 && ne_ev < 64) tr_e[1][ne_ev++] = clock64();
+#endif
+        };
+        // loads accumulator columns [c0, c0 + 32) of this thread's row (those below `width`)
+        auto ld_acc32 = [&](float* v, int c0, int width) {
+            umma::tmem_ld16(zt + c0, v);
+            if (c0 + 16 < width) umma::tmem_ld16(zt + c0 + 16, v + 16);
+            umma::tmem_ld_wait();
+        };
+        // db_layer[c0 + lane] += column sum of this warp's 32 rows (fixed order, no atomics)
+        auto colsum32 = [&](float* v, int c0, int width, int layer) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (c0 + c >= width) v[c] = 0.0f;
+            const float sum = warp_colsum32(v, lane);
+            mydb[layer * kMaxW + c0 + lane] += sum;
+        };
+        bool first = true;
+        if (xpre) fetch_x(2 * static_cast<int64_t>(blockIdx.x) + g);
+        for (int64_t tile = 2 * static_cast<int64_t>(blockIdx.x) + g; tile < ntiles; tile += 2 * G) {
+            const int64_t row = tile * kRows + r;
+            const bool valid = row < a.rows;
+            if (learn && !first) wait_mma();  // previous tile's last MMAs (dW_0) released X and dZ
+            first = false;
+            // ---- input tile (f32 -> bf16)
+            if (!xpre) {
+                for (int c0 = 0; c0 < din0; c0 += 8) {
+                    float u[8];
+                    for (int j = 0; j < 8; ++j) {
+                        const int c = c0 + j;
+                        u[j] = (valid && c < a.in_cols) ? a.X[row * a.in_cols + c] : 0.0f;
+                    }
+                    umma::st_row8(smem + C.x[g], din0, r, c0, u);
+                }
+            } else {
+#pragma unroll
+                for (int c0 = 0; c0 < kXPre; c0 += 8)
+                    if (c0 < din0)
+                        *reinterpret_cast<uint4*>(smem + C.x[g] + umma::tile_offset(r, c0, din0)) =
+                            make_uint4(xnext[c0 / 2], xnext[c0 / 2 + 1], xnext[c0 / 2 + 2], xnext[c0 / 2 + 3]);
+                fetch_x(tile + 2 * G);
+            }
+            int act_r = 0;
+            float lpo_r = 0.0f, adv_r = 0.0f, ret_r = 0.0f, val_r = 0.0f;
+            if (learn && valid) {
+                if (a.kind != kNetPolicyPpo) ret_r = a.ret[row];
+                if (a.kind != kNetCritic) act_r = a.actions[row];
+                if (a.kind == kNetPolicyPpo) {
+                    lpo_r = a.logp_old[row];
+                    adv_r = a.adv[row];
+                }
+                if (a.kind == kNetPolicyA3c || reuse) val_r = a.values_in[row];
+            }
+            float out[16];
+            if (fwd) {
+                signal();  // X ready
+                for (int l = 0; l < L; ++l) {
+                    const int dout = n.dout[l];
+                    wait_mma();
+                    const float* bl = bias + l * kMaxW;
+                    if (l + 1 < L) {
+                        uint8_t* dst = smem + C.ring[g][l & 1];
+                        // 32 columns of H_l = act(Z + b); FULL: no per-chunk guards, so the
+                        // compiler interleaves the four 8-column chains
+                        auto half = [&]<bool FULL>(int h0) {
+                            float z[32];
+                            umma::tmem_ld16(zt + h0, z);
+                            if (FULL || h0 + 16 < dout) umma::tmem_ld16(zt + h0 + 16, z + 16);
+                            umma::tmem_ld_wait();
+#pragma unroll
+                            for (int c = 0; c < 32; c += 8) {
+                                if (FULL || h0 + c < dout) {
+                                    const float4 b0 = *reinterpret_cast<const float4*>(bl + h0 + c);
+                                    const float4 b1 = *reinterpret_cast<const float4*>(bl + h0 + c + 4);
+                                    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                                    uint32_t p[4];
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) {
+                                        const float z0 = z[c + 2 * i] + bb[2 * i];
+                                        const float z1 = z[c + 2 * i + 1] + bb[2 * i + 1];
+                                        p[i] = a.act == 0 ? umma::pack_bf16x2(tanh_fast(z0), tanh_fast(z1))
+                                                          : umma::pack_bf16x2(fmaxf(z0, 0.0f), fmaxf(z1, 0.0f));
+                                    }
+                                    *reinterpret_cast<uint4*>(dst + umma::tile_offset(r, h0 + c, dout)) =
+                                        make_uint4(p[0], p[1], p[2], p[3]);
+                                }
+                            }
+                        };
+                        if (dout == kMaxW) {
+                            half.template operator()<true>(0);
+                            half.template operator()<true>(32);
+                        } else {
+                            for (int h0 = 0; h0 < dout; h0 += 32) half.template operator()<false>(h0);
+                        }
+                        signal();  // H_l ready
+                    } else {
+                        float z[32];
+                        ld_acc32(z, 0, 16);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) out[j] = z[j] + bl[j];
+                    }
+                }
+            } else {
+                out[0] = val_r;
+            }
+            if (!learn) {  // values pass
+                if (valid) {
+                    if (a.split_rows >= 0 && row >= a.split_rows)
+                        a.values_out2[row - a.split_rows] = out[0];
+                    else
+                        a.values_out[row] = out[0];
+                }
+                continue;
+            }
+            // ---- loss epilogue (rl.cpp:137-202 semantics, f32) -> dZ_{L-1}
+            {
+                float dz[32];  // output layer width <= 16 (the loss epilogue owns the whole row)
+#pragma unroll
+                for (int j = 0; j < 32; ++j) dz[j] = 0.0f;
+                if (valid) {
+                    if (a.kind == kNetCritic) {  // value MSE: dV = 2 c_v (V - R) / N
+                        const float verr = out[0] - ret_r;
+                        dz[0] = static_cast<float>(2.0 * a.value_coef * a.inv_n) * verr;
+                        vl_acc += static_cast<float>(a.value_coef * a.inv_n) * verr * verr;
+                    } else {  // policy: clipped surrogate (PPO) or A3C policy gradient, + entropy bonus
+                        const int A = n.rout[L - 1];
+                        float mx = out[0];
+                        for (int j = 1; j < A; ++j) mx = fmaxf(mx, out[j]);
+                        float den = 0.0f;
+                        for (int j = 0; j < A; ++j) den += __expf(out[j] - mx);
+                        const float lden = __logf(den);
+                        float p[16], lp[16], H = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            lp[j] = out[j] - mx - lden;
+                            p[j] = j < A ? __expf(lp[j]) : 0.0f;
+                            if (j < A) H -= p[j] * lp[j];
+                        }
+                        const float inv_n = static_cast<float>(a.inv_n);
+                        float lpa = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (j == act_r) lpa = lp[j];
+                        float coef;
+                        if (a.kind == kNetPolicyPpo) {
+                            float adv = adv_r;
+                            if (a.adv_stats) {
+                                const double sd = a.adv_stats[1];
+                                if (!(sd < 1e-8)) adv = static_cast<float>((adv - a.adv_stats[0]) / (sd + 1e-8));
+                            }
+                            const float ratio = __expf(lpa - lpo_r);
+                            const float clipped = fminf(fmaxf(ratio, 1.0f - a.clip_eps), 1.0f + a.clip_eps);
+                            const float s1 = ratio * adv, s2 = clipped * adv;
+                            pl_acc -= fminf(s1, s2) * inv_n;
+                            coef = s1 <= s2 ? -inv_n * ratio * adv : 0.0f;
+                        } else {  // A3C: advantage R - V (rl.cpp:188)
+                            const float adv = ret_r - val_r;
+                            pl_acc -= lpa * adv * inv_n;
+                            coef = -inv_n * adv;
+                        }
+                        en_acc += H * inv_n;
+                        const float eci = static_cast<float>(a.entropy_coef) * inv_n;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (j < A) dz[j] = coef * ((j == act_r ? 1.0f : 0.0f) - p[j]) + eci * p[j] * (lp[j] + H);
+                    }
+                }
+                const int wo = n.dout[L - 1];
+                uint8_t* dst = smem + C.dz[g][dzslot(L - 1)];
+#pragma unroll
+                for (int c0 = 0; c0 < 16; c0 += 8) {
+                    if (c0 < wo) {
+                        // round to the bf16 operand first so db sums exactly what dW sees
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) dz[c0 + i] = __bfloat162float(__float2bfloat16(dz[c0 + i]));
+                        umma::st_row8(dst, wo, r, c0, dz + c0);
+                    }
+                }
+                signal();  // dZ_{L-1} ready
+                colsum32(dz, 0, wo, L - 1);
+            }
+            // ---- backward epilogues: dZ_{m-1} = dH_m * act'(H_{m-1})
+            for (int m = L - 1; m >= 1; --m) {
+                const int di = n.din[m];
+                wait_mma();
+                const int s = (m - 1) & 1;
+                if (!resident(m - 1)) {
+                    umma::mbar_wait(&ldbar[g][s], ph_ld[s]);
+                    ph_ld[s] ^= 1;
+                }
+                const uint8_t* hs = smem + C.ring[g][s];
+                uint8_t* dst = smem + C.dz[g][dzslot(m - 1)];
+                auto half = [&]<bool FULL>(int h0) {
+                    float gv[32];
+                    umma::tmem_ld16(zt + h0, gv);
+                    if (FULL || h0 + 16 < di) umma::tmem_ld16(zt + h0 + 16, gv + 16);
+                    umma::tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 32; c += 8) {
+                        if (FULL || h0 + c < di) {
+                            float y[8];
+                            umma::ld_row8(hs, di, r, h0 + c, y);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const float d = a.act == 0 ? gv[c + i] * (1.0f - y[i] * y[i])
+                                                           : (y[i] > 0.0f ? gv[c + i] : 0.0f);
+                                gv[c + i] = __bfloat162float(__float2bfloat16(d));
+                            }
+                            umma::st_row8(dst, di, r, h0 + c, gv + c);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) gv[c + i] = 0.0f;
+                        }
+                    }
+                    if (h0 + 32 >= di) signal();  // dZ_{m-1} complete: hand it to the producer
+                    mydb[(m - 1) * kMaxW + h0 + lane] += warp_colsum32(gv, lane);
+                };
+                if (di == kMaxW) {
+                    half.template operator()<true>(0);
+                    half.template operator()<true>(32);
+                } else {
+                    for (int h0 = 0; h0 < di; h0 += 32) half.template operator()<false>(h0);
+                }
+            }
+        }
+        if (learn && !first) wait_mma();  // the last tile's dW_0
+        // ---- loss partials of this warp
+        for (int off = 16; off > 0; off >>= 1) {
+            pl_acc += __shfl_xor_sync(0xffffffffu, pl_acc, off);
+            vl_acc += __shfl_xor_sync(0xffffffffu, vl_acc, off);
+            en_acc += __shfl_xor_sync(0xffffffffu, en_acc, off);
+        }
+        if (lane == 0) {
+            float* ls = reinterpret_cast<float*>(smem + C.loss);
+            ls[w * 3 + 0] = pl_acc;
+            ls[w * 3 + 1] = vl_acc;
+            ls[w * 3 + 2] = en_acc;
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+
+    // ---- per-CTA partials: dW from TMEM, db and loss terms from shared memory (fixed order)
+    if (learn && w < kEpiWarps) {
+        const int q = w & 3, half = w >> 2;
+        const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
+        const bool any = 2 * static_cast<int64_t>(blockIdx.x) < ntiles;
+        float* part = a.partials + static_cast<int64_t>(blockIdx.x) * a.part_stride;
+        for (int l = 0; l < L; ++l) {
+            const int dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
+            const int lo = (l & 1) ? 16 : 0;
+            const uint32_t col = 128u + 64u * static_cast<uint32_t>(l >> 1);
+            for (int c0 = 16 * half; c0 < dout; c0 += 32) {
+                float v[16];
+                umma::tmem_ld16(tmem + lane_base + col + c0, v);
+                umma::tmem_ld_wait();
+                const int mrow = lane - lo;  // dW row (input index) held by this lane
+                if (any && mrow >= 0 && mrow < 16) {
+                    const int i = mrow + 16 * q;
+                    if (i < ri)
+                        for (int j = 0; j < 16; ++j)
+                            if (c0 + j < ro) part[n.woff[l] - n.woff[0] + i * ro + c0 + j] = v[j];
+                }
+            }
+            for (int o = t; o < ro; o += 32 * kEpiWarps) {
+                float s = 0.0f;
+                for (int k = 0; k < kEpiWarps; ++k) s += dbacc[(k * kMaxLayers + l) * kMaxW + o];
+                part[n.boff[l] - n.woff[0] + o] = s;
+            }
+        }
+        if (t < 3) {
+            const float* ls = reinterpret_cast<const float*>(smem + C.loss);
+            float s = 0.0f;
+            for (int k = 0; k < kEpiWarps; ++k) s += ls[k * 3 + t];
+            a.loss_partials[blockIdx.x * 3 + t] = s;
+        }
+        if (!any)
+            for (int64_t i = t; i < a.part_stride; i += 32 * kEpiWarps) part[i] = 0.0f;
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (w == 0) umma::tmem_free<512>(tmem);
+#ifdef FLW_LEARN_TRACE
+    if (blockIdx.x == 0 && t == 0 && a.mode == 1) {
+        const long long t0 = tr_p[0][0];
+        for (int i = 0; i < ne_ev; ++i)
+            printf("E %2d wait %7lld got %7lld signal %7lld\n", i, tr_e[0][i] - t0, tr_e[1][i] - t0, tr_e[2][i] - t0);
+        for (int i = 0; i < 6; ++i)
+            printf("F %2d ld0 %7lld done0 %7lld ld1 %7lld done1 %7lld stored %7lld\n", i, tr_f[0][i] - t0,
+                   tr_f[1][i] - t0, tr_f[2][i] - t0, tr_f[3][i] - t0, tr_f[4][i] - t0);
+    }
+    if (blockIdx.x == 0 && t == 32 * kEpiWarps && a.mode == 1) {
+        const long long t0 = tr_p[0][0];
+        for (int i = 0; i < np_ev; ++i)
+            printf("P %2d epi %7lld a %7lld b %7lld commit %7lld\n", i, tr_p[0][i] - t0, tr_p[2][i] - t0,
+                   tr_p[3][i] - t0, tr_p[1][i] - t0);
+    }
+#endif
+}
+
+}  // namespace
+
+size_t fast_learn_smem_bytes(const FastNet& n) { return carve_learn(n).total; }
+size_t fast_learn_scratch_bytes(const FastNet& n) { return carve_learn(n).hbytes; }
+
+void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid) {
+    const size_t smem = carve_learn(a.net).total;
+    if (smem > 227u * 1024u) throw Error(Errc::Config, "fast numerics: network too wide/deep for one SM's shared memory");
+    // per-device attribute: set on every launch (cheap, and legal inside stream capture)
+    FLW_CUDA(cudaFuncSetAttribute(k_learn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_learn<<<grid, kThreads, smem, s>>>(a);
+}
+
+}  // namespace flw

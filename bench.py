@@ -306,7 +306,8 @@ def bench_ours(args, world, rank, local):
                        "l2": "per-episode working set (activations, ~0.9 GB) exceeds the 126 MB L2"},
             "episode_ms": episode_ms, "gpu_launches": stats["graph_kernels"] * args.steps,
             "clocks": clk.summary(), "e2e": e2e, "roofline": roofline, "kernel_shares": shares}
-    line["hbm_kernels"] = hbm_microbenchmarks(peaks)
+    if not args.no_microbench:
+        line["hbm_kernels"] = hbm_microbenchmarks(peaks)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
@@ -321,6 +322,8 @@ def main():
     ap.add_argument("--numerics", choices=["exact", "fast"], default="fast")
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-microbench", action="store_true",
+                    help="skip the scaled HBM kernel sweeps (profiling runs: the launch list then holds episodes only)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

@@ -101,6 +101,25 @@ __device__ __forceinline__ float tanh_fast(float x) {
     return y;
 }
 
+// tanh on the FMA pipe (packed f32x2): odd polynomial of degree 17 on [-4, 4], saturated beyond;
+// max abs error 1.7e-3 (below bf16 resolution near 1). Half of each 8-column chunk uses it, the
+// other half MUFU.TANH, so the two pipes share the activation work.
+__device__ __forceinline__ float2 tanh_poly2(float2 x) {
+    x.x = fminf(fmaxf(x.x, -4.0f), 4.0f);
+    x.y = fminf(fmaxf(x.y, -4.0f), 4.0f);
+    const float2 t = __fmul2_rn(x, x);
+    float2 p = make_float2(1.0064061584103001e-08f, 1.0064061584103001e-08f);
+    p = __ffma2_rn(p, t, make_float2(-7.318681696233398e-07f, -7.318681696233398e-07f));
+    p = __ffma2_rn(p, t, make_float2(2.24064351641573e-05f, 2.24064351641573e-05f));
+    p = __ffma2_rn(p, t, make_float2(-0.00037694742786698043f, -0.00037694742786698043f));
+    p = __ffma2_rn(p, t, make_float2(0.0038315874990075827f, 0.0038315874990075827f));
+    p = __ffma2_rn(p, t, make_float2(-0.024628829210996628f, -0.024628829210996628f));
+    p = __ffma2_rn(p, t, make_float2(0.10449711978435516f, 0.10449711978435516f));
+    p = __ffma2_rn(p, t, make_float2(-0.3220818042755127f, -0.3220818042755127f));
+    p = __ffma2_rn(p, t, make_float2(1.0f, 1.0f));
+    return __fmul2_rn(p, x);
+}
+
 // bf16x2 MUFU tanh: two activations per SFU op; the result is already the packed bf16 operand.
 __device__ __forceinline__ uint32_t tanh_bf16x2(uint32_t x) {
     uint32_t y;
@@ -229,23 +248,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                         const uint32_t zt = tmem + 64u * static_cast<uint32_t>(g);
                         if (j < nfwd) {  // ---- forward layer l: Z = In_l W_l^T
                             const int l = j, di = n.din[l], dout = n.dout[l];
-                            // stream H_{l-1} out: to this group's scratch (learn: reloaded by the
-                            // backward) or to the values pass's save area (the critic learn's input)
-                            bool stored = false;
-                            if (l >= 1) {
-                                uint8_t* dst = nullptr;
-                                if (learn) {
-                                    if (!resident(l - 1))
-                                        dst = a.hscratch + static_cast<size_t>(2 * blockIdx.x + g) * C.hbytes;
-                                } else if (a.hsave && tl[g] < a.save_tiles) {
-                                    dst = a.hsave + static_cast<size_t>(tl[g]) * C.hbytes;
-                                }
-                                if (dst) {
-                                    bulk_store(dst + C.hoff[l - 1], smem + C.ring[g][(l - 1) & 1],
-                                               kRows * n.dout[l - 1] * 2);
-                                    stored = true;
-                                }
-                            }
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
 #endif
@@ -257,18 +259,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[3][np_ev] = clock64();
 #endif
-                            // the epilogue of this stage overwrites the ring slot of H_{l-2}
-                            if (stored)
-                                bulk_wait_read1();
-                            else
-                                umma::bulk_wait_read();
                             umma::commit(&mma_done[g]);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
 #endif
                         } else {  // ---- backward layer m
                             const int m = L - 1 - (j - nfwd);
-                            if (m == L - 1) umma::bulk_wait_all();  // saved activations landed
                             if (m >= 1 && !resident(m - 1)) {       // stream H_{m-1} in, one stage ahead
                                 const int s = (m - 1) & 1;
                                 bulk_load(smem + C.ring[g][s], hsrc(g, tl[g]) + C.hoff[m - 1],
@@ -284,9 +280,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                                 }
                                 issue_dw(g, m + 1, sbase + C.ring[g][m & 1]);
                             }
-#ifdef FLW_LEARN_TRACE
-                            if (g == 0 && np_ev < 64) tr_p[3][np_ev] = clock64();
-#endif
                             if (m >= 1) {  // dH_m = dZ_m W_m  (N = din_m)
                                 const int di = n.din[m], dout = n.dout[m];
                                 const uint32_t id = umma::idesc_bf16(128, di, false, true);
@@ -305,7 +298,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     }
                 }
             }
-            umma::bulk_wait_all();
         }
     } else {
         // ================================================================ epilogue groups
@@ -330,7 +322,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             }
         };
         auto signal = [&]() {  // operand tile stored: hand it to the producer
+            // generic-proxy writes (shared operand tiles, global activation images) -> visible to
+            // the tensor core and to the producer's later TMA bulk loads
             umma::fence_async_smem();
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
             umma::fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(&epi_done[g]);
@@ -408,6 +403,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     const float* bl = bias + l * kMaxW;
                     if (l + 1 < L) {
                         uint8_t* dst = smem + C.ring[g][l & 1];
+                        // the same 16-byte chunks also go to global memory (the smem image of the
+                        // tile): this group's scratch (learn: reloaded by the backward) or the
+                        // values pass's save area (the critic learn's input)
+                        uint8_t* gdst = nullptr;
+                        if (learn) {
+                            if (!resident(l)) gdst = a.hscratch + static_cast<size_t>(2 * blockIdx.x + g) * C.hbytes;
+                        } else if (a.hsave && tile < a.save_tiles) {
+                            gdst = a.hsave + static_cast<size_t>(tile) * C.hbytes;
+                        }
+                        if (gdst) gdst += C.hoff[l];
                         // 32 columns of H_l = act(Z + b); FULL: no per-chunk guards, so the
                         // compiler interleaves the four 8-column chains
                         auto half = [&]<bool FULL>(int h0) {
@@ -426,11 +431,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                                     for (int i = 0; i < 4; ++i) {
                                         const float z0 = z[c + 2 * i] + bb[2 * i];
                                         const float z1 = z[c + 2 * i + 1] + bb[2 * i + 1];
-                                        p[i] = a.act == 0 ? umma::pack_bf16x2(tanh_fast(z0), tanh_fast(z1))
-                                                          : umma::pack_bf16x2(fmaxf(z0, 0.0f), fmaxf(z1, 0.0f));
+                                        if (a.act != 0) {
+                                            p[i] = umma::pack_bf16x2(fmaxf(z0, 0.0f), fmaxf(z1, 0.0f));
+                                        } else if (i < 2) {
+                                            p[i] = umma::pack_bf16x2(tanh_fast(z0), tanh_fast(z1));
+                                        } else {
+                                            const float2 y2 = tanh_poly2(make_float2(z0, z1));
+                                            p[i] = umma::pack_bf16x2(y2.x, y2.y);
+                                        }
                                     }
-                                    *reinterpret_cast<uint4*>(dst + umma::tile_offset(r, h0 + c, dout)) =
-                                        make_uint4(p[0], p[1], p[2], p[3]);
+                                    const uint32_t off = umma::tile_offset(r, h0 + c, dout);
+                                    const uint4 v4 = make_uint4(p[0], p[1], p[2], p[3]);
+                                    *reinterpret_cast<uint4*>(dst + off) = v4;
+                                    if (gdst) *reinterpret_cast<uint4*>(gdst + off) = v4;
                                 }
                             }
                         };
@@ -538,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                 }
                 const uint8_t* hs = smem + C.ring[g][s];
                 uint8_t* dst = smem + C.dz[g][dzslot(m - 1)];
-                auto half = [&]<bool FULL>(int h0) {
+                auto half = [&]<bool FULL, int h0>() {
                     float gv[32];
                     umma::tmem_ld16(zt + h0, gv);
                     if (FULL || h0 + 16 < di) umma::tmem_ld16(zt + h0 + 16, gv + 16);
@@ -548,13 +561,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                         if (FULL || h0 + c < di) {
                             float y[8];
                             umma::ld_row8(hs, di, r, h0 + c, y);
+                            uint32_t pk[4];
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                const float d = a.act == 0 ? gv[c + i] * (1.0f - y[i] * y[i])
-                                                           : (y[i] > 0.0f ? gv[c + i] : 0.0f);
-                                gv[c + i] = __bfloat162float(__float2bfloat16(d));
+                            for (int i = 0; i < 4; ++i) {
+                                const float2 yy = make_float2(y[2 * i], y[2 * i + 1]);
+                                const float2 gg = make_float2(gv[c + 2 * i], gv[c + 2 * i + 1]);
+                                float2 d;
+                                if (a.act == 0) {  // dZ = dH (1 - y^2), packed f32x2 on the FMA pipe
+                                    const float2 om = __ffma2_rn(make_float2(-yy.x, -yy.y), yy, make_float2(1.0f, 1.0f));
+                                    d = __fmul2_rn(gg, om);
+                                } else {
+                                    d = make_float2(yy.x > 0.0f ? gg.x : 0.0f, yy.y > 0.0f ? gg.y : 0.0f);
+                                }
+                                pk[i] = umma::pack_bf16x2(d.x, d.y);
+                                // db sums exactly the bf16 operand dW sees
+                                gv[c + 2 * i] = __uint_as_float(pk[i] << 16);
+                                gv[c + 2 * i + 1] = __uint_as_float(pk[i] & 0xFFFF0000u);
                             }
-                            umma::st_row8(dst, di, r, h0 + c, gv + c);
+                            *reinterpret_cast<uint4*>(dst + umma::tile_offset(r, h0 + c, di)) =
+                                make_uint4(pk[0], pk[1], pk[2], pk[3]);
                         } else {
 #pragma unroll
                             for (int i = 0; i < 8; ++i) gv[c + i] = 0.0f;
@@ -564,10 +589,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     mydb[(m - 1) * kMaxW + h0 + lane] += warp_colsum32(gv, lane);
                 };
                 if (di == kMaxW) {
-                    half.template operator()<true>(0);
-                    half.template operator()<true>(32);
+                    half.template operator()<true, 0>();
+                    half.template operator()<true, 32>();
                 } else {
-                    for (int h0 = 0; h0 < di; h0 += 32) half.template operator()<false>(h0);
+                    half.template operator()<false, 0>();
+                    if (32 < di) half.template operator()<false, 32>();
                 }
             }
         }

@@ -78,6 +78,14 @@ enum { FLW_NUMERICS_EXACT = 0, FLW_NUMERICS_FAST = 1 };
  * [env_lo, env_hi) of env_total on CUDA device `device`. */
 int flw_dpd_create(const char* algo_json, int device, uint64_t seed, int64_t env_lo, int64_t env_hi,
                    int64_t env_total, int numerics, flw_dpd** out);
+/* R consecutive units folded into one engine on one GPU (R > #GPUs replicas):
+ * [env_lo, env_hi) is split like split_envs (plan.cpp:46-55); each replica keeps its own
+ * advantage statistics, loss mean, gradient and reward sum, and the gradients are averaged in
+ * unit order (local_run.cpp:408-411). A gradient group then has R units per rank. */
+int flw_dpd_create_replicas(const char* algo_json, int device, uint64_t seed, int64_t env_lo, int64_t env_hi,
+                            int64_t env_total, int numerics, int replicas, flw_dpd** out);
+/* Per-replica reward sums of the last episode, unit order (exact numerics). */
+int flw_dpd_replica_rewards(flw_dpd* e, double* out, int64_t cap);
 int flw_dpd_destroy(flw_dpd* e);
 
 /* Gradient group (GradSync, local_run.cpp:379-414): rank 0 creates an id (128 bytes), the

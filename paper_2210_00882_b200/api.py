@@ -73,13 +73,24 @@ class DpdEngine:
     """flw_dpd: one DP-D unit owning envs [env_lo, env_hi) of env_total on `device`."""
 
     def __init__(self, algo, device: int = 0, seed: int = 0, env_lo: int = 0, env_hi: int | None = None,
-                 env_total: int | None = None, numerics: str = "exact"):
+                 env_total: int | None = None, numerics: str = "exact", replicas: int = 1):
         a = json.loads(algo) if isinstance(algo, str) else algo
         total = int(a.get("env", {}).get("num", 1)) if env_total is None else env_total
         hi = total if env_hi is None else env_hi
         num = {"exact": N.FLW_NUMERICS_EXACT, "fast": N.FLW_NUMERICS_FAST}[numerics]
         self._h = C.c_void_p()
-        N.check(N.lib().flw_dpd_create(_json(a), device, seed, env_lo, hi, total, num, C.byref(self._h)))
+        self.replicas = replicas
+        if replicas == 1:
+            N.check(N.lib().flw_dpd_create(_json(a), device, seed, env_lo, hi, total, num, C.byref(self._h)))
+        else:
+            N.check(N.lib().flw_dpd_create_replicas(_json(a), device, seed, env_lo, hi, total, num, replicas,
+                                                    C.byref(self._h)))
+
+    def replica_rewards(self):
+        """Per-replica reward sums of the last episode (unit order)."""
+        out = (C.c_double * self.replicas)()
+        N.check(N.lib().flw_dpd_replica_rewards(self._h, out, self.replicas))
+        return list(out)
 
     def close(self):
         if self._h:

@@ -31,6 +31,7 @@ struct flw_program {
     DeployConfig deploy;
     Plan plan;
     Numerics numerics = Numerics::Exact;
+    int reps_per_gpu = 0;  // deploy "replicas_per_gpu": units folded per engine (0: only when k > #GPUs)
     // Engines persist across flw_run_local calls on the same program (re-initialised per run):
     // device buffers and the captured episode graph are set up once.
     std::vector<std::unique_ptr<Engine>> engines;
@@ -136,61 +137,83 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
         fail(Errc::Runtime, "no CUDA device visible: the DP-D engine has no CPU fallback");
-    if (k > ndev)
-        fail(Errc::InsufficientSlots, "dp-d plan has " + std::to_string(k) + " units but only " +
-                                          std::to_string(ndev) + " GPUs are visible (one accel slot = one GPU)");
-    bool reuse = static_cast<int>(p.engines.size()) == k && p.unpartitioned_engines == unpart;
+    // One engine per GPU. More units than GPUs fold R = k / #GPUs consecutive units into each
+    // engine (each keeps its own statistics, loss mean, gradient and reward sum).
+    int R = 1;
+    if (p.reps_per_gpu > 0) {
+        R = p.reps_per_gpu;
+        if (k % R != 0 || k / R > ndev)
+            fail(Errc::InsufficientSlots, "replicas_per_gpu=" + std::to_string(R) + " does not fold " +
+                                              std::to_string(k) + " units onto " + std::to_string(ndev) + " GPUs");
+    } else if (k > ndev) {
+        if (k % ndev != 0)
+            fail(Errc::InsufficientSlots, "dp-d plan has " + std::to_string(k) + " units but " + std::to_string(ndev) +
+                                              " GPUs are visible: folding needs k to be a multiple of the GPU count");
+        R = k / ndev;
+    }
+    const int ng = k / R;
+    bool reuse = static_cast<int>(p.engines.size()) == ng && p.unpartitioned_engines == unpart &&
+                 (ng == 0 || p.engines[0]->replicas() == R);
     if (!reuse) {
         p.engines.clear();
-        for (const Unit& u : units)
-            p.engines.push_back(std::make_unique<Engine>(p.algo, u.id, seed, u.env_lo, u.env_hi, p.algo.envs,
-                                                         p.numerics));
+        for (int g = 0; g < ng; ++g) {
+            const Unit& first = units[static_cast<size_t>(g * R)];
+            const Unit& last = units[static_cast<size_t>(g * R + R - 1)];
+            p.engines.push_back(std::make_unique<Engine>(p.algo, g, seed, first.env_lo, last.env_hi, p.algo.envs,
+                                                         p.numerics, R));
+        }
         p.unpartitioned_engines = unpart;
-        if (k > 1) {
+        if (ng > 1) {
             std::vector<int> devs;
-            for (const Unit& u : units) devs.push_back(u.id);
+            for (int g = 0; g < ng; ++g) devs.push_back(g);
             auto comms = Comm::init_all(devs);
             std::vector<Comm*> cs;
-            for (int r = 0; r < k; ++r) {
-                auto c = std::make_unique<Comm>(comms[r], r, k);
+            for (int g = 0; g < ng; ++g) {
+                auto c = std::make_unique<Comm>(comms[g], g, ng);
                 cs.push_back(c.get());
-                p.engines[r]->set_eager_collectives(true);
-                p.engines[r]->set_comm(std::move(c));
+                p.engines[g]->set_eager_collectives(true);
+                p.engines[g]->set_comm(std::move(c));
             }
-            Comm::connect_all(cs, devs, p.engines[0]->shape().P);
+            Comm::connect_all(cs, devs, static_cast<int64_t>(R) * p.engines[0]->shape().P);
         }
     } else {
         for (auto& e : p.engines) e->reinit(seed);
     }
     eps.assign(static_cast<size_t>(episodes), {});
+    // reward sum of every unit and episode, folded in unit order below (local_run.cpp:560-570)
     std::vector<std::vector<double>> rsum(static_cast<size_t>(k), std::vector<double>(episodes, 0.0));
     const ProgramShape& s = p.engines[0]->shape();
     // Reference byte accounting of the GradSync channel: k(k-1) legs x learn iters x (14 + 8P).
     const int64_t per_ep_bytes = k > 1 ? static_cast<int64_t>(k) * (k - 1) * s.learn_iters * (14 + 8 * s.P) : 0;
     std::mutex err_mu;
     std::string first_error;
-    if (k == 1) {
+    auto run_one = [&](int g, int64_t ep) {
+        p.engines[g]->run_episode(ep);
+        const std::vector<double> v = p.engines[g]->replica_reward_sums();
+        for (int r = 0; r < R; ++r) rsum[static_cast<size_t>(g * R + r)][static_cast<size_t>(ep)] = v[static_cast<size_t>(r)];
+    };
+    if (ng == 1) {
         for (int64_t ep = 0; ep < episodes; ++ep) {
             auto t0 = std::chrono::steady_clock::now();
-            rsum[0][static_cast<size_t>(ep)] = p.engines[0]->run_episode(ep);
+            run_one(0, ep);
             auto t1 = std::chrono::steady_clock::now();
             eps[static_cast<size_t>(ep)].wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         }
     } else {
-        // Every unit's episode graph segments are captured before any unit launches.
+        // Every engine's episode graph segments are captured before any engine launches.
         for (auto& e : p.engines) e->prepare();
-        std::barrier gate(k + 1);
+        std::barrier gate(ng + 1);
         std::vector<std::thread> threads;
-        for (int r = 0; r < k; ++r)
-            threads.emplace_back([&, r] {
+        for (int g = 0; g < ng; ++g)
+            threads.emplace_back([&, g] {
                 for (int64_t ep = 0; ep < episodes; ++ep) {
                     gate.arrive_and_wait();  // raise_gate(ep)
                     try {
-                        flw_trace(("unit " + std::to_string(r) + " episode " + std::to_string(ep)).c_str());
-                        if (first_error.empty()) rsum[r][static_cast<size_t>(ep)] = p.engines[r]->run_episode(ep);
+                        flw_trace(("engine " + std::to_string(g) + " episode " + std::to_string(ep)).c_str());
+                        if (first_error.empty()) run_one(g, ep);
                     } catch (const std::exception& e) {
-                        std::lock_guard<std::mutex> g(err_mu);
-                        if (first_error.empty()) first_error = "unit " + std::to_string(r) + ": " + e.what();
+                        std::lock_guard<std::mutex> lk2(err_mu);
+                        if (first_error.empty()) first_error = "unit " + std::to_string(g * R) + ": " + e.what();
                         // peers may be blocked inside a collective waiting for this unit
                         for (auto& en : p.engines)
                             if (en->comm()) en->comm()->abort();
@@ -241,6 +264,7 @@ int flw_program_create(const char* algo_json, const char* deploy_json, flw_progr
             p->deploy = parse_deploy_config(deploy_json);
             auto j = nlohmann::json::parse(deploy_json);
             if (j.contains("numerics")) p->numerics = numerics_from(j["numerics"].get<std::string>());
+            if (j.contains("replicas_per_gpu")) p->reps_per_gpu = j["replicas_per_gpu"].get<int>();
         } else {
             p->deploy = DeployConfig{{"local"}, 8, 8, Policy::DpA};  // capi.cpp:211-212 default
         }
@@ -298,6 +322,28 @@ int flw_dpd_create(const char* algo_json, int device, uint64_t seed, int64_t env
         auto h = std::make_unique<flw_dpd>();
         h->engine = std::make_unique<Engine>(a, device, seed, env_lo, env_hi, env_total, static_cast<Numerics>(numerics));
         *out = h.release();
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_create_replicas(const char* algo_json, int device, uint64_t seed, int64_t env_lo, int64_t env_hi,
+                            int64_t env_total, int numerics, int replicas, flw_dpd** out) {
+    return guarded([&] {
+        AlgoConfig a = parse_algo_config(algo_json ? algo_json : "{}");
+        if (numerics != FLW_NUMERICS_EXACT && numerics != FLW_NUMERICS_FAST) fail(Errc::Config, "bad numerics");
+        auto h = std::make_unique<flw_dpd>();
+        h->engine = std::make_unique<Engine>(a, device, seed, env_lo, env_hi, env_total, static_cast<Numerics>(numerics),
+                                             replicas);
+        *out = h.release();
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_replica_rewards(flw_dpd* e, double* out, int64_t cap) {
+    return guarded([&] {
+        const std::vector<double> v = eng(e).replica_reward_sums();
+        if (cap < static_cast<int64_t>(v.size())) fail(Errc::Config, "output buffer too small");
+        std::copy(v.begin(), v.end(), out);
         return FLW_OK;
     });
 }

@@ -63,6 +63,15 @@ struct Engine::Bufs {
     uint8_t* hscratch = nullptr;        // k_learn per-(CTA, group) activation scratch
     int grid2 = 0;                      // k_learn grid (two tiles per CTA in flight)
     double *block_sums = nullptr, *rsum_scratch = nullptr;
+    // R > 1 replicas: env -> replica map, replica-major trajectory copies (exact), per-replica
+    // gradient slots [R, P], advantage statistics [R, 2] and row weights (fast)
+    int32_t* rep_of_env = nullptr;
+    int64_t *rep_off = nullptr, *rep_n = nullptr;
+    float *pstates = nullptr, *plogp = nullptr, *prew = nullptr, *pdone = nullptr;
+    int32_t* pact = nullptr;
+    double* prew_d = nullptr;
+    float* gslots = nullptr;
+    float* rep_w = nullptr;
     std::vector<void*> owned;
 
     template <typename T>
@@ -95,8 +104,9 @@ int act_of(const AlgoConfig& c) { return c.activation == "relu" ? kRelu : kTanh;
 }  // namespace
 
 Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo, int64_t env_hi, int64_t env_total,
-               Numerics numerics)
-    : cfg_(cfg), device_(device), seed_(seed), lo_(env_lo), hi_(env_hi), etot_(env_total), numerics_(numerics) {
+               Numerics numerics, int replicas)
+    : cfg_(cfg), device_(device), seed_(seed), lo_(env_lo), hi_(env_hi), etot_(env_total), numerics_(numerics),
+      nrep_(replicas) {
     cfg_.validate();
     shape_ = program_shape(cfg_);
     if (!shape_.accel_capable)
@@ -112,6 +122,18 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     if (env_hi <= env_lo || env_lo < 0 || env_hi > env_total) fail(Errc::Config, "bad env range");
     if (shape_.n_actions > 16) fail(Errc::Config, "at most 16 discrete actions are supported");
     E_ = env_hi - env_lo;
+    if (nrep_ < 1 || nrep_ > E_) fail(Errc::Config, "replicas per engine must be in [1, envs]");
+    if (nrep_ > 1 && mappo_) fail(Errc::Config, "MAPPO runs one replica per GPU in this build");
+    {  // split_envs (plan.cpp:46-55): contiguous ranges, the remainder to the low replicas
+        const int64_t base = E_ / nrep_, rem = E_ % nrep_;
+        int64_t off = 0;
+        for (int r = 0; r < nrep_; ++r) {
+            const int64_t n = base + (r < rem ? 1 : 0);
+            rep_off_.push_back(off);
+            rep_n_.push_back(n);
+            off += n;
+        }
+    }
     R_ = static_cast<int64_t>(shape_.n_agents) * E_;
     T_ = cfg_.steps_per_episode;
     TR_ = T_ * R_;
@@ -155,7 +177,7 @@ void Engine::set_comm(std::unique_ptr<Comm> comm) {
     comm_ = std::move(comm);
     FLW_CUDA(cudaSetDevice(device_));  // the gather buffer must live on this engine's GPU
     if (comm_ && numerics_ == Numerics::Exact && !b_->gather) {
-        b_->gather = b_->alloc<float>(static_cast<int64_t>(comm_->nranks()) * shape_.P);
+        b_->gather = b_->alloc<float>(static_cast<int64_t>(comm_->nranks()) * nrep_ * shape_.P);
     }
 }
 
@@ -213,9 +235,36 @@ void Engine::alloc() {
     }
     b.adv = b.alloc<float>(TR_);
     b.ret = b.alloc<float>(TR_);
-    b.stats = b.alloc<double>(2);
+    b.stats = b.alloc<double>(2 * nrep_);
     b.loss = b.alloc<float>(1);
-    b.rsum = b.alloc<double>(1);
+    b.rsum = b.alloc<double>(nrep_);
+    if (nrep_ > 1) {
+        std::vector<int32_t> roe(static_cast<size_t>(E_));
+        for (int r = 0; r < nrep_; ++r)
+            for (int64_t e = rep_off_[r]; e < rep_off_[r] + rep_n_[r]; ++e) roe[static_cast<size_t>(e)] = r;
+        b.rep_of_env = b.alloc<int32_t>(E_);
+        b.rep_off = b.alloc<int64_t>(nrep_);
+        b.rep_n = b.alloc<int64_t>(nrep_);
+        FLW_CUDA(cudaMemcpy(b.rep_of_env, roe.data(), roe.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        FLW_CUDA(cudaMemcpy(b.rep_off, rep_off_.data(), rep_off_.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        FLW_CUDA(cudaMemcpy(b.rep_n, rep_n_.data(), rep_n_.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        if (numerics_ == Numerics::Exact) {
+            b.pstates = b.alloc<float>(TR_ * S);
+            b.pact = b.alloc<int32_t>(TR_);
+            b.plogp = b.alloc<float>(TR_);
+            b.prew = b.alloc<float>(TR_);
+            b.pdone = b.alloc<float>(TR_);
+            b.prew_d = b.alloc<double>(TR_);
+            b.gslots = b.alloc<float>(static_cast<int64_t>(nrep_) * s.P);
+        } else {
+            // fast: row weight 1 / (R * T * E_r) folds the replica means and their average
+            std::vector<float> w(static_cast<size_t>(nrep_));
+            for (int r = 0; r < nrep_; ++r)
+                w[static_cast<size_t>(r)] = static_cast<float>(1.0 / (static_cast<double>(nrep_) * T_ * rep_n_[r]));
+            b.rep_w = b.alloc<float>(nrep_);
+            FLW_CUDA(cudaMemcpy(b.rep_w, w.data(), w.size() * sizeof(float), cudaMemcpyHostToDevice));
+        }
+    }
     if (numerics_ == Numerics::Fast) {
         // Fused tensor-core learn kernels: per-CTA dW partials replace the per-layer activations.
         auto make_net = [&](int net) {
@@ -266,24 +315,32 @@ void Engine::alloc() {
     b.last_value = b.Hl[L - 1];
     b.adv_d = b.alloc<double>(TR_);
     b.terms = b.alloc<double>(3 * TR_);
-    // dW tile table: every (net, layer) as 32(t, incl. the bias row t == K) x 32(j) tiles.
+    // dW tile table: every (replica, net, layer) as 32(t, incl. the bias row t == K) x 32(j)
+    // tiles; replica r's chains run over its own T*E_r rows (replica-major copies) into its
+    // gradient slot.
     std::vector<DwTile> tiles;
-    for (int net = 0; net < 2; ++net) {
-        const auto& d = net == 0 ? s.pdims : s.cdims;
-        const auto& H = net == 0 ? b.Hp : b.Hc;
-        const auto& DZ = net == 0 ? b.DZp : b.DZc;
-        for (int l = 0; l < L; ++l) {
-            int K = d[l], N = d[l + 1];
-            for (int t0 = 0; t0 <= K; t0 += 32)
-                for (int j0 = 0; j0 < N; j0 += 32) {
-                    DwTile t{};
-                    t.H = l == 0 ? ((net == 1 && mappo_) ? b.cin : b.states) : H[l - 1];
-                    t.DZ = DZ[l];
-                    t.gW = b.grads + s.woff[net][l];
-                    t.gB = b.grads + s.boff[net][l];
-                    t.K = K, t.N = N, t.t0 = t0, t.j0 = j0;
-                    tiles.push_back(t);
-                }
+    for (int r = 0; r < nrep_; ++r) {
+        const int64_t row0 = T_ * rep_off_[r];
+        float* g = nrep_ > 1 ? b.gslots + static_cast<int64_t>(r) * s.P : b.grads;
+        const float* X0 = nrep_ > 1 ? b.pstates : b.states;
+        for (int net = 0; net < 2; ++net) {
+            const auto& d = net == 0 ? s.pdims : s.cdims;
+            const auto& H = net == 0 ? b.Hp : b.Hc;
+            const auto& DZ = net == 0 ? b.DZp : b.DZc;
+            for (int l = 0; l < L; ++l) {
+                int K = d[l], N = d[l + 1];
+                for (int t0 = 0; t0 <= K; t0 += 32)
+                    for (int j0 = 0; j0 < N; j0 += 32) {
+                        DwTile t{};
+                        t.H = (l == 0 ? ((net == 1 && mappo_) ? b.cin : X0) : H[l - 1]) + row0 * K;
+                        t.DZ = DZ[l] + row0 * N;
+                        t.gW = g + s.woff[net][l];
+                        t.gB = g + s.boff[net][l];
+                        t.K = K, t.N = N, t.t0 = t0, t.j0 = j0;
+                        t.rows = T_ * rep_n_[r] * (mappo_ ? s.n_agents : 1);
+                        tiles.push_back(t);
+                    }
+            }
         }
     }
     b.ntiles = static_cast<int>(tiles.size());
@@ -514,6 +571,9 @@ void Engine::enq_learn_fast() {
     f.entropy_coef = cfg_.entropy_coef;
     f.clip_eps = static_cast<float>(cfg_.clip_eps);
     f.split_rows = -1;
+    f.rep_of_env = nrep_ > 1 ? b.rep_of_env : nullptr;
+    f.rep_w = b.rep_w;
+    f.rep_E = E_;
     fast_build_wimg(stream_, b.params, b.crit, b.wimg_c);
     fast_build_wimg(stream_, b.params, b.pol, b.wimg_p);
     // values = critic(states), last_value = critic(last_next)
@@ -536,7 +596,8 @@ void Engine::enq_learn_fast() {
     f.save_tiles = hreuse ? (TR_ + 127) / 128 : 0;
     // k_learn (warp-specialised, two tiles per SM) unless FLW_LEARN_V1 selects the
     // single-tile kernel (A/B measurement only)
-    static const bool v1 = std::getenv("FLW_LEARN_V1") != nullptr;
+    static const bool v1_env = std::getenv("FLW_LEARN_V1") != nullptr;
+    const bool v1 = v1_env && nrep_ == 1;
     const int lgrid = v1 ? b.grid : b.grid2;
     auto launch = [&](int grid) {
         if (v1)
@@ -553,6 +614,8 @@ void Engine::enq_learn_fast() {
     probe_begin("gae");
     fast_gae(stream_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
              b.block_sums, b.stats);
+    if (nrep_ > 1 && ppo && cfg_.normalize_adv)  // each folded unit normalises over its own rows
+        fast_rep_adv_stats(stream_, b.adv, T_, E_, b.rep_off, b.rep_n, nrep_, b.stats);
     probe_end();
     // learn: policy then critic, each a persistent fused kernel
     f.mode = 1;
@@ -597,20 +660,37 @@ void Engine::enq_learn_grads() {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions, L = s.L;
-    const float* X = b.states;  // [T*R, S] t-major policy rows
+    // R > 1: the replica-major copies made after the rollout (enq_permute_replicas), so every
+    // replica's rows are one contiguous t-major block [T, E_r]
+    const bool rep = nrep_ > 1;
+    const float* X = rep ? b.pstates : b.states;  // [T*R, S] t-major policy rows
     // critic rows: the states themselves (PPO/A3C) or [joint | one-hot] (MAPPO); block T holds
     // the last step's next rows (last_next / last nci, programs.cpp:240-245, 422-427)
-    const float* Xc = mappo_ ? b.cin : b.states;
-    const float* last_next = Xc + T_ * R_ * s.crit_in;
+    const float* Xc = mappo_ ? b.cin : X;
+    const float* last_next = (mappo_ ? b.cin : b.states) + T_ * R_ * s.crit_in;
+    const float* rew = rep ? b.prew : b.rew;
+    const float* done_f = rep ? b.pdone : b.done_f;
+    const int32_t* actions = rep ? b.pact : b.actions;
+    const float* logp = rep ? b.plogp : b.logp;
+    (void)S;
     enq_mlp_forward(1, Xc, TR_, b.Hc.data());         // values = critic(states | ci)
     enq_mlp_forward(1, last_next, R_, b.Hl.data());   // last_value = critic(last_next | last nci)
     const bool ppo = s.algo != Algo::A3c;
-    exact_gae(stream_, b.rew, b.Hc[L - 1], b.done_f, b.Hl[L - 1], TR_, R_, cfg_.gamma, cfg_.lam, b.adv_d, b.ret, ppo);
-    if (ppo) exact_normalize(stream_, b.adv_d, TR_, cfg_.normalize_adv, b.stats, b.adv);
     enq_mlp_forward(0, X, TR_, b.Hp.data());          // logits_new = policy(states)
-    exact_loss_rows(stream_, ppo ? 0 : 1, b.Hp[L - 1], b.Hc[L - 1], b.actions, b.logp, b.adv, b.ret, TR_, A,
-                    cfg_.clip_eps, cfg_.value_coef, cfg_.entropy_coef, b.DZp[L - 1], b.DZc[L - 1], b.terms);
-    // Adjoint chains (row-parallel), then every dW/db chain of both nets in one launch.
+    // Per replica (= per reference unit): GAE over its E_r streams, advantage normalisation
+    // with its own statistics, loss mean over its T*E_r rows.
+    for (int r = 0; r < nrep_; ++r) {
+        const int64_t ro = T_ * rep_off_[r] * (mappo_ ? s.n_agents : 1);
+        const int64_t nr = rep_n_[r] * (mappo_ ? s.n_agents : 1), tr = T_ * nr;
+        const int64_t lo = rep_off_[r] * (mappo_ ? s.n_agents : 1);
+        exact_gae(stream_, rew + ro, b.Hc[L - 1] + ro, done_f + ro, b.Hl[L - 1] + lo, tr, nr, cfg_.gamma, cfg_.lam,
+                  b.adv_d + ro, b.ret + ro, ppo);
+        if (ppo) exact_normalize(stream_, b.adv_d + ro, tr, cfg_.normalize_adv, b.stats + 2 * r, b.adv + ro);
+        exact_loss_rows(stream_, ppo ? 0 : 1, b.Hp[L - 1] + ro * A, b.Hc[L - 1] + ro, actions + ro, logp + ro,
+                        b.adv + ro, b.ret + ro, tr, A, cfg_.clip_eps, cfg_.value_coef, cfg_.entropy_coef,
+                        b.DZp[L - 1] + ro * A, b.DZc[L - 1] + ro, b.terms + 3 * ro);
+    }
+    // Adjoint chains (row-parallel), then every dW/db chain of both nets (and replicas) in one launch.
     for (int net = 0; net < 2; ++net) {
         const auto& d = net == 0 ? s.pdims : s.cdims;
         const auto& H = net == 0 ? b.Hp : b.Hc;
@@ -619,7 +699,18 @@ void Engine::enq_learn_grads() {
             exact_layer_dh(stream_, DZ[l], b.params + s.woff[net][l], H[l - 1], DZ[l - 1], TR_, d[l], d[l + 1],
                            act_of(cfg_));
     }
-    exact_dw(stream_, b.tiles, b.ntiles, TR_);
+    exact_dw(stream_, b.tiles, b.ntiles);
+}
+
+void Engine::enq_permute_replicas() {
+    Bufs& b = *b_;
+    ReplicaMap m{b.rep_of_env, b.rep_off, b.rep_n};
+    permute_rows_f32(stream_, b.states, b.pstates, T_, E_, shape_.obs_dim, m);
+    permute_rows_i32(stream_, b.actions, b.pact, T_, E_, m);
+    permute_rows_f32(stream_, b.logp, b.plogp, T_, E_, 1, m);
+    permute_rows_f32(stream_, b.rew, b.prew, T_, E_, 1, m);
+    permute_rows_f32(stream_, b.done_f, b.pdone, T_, E_, 1, m);
+    permute_rows_f64(stream_, b.rew_d, b.prew_d, T_, E_, m);
 }
 
 void Engine::enq_grad_sync_and_adam() {
@@ -628,15 +719,20 @@ void Engine::enq_grad_sync_and_adam() {
     adam_tick(stream_, b.ctx, b.bc_table, b.bc_len);
     const double* g64 = nullptr;
     double gscale = 1.0;
+    const bool rep = nrep_ > 1 && numerics_ == Numerics::Exact;
     if (comm_ && comm_->nranks() > 1) {
         if (numerics_ == Numerics::Exact) {
-            // GradSync (local_run.cpp:379-414): AllGather then the mean in unit-id (= rank) order.
-            auto op = [this, &b, P = s.P] { comm_->all_gather(b.grads, b.gather, P, stream_); };
+            // GradSync (local_run.cpp:379-414): AllGather then the mean in unit-id order; with
+            // R replicas per GPU each rank contributes its R consecutive units' gradients.
+            const float* send = rep ? b.gslots : b.grads;
+            const int64_t cnt = static_cast<int64_t>(nrep_) * s.P;
+            const int k = comm_->nranks() * nrep_;
+            auto op = [this, &b, send, cnt] { comm_->all_gather(send, b.gather, cnt, stream_); };
             if (eager_coll_ && capturing_)
                 segment_break(op);
             else
                 op();
-            exact_grad_mean(stream_, b.gather, comm_->nranks(), s.P, b.gmean);
+            exact_grad_mean(stream_, b.gather, k, s.P, b.gmean);
             g64 = b.gmean;
         } else {
             // Fast: in-place NCCL sum over NVLink, the 1/k of the mean folded into Adam.
@@ -647,6 +743,9 @@ void Engine::enq_grad_sync_and_adam() {
                 op();
             gscale = 1.0 / static_cast<double>(comm_->nranks());
         }
+    } else if (rep) {  // one GPU, R units: the ordered mean of the local slots
+        exact_grad_mean(stream_, b.gslots, nrep_, s.P, b.gmean);
+        g64 = b.gmean;
     }
     probe_begin("adam");
     exact_adam(stream_, b.ctx, b.params, b.grads, g64, b.m, b.v, s.P, cfg_.lr, 0.9, 0.999, 1e-8, gscale);
@@ -654,15 +753,21 @@ void Engine::enq_grad_sync_and_adam() {
 }
 
 void Engine::enq_reward_sum() {
-    // Episode reward sum in the reference's order: steps outer, envs inner (interp.cpp:257).
-    if (numerics_ == Numerics::Fast)
+    // Episode reward sum in the reference's order: steps outer, envs inner (interp.cpp:257),
+    // one chain per replica (= unit) over its own envs.
+    if (numerics_ == Numerics::Fast) {
         fast_sum(side_, b_->rew_d, T_ * E_, b_->rsum_scratch, b_->rsum);
-    else
+    } else if (nrep_ == 1) {
         exact_seq_sum(side_, b_->rew_d, T_ * E_, b_->rsum);
+    } else {
+        for (int r = 0; r < nrep_; ++r)
+            exact_seq_sum(side_, b_->prew_d + T_ * rep_off_[r], T_ * rep_n_[r], b_->rsum + r);
+    }
 }
 
 // ------------------------------------------------------------------- phase-level API
 void Engine::reset(int64_t ep) {
+    if (nrep_ > 1) fail(Errc::Config, "the phase-level API drives one replica per engine (use run_episode)");
     FLW_CUDA(cudaSetDevice(device_));
     set_episode(ep);
     enq_reset();
@@ -733,6 +838,7 @@ void Engine::build_graph() {
     else
         for (int64_t st = 0; st < T_; ++st) enq_step(st);
     probe_end();
+    if (nrep_ > 1 && numerics_ == Numerics::Exact) enq_permute_replicas();
     FLW_CUDA(cudaEventRecord(ev_fork_, stream_));
     FLW_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
     enq_reward_sum();
@@ -808,13 +914,21 @@ void Engine::enqueue_episodes(int64_t first, int64_t count) {
     if (!graph_) build_graph();
     FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, &first, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
     for (int64_t i = 0; i < count; ++i) launch_graph();
-    steps_ += T_ * count;
+    steps_ += T_ * count * nrep_;
     cur_step_ = T_;
 }
 
 double Engine::last_reward_sum() {
-    double r = 0.0;
-    FLW_CUDA(cudaMemcpy(&r, b_->rsum, sizeof(double), cudaMemcpyDeviceToHost));
+    double total = 0.0;
+    for (double v : replica_reward_sums()) total += v;
+    return total;
+}
+
+std::vector<double> Engine::replica_reward_sums() {
+    FLW_CUDA(cudaSetDevice(device_));
+    std::vector<double> r(static_cast<size_t>(nrep_), 0.0);
+    const int n = numerics_ == Numerics::Exact ? nrep_ : 1;
+    FLW_CUDA(cudaMemcpy(r.data(), b_->rsum, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost));
     return r;
 }
 
@@ -833,7 +947,7 @@ double Engine::run_episode(int64_t ep, float* device_ms) {
     flw_trace("run_episode: launched");
     FLW_CUDA(cudaStreamSynchronize(stream_));
     flw_trace("run_episode: synced");
-    steps_ += T_;
+    steps_ += T_ * nrep_;
     cur_step_ = T_;
     if (device_ms) FLW_CUDA(cudaEventElapsedTime(device_ms, ev_t0_, ev_t1_));
     return last_reward_sum();

@@ -34,8 +34,12 @@ class Comm;  // NCCL gradient group (comm.hpp)
 
 class Engine {
   public:
+    // `replicas` > 1 folds that many consecutive units (reference replicas with contiguous env
+    // ranges split like split_envs, plan.cpp:46-55) into this engine: each keeps its own
+    // advantage statistics, loss mean, gradient and reward sum; gradients are averaged in unit
+    // order (local_run.cpp:408-411) before Adam.
     Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo, int64_t env_hi, int64_t env_total,
-           Numerics numerics);
+           Numerics numerics, int replicas = 1);
     ~Engine();
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -59,6 +63,10 @@ class Engine {
     // Enqueue `count` episodes starting at `first` back to back (no host sync in between).
     void enqueue_episodes(int64_t first, int64_t count);
     double last_reward_sum();
+    // Per-replica reward sums of the last episode, in unit order (exact numerics; fast numerics
+    // report the unit total in slot 0).
+    std::vector<double> replica_reward_sums();
+    int replicas() const { return nrep_; }
     void sync();
     cudaStream_t stream() const { return stream_; }
 
@@ -109,6 +117,9 @@ class Engine {
     uint64_t seed_;
     int64_t lo_, hi_, etot_, E_, R_, T_, TR_;
     bool mappo_ = false;   // agent-major rows R = n*E, critic on [joint obs | agent one-hot]
+    int nrep_ = 1;                          // replicas folded into this engine
+    std::vector<int64_t> rep_off_, rep_n_;  // replica env offset (relative to lo_) and size
+    void enq_permute_replicas();
     Numerics numerics_;
     cudaStream_t stream_ = nullptr, side_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_t0_ = nullptr, ev_t1_ = nullptr;

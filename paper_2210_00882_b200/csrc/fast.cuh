@@ -47,6 +47,11 @@ struct FastLearnArgs {
     int64_t save_tiles;
     int hload;
     uint8_t* hscratch;         // k_learn: per (CTA, group) hidden-activation scratch [grid*2][hbytes]
+    // R > 1 replicas folded into the unit: row -> replica via env (row % rep_E); per-replica row
+    // weight (1 / (R * T * E_r)) replaces inv_n and adv_stats is indexed [replica][2]
+    const int32_t* rep_of_env;
+    const float* rep_w;
+    int64_t rep_E;
     double inv_n, value_coef, entropy_coef;
     float clip_eps;
     float* partials;           // [grid, part_stride]
@@ -72,6 +77,8 @@ void fast_gae(cudaStream_t s, const float* rew, const float* values, const float
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
               double* block_sums, double* stats);
 void fast_sum(cudaStream_t s, const double* x, int64_t n, double* scratch, double* out);
+void fast_rep_adv_stats(cudaStream_t s, const float* adv, int64_t T, int64_t E, const int64_t* rep_off,
+                        const int64_t* rep_n, int R, double* stats);
 
 struct FastRolloutArgs {     // whole-episode rollout, all T steps in one launch
     const float* params;     // policy params (flat, reference layout)

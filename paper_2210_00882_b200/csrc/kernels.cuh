@@ -56,6 +56,7 @@ struct DwTile {           // one 32(t) x 32(j) block of dW_l = H_{l-1}^T dZ_l (+
     float* gW;            // [K, N] slice of the flat gradient
     float* gB;            // [N]
     int K, N, t0, j0;
+    int64_t rows;         // M: rows of this chain (one replica's T*E_r rows)
 };
 
 // ---------------------------------------------------------------- exact (FP64-accumulate) path
@@ -74,7 +75,17 @@ void exact_loss_rows(cudaStream_t s, int algo, const float* logits, const float*
                      const float* logp_old, const float* adv, const float* ret, int64_t n, int A, double clip_eps,
                      double value_coef, double entropy_coef, float* dlogits, float* dvalues, double* terms);
 void exact_loss_reduce(cudaStream_t s, const double* terms, int64_t n, double entropy_coef, float* loss);
-void exact_dw(cudaStream_t s, const DwTile* tiles, int ntiles, int64_t M);
+void exact_dw(cudaStream_t s, const DwTile* tiles, int ntiles);
+// R replicas per unit: t-major [T, E, w] trajectory rows -> replica-major [r][T][E_r][w] so that
+// every replica's rows (its own unit's BufferSample, interp.cpp:297-301) are contiguous.
+struct ReplicaMap {
+    const int32_t* rep_of_env;  // [E]
+    const int64_t* rep_off;     // [R] first env of replica r (relative to the unit)
+    const int64_t* rep_n;       // [R] envs of replica r
+};
+void permute_rows_f32(cudaStream_t s, const float* src, float* dst, int64_t T, int64_t E, int w, const ReplicaMap& m);
+void permute_rows_i32(cudaStream_t s, const int32_t* src, int32_t* dst, int64_t T, int64_t E, const ReplicaMap& m);
+void permute_rows_f64(cudaStream_t s, const double* src, double* dst, int64_t T, int64_t E, const ReplicaMap& m);
 void exact_grad_mean(cudaStream_t s, const float* gathered, int k, int64_t P, double* mean);
 void begin_episode(cudaStream_t s, DeviceCtx* ctx);  // ctx->episode = ctx->next_episode++
 void adam_tick(cudaStream_t s, DeviceCtx* ctx, const double2* bc_table, int64_t table_len);

@@ -358,11 +358,12 @@ __global__ void k_loss_reduce(const double* __restrict__ terms, int64_t n, doubl
 constexpr int kDwRows = 128;
 constexpr int kDwPer = kDwRows / 8;  // rows per thread per chunk (8 warps)
 
-__global__ void __launch_bounds__(256) k_dw(const DwTile* __restrict__ tiles, int64_t M) {
+__global__ void __launch_bounds__(256) k_dw(const DwTile* __restrict__ tiles) {
     extern __shared__ double dw_smem[];
     double(*Hs)[kDwRows][33] = reinterpret_cast<double(*)[kDwRows][33]>(dw_smem);
     double(*Ds)[kDwRows][33] = reinterpret_cast<double(*)[kDwRows][33]>(dw_smem + 2 * kDwRows * 33);
     const DwTile tl = tiles[blockIdx.x];
+    const int64_t M = tl.rows;
     const int tx = threadIdx.x & 31, tg = threadIdx.x >> 5;
     const int K = tl.K, N = tl.N;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -514,11 +515,37 @@ void exact_loss_reduce(cudaStream_t s, const double* terms, int64_t n, double en
     k_loss_reduce<<<1, 1, 0, s>>>(terms, n, entropy_coef, loss);
 }
 
-void exact_dw(cudaStream_t s, const DwTile* tiles, int ntiles, int64_t M) {
+template <typename V>
+__global__ void k_permute_rows(const V* __restrict__ src, V* __restrict__ dst, int64_t T, int64_t E, int w,
+                               ReplicaMap m) {
+    const int64_t n = T * E * w;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t c = i % w, row = i / w, t = row / E, e = row % E;
+        const int r = m.rep_of_env[e];
+        const int64_t off = m.rep_off[r], er = m.rep_n[r];
+        dst[((T * off + t * er) + (e - off)) * w + c] = src[i];
+    }
+}
+
+void permute_rows_f32(cudaStream_t s, const float* src, float* dst, int64_t T, int64_t E, int w, const ReplicaMap& m) {
+    k_permute_rows<float><<<static_cast<unsigned>(std::min<int64_t>(4096, blocks_for(T * E * w, 256))), 256, 0, s>>>(
+        src, dst, T, E, w, m);
+}
+void permute_rows_i32(cudaStream_t s, const int32_t* src, int32_t* dst, int64_t T, int64_t E, const ReplicaMap& m) {
+    k_permute_rows<int32_t><<<static_cast<unsigned>(std::min<int64_t>(4096, blocks_for(T * E, 256))), 256, 0, s>>>(
+        src, dst, T, E, 1, m);
+}
+void permute_rows_f64(cudaStream_t s, const double* src, double* dst, int64_t T, int64_t E, const ReplicaMap& m) {
+    k_permute_rows<double><<<static_cast<unsigned>(std::min<int64_t>(4096, blocks_for(T * E, 256))), 256, 0, s>>>(
+        src, dst, T, E, 1, m);
+}
+
+void exact_dw(cudaStream_t s, const DwTile* tiles, int ntiles) {
     const size_t smem = 4 * kDwRows * 33 * sizeof(double);
     // per-device attribute: set on every launch (cheap, and legal inside stream capture)
     FLW_CUDA(cudaFuncSetAttribute(k_dw, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    if (ntiles > 0) k_dw<<<ntiles, 256, smem, s>>>(tiles, M);
+    if (ntiles > 0) k_dw<<<ntiles, 256, smem, s>>>(tiles);
 }
 
 void exact_grad_mean(cudaStream_t s, const float* gathered, int k, int64_t P, double* mean) {

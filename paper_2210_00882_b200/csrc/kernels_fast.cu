@@ -550,6 +550,38 @@ __global__ void __launch_bounds__(256) k_adv_stats(const double* __restrict__ bl
     }
 }
 
+// Per-replica advantage statistics (R units folded into one engine, each normalising over its
+// own T*E_r rows like its own interpreter, rl.cpp:97-107): one CTA per replica, fixed order.
+__global__ void __launch_bounds__(256) k_rep_adv_stats(const float* __restrict__ adv, int64_t T, int64_t E,
+                                                       const int64_t* __restrict__ rep_off,
+                                                       const int64_t* __restrict__ rep_n, double* stats) {
+    __shared__ double s1[256], s2[256];
+    const int r = blockIdx.x;
+    const int64_t off = rep_off[r], er = rep_n[r], n = T * er;
+    double a1 = 0.0, a2 = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += 256) {
+        const double x = adv[(i / er) * E + off + i % er];
+        a1 += x;
+        a2 += x * x;
+    }
+    s1[threadIdx.x] = a1;
+    s2[threadIdx.x] = a2;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            s1[threadIdx.x] += s1[threadIdx.x + o];
+            s2[threadIdx.x] += s2[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double mean = s1[0] / static_cast<double>(n);
+        const double var = s2[0] / static_cast<double>(n) - mean * mean;
+        stats[2 * r] = mean;
+        stats[2 * r + 1] = sqrt(var > 0.0 ? var : 0.0);
+    }
+}
+
 // Parallel episode reward sum (fast numerics): block tree sums in double, fixed block order.
 __global__ void __launch_bounds__(256) k_block_sum(const double* __restrict__ x, int64_t n, double* block_out) {
     __shared__ double s[256];
@@ -610,6 +642,11 @@ void fast_gae(cudaStream_t s, const float* rew, const float* values, const float
     k_fast_gae<<<nb, 256, 0, s>>>(rew, values, done_f, last_value, TR / R, R, gamma, lam, adv, ret, with_adv,
                                   block_sums);
     if (with_adv) k_adv_stats<<<1, 256, 0, s>>>(block_sums, nb, TR, stats);
+}
+
+void fast_rep_adv_stats(cudaStream_t s, const float* adv, int64_t T, int64_t E, const int64_t* rep_off,
+                        const int64_t* rep_n, int R, double* stats) {
+    k_rep_adv_stats<<<R, 256, 0, s>>>(adv, T, E, rep_off, rep_n, stats);
 }
 
 void fast_sum(cudaStream_t s, const double* x, int64_t n, double* scratch, double* out) {

@@ -479,10 +479,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) dz[j] = 0.0f;
                 if (valid) {
+                    float inv_n = static_cast<float>(a.inv_n);
+                    const double* ast = a.adv_stats;
+                    if (a.rep_of_env) {  // folded replicas: this row's unit weight and statistics
+                        const int rr = a.rep_of_env[row % a.rep_E];
+                        inv_n = a.rep_w[rr];
+                        if (ast) ast += 2 * rr;
+                    }
                     if (a.kind == kNetCritic) {  // value MSE: dV = 2 c_v (V - R) / N
                         const float verr = out[0] - ret_r;
-                        dz[0] = static_cast<float>(2.0 * a.value_coef * a.inv_n) * verr;
-                        vl_acc += static_cast<float>(a.value_coef * a.inv_n) * verr * verr;
+                        dz[0] = static_cast<float>(2.0 * a.value_coef) * inv_n * verr;
+                        vl_acc += static_cast<float>(a.value_coef) * inv_n * verr * verr;
                     } else {  // policy: clipped surrogate (PPO) or A3C policy gradient, + entropy bonus
                         const int A = n.rout[L - 1];
                         float mx = out[0];
@@ -497,7 +504,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                             p[j] = j < A ? __expf(lp[j]) : 0.0f;
                             if (j < A) H -= p[j] * lp[j];
                         }
-                        const float inv_n = static_cast<float>(a.inv_n);
                         float lpa = 0.0f;
 #pragma unroll
                         for (int j = 0; j < 16; ++j)
@@ -505,9 +511,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                         float coef;
                         if (a.kind == kNetPolicyPpo) {
                             float adv = adv_r;
-                            if (a.adv_stats) {
-                                const double sd = a.adv_stats[1];
-                                if (!(sd < 1e-8)) adv = static_cast<float>((adv - a.adv_stats[0]) / (sd + 1e-8));
+                            if (ast) {
+                                const double sd = ast[1];
+                                if (!(sd < 1e-8)) adv = static_cast<float>((adv - ast[0]) / (sd + 1e-8));
                             }
                             const float ratio = __expf(lpa - lpo_r);
                             const float clipped = fminf(fmaxf(ratio, 1.0f - a.clip_eps), 1.0f + a.clip_eps);

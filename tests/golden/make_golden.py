@@ -52,6 +52,13 @@ RUN_CASES = {
                          "policy_net": {"hidden": [8, 8]}, "loop": {"episodes": 3, "steps_per_episode": 8}}, 4, 3),
     "dpd_a3c_k4": ({"algorithm": "a3c", "actor": {"num": 4}, "env": {"type": "gridline", "num": 4},
                     "policy_net": {"hidden": [8, 8]}, "loop": {"episodes": 3, "steps_per_episode": 8}}, 2, 4),
+    # BASELINE configs[4] (C5) shape: A3C, 24 actors = 24 gridline envs, T=32 (small net)
+    "dpd_a3c_k24": ({"algorithm": "a3c", "actor": {"num": 24}, "env": {"type": "gridline", "num": 24},
+                     "policy_net": {"hidden": [16, 16]}, "loop": {"episodes": 3, "steps_per_episode": 32}}, 5, 24),
+    # uneven replicas (20 envs over 6: 4,4,3,3,3,3) with per-replica advantage normalisation
+    "dpd_k6_synth_uneven": ({"algorithm": "ppo", "actor": {"num": 6}, "env": {"type": "synth17x6", "num": 20},
+                             "policy_net": {"hidden": [16, 16]}, "loop": {"episodes": 3, "steps_per_episode": 8}},
+                            11, 6),
 }
 
 
@@ -86,19 +93,23 @@ def build_ref():
 
 
 def main():
+    only = set(sys.argv[1:])
     build_ref()
     with tempfile.TemporaryDirectory() as tmp:
         plans = []
-        for i, (algo, deploy) in enumerate(PLAN_CASES):
+        for i, (algo, deploy) in enumerate(PLAN_CASES if not only else []):
             ap, dp = os.path.join(tmp, f"pa{i}.json"), os.path.join(tmp, f"pd{i}.json")
             json.dump(algo, open(ap, "w"))
             json.dump(deploy, open(dp, "w"))
             out = subprocess.run([pyoracle.REF_TOOL, "plan", ap, dp], check=True, capture_output=True,
                                  text=True).stdout
             plans.append({"algo": algo, "deploy": deploy, **json.loads(out)})
-        json.dump(plans, open(os.path.join(HERE, "plans.json"), "w"), indent=1)
+        if not only:
+            json.dump(plans, open(os.path.join(HERE, "plans.json"), "w"), indent=1)
         print("plans", len(plans))
         for name, (algo, seed) in TRACE_CASES.items():
+            if only and name not in only:
+                continue
             ap = os.path.join(tmp, name + ".json")
             json.dump(algo, open(ap, "w"))
             prefix = os.path.join(tmp, name)
@@ -109,12 +120,15 @@ def main():
                                 **{k.replace("/", "__"): v for k, v in tr.items()})
             print("trace", name, len(tr), "tensors")
         for name, (algo, seed, k) in RUN_CASES.items():
+            if only and name not in only:
+                continue
             algo = dict(algo)
             algo["actor"] = {"num": k}
             ap = os.path.join(tmp, name + ".json")
             dp = os.path.join(tmp, name + "_deploy.json")
             json.dump(algo, open(ap, "w"))
-            json.dump({"workers": ["local"], "slots_per_worker": {"cpu": 16, "accel": 16},
+            slots = max(16, k)
+            json.dump({"workers": ["local"], "slots_per_worker": {"cpu": slots, "accel": slots},
                        "distribution_policy": "dp-d"}, open(dp, "w"))
             out = subprocess.run([pyoracle.REF_TOOL, "run", ap, dp, str(seed), "--params"], check=True,
                                  capture_output=True, text=True).stdout

@@ -54,6 +54,7 @@ struct Engine::Bufs {
     float *values = nullptr, *last_value = nullptr;
     // MAPPO: joint observation blocks [(T+1), E, W] and critic input rows [(T+1), n*E, W+n]
     float *joint = nullptr, *cin = nullptr;
+    double* cprefix = nullptr;  // MAPPO compact critic: joint prefix chains [(T+1)*E, H0]
     // fast numerics
     FastNet pol{}, crit{};
     int grid = 0;                       // persistent CTAs of the fused learn kernel
@@ -231,7 +232,9 @@ void Engine::alloc() {
     b.rew_d = b.alloc<double>(T_ * E_);
     if (mappo_) {  // joint obs per env and the critic rows [joint | one-hot] per (agent, env)
         b.joint = b.alloc<float>((T_ + 1) * E_ * s.state_w);
-        b.cin = b.alloc<float>((T_ + 1) * R_ * s.crit_in);
+        // compact critic: [joint | one-hot] rows are never materialised (n x smaller; n=64,
+        // E=2048 would need 145 GB), layer 0 reads the joint prefix chains + W[J+a]
+        b.cprefix = b.alloc<double>((T_ + 1) * E_ * s.cdims[1]);
     }
     b.adv = b.alloc<float>(TR_);
     b.ret = b.alloc<float>(TR_);
@@ -332,7 +335,13 @@ void Engine::alloc() {
                 for (int t0 = 0; t0 <= K; t0 += 32)
                     for (int j0 = 0; j0 < N; j0 += 32) {
                         DwTile t{};
-                        t.H = (l == 0 ? ((net == 1 && mappo_) ? b.cin : X0) : H[l - 1]) + row0 * K;
+                        t.H = (l == 0 ? X0 : H[l - 1]) + row0 * K;
+                        if (l == 0 && net == 1 && mappo_) {  // compact [joint | one-hot] by index
+                            t.H = b.joint;
+                            t.cn = s.n_agents;
+                            t.cE = E_;
+                            t.cJ = s.state_w;
+                        }
                         t.DZ = DZ[l] + row0 * N;
                         t.gW = g + s.woff[net][l];
                         t.gB = g + s.boff[net][l];
@@ -453,11 +462,11 @@ void Engine::enq_reset() {
                     shape_.obs_dim, seed_);
 }
 
-void Engine::enq_mlp_forward(int net, const float* X, int64_t M, float* const* H) {
+void Engine::enq_mlp_forward(int net, const float* X, int64_t M, float* const* H, int first_layer) {
     const ProgramShape& s = shape_;
     const auto& d = net == 0 ? s.pdims : s.cdims;
-    const float* in = X;
-    for (int l = 0; l < s.L; ++l) {
+    const float* in = first_layer > 0 ? H[first_layer - 1] : X;
+    for (int l = first_layer; l < s.L; ++l) {
         exact_layer_fwd(stream_, in, b_->params + s.woff[net][l], b_->params + s.boff[net][l], H[l], M, d[l], d[l + 1],
                         l + 1 < s.L ? act_of(cfg_) : kNone);
         in = H[l];
@@ -666,15 +675,23 @@ void Engine::enq_learn_grads() {
     const float* X = rep ? b.pstates : b.states;  // [T*R, S] t-major policy rows
     // critic rows: the states themselves (PPO/A3C) or [joint | one-hot] (MAPPO); block T holds
     // the last step's next rows (last_next / last nci, programs.cpp:240-245, 422-427)
-    const float* Xc = mappo_ ? b.cin : X;
-    const float* last_next = (mappo_ ? b.cin : b.states) + T_ * R_ * s.crit_in;
+    const float* Xc = X;
+    const float* last_next = b.states + T_ * R_ * s.crit_in;
     const float* rew = rep ? b.prew : b.rew;
     const float* done_f = rep ? b.pdone : b.done_f;
     const int32_t* actions = rep ? b.pact : b.actions;
     const float* logp = rep ? b.plogp : b.logp;
     (void)S;
-    enq_mlp_forward(1, Xc, TR_, b.Hc.data());         // values = critic(states | ci)
-    enq_mlp_forward(1, last_next, R_, b.Hl.data());   // last_value = critic(last_next | last nci)
+    if (mappo_) {  // compact critic layer 0 over all T+1 blocks, then layers 1.. per row
+        exact_mappo_critic0(stream_, b.joint, b.params + s.woff[1][0], b.params + s.boff[1][0], T_ + 1, E_,
+                            s.n_agents, s.state_w, s.cdims[1], b.cprefix, b.Hc[0], b.Hl[0],
+                            L > 1 ? act_of(cfg_) : kNone);
+        enq_mlp_forward(1, nullptr, TR_, b.Hc.data(), 1);
+        enq_mlp_forward(1, nullptr, R_, b.Hl.data(), 1);
+    } else {
+        enq_mlp_forward(1, Xc, TR_, b.Hc.data());         // values = critic(states | ci)
+        enq_mlp_forward(1, last_next, R_, b.Hl.data());   // last_value = critic(last_next | last nci)
+    }
     const bool ppo = s.algo != Algo::A3c;
     enq_mlp_forward(0, X, TR_, b.Hp.data());          // logits_new = policy(states)
     // Per replica (= per reference unit): GAE over its E_r streams, advantage normalisation
@@ -1043,7 +1060,17 @@ void Engine::read_tensor(const std::string& n, double* out) {
         }
         if (n == "sample") {  // rows_state | action | reward | ci | nci | done | logp (programs.cpp:410-411)
             auto st = d2h(b.states, TR_ * S);
-            auto ci = d2h(b.cin, (T_ + 1) * R_ * C);
+            // critic input rows [joint(t,e) | onehot(a)] rebuilt from the compact joint blocks
+            const int64_t Wj = C - shape_.n_agents;
+            auto jt = d2h(b.joint, (T_ + 1) * E_ * Wj);
+            std::vector<double> ci(static_cast<size_t>((T_ + 1) * R_ * C), 0.0);
+            for (int64_t blk = 0; blk <= T_; ++blk)
+                for (int64_t a = 0; a < shape_.n_agents; ++a)
+                    for (int64_t e = 0; e < E_; ++e) {
+                        double* crow = ci.data() + ((blk * R_) + a * E_ + e) * C;
+                        for (int64_t j = 0; j < Wj; ++j) crow[j] = jt[static_cast<size_t>((blk * E_ + e) * Wj + j)];
+                        crow[Wj + a] = 1.0;
+                    }
             auto act = d2h(b.actions, TR_);
             auto rw = d2h(b.rew, TR_);
             auto dn = d2h(b.done_f, TR_);

@@ -108,7 +108,7 @@ class Engine {
     void enq_learn_grads();
     void enq_grad_sync_and_adam();
     void enq_reward_sum();
-    void enq_mlp_forward(int net, const float* X, int64_t M, float* const* H);
+    void enq_mlp_forward(int net, const float* X, int64_t M, float* const* H, int first_layer = 0);
     void build_graph();
 
     AlgoConfig cfg_;

@@ -57,6 +57,10 @@ struct DwTile {           // one 32(t) x 32(j) block of dW_l = H_{l-1}^T dZ_l (+
     float* gB;            // [N]
     int K, N, t0, j0;
     int64_t rows;         // M: rows of this chain (one replica's T*E_r rows)
+    // MAPPO compact critic layer 0 (cn > 0): the input row (t, a*E+e) is [joint(t,e) | onehot(a)],
+    // read from H = joint [(T+1)*E, cJ] by index - same values, same row order as the reference
+    int cn = 0, cJ = 0;
+    int64_t cE = 0;
 };
 
 // ---------------------------------------------------------------- exact (FP64-accumulate) path
@@ -76,6 +80,12 @@ void exact_loss_rows(cudaStream_t s, int algo, const float* logits, const float*
                      double value_coef, double entropy_coef, float* dlogits, float* dvalues, double* terms);
 void exact_loss_reduce(cudaStream_t s, const double* terms, int64_t n, double entropy_coef, float* loss);
 void exact_dw(cudaStream_t s, const DwTile* tiles, int ntiles);
+// MAPPO critic layer 0 without materialising [joint | one-hot] (programs.cpp:390-402): the
+// reference's left-to-right dot over the row is the joint prefix chain (identical for the n
+// agents of an env) followed by +1*W[J+a] (the one-hot zeros add exact zeros). prefix[blk*E+e]
+// is that chain in double; rows (blk, a, e) then get f32(f32(prefix + W[J+a]) + b) and act.
+void exact_mappo_critic0(cudaStream_t s, const float* joint, const float* W0, const float* b0, int64_t blocks,
+                         int64_t E, int n, int J, int N, double* prefix, float* out_rows, float* out_last, int act);
 // R replicas per unit: t-major [T, E, w] trajectory rows -> replica-major [r][T][E_r][w] so that
 // every replica's rows (its own unit's BufferSample, interp.cpp:297-301) are contiguous.
 struct ReplicaMap {

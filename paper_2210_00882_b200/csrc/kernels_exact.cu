@@ -374,7 +374,13 @@ __global__ void __launch_bounds__(256) k_dw(const DwTile* __restrict__ tiles) {
             int rr = tg + 8 * q;
             int64_t row = i0 + rr;
             int t = tl.t0 + tx, j = tl.j0 + tx;
-            hreg[q] = row < M ? (t < K ? tl.H[row * K + t] : (t == K ? 1.0f : 0.0f)) : 0.0f;
+            if (tl.cn > 0 && row < M && t < K) {  // compact MAPPO critic input [joint | one-hot]
+                const int64_t per = static_cast<int64_t>(tl.cn) * tl.cE;
+                const int64_t tb = row / per, rem = row % per, a = rem / tl.cE, e = rem % tl.cE;
+                hreg[q] = t < tl.cJ ? tl.H[(tb * tl.cE + e) * tl.cJ + t] : (t - tl.cJ == a ? 1.0f : 0.0f);
+            } else {
+                hreg[q] = row < M ? (t < K ? tl.H[row * K + t] : (t == K ? 1.0f : 0.0f)) : 0.0f;
+            }
             dreg[q] = (row < M && j < N) ? tl.DZ[row * N + j] : 0.0f;
         }
     };
@@ -539,6 +545,79 @@ void permute_rows_i32(cudaStream_t s, const int32_t* src, int32_t* dst, int64_t 
 void permute_rows_f64(cudaStream_t s, const double* src, double* dst, int64_t T, int64_t E, const ReplicaMap& m) {
     k_permute_rows<double><<<static_cast<unsigned>(std::min<int64_t>(4096, blocks_for(T * E, 256))), 256, 0, s>>>(
         src, dst, T, E, 1, m);
+}
+
+// joint prefix chains: prefix[r][c] = sum_i joint[r][i] * W0[i][c], i ascending from 0.0 (the
+// first J terms of the reference's dot over [joint | one-hot]), kept in double.
+__global__ void __launch_bounds__(256) k_mappo_prefix(const float* __restrict__ in, const float* __restrict__ W,
+                                                      double* __restrict__ out, int64_t M, int K, int N) {
+    __shared__ double As[32][33];
+    __shared__ double Bs[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int c0 = blockIdx.y * 32;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < K; k0 += 32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            int rr = ty + 8 * q;
+            int64_t row = r0 + rr;
+            int kk = k0 + tx;
+            As[rr][tx] = (row < M && kk < K) ? static_cast<double>(in[row * K + kk]) : 0.0;
+            int kr = ty + 8 * q;
+            int kg = k0 + kr, cc = c0 + tx;
+            Bs[kr][tx] = (kg < K && cc < N) ? static_cast<double>(W[static_cast<int64_t>(kg) * N + cc]) : 0.0;
+        }
+        __syncthreads();
+        const int kmax = min(32, K - k0);
+        for (int k = 0; k < kmax; ++k) {
+            double bv = Bs[k][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][k], bv, acc[q]);
+        }
+        __syncthreads();
+    }
+    const int col = c0 + tx;
+    if (col >= N) return;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        int64_t row = r0 + ty + 8 * q;
+        if (row < M) out[row * N + col] = acc[q];
+    }
+}
+
+template <int ACT>
+__global__ void k_mappo_expand0(const double* __restrict__ prefix, const float* __restrict__ W, const float* __restrict__ b,
+                                int64_t blocks, int64_t E, int n, int J, int N, float* out_rows, float* out_last) {
+    const int64_t total = blocks * n * E * N;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % N);
+        const int64_t row = i / N;  // (blk, a, e) agent-major inside a block
+        const int64_t blk = row / (n * E), rem = row % (n * E), a = rem / E, e = rem % E;
+        const double acc = __dadd_rn(prefix[(blk * E + e) * N + c], static_cast<double>(W[(J + a) * N + c]));
+        double z = f32r(acc);
+        double za = f32r(__dadd_rn(z, static_cast<double>(b[c])));
+        double h = za;
+        if (ACT == kTanh) h = f32r(tanh(za));
+        if (ACT == kRelu) h = za > 0 ? za : 0.0;
+        float* dst = blk + 1 < blocks ? out_rows + row * N : out_last + rem * N;
+        dst[c] = static_cast<float>(h);
+    }
+}
+
+void exact_mappo_critic0(cudaStream_t s, const float* joint, const float* W0, const float* b0, int64_t blocks,
+                         int64_t E, int n, int J, int N, double* prefix, float* out_rows, float* out_last, int act) {
+    const int64_t M = blocks * E;
+    dim3 g(static_cast<unsigned>((M + 31) / 32), static_cast<unsigned>((N + 31) / 32));
+    k_mappo_prefix<<<g, 256, 0, s>>>(joint, W0, prefix, M, J, N);
+    const unsigned nb = static_cast<unsigned>(std::min<int64_t>(8192, blocks_for(blocks * n * E * N, 256)));
+    if (act == kTanh)
+        k_mappo_expand0<kTanh><<<nb, 256, 0, s>>>(prefix, W0, b0, blocks, E, n, J, N, out_rows, out_last);
+    else if (act == kRelu)
+        k_mappo_expand0<kRelu><<<nb, 256, 0, s>>>(prefix, W0, b0, blocks, E, n, J, N, out_rows, out_last);
+    else
+        k_mappo_expand0<kNone><<<nb, 256, 0, s>>>(prefix, W0, b0, blocks, E, n, J, N, out_rows, out_last);
 }
 
 void exact_dw(cudaStream_t s, const DwTile* tiles, int ntiles) {

@@ -6,7 +6,8 @@
 // C = W + n critic input width):
 //   joint[t][e][W]            the env observation (state_in of the reference)
 //   prows[t][a*E+e][S]        policy input rows (the per-agent Slice + Concat, programs.cpp:100-109)
-//   cin[t][a*E+e][C]          critic input rows [joint(t,e) | onehot(a)] (programs.cpp:390-402)
+//   cin[t][a*E+e][C]          critic input rows [joint(t,e) | onehot(a)] (programs.cpp:390-402);
+//                             optional: the engine's compact critic reads joint + the agent id instead
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -38,6 +39,7 @@ __device__ void spread_emit(const double* est, int64_t E, int64_t e, int n, floa
             jrow[a * S + 3 + 2 * l] = pr[3 + 2 * l] = dy;
         }
     }
+    if (!cin) return;  // compact critic (the engine default): [joint | one-hot] is never materialised
     for (int a = 0; a < n; ++a) {
         float* crow = cin + (blk * R + static_cast<int64_t>(a) * E + e) * C;
         for (int j = 0; j < W; ++j) crow[j] = jrow[j];

@@ -428,14 +428,25 @@ __global__ void __launch_bounds__(256) k_build_wimg(const float* __restrict__ pa
 // critic's partials following the policy's in the flat gradient.
 __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict__ pp, const float* __restrict__ pc,
                                                          int nparts, int64_t Pp, int64_t Pc, float* grads) {
-    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= Pp + Pc) return;
-    const float* src = i < Pp ? pp + i : pc + (i - Pp);
+    // 32 parameters per block (lane = parameter, coalesced rows); warp w sums partials
+    // w, w+8, ... in order, then the 8 warp sums are added in warp order: a fixed tree.
+    __shared__ float ws[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * 32LL + lane;
+    const bool ok = i < Pp + Pc;
+    const float* src = !ok ? pp : (i < Pp ? pp + i : pc + (i - Pp));
     const int64_t stride = i < Pp ? Pp : Pc;
     float s = 0.0f;
-#pragma unroll 8
-    for (int p = 0; p < nparts; ++p) s += src[p * stride];
-    grads[i] = s;
+    if (ok)
+        for (int p = w; p < nparts; p += 8) s += src[p * stride];
+    ws[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && ok) {
+        float t = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += ws[k][lane];
+        grads[i] = t;
+    }
 }
 
 __global__ void k_reduce_loss(const float* __restrict__ lp, int nparts, int nsets, double ec, float* loss) {
@@ -614,7 +625,7 @@ size_t fast_hsave_bytes(const FastNet& n) {
 }
 
 void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv_bfloat16* img) {
-    k_build_wimg<<<16, 256, 0, s>>>(params, n, img);
+    k_build_wimg<<<148, 256, 0, s>>>(params, n, img);
 }
 
 void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid) {
@@ -626,8 +637,8 @@ void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid) {
 
 void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int nparts, int64_t Pp, int64_t Pc,
                           float* grads) {
-    k_reduce_partials<<<static_cast<unsigned>((Pp + Pc + 255) / 256), 256, 0, s>>>(part_p, part_c, nparts, Pp, Pc,
-                                                                                   grads);
+    k_reduce_partials<<<static_cast<unsigned>((Pp + Pc + 31) / 32), 256, 0, s>>>(part_p, part_c, nparts, Pp, Pc,
+                                                                                 grads);
 }
 
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int nparts, int nsets, double entropy_coef,

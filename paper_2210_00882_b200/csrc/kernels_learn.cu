@@ -322,10 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             }
         };
         auto signal = [&]() {  // operand tile stored: hand it to the producer
-            // generic-proxy writes (shared operand tiles, global activation images) -> visible to
-            // the tensor core and to the producer's later TMA bulk loads
+            // generic-proxy shared-memory writes (operand tiles) -> visible to the tensor core
             umma::fence_async_smem();
-            asm volatile("fence.proxy.async.global;\n" ::: "memory");
             umma::fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(&epi_done[g]);
@@ -543,6 +541,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                         umma::st_row8(dst, wo, r, c0, dz + c0);
                     }
                 }
+                // the tile's global activation images (written during the forward) -> visible to
+                // the producer's TMA bulk loads of the backward, which all follow this arrival
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");
                 signal();  // dZ_{L-1} ready
                 colsum32(dz, 0, wo, L - 1);
             }

@@ -19,8 +19,14 @@ namespace flw {
 
 namespace {
 
-constexpr int kEnvsPerCta = 32;
-constexpr int kGroups = 8;                         // thread groups of 16 (output quads)
+#ifndef FLW_ROLLOUT_EPC
+#define FLW_ROLLOUT_EPC 32
+#endif
+constexpr int kEnvsPerCta = FLW_ROLLOUT_EPC;  // envs per CTA (A/B: -DFLW_ROLLOUT_EPC=16)
+#ifndef FLW_ROLLOUT_GROUPS
+#define FLW_ROLLOUT_GROUPS 8
+#endif
+constexpr int kGroups = FLW_ROLLOUT_GROUPS;        // thread groups of 16 (output quads)
 constexpr int kNE = kEnvsPerCta / kGroups;         // envs per group: 4
 constexpr int kThreads = kGroups * 16;             // 128
 constexpr int kHStride = 68;   // activation row stride (floats): 16B aligned, spreads banks
@@ -28,17 +34,7 @@ constexpr int kHStride = 68;   // activation row stride (floats): 16B aligned, s
 __host__ __device__ inline int pad4(int x) { return (x + 3) & ~3; }
 
 struct RolloutSmem {
-    uint32_t w[kMaxLayers], b[kMaxLayers], h[2], env, total;
-};
-
-// per-step env scratch shared by the 4 warps (PolicyApply exps, synth17x6 state / new state /
-// squared terms, chosen action and done flag per env)
-struct EnvScratch {
-    double pexp[kEnvsPerCta][16];
-    double st[2][kEnvsPerCta][kSynthObs];
-    double sq[kEnvsPerCta][kSynthObs];
-    int32_t chosen[kEnvsPerCta];
-    int32_t done[kEnvsPerCta];
+    uint32_t w[kMaxLayers], b[kMaxLayers], h[2], total;
 };
 
 // W_l stored [pad4(in) x pad4(out)] row-major (zero padded) so the input loop runs in float4 steps.
@@ -55,13 +51,20 @@ __host__ __device__ inline RolloutSmem rollout_carve(const FastRolloutArgs& a) {
     off += kEnvsPerCta * kHStride * 4;
     s.h[1] = off;
     off += kEnvsPerCta * kHStride * 4;
-    s.env = (off + 15) & ~15u;
-    off = s.env + static_cast<uint32_t>(sizeof(EnvScratch));
     s.total = off;
     return s;
 }
 
 __device__ __forceinline__ double dmaxd(double a, double b) { return a < b ? b : a; }
+
+// MUFU tanh (max rel. error ~2^-11): the hidden activations of the fast rollout. The sampled
+// actions stay those of the exact path except within ~1e-4 of a cumulative-probability boundary
+// (tests/test_fast_gpu.py bounds the flip rate).
+__device__ __forceinline__ float tanh_mufu(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 template <int ENV>
 __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* __restrict__ ctx, FastRolloutArgs a) {
@@ -98,11 +101,6 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     if (live) {
 #pragma unroll
         for (int j = 0; j < SW; ++j) st[j] = a.est[j * E + e];
-        if (ENV == 1) {
-            EnvScratch& X = *reinterpret_cast<EnvScratch*>(smem + S.env);
-#pragma unroll
-            for (int j = 0; j < SW; ++j) X.st[0][t][j] = st[j];
-        }
         done = a.done[e] != 0;
         stepc = a.stepc[e];
         for (int j = 0; j < S_; ++j) h0[t * kHStride + j] = a.states[(a.step0 * E + e) * S_ + j];
@@ -158,7 +156,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                     float v[4] = {lo[k].x + bias.x, lo[k].y + bias.y, hi[k].x + bias.z, hi[k].y + bias.w};
                     if (!last) {
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) v[j] = a.act == 0 ? tanhf(v[j]) : fmaxf(v[j], 0.0f);
+                        for (int j = 0; j < 4; ++j) v[j] = a.act == 0 ? tanh_mufu(v[j]) : fmaxf(v[j], 0.0f);
                     }
                     *reinterpret_cast<float4*>(obase + (g + kGroups * k) * kHStride + o0) =
                         make_float4(v[0], v[1], v[2], v[3]);
@@ -170,93 +168,8 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
 #ifdef FLW_LEARN_TRACE
         if (step - a.step0 < 8) tr1[step - a.step0] = clock64();
 #endif
-        // ---- PolicyApply + EnvStep
-        if (ENV == 1) {
-            // synth17x6: the per-env work is spread over all 4 warps (lane = env, warp = action /
-            // state-dimension slice); every sum keeps the reference order on one thread.
-            EnvScratch& X = *reinterpret_cast<EnvScratch*>(smem + S.env);
-            const int le = t & 31, wv = t >> 5;
-            const float* lg = reinterpret_cast<const float*>(smem + S.h[cur]) + le * kHStride;
-            {
-                double mx = lg[0];
-                for (int c = 1; c < A; ++c) mx = dmaxd(mx, static_cast<double>(lg[c]));
-                for (int c = wv; c < A; c += 4) X.pexp[le][c] = exp(__dsub_rn(static_cast<double>(lg[c]), mx));
-            }
-            __syncthreads();
-            if (owner) {
-                double p[16], den = 0.0;
-                for (int c = 0; c < A; ++c) den = __dadd_rn(den, X.pexp[t][c]);
-                for (int c = 0; c < A; ++c) p[c] = f32r(__ddiv_rn(X.pexp[t][c], den));
-                const double u = rng_uniform(rng_key(a.seed, kActionStream, ep, static_cast<uint64_t>(step),
-                                                     static_cast<uint64_t>(a.env_lo + e)));
-                double cum = 0.0;
-                int chosen = A - 1;
-                for (int c = 0; c < A; ++c) {
-                    cum = __dadd_rn(cum, p[c]);
-                    if (u < cum) {
-                        chosen = c;
-                        break;
-                    }
-                }
-                X.chosen[t] = chosen;
-                X.done[t] = done ? 1 : 0;
-                if (live) a.logp[step * E + e] = static_cast<float>(log(dmaxd(p[chosen], 1e-30)));
-            }
-            __syncthreads();
-            {  // dynamics, dims i = wv, wv+4, ... (synth17x6, oracle/refx/env_ext.cpp)
-                const int cb = static_cast<int>(step - a.step0) & 1;
-                const double* old = X.st[cb][le];
-                double* nw = X.st[cb ^ 1][le];
-                const double* tb = a.env.synth_b + X.chosen[le] * kSynthObs;
-                const bool dn = X.done[le] != 0;
-                for (int i = wv; i < kSynthObs; i += 4) {
-                    double v = old[i];
-                    if (!dn) {
-                        const double t4 = __dadd_rn(
-                            __dsub_rn(__dmul_rn(0.3, old[(i + 1) % kSynthObs]), __dmul_rn(0.5, old[i])), tb[i]);
-                        v = __dadd_rn(old[i], __dmul_rn(0.05, t4));
-                    }
-                    nw[i] = v;
-                    X.sq[le][i] = __dmul_rn(v, v);
-                }
-            }
-            __syncthreads();
-            if (owner) {
-                const int nb = (static_cast<int>(step - a.step0) & 1) ^ 1;
-                const double* nst = X.st[nb][t];
-                float* h0w = reinterpret_cast<float*>(smem + S.h[0]) + t * kHStride;  // next layer-0 input
-                double rew = 0.0;
-                bool d = done;
-                if (!done) {
-                    double sq = 0.0, m = 0.0;
-                    for (int i = 0; i < kSynthObs; ++i) {
-                        sq = __dadd_rn(sq, X.sq[t][i]);
-                        const double av = nst[i] < 0.0 ? -nst[i] : nst[i];
-                        m = av > m ? av : m;
-                    }
-                    rew = __dsub_rn(1.0, __ddiv_rn(sq, static_cast<double>(kSynthObs)));
-                    d = m > 2.0;
-                    if (a.env.max_steps > 0 && stepc + 1 >= a.env.max_steps) d = true;
-                    stepc += 1;
-                }
-                if (live) {
-                    const int64_t ti = step * E + e;
-                    a.actions[ti] = X.chosen[t];
-                    a.reward[ti] = done ? 0.0f : static_cast<float>(rew);
-                    a.reward_d[ti] = done ? 0.0 : rew;
-                    a.done_f[ti] = (done || d) ? 1.0f : 0.0f;
-                    float* ntr = a.states + ((step + 1) * E + e) * S_;
-#pragma unroll
-                    for (int i = 0; i < kSynthObs; ++i) {
-                        const float o = static_cast<float>(nst[i]);
-                        ntr[i] = o;
-                        h0w[i] = o;
-                    }
-                }
-                for (int j = S_; j < pad4(S_); ++j) h0w[j] = 0.0f;
-                done = done || d;
-            }
-        } else if (owner) {
+        // ---- PolicyApply + EnvStep: one owner thread per env
+        if (owner) {
             const float* logits = reinterpret_cast<const float*>(smem + S.h[cur]) + t * kHStride;
             float* h0w = reinterpret_cast<float*>(smem + S.h[0]) + t * kHStride;  // next layer-0 input
             double l[16], p[16];
@@ -353,11 +266,6 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
         for (int i = 0; i < 8; ++i) printf("R step %d mlp %lld owner %lld\n", i, tr1[i] - tr0[i], tr2[i] - tr1[i]);
 #endif
     if (live) {
-        if (ENV == 1) {
-            const EnvScratch& X = *reinterpret_cast<const EnvScratch*>(smem + S.env);
-#pragma unroll
-            for (int j = 0; j < SW; ++j) st[j] = X.st[static_cast<int>(a.nsteps) & 1][t][j];
-        }
 #pragma unroll
         for (int j = 0; j < SW; ++j) a.est[j * E + e] = st[j];
         a.done[e] = done ? 1 : 0;

@@ -239,7 +239,7 @@ def bench_reference(args, world, rank):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32-storage/f64-accumulate", "data": "synthetic (synth17x6 env)",
             "impl": "reference",
-            "config": {"workload": f"C2 sample: PPO synth17x6, {envs} envs, 7-layer MLP (hidden 6x64), T=32, "
+            "config": {"workload": f"C2 sample: PPO synth17x6, {envs} envs, 7-layer MLP (hidden 6x{HIDDEN[0]}), T=32, "
                                    f"train_iters=4, dp-d with {k} CPU replicas", "envs": envs, "replicas": k},
             "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": cores, "kind": "reference",
                              "sample": f"{envs} envs per episode, {k} replica threads"},
@@ -300,7 +300,7 @@ def bench_ours(args, world, rank, local):
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f32-storage/f64-accumulate" if args.numerics == "exact" else "bf16-mma/f32-accumulate",
             "data": "synthetic (synth17x6 env, seeded)",
-            "config": {"workload": "C2: PPO synth17x6, 4096 envs/GPU, 7-layer MLP (hidden 6x64), T=32, "
+            "config": {"workload": f"C2: PPO synth17x6, 4096 envs/GPU, 7-layer MLP (hidden 6x{HIDDEN[0]}), T=32, "
                                    "train_iters=4, dp-d fused loop", "envs_total": total, "envs_per_gpu":
                        ENVS_PER_GPU, "numerics": args.numerics, "parallelism": f"dp{world}",
                        "l2": "per-episode working set (activations, ~0.9 GB) exceeds the 126 MB L2"},
@@ -322,9 +322,14 @@ def main():
     ap.add_argument("--numerics", choices=["exact", "fast"], default="fast")
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--hidden", type=int, default=64,
+                    help="hidden width H of the 7-layer MLP (SURVEY §8: H=64, also report H=256; fast numerics "
+                         "supports H <= 64)")
     ap.add_argument("--no-microbench", action="store_true",
                     help="skip the scaled HBM kernel sweeps (profiling runs: the launch list then holds episodes only)")
     args = ap.parse_args()
+    global HIDDEN
+    HIDDEN = [args.hidden] * 6
     world, rank, local = dist_setup()
     if args.impl == "reference":
         bench_reference(args, world, rank)

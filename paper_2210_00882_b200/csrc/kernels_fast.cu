@@ -471,7 +471,7 @@ __global__ void k_reduce_loss(const float* __restrict__ lp, int nparts, int nset
 // Thread per stream (rl.cpp:28-95 recurrences in double); the T-loop is processed in chunks of 8
 // steps whose loads are issued together. Per-block sums of adv and adv^2 feed the normalisation
 // statistics, combined in fixed block order by k_adv_stats.
-__global__ void __launch_bounds__(256) k_fast_gae(const float* __restrict__ rew, const float* __restrict__ values,
+__global__ void __launch_bounds__(256, 4) k_fast_gae(const float* __restrict__ rew, const float* __restrict__ values,
                                                   const float* __restrict__ done_f,
                                                   const float* __restrict__ last_value, int64_t T, int64_t R,
                                                   double gamma, double lam, float* adv, float* ret, bool with_adv,

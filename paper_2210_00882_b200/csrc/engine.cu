@@ -603,21 +603,12 @@ void Engine::enq_learn_fast() {
     static const bool hreuse = std::getenv("FLW_NO_HREUSE") == nullptr;
     f.hsave = hreuse ? b.hsave : nullptr;
     f.save_tiles = hreuse ? (TR_ + 127) / 128 : 0;
-    // k_learn (warp-specialised, two tiles per SM) unless FLW_LEARN_V1 selects the
-    // single-tile kernel (A/B measurement only)
-    static const bool v1_env = std::getenv("FLW_LEARN_V1") != nullptr;
-    const bool v1 = v1_env && nrep_ == 1;
-    const int lgrid = v1 ? b.grid : b.grid2;
-    auto launch = [&](int grid) {
-        if (v1)
-            fast_mlp(stream_, f, grid);
-        else
-            fast_learn(stream_, f, grid);
-    };
+    // k_learn: warp-specialised, two tiles per SM in flight
+    const int lgrid = b.grid2;
+    auto launch = [&](int grid) { fast_learn(stream_, f, grid); };
     f.hscratch = b.hscratch;
     probe_begin("critic_fwd");
-    launch(static_cast<int>(std::min<int64_t>(
-        lgrid, v1 ? (f.rows + 127) / 128 : ((f.rows + 127) / 128 + 1) / 2)));
+    launch(static_cast<int>(std::min<int64_t>(lgrid, ((f.rows + 127) / 128 + 1) / 2)));
     probe_end();
     f.split_rows = -1;
     probe_begin("gae");

@@ -59,14 +59,13 @@ struct FastLearnArgs {
     float* loss_partials;      // [grid, 3]
 };
 
-size_t fast_mlp_smem_bytes(const FastNet& n);
 size_t fast_wimg_bytes(const FastNet& n);  // bytes of the weight-tile image (smem prefix)
 size_t fast_hsave_bytes(const FastNet& n); // bytes of one tile's hidden-activation tiles
 // Builds the bf16 W^T tile image of one net from the f32 params (once per train iteration,
 // shared by every CTA of the critic-forward / learn kernels that follow).
 void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv_bfloat16* img);
-void fast_mlp(cudaStream_t s, const FastLearnArgs& a, int grid);
-// Warp-specialised two-tiles-per-SM learn kernel (kernels_learn.cu); same arguments.
+// Warp-specialised two-tiles-per-SM learn kernel (kernels_learn.cu): mode 0 values pass,
+// mode 1 one train iteration of one net.
 void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid);
 size_t fast_learn_smem_bytes(const FastNet& n);
 size_t fast_learn_scratch_bytes(const FastNet& n);  // hidden bytes of one 128-row tile

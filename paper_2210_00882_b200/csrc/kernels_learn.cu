@@ -91,9 +91,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ void bulk_wait_read1() {
-    asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-}
 
 __device__ __forceinline__ float tanh_fast(float x) {
     float y;
@@ -120,22 +117,12 @@ __device__ __forceinline__ float2 tanh_poly2(float2 x) {
     return __fmul2_rn(p, x);
 }
 
-// bf16x2 MUFU tanh: two activations per SFU op; the result is already the packed bf16 operand.
-__device__ __forceinline__ uint32_t tanh_bf16x2(uint32_t x) {
-    uint32_t y;
-    asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
-    return y;
-}
 
 __device__ __forceinline__ void bulk_load(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint64_t* bar) {
     umma::mbar_expect_tx(bar, bytes);
     for (uint32_t o = 0; o < bytes; o += 16384u) umma::bulk_g2s(dst + o, src + o, min(16384u, bytes - o), bar);
 }
 
-__device__ __forceinline__ void bulk_store(uint8_t* dst, const uint8_t* src, uint32_t bytes) {
-    for (uint32_t o = 0; o < bytes; o += 16384u) umma::bulk_s2g(dst + o, src + o, min(16384u, bytes - o));
-    umma::bulk_commit();
-}
 
 // Column sums over the warp's 32 rows of a 32-wide row slice held one row per lane: a
 // reduce-scatter butterfly (31 shuffles); lane l ends with the sum of column l.

@@ -264,6 +264,11 @@ def bench_ours(args, world, rank, local):
         obj = [DpdEngine.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         eng.comm_init(obj[0], rank, world)
+        if args.numerics == "fast" and args.exchange == "p2p":
+            # gradient exchange over NVLink peer memory (CUDA IPC), fused with reduce + Adam
+            hs = [None] * world
+            dist.all_gather_object(hs, eng.p2p_export(world))
+            eng.p2p_import(hs, rank)
     # warm-up (also captures the episode graph, with CUDA-event probes around the main kernels)
     eng.enable_probes(True)
     eng.run_episodes(0, args.warmup)
@@ -303,6 +308,7 @@ def bench_ours(args, world, rank, local):
             "config": {"workload": f"C2: PPO synth17x6, 4096 envs/GPU, 7-layer MLP (hidden 6x{HIDDEN[0]}), T=32, "
                                    "train_iters=4, dp-d fused loop", "envs_total": total, "envs_per_gpu":
                        ENVS_PER_GPU, "numerics": args.numerics, "parallelism": f"dp{world}",
+                       "exchange": (args.exchange if args.numerics == "fast" else "nccl") if world > 1 else None,
                        "l2": "per-episode working set (activations, ~0.9 GB) exceeds the 126 MB L2"},
             "episode_ms": episode_ms, "gpu_launches": stats["graph_kernels"] * args.steps,
             "clocks": clk.summary(), "e2e": e2e, "roofline": roofline, "kernel_shares": shares}
@@ -322,6 +328,8 @@ def main():
     ap.add_argument("--numerics", choices=["exact", "fast"], default="fast")
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 fast numerics: gradient exchange over NVLink peer memory (one fused kernel) or NCCL")
     ap.add_argument("--hidden", type=int, default=64,
                     help="hidden width H of the 7-layer MLP (SURVEY §8: H=64, also report H=256; fast numerics "
                          "supports H <= 64)")

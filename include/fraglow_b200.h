@@ -93,6 +93,13 @@ int flw_dpd_destroy(flw_dpd* e);
 int flw_dpd_comm_unique_id(char* out_id, int64_t cap);
 int flw_dpd_comm_init(flw_dpd* e, const char* id, int64_t id_len, int rank, int nranks);
 
+/* Fast numerics, one unit per GPU: gradient exchange over NVLink peer memory instead of NCCL
+ * (reduce of the per-CTA partials + all-reduce + Adam in one kernel). Every rank exports the
+ * CUDA IPC handle (64 bytes) of its exchange region, the caller gathers the k handles in rank
+ * order and every rank imports them. */
+int flw_dpd_p2p_export(flw_dpd* e, int nranks, char* out_handle, int64_t cap);
+int flw_dpd_p2p_import(flw_dpd* e, const char* handles, int64_t len, int rank, int nranks);
+
 /* One whole episode (Reset, T x Step, I x Learn) as a replayed CUDA graph. reward_sum is the
  * episode's summed env reward over this unit's envs (interp.cpp:257); device_ms the graph time. */
 int flw_dpd_run_episode(flw_dpd* e, int64_t episode, double* reward_sum, float* device_ms);

@@ -110,6 +110,18 @@ class DpdEngine:
         N.check(N.lib().flw_dpd_comm_unique_id(buf, 128))
         return buf.raw
 
+    def p2p_export(self, nranks: int) -> bytes:
+        """CUDA IPC handle of this unit's peer-memory exchange region (fast numerics)."""
+        buf = C.create_string_buffer(64)
+        N.check(N.lib().flw_dpd_p2p_export(self._h, nranks, buf, 64))
+        return buf.raw
+
+    def p2p_import(self, handles: list, rank: int):
+        """Map every rank's exchange region (handles in rank order): gradients then move over
+        NVLink peer memory inside one fused reduce/all-reduce/Adam kernel instead of NCCL."""
+        blob = b"".join(handles)
+        N.check(N.lib().flw_dpd_p2p_import(self._h, blob, len(blob), rank, len(handles)))
+
     def comm_init(self, uid: bytes, rank: int, nranks: int):
         N.check(N.lib().flw_dpd_comm_init(self._h, uid, len(uid), rank, nranks))
 

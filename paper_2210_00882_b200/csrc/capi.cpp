@@ -32,6 +32,7 @@ struct flw_program {
     Plan plan;
     Numerics numerics = Numerics::Exact;
     int reps_per_gpu = 0;  // deploy "replicas_per_gpu": units folded per engine (0: only when k > #GPUs)
+    std::string exchange = "p2p";  // deploy "exchange": gradient exchange of fast numerics, "p2p" | "nccl"
     // Engines persist across flw_run_local calls on the same program (re-initialised per run):
     // device buffers and the captured episode graph are set up once.
     std::vector<std::unique_ptr<Engine>> engines;
@@ -175,6 +176,33 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
                 p.engines[g]->set_comm(std::move(c));
             }
             Comm::connect_all(cs, devs, static_cast<int64_t>(R) * p.engines[0]->shape().P);
+            // fast numerics, one unit per GPU: gradient exchange over NVLink peer memory when
+            // every pair of GPUs can address each other (deploy "exchange": "nccl" opts out)
+            bool p2p = p.numerics == Numerics::Fast && R == 1 && p.exchange != "nccl";
+            for (int a = 0; p2p && a < ng; ++a)
+                for (int b2 = 0; p2p && b2 < ng; ++b2) {
+                    int ok = 0;
+                    if (a != b2 && (cudaDeviceCanAccessPeer(&ok, a, b2) != cudaSuccess || !ok)) p2p = false;
+                }
+            if (p2p) {
+                std::vector<void*> regions;
+                for (int g = 0; g < ng; ++g) {
+                    p.engines[g]->alloc_p2p_region(ng);
+                    regions.push_back(p.engines[g]->p2p_region());
+                }
+                for (int g = 0; g < ng; ++g) {
+                    FLW_CUDA(cudaSetDevice(g));
+                    for (int h = 0; h < ng; ++h)
+                        if (h != g) {
+                            cudaError_t err = cudaDeviceEnablePeerAccess(h, 0);
+                            if (err == cudaErrorPeerAccessAlreadyEnabled)
+                                cudaGetLastError();
+                            else
+                                FLW_CUDA(err);
+                        }
+                    p.engines[g]->set_p2p_peers(g, ng, regions);
+                }
+            }
         }
     } else {
         for (auto& e : p.engines) e->reinit(seed);
@@ -265,6 +293,7 @@ int flw_program_create(const char* algo_json, const char* deploy_json, flw_progr
             auto j = nlohmann::json::parse(deploy_json);
             if (j.contains("numerics")) p->numerics = numerics_from(j["numerics"].get<std::string>());
             if (j.contains("replicas_per_gpu")) p->reps_per_gpu = j["replicas_per_gpu"].get<int>();
+            if (j.contains("exchange")) p->exchange = j["exchange"].get<std::string>();
         } else {
             p->deploy = DeployConfig{{"local"}, 8, 8, Policy::DpA};  // capi.cpp:211-212 default
         }
@@ -360,6 +389,44 @@ int flw_dpd_comm_unique_id(char* out_id, int64_t cap) {
         std::string id = Comm::new_unique_id();
         if (cap < static_cast<int64_t>(id.size())) fail(Errc::Config, "unique id buffer too small");
         std::memcpy(out_id, id.data(), id.size());
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_p2p_export(flw_dpd* e, int nranks, char* out_handle, int64_t cap) {
+    return guarded([&] {
+        Engine& en = eng(e);
+        if (cap < static_cast<int64_t>(sizeof(cudaIpcMemHandle_t))) fail(Errc::Config, "handle buffer too small");
+        en.alloc_p2p_region(nranks);
+        FLW_CUDA(cudaSetDevice(en.device()));
+        cudaIpcMemHandle_t h;
+        FLW_CUDA(cudaIpcGetMemHandle(&h, en.p2p_region()));
+        std::memcpy(out_handle, &h, sizeof(h));
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_p2p_import(flw_dpd* e, const char* handles, int64_t len, int rank, int nranks) {
+    return guarded([&] {
+        Engine& en = eng(e);
+        const int64_t hb = static_cast<int64_t>(sizeof(cudaIpcMemHandle_t));
+        if (len != hb * nranks) fail(Errc::Config, "expected nranks IPC handles");
+        en.alloc_p2p_region(nranks);
+        FLW_CUDA(cudaSetDevice(en.device()));
+        std::vector<void*> regions(static_cast<size_t>(nranks), nullptr);
+        for (int r = 0; r < nranks; ++r) {
+            if (r == rank) {
+                regions[static_cast<size_t>(r)] = en.p2p_region();
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, handles + hb * r, sizeof(h));
+            void* ptr = nullptr;
+            FLW_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            en.adopt_ipc_mapping(ptr);
+            regions[static_cast<size_t>(r)] = ptr;
+        }
+        en.set_p2p_peers(rank, nranks, regions);
         return FLW_OK;
     });
 }

@@ -11,6 +11,7 @@
 #include "engine.hpp"
 
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <vector>
 
@@ -19,6 +20,7 @@
 #include "comm.hpp"
 #include "common.cuh"
 #include "fast.cuh"
+#include "p2p.cuh"
 #include "kernels.cuh"
 
 namespace flw {
@@ -63,6 +65,7 @@ struct Engine::Bufs {
     uint8_t* hsave = nullptr;           // critic hidden activations of the values pass (bf16 tiles)
     uint8_t* hscratch = nullptr;        // k_learn per-(CTA, group) activation scratch
     int grid2 = 0;                      // k_learn grid (two tiles per CTA in flight)
+    int lgrid = 0;                      // CTA partial slots written by the last learn launch
     double *block_sums = nullptr, *rsum_scratch = nullptr;
     // R > 1 replicas: env -> replica map, replica-major trajectory copies (exact), per-replica
     // gradient slots [R, P], advantage statistics [R, 2] and row weights (fast)
@@ -154,6 +157,8 @@ Engine::~Engine() {
     if (stream_) cudaStreamSynchronize(stream_);
     destroy_graph();
     comm_.reset();
+    for (void* q : p2p_ipc_opened_) cudaIpcCloseMemHandle(q);
+    if (p2p_region_ptr_) cudaFree(p2p_region_ptr_);
     b_.reset();
     for (cudaEvent_t e : {ev_fork_, ev_join_, ev_t0_, ev_t1_})
         if (e) cudaEventDestroy(e);
@@ -171,6 +176,40 @@ void Engine::destroy_graph() {
 void Engine::set_eager_collectives(bool on) {
     if (on != eager_coll_) destroy_graph();
     eager_coll_ = on;
+}
+
+int64_t Engine::p2p_region_bytes() const { return p2p_layout(p2p_k_ > 0 ? p2p_k_ : 1, shape_.P).bytes; }
+
+void* Engine::p2p_region() {
+    if (numerics_ != Numerics::Fast || nrep_ > 1)
+        fail(Errc::Config, "the peer-memory exchange serves fast numerics with one unit per GPU");
+    if (!p2p_region_ptr_) fail(Errc::Config, "call set_p2p_group first (region size depends on k)");
+    return p2p_region_ptr_;
+}
+
+void Engine::set_p2p_peers(int rank, int k, const std::vector<void*>& regions) {
+    FLW_CUDA(cudaSetDevice(device_));
+    if (static_cast<int>(regions.size()) != k || rank < 0 || rank >= k) fail(Errc::Config, "bad p2p group");
+    destroy_graph();
+    if (!p2p_peers_dev_) p2p_peers_dev_ = reinterpret_cast<uint8_t**>(b_->alloc<uint8_t*>(64));
+    if (k > 64) fail(Errc::Config, "at most 64 ranks");
+    FLW_CUDA(cudaMemcpy(p2p_peers_dev_, regions.data(), sizeof(void*) * regions.size(), cudaMemcpyHostToDevice));
+    p2p_rank_ = rank;
+    p2p_k_ = k;
+}
+
+void Engine::alloc_p2p_region(int k) {
+    FLW_CUDA(cudaSetDevice(device_));
+    if (numerics_ != Numerics::Fast || nrep_ > 1)
+        fail(Errc::Config, "the peer-memory exchange serves fast numerics with one unit per GPU");
+    const P2pLayout L = p2p_layout(k, shape_.P);
+    if (!p2p_region_ptr_) {
+        FLW_CUDA(cudaMalloc(&p2p_region_ptr_, static_cast<size_t>(L.bytes)));  // plain cudaMalloc: IPC-exportable
+        FLW_CUDA(cudaMemset(p2p_region_ptr_, 0, static_cast<size_t>(L.bytes)));
+        p2p_alloc_k_ = k;
+    } else if (p2p_alloc_k_ != k) {
+        fail(Errc::Config, "p2p region already sized for another group");
+    }
 }
 
 void Engine::set_comm(std::unique_ptr<Comm> comm) {
@@ -385,7 +424,7 @@ void Engine::reinit(uint64_t seed) {
     init_params();
     FLW_CUDA(cudaMemset(b_->m, 0, static_cast<size_t>(shape_.P) * sizeof(double)));
     FLW_CUDA(cudaMemset(b_->v, 0, static_cast<size_t>(shape_.P) * sizeof(double)));
-    FLW_CUDA(cudaMemset(b_->ctx, 0, sizeof(DeviceCtx)));
+    FLW_CUDA(cudaMemset(b_->ctx, 0, offsetof(DeviceCtx, coll_seq)));  // keep the exchange epoch
     steps_ = 0;
     cur_step_ = 0;
 }
@@ -649,9 +688,12 @@ void Engine::enq_learn_fast() {
     probe_begin("learn_critic");
     launch(lgrid);
     probe_end();
-    probe_begin("reduce");
-    fast_reduce_partials(stream_, b.part_p, b.part_c, lgrid, s.P_policy, s.P - s.P_policy, b.grads);
-    probe_end();
+    b.lgrid = lgrid;
+    if (!p2p_enabled()) {  // with peer-memory exchange the reduction is fused into the exchange
+        probe_begin("reduce");
+        fast_reduce_partials(stream_, b.part_p, b.part_c, lgrid, s.P_policy, s.P - s.P_policy, b.grads);
+        probe_end();
+    }
     fast_reduce_loss(stream_, b.loss_parts, lgrid, 2, cfg_.entropy_coef, b.loss);
 }
 
@@ -725,6 +767,37 @@ void Engine::enq_grad_sync_and_adam() {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     adam_tick(stream_, b.ctx, b.bc_table, b.bc_len);
+    if (p2p_enabled() && numerics_ == Numerics::Fast) {
+        // reduce the CTA partials + all-reduce over NVLink peer memory + Adam: one kernel
+        const P2pLayout Lo = p2p_layout(p2p_k_, s.P);
+        P2pArgs a{};
+        a.part_p = b.part_p;
+        a.part_c = b.part_c;
+        a.nparts = b.lgrid;
+        a.Pp = s.P_policy;
+        a.Pc = s.P - s.P_policy;
+        a.rank = p2p_rank_;
+        a.k = p2p_k_;
+        a.peers = p2p_peers_dev_;
+        a.off_inbox = Lo.off_inbox;
+        a.off_grads = Lo.off_grads;
+        a.off_sflag = Lo.off_sflag;
+        a.off_dflag = Lo.off_dflag;
+        a.ctx = b.ctx;
+        a.params = b.params;
+        a.m = b.m;
+        a.v = b.v;
+        a.lr = cfg_.lr;
+        a.b1 = 0.9;
+        a.b2 = 0.999;
+        a.eps = 1e-8;
+        a.gscale = 1.0 / static_cast<double>(p2p_k_);
+        coll_tick(stream_, b.ctx);
+        probe_begin("exchange_adam");
+        reduce_allreduce_adam(stream_, a);
+        probe_end();
+        return;
+    }
     const double* g64 = nullptr;
     double gscale = 1.0;
     const bool rep = nrep_ > 1 && numerics_ == Numerics::Exact;

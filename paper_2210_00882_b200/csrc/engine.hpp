@@ -28,6 +28,7 @@ struct DeviceCtx {      // device-resident episode context (read by kernels insi
     int64_t next_episode;  // consumed by the graph's first node, so replays can be queued back to back
     int64_t adam_t;
     double bc1, bc2;    // Adam bias corrections 1 - beta^t, from a host-computed table
+    uint64_t coll_seq;  // peer-memory exchange epoch: monotonically increasing, never reset
 };
 
 class Comm;  // NCCL gradient group (comm.hpp)
@@ -47,6 +48,15 @@ class Engine {
     // Gradient group (GradSync): rank = unit id, nranks = k. Takes ownership.
     void set_comm(std::unique_ptr<Comm> comm);
     Comm* comm() { return comm_.get(); }
+    // Peer-memory gradient exchange (fast numerics, k GPUs): this rank's exchange region, and
+    // the regions of all k ranks as mapped into this process (own entry included). When set,
+    // reduce + all-reduce + Adam run as one kernel (kernels_p2p.cu) instead of NCCL.
+    void* p2p_region();
+    int64_t p2p_region_bytes() const;
+    void alloc_p2p_region(int k);  // before p2p_region(): the layout depends on k
+    void adopt_ipc_mapping(void* p) { p2p_ipc_opened_.push_back(p); }  // closed by the destructor
+    void set_p2p_peers(int rank, int k, const std::vector<void*>& regions);
+    bool p2p_enabled() const { return p2p_k_ > 1; }
     void set_eager_collectives(bool on);
     void prepare();  // captures the episode graph now (before any peer launches its own)
 
@@ -117,6 +127,11 @@ class Engine {
     uint64_t seed_;
     int64_t lo_, hi_, etot_, E_, R_, T_, TR_;
     bool mappo_ = false;   // agent-major rows R = n*E, critic on [joint obs | agent one-hot]
+    int p2p_rank_ = 0, p2p_k_ = 0;
+    void* p2p_region_ptr_ = nullptr;
+    int p2p_alloc_k_ = 0;
+    std::vector<void*> p2p_ipc_opened_;
+    uint8_t** p2p_peers_dev_ = nullptr;
     int nrep_ = 1;                          // replicas folded into this engine
     std::vector<int64_t> rep_off_, rep_n_;  // replica env offset (relative to lo_) and size
     void enq_permute_replicas();

@@ -76,8 +76,10 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
     const float* src = !ok ? pp : (i < Pp ? pp + i : pc + (i - Pp));
     const int64_t stride = i < Pp ? Pp : Pc;
     float s = 0.0f;
-    if (ok)
-        for (int p = w; p < nparts; p += 8) s += src[p * stride];
+    if (ok) {
+#pragma unroll 8
+        for (int p = w; p < nparts; p += 8) s += src[p * stride];  // loads hoisted, adds in order
+    }
     ws[w][lane] = s;
     __syncthreads();
     if (w == 0 && ok) {

@@ -1,0 +1,34 @@
+// Gradient exchange over NVLink peer memory (kernels_p2p.cu): the fused
+// reduce -> all-reduce -> Adam step of fast numerics on k GPUs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace flw {
+
+struct DeviceCtx;
+
+struct P2pLayout {  // byte offsets inside every rank's exchange region
+    int64_t off_inbox, off_grads, off_sflag, off_dflag, bytes;
+};
+P2pLayout p2p_layout(int k, int64_t P);
+
+struct P2pArgs {
+    const float* part_p;  // [nparts, Pp] per-CTA dW partials of the policy net
+    const float* part_c;  // [nparts, Pc] ... of the critic
+    int nparts;
+    int64_t Pp, Pc;
+    int rank, k;
+    uint8_t* const* peers;  // device array [k]: every rank's exchange region, mapped here
+    int64_t off_inbox, off_grads, off_sflag, off_dflag;
+    const DeviceCtx* ctx;   // coll_seq (epoch), Adam bias corrections
+    float* params;
+    double *m, *v;
+    double lr, b1, b2, eps, gscale;
+};
+
+void coll_tick(cudaStream_t s, DeviceCtx* ctx);  // ++ctx->coll_seq (one per exchange)
+void reduce_allreduce_adam(cudaStream_t s, const P2pArgs& a);
+
+}  // namespace flw

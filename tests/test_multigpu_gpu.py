@@ -48,3 +48,31 @@ def test_fast_two_gpus_runs_and_learns():
                           "numerics": "fast"})
     csv, s = prog.run_local(seed=1, reward_threshold=0.9)
     assert s["time_to_threshold_ms"] >= 0, csv
+
+
+@pytest.mark.parametrize("gpus", [2, 4])
+def test_fast_peer_memory_exchange_matches_nccl(gpus):
+    """Fast numerics on k GPUs: the fused reduce + NVLink peer-memory all-reduce + Adam kernel
+    against the NCCL path. Same per-rank reduction order; at k=2 the cross-rank sum is a single
+    addition either way, so the trained parameters must be identical."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    from paper_2210_00882_b200 import Program
+
+    algo = {"algorithm": "ppo", "actor": {"num": gpus}, "env": {"type": "synth17x6", "num": 512 * gpus},
+            "policy_net": {"hidden": [64, 64, 64]}, "loop": {"episodes": 4, "steps_per_episode": 16}}
+    out = {}
+    for ex in ("p2p", "nccl"):
+        prog = Program(algo, {"slots_per_worker": {"cpu": gpus, "accel": gpus}, "distribution_policy": "dp-d",
+                              "numerics": "fast", "exchange": ex})
+        csv, s = prog.run_local(seed=3)
+        out[ex] = (csv, s)
+    sp, sn = out["p2p"][1], out["nccl"][1]
+    if gpus == 2:
+        assert sp["param_checksum"] == sn["param_checksum"]
+        assert sp["param_l2"] == sn["param_l2"]
+    else:
+        assert sp["param_l2"] == pytest.approx(sn["param_l2"], rel=1e-5)
+    rp = [float(l.split(",")[2]) for l in out["p2p"][0].strip().split("\n")[1:]]
+    rn = [float(l.split(",")[2]) for l in out["nccl"][0].strip().split("\n")[1:]]
+    np.testing.assert_allclose(rp, rn, rtol=1e-4)

@@ -65,7 +65,7 @@ struct Engine::Bufs {
     uint8_t* hsave = nullptr;           // critic hidden activations of the values pass (bf16 tiles)
     uint8_t* hscratch = nullptr;        // k_learn per-(CTA, group) activation scratch
     int grid2 = 0;                      // k_learn grid (two tiles per CTA in flight)
-    int lgrid = 0;                      // CTA partial slots written by the last learn launch
+    int lgrid_p = 0, lgrid_c = 0;       // CTA partial slots written by the last policy / critic learn
     double *block_sums = nullptr, *rsum_scratch = nullptr;
     // R > 1 replicas: env -> replica map, replica-major trajectory copies (exact), per-replica
     // gradient slots [R, P], advantage statistics [R, 2] and row weights (fast)
@@ -144,6 +144,9 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     FLW_CUDA(cudaSetDevice(device_));
     FLW_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     FLW_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    FLW_CUDA(cudaStreamCreateWithFlags(&side2_, cudaStreamNonBlocking));
+    FLW_CUDA(cudaEventCreateWithFlags(&ev_lfork_, cudaEventDisableTiming));
+    FLW_CUDA(cudaEventCreateWithFlags(&ev_ljoin_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreate(&ev_t0_));
@@ -160,9 +163,10 @@ Engine::~Engine() {
     for (void* q : p2p_ipc_opened_) cudaIpcCloseMemHandle(q);
     if (p2p_region_ptr_) cudaFree(p2p_region_ptr_);
     b_.reset();
-    for (cudaEvent_t e : {ev_fork_, ev_join_, ev_t0_, ev_t1_})
+    for (cudaEvent_t e : {ev_fork_, ev_join_, ev_t0_, ev_t1_, ev_lfork_, ev_ljoin_})
         if (e) cudaEventDestroy(e);
     if (side_) cudaStreamDestroy(side_);
+    if (side2_) cudaStreamDestroy(side2_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -674,27 +678,48 @@ void Engine::enq_learn_fast() {
     f.partials = b.part_p;
     f.part_stride = s.P_policy;
     f.loss_partials = b.loss_parts;
+    // The policy and critic learn kernels run CONCURRENTLY on disjoint SMs (two streams), the
+    // SMs split in proportion to their per-tile cost (the critic skips its forward), so both
+    // finish together instead of each paying its own tail.
+    int gp = lgrid, gc = lgrid;
+    const bool concurrent = hreuse && lgrid >= 8;  // the critic reads hsave, not hscratch
+    if (concurrent) {
+        static const double split = std::getenv("FLW_LEARN_SPLIT") ? std::atof(std::getenv("FLW_LEARN_SPLIT")) : 0.6;
+        gp = std::max(1, std::min(lgrid - 1, static_cast<int>(lgrid * split + 0.5)));
+        gc = std::max(1, lgrid - gp);
+        FLW_CUDA(cudaEventRecord(ev_lfork_, stream_));
+        FLW_CUDA(cudaStreamWaitEvent(side2_, ev_lfork_, 0));
+    }
+    f.loss_partials = b.loss_parts;
     probe_begin("learn_policy");
-    launch(lgrid);
+    launch(gp);
     probe_end();
-    f.net = b.crit;
-    f.wimg = b.wimg_c;
-    f.hsave = hreuse ? b.hsave : nullptr;  // same params as the values pass: same activations
-    f.hload = hreuse ? 1 : 0;
-    f.kind = kNetCritic;
-    f.partials = b.part_c;
-    f.part_stride = s.P - s.P_policy;
-    f.loss_partials = b.loss_parts + 3 * lgrid;
-    probe_begin("learn_critic");
-    launch(lgrid);
-    probe_end();
-    b.lgrid = lgrid;
-    if (!p2p_enabled()) {  // with peer-memory exchange the reduction is fused into the exchange
-        probe_begin("reduce");
-        fast_reduce_partials(stream_, b.part_p, b.part_c, lgrid, s.P_policy, s.P - s.P_policy, b.grads);
+    FastLearnArgs fc = f;
+    fc.net = b.crit;
+    fc.wimg = b.wimg_c;
+    fc.hsave = hreuse ? b.hsave : nullptr;  // same params as the values pass: same activations
+    fc.hload = hreuse ? 1 : 0;
+    fc.kind = kNetCritic;
+    fc.partials = b.part_c;
+    fc.part_stride = s.P - s.P_policy;
+    fc.loss_partials = b.loss_parts + 3 * gp;
+    if (concurrent) {
+        fast_learn(side2_, fc, gc);
+        FLW_CUDA(cudaEventRecord(ev_ljoin_, side2_));
+        FLW_CUDA(cudaStreamWaitEvent(stream_, ev_ljoin_, 0));
+    } else {
+        probe_begin("learn_critic");
+        fast_learn(stream_, fc, gc);
         probe_end();
     }
-    fast_reduce_loss(stream_, b.loss_parts, lgrid, 2, cfg_.entropy_coef, b.loss);
+    b.lgrid_p = gp;
+    b.lgrid_c = gc;
+    if (!p2p_enabled()) {  // with peer-memory exchange the reduction is fused into the exchange
+        probe_begin("reduce");
+        fast_reduce_partials(stream_, b.part_p, b.part_c, gp, gc, s.P_policy, s.P - s.P_policy, b.grads);
+        probe_end();
+    }
+    fast_reduce_loss(stream_, b.loss_parts, gp, gc, cfg_.entropy_coef, b.loss);
 }
 
 void Engine::enq_learn_grads() {
@@ -773,7 +798,8 @@ void Engine::enq_grad_sync_and_adam() {
         P2pArgs a{};
         a.part_p = b.part_p;
         a.part_c = b.part_c;
-        a.nparts = b.lgrid;
+        a.np = b.lgrid_p;
+        a.nc = b.lgrid_c;
         a.Pp = s.P_policy;
         a.Pc = s.P - s.P_policy;
         a.rank = p2p_rank_;

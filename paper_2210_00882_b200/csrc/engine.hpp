@@ -136,8 +136,9 @@ class Engine {
     std::vector<int64_t> rep_off_, rep_n_;  // replica env offset (relative to lo_) and size
     void enq_permute_replicas();
     Numerics numerics_;
-    cudaStream_t stream_ = nullptr, side_ = nullptr;
+    cudaStream_t stream_ = nullptr, side_ = nullptr, side2_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_t0_ = nullptr, ev_t1_ = nullptr;
+    cudaEvent_t ev_lfork_ = nullptr, ev_ljoin_ = nullptr;  // policy || critic learn fork/join
     std::unique_ptr<Bufs> b_;
     std::unique_ptr<Comm> comm_;
     cudaGraphExec_t graph_ = nullptr;  // == segs_[0]

@@ -69,9 +69,10 @@ void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv
 void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid);
 size_t fast_learn_smem_bytes(const FastNet& n);
 size_t fast_learn_scratch_bytes(const FastNet& n);  // hidden bytes of one 128-row tile
-void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int nparts, int64_t Pp, int64_t Pc,
-                          float* grads);
-void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int nparts, int nsets, double entropy_coef, float* loss);
+// fixed-order sums of the per-CTA partial slots: np policy slots, nc critic slots
+void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int np, int nc, int64_t Pp,
+                          int64_t Pc, float* grads);
+void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss);
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
               double* block_sums, double* stats);

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) k_build_wimg(const float* __restrict__ pa
 // grads[p] = sum over CTA partials in CTA order (deterministic); both nets in one launch, the
 // critic's partials following the policy's in the flat gradient.
 __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict__ pp, const float* __restrict__ pc,
-                                                         int nparts, int64_t Pp, int64_t Pc, float* grads) {
+                                                         int np, int nc, int64_t Pp, int64_t Pc, float* grads) {
     // 32 parameters per block (lane = parameter, coalesced rows); warp w sums partials
     // w, w+8, ... in order, then the 8 warp sums are added in warp order: a fixed tree.
     __shared__ float ws[8][32];
@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
     const bool ok = i < Pp + Pc;
     const float* src = !ok ? pp : (i < Pp ? pp + i : pc + (i - Pp));
     const int64_t stride = i < Pp ? Pp : Pc;
+    const int nparts = i < Pp ? np : nc;
     float s = 0.0f;
     if (ok) {
 #pragma unroll 8
@@ -90,16 +91,15 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
     }
 }
 
-__global__ void k_reduce_loss(const float* __restrict__ lp, int nparts, int nsets, double ec, float* loss) {
+__global__ void k_reduce_loss(const float* __restrict__ lp, int np, int nc, double ec, float* loss) {
     const int lane = threadIdx.x;
     double pl = 0, vl = 0, en = 0;
-    for (int s = 0; s < nsets; ++s)
-        for (int p = lane; p < nparts; p += 32) {
-            const float* q = lp + (s * nparts + p) * 3;
-            pl += q[0];
-            vl += q[1];
-            en += q[2];
-        }
+    for (int p = lane; p < np + nc; p += 32) {  // policy slots [0, np), critic slots [np, np + nc)
+        const float* q = lp + p * 3;
+        pl += q[0];
+        vl += q[1];
+        en += q[2];
+    }
     for (int off = 16; off > 0; off >>= 1) {
         pl += __shfl_xor_sync(0xffffffffu, pl, off);
         vl += __shfl_xor_sync(0xffffffffu, vl, off);
@@ -266,15 +266,14 @@ void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv
 }
 
 
-void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int nparts, int64_t Pp, int64_t Pc,
-                          float* grads) {
-    k_reduce_partials<<<static_cast<unsigned>((Pp + Pc + 31) / 32), 256, 0, s>>>(part_p, part_c, nparts, Pp, Pc,
+void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int np, int nc, int64_t Pp,
+                          int64_t Pc, float* grads) {
+    k_reduce_partials<<<static_cast<unsigned>((Pp + Pc + 31) / 32), 256, 0, s>>>(part_p, part_c, np, nc, Pp, Pc,
                                                                                  grads);
 }
 
-void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int nparts, int nsets, double entropy_coef,
-                      float* loss) {
-    k_reduce_loss<<<1, 32, 0, s>>>(loss_parts, nparts, nsets, entropy_coef, loss);
+void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss) {
+    k_reduce_loss<<<1, 32, 0, s>>>(loss_parts, np, nc, entropy_coef, loss);
 }
 
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,

@@ -49,10 +49,11 @@ __global__ void __launch_bounds__(256) k_reduce_push(P2pArgs a) {
     const bool ok = i < P;
     const float* src = !ok ? a.part_p : (i < a.Pp ? a.part_p + i : a.part_c + (i - a.Pp));
     const int64_t stride = i < a.Pp ? a.Pp : a.Pc;
+    const int nparts = i < a.Pp ? a.np : a.nc;
     float s = 0.0f;
     if (ok) {
 #pragma unroll 8
-        for (int p = w; p < a.nparts; p += 8) s += src[p * stride];  // loads hoisted, adds in order
+        for (int p = w; p < nparts; p += 8) s += src[p * stride];  // loads hoisted, adds in order
     }
     ws[w][lane] = s;
     __syncthreads();

@@ -17,7 +17,7 @@ P2pLayout p2p_layout(int k, int64_t P);
 struct P2pArgs {
     const float* part_p;  // [nparts, Pp] per-CTA dW partials of the policy net
     const float* part_c;  // [nparts, Pc] ... of the critic
-    int nparts;
+    int np, nc;  // partial slots written by the policy / critic learn launches
     int64_t Pp, Pc;
     int rank, k;
     uint8_t* const* peers;  // device array [k]: every rank's exchange region, mapped here

@@ -179,6 +179,16 @@ def roofline_for(tag: str, ms: float, envs: int, peaks: dict) -> dict:
     pol = [17] + HIDDEN + [6]
     cri = [17] + HIDDEN + [1]
     rows = envs * T_STEPS
+    if tag == "learn":  # policy || critic learn kernels, concurrent on a 60/40 SM split
+        pf, pdh = mlp_macs(pol)
+        cf, cdh = mlp_macs(cri)
+        # policy: forward + dW + dH; critic: dW + dH (its forward is the values pass, reused)
+        flops = 2.0 * rows * ((pf + pf + pdh) + (cf + cdh))
+        ach = flops / (ms * 1e-3) / 1e12
+        return {"kernel": "learn (k_learn policy || k_learn critic, concurrent)", "bound": "tensor", "achieved": ach,
+                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": ach / peaks["bf16_tflops"],
+                "traffic": ncu_traffic("learn"), "peak_source": peaks["source"],
+                "work_per_launch": f"{flops:.4g} FLOP ({rows} rows, both nets)", "launch_ms": ms}
     if tag in ("learn_policy", "learn_critic", "critic_fwd"):
         dims = pol if tag == "learn_policy" else cri
         fwd, dh = mlp_macs(dims)
@@ -299,7 +309,12 @@ def bench_ours(args, world, rank, local):
     episode_ms = dev_ms / args.steps
     shares = {k: {"ms_per_episode": sum(v), "launches": len(v), "share": sum(v) / episode_ms} for k, v in probes.items()}
     dom = max(shares, key=lambda k: shares[k]["ms_per_episode"]) if shares else None
-    roofline = roofline_for(dom, sum(probes[dom]) / len(probes[dom]), ENVS_PER_GPU, peaks) if dom else None
+    if dom == "learn_policy" and "learn_critic" not in probes:
+        dom = "learn"  # the critic learn kernel runs inside the policy kernel's window
+        probes_dom = probes["learn_policy"]
+    else:
+        probes_dom = probes.get(dom, [])
+    roofline = roofline_for(dom, sum(probes_dom) / len(probes_dom), ENVS_PER_GPU, peaks) if dom else None
     line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,

@@ -67,6 +67,7 @@ struct Engine::Bufs {
     int grid2 = 0;                      // k_learn grid (two tiles per CTA in flight)
     int lgrid_p = 0, lgrid_c = 0;       // CTA partial slots written by the last policy / critic learn
     double *block_sums = nullptr, *rsum_scratch = nullptr;
+    unsigned* gae_counter = nullptr;  // last-block-done counter of the fused GAE statistics
     // R > 1 replicas: env -> replica map, replica-major trajectory copies (exact), per-replica
     // gradient slots [R, P], advantage statistics [R, 2] and row weights (fast)
     int32_t* rep_of_env = nullptr;
@@ -345,6 +346,7 @@ void Engine::alloc() {
         b.hscratch = b.alloc<uint8_t>(static_cast<int64_t>(
             std::max(fast_learn_scratch_bytes(b.pol), fast_learn_scratch_bytes(b.crit)) * 2 * b.grid2));
         b.block_sums = b.alloc<double>(2 * ((R_ + 255) / 256));
+        b.gae_counter = b.alloc<unsigned>(1);
         b.rsum_scratch = b.alloc<double>(256);
         b.values = b.alloc<float>(TR_);
         b.last_value = b.alloc<float>(R_);
@@ -626,8 +628,7 @@ void Engine::enq_learn_fast() {
     f.rep_of_env = nrep_ > 1 ? b.rep_of_env : nullptr;
     f.rep_w = b.rep_w;
     f.rep_E = E_;
-    fast_build_wimg(stream_, b.params, b.crit, b.wimg_c);
-    fast_build_wimg(stream_, b.params, b.pol, b.wimg_p);
+    fast_build_wimg(stream_, b.params, b.crit, b.wimg_c, b.pol, b.wimg_p);
     // values = critic(states), last_value = critic(last_next)
     f.net = b.crit;
     f.wimg = b.wimg_c;
@@ -656,7 +657,7 @@ void Engine::enq_learn_fast() {
     f.split_rows = -1;
     probe_begin("gae");
     fast_gae(stream_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
-             b.block_sums, b.stats);
+             b.block_sums, b.stats, b.gae_counter);
     if (nrep_ > 1 && ppo && cfg_.normalize_adv)  // each folded unit normalises over its own rows
         fast_rep_adv_stats(stream_, b.adv, T_, E_, b.rep_off, b.rep_n, nrep_, b.stats);
     probe_end();
@@ -719,7 +720,7 @@ void Engine::enq_learn_fast() {
         fast_reduce_partials(stream_, b.part_p, b.part_c, gp, gc, s.P_policy, s.P - s.P_policy, b.grads);
         probe_end();
     }
-    fast_reduce_loss(stream_, b.loss_parts, gp, gc, cfg_.entropy_coef, b.loss);
+    // the scalar loss is not an input of anything downstream: reduced on demand (read_tensor)
 }
 
 void Engine::enq_learn_grads() {
@@ -1201,7 +1202,13 @@ void Engine::read_tensor(const std::string& n, double* out) {
     if (n == "ret") return put(d2h(b.ret, TR_));
     if (n == "logits_new") return put(d2h(b.Hp[L - 1], TR_ * A));
     if (n == "dlogits") return put(d2h(b.DZp[L - 1], TR_ * A));
-    if (n == "loss") return put(d2h(b.loss, 1));
+    if (n == "loss") {
+        if (fast) {  // reduce the last learn launch's per-CTA loss partials now
+            fast_reduce_loss(stream_, b.loss_parts, b.lgrid_p, b.lgrid_c, cfg_.entropy_coef, b.loss);
+            FLW_CUDA(cudaStreamSynchronize(stream_));
+        }
+        return put(d2h(b.loss, 1));
+    }
     if (n == "grads") return put(d2h(b.grads, shape_.P));
     if (n == "pa" || n == "envstep") {
         auto act = d2h(b.actions + last * E_, E_);

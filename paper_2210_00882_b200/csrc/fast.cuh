@@ -63,7 +63,8 @@ size_t fast_wimg_bytes(const FastNet& n);  // bytes of the weight-tile image (sm
 size_t fast_hsave_bytes(const FastNet& n); // bytes of one tile's hidden-activation tiles
 // Builds the bf16 W^T tile image of one net from the f32 params (once per train iteration,
 // shared by every CTA of the critic-forward / learn kernels that follow).
-void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv_bfloat16* img);
+void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n0, __nv_bfloat16* img0, const FastNet& n1,
+                     __nv_bfloat16* img1);  // both nets in one launch
 // Warp-specialised two-tiles-per-SM learn kernel (kernels_learn.cu): mode 0 values pass,
 // mode 1 one train iteration of one net.
 void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid);
@@ -75,7 +76,7 @@ void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss);
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
-              double* block_sums, double* stats);
+              double* block_sums, double* stats, unsigned* done_counter = nullptr);  // counter: fused stats
 void fast_sum(cudaStream_t s, const double* x, int64_t n, double* scratch, double* out);
 void fast_rep_adv_stats(cudaStream_t s, const float* adv, int64_t T, int64_t E, const int64_t* rep_off,
                         const int64_t* rep_n, int R, double* stats);

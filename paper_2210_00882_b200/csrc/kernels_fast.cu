@@ -48,8 +48,11 @@ __host__ __device__ inline Smem carve(const FastNet& n) {
 
 // Weight-tile image: W_l^T as [dout x din] K-major bf16 core-matrix tiles, zero padded, at the
 // offsets carve() assigns; k_learn copies it into the front of its shared memory once per CTA.
-__global__ void __launch_bounds__(256) k_build_wimg(const float* __restrict__ params, FastNet n,
-                                                    __nv_bfloat16* __restrict__ img) {
+__global__ void __launch_bounds__(256) k_build_wimg(const float* __restrict__ params, FastNet n0,
+                                                    __nv_bfloat16* __restrict__ img0, FastNet n1,
+                                                    __nv_bfloat16* __restrict__ img1) {
+    const FastNet& n = blockIdx.y == 0 ? n0 : n1;  // blockIdx.y: which net (both in one launch)
+    __nv_bfloat16* img = blockIdx.y == 0 ? img0 : img1;
     const Smem S = carve(n);
     for (int l = 0; l < n.L; ++l) {
         const int di = n.din[l], dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(256, 4) k_fast_gae(const float* __restrict__ r
                                                   const float* __restrict__ done_f,
                                                   const float* __restrict__ last_value, int64_t T, int64_t R,
                                                   double gamma, double lam, float* adv, float* ret, bool with_adv,
-                                                  double* block_sums) {
+                                                  double* block_sums, double* stats, unsigned* done_counter) {
     __shared__ double s1[256], s2[256];
     int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     double a1 = 0.0, a2 = 0.0;
@@ -171,6 +174,40 @@ __global__ void __launch_bounds__(256, 4) k_fast_gae(const float* __restrict__ r
     if (threadIdx.x == 0) {
         block_sums[2 * blockIdx.x] = s1[0];
         block_sums[2 * blockIdx.x + 1] = s2[0];
+    }
+    if (!done_counter || !with_adv) return;
+    // the last block to finish combines the block sums (fixed block order -> deterministic)
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(done_counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    a1 = 0.0;
+    a2 = 0.0;
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 256) {
+        a1 += __ldcg(block_sums + 2 * b);
+        a2 += __ldcg(block_sums + 2 * b + 1);
+    }
+    s1[threadIdx.x] = a1;
+    s2[threadIdx.x] = a2;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+        if (threadIdx.x < off) {
+            s1[threadIdx.x] += s1[threadIdx.x + off];
+            s2[threadIdx.x] += s2[threadIdx.x + off];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double n = static_cast<double>(T * R);
+        const double mean = s1[0] / n;
+        const double var = s2[0] / n - mean * mean;
+        stats[0] = mean;
+        stats[1] = sqrt(var > 0.0 ? var : 0.0);
+        *done_counter = 0;  // ready for the next launch
     }
 }
 
@@ -261,8 +298,9 @@ __global__ void k_sum_blocks(const double* __restrict__ b, int n, double* out) {
 size_t fast_wimg_bytes(const FastNet& n) { return carve(n).x; }
 size_t fast_hsave_bytes(const FastNet& n) { return carve(n).hbytes; }
 
-void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n, __nv_bfloat16* img) {
-    k_build_wimg<<<148, 256, 0, s>>>(params, n, img);
+void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n0, __nv_bfloat16* img0, const FastNet& n1,
+                     __nv_bfloat16* img1) {
+    k_build_wimg<<<dim3(64, 2), 256, 0, s>>>(params, n0, img0, n1, img1);
 }
 
 
@@ -278,11 +316,11 @@ void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, d
 
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
-              double* block_sums, double* stats) {
+              double* block_sums, double* stats, unsigned* done_counter) {
     const int nb = static_cast<int>((R + 255) / 256);
     k_fast_gae<<<nb, 256, 0, s>>>(rew, values, done_f, last_value, TR / R, R, gamma, lam, adv, ret, with_adv,
-                                  block_sums);
-    if (with_adv) k_adv_stats<<<1, 256, 0, s>>>(block_sums, nb, TR, stats);
+                                  block_sums, stats, done_counter);
+    if (with_adv && !done_counter) k_adv_stats<<<1, 256, 0, s>>>(block_sums, nb, TR, stats);
 }
 
 void fast_rep_adv_stats(cudaStream_t s, const float* adv, int64_t T, int64_t E, const int64_t* rep_off,

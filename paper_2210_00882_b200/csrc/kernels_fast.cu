@@ -115,7 +115,8 @@ __global__ void k_reduce_loss(const float* __restrict__ lp, int np, int nc, doub
 // Thread per stream (rl.cpp:28-95 recurrences in double); the T-loop is processed in chunks of 8
 // steps whose loads are issued together. Per-block sums of adv and adv^2 feed the normalisation
 // statistics, combined in fixed block order by k_adv_stats.
-__global__ void __launch_bounds__(256, 4) k_fast_gae(const float* __restrict__ rew, const float* __restrict__ values,
+template <int CH, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fast_gae(const float* __restrict__ rew, const float* __restrict__ values,
                                                   const float* __restrict__ done_f,
                                                   const float* __restrict__ last_value, int64_t T, int64_t R,
                                                   double gamma, double lam, float* adv, float* ret, bool with_adv,
@@ -127,10 +128,10 @@ __global__ void __launch_bounds__(256, 4) k_fast_gae(const float* __restrict__ r
         const double gl = gamma * lam;
         const double lv = last_value[s];
         double acc = 0.0, running = lv, next_v = lv;
-        for (int64_t hi = T - 1; hi >= 0; hi -= 8) {
-            float rr[8], vv[8], dd[8];
+        for (int64_t hi = T - 1; hi >= 0; hi -= CH) {
+            float rr[CH], vv[CH], dd[CH];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < CH; ++j) {
                 int64_t tt = hi - j;
                 if (tt >= 0) {
                     int64_t i = tt * R + s;
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(256, 4) k_fast_gae(const float* __restrict__ r
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < CH; ++j) {
                 int64_t tt = hi - j;
                 if (tt < 0) break;
                 int64_t i = tt * R + s;
@@ -318,8 +319,14 @@ void fast_gae(cudaStream_t s, const float* rew, const float* values, const float
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
               double* block_sums, double* stats, unsigned* done_counter) {
     const int nb = static_cast<int>((R + 255) / 256);
-    k_fast_gae<<<nb, 256, 0, s>>>(rew, values, done_f, last_value, TR / R, R, gamma, lam, adv, ret, with_adv,
-                                  block_sums, stats, done_counter);
+    // few streams (the episode, C2: 4096): latency-bound, every step's loads issued at once;
+    // many streams (scaled sweeps): occupancy-bound, 8-step chunks at 4 blocks per SM
+    if (R <= 65536)
+        k_fast_gae<32, 1><<<nb, 256, 0, s>>>(rew, values, done_f, last_value, TR / R, R, gamma, lam, adv, ret,
+                                             with_adv, block_sums, stats, done_counter);
+    else
+        k_fast_gae<8, 4><<<nb, 256, 0, s>>>(rew, values, done_f, last_value, TR / R, R, gamma, lam, adv, ret,
+                                            with_adv, block_sums, stats, done_counter);
     if (with_adv && !done_counter) k_adv_stats<<<1, 256, 0, s>>>(block_sums, nb, TR, stats);
 }
 

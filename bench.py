@@ -327,6 +327,10 @@ def bench_ours(args, world, rank, local):
                        "l2": "per-episode working set (activations, ~0.9 GB) exceeds the 126 MB L2"},
             "episode_ms": episode_ms, "gpu_launches": stats["graph_kernels"] * args.steps,
             "clocks": clk.summary(), "e2e": e2e, "roofline": roofline, "kernel_shares": shares}
+    if "rollout" in probes:  # "also report rollout-only"
+        r_ms = sum(probes["rollout"])
+        line["rollout_only"] = {"value": total * T_STEPS / (r_ms * 1e-3), "unit": "env-steps/s",
+                                "ms_per_episode": r_ms, "note": "Reset + 32 fused policy/env steps, per GPU x N"}
     if not args.no_microbench:
         line["hbm_kernels"] = hbm_microbenchmarks(peaks)
     if world == 1 and not args.no_cpu_baseline:

@@ -74,3 +74,33 @@ def test_last_error_is_thread_local():
     t2 = threading.Thread(target=bad, args=("b", {"algorithm": "ppo", "env": {"type": "nope"}}))
     t1.start(), t2.start(), t1.join(), t2.join()
     assert errs["a"].startswith("ConfigError") and errs["b"].startswith("UnknownEnv")
+
+
+def test_engine_fails_loudly_without_a_gpu():
+    """The product path has no CPU fallback: creating an engine or running a program on a host
+    without a visible CUDA device returns a runtime error through the ABI."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    from paper_2210_00882_b200 import DpdEngine
+
+    algo = {"algorithm": "ppo", "env": {"type": "gridline", "num": 4}}
+    with pytest.raises(FlwError) as ei:
+        DpdEngine(algo, numerics="exact")
+    assert ei.value.code == N.FLW_ERR_RUNTIME
+    with pytest.raises(FlwError) as ei:
+        DpdEngine(algo, numerics="fast", replicas=2)
+    assert ei.value.code == N.FLW_ERR_RUNTIME
+    p = Program(algo, {"distribution_policy": "dp-d"})
+    with pytest.raises(FlwError) as ei:
+        p.run_local(seed=1)
+    assert ei.value.code == N.FLW_ERR_RUNTIME and "no CUDA device" in ei.value.message
+
+
+def test_deploy_extension_keys_are_accepted_and_validated():
+    algo = {"algorithm": "ppo", "env": {"type": "gridline", "num": 8}, "actor": {"num": 4}}
+    p = Program(algo, {"distribution_policy": "dp-d", "slots_per_worker": {"cpu": 4, "accel": 4},
+                       "numerics": "fast", "replicas_per_gpu": 2, "exchange": "nccl"})
+    # the plan itself is the reference's (the extension keys only steer the engine)
+    assert len(json.loads(p.dump())["instances"]) == 4

@@ -57,11 +57,10 @@ __global__ void __launch_bounds__(256) k_reduce_push(P2pArgs a) {
     }
     ws[w][lane] = s;
     __syncthreads();
-    if (w < a.k) {  // warp r pushes the chunk to rank r
-        float t = 0.0f;
+    float t = 0.0f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) t += ws[k][lane];
-        const int r = w;
+    for (int k = 0; k < 8; ++k) t += ws[k][lane];
+    for (int r = w; r < a.k; r += 8) {  // warp w pushes the chunk to ranks w, w+8, ...
         // inbox[epoch & 1]: rank r may still be reading the previous exchange's buffer
         float* inbox = reinterpret_cast<float*>(a.peers[r] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
         if (ok) inbox[static_cast<int64_t>(a.rank) * P + i] = t;
@@ -82,8 +81,8 @@ __global__ void __launch_bounds__(32) k_sum_adam(P2pArgs a) {
     const uint64_t epoch = a.ctx->coll_seq;
     const int64_t P = a.Pp + a.Pc;
     const uint64_t* flag = reinterpret_cast<const uint64_t*>(a.peers[a.rank] + a.off_sflag) + static_cast<int64_t>(c) * a.k;
-    if (lane < a.k)
-        while (ld_acquire_sys(flag + lane) < epoch) __nanosleep(32);
+    for (int r = lane; r < a.k; r += 32)
+        while (ld_acquire_sys(flag + r) < epoch) __nanosleep(32);
     __syncwarp();
     const int64_t i = 32LL * c + lane;
     if (i >= P) return;

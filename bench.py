@@ -275,10 +275,21 @@ def bench_ours(args, world, rank, local):
         dist.broadcast_object_list(obj, src=0)
         eng.comm_init(obj[0], rank, world)
         if args.numerics == "fast" and args.exchange == "p2p":
-            # gradient exchange over NVLink peer memory (CUDA IPC), fused with reduce + Adam
-            hs = [None] * world
-            dist.all_gather_object(hs, eng.p2p_export(world))
-            eng.p2p_import(hs, rank)
+            # gradient exchange over NVLink peer memory (CUDA IPC), fused with reduce + Adam;
+            # the group falls back to NCCL together if any rank cannot map its peers
+            ok = True
+            try:
+                hs = [None] * world
+                dist.all_gather_object(hs, eng.p2p_export(world))
+                eng.p2p_import(hs, rank)
+            except Exception as exc:  # noqa: BLE001
+                print(f"rank {rank}: peer-memory exchange unavailable ({exc}); using NCCL", file=sys.stderr)
+                ok = False
+            oks = [None] * world
+            dist.all_gather_object(oks, ok)
+            if not all(oks):
+                eng.p2p_disable()
+                args.exchange = "nccl"
     # warm-up (also captures the episode graph, with CUDA-event probes around the main kernels)
     eng.enable_probes(True)
     eng.run_episodes(0, args.warmup)

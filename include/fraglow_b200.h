@@ -99,6 +99,8 @@ int flw_dpd_comm_init(flw_dpd* e, const char* id, int64_t id_len, int rank, int 
  * order and every rank imports them. */
 int flw_dpd_p2p_export(flw_dpd* e, int nranks, char* out_handle, int64_t cap);
 int flw_dpd_p2p_import(flw_dpd* e, const char* handles, int64_t len, int rank, int nranks);
+/* Back to the NCCL exchange (every rank of the group must make the same choice). */
+int flw_dpd_p2p_disable(flw_dpd* e);
 
 /* One whole episode (Reset, T x Step, I x Learn) as a replayed CUDA graph. reward_sum is the
  * episode's summed env reward over this unit's envs (interp.cpp:257); device_ms the graph time. */

@@ -60,6 +60,7 @@ def lib():
         "flw_dpd_replica_rewards": (ci, [vp, P(C.c_double), i64]),
         "flw_dpd_p2p_export": (ci, [vp, ci, C.c_char_p, i64]),
         "flw_dpd_p2p_import": (ci, [vp, C.c_char_p, i64, ci, ci]),
+        "flw_dpd_p2p_disable": (ci, [vp]),
         "flw_dpd_destroy": (ci, [vp]),
         "flw_dpd_comm_unique_id": (ci, [C.c_char_p, i64]),
         "flw_dpd_comm_init": (ci, [vp, C.c_char_p, i64, ci, ci]),

@@ -122,6 +122,9 @@ class DpdEngine:
         blob = b"".join(handles)
         N.check(N.lib().flw_dpd_p2p_import(self._h, blob, len(blob), rank, len(handles)))
 
+    def p2p_disable(self):
+        N.check(N.lib().flw_dpd_p2p_disable(self._h))
+
     def comm_init(self, uid: bytes, rank: int, nranks: int):
         N.check(N.lib().flw_dpd_comm_init(self._h, uid, len(uid), rank, nranks))
 

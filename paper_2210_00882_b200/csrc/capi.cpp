@@ -431,6 +431,13 @@ int flw_dpd_p2p_import(flw_dpd* e, const char* handles, int64_t len, int rank, i
     });
 }
 
+int flw_dpd_p2p_disable(flw_dpd* e) {
+    return guarded([&] {
+        eng(e).disable_p2p();
+        return FLW_OK;
+    });
+}
+
 int flw_dpd_comm_init(flw_dpd* e, const char* id, int64_t id_len, int rank, int nranks) {
     return guarded([&] {
         Engine& en = eng(e);

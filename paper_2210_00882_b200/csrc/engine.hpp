@@ -57,6 +57,10 @@ class Engine {
     void adopt_ipc_mapping(void* p) { p2p_ipc_opened_.push_back(p); }  // closed by the destructor
     void set_p2p_peers(int rank, int k, const std::vector<void*>& regions);
     bool p2p_enabled() const { return p2p_k_ > 1; }
+    void disable_p2p() {  // back to the NCCL exchange (the group must agree; see bench.py)
+        destroy_graph();
+        p2p_k_ = 0;
+    }
     void set_eager_collectives(bool on);
     void prepare();  // captures the episode graph now (before any peer launches its own)
 

@@ -228,9 +228,15 @@ def cpu_baseline(target_s: float = 12.0) -> dict:
     envs, k = reference_sample(cores, target_s)
     r = run_reference(envs, k, episodes=1)
     ms = sum(e["wall_ms"] for e in r["episodes"])
+    # the same path on ONE core (one dp-d unit), bounded sample
+    e1 = int(max(8, min(ENVS_PER_GPU, round(0.4 * target_s / 0.023))))
+    r1 = run_reference(e1, 1, episodes=1)
+    ms1 = sum(e["wall_ms"] for e in r1["episodes"])
     return {"value": envs * T_STEPS * len(r["episodes"]) / (ms / 1e3), "unit": "env-steps/s", "cores": cores,
             "kind": "reference",
-            "sample": f"1 episode of C2 at {envs} envs (dp-d, {k} replica threads), {ms / 1e3:.1f} s"}
+            "sample": f"1 episode of C2 at {envs} envs (dp-d, {k} replica threads), {ms / 1e3:.1f} s",
+            "single_core": {"value": e1 * T_STEPS / (ms1 / 1e3), "unit": "env-steps/s", "cores": 1,
+                            "sample": f"1 episode of C2 at {e1} envs (dp-d, 1 unit), {ms1 / 1e3:.1f} s"}}
 
 
 def bench_reference(args, world, rank):

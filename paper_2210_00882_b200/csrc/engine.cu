@@ -119,8 +119,8 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     mappo_ = shape_.algo == Algo::Mappo;
     if (mappo_ && shape_.env != EnvKind::SpreadLite)
         fail(Errc::PolicyInapplicable, "MAPPO runs on spread_lite (the reference's multi-agent env)");
-    if (mappo_ && numerics == Numerics::Fast)
-        fail(Errc::Config, "MAPPO is served with numerics=exact in this build");
+    if (mappo_ && numerics == Numerics::Fast && (shape_.crit_in > 64 || shape_.obs_dim > 64))
+        fail(Errc::Config, "fast MAPPO needs critic inputs <= 64 wide (2n^2+3n: n <= 4); use numerics=exact");
     if (mappo_ && shape_.n_agents > 64) fail(Errc::Config, "at most 64 agents");
     if (!mappo_ && shape_.env == EnvKind::SpreadLite)
         fail(Errc::PolicyInapplicable, "PPO/A3C need a single-agent env (spread_lite is multi-agent)");
@@ -279,6 +279,8 @@ void Engine::alloc() {
         // compact critic: [joint | one-hot] rows are never materialised (n x smaller; n=64,
         // E=2048 would need 145 GB), layer 0 reads the joint prefix chains + W[J+a]
         b.cprefix = b.alloc<double>((T_ + 1) * E_ * s.cdims[1]);
+        // fast numerics (n <= 4): the tensor-core learn kernels read [joint | one-hot] rows
+        if (numerics_ == Numerics::Fast) b.cin = b.alloc<float>((T_ + 1) * R_ * s.crit_in);
     }
     b.adv = b.alloc<float>(TR_);
     b.ret = b.alloc<float>(TR_);
@@ -551,7 +553,7 @@ void Engine::enq_rollout_fast(int64_t step0, int64_t nsteps) {
 }
 
 void Engine::enq_step(int64_t st) {
-    if (numerics_ == Numerics::Fast) return enq_rollout_fast(st, 1);
+    if (numerics_ == Numerics::Fast && !mappo_) return enq_rollout_fast(st, 1);
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions;
@@ -634,7 +636,11 @@ void Engine::enq_learn_fast() {
     f.wimg = b.wimg_c;
     f.kind = kNetCritic;
     f.mode = 0;
-    f.X = b.states;
+    // critic rows: the states (PPO/A3C) or [joint | one-hot] per agent row (MAPPO, n <= 4)
+    const float* Xc = mappo_ ? b.cin : b.states;
+    const int Cin = mappo_ ? s.crit_in : S;
+    f.X = Xc;
+    f.in_cols = Cin;
     f.rows = TR_;
     // states block T (= last_next) directly follows the T*E trajectory rows, so ONE launch over
     // T*E + E rows yields values and last_value (values_out rows >= T*E go to last_value).
@@ -664,6 +670,7 @@ void Engine::enq_learn_fast() {
     // learn: policy then critic, each a persistent fused kernel
     f.mode = 1;
     f.X = b.states;
+    f.in_cols = S;
     f.rows = TR_;
     f.actions = b.actions;
     f.logp_old = b.logp;
@@ -696,6 +703,8 @@ void Engine::enq_learn_fast() {
     launch(gp);
     probe_end();
     FastLearnArgs fc = f;
+    fc.X = Xc;
+    fc.in_cols = Cin;
     fc.net = b.crit;
     fc.wimg = b.wimg_c;
     fc.hsave = hreuse ? b.hsave : nullptr;  // same params as the values pass: same activations
@@ -941,9 +950,9 @@ void Engine::build_graph() {
     enq_reset();
     trace_capture("reset");
     probe_begin("rollout");
-    if (numerics_ == Numerics::Fast)
+    if (numerics_ == Numerics::Fast && !mappo_)
         enq_rollout_fast(0, T_);
-    else
+    else  // exact rollout (also fast MAPPO: the multi-agent rollout is the exact one)
         for (int64_t st = 0; st < T_; ++st) enq_step(st);
     probe_end();
     if (nrep_ > 1 && numerics_ == Numerics::Exact) enq_permute_replicas();

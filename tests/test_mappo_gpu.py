@@ -73,3 +73,38 @@ def test_mappo_episodes_match_oracle(n_agents):
     got = [eng.run_episode(ep)[0] / 16 for ep in range(3)]
     _close("rewards", got, rew)
     _close("params", eng.params(), par)
+
+
+@pytest.mark.parametrize("n_agents", [3, 4])
+def test_fast_mappo_tracks_exact(n_agents):
+    """Fast numerics for MAPPO (n <= 4, critic input 2n^2+3n <= 64): the exact multi-agent
+    rollout + the tensor-core learn kernels over [joint | one-hot] rows. The first episode's
+    rollout is bit-exact (same parameters, exact rollout); afterwards the bf16 learn keeps the
+    trained parameters close to the exact run."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2210_00882_b200 import DpdEngine
+
+    algo = {"algorithm": "mappo", "agent": {"num": n_agents},
+            "env": {"type": "spread_lite", "num": 256, "params": {"accel": 1}},
+            "policy_net": {"hidden": [64, 64]}, "loop": {"episodes": 4, "steps_per_episode": 16}}
+    ex = DpdEngine(algo, seed=5, numerics="exact")
+    fa = DpdEngine(algo, seed=5, numerics="fast")
+    r_ex = [ex.run_episode(ep)[0] for ep in range(4)]
+    r_fa = [fa.run_episode(ep)[0] for ep in range(4)]
+    # identical rollout before any learning (the reward sum itself is a parallel sum in fast mode)
+    assert r_fa[0] == pytest.approx(r_ex[0], rel=1e-12)
+    np.testing.assert_allclose(r_fa, r_ex, rtol=5e-2)
+    p_ex, p_fa = np.asarray(ex.params()), np.asarray(fa.params())
+    rel = np.linalg.norm(p_fa - p_ex) / np.linalg.norm(p_ex)
+    assert rel < 2e-2, rel
+
+
+def test_fast_mappo_refuses_wide_critic():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2210_00882_b200 import DpdEngine, FlwError
+
+    algo = {"algorithm": "mappo", "agent": {"num": 8}, "env": {"type": "spread_lite", "num": 16, "params": {"accel": 1}}}
+    with pytest.raises(FlwError):
+        DpdEngine(algo, seed=5, numerics="fast")

@@ -38,15 +38,17 @@ def ref_point(n: int, envs: int, seed: int) -> dict:
             "env_steps_per_s": envs * 32 / (ms * 1e-3)}
 
 
-def ours_point(n: int, envs: int, episodes: int, seed: int) -> dict:
+def ours_point(n: int, envs: int, episodes: int, seed: int, numerics: str = "exact") -> dict:
     from paper_2210_00882_b200 import Program
 
     prog = Program(algo(n, envs, episodes), {"workers": ["local"], "slots_per_worker": {"cpu": 1, "accel": 1},
-                                             "distribution_policy": "dp-d", "numerics": "exact"})
+                                             "distribution_policy": "dp-d", "numerics": numerics})
     prog.run_local(seed=seed, episodes=1)  # engine build + graph capture
     csv, _ = prog.run_local(seed=seed)
     ms = statistics.median(float(l.split(",")[1]) for l in csv.strip().split("\n")[1:])
-    return {"arm": "ours dp-d fused, 1 x B200, numerics=exact (compact critic)", "agents": n, "envs": envs,
+    arm = ("ours dp-d fused, 1 x B200, numerics=exact (compact critic)" if numerics == "exact" else
+           "ours dp-d fused, 1 x B200, numerics=fast (exact rollout, tensor-core learn)")
+    return {"arm": arm, "agents": n, "envs": envs,
             "episode_ms": ms, "env_steps_per_s": envs * 32 / (ms * 1e-3)}
 
 
@@ -64,6 +66,8 @@ def main():
             print(json.dumps({"config": "C3", **ours_point(n, envs, a.episodes, a.seed)}), flush=True)
     for n in (int(x) for x in a.agents.split(",")):
         print(json.dumps({"config": "C3", **ours_point(n, a.envs, a.episodes, a.seed)}), flush=True)
+        if 2 * n * n + 3 * n <= 64:  # fast numerics: critic input [joint | one-hot] <= 64 wide
+            print(json.dumps({"config": "C3", **ours_point(n, a.envs, a.episodes, a.seed, "fast")}), flush=True)
 
 
 if __name__ == "__main__":

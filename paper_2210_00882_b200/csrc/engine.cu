@@ -347,7 +347,7 @@ void Engine::alloc() {
         b.grid2 = static_cast<int>(std::min<int64_t>(sms, ((TR_ + 127) / 128 + 1) / 2));
         b.hscratch = b.alloc<uint8_t>(static_cast<int64_t>(
             std::max(fast_learn_scratch_bytes(b.pol), fast_learn_scratch_bytes(b.crit)) * 2 * b.grid2));
-        b.block_sums = b.alloc<double>(2 * ((R_ + 255) / 256));
+        b.block_sums = b.alloc<double>(2 * ((R_ + 31) / 32));  // per GAE block (32 or 256 streams)
         b.gae_counter = b.alloc<unsigned>(1);
         b.rsum_scratch = b.alloc<double>(256);
         b.values = b.alloc<float>(TR_);

@@ -240,6 +240,129 @@ __global__ void __launch_bounds__(256) k_adv_stats(const double* __restrict__ bl
     }
 }
 
+// Warp-shuffle reverse scan (T = 32, the reference default): one block = 32 streams x 32 steps.
+// The [T][R] tile is staged through shared memory (coalesced rows), then warp w owns stream w
+// with lane = step t. Both recurrences are affine, x_t = b_t + a_t x_{t+1} (rl.cpp:28-47, 66-79:
+// GAE a_t = (1 - done_t) gamma lambda, returns a_t = (1 - done_t) gamma), so a 5-step shuffle
+// scan of (a, b) pairs replaces the 32-step chain. Double precision, like the sequential kernel.
+__device__ __forceinline__ void rscan_affine(double& a, double& b, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double an = __shfl_down_sync(0xffffffffu, a, off);
+        const double bn = __shfl_down_sync(0xffffffffu, b, off);
+        if (lane + off < 32) {
+            b = b + a * bn;
+            a = a * an;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_gae_scan32(const float* __restrict__ rew, const float* __restrict__ values,
+                                                     const float* __restrict__ done_f,
+                                                     const float* __restrict__ last_value, int64_t R, double gamma,
+                                                     double lam, float* adv, float* ret, bool with_adv,
+                                                     double* block_sums, double* stats, unsigned* done_counter) {
+    __shared__ float sr[32][33], sv[32][33], sd[32][33];
+    __shared__ double w1[32], w2[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * 32;
+    {  // coalesced staging: warp w loads step t = w of the block's 32 streams
+        const int64_t i = static_cast<int64_t>(w) * R + s0 + lane;
+        const bool ok = s0 + lane < R;
+        sr[w][lane] = ok ? rew[i] : 0.0f;
+        sv[w][lane] = ok ? values[i] : 0.0f;
+        sd[w][lane] = ok ? done_f[i] : 1.0f;
+    }
+    __syncthreads();
+    const int64_t st = s0 + w;  // this warp's stream; lane = step t
+    const bool live = st < R;
+    const int t = lane;
+    const bool done = sd[t][w] > 0.5f;
+    const double r = sr[t][w], v = sv[t][w];
+    const double lv = live ? static_cast<double>(last_value[st]) : 0.0;
+    const double vnext = t == 31 ? lv : static_cast<double>(sv[t + 1][w]);
+    // GAE: acc_t = delta_t + (done_t ? 0 : gamma lambda) acc_{t+1}, acc_32 = 0
+    double a = done ? 0.0 : gamma * lam;
+    double b = (r + gamma * (done ? 0.0 : vnext)) - v;
+    rscan_affine(a, b, lane);
+    const double acc = b;  // + a * 0
+    // returns: run_t = r_t + (done_t ? 0 : gamma) run_{t+1}, run_32 = last_value
+    double ar = done ? 0.0 : gamma, br = r;
+    rscan_affine(ar, br, lane);
+    const double run = br + ar * lv;
+    __syncthreads();
+    sr[t][w] = static_cast<float>(run);  // reuse the tiles for the transposed stores
+    sv[t][w] = static_cast<float>(acc);
+    double a1 = (live && with_adv) ? acc : 0.0, a2 = a1 * a1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+        a2 += __shfl_xor_sync(0xffffffffu, a2, off);
+    }
+    if (lane == 0) {
+        w1[w] = a1;
+        w2[w] = a2;
+    }
+    __syncthreads();
+    {
+        const int64_t i = static_cast<int64_t>(w) * R + s0 + lane;
+        if (s0 + lane < R) {
+            ret[i] = sr[w][lane];
+            if (with_adv) adv[i] = sv[w][lane];
+        }
+    }
+    if (w == 0) {  // block sums in warp order, then the last block combines them (fixed order)
+        double b1 = w1[lane], b2 = w2[lane];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            b1 += __shfl_xor_sync(0xffffffffu, b1, off);
+            b2 += __shfl_xor_sync(0xffffffffu, b2, off);
+        }
+        if (lane == 0) {
+            block_sums[2 * blockIdx.x] = b1;
+            block_sums[2 * blockIdx.x + 1] = b2;
+        }
+    }
+    if (!done_counter || !with_adv) return;
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(done_counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double c1 = 0.0, c2 = 0.0;
+    for (int k = threadIdx.x; k < static_cast<int>(gridDim.x); k += 1024) {
+        c1 += __ldcg(block_sums + 2 * k);
+        c2 += __ldcg(block_sums + 2 * k + 1);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        c1 += __shfl_xor_sync(0xffffffffu, c1, off);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, off);
+    }
+    __syncthreads();
+    if (lane == 0) {
+        w1[w] = c1;
+        w2[w] = c2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t1 = 0.0, t2 = 0.0;
+        for (int k = 0; k < 32; ++k) {
+            t1 += w1[k];
+            t2 += w2[k];
+        }
+        const double n = static_cast<double>(32 * R);
+        const double mean = t1 / n;
+        const double var = t2 / n - mean * mean;
+        stats[0] = mean;
+        stats[1] = sqrt(var > 0.0 ? var : 0.0);
+        *done_counter = 0;
+    }
+}
+
 // Per-replica advantage statistics (R units folded into one engine, each normalising over its
 // own T*E_r rows like its own interpreter, rl.cpp:97-107): one CTA per replica, fixed order.
 __global__ void __launch_bounds__(256) k_rep_adv_stats(const float* __restrict__ adv, int64_t T, int64_t E,
@@ -318,9 +441,18 @@ void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, d
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
               double* block_sums, double* stats, unsigned* done_counter) {
+    // T = 32 with few streams (the episode: latency-bound): warp-shuffle reverse scan, lane = step.
+    // Many streams (bandwidth-bound sweeps): the chunked thread-per-stream recurrence, which needs
+    // no shuffles (the scan's 40 shuffles per stream would cap it at ~20% of HBM bandwidth).
+    if (TR == 32 * R && done_counter && R <= 65536) {
+        const int nb32 = static_cast<int>((R + 31) / 32);
+        k_gae_scan32<<<nb32, 1024, 0, s>>>(rew, values, done_f, last_value, R, gamma, lam, adv, ret, with_adv,
+                                           block_sums, stats, done_counter);
+        return;
+    }
     const int nb = static_cast<int>((R + 255) / 256);
-    // few streams (the episode, C2: 4096): latency-bound, every step's loads issued at once;
-    // many streams (scaled sweeps): occupancy-bound, 8-step chunks at 4 blocks per SM
+    // few streams: latency-bound, every step's loads issued at once; many streams (scaled
+    // sweeps): occupancy-bound, 8-step chunks at 4 blocks per SM
     if (R <= 65536)
         k_fast_gae<32, 1><<<nb, 256, 0, s>>>(rew, values, done_f, last_value, TR / R, R, gamma, lam, adv, ret,
                                              with_adv, block_sums, stats, done_counter);

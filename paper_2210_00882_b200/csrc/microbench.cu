@@ -127,14 +127,17 @@ void microbench(const std::string& which, int64_t n, int iters, double* ms, doub
         float* lv = d.get<float>(R);
         float* adv = d.get<float>(T * R);
         float* ret = d.get<float>(T * R);
-        double* bs = d.get<double>(2 * ((R + 255) / 256));
+        double* bs = d.get<double>(2 * ((R + 31) / 32));
         double* st = d.get<double>(2);
+        unsigned* cnt = d.get<unsigned>(1);
+        FLW_CUDA(cudaMemset(cnt, 0, sizeof(unsigned)));
         k_init_f32<<<g, blk>>>(r, T * R, 1, -1.f, 1.f);
         k_init_f32<<<g, blk>>>(v, T * R, 2, -1.f, 1.f);
         k_init_f32<<<g, blk>>>(dn, T * R, 3, -18.f, 1.f);  // > 0.5 with probability ~0.03 (done)
         k_init_f32<<<g, blk>>>(lv, R, 4, -1.f, 1.f);
         FLW_CUDA(cudaGetLastError());
-        *ms = time_launches([&] { fast_gae(0, r, v, dn, lv, T * R, R, 0.99, 0.95, adv, ret, true, bs, st); }, iters);
+        *ms = time_launches([&] { fast_gae(0, r, v, dn, lv, T * R, R, 0.99, 0.95, adv, ret, true, bs, st, cnt); },
+                            iters);
         *bytes = static_cast<double>(T * R) * 20.0 + static_cast<double>(R) * 4.0;
     } else if (which == "adam") {
         float* p = d.get<float>(n);

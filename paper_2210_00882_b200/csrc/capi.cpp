@@ -178,7 +178,8 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
             Comm::connect_all(cs, devs, static_cast<int64_t>(R) * p.engines[0]->shape().P);
             // fast numerics, one unit per GPU: gradient exchange over NVLink peer memory when
             // every pair of GPUs can address each other (deploy "exchange": "nccl" opts out)
-            bool p2p = p.numerics == Numerics::Fast && R == 1 && p.exchange != "nccl";
+            bool p2p = p.exchange != "nccl";
+            for (auto& e : p.engines) p2p = p2p && e->p2p_capable();
             for (int a = 0; p2p && a < ng; ++a)
                 for (int b2 = 0; p2p && b2 < ng; ++b2) {
                     int ok = 0;

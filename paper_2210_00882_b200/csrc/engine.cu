@@ -10,6 +10,8 @@
 //   params  f32 [P], m/v f64 [P], grads f32 [P]   flat, reference parameter order
 #include "engine.hpp"
 
+#include <cublas_v2.h>
+
 #include <cmath>
 #include <cstddef>
 #include <cstring>
@@ -57,6 +59,10 @@ struct Engine::Bufs {
     // MAPPO: joint observation blocks [(T+1), E, W] and critic input rows [(T+1), n*E, W+n]
     float *joint = nullptr, *cin = nullptr;
     double* cprefix = nullptr;  // MAPPO compact critic: joint prefix chains [(T+1)*E, H0]
+    // fast MAPPO compact critic (n > 4): joint GEMM, layer-0 rows, input gradients, per-env sums
+    float *h0 = nullptr, *cP = nullptr, *dz0 = nullptr, *cS = nullptr;
+    cublasHandle_t blas = nullptr;
+    uint8_t* blas_ws = nullptr;
     // fast numerics
     FastNet pol{}, crit{};
     int grid = 0;                       // persistent CTAs of the fused learn kernel
@@ -88,9 +94,17 @@ struct Engine::Bufs {
         return static_cast<T*>(p);
     }
     ~Bufs() {
+        if (blas) cublasDestroy(blas);
         for (void* p : owned) cudaFree(p);
     }
 };
+
+#define FLW_CUBLAS(x)                                                                          \
+    do {                                                                                       \
+        cublasStatus_t st_ = (x);                                                              \
+        if (st_ != CUBLAS_STATUS_SUCCESS)                                                      \
+            throw ::flw::Error(::flw::Errc::Runtime, "cuBLAS error " + std::to_string(st_));  \
+    } while (0)
 
 namespace {
 
@@ -119,8 +133,11 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     mappo_ = shape_.algo == Algo::Mappo;
     if (mappo_ && shape_.env != EnvKind::SpreadLite)
         fail(Errc::PolicyInapplicable, "MAPPO runs on spread_lite (the reference's multi-agent env)");
-    if (mappo_ && numerics == Numerics::Fast && (shape_.crit_in > 64 || shape_.obs_dim > 64))
-        fail(Errc::Config, "fast MAPPO needs critic inputs <= 64 wide (2n^2+3n: n <= 4); use numerics=exact");
+    if (mappo_ && numerics == Numerics::Fast && shape_.obs_dim > 64)
+        fail(Errc::Config, "fast MAPPO needs per-agent observations <= 64 wide (n <= 31); use numerics=exact");
+    // fast MAPPO with a critic input wider than the fused kernel's 64 columns (n > 4): the
+    // compact critic - layer 0 as a joint GEMM once per env + W[J+a], the rest fused
+    cfast_ = mappo_ && numerics == Numerics::Fast && shape_.crit_in > 64;
     if (mappo_ && shape_.n_agents > 64) fail(Errc::Config, "at most 64 agents");
     if (!mappo_ && shape_.env == EnvKind::SpreadLite)
         fail(Errc::PolicyInapplicable, "PPO/A3C need a single-agent env (spread_lite is multi-agent)");
@@ -186,7 +203,7 @@ void Engine::set_eager_collectives(bool on) {
 int64_t Engine::p2p_region_bytes() const { return p2p_layout(p2p_k_ > 0 ? p2p_k_ : 1, shape_.P).bytes; }
 
 void* Engine::p2p_region() {
-    if (numerics_ != Numerics::Fast || nrep_ > 1)
+    if (numerics_ != Numerics::Fast || nrep_ > 1 || cfast_)
         fail(Errc::Config, "the peer-memory exchange serves fast numerics with one unit per GPU");
     if (!p2p_region_ptr_) fail(Errc::Config, "call set_p2p_group first (region size depends on k)");
     return p2p_region_ptr_;
@@ -205,7 +222,7 @@ void Engine::set_p2p_peers(int rank, int k, const std::vector<void*>& regions) {
 
 void Engine::alloc_p2p_region(int k) {
     FLW_CUDA(cudaSetDevice(device_));
-    if (numerics_ != Numerics::Fast || nrep_ > 1)
+    if (numerics_ != Numerics::Fast || nrep_ > 1 || cfast_)
         fail(Errc::Config, "the peer-memory exchange serves fast numerics with one unit per GPU");
     const P2pLayout L = p2p_layout(k, shape_.P);
     if (!p2p_region_ptr_) {
@@ -280,7 +297,7 @@ void Engine::alloc() {
         // E=2048 would need 145 GB), layer 0 reads the joint prefix chains + W[J+a]
         b.cprefix = b.alloc<double>((T_ + 1) * E_ * s.cdims[1]);
         // fast numerics (n <= 4): the tensor-core learn kernels read [joint | one-hot] rows
-        if (numerics_ == Numerics::Fast) b.cin = b.alloc<float>((T_ + 1) * R_ * s.crit_in);
+        if (numerics_ == Numerics::Fast && !cfast_) b.cin = b.alloc<float>((T_ + 1) * R_ * s.crit_in);
     }
     b.adv = b.alloc<float>(TR_);
     b.ret = b.alloc<float>(TR_);
@@ -316,17 +333,18 @@ void Engine::alloc() {
     }
     if (numerics_ == Numerics::Fast) {
         // Fused tensor-core learn kernels: per-CTA dW partials replace the per-layer activations.
-        auto make_net = [&](int net) {
+        auto make_net = [&](int net, int first = 0) {  // layers [first, L) of the net
             const auto& d = net == 0 ? s.pdims : s.cdims;
             FastNet n{};
-            n.L = L;
-            for (int l = 0; l < L; ++l) {
-                n.rin[l] = d[l];
-                n.rout[l] = d[l + 1];
-                n.din[l] = (d[l] + 15) / 16 * 16;
-                n.dout[l] = (d[l + 1] + 15) / 16 * 16;
-                n.woff[l] = s.woff[net][l];
-                n.boff[l] = s.boff[net][l];
+            n.L = L - first;
+            for (int l = 0; l < n.L; ++l) {
+                const int ll = l + first;
+                n.rin[l] = d[ll];
+                n.rout[l] = d[ll + 1];
+                n.din[l] = (d[ll] + 15) / 16 * 16;
+                n.dout[l] = (d[ll + 1] + 15) / 16 * 16;
+                n.woff[l] = s.woff[net][ll];
+                n.boff[l] = s.boff[net][ll];
                 if (n.din[l] > 64 || n.dout[l] > 64)
                     fail(Errc::Config, "fast numerics supports MLP widths up to 64 (use numerics=exact)");
             }
@@ -334,7 +352,21 @@ void Engine::alloc() {
         };
         if (L > kMaxLayers) fail(Errc::Config, "fast numerics supports at most 8 layers");
         b.pol = make_net(0);
-        b.crit = make_net(1);
+        if (cfast_) {
+            if (L < 2 || s.cdims[1] > 64) fail(Errc::Config, "compact fast critic needs >= 2 layers, hidden <= 64");
+            b.crit = make_net(1, 1);  // the critic without its layer 0
+            const int H0 = s.cdims[1];
+            b.h0 = b.alloc<float>((T_ + 1) * R_ * H0);
+            b.cP = b.alloc<float>((T_ + 1) * E_ * H0);
+            b.dz0 = b.alloc<float>(TR_ * H0);
+            b.cS = b.alloc<float>(T_ * E_ * H0);
+            FLW_CUBLAS(cublasCreate(&b.blas));
+            FLW_CUBLAS(cublasSetMathMode(b.blas, CUBLAS_TF32_TENSOR_OP_MATH));
+            b.blas_ws = b.alloc<uint8_t>(32 << 20);
+            FLW_CUBLAS(cublasSetWorkspace(b.blas, b.blas_ws, 32 << 20));
+        } else {
+            b.crit = make_net(1);
+        }
         int sms = 0;
         FLW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         b.grid = static_cast<int>(std::min<int64_t>(sms, (TR_ + 127) / 128));
@@ -636,9 +668,20 @@ void Engine::enq_learn_fast() {
     f.wimg = b.wimg_c;
     f.kind = kNetCritic;
     f.mode = 0;
-    // critic rows: the states (PPO/A3C) or [joint | one-hot] per agent row (MAPPO, n <= 4)
-    const float* Xc = mappo_ ? b.cin : b.states;
-    const int Cin = mappo_ ? s.crit_in : S;
+    // critic rows: the states (PPO/A3C), [joint | one-hot] per agent row (MAPPO, n <= 4), or
+    // the compact critic's layer-0 activations (MAPPO, n > 4)
+    const int H0 = s.cdims[1], J = s.state_w;
+    if (cfast_) {
+        // P[(T+1)*E, H0] = joint . W_J  (row-major; cuBLAS column-major: P^T = W_J^T . joint^T)
+        const float one = 1.0f, zero = 0.0f;
+        FLW_CUBLAS(cublasSetStream(b.blas, stream_));
+        FLW_CUBLAS(cublasSgemm(b.blas, CUBLAS_OP_N, CUBLAS_OP_N, H0, static_cast<int>((T_ + 1) * E_), J, &one,
+                               b.params + s.woff[1][0], H0, b.joint, J, &zero, b.cP, H0));
+        mappo_fast_h0(stream_, b.cP, b.params + s.woff[1][0], b.params + s.boff[1][0], T_ + 1, E_, s.n_agents, J, H0,
+                      act_of(cfg_), b.h0);
+    }
+    const float* Xc = cfast_ ? b.h0 : (mappo_ ? b.cin : b.states);
+    const int Cin = cfast_ ? H0 : (mappo_ ? s.crit_in : S);
     f.X = Xc;
     f.in_cols = Cin;
     f.rows = TR_;
@@ -711,7 +754,10 @@ void Engine::enq_learn_fast() {
     fc.hload = hreuse ? 1 : 0;
     fc.kind = kNetCritic;
     fc.partials = b.part_c;
-    fc.part_stride = s.P - s.P_policy;
+    // compact critic: the fused kernel owns layers 1.. (and reports dZ wrt its input rows)
+    const int64_t c_off = cfast_ ? static_cast<int64_t>(J + s.n_agents) * H0 + H0 : 0;
+    fc.part_stride = s.P - s.P_policy - c_off;
+    fc.dx_out = cfast_ ? b.dz0 : nullptr;
     fc.loss_partials = b.loss_parts + 3 * gp;
     if (concurrent) {
         fast_learn(side2_, fc, gc);
@@ -726,8 +772,17 @@ void Engine::enq_learn_fast() {
     b.lgrid_c = gc;
     if (!p2p_enabled()) {  // with peer-memory exchange the reduction is fused into the exchange
         probe_begin("reduce");
-        fast_reduce_partials(stream_, b.part_p, b.part_c, gp, gc, s.P_policy, s.P - s.P_policy, b.grads);
+        fast_reduce_partials(stream_, b.part_p, b.part_c, gp, gc, s.P_policy, s.P - s.P_policy - c_off, b.grads,
+                             c_off);
         probe_end();
+    }
+    if (cfast_) {  // critic layer-0 gradients: one-hot rows, bias, and dW_J = joint^T . S (cuBLAS)
+        float* g0 = b.grads + s.woff[1][0];
+        mappo_fast_layer0_grads(stream_, b.dz0, T_, E_, s.n_agents, H0, b.cS, g0 + static_cast<int64_t>(J) * H0,
+                                b.grads + s.boff[1][0]);
+        const float one = 1.0f, zero = 0.0f;
+        FLW_CUBLAS(cublasSgemm(b.blas, CUBLAS_OP_N, CUBLAS_OP_T, H0, J, static_cast<int>(T_ * E_), &one, b.cS, H0,
+                               b.joint, J, &zero, g0, H0));
     }
     // the scalar loss is not an input of anything downstream: reduced on demand (read_tensor)
 }

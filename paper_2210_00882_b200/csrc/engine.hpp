@@ -57,6 +57,7 @@ class Engine {
     void adopt_ipc_mapping(void* p) { p2p_ipc_opened_.push_back(p); }  // closed by the destructor
     void set_p2p_peers(int rank, int k, const std::vector<void*>& regions);
     bool p2p_enabled() const { return p2p_k_ > 1; }
+    bool p2p_capable() const { return numerics_ == Numerics::Fast && nrep_ == 1 && !cfast_; }
     void disable_p2p() {  // back to the NCCL exchange (the group must agree; see bench.py)
         destroy_graph();
         p2p_k_ = 0;
@@ -131,6 +132,7 @@ class Engine {
     uint64_t seed_;
     int64_t lo_, hi_, etot_, E_, R_, T_, TR_;
     bool mappo_ = false;   // agent-major rows R = n*E, critic on [joint obs | agent one-hot]
+    bool cfast_ = false;   // fast MAPPO with the compact critic (critic input > 64 wide)
     int p2p_rank_ = 0, p2p_k_ = 0;
     void* p2p_region_ptr_ = nullptr;
     int p2p_alloc_k_ = 0;

@@ -52,6 +52,9 @@ struct FastLearnArgs {
     const int32_t* rep_of_env;
     const float* rep_w;
     int64_t rep_E;
+    // learn mode: also write dZ wrt the input pre-activation, dH_0 * act'(X) (X = the input rows
+    // are activations of an outer layer): f32 [rows, in_cols]. The MAPPO compact critic uses it.
+    float* dx_out;
     double inv_n, value_coef, entropy_coef;
     float clip_eps;
     float* partials;           // [grid, part_stride]
@@ -72,7 +75,13 @@ size_t fast_learn_smem_bytes(const FastNet& n);
 size_t fast_learn_scratch_bytes(const FastNet& n);  // hidden bytes of one 128-row tile
 // fixed-order sums of the per-CTA partial slots: np policy slots, nc critic slots
 void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int np, int nc, int64_t Pp,
-                          int64_t Pc, float* grads);
+                          int64_t Pc, float* grads, int64_t c_off = 0);  // critic slots land at Pp + c_off
+// MAPPO compact critic (fast numerics, n > 4): layer-0 rows from the joint GEMM P, and the
+// layer-0 gradients (per-env agent sums S for the joint GEMM, one-hot rows, bias) from dz0.
+void mappo_fast_h0(cudaStream_t s, const float* P, const float* W0, const float* b0, int64_t blocks, int64_t E, int n,
+                   int J, int H, int act, float* h0);
+void mappo_fast_layer0_grads(cudaStream_t s, const float* dz0, int64_t T, int64_t E, int n, int H, float* S,
+                             float* gWoh, float* gb0);
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss);
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,

@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(256) k_build_wimg(const float* __restrict__ pa
 // grads[p] = sum over CTA partials in CTA order (deterministic); both nets in one launch, the
 // critic's partials following the policy's in the flat gradient.
 __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict__ pp, const float* __restrict__ pc,
-                                                         int np, int nc, int64_t Pp, int64_t Pc, float* grads) {
+                                                         int np, int nc, int64_t Pp, int64_t Pc, int64_t c_off,
+                                                         float* grads) {
     // 32 parameters per block (lane = parameter, coalesced rows); warp w sums partials
     // w, w+8, ... in order, then the 8 warp sums are added in warp order: a fixed tree.
     __shared__ float ws[8][32];
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
         float t = 0.0f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) t += ws[k][lane];
-        grads[i] = t;
+        grads[i < Pp ? i : i + c_off] = t;
     }
 }
 
@@ -363,6 +364,89 @@ __global__ void __launch_bounds__(1024) k_gae_scan32(const float* __restrict__ r
     }
 }
 
+// ---- MAPPO compact critic (fast numerics, n > 4; programs.cpp:390-402): the critic's layer 0
+// over [joint(t,e) | onehot(a)] is P[t,e] = joint . W_J (a cuBLAS TF32 GEMM, once per env)
+// plus the row W[J+a]; its gradients come back from the input-gradient stage of k_learn.
+template <int ACT>
+__global__ void k_mappo_h0(const float* __restrict__ P, const float* __restrict__ W0, const float* __restrict__ b0,
+                           int64_t blocks, int64_t E, int n, int J, int H, float* __restrict__ h0) {
+    const int64_t total = blocks * n * E * H;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % H);
+        const int64_t row = i / H, blk = row / (n * E), rem = row % (n * E), a = rem / E, e = rem % E;
+        float z = P[(blk * E + e) * H + c] + W0[(J + a) * H + c] + b0[c];
+        if (ACT == 0) z = tanhf(z);
+        if (ACT == 1) z = fmaxf(z, 0.0f);
+        h0[i] = z;
+    }
+}
+
+// S[t,e] = sum_a dz0[t,a,e] (the joint rows' gradient, fixed agent order)
+__global__ void k_mappo_sum_agents(const float* __restrict__ dz0, int64_t T, int64_t E, int n, int H, float* S) {
+    const int64_t total = T * E * H;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % H);
+        const int64_t te = i / H, t = te / E, e = te % E;
+        float acc = 0.0f;
+        for (int a = 0; a < n; ++a) acc += dz0[((t * n + a) * E + e) * H + c];
+        S[i] = acc;
+    }
+}
+
+// dW_onehot[a][c] = sum_{t,e} dz0[t,a,e][c]: block (a, 32 columns), 8 warps stride the rows,
+// combined in warp order (deterministic)
+__global__ void __launch_bounds__(256) k_mappo_onehot_grad(const float* __restrict__ dz0, int64_t T, int64_t E, int n,
+                                                           int H, float* gWoh) {
+    __shared__ float ws[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int a = blockIdx.x, c = blockIdx.y * 32 + lane;
+    float s = 0.0f;
+    if (c < H)
+        for (int64_t te = w; te < T * E; te += 8) {
+            const int64_t t = te / E, e = te % E;
+            s += dz0[((t * n + a) * E + e) * H + c];
+        }
+    ws[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && c < H) {
+        float tsum = 0.0f;
+        for (int k = 0; k < 8; ++k) tsum += ws[k][lane];
+        gWoh[a * H + c] = tsum;
+    }
+}
+
+// db0[c] = sum_a dW_onehot[a][c] (every row has exactly one agent)
+__global__ void k_mappo_bias_grad(const float* __restrict__ gWoh, int n, int H, float* gb0) {
+    const int c = threadIdx.x;
+    if (c >= H) return;
+    float s = 0.0f;
+    for (int a = 0; a < n; ++a) s += gWoh[a * H + c];
+    gb0[c] = s;
+}
+
+}  // namespace
+
+void mappo_fast_h0(cudaStream_t s, const float* P, const float* W0, const float* b0, int64_t blocks, int64_t E, int n,
+                   int J, int H, int act, float* h0) {
+    const unsigned nb = static_cast<unsigned>(std::min<int64_t>(8192, (blocks * n * E * H + 255) / 256));
+    if (act == 0)
+        k_mappo_h0<0><<<nb, 256, 0, s>>>(P, W0, b0, blocks, E, n, J, H, h0);
+    else
+        k_mappo_h0<1><<<nb, 256, 0, s>>>(P, W0, b0, blocks, E, n, J, H, h0);
+}
+
+void mappo_fast_layer0_grads(cudaStream_t s, const float* dz0, int64_t T, int64_t E, int n, int H, float* S,
+                             float* gWoh, float* gb0) {
+    const unsigned nb = static_cast<unsigned>(std::min<int64_t>(8192, (T * E * H + 255) / 256));
+    k_mappo_sum_agents<<<nb, 256, 0, s>>>(dz0, T, E, n, H, S);
+    k_mappo_onehot_grad<<<dim3(n, (H + 31) / 32), 256, 0, s>>>(dz0, T, E, n, H, gWoh);
+    k_mappo_bias_grad<<<1, 64, 0, s>>>(gWoh, n, H, gb0);
+}
+
+namespace {
+
 // Per-replica advantage statistics (R units folded into one engine, each normalising over its
 // own T*E_r rows like its own interpreter, rl.cpp:97-107): one CTA per replica, fixed order.
 __global__ void __launch_bounds__(256) k_rep_adv_stats(const float* __restrict__ adv, int64_t T, int64_t E,
@@ -429,9 +513,9 @@ void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n0, __n
 
 
 void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int np, int nc, int64_t Pp,
-                          int64_t Pc, float* grads) {
+                          int64_t Pc, float* grads, int64_t c_off) {
     k_reduce_partials<<<static_cast<unsigned>((Pp + Pc + 31) / 32), 256, 0, s>>>(part_p, part_c, np, nc, Pp, Pc,
-                                                                                 grads);
+                                                                                 c_off, grads);
 }
 
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss) {

@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     const bool reuse = learn && a.hload && L > 1;  // critic: forward skipped, activations streamed in
     const bool fwd = !reuse;
     const int nfwd = fwd ? L : 0;
-    const int njobs = learn ? nfwd + L : L;
+    const bool dx = learn && a.dx_out;  // also dZ wrt the net input (one extra stage per tile)
+    const int njobs = learn ? nfwd + L + (dx ? 1 : 0) : L;
     float* bias = reinterpret_cast<float*>(smem + C.bias);
     float* dbacc = reinterpret_cast<float*>(smem + C.dbacc);
     // hidden H_k is resident in the ring from the forward (never reloaded) for the last two
@@ -250,6 +251,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
 #endif
+                        } else if (j == nfwd + L) {  // ---- dx mode: the tile's last MMAs, dW_0
+                            issue_dw(g, 0, sbase + C.x[g]);
+                            umma::commit(&mma_done[g]);
                         } else {  // ---- backward layer m
                             const int m = L - 1 - (j - nfwd);
                             if (m >= 1 && !resident(m - 1)) {       // stream H_{m-1} in, one stage ahead
@@ -274,6 +278,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                                 for (int kb = 0; kb < dout / 16; ++kb)
                                     umma::mma_bf16(zt, umma::desc_kmajor(dzt, dout, kb),
                                                    umma::desc_mnmajor(sbase + C.wt[m], di, kb), id, kb > 0);
+                            } else if (dx) {  // dH_0 = dZ_0 W_0: gradient wrt the input (dW_0 next job)
+                                const int di = n.din[0], dout = n.dout[0];
+                                const uint32_t id = umma::idesc_bf16(128, di, false, true);
+                                const uint32_t dzt = sbase + C.dz[g][dzslot(0)];
+                                for (int kb = 0; kb < dout / 16; ++kb)
+                                    umma::mma_bf16(zt, umma::desc_kmajor(dzt, dout, kb),
+                                                   umma::desc_mnmajor(sbase + C.wt[0], di, kb), id, kb > 0);
                             } else {
                                 issue_dw(g, 0, sbase + C.x[g]);
                             }
@@ -589,6 +600,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     half.template operator()<false, 0>();
                     if (32 < di) half.template operator()<false, 32>();
                 }
+            }
+            if (dx) {  // dZ wrt the input pre-activation: dH_0 * act'(X), X = the input tile (bf16)
+                wait_mma();
+                const int di = n.din[0];
+                for (int h0 = 0; h0 < di; h0 += 32) {
+                    float gv[32];
+                    ld_acc32(gv, h0, di);
+#pragma unroll
+                    for (int c = 0; c < 32; c += 8) {
+                        if (h0 + c < di) {
+                            float y[8];
+                            umma::ld_row8(smem + C.x[g], di, r, h0 + c, y);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const int col = h0 + c + i;
+                                const float d = a.act == 0 ? gv[c + i] * (1.0f - y[i] * y[i])
+                                                           : (y[i] > 0.0f ? gv[c + i] : 0.0f);
+                                if (valid && col < a.in_cols) a.dx_out[row * a.in_cols + col] = d;
+                            }
+                        }
+                    }
+                }
+                signal();
             }
         }
         if (learn && !first) wait_mma();  // the last tile's dW_0

@@ -100,11 +100,25 @@ def test_fast_mappo_tracks_exact(n_agents):
     assert rel < 2e-2, rel
 
 
-def test_fast_mappo_refuses_wide_critic():
+@pytest.mark.parametrize("n_agents", [6, 10])
+def test_fast_mappo_compact_critic_tracks_exact(n_agents):
+    """n > 4: the critic input [joint | one-hot] (2n^2+3n) is wider than the fused kernel, so
+    its layer 0 runs compact - a TF32 joint GEMM once per env plus W[J+a] - and its gradients
+    come from the fused kernel's input-gradient stage (dW_J = joint^T . sum_a dZ0, one-hot rows,
+    bias). Same checks as the direct path."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    from paper_2210_00882_b200 import DpdEngine, FlwError
+    from paper_2210_00882_b200 import DpdEngine
 
-    algo = {"algorithm": "mappo", "agent": {"num": 8}, "env": {"type": "spread_lite", "num": 16, "params": {"accel": 1}}}
-    with pytest.raises(FlwError):
-        DpdEngine(algo, seed=5, numerics="fast")
+    algo = {"algorithm": "mappo", "agent": {"num": n_agents},
+            "env": {"type": "spread_lite", "num": 128, "params": {"accel": 1}},
+            "policy_net": {"hidden": [64, 64]}, "loop": {"episodes": 4, "steps_per_episode": 16}}
+    ex = DpdEngine(algo, seed=5, numerics="exact")
+    fa = DpdEngine(algo, seed=5, numerics="fast")
+    r_ex = [ex.run_episode(ep)[0] for ep in range(4)]
+    r_fa = [fa.run_episode(ep)[0] for ep in range(4)]
+    assert r_fa[0] == pytest.approx(r_ex[0], rel=1e-12)
+    np.testing.assert_allclose(r_fa, r_ex, rtol=5e-2)
+    p_ex, p_fa = np.asarray(ex.params()), np.asarray(fa.params())
+    rel = np.linalg.norm(p_fa - p_ex) / np.linalg.norm(p_ex)
+    assert rel < 2e-2, rel

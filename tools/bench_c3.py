@@ -47,7 +47,8 @@ def ours_point(n: int, envs: int, episodes: int, seed: int, numerics: str = "exa
     csv, _ = prog.run_local(seed=seed)
     ms = statistics.median(float(l.split(",")[1]) for l in csv.strip().split("\n")[1:])
     arm = ("ours dp-d fused, 1 x B200, numerics=exact (compact critic)" if numerics == "exact" else
-           "ours dp-d fused, 1 x B200, numerics=fast (exact rollout, tensor-core learn)")
+           "ours dp-d fused, 1 x B200, numerics=fast (exact rollout, tensor-core learn"
+           + (", compact critic: TF32 joint GEMM)" if 2 * n * n + 3 * n > 64 else ")"))
     return {"arm": arm, "agents": n, "envs": envs,
             "episode_ms": ms, "env_steps_per_s": envs * 32 / (ms * 1e-3)}
 
@@ -59,14 +60,16 @@ def main():
     ap.add_argument("--episodes", type=int, default=3)
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-ref", action="store_true")
+    ap.add_argument("--fast-only", action="store_true")
     a = ap.parse_args()
     if not a.no_ref:
         for n, envs in ((3, 2048), (8, 256)):
             print(json.dumps({"config": "C3", **ref_point(n, envs, a.seed)}), flush=True)
             print(json.dumps({"config": "C3", **ours_point(n, envs, a.episodes, a.seed)}), flush=True)
     for n in (int(x) for x in a.agents.split(",")):
-        print(json.dumps({"config": "C3", **ours_point(n, a.envs, a.episodes, a.seed)}), flush=True)
-        if 2 * n * n + 3 * n <= 64:  # fast numerics: critic input [joint | one-hot] <= 64 wide
+        if not a.fast_only:
+            print(json.dumps({"config": "C3", **ours_point(n, a.envs, a.episodes, a.seed)}), flush=True)
+        if 2 + 2 * n <= 64:  # fast numerics: per-agent observation <= 64 wide (n <= 31)
             print(json.dumps({"config": "C3", **ours_point(n, a.envs, a.episodes, a.seed, "fast")}), flush=True)
 
 

@@ -60,7 +60,7 @@ struct Engine::Bufs {
     float *joint = nullptr, *cin = nullptr;
     double* cprefix = nullptr;  // MAPPO compact critic: joint prefix chains [(T+1)*E, H0]
     // fast MAPPO compact critic (n > 4): joint GEMM, layer-0 rows, input gradients, per-env sums
-    float *h0 = nullptr, *cP = nullptr, *dz0 = nullptr, *cS = nullptr;
+    float *h0 = nullptr, *cP = nullptr, *dz0 = nullptr, *cS = nullptr, *cpart = nullptr;
     cublasHandle_t blas = nullptr;
     uint8_t* blas_ws = nullptr;
     // fast numerics
@@ -360,6 +360,7 @@ void Engine::alloc() {
             b.cP = b.alloc<float>((T_ + 1) * E_ * H0);
             b.dz0 = b.alloc<float>(TR_ * H0);
             b.cS = b.alloc<float>(T_ * E_ * H0);
+            b.cpart = b.alloc<float>(T_ * s.n_agents * H0);
             FLW_CUBLAS(cublasCreate(&b.blas));
             FLW_CUBLAS(cublasSetMathMode(b.blas, CUBLAS_TF32_TENSOR_OP_MATH));
             b.blas_ws = b.alloc<uint8_t>(32 << 20);
@@ -778,8 +779,8 @@ void Engine::enq_learn_fast() {
     }
     if (cfast_) {  // critic layer-0 gradients: one-hot rows, bias, and dW_J = joint^T . S (cuBLAS)
         float* g0 = b.grads + s.woff[1][0];
-        mappo_fast_layer0_grads(stream_, b.dz0, T_, E_, s.n_agents, H0, b.cS, g0 + static_cast<int64_t>(J) * H0,
-                                b.grads + s.boff[1][0]);
+        mappo_fast_layer0_grads(stream_, b.dz0, T_, E_, s.n_agents, H0, b.cS, b.cpart,
+                                g0 + static_cast<int64_t>(J) * H0, b.grads + s.boff[1][0]);
         const float one = 1.0f, zero = 0.0f;
         FLW_CUBLAS(cublasSgemm(b.blas, CUBLAS_OP_N, CUBLAS_OP_T, H0, J, static_cast<int>(T_ * E_), &one, b.cS, H0,
                                b.joint, J, &zero, g0, H0));

@@ -81,7 +81,7 @@ void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part
 void mappo_fast_h0(cudaStream_t s, const float* P, const float* W0, const float* b0, int64_t blocks, int64_t E, int n,
                    int J, int H, int act, float* h0);
 void mappo_fast_layer0_grads(cudaStream_t s, const float* dz0, int64_t T, int64_t E, int n, int H, float* S,
-                             float* gWoh, float* gb0);
+                             float* part, float* gWoh, float* gb0);  // part: scratch [T, n, H]
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss);
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,

@@ -395,26 +395,41 @@ __global__ void k_mappo_sum_agents(const float* __restrict__ dz0, int64_t T, int
     }
 }
 
-// dW_onehot[a][c] = sum_{t,e} dz0[t,a,e][c]: block (a, 32 columns), 8 warps stride the rows,
-// combined in warp order (deterministic)
-__global__ void __launch_bounds__(256) k_mappo_onehot_grad(const float* __restrict__ dz0, int64_t T, int64_t E, int n,
-                                                           int H, float* gWoh) {
+// dW_onehot[a][c] = sum_{t,e} dz0[t,a,e][c], in two fixed-order passes: block (t, a) sums its
+// E rows (8 warps stride e, lane = column, combined in warp order) into part[t][a][c], then the
+// T partials are added in order
+__global__ void __launch_bounds__(256) k_mappo_onehot_part(const float* __restrict__ dz0, int64_t E, int n, int H,
+                                                           float* part) {
     __shared__ float ws[8][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int a = blockIdx.x, c = blockIdx.y * 32 + lane;
-    float s = 0.0f;
-    if (c < H)
-        for (int64_t te = w; te < T * E; te += 8) {
-            const int64_t t = te / E, e = te % E;
-            s += dz0[((t * n + a) * E + e) * H + c];
+    const int64_t t = blockIdx.x;
+    const int a = blockIdx.y;
+    const float* base = dz0 + ((t * n + a) * E) * H;
+    for (int c0 = 0; c0 < H; c0 += 32) {
+        const int c = c0 + lane;
+        float s = 0.0f;
+        if (c < H) {
+#pragma unroll 8
+            for (int64_t e = w; e < E; e += 8) s += base[e * H + c];
         }
-    ws[w][lane] = s;
-    __syncthreads();
-    if (w == 0 && c < H) {
-        float tsum = 0.0f;
-        for (int k = 0; k < 8; ++k) tsum += ws[k][lane];
-        gWoh[a * H + c] = tsum;
+        ws[w][lane] = s;
+        __syncthreads();
+        if (w == 0 && c < H) {
+            float tsum = 0.0f;
+            for (int k = 0; k < 8; ++k) tsum += ws[k][lane];
+            part[(t * n + a) * H + c] = tsum;
+        }
+        __syncthreads();
     }
+}
+
+__global__ void k_mappo_onehot_sum(const float* __restrict__ part, int64_t T, int n, int H, float* gWoh) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (a, c)
+    if (i >= n * H) return;
+    const int a = i / H, c = i % H;
+    float s = 0.0f;
+    for (int64_t t = 0; t < T; ++t) s += part[(t * n + a) * H + c];
+    gWoh[a * H + c] = s;
 }
 
 // db0[c] = sum_a dW_onehot[a][c] (every row has exactly one agent)
@@ -438,10 +453,11 @@ void mappo_fast_h0(cudaStream_t s, const float* P, const float* W0, const float*
 }
 
 void mappo_fast_layer0_grads(cudaStream_t s, const float* dz0, int64_t T, int64_t E, int n, int H, float* S,
-                             float* gWoh, float* gb0) {
+                             float* part, float* gWoh, float* gb0) {
     const unsigned nb = static_cast<unsigned>(std::min<int64_t>(8192, (T * E * H + 255) / 256));
     k_mappo_sum_agents<<<nb, 256, 0, s>>>(dz0, T, E, n, H, S);
-    k_mappo_onehot_grad<<<dim3(n, (H + 31) / 32), 256, 0, s>>>(dz0, T, E, n, H, gWoh);
+    k_mappo_onehot_part<<<dim3(static_cast<unsigned>(T), n), 256, 0, s>>>(dz0, E, n, H, part);
+    k_mappo_onehot_sum<<<(n * H + 255) / 256, 256, 0, s>>>(part, T, n, H, gWoh);
     k_mappo_bias_grad<<<1, 64, 0, s>>>(gWoh, n, H, gb0);
 }
 

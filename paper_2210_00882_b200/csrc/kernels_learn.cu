@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     __shared__ Carve C;  // offsets live in shared memory, not in 40 registers per thread
 #ifdef FLW_LEARN_TRACE
     __shared__ long long tr_p[4][64], tr_e[3][64], tr_f[5][16];
-    int np_ev = 0, ne_ev = 0;
+    int np_ev = 0, ne_ev = 0, nf_ev = 0;
 #endif
     const FastNet& n = a.net;
     if (threadIdx.x == 0) C = carve_learn(n);
@@ -192,9 +192,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     const uint32_t sbase = umma::smem_u32(smem);
 
     if (w == kEpiWarps) {
-        // ================================================================ producer (one lane)
-        if (lane == 0) {
-            bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
+        // ================================================================ producer (whole warp)
+        // The warp runs the issue loop converged (warp-uniform control flow and operands); one
+        // elected lane issues each tcgen05.mma / commit / bulk copy (umma::mma_bf16_warp).
+        {
+            if (umma::elect_one()) bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
+            __syncwarp();
             umma::mbar_wait(&wbar, 0);
             uint32_t ph_epi[2] = {0, 0}, ph_ld[2][2] = {{0, 0}, {0, 0}};
             bool dw_init[kMaxLayers];
@@ -211,8 +214,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                 const uint32_t dzt = sbase + C.dz[g][dzslot(l)];
                 const uint32_t id = umma::idesc_bf16(64, dout, true, true);
                 for (int kb = 0; kb < kRows / 16; ++kb) {
-                    umma::mma_bf16(dw_tmem(l), umma::desc_mnmajor(hin, di, kb), umma::desc_mnmajor(dzt, dout, kb), id,
-                                   dw_init[l] || kb > 0);
+                    umma::mma_bf16_warp(dw_tmem(l), umma::desc_mnmajor(hin, di, kb), umma::desc_mnmajor(dzt, dout, kb),
+                                        id, dw_init[l] || kb > 0);
                 }
                 dw_init[l] = true;
             };
@@ -242,24 +245,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                             const uint32_t in = l == 0 ? sbase + C.x[g] : sbase + C.ring[g][(l - 1) & 1];
                             const uint32_t id = umma::idesc_bf16(128, dout, false, false);
                             for (int kb = 0; kb < di / 16; ++kb)
-                                umma::mma_bf16(zt, umma::desc_kmajor(in, di, kb),
+                                umma::mma_bf16_warp(zt, umma::desc_kmajor(in, di, kb),
                                                umma::desc_kmajor(sbase + C.wt[l], di, kb), id, kb > 0);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[3][np_ev] = clock64();
 #endif
-                            umma::commit(&mma_done[g]);
+                            umma::commit_warp(&mma_done[g]);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
 #endif
                         } else if (j == nfwd + L) {  // ---- dx mode: the tile's last MMAs, dW_0
                             issue_dw(g, 0, sbase + C.x[g]);
-                            umma::commit(&mma_done[g]);
+                            umma::commit_warp(&mma_done[g]);
                         } else {  // ---- backward layer m
                             const int m = L - 1 - (j - nfwd);
                             if (m >= 1 && !resident(m - 1)) {       // stream H_{m-1} in, one stage ahead
                                 const int s = (m - 1) & 1;
-                                bulk_load(smem + C.ring[g][s], hsrc(g, tl[g]) + C.hoff[m - 1],
-                                          kRows * n.dout[m - 1] * 2, &ldbar[g][s]);
+                                if (umma::elect_one())
+                                    bulk_load(smem + C.ring[g][s], hsrc(g, tl[g]) + C.hoff[m - 1],
+                                              kRows * n.dout[m - 1] * 2, &ldbar[g][s]);
+                                __syncwarp();
                             }
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
@@ -276,19 +281,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                                 const uint32_t id = umma::idesc_bf16(128, di, false, true);
                                 const uint32_t dzt = sbase + C.dz[g][dzslot(m)];
                                 for (int kb = 0; kb < dout / 16; ++kb)
-                                    umma::mma_bf16(zt, umma::desc_kmajor(dzt, dout, kb),
+                                    umma::mma_bf16_warp(zt, umma::desc_kmajor(dzt, dout, kb),
                                                    umma::desc_mnmajor(sbase + C.wt[m], di, kb), id, kb > 0);
                             } else if (dx) {  // dH_0 = dZ_0 W_0: gradient wrt the input (dW_0 next job)
                                 const int di = n.din[0], dout = n.dout[0];
                                 const uint32_t id = umma::idesc_bf16(128, di, false, true);
                                 const uint32_t dzt = sbase + C.dz[g][dzslot(0)];
                                 for (int kb = 0; kb < dout / 16; ++kb)
-                                    umma::mma_bf16(zt, umma::desc_kmajor(dzt, dout, kb),
+                                    umma::mma_bf16_warp(zt, umma::desc_kmajor(dzt, dout, kb),
                                                    umma::desc_mnmajor(sbase + C.wt[0], di, kb), id, kb > 0);
                             } else {
                                 issue_dw(g, 0, sbase + C.x[g]);
                             }
-                            umma::commit(&mma_done[g]);
+                            umma::commit_warp(&mma_done[g]);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
 #endif
@@ -409,6 +414,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                             gdst = a.hsave + static_cast<size_t>(tile) * C.hbytes;
                         }
                         if (gdst) gdst += C.hoff[l];
+                        // the bulk store that read this ring slot two layers ago must be done
+                        if (lane == 0) umma::bulk_wait_read();
+                        __syncwarp();
                         // 32 columns of H_l = act(Z + b); FULL: no per-chunk guards, so the
                         // compiler interleaves the four 8-column chains
                         auto half = [&]<bool FULL>(int h0) {
@@ -439,17 +447,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                                     const uint32_t off = umma::tile_offset(r, h0 + c, dout);
                                     const uint4 v4 = make_uint4(p[0], p[1], p[2], p[3]);
                                     *reinterpret_cast<uint4*>(dst + off) = v4;
-                                    if (gdst) *reinterpret_cast<uint4*>(gdst + off) = v4;
                                 }
                             }
                         };
+#ifdef FLW_LEARN_TRACE
+                        const bool trf = learn && g == 0 && t == 0 && nf_ev < 16;
+                        if (trf) tr_f[0][nf_ev] = clock64();
+#endif
                         if (dout == kMaxW) {
                             half.template operator()<true>(0);
+#ifdef FLW_LEARN_TRACE
+                            if (trf) tr_f[1][nf_ev] = clock64();
+#endif
                             half.template operator()<true>(32);
                         } else {
                             for (int h0 = 0; h0 < dout; h0 += 32) half.template operator()<false>(h0);
                         }
+#ifdef FLW_LEARN_TRACE
+                        if (trf) tr_f[2][nf_ev] = clock64();
+#endif
                         signal();  // H_l ready
+#ifdef FLW_LEARN_TRACE
+                        if (trf) tr_f[3][nf_ev] = clock64();
+#endif
+                        // this warp's 32 rows of the tile image are contiguous (4 core-matrix row
+                        // blocks): one TMA bulk store, off the epilogue's critical path
+                        if (gdst && lane == 0) {
+                            const uint32_t wb = static_cast<uint32_t>(dout) * 64u, wo = static_cast<uint32_t>(q) * wb;
+                            umma::bulk_s2g(gdst + wo, dst + wo, wb);
+                            umma::bulk_commit();
+                        }
+#ifdef FLW_LEARN_TRACE
+                        if (trf) tr_f[4][nf_ev++] = clock64();
+#endif
                     } else {
                         float z[32];
                         ld_acc32(z, 0, 16);
@@ -541,6 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                 }
                 // the tile's global activation images (written during the forward) -> visible to
                 // the producer's TMA bulk loads of the backward, which all follow this arrival
+                if (lane == 0) umma::bulk_wait_all();  // the forward's bulk stores are in global memory
+                __syncwarp();
                 asm volatile("fence.proxy.async.global;\n" ::: "memory");
                 signal();  // dZ_{L-1} ready
                 colsum32(dz, 0, wo, L - 1);
@@ -625,6 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                 signal();
             }
         }
+        if (lane == 0) umma::bulk_wait_all();  // values pass: the saved activations are written
         if (learn && !first) wait_mma();  // the last tile's dW_0
         // ---- loss partials of this warp
         for (int off = 16; off > 0; off >>= 1) {
@@ -688,8 +721,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
         const long long t0 = tr_p[0][0];
         for (int i = 0; i < ne_ev; ++i)
             printf("E %2d wait %7lld got %7lld signal %7lld\n", i, tr_e[0][i] - t0, tr_e[1][i] - t0, tr_e[2][i] - t0);
-        for (int i = 0; i < 6; ++i)
-            printf("F %2d ld0 %7lld done0 %7lld ld1 %7lld done1 %7lld stored %7lld\n", i, tr_f[0][i] - t0,
+        for (int i = 0; i < nf_ev; ++i)
+            printf("F %2d start %7lld half0 %7lld stores %7lld signaled %7lld bulk %7lld\n", i, tr_f[0][i] - t0,
                    tr_f[1][i] - t0, tr_f[2][i] - t0, tr_f[3][i] - t0, tr_f[4][i] - t0);
     }
     if (blockIdx.x == 0 && t == 32 * kEpiWarps && a.mode == 1) {

@@ -64,6 +64,37 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate ? 1u : 0u));
 }
 
+// Warp-collective forms: the WHOLE (converged) warp executes them and one lane elected inside the
+// asm issues the instruction. Issuing from a single-thread branch (`if (lane == 0)`) makes ptxas
+// move every operand to uniform registers through an R2UR.BROADCAST loop per MMA: measured
+// ~140 cycles per tcgen05.mma for ANY shape, vs 49 (M128 N64), 33 (M64 N64) and 65 (M128 N128,
+// = the dense peak) cycles with warp-uniform operands (tools/umma_rate2.cu / umma_rate3.cu,
+// profiles/r01_umma_issue.txt).
+__device__ __forceinline__ void mma_bf16_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              bool accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate ? 1u : 0u));
+}
+
+__device__ __forceinline__ void commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // Arrive on an mbarrier once every previously issued tcgen05.mma of this thread completed.
 __device__ __forceinline__ void commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(

@@ -40,6 +40,10 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (kEpiWarps + 1);
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
 constexpr int kXPre = 32;                      // input columns prefetched in registers
+#ifndef FLW_TANH_MUFU_PAIRS
+#define FLW_TANH_MUFU_PAIRS 4
+#endif
+constexpr int kMufuPairs = FLW_TANH_MUFU_PAIRS;  // of each 8-column chunk's 4 pairs: MUFU, rest poly
 
 struct Carve {
     uint32_t wt[kMaxLayers], wbytes;
@@ -142,6 +146,11 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
     return v[0];
 }
 
+// MODE 0: values pass (critic forward, saves activations); 1: learn (forward + backward);
+// 2: learn reusing the values pass's activations (backward only). ACT 0: tanh, 1: relu.
+// Compile-time modes keep each instantiation's code small (the stage loops are instruction-
+// cache sensitive) and branch-free per activation chunk.
+template <int MODE, int ACT>
 __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mma_done[2], epi_done[2], ldbar[2][2], wbar;
@@ -158,8 +167,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     const int L = n.L;
     const int64_t ntiles = (a.rows + kRows - 1) / kRows;
     const int G = gridDim.x;
-    const bool learn = a.mode == 1;
-    const bool reuse = learn && a.hload && L > 1;  // critic: forward skipped, activations streamed in
+    constexpr bool learn = MODE != 0;
+    constexpr bool reuse = MODE == 2;  // critic: forward skipped, activations streamed in
     const bool fwd = !reuse;
     const int nfwd = fwd ? L : 0;
     const bool dx = learn && a.dx_out;  // also dZ wrt the net input (one extra stage per tile)
@@ -435,9 +444,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                                     for (int i = 0; i < 4; ++i) {
                                         const float z0 = z[c + 2 * i] + bb[2 * i];
                                         const float z1 = z[c + 2 * i + 1] + bb[2 * i + 1];
-                                        if (a.act != 0) {
+                                        if constexpr (ACT != 0) {
                                             p[i] = umma::pack_bf16x2(fmaxf(z0, 0.0f), fmaxf(z1, 0.0f));
-                                        } else if (i < 2) {
+                                        } else if (i < kMufuPairs) {
                                             p[i] = umma::pack_bf16x2(tanh_fast(z0), tanh_fast(z1));
                                         } else {
                                             const float2 y2 = tanh_poly2(make_float2(z0, z1));
@@ -604,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                                 const float2 yy = make_float2(y[2 * i], y[2 * i + 1]);
                                 const float2 gg = make_float2(gv[c + 2 * i], gv[c + 2 * i + 1]);
                                 float2 d;
-                                if (a.act == 0) {  // dZ = dH (1 - y^2), packed f32x2 on the FMA pipe
+                                if constexpr (ACT == 0) {  // dZ = dH (1 - y^2), packed f32x2 on the FMA pipe
                                     const float2 om = __ffma2_rn(make_float2(-yy.x, -yy.y), yy, make_float2(1.0f, 1.0f));
                                     d = __fmul2_rn(gg, om);
                                 } else {
@@ -632,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     half.template operator()<false, 0>();
                     if (32 < di) half.template operator()<false, 32>();
                 }
+
             }
             if (dx) {  // dZ wrt the input pre-activation: dH_0 * act'(X), X = the input tile (bf16)
                 wait_mma();
@@ -647,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #pragma unroll
                             for (int i = 0; i < 8; ++i) {
                                 const int col = h0 + c + i;
-                                const float d = a.act == 0 ? gv[c + i] * (1.0f - y[i] * y[i])
+                                const float d = ACT == 0 ? gv[c + i] * (1.0f - y[i] * y[i])
                                                            : (y[i] > 0.0f ? gv[c + i] : 0.0f);
                                 if (valid && col < a.in_cols) a.dx_out[row * a.in_cols + col] = d;
                             }
@@ -717,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     __syncthreads();
     if (w == 0) umma::tmem_free<512>(tmem);
 #ifdef FLW_LEARN_TRACE
-    if (blockIdx.x == 0 && t == 0 && a.mode == 1) {
+    if (blockIdx.x == 0 && t == 0 && MODE != 0) {
         const long long t0 = tr_p[0][0];
         for (int i = 0; i < ne_ev; ++i)
             printf("E %2d wait %7lld got %7lld signal %7lld\n", i, tr_e[0][i] - t0, tr_e[1][i] - t0, tr_e[2][i] - t0);
@@ -725,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             printf("F %2d start %7lld half0 %7lld stores %7lld signaled %7lld bulk %7lld\n", i, tr_f[0][i] - t0,
                    tr_f[1][i] - t0, tr_f[2][i] - t0, tr_f[3][i] - t0, tr_f[4][i] - t0);
     }
-    if (blockIdx.x == 0 && t == 32 * kEpiWarps && a.mode == 1) {
+    if (blockIdx.x == 0 && t == 32 * kEpiWarps && MODE != 0) {
         const long long t0 = tr_p[0][0];
         for (int i = 0; i < np_ev; ++i)
             printf("P %2d epi %7lld a %7lld b %7lld commit %7lld\n", i, tr_p[0][i] - t0, tr_p[2][i] - t0,
@@ -742,9 +752,21 @@ size_t fast_learn_scratch_bytes(const FastNet& n) { return carve_learn(n).hbytes
 void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid) {
     const size_t smem = carve_learn(a.net).total;
     if (smem > 227u * 1024u) throw Error(Errc::Config, "fast numerics: network too wide/deep for one SM's shared memory");
-    // per-device attribute: set on every launch (cheap, and legal inside stream capture)
-    FLW_CUDA(cudaFuncSetAttribute(k_learn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    k_learn<<<grid, kThreads, smem, s>>>(a);
+    const int mode = a.mode != 1 ? 0 : (a.hload && a.net.L > 1 ? 2 : 1);
+    auto go = [&](auto kern) {
+        // per-device attribute: set on every launch (cheap, and legal inside stream capture)
+        FLW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<grid, kThreads, smem, s>>>(a);
+    };
+    if (a.act == 0) {
+        if (mode == 0) go(k_learn<0, 0>);
+        else if (mode == 1) go(k_learn<1, 0>);
+        else go(k_learn<2, 0>);
+    } else {
+        if (mode == 0) go(k_learn<0, 1>);
+        else if (mode == 1) go(k_learn<1, 1>);
+        else go(k_learn<2, 1>);
+    }
 }
 
 }  // namespace flw

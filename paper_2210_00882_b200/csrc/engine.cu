@@ -74,6 +74,7 @@ struct Engine::Bufs {
     int lgrid_p = 0, lgrid_c = 0;       // CTA partial slots written by the last policy / critic learn
     double *block_sums = nullptr, *rsum_scratch = nullptr;
     unsigned* gae_counter = nullptr;  // last-block-done counter of the fused GAE statistics
+    unsigned* upd_counter = nullptr;  // last-block-done counter of k_reduce_adam
     // R > 1 replicas: env -> replica map, replica-major trajectory copies (exact), per-replica
     // gradient slots [R, P], advantage statistics [R, 2] and row weights (fast)
     int32_t* rep_of_env = nullptr;
@@ -382,6 +383,7 @@ void Engine::alloc() {
             std::max(fast_learn_scratch_bytes(b.pol), fast_learn_scratch_bytes(b.crit)) * 2 * b.grid2));
         b.block_sums = b.alloc<double>(2 * ((R_ + 31) / 32));  // per GAE block (32 or 256 streams)
         b.gae_counter = b.alloc<unsigned>(1);
+        b.upd_counter = b.alloc<unsigned>(1);
         b.rsum_scratch = b.alloc<double>(256);
         b.values = b.alloc<float>(TR_);
         b.last_value = b.alloc<float>(R_);
@@ -663,7 +665,9 @@ void Engine::enq_learn_fast() {
     f.rep_of_env = nrep_ > 1 ? b.rep_of_env : nullptr;
     f.rep_w = b.rep_w;
     f.rep_E = E_;
-    fast_build_wimg(stream_, b.params, b.crit, b.wimg_c, b.pol, b.wimg_p);
+    // the weight images: built at the first train iteration of an episode; later iterations use
+    // the images the previous iteration's fused update (k_reduce_adam) wrote
+    if (learn_iter_ == 0 || !prev_fused_) fast_build_wimg(stream_, b.params, b.crit, b.wimg_c, b.pol, b.wimg_p);
     // values = critic(states), last_value = critic(last_next)
     f.net = b.crit;
     f.wimg = b.wimg_c;
@@ -771,7 +775,9 @@ void Engine::enq_learn_fast() {
     }
     b.lgrid_p = gp;
     b.lgrid_c = gc;
-    if (!p2p_enabled()) {  // with peer-memory exchange the reduction is fused into the exchange
+    // one GPU, one unit, no exchange: the reduction is fused with Adam (enq_grad_sync_and_adam)
+    fused_pending_ = fuse_ok_ && !p2p_enabled() && !(comm_ && comm_->nranks() > 1) && !cfast_ && nrep_ == 1;
+    if (!p2p_enabled() && !fused_pending_) {  // with peer-memory exchange the reduction is fused into the exchange
         probe_begin("reduce");
         fast_reduce_partials(stream_, b.part_p, b.part_c, gp, gc, s.P_policy, s.P - s.P_policy - c_off, b.grads,
                              c_off);
@@ -857,6 +863,37 @@ void Engine::enq_permute_replicas() {
 void Engine::enq_grad_sync_and_adam() {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
+    prev_fused_ = fused_pending_;
+    if (fused_pending_) {  // partial reduction + Adam + weight images, one launch
+        fused_pending_ = false;
+        FastUpdateArgs u{};
+        u.pp = b.part_p;
+        u.pc = b.part_c;
+        u.np = b.lgrid_p;
+        u.nc = b.lgrid_c;
+        u.Pp = s.P_policy;
+        u.Pc = s.P - s.P_policy;
+        u.ctx = b.ctx;
+        u.bc_table = b.bc_table;
+        u.bc_len = b.bc_len;
+        u.params = b.params;
+        u.grads = b.grads;
+        u.m = b.m;
+        u.v = b.v;
+        u.lr = cfg_.lr;
+        u.b1 = 0.9;
+        u.b2 = 0.999;
+        u.eps = 1e-8;
+        u.pol = b.pol;
+        u.crit = b.crit;
+        u.img_p = b.wimg_p;
+        u.img_c = b.wimg_c;
+        u.counter = b.upd_counter;
+        probe_begin("reduce");
+        fast_reduce_adam(stream_, u);
+        probe_end();
+        return;
+    }
     adam_tick(stream_, b.ctx, b.bc_table, b.bc_len);
     if (p2p_enabled() && numerics_ == Numerics::Fast) {
         // reduce the CTA partials + all-reduce over NVLink peer memory + Adam: one kernel
@@ -963,6 +1000,7 @@ void Engine::learn_grads(int64_t ep, int64_t k) {
     (void)k;
     FLW_CUDA(cudaSetDevice(device_));
     set_episode(ep);
+    learn_iter_ = 0;
     enq_learn_grads();
     if (numerics_ == Numerics::Exact) exact_loss_reduce(stream_, b_->terms, TR_, cfg_.entropy_coef, b_->loss);
     FLW_CUDA(cudaStreamSynchronize(stream_));
@@ -986,7 +1024,10 @@ void Engine::learn(int64_t ep, int64_t k) {
     (void)k;
     FLW_CUDA(cudaSetDevice(device_));
     set_episode(ep);
+    learn_iter_ = 0;
+    fuse_ok_ = true;  // the update follows right away
     enq_learn_grads();
+    fuse_ok_ = false;
     if (numerics_ == Numerics::Exact) exact_loss_reduce(stream_, b_->terms, TR_, cfg_.entropy_coef, b_->loss);
     enq_grad_sync_and_adam();
     FLW_CUDA(cudaStreamSynchronize(stream_));
@@ -1021,12 +1062,16 @@ void Engine::build_graph() {
     trace_capture("rollout+reward");
     for (int64_t k = 0; k < shape_.learn_iters; ++k) {
         if (numerics_ == Numerics::Exact) probe_begin("learn_grads");
+        learn_iter_ = k;
+        fuse_ok_ = true;  // the update follows right away
         enq_learn_grads();
+        fuse_ok_ = false;
         trace_capture("learn_grads");
         if (numerics_ == Numerics::Exact) probe_end();
         enq_grad_sync_and_adam();
         trace_capture("sync+adam");
     }
+    learn_iter_ = 0;
     if (!eager_coll_) FLW_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
     end_segment();
     graph_ = segs_.front();

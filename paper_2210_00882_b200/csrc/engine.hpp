@@ -168,6 +168,11 @@ class Engine {
     };
     bool probes_on_ = false;
     bool capturing_ = false;
+    // fast numerics, 1 GPU: the train iteration's update as one fused launch (k_reduce_adam)
+    int64_t learn_iter_ = 0;      // train iteration being enqueued (0: weight images rebuilt)
+    bool fuse_ok_ = false;        // enq_grad_sync_and_adam follows the learn being enqueued
+    bool fused_pending_ = false;  // the learn left its partials for k_reduce_adam
+    bool prev_fused_ = false;     // the last update also refreshed the weight images
     std::vector<Probe> probes_;
     int open_probe_ = -1;
     void probe_begin(const char* tag);

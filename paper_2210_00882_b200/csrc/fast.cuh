@@ -74,6 +74,23 @@ void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid);
 size_t fast_learn_smem_bytes(const FastNet& n);
 size_t fast_learn_scratch_bytes(const FastNet& n);  // hidden bytes of one 128-row tile
 // fixed-order sums of the per-CTA partial slots: np policy slots, nc critic slots
+struct DeviceCtx;
+struct FastUpdateArgs {      // k_reduce_adam: partial reduction + Adam + weight image, one launch
+    const float *pp, *pc;    // per-CTA dW partials of the policy / critic learn kernels
+    int np, nc;
+    int64_t Pp, Pc;          // policy / critic parameter counts (critic follows the policy)
+    DeviceCtx* ctx;          // Adam step counter and bias corrections
+    const double2* bc_table;
+    int64_t bc_len;
+    float* params;
+    float* grads;            // the reduced gradient (kept for read-back)
+    double *m, *v;
+    double lr, b1, b2, eps;
+    FastNet pol, crit;
+    __nv_bfloat16 *img_p, *img_c;
+    unsigned* counter;       // zero between launches
+};
+void fast_reduce_adam(cudaStream_t s, const FastUpdateArgs& a);
 void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int np, int nc, int64_t Pp,
                           int64_t Pc, float* grads, int64_t c_off = 0);  // critic slots land at Pp + c_off
 // MAPPO compact critic (fast numerics, n > 4): layer-0 rows from the joint GEMM P, and the

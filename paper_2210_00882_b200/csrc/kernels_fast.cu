@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "engine.hpp"
 #include "fast.cuh"
 #include "umma.cuh"
 
@@ -92,6 +93,72 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
 #pragma unroll
         for (int k = 0; k < 8; ++k) t += ws[k][lane];
         grads[i < Pp ? i : i + c_off] = t;
+    }
+}
+
+// One train iteration's parameter update fused into a single launch (1 GPU, no exchange): the
+// fixed-order reduction of the per-CTA dW partials (as k_reduce_partials), Adam with double
+// moments (mlp.cpp:480-495, as k_adam) and the bf16 weight-image entry of every weight (as
+// k_build_wimg), so the next train iteration's learn kernels read the updated image without a
+// build launch. The Adam step counter and its bias corrections (as k_adam_tick) are advanced by
+// the last block to finish (every block has read the old counter by then).
+__global__ void __launch_bounds__(256) k_reduce_adam(FastUpdateArgs a) {
+    __shared__ float ws[8][32];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * 32LL + lane;
+    const int64_t P = a.Pp + a.Pc;
+    const bool ok = i < P;
+    const float* src = !ok ? a.pp : (i < a.Pp ? a.pp + i : a.pc + (i - a.Pp));
+    const int64_t stride = i < a.Pp ? a.Pp : a.Pc;
+    const int nparts = i < a.Pp ? a.np : a.nc;
+    float s = 0.0f;
+    if (ok) {
+#pragma unroll 8
+        for (int p = w; p < nparts; p += 8) s += src[p * stride];
+    }
+    ws[w][lane] = s;
+    const int64_t t = a.ctx->adam_t + 1;
+    const double bc1 = t <= a.bc_len ? a.bc_table[t - 1].x : 1.0 - pow(0.9, static_cast<double>(t));
+    const double bc2 = t <= a.bc_len ? a.bc_table[t - 1].y : 1.0 - pow(0.999, static_cast<double>(t));
+    __syncthreads();
+    if (w == 0 && ok) {
+        float gsum = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) gsum += ws[k][lane];
+        a.grads[i] = gsum;
+        const double g = static_cast<double>(gsum);
+        const double mi = __dadd_rn(__dmul_rn(a.b1, a.m[i]), __dmul_rn(__dsub_rn(1.0, a.b1), g));
+        const double vi = __dadd_rn(__dmul_rn(a.b2, a.v[i]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, a.b2), g), g));
+        a.m[i] = mi;
+        a.v[i] = vi;
+        const double mhat = __ddiv_rn(mi, bc1), vhat = __ddiv_rn(vi, bc2);
+        const float next = static_cast<float>(__dsub_rn(
+            static_cast<double>(a.params[i]), __ddiv_rn(__dmul_rn(a.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), a.eps))));
+        a.params[i] = next;
+        // weight-image entry (biases are read from params by the learn kernels)
+        const bool pol = i < a.Pp;
+        const FastNet& n = pol ? a.pol : a.crit;
+        for (int l = 0; l < n.L; ++l) {
+            const int64_t r = i - n.woff[l];
+            if (r >= 0 && r < static_cast<int64_t>(n.rin[l]) * n.rout[l]) {
+                const int c = static_cast<int>(r / n.rout[l]), o = static_cast<int>(r % n.rout[l]);
+                const Smem S = carve(n);
+                (pol ? a.img_p : a.img_c)[(S.wt[l] + umma::tile_offset(o, c, n.din[l])) / 2] = __float2bfloat16(next);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        a.ctx->adam_t = t;
+        a.ctx->bc1 = bc1;
+        a.ctx->bc2 = bc2;
+        *a.counter = 0u;
     }
 }
 
@@ -532,6 +599,10 @@ void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part
                           int64_t Pc, float* grads, int64_t c_off) {
     k_reduce_partials<<<static_cast<unsigned>((Pp + Pc + 31) / 32), 256, 0, s>>>(part_p, part_c, np, nc, Pp, Pc,
                                                                                  c_off, grads);
+}
+
+void fast_reduce_adam(cudaStream_t s, const FastUpdateArgs& a) {
+    k_reduce_adam<<<static_cast<unsigned>((a.Pp + a.Pc + 31) / 32), 256, 0, s>>>(a);
 }
 
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss) {

@@ -70,7 +70,7 @@ struct Engine::Bufs {
     __nv_bfloat16 *wimg_p = nullptr, *wimg_c = nullptr;
     uint8_t* hsave = nullptr;           // critic hidden activations of the values pass (bf16 tiles)
     uint8_t* hscratch = nullptr;        // k_learn per-(CTA, group) activation scratch
-    int grid2 = 0;                      // k_learn grid (two tiles per CTA in flight)
+    int grid2 = 0;                      // k_learn grid (fast_learn_groups() tiles per CTA in flight)
     int lgrid_p = 0, lgrid_c = 0;       // CTA partial slots written by the last policy / critic learn
     double *block_sums = nullptr, *rsum_scratch = nullptr;
     unsigned* gae_counter = nullptr;  // last-block-done counter of the fused GAE statistics
@@ -378,9 +378,10 @@ void Engine::alloc() {
         b.wimg_p = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.pol) / 2));
         b.wimg_c = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.crit) / 2));
         b.hsave = b.alloc<uint8_t>(static_cast<int64_t>(fast_hsave_bytes(b.crit)) * ((TR_ + 127) / 128));
-        b.grid2 = static_cast<int>(std::min<int64_t>(sms, ((TR_ + 127) / 128 + 1) / 2));
+        const int64_t grp = fast_learn_groups();
+        b.grid2 = static_cast<int>(std::min<int64_t>(sms, ((TR_ + 127) / 128 + grp - 1) / grp));
         b.hscratch = b.alloc<uint8_t>(static_cast<int64_t>(
-            std::max(fast_learn_scratch_bytes(b.pol), fast_learn_scratch_bytes(b.crit)) * 2 * b.grid2));
+            std::max(fast_learn_scratch_bytes(b.pol), fast_learn_scratch_bytes(b.crit)) * grp * b.grid2));
         b.block_sums = b.alloc<double>(2 * ((R_ + 31) / 32));  // per GAE block (32 or 256 streams)
         b.gae_counter = b.alloc<unsigned>(1);
         b.upd_counter = b.alloc<unsigned>(1);
@@ -706,7 +707,8 @@ void Engine::enq_learn_fast() {
     auto launch = [&](int grid) { fast_learn(stream_, f, grid); };
     f.hscratch = b.hscratch;
     probe_begin("critic_fwd");
-    launch(static_cast<int>(std::min<int64_t>(lgrid, ((f.rows + 127) / 128 + 1) / 2)));
+    const int64_t grp = fast_learn_groups();
+    launch(static_cast<int>(std::min<int64_t>(lgrid, ((f.rows + 127) / 128 + grp - 1) / grp)));
     probe_end();
     f.split_rows = -1;
     probe_begin("gae");

@@ -46,7 +46,7 @@ struct FastLearnArgs {
     uint8_t* hsave;
     int64_t save_tiles;
     int hload;
-    uint8_t* hscratch;         // k_learn: per (CTA, group) hidden-activation scratch [grid*2][hbytes]
+    uint8_t* hscratch;         // k_learn: per (CTA, group) activation scratch [grid * groups][hbytes]
     // R > 1 replicas folded into the unit: row -> replica via env (row % rep_E); per-replica row
     // weight (1 / (R * T * E_r)) replaces inv_n and adv_stats is indexed [replica][2]
     const int32_t* rep_of_env;
@@ -63,7 +63,7 @@ struct FastLearnArgs {
 };
 
 size_t fast_wimg_bytes(const FastNet& n);  // bytes of the weight-tile image (smem prefix)
-size_t fast_hsave_bytes(const FastNet& n); // bytes of one tile's hidden-activation tiles
+size_t fast_hsave_bytes(const FastNet& n); // bytes of one tile's saved tiles (X, hidden activations)
 // Builds the bf16 W^T tile image of one net from the f32 params (once per train iteration,
 // shared by every CTA of the critic-forward / learn kernels that follow).
 void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n0, __nv_bfloat16* img0, const FastNet& n1,
@@ -73,6 +73,7 @@ void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n0, __n
 void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid);
 size_t fast_learn_smem_bytes(const FastNet& n);
 size_t fast_learn_scratch_bytes(const FastNet& n);  // hidden bytes of one 128-row tile
+int fast_learn_groups();  // tiles in flight per k_learn CTA
 // fixed-order sums of the per-CTA partial slots: np policy slots, nc critic slots
 struct DeviceCtx;
 struct FastUpdateArgs {      // k_reduce_adam: partial reduction + Adam + weight image, one launch

@@ -42,7 +42,7 @@ __host__ __device__ inline Smem carve(const FastNet& n) {
         off = align_up(off + static_cast<uint32_t>(n.dout[l] * n.din[l] * 2), 128);
     }
     s.x = off;  // end of the weight image
-    s.hbytes = 0;
+    s.hbytes = static_cast<uint32_t>(kRows * n.din[0] * 2);  // the input tile X, then H_0 .. H_{L-2}
     for (int l = 0; l + 1 < n.L; ++l) s.hbytes += static_cast<uint32_t>(kRows * n.dout[l] * 2);
     return s;
 }

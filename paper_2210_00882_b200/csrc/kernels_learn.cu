@@ -36,7 +36,8 @@ namespace {
 
 constexpr int kRows = 128;
 constexpr int kMaxW = 64;
-constexpr int kEpiWarps = 8;
+constexpr int kGroups = 3;  // tiles in flight per CTA (one epilogue group of 4 warps each)
+constexpr int kEpiWarps = 4 * kGroups;
 constexpr int kThreads = 32 * (kEpiWarps + 1);
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
 constexpr int kXPre = 32;                      // input columns prefetched in registers
@@ -47,9 +48,9 @@ constexpr int kMufuPairs = FLW_TANH_MUFU_PAIRS;  // of each 8-column chunk's 4 p
 
 struct Carve {
     uint32_t wt[kMaxLayers], wbytes;
-    uint32_t x[2], ring[2][2], dz[2][2];
+    uint32_t ring[kGroups][2], dz[kGroups];  // ring slot 1 also holds the input tile X
     uint32_t bias, dbacc, loss, total;
-    uint32_t hoff[kMaxLayers], hbytes;  // hidden tile offsets inside one tile's saved activations
+    uint32_t hoff[kMaxLayers + 1], hbytes;  // saved tile images: hoff[k + 1] = H_k, hoff[0] = X
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
@@ -63,17 +64,13 @@ __host__ __device__ inline Carve carve_learn(const FastNet& n) {
     }
     c.wbytes = off;
     off = align_up(off, 1024);
-    for (int g = 0; g < 2; ++g) {
-        c.x[g] = off;
-        off = align_up(off + kRows * n.din[0] * 2, 1024);
+    for (int g = 0; g < kGroups; ++g) {
         for (int s = 0; s < 2; ++s) {
             c.ring[g][s] = off;
             off += kSlot;
         }
-        for (int s = 0; s < 2; ++s) {
-            c.dz[g][s] = off;
-            off += kSlot;
-        }
+        c.dz[g] = off;
+        off += kSlot;
     }
     c.bias = off;
     off += kMaxLayers * kMaxW * 4;
@@ -82,9 +79,10 @@ __host__ __device__ inline Carve carve_learn(const FastNet& n) {
     c.loss = off;
     off += kEpiWarps * 3 * 4;
     c.total = off + 2048;  // slack: M=64 MN-major reads of narrow tiles run past their end
-    uint32_t h = 0;
+    uint32_t h = static_cast<uint32_t>(kRows * n.din[0] * 2);  // X first
+    c.hoff[0] = 0;
     for (int l = 0; l + 1 < n.L; ++l) {
-        c.hoff[l] = h;
+        c.hoff[l + 1] = h;
         h += static_cast<uint32_t>(kRows * n.dout[l] * 2);
     }
     c.hbytes = h;
@@ -153,7 +151,7 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 template <int MODE, int ACT>
 __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t mma_done[2], epi_done[2], ldbar[2][2], wbar;
+    __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar;
     __shared__ uint32_t tslot;
     __shared__ Carve C;  // offsets live in shared memory, not in 40 registers per thread
 #ifdef FLW_LEARN_TRACE
@@ -172,16 +170,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     const bool fwd = !reuse;
     const int nfwd = fwd ? L : 0;
     const bool dx = learn && a.dx_out;  // also dZ wrt the net input (one extra stage per tile)
-    const int njobs = learn ? nfwd + L + (dx ? 1 : 0) : L;
+    const int njobs = learn ? nfwd + L : L;
     float* bias = reinterpret_cast<float*>(smem + C.bias);
     float* dbacc = reinterpret_cast<float*>(smem + C.dbacc);
-    // hidden H_k is resident in the ring from the forward (never reloaded) for the last two
+    // H_k (k = -1: the input tile X) lives in ring slot k & 1; the last two the forward wrote
+    // stay resident there (never reloaded)
     auto resident = [&](int k) { return fwd && (k == L - 2 || k == L - 3); };
-    auto dzslot = [&](int k) { return (L - 1 - k) & 1; };
+    auto hwidth = [&](int k) { return k < 0 ? n.din[0] : n.dout[k]; };
 
     // ---- setup
     if (t == 0) {
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < kGroups; ++g) {
             umma::mbar_init(&mma_done[g], 1);
             umma::mbar_init(&epi_done[g], 4);
             umma::mbar_init(&ldbar[g][0], 1);
@@ -208,19 +207,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             if (umma::elect_one()) bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
             __syncwarp();
             umma::mbar_wait(&wbar, 0);
-            uint32_t ph_epi[2] = {0, 0}, ph_ld[2][2] = {{0, 0}, {0, 0}};
+            uint32_t ph_epi[kGroups] = {}, ph_ld[kGroups][2] = {};
             bool dw_init[kMaxLayers];
             for (int l = 0; l < kMaxLayers; ++l) dw_init[l] = false;
             auto dw_tmem = [&](int l) {
-                return tmem + 128u + 64u * static_cast<uint32_t>(l >> 1) + ((l & 1) ? (16u << 16) : 0u);
+                return tmem + 64u * kGroups + 64u * static_cast<uint32_t>(l >> 1) + ((l & 1) ? (16u << 16) : 0u);
             };
             auto hsrc = [&](int g, int64_t tile) -> uint8_t* {
                 return reuse ? a.hsave + static_cast<size_t>(tile) * C.hbytes
-                             : a.hscratch + static_cast<size_t>(2 * blockIdx.x + g) * C.hbytes;
+                             : a.hscratch + static_cast<size_t>(kGroups * blockIdx.x + g) * C.hbytes;
+            };
+            auto load_h = [&](int g, int64_t tile, int k) {  // H_k (k = -1: X) -> ring slot k & 1
+                if (umma::elect_one())
+                    bulk_load(smem + C.ring[g][k & 1], hsrc(g, tile) + C.hoff[k + 1],
+                              static_cast<uint32_t>(kRows * hwidth(k) * 2), &ldbar[g][k & 1]);
+                __syncwarp();
             };
             auto issue_dw = [&](int g, int l, uint32_t hin) {  // dW_l += H_{l-1}^T dZ_l  (M = din_l)
                 const int di = n.din[l], dout = n.dout[l];
-                const uint32_t dzt = sbase + C.dz[g][dzslot(l)];
+                const uint32_t dzt = sbase + C.dz[g];
                 const uint32_t id = umma::idesc_bf16(64, dout, true, true);
                 for (int kb = 0; kb < kRows / 16; ++kb) {
                     umma::mma_bf16_warp(dw_tmem(l), umma::desc_mnmajor(hin, di, kb), umma::desc_mnmajor(dzt, dout, kb),
@@ -229,15 +234,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                 dw_init[l] = true;
             };
             for (int64_t it = 0;; ++it) {
-                int64_t tl[2];
-                bool has[2];
-                for (int g = 0; g < 2; ++g) {
-                    tl[g] = it * 2 * G + 2 * static_cast<int64_t>(blockIdx.x) + g;
+                int64_t tl[kGroups];
+                bool has[kGroups], any = false;
+                for (int g = 0; g < kGroups; ++g) {
+                    tl[g] = it * kGroups * G + kGroups * static_cast<int64_t>(blockIdx.x) + g;
                     has[g] = tl[g] < ntiles;
+                    any = any || has[g];
                 }
-                if (!has[0] && !has[1]) break;
+                if (!any) break;
                 for (int j = 0; j < njobs; ++j) {
-                    for (int g = 0; g < 2; ++g) {
+                    for (int g = 0; g < kGroups; ++g) {
                         if (!has[g]) continue;
                         umma::mbar_wait(&epi_done[g], ph_epi[g]);
                         ph_epi[g] ^= 1;
@@ -251,7 +257,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
 #endif
-                            const uint32_t in = l == 0 ? sbase + C.x[g] : sbase + C.ring[g][(l - 1) & 1];
+                            {  // H_{l-1} (X for l = 0) is complete in its ring slot: save it (TMA bulk store)
+                                const int hk = l - 1;
+                                uint8_t* gdst = nullptr;
+                                if (learn) {
+                                    if (!resident(hk))
+                                        gdst = a.hscratch + static_cast<size_t>(kGroups * blockIdx.x + g) * C.hbytes;
+                                } else if (a.hsave && tl[g] < a.save_tiles) {
+                                    gdst = a.hsave + static_cast<size_t>(tl[g]) * C.hbytes;
+                                }
+                                if (lane == 0) {
+                                    if (gdst) {
+                                        umma::bulk_s2g(gdst + C.hoff[hk + 1], smem + C.ring[g][hk & 1],
+                                                       static_cast<uint32_t>(kRows * hwidth(hk) * 2));
+                                        umma::bulk_commit();
+                                    }
+                                    // every older store has read its slot: the epilogue may overwrite
+                                    // the slot of H_{l-2} once this job's MMAs commit
+                                    umma::bulk_wait_read1();
+                                }
+                                __syncwarp();
+                            }
+                            const uint32_t in = sbase + C.ring[g][(l - 1) & 1];
                             const uint32_t id = umma::idesc_bf16(128, dout, false, false);
                             for (int kb = 0; kb < di / 16; ++kb)
                                 umma::mma_bf16_warp(zt, umma::desc_kmajor(in, di, kb),
@@ -263,45 +290,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
 #endif
-                        } else if (j == nfwd + L) {  // ---- dx mode: the tile's last MMAs, dW_0
-                            issue_dw(g, 0, sbase + C.x[g]);
-                            umma::commit_warp(&mma_done[g]);
-                        } else {  // ---- backward layer m
+                        } else {  // ---- backward layer m: dH_m = dZ_m W_m and dW_m = H_{m-1}^T dZ_m
                             const int m = L - 1 - (j - nfwd);
-                            if (m >= 1 && !resident(m - 1)) {       // stream H_{m-1} in, one stage ahead
-                                const int s = (m - 1) & 1;
-                                if (umma::elect_one())
-                                    bulk_load(smem + C.ring[g][s], hsrc(g, tl[g]) + C.hoff[m - 1],
-                                              kRows * n.dout[m - 1] * 2, &ldbar[g][s]);
-                                __syncwarp();
+                            if (j == nfwd) {
+                                if (fwd) {  // the forward's bulk stores are in global memory
+                                    if (lane == 0) umma::bulk_wait_all();
+                                    __syncwarp();
+                                }
+                                if (!resident(m - 1)) load_h(g, tl[g], m - 1);
                             }
+                            // prefetch H_{m-2} into the slot H_m freed (its readers were stage m + 1)
+                            if (m - 2 >= -1 && !resident(m - 2)) load_h(g, tl[g], m - 2);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
 #endif
-                            if (m + 1 <= L - 1) {  // deferred dW_{m+1} (needs H_m)
-                                if (!resident(m)) {
-                                    umma::mbar_wait(&ldbar[g][m & 1], ph_ld[g][m & 1]);
-                                    ph_ld[g][m & 1] ^= 1;
-                                }
-                                issue_dw(g, m + 1, sbase + C.ring[g][m & 1]);
+                            const int sh = (m - 1) & 1;
+                            if (!resident(m - 1)) {
+                                umma::mbar_wait(&ldbar[g][sh], ph_ld[g][sh]);
+                                ph_ld[g][sh] ^= 1;
                             }
-                            if (m >= 1) {  // dH_m = dZ_m W_m  (N = din_m)
+                            if (m >= 1 || dx) {  // dH_m (m = 0: gradient wrt the input, dx mode)
                                 const int di = n.din[m], dout = n.dout[m];
                                 const uint32_t id = umma::idesc_bf16(128, di, false, true);
-                                const uint32_t dzt = sbase + C.dz[g][dzslot(m)];
+                                const uint32_t dzt = sbase + C.dz[g];
                                 for (int kb = 0; kb < dout / 16; ++kb)
                                     umma::mma_bf16_warp(zt, umma::desc_kmajor(dzt, dout, kb),
-                                                   umma::desc_mnmajor(sbase + C.wt[m], di, kb), id, kb > 0);
-                            } else if (dx) {  // dH_0 = dZ_0 W_0: gradient wrt the input (dW_0 next job)
-                                const int di = n.din[0], dout = n.dout[0];
-                                const uint32_t id = umma::idesc_bf16(128, di, false, true);
-                                const uint32_t dzt = sbase + C.dz[g][dzslot(0)];
-                                for (int kb = 0; kb < dout / 16; ++kb)
-                                    umma::mma_bf16_warp(zt, umma::desc_kmajor(dzt, dout, kb),
-                                                   umma::desc_mnmajor(sbase + C.wt[0], di, kb), id, kb > 0);
-                            } else {
-                                issue_dw(g, 0, sbase + C.x[g]);
+                                                        umma::desc_mnmajor(sbase + C.wt[m], di, kb), id, kb > 0);
                             }
+                            issue_dw(g, m, sbase + C.ring[g][sh]);
                             umma::commit_warp(&mma_done[g]);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
@@ -310,6 +326,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     }
                 }
             }
+            if (lane == 0) umma::bulk_wait_all();  // values pass: saved activations written, slots read
+            __syncwarp();
         }
     } else {
         // ================================================================ epilogue groups
@@ -369,29 +387,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             mydb[layer * kMaxW + c0 + lane] += sum;
         };
         bool first = true;
-        if (xpre) fetch_x(2 * static_cast<int64_t>(blockIdx.x) + g);
-        for (int64_t tile = 2 * static_cast<int64_t>(blockIdx.x) + g; tile < ntiles; tile += 2 * G) {
+        uint8_t* const xs = smem + C.ring[g][1];  // the input tile X lives in ring slot 1
+        if (xpre && fwd) fetch_x(kGroups * static_cast<int64_t>(blockIdx.x) + g);
+        for (int64_t tile = kGroups * static_cast<int64_t>(blockIdx.x) + g; tile < ntiles; tile += kGroups * G) {
             const int64_t row = tile * kRows + r;
             const bool valid = row < a.rows;
-            if (learn && !first) wait_mma();  // previous tile's last MMAs (dW_0) released X and dZ
+            // previous tile's last MMAs (dW_0) released X and dZ (dx mode: waited by its epilogue)
+            if (learn && !first && !dx) wait_mma();
             first = false;
-            // ---- input tile (f32 -> bf16)
-            if (!xpre) {
+            // ---- input tile (f32 -> bf16); learn-reuse: X comes from the values pass's save area
+            if (!fwd) {
+            } else if (!xpre) {
                 for (int c0 = 0; c0 < din0; c0 += 8) {
                     float u[8];
                     for (int j = 0; j < 8; ++j) {
                         const int c = c0 + j;
                         u[j] = (valid && c < a.in_cols) ? a.X[row * a.in_cols + c] : 0.0f;
                     }
-                    umma::st_row8(smem + C.x[g], din0, r, c0, u);
+                    umma::st_row8(xs, din0, r, c0, u);
                 }
             } else {
 #pragma unroll
                 for (int c0 = 0; c0 < kXPre; c0 += 8)
                     if (c0 < din0)
-                        *reinterpret_cast<uint4*>(smem + C.x[g] + umma::tile_offset(r, c0, din0)) =
+                        *reinterpret_cast<uint4*>(xs + umma::tile_offset(r, c0, din0)) =
                             make_uint4(xnext[c0 / 2], xnext[c0 / 2 + 1], xnext[c0 / 2 + 2], xnext[c0 / 2 + 3]);
-                fetch_x(tile + 2 * G);
+                fetch_x(tile + kGroups * G);
             }
             int act_r = 0;
             float lpo_r = 0.0f, adv_r = 0.0f, ret_r = 0.0f, val_r = 0.0f;
@@ -413,19 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     const float* bl = bias + l * kMaxW;
                     if (l + 1 < L) {
                         uint8_t* dst = smem + C.ring[g][l & 1];
-                        // the same 16-byte chunks also go to global memory (the smem image of the
-                        // tile): this group's scratch (learn: reloaded by the backward) or the
-                        // values pass's save area (the critic learn's input)
-                        uint8_t* gdst = nullptr;
-                        if (learn) {
-                            if (!resident(l)) gdst = a.hscratch + static_cast<size_t>(2 * blockIdx.x + g) * C.hbytes;
-                        } else if (a.hsave && tile < a.save_tiles) {
-                            gdst = a.hsave + static_cast<size_t>(tile) * C.hbytes;
-                        }
-                        if (gdst) gdst += C.hoff[l];
-                        // the bulk store that read this ring slot two layers ago must be done
-                        if (lane == 0) umma::bulk_wait_read();
-                        __syncwarp();
+                        // (the producer bulk-stores the finished tile for the backward / critic learn)
                         // 32 columns of H_l = act(Z + b); FULL: no per-chunk guards, so the
                         // compiler interleaves the four 8-column chains
                         auto half = [&]<bool FULL>(int h0) {
@@ -479,13 +488,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #ifdef FLW_LEARN_TRACE
                         if (trf) tr_f[3][nf_ev] = clock64();
 #endif
-                        // this warp's 32 rows of the tile image are contiguous (4 core-matrix row
-                        // blocks): one TMA bulk store, off the epilogue's critical path
-                        if (gdst && lane == 0) {
-                            const uint32_t wb = static_cast<uint32_t>(dout) * 64u, wo = static_cast<uint32_t>(q) * wb;
-                            umma::bulk_s2g(gdst + wo, dst + wo, wb);
-                            umma::bulk_commit();
-                        }
 #ifdef FLW_LEARN_TRACE
                         if (trf) tr_f[4][nf_ev++] = clock64();
 #endif
@@ -568,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     }
                 }
                 const int wo = n.dout[L - 1];
-                uint8_t* dst = smem + C.dz[g][dzslot(L - 1)];
+                uint8_t* dst = smem + C.dz[g];
 #pragma unroll
                 for (int c0 = 0; c0 < 16; c0 += 8) {
                     if (c0 < wo) {
@@ -578,11 +580,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                         umma::st_row8(dst, wo, r, c0, dz + c0);
                     }
                 }
-                // the tile's global activation images (written during the forward) -> visible to
-                // the producer's TMA bulk loads of the backward, which all follow this arrival
-                if (lane == 0) umma::bulk_wait_all();  // the forward's bulk stores are in global memory
-                __syncwarp();
-                asm volatile("fence.proxy.async.global;\n" ::: "memory");
                 signal();  // dZ_{L-1} ready
                 colsum32(dz, 0, wo, L - 1);
             }
@@ -596,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     ph_ld[s] ^= 1;
                 }
                 const uint8_t* hs = smem + C.ring[g][s];
-                uint8_t* dst = smem + C.dz[g][dzslot(m - 1)];
+                uint8_t* dst = smem + C.dz[g];
                 auto half = [&]<bool FULL, int h0>() {
                     float gv[32];
                     umma::tmem_ld16(zt + h0, gv);
@@ -643,8 +640,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                 }
 
             }
+            if (!resident(-1) && !dx) ph_ld[1] ^= 1;  // X's reload (stage 0): consumed by the producer only
             if (dx) {  // dZ wrt the input pre-activation: dH_0 * act'(X), X = the input tile (bf16)
                 wait_mma();
+                if (!resident(-1)) {
+                    umma::mbar_wait(&ldbar[g][1], ph_ld[1]);
+                    ph_ld[1] ^= 1;
+                }
                 const int di = n.din[0];
                 for (int h0 = 0; h0 < di; h0 += 32) {
                     float gv[32];
@@ -653,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     for (int c = 0; c < 32; c += 8) {
                         if (h0 + c < di) {
                             float y[8];
-                            umma::ld_row8(smem + C.x[g], di, r, h0 + c, y);
+                            umma::ld_row8(xs, di, r, h0 + c, y);
 #pragma unroll
                             for (int i = 0; i < 8; ++i) {
                                 const int col = h0 + c + i;
@@ -664,11 +666,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                         }
                     }
                 }
-                signal();
             }
         }
-        if (lane == 0) umma::bulk_wait_all();  // values pass: the saved activations are written
-        if (learn && !first) wait_mma();  // the last tile's dW_0
+        if (learn && !first && !dx) wait_mma();  // the last tile's dW_0
         // ---- loss partials of this warp
         for (int off = 16; off > 0; off >>= 1) {
             pl_acc += __shfl_xor_sync(0xffffffffu, pl_acc, off);
@@ -690,13 +690,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     if (learn && w < kEpiWarps) {
         const int q = w & 3, half = w >> 2;
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
-        const bool any = 2 * static_cast<int64_t>(blockIdx.x) < ntiles;
+        const bool any = kGroups * static_cast<int64_t>(blockIdx.x) < ntiles;
         float* part = a.partials + static_cast<int64_t>(blockIdx.x) * a.part_stride;
         for (int l = 0; l < L; ++l) {
             const int dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
             const int lo = (l & 1) ? 16 : 0;
-            const uint32_t col = 128u + 64u * static_cast<uint32_t>(l >> 1);
-            for (int c0 = 16 * half; c0 < dout; c0 += 32) {
+            const uint32_t col = 64u * kGroups + 64u * static_cast<uint32_t>(l >> 1);
+            for (int c0 = 16 * half; c0 < dout; c0 += 16 * kGroups) {
                 float v[16];
                 umma::tmem_ld16(tmem + lane_base + col + c0, v);
                 umma::tmem_ld_wait();
@@ -748,6 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 
 size_t fast_learn_smem_bytes(const FastNet& n) { return carve_learn(n).total; }
 size_t fast_learn_scratch_bytes(const FastNet& n) { return carve_learn(n).hbytes; }
+int fast_learn_groups() { return kGroups; }
 
 void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid) {
     const size_t smem = carve_learn(a.net).total;

@@ -218,9 +218,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                              : a.hscratch + static_cast<size_t>(kGroups * blockIdx.x + g) * C.hbytes;
             };
             auto load_h = [&](int g, int64_t tile, int k) {  // H_k (k = -1: X) -> ring slot k & 1
-                if (umma::elect_one())
-                    bulk_load(smem + C.ring[g][k & 1], hsrc(g, tile) + C.hoff[k + 1],
-                              static_cast<uint32_t>(kRows * hwidth(k) * 2), &ldbar[g][k & 1]);
+                if (umma::elect_one()) {
+                    const uint32_t bytes = static_cast<uint32_t>(kRows * hwidth(k) * 2);
+                    umma::mbar_expect_tx(&ldbar[g][k & 1], bytes);
+                    umma::bulk_g2s_hint(smem + C.ring[g][k & 1], hsrc(g, tile) + C.hoff[k + 1], bytes,
+                                        &ldbar[g][k & 1], umma::policy_evict_first());  // read once
+                }
                 __syncwarp();
             };
             auto issue_dw = [&](int g, int l, uint32_t hin) {  // dW_l += H_{l-1}^T dZ_l  (M = din_l)
@@ -267,9 +270,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                                     gdst = a.hsave + static_cast<size_t>(tl[g]) * C.hbytes;
                                 }
                                 if (lane == 0) {
-                                    if (gdst) {
-                                        umma::bulk_s2g(gdst + C.hoff[hk + 1], smem + C.ring[g][hk & 1],
-                                                       static_cast<uint32_t>(kRows * hwidth(hk) * 2));
+                                    if (gdst) {  // the critic learn re-reads the values pass's tiles: keep in L2
+                                        umma::bulk_s2g_hint(gdst + C.hoff[hk + 1], smem + C.ring[g][hk & 1],
+                                                            static_cast<uint32_t>(kRows * hwidth(hk) * 2),
+                                                            learn ? umma::policy_evict_first() : umma::policy_evict_last());
                                         umma::bulk_commit();
                                     }
                                     // every older store has read its slot: the epilogue may overwrite

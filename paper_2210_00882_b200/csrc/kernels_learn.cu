@@ -89,6 +89,12 @@ __host__ __device__ inline Carve carve_learn(const FastNet& n) {
     return c;
 }
 
+// Marks a value warp-uniform for ptxas (a lane-0 broadcast): descriptors and TMEM addresses built
+// from such values stay in uniform registers, so each tcgen05.mma issues without per-operand
+// R2UR.BROADCAST moves.
+__device__ __forceinline__ uint32_t uni(uint32_t x) { return __shfl_sync(0xffffffffu, x, 0); }
+__device__ __forceinline__ int uni(int x) { return __shfl_sync(0xffffffffu, x, 0); }
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_u32(bar)) : "memory");
 }
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     const FastNet& n = a.net;
     if (threadIdx.x == 0) C = carve_learn(n);
     __syncthreads();
-    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    const int t = threadIdx.x, w = uni(static_cast<int>(t >> 5)), lane = t & 31;
     const int L = n.L;
     const int64_t ntiles = (a.rows + kRows - 1) / kRows;
     const int G = gridDim.x;
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
-    const uint32_t tmem = tslot;
+    const uint32_t tmem = uni(tslot);
     const uint32_t sbase = umma::smem_u32(smem);
 
     if (w == kEpiWarps) {
@@ -228,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             };
             auto issue_dw = [&](int g, int l, uint32_t hin) {  // dW_l += H_{l-1}^T dZ_l  (M = din_l)
                 const int di = n.din[l], dout = n.dout[l];
-                const uint32_t dzt = sbase + C.dz[g];
+                const uint32_t dzt = uni(sbase + C.dz[g]);
                 const uint32_t id = umma::idesc_bf16(64, dout, true, true);
                 for (int kb = 0; kb < kRows / 16; ++kb) {
                     umma::mma_bf16_warp(dw_tmem(l), umma::desc_mnmajor(hin, di, kb), umma::desc_mnmajor(dzt, dout, kb),
@@ -282,11 +288,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                                 }
                                 __syncwarp();
                             }
-                            const uint32_t in = sbase + C.ring[g][(l - 1) & 1];
+                            const uint32_t in = uni(sbase + C.ring[g][(l - 1) & 1]);
+                            const uint32_t wl = uni(sbase + C.wt[l]);
                             const uint32_t id = umma::idesc_bf16(128, dout, false, false);
                             for (int kb = 0; kb < di / 16; ++kb)
                                 umma::mma_bf16_warp(zt, umma::desc_kmajor(in, di, kb),
-                                               umma::desc_kmajor(sbase + C.wt[l], di, kb), id, kb > 0);
+                                               umma::desc_kmajor(wl, di, kb), id, kb > 0);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[3][np_ev] = clock64();
 #endif
@@ -316,12 +323,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                             if (m >= 1 || dx) {  // dH_m (m = 0: gradient wrt the input, dx mode)
                                 const int di = n.din[m], dout = n.dout[m];
                                 const uint32_t id = umma::idesc_bf16(128, di, false, true);
-                                const uint32_t dzt = sbase + C.dz[g];
+                                const uint32_t dzt = uni(sbase + C.dz[g]), wm = uni(sbase + C.wt[m]);
                                 for (int kb = 0; kb < dout / 16; ++kb)
                                     umma::mma_bf16_warp(zt, umma::desc_kmajor(dzt, dout, kb),
-                                                        umma::desc_mnmajor(sbase + C.wt[m], di, kb), id, kb > 0);
+                                                        umma::desc_mnmajor(wm, di, kb), id, kb > 0);
                             }
-                            issue_dw(g, m, sbase + C.ring[g][sh]);
+                            issue_dw(g, m, uni(sbase + C.ring[g][sh]));
                             umma::commit_warp(&mma_done[g]);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();

@@ -923,6 +923,13 @@ void Engine::enq_grad_sync_and_adam() {
         a.b2 = 0.999;
         a.eps = 1e-8;
         a.gscale = 1.0 / static_cast<double>(p2p_k_);
+        if (!cfast_) {  // the exchange's Adam also refreshes the weight images
+            a.pol = b.pol;
+            a.crit = b.crit;
+            a.img_p = b.wimg_p;
+            a.img_c = b.wimg_c;
+            prev_fused_ = true;
+        }
         coll_tick(stream_, b.ctx);
         probe_begin("exchange_adam");
         reduce_allreduce_adam(stream_, a);

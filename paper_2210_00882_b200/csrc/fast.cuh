@@ -75,6 +75,23 @@ size_t fast_learn_smem_bytes(const FastNet& n);
 size_t fast_learn_scratch_bytes(const FastNet& n);  // hidden bytes of one 128-row tile
 int fast_learn_groups();  // tiles in flight per k_learn CTA
 // fixed-order sums of the per-CTA partial slots: np policy slots, nc critic slots
+// Element index of flat parameter p (absolute, params layout) in its net's bf16 weight-tile image
+// (W_l^T as [dout x din] K-major core-matrix tiles at 128-byte aligned per-layer offsets, the
+// layout k_build_wimg writes), or -1 when p is not a weight of this net.
+__host__ __device__ inline int64_t wimg_elem(const FastNet& n, int64_t p) {
+    uint32_t off = 0;
+    for (int l = 0; l < n.L; ++l) {
+        const int64_t r = p - n.woff[l];
+        if (r >= 0 && r < static_cast<int64_t>(n.rin[l]) * n.rout[l]) {
+            const int c = static_cast<int>(r / n.rout[l]), o = static_cast<int>(r % n.rout[l]), C = n.din[l];
+            const uint32_t t = static_cast<uint32_t>((o >> 3) * (C * 16) + (c >> 3) * 128 + (o & 7) * 16 + (c & 7) * 2);
+            return static_cast<int64_t>((off + t) / 2);
+        }
+        off = (off + static_cast<uint32_t>(n.dout[l] * n.din[l] * 2) + 127u) / 128u * 128u;
+    }
+    return -1;
+}
+
 struct DeviceCtx;
 struct FastUpdateArgs {      // k_reduce_adam: partial reduction + Adam + weight image, one launch
     const float *pp, *pc;    // per-CTA dW partials of the policy / critic learn kernels

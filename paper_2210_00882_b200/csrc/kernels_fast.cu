@@ -138,15 +138,8 @@ __global__ void __launch_bounds__(256) k_reduce_adam(FastUpdateArgs a) {
         a.params[i] = next;
         // weight-image entry (biases are read from params by the learn kernels)
         const bool pol = i < a.Pp;
-        const FastNet& n = pol ? a.pol : a.crit;
-        for (int l = 0; l < n.L; ++l) {
-            const int64_t r = i - n.woff[l];
-            if (r >= 0 && r < static_cast<int64_t>(n.rin[l]) * n.rout[l]) {
-                const int c = static_cast<int>(r / n.rout[l]), o = static_cast<int>(r % n.rout[l]);
-                const Smem S = carve(n);
-                (pol ? a.img_p : a.img_c)[(S.wt[l] + umma::tile_offset(o, c, n.din[l])) / 2] = __float2bfloat16(next);
-            }
-        }
+        const int64_t e = wimg_elem(pol ? a.pol : a.crit, i);
+        if (e >= 0) (pol ? a.img_p : a.img_c)[e] = __float2bfloat16(next);
     }
     __syncthreads();
     if (threadIdx.x == 0) {

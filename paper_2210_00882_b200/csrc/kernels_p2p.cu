@@ -100,6 +100,11 @@ __global__ void __launch_bounds__(32) k_sum_adam(P2pArgs a) {
     const double next = __dsub_rn(static_cast<double>(a.params[i]),
                                   __ddiv_rn(__dmul_rn(a.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), a.eps)));
     a.params[i] = static_cast<float>(next);
+    if (a.img_p) {  // weight-image entry for the next train iteration's learn kernels
+        const bool pol = i < a.Pp;
+        const int64_t e = wimg_elem(pol ? a.pol : a.crit, i);
+        if (e >= 0) (pol ? a.img_p : a.img_c)[e] = __float2bfloat16(static_cast<float>(next));
+    }
 }
 
 }  // namespace

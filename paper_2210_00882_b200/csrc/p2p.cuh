@@ -2,8 +2,11 @@
 // reduce -> all-reduce -> Adam step of fast numerics on k GPUs.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include "fast.cuh"
 
 namespace flw {
 
@@ -26,6 +29,9 @@ struct P2pArgs {
     float* params;
     double *m, *v;
     double lr, b1, b2, eps, gscale;
+    // optional: also refresh the bf16 weight-tile images (null: the next learn rebuilds them)
+    FastNet pol, crit;
+    __nv_bfloat16 *img_p, *img_c;
 };
 
 void coll_tick(cudaStream_t s, DeviceCtx* ctx);  // ++ctx->coll_seq (one per exchange)

@@ -1,10 +1,12 @@
 // Fast-numerics rollout: the whole episode's T steps in ONE launch. Each CTA owns 32 envs for
 // the whole episode; per step it runs
-//   policy MLP   on the tensor cores with f32 accuracy: mma.sync m16n8k8 TF32 in the 3xTF32 split
-//                (x = hi + lo; x.w ~ lo.hi + hi.lo + hi.hi, f32 accumulate), so the logits keep
-//                ~2^-20 relative error. Warp w owns env rows [16(w%2), +16) and output tiles w/2
-//                and w/2 + 4 of every layer (8 warps for 32 envs); activations and W^T in shared
-//                memory with row strides = 4 (mod 32) (conflict-free fragment loads)
+//   policy MLP   on the tensor cores with f32 accuracy: mma.sync m16n8k16 F16 in a 3-term split
+//                (x = hi + lo, hi = f16(x), lo = f16(x - hi), carrying ~22 significant bits;
+//                x.w ~ lo.hi + hi.lo + hi.hi with f32 accumulation). Weights are split once per
+//                launch and activations when they are produced, so the MMA loop only loads
+//                fragments. Warp w owns env rows [16(w%2), +16) and output tiles w/2, w/2 + 4 of
+//                every layer (8 warps for 32 envs); fragment row strides = 8 (mod 64) halves
+//                (conflict-free loads). Valid for |activations|, |obs|, |weights| < 65504 (f16).
 //   PolicyApply  one thread per env (warp 0): the reference's double-precision softmax /
 //                inverse-CDF sampling on the f32 logits (interp.cpp:175-203)
 //   EnvStep      same thread, env state in its registers, bit-exact double dynamics (envs.cuh)
@@ -13,6 +15,9 @@
 // activations between steps. The rollout is a chain of T x L dependent layers over only 32 envs
 // per CTA, so it is latency-bound: a tcgen05 tile (M >= 64 rows per CTA, TMEM round trip per
 // layer) would idle more than half the SMs at E = 4096; the warp-level MMA keeps all CTAs busy.
+// The legacy MMA issues at <= 0.5 instructions/clk per SM for both m16n8k8 TF32 and m16n8k16
+// F16 (profiles/r01_mma_sync_rate.txt), so the F16 split does the same work in half the MMAs.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -30,32 +35,47 @@ constexpr int kEnvsPerCta = FLW_ROLLOUT_EPC;  // 16 or 32 (A/B: -DFLW_ROLLOUT_EP
 constexpr int kMT = kEnvsPerCta / 16;          // 16-row MMA tiles of envs
 constexpr int kWarps = 4 * kMT;                // warp (mt, nt0): output tiles nt0 and nt0 + 4
 constexpr int kThreads = 32 * kWarps;
-constexpr int kHStride = 68;  // hidden activation row stride (floats): >= 64, = 4 (mod 32)
+constexpr int kLStride = 20;  // f32 logits row stride (floats, >= 16)
 
 __host__ __device__ inline int pad8(int x) { return (x + 7) & ~7; }
-// row stride (floats) of a [rows x k] f32 matrix read as MMA fragments: >= pad8(k), = 4 (mod 32)
-__host__ __device__ inline int kstride(int k) { return ((pad8(k) + 31) & ~31) + 4; }
+__host__ __device__ inline int pad16(int x) { return (x + 15) & ~15; }
+// row stride (halves) of an f16 [rows x k] matrix read as MMA fragments: >= pad16(k), = 8 (mod 64)
+__host__ __device__ inline int hstride(int k) { return ((pad16(k) + 63) & ~63) + 8; }
 
 struct RolloutSmem {
-    uint32_t w[kMaxLayers], b[kMaxLayers], x, h[2], total;
+    uint32_t whi[kMaxLayers], wlo[kMaxLayers], b[kMaxLayers];
+    uint32_t xhi, xlo, hhi[2], hlo[2], logits, total;
 };
 
-// W_l^T stored [pad8(out) x kstride(in)] (zero padded): row n = the weights of output n.
+// W_l^T as f16 hi / lo [pad8(out) x hstride(in)] (zero padded): row n = the weights of output n.
 __host__ __device__ inline RolloutSmem rollout_carve(const FastRolloutArgs& a) {
     RolloutSmem s{};
     uint32_t off = 0;
     for (int l = 0; l < a.L; ++l) {
-        s.w[l] = off;
-        off += static_cast<uint32_t>(pad8(a.dims[l + 1]) * kstride(a.dims[l]) * 4);
+        const uint32_t wb = static_cast<uint32_t>(pad8(a.dims[l + 1]) * hstride(a.dims[l]) * 2);
+        s.whi[l] = off;
+        off += wb;
+        s.wlo[l] = off;
+        off += wb;
         s.b[l] = off;
         off += static_cast<uint32_t>(pad8(a.dims[l + 1]) * 4);
     }
-    s.x = off;
-    off += static_cast<uint32_t>(kEnvsPerCta * kstride(a.dims[0]) * 4);
-    s.h[0] = off;
-    off += kEnvsPerCta * kHStride * 4;
-    s.h[1] = off;
-    off += kEnvsPerCta * kHStride * 4;
+    const uint32_t xb = static_cast<uint32_t>(kEnvsPerCta * hstride(a.dims[0]) * 2);
+    s.xhi = off;
+    off += xb;
+    s.xlo = off;
+    off += xb;
+    int hmax = 8;
+    for (int l = 1; l < a.L; ++l) hmax = a.dims[l] > hmax ? a.dims[l] : hmax;
+    const uint32_t hb = static_cast<uint32_t>(kEnvsPerCta * hstride(hmax) * 2);
+    for (int i = 0; i < 2; ++i) {
+        s.hhi[i] = off;
+        off += hb;
+        s.hlo[i] = off;
+        off += hb;
+    }
+    s.logits = off;
+    off += kEnvsPerCta * kLStride * 4;
     s.total = off;
     return s;
 }
@@ -71,31 +91,21 @@ __device__ __forceinline__ float tanh_mufu(float x) {
     return y;
 }
 
-// x = hi + lo: hi = x truncated to TF32 (19 bits), lo = x - hi exactly (|lo| < 2^-10 |x|); the
-// tensor core reads lo's top 19 bits, so x is carried to ~2^-20 relative. Two instructions
-// (cvt.rna.tf32.f32 is a 4-instruction sequence on sm_100a).
-__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-    hi = __float_as_uint(x) & 0xFFFFE000u;
-    lo = __float_as_uint(x - __uint_as_float(hi));
+// (x0, x1) -> f16x2 hi = rn(x), lo = rn(x - hi)
+__device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(x0, x1);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
-__device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, const uint32_t* b) {
+__device__ __forceinline__ void mma_f16(float* d, const uint32_t* a, const uint32_t* b) {
     asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
-}
-
-// acc += A[16 x 8] . W^T tile (8 outputs) in 3xTF32; A fragment already split.
-__device__ __forceinline__ void mma3(float* acc, const uint32_t* ahi, const uint32_t* alo, const float* wrow,
-                                     int kc) {
-    uint32_t bhi[2], blo[2];
-    split_tf32(wrow[kc], bhi[0], blo[0]);
-    split_tf32(wrow[kc + 4], bhi[1], blo[1]);
-    mma_tf32(acc, alo, bhi);
-    mma_tf32(acc, ahi, blo);
-    mma_tf32(acc, ahi, bhi);
 }
 
 template <int ENV>
@@ -105,21 +115,27 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int64_t E = a.E, e0 = static_cast<int64_t>(blockIdx.x) * kEnvsPerCta;
     const int S_ = a.S, A = a.A;
-    const int xs = kstride(a.dims[0]);
-    // weights: W_l^T [pad8(out) x kstride(in)], zero padded
+    const int xs = hstride(a.dims[0]);
+    int hmax = 8;
+    for (int l = 1; l < a.L; ++l) hmax = a.dims[l] > hmax ? a.dims[l] : hmax;
+    const int hs = hstride(hmax);
+    // weights: W_l^T [pad8(out) x hstride(in)] f16 hi / lo, zero padded (split once per launch)
     for (int l = 0; l < a.L; ++l) {
-        const int in = a.dims[l], out = a.dims[l + 1], ks = kstride(in), op = pad8(out);
-        float* W = reinterpret_cast<float*>(smem + S.w[l]);
+        const int in = a.dims[l], out = a.dims[l + 1], ks = hstride(in), op = pad8(out);
+        __half* Wh = reinterpret_cast<__half*>(smem + S.whi[l]);
+        __half* Wl = reinterpret_cast<__half*>(smem + S.wlo[l]);
         float* B = reinterpret_cast<float*>(smem + S.b[l]);
         for (int i = t; i < op * ks; i += kThreads) {
             const int o = i / ks, ii = i % ks;
-            W[i] = (o < out && ii < in) ? a.params[a.woff[l] + ii * out + o] : 0.0f;
+            const float w = (o < out && ii < in) ? a.params[a.woff[l] + ii * out + o] : 0.0f;
+            const __half h = __float2half_rn(w);
+            Wh[i] = h;
+            Wl[i] = __float2half_rn(w - __half2float(h));
         }
         for (int o = t; o < op; o += kThreads) B[o] = o < out ? a.params[a.boff[l] + o] : 0.0f;
     }
     // zero the activation buffers once: padded input columns must read as 0
-    for (int i = t; i < kEnvsPerCta * xs + 2 * kEnvsPerCta * kHStride; i += kThreads)
-        reinterpret_cast<float*>(smem + S.x)[i] = 0.0f;
+    for (uint32_t i = t; i < (S.logits - S.xhi) / 4; i += kThreads) reinterpret_cast<uint32_t*>(smem + S.xhi)[i] = 0u;
     __syncthreads();
     // ---- env owner threads (warp 0): env state in registers
     const bool owner = t < kEnvsPerCta;
@@ -131,18 +147,25 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     for (int j = 0; j < SW; ++j) st[j] = 0.0;
     bool done = false;
     int32_t stepc = 0;
-    float* xb = reinterpret_cast<float*>(smem + S.x);
+    __half* xhi = reinterpret_cast<__half*>(smem + S.xhi);
+    __half* xlo = reinterpret_cast<__half*>(smem + S.xlo);
+    auto put_obs = [&](int j, float o) {  // next layer-0 input, split
+        const __half h = __float2half_rn(o);
+        xhi[t * xs + j] = h;
+        xlo[t * xs + j] = __float2half_rn(o - __half2float(h));
+    };
     if (live) {
 #pragma unroll
         for (int j = 0; j < SW; ++j) st[j] = a.est[j * E + e];
         done = a.done[e] != 0;
         stepc = a.stepc[e];
-        for (int j = 0; j < S_; ++j) xb[t * xs + j] = a.states[(a.step0 * E + e) * S_ + j];
+        for (int j = 0; j < S_; ++j) put_obs(j, a.states[(a.step0 * E + e) * S_ + j]);
     }
     __syncthreads();
     const uint64_t ep = static_cast<uint64_t>(ctx->episode);
     const int mt = warp % kMT, nt0 = warp / kMT;
-    const int ar = 16 * mt + (lane >> 2), ac = lane & 3;  // fragment row / k-column of this lane
+    const int g8 = lane >> 2, c4 = lane & 3;
+    const int ar = 16 * mt + g8;  // fragment row of this lane (and ar + 8)
 
 #ifdef FLW_LEARN_TRACE
     long long tr0[8], tr1[8], tr2[8];
@@ -152,40 +175,56 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
         if (step - a.step0 < 8) tr0[step - a.step0] = clock64();
 #endif
         for (int l = 0; l < a.L; ++l) {
-            const int in = a.dims[l], out = a.dims[l + 1], KT = pad8(in) / 8, NT = pad8(out) / 8;
-            const float* Ain = l == 0 ? xb : reinterpret_cast<const float*>(smem + S.h[(l - 1) & 1]);
-            const int as = l == 0 ? xs : kHStride;
-            const float* W = reinterpret_cast<const float*>(smem + S.w[l]);
+            const int in = a.dims[l], out = a.dims[l + 1], KT = pad16(in) / 16, NT = pad8(out) / 8;
+            const bool first = l == 0, last = l + 1 == a.L;
+            const uint32_t* Ahi = reinterpret_cast<const uint32_t*>(smem + (first ? S.xhi : S.hhi[(l - 1) & 1]));
+            const uint32_t* Alo = reinterpret_cast<const uint32_t*>(smem + (first ? S.xlo : S.hlo[(l - 1) & 1]));
+            const int as2 = (first ? xs : hs) / 2;  // row stride in 32-bit words
+            const int ws2 = hstride(in) / 2;
+            const uint32_t* Whi = reinterpret_cast<const uint32_t*>(smem + S.whi[l]);
+            const uint32_t* Wlo = reinterpret_cast<const uint32_t*>(smem + S.wlo[l]);
             const float* B = reinterpret_cast<const float*>(smem + S.b[l]);
-            float* Out = reinterpret_cast<float*>(smem + S.h[l & 1]);
-            const int ws = kstride(in);
-            const bool last = l + 1 == a.L;
             if (nt0 < NT) {
                 const bool two = nt0 + 4 < NT;
                 float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
-                const float* w0 = W + (8 * nt0 + (lane >> 2)) * ws + ac;
-                const float* w1 = w0 + 32 * ws;
-                const float* a0 = Ain + ar * as + ac;
-#pragma unroll 4
+                const int aoff = ar * as2 + c4, w0off = (8 * nt0 + g8) * ws2 + c4, w1off = w0off + 32 * ws2;
+#pragma unroll 2
                 for (int k = 0; k < KT; ++k) {
-                    uint32_t ahi[4], alo[4];
-                    split_tf32(a0[8 * k], ahi[0], alo[0]);
-                    split_tf32(a0[8 * k + 8 * as], ahi[1], alo[1]);
-                    split_tf32(a0[8 * k + 4], ahi[2], alo[2]);
-                    split_tf32(a0[8 * k + 8 * as + 4], ahi[3], alo[3]);
-                    mma3(acc0, ahi, alo, w0, 8 * k);
-                    if (two) mma3(acc1, ahi, alo, w1, 8 * k);
+                    const int ko = 8 * k;  // 16 halves = 8 words
+                    const uint32_t ahi[4] = {Ahi[aoff + ko], Ahi[aoff + ko + 8 * as2], Ahi[aoff + ko + 4],
+                                             Ahi[aoff + ko + 8 * as2 + 4]};
+                    const uint32_t alo[4] = {Alo[aoff + ko], Alo[aoff + ko + 8 * as2], Alo[aoff + ko + 4],
+                                             Alo[aoff + ko + 8 * as2 + 4]};
+                    const uint32_t bhi[2] = {Whi[w0off + ko], Whi[w0off + ko + 4]};
+                    const uint32_t blo[2] = {Wlo[w0off + ko], Wlo[w0off + ko + 4]};
+                    mma_f16(acc0, alo, bhi);
+                    mma_f16(acc0, ahi, blo);
+                    mma_f16(acc0, ahi, bhi);
+                    if (two) {
+                        const uint32_t chi[2] = {Whi[w1off + ko], Whi[w1off + ko + 4]};
+                        const uint32_t clo[2] = {Wlo[w1off + ko], Wlo[w1off + ko + 4]};
+                        mma_f16(acc1, alo, chi);
+                        mma_f16(acc1, ahi, clo);
+                        mma_f16(acc1, ahi, chi);
+                    }
                 }
                 auto store = [&](const float* acc, int nt) {
-                    const int n = 8 * nt + 2 * ac;
+                    const int n = 8 * nt + 2 * c4;
                     const float b0 = B[n], b1 = B[n + 1];
                     float v[4] = {acc[0] + b0, acc[1] + b1, acc[2] + b0, acc[3] + b1};
-                    if (!last) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) v[j] = a.act == 0 ? tanh_mufu(v[j]) : fmaxf(v[j], 0.0f);
+                    if (last) {  // f32 logits for the owner threads
+                        float* lg = reinterpret_cast<float*>(smem + S.logits);
+                        *reinterpret_cast<float2*>(lg + ar * kLStride + n) = make_float2(v[0], v[1]);
+                        *reinterpret_cast<float2*>(lg + (ar + 8) * kLStride + n) = make_float2(v[2], v[3]);
+                        return;
                     }
-                    *reinterpret_cast<float2*>(Out + ar * kHStride + n) = make_float2(v[0], v[1]);
-                    *reinterpret_cast<float2*>(Out + (ar + 8) * kHStride + n) = make_float2(v[2], v[3]);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = a.act == 0 ? tanh_mufu(v[j]) : fmaxf(v[j], 0.0f);
+                    uint32_t* Ohi = reinterpret_cast<uint32_t*>(smem + S.hhi[l & 1]);
+                    uint32_t* Olo = reinterpret_cast<uint32_t*>(smem + S.hlo[l & 1]);
+                    const int o2 = n / 2;
+                    split_f16x2(v[0], v[1], Ohi[ar * (hs / 2) + o2], Olo[ar * (hs / 2) + o2]);
+                    split_f16x2(v[2], v[3], Ohi[(ar + 8) * (hs / 2) + o2], Olo[(ar + 8) * (hs / 2) + o2]);
                 };
                 store(acc0, nt0);
                 if (two) store(acc1, nt0 + 4);
@@ -197,8 +236,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
 #endif
         // ---- PolicyApply + EnvStep: one owner thread per env
         if (owner) {
-            const float* logits = reinterpret_cast<const float*>(smem + S.h[(a.L - 1) & 1]) + t * kHStride;
-            float* h0w = xb + t * xs;  // next layer-0 input
+            const float* logits = reinterpret_cast<const float*>(smem + S.logits) + t * kLStride;
             double l[16], p[16];
             double mx = logits[0];
             for (int c = 0; c < A; ++c) {
@@ -270,13 +308,13 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                 if (ENV == 0) {
                     const float o = static_cast<float>(__ddiv_rn(st[0], __dsub_rn(st[1], 1.0)));
                     nt[0] = o;
-                    h0w[0] = o;
+                    put_obs(0, o);
                 } else {
 #pragma unroll
                     for (int i = 0; i < kSynthObs; ++i) {
                         const float o = static_cast<float>(st[i]);
                         nt[i] = o;
-                        h0w[i] = o;
+                        put_obs(i, o);
                     }
                 }
             }

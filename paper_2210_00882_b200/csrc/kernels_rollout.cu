@@ -80,8 +80,6 @@ __host__ __device__ inline RolloutSmem rollout_carve(const FastRolloutArgs& a) {
     return s;
 }
 
-__device__ __forceinline__ double dmaxd(double a, double b) { return a < b ? b : a; }
-
 // MUFU tanh (max rel. error ~2^-11): the hidden activations of the fast rollout. The sampled
 // actions stay those of the exact path except within ~1e-4 of a cumulative-probability boundary
 // (tests/test_fast_gpu.py bounds the flip rate).
@@ -236,25 +234,26 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
 #endif
         // ---- PolicyApply + EnvStep: one owner thread per env
         if (owner) {
+            // softmax in f32 (the reference's is double, rounded to f32: the probabilities differ
+            // by <= ~1 f32 ulp, far below the f32-logit deviation the fast path already has);
+            // the draw and the inverse-CDF walk are the reference's (double u, double cumsum)
             const float* logits = reinterpret_cast<const float*>(smem + S.logits) + t * kLStride;
-            double l[16], p[16];
-            double mx = logits[0];
+            float p[16];
+            float mx = logits[0];
+            for (int c = 1; c < A; ++c) mx = fmaxf(mx, logits[c]);
+            float den = 0.0f;
             for (int c = 0; c < A; ++c) {
-                l[c] = logits[c];
-                mx = dmaxd(mx, l[c]);
+                p[c] = __expf(logits[c] - mx);
+                den += p[c];
             }
-            double den = 0.0;
-            for (int c = 0; c < A; ++c) {
-                p[c] = exp(__dsub_rn(l[c], mx));  // the same value the reference computes twice
-                den = __dadd_rn(den, p[c]);
-            }
-            for (int c = 0; c < A; ++c) p[c] = f32r(__ddiv_rn(p[c], den));
+            const float rden = 1.0f / den;
+            for (int c = 0; c < A; ++c) p[c] *= rden;
             const double u = rng_uniform(
                 rng_key(a.seed, kActionStream, ep, static_cast<uint64_t>(step), static_cast<uint64_t>(a.env_lo + e)));
             double cum = 0.0;
             int chosen = A - 1;
             for (int c = 0; c < A; ++c) {
-                cum = __dadd_rn(cum, p[c]);
+                cum = __dadd_rn(cum, static_cast<double>(p[c]));
                 if (u < cum) {
                     chosen = c;
                     break;
@@ -300,7 +299,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             if (live) {
                 const int64_t ti = step * E + e;
                 a.actions[ti] = chosen;
-                a.logp[ti] = static_cast<float>(log(dmaxd(p[chosen], 1e-30)));
+                a.logp[ti] = __logf(fmaxf(p[chosen], 1e-30f));
                 a.reward[ti] = done ? 0.0f : static_cast<float>(rew);
                 a.reward_d[ti] = done ? 0.0 : rew;
                 a.done_f[ti] = (done || d) ? 1.0f : 0.0f;

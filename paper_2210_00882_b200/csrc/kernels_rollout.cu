@@ -3,10 +3,12 @@
 //   policy MLP   on the tensor cores with f32 accuracy: mma.sync m16n8k16 F16 in a 3-term split
 //                (x = hi + lo, hi = f16(x), lo = f16(x - hi), carrying ~22 significant bits;
 //                x.w ~ lo.hi + hi.lo + hi.hi with f32 accumulation). Weights are split once per
-//                launch and activations when they are produced, so the MMA loop only loads
-//                fragments. Warp w owns env rows [16(w%2), +16) and output tiles w/2, w/2 + 4 of
-//                every layer (8 warps for 32 envs); fragment row strides = 8 (mod 64) halves
-//                (conflict-free loads). Valid for |activations|, |obs|, |weights| < 65504 (f16).
+//                launch and activations when they are produced, and both live in shared memory
+//                in FRAGMENT-MAJOR order ([tile][k-step][lane] x 16 B): every MMA operand is one
+//                conflict-free 128-bit load. Warp w owns env rows [16(w%2), +16) and the output
+//                tiles 2(w/2), 2(w/2)+1 of every layer, so its two accumulator fragments ARE the
+//                next layer's A fragment for k-step w/2 (one 128-bit store each for hi and lo).
+//                Valid for |activations|, |obs|, |weights| < 65504 (f16).
 //   PolicyApply  one thread per env (warp 0): the reference's double-precision softmax /
 //                inverse-CDF sampling on the f32 logits (interp.cpp:175-203)
 //   EnvStep      same thread, env state in its registers, bit-exact double dynamics (envs.cuh)
@@ -39,40 +41,34 @@ constexpr int kLStride = 20;  // f32 logits row stride (floats, >= 16)
 
 __host__ __device__ inline int pad8(int x) { return (x + 7) & ~7; }
 __host__ __device__ inline int pad16(int x) { return (x + 15) & ~15; }
-// row stride (halves) of an f16 [rows x k] matrix read as MMA fragments: >= pad16(k), = 8 (mod 64)
-__host__ __device__ inline int hstride(int k) { return ((pad16(k) + 63) & ~63) + 8; }
+// fragment-major operand images (16 B per lane per fragment):
+//   weights of layer l: [NT = pad8(out)/8][KT = pad16(in)/16][32 lanes] x {b0 hi, b1 hi, b0 lo, b1 lo}
+//   activations:        [kMT][KT][32 lanes] x {a0..a3} for hi and for lo (separate images)
+__host__ __device__ inline uint32_t wfrag_bytes(int in, int out) {
+    return static_cast<uint32_t>((pad8(out) / 8) * (pad16(in) / 16) * 32 * 16);
+}
+__host__ __device__ inline uint32_t afrag_bytes(int k) { return static_cast<uint32_t>(kMT * (pad16(k) / 16) * 32 * 16); }
 
 struct RolloutSmem {
-    uint32_t whi[kMaxLayers], wlo[kMaxLayers], b[kMaxLayers];
-    uint32_t xhi, xlo, hhi[2], hlo[2], logits, total;
+    uint32_t w0, xhi, xlo, hhi[2], hlo[2], logits, total;  // weights: layers back to back from w0
 };
 
-// W_l^T as f16 hi / lo [pad8(out) x hstride(in)] (zero padded): row n = the weights of output n.
 __host__ __device__ inline RolloutSmem rollout_carve(const FastRolloutArgs& a) {
     RolloutSmem s{};
     uint32_t off = 0;
-    for (int l = 0; l < a.L; ++l) {
-        const uint32_t wb = static_cast<uint32_t>(pad8(a.dims[l + 1]) * hstride(a.dims[l]) * 2);
-        s.whi[l] = off;
-        off += wb;
-        s.wlo[l] = off;
-        off += wb;
-        s.b[l] = off;
-        off += static_cast<uint32_t>(pad8(a.dims[l + 1]) * 4);
-    }
-    const uint32_t xb = static_cast<uint32_t>(kEnvsPerCta * hstride(a.dims[0]) * 2);
+    s.w0 = off;
+    for (int l = 0; l < a.L; ++l) off += wfrag_bytes(a.dims[l], a.dims[l + 1]) + static_cast<uint32_t>(pad16(a.dims[l + 1]) * 4);
     s.xhi = off;
-    off += xb;
+    off += afrag_bytes(a.dims[0]);
     s.xlo = off;
-    off += xb;
-    int hmax = 8;
+    off += afrag_bytes(a.dims[0]);
+    int hmax = 16;
     for (int l = 1; l < a.L; ++l) hmax = a.dims[l] > hmax ? a.dims[l] : hmax;
-    const uint32_t hb = static_cast<uint32_t>(kEnvsPerCta * hstride(hmax) * 2);
     for (int i = 0; i < 2; ++i) {
         s.hhi[i] = off;
-        off += hb;
+        off += afrag_bytes(hmax);
         s.hlo[i] = off;
-        off += hb;
+        off += afrag_bytes(hmax);
     }
     s.logits = off;
     off += kEnvsPerCta * kLStride * 4;
@@ -113,26 +109,31 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int64_t E = a.E, e0 = static_cast<int64_t>(blockIdx.x) * kEnvsPerCta;
     const int S_ = a.S, A = a.A;
-    const int xs = hstride(a.dims[0]);
-    int hmax = 8;
-    for (int l = 1; l < a.L; ++l) hmax = a.dims[l] > hmax ? a.dims[l] : hmax;
-    const int hs = hstride(hmax);
-    // weights: W_l^T [pad8(out) x hstride(in)] f16 hi / lo, zero padded (split once per launch)
-    for (int l = 0; l < a.L; ++l) {
-        const int in = a.dims[l], out = a.dims[l + 1], ks = hstride(in), op = pad8(out);
-        __half* Wh = reinterpret_cast<__half*>(smem + S.whi[l]);
-        __half* Wl = reinterpret_cast<__half*>(smem + S.wlo[l]);
-        float* B = reinterpret_cast<float*>(smem + S.b[l]);
-        for (int i = t; i < op * ks; i += kThreads) {
-            const int o = i / ks, ii = i % ks;
-            const float w = (o < out && ii < in) ? a.params[a.woff[l] + ii * out + o] : 0.0f;
-            const __half h = __float2half_rn(w);
-            Wh[i] = h;
-            Wl[i] = __float2half_rn(w - __half2float(h));
+    const int KT0 = pad16(a.dims[0]) / 16;
+    // weights: fragment-major W_l^T images, f16 hi / lo (split once per launch), then the f32 bias
+    {
+        uint32_t off = S.w0;
+        for (int l = 0; l < a.L; ++l) {
+            const int in = a.dims[l], out = a.dims[l + 1], NT = pad8(out) / 8, KT = pad16(in) / 16;
+            uint32_t* Wf = reinterpret_cast<uint32_t*>(smem + off);
+            for (int i = t; i < NT * KT * 32 * 2; i += kThreads) {  // (nt, kk, lane, fragment reg)
+                const int r = i & 1, ln = (i >> 1) & 31, kk = (i >> 6) % KT, nt = (i >> 6) / KT;
+                const int n = 8 * nt + (ln >> 2), k = 16 * kk + 8 * r + 2 * (ln & 3);
+                float w[2];
+                for (int h = 0; h < 2; ++h)
+                    w[h] = (n < out && k + h < in) ? a.params[a.woff[l] + static_cast<int64_t>(k + h) * out + n] : 0.0f;
+                uint32_t hi, lo;
+                split_f16x2(w[0], w[1], hi, lo);
+                Wf[4 * ((nt * KT + kk) * 32 + ln) + r] = hi;
+                Wf[4 * ((nt * KT + kk) * 32 + ln) + 2 + r] = lo;
+            }
+            off += wfrag_bytes(in, out);
+            float* B = reinterpret_cast<float*>(smem + off);
+            for (int o = t; o < pad16(out); o += kThreads) B[o] = o < out ? a.params[a.boff[l] + o] : 0.0f;
+            off += static_cast<uint32_t>(pad16(out) * 4);
         }
-        for (int o = t; o < op; o += kThreads) B[o] = o < out ? a.params[a.boff[l] + o] : 0.0f;
     }
-    // zero the activation buffers once: padded input columns must read as 0
+    // zero the activation images once: padded input columns must read as 0
     for (uint32_t i = t; i < (S.logits - S.xhi) / 4; i += kThreads) reinterpret_cast<uint32_t*>(smem + S.xhi)[i] = 0u;
     __syncthreads();
     // ---- env owner threads (warp 0): env state in registers
@@ -147,10 +148,13 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     int32_t stepc = 0;
     __half* xhi = reinterpret_cast<__half*>(smem + S.xhi);
     __half* xlo = reinterpret_cast<__half*>(smem + S.xlo);
-    auto put_obs = [&](int j, float o) {  // next layer-0 input, split
+    auto put_obs = [&](int j, float o) {  // next layer-0 input element (row t, column j), split
+        const int rr = t & 15, kc = j & 15;
+        const int ln = 4 * (rr & 7) + ((kc & 7) >> 1), reg = 2 * (kc >> 3) + (rr >> 3);
+        const int el = 2 * (4 * (((t >> 4) * KT0 + (j >> 4)) * 32 + ln) + reg) + (kc & 1);
         const __half h = __float2half_rn(o);
-        xhi[t * xs + j] = h;
-        xlo[t * xs + j] = __float2half_rn(o - __half2float(h));
+        xhi[el] = h;
+        xlo[el] = __float2half_rn(o - __half2float(h));
     };
     if (live) {
 #pragma unroll
@@ -161,7 +165,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     }
     __syncthreads();
     const uint64_t ep = static_cast<uint64_t>(ctx->episode);
-    const int mt = warp % kMT, nt0 = warp / kMT;
+    const int mt = warp % kMT, jw = warp / kMT;  // env tile, output tile pair (2jw, 2jw + 1)
     const int g8 = lane >> 2, c4 = lane & 3;
     const int ar = 16 * mt + g8;  // fragment row of this lane (and ar + 8)
 
@@ -172,60 +176,65 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
 #ifdef FLW_LEARN_TRACE
         if (step - a.step0 < 8) tr0[step - a.step0] = clock64();
 #endif
+        uint32_t woff = S.w0;
         for (int l = 0; l < a.L; ++l) {
             const int in = a.dims[l], out = a.dims[l + 1], KT = pad16(in) / 16, NT = pad8(out) / 8;
-            const bool first = l == 0, last = l + 1 == a.L;
-            const uint32_t* Ahi = reinterpret_cast<const uint32_t*>(smem + (first ? S.xhi : S.hhi[(l - 1) & 1]));
-            const uint32_t* Alo = reinterpret_cast<const uint32_t*>(smem + (first ? S.xlo : S.hlo[(l - 1) & 1]));
-            const int as2 = (first ? xs : hs) / 2;  // row stride in 32-bit words
-            const int ws2 = hstride(in) / 2;
-            const uint32_t* Whi = reinterpret_cast<const uint32_t*>(smem + S.whi[l]);
-            const uint32_t* Wlo = reinterpret_cast<const uint32_t*>(smem + S.wlo[l]);
-            const float* B = reinterpret_cast<const float*>(smem + S.b[l]);
-            if (nt0 < NT) {
-                const bool two = nt0 + 4 < NT;
+            const bool last = l + 1 == a.L;
+            const uint4* Ahi = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xhi : S.hhi[(l - 1) & 1]));
+            const uint4* Alo = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xlo : S.hlo[(l - 1) & 1]));
+            const uint4* Wf = reinterpret_cast<const uint4*>(smem + woff);
+            const float* B = reinterpret_cast<const float*>(smem + woff + wfrag_bytes(in, out));
+            woff += wfrag_bytes(in, out) + static_cast<uint32_t>(pad16(out) * 4);
+            const int n0 = 2 * jw;
+            if (n0 < NT) {
+                const bool two = n0 + 1 < NT;
                 float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
-                const int aoff = ar * as2 + c4, w0off = (8 * nt0 + g8) * ws2 + c4, w1off = w0off + 32 * ws2;
-#pragma unroll 2
-                for (int k = 0; k < KT; ++k) {
-                    const int ko = 8 * k;  // 16 halves = 8 words
-                    const uint32_t ahi[4] = {Ahi[aoff + ko], Ahi[aoff + ko + 8 * as2], Ahi[aoff + ko + 4],
-                                             Ahi[aoff + ko + 8 * as2 + 4]};
-                    const uint32_t alo[4] = {Alo[aoff + ko], Alo[aoff + ko + 8 * as2], Alo[aoff + ko + 4],
-                                             Alo[aoff + ko + 8 * as2 + 4]};
-                    const uint32_t bhi[2] = {Whi[w0off + ko], Whi[w0off + ko + 4]};
-                    const uint32_t blo[2] = {Wlo[w0off + ko], Wlo[w0off + ko + 4]};
-                    mma_f16(acc0, alo, bhi);
-                    mma_f16(acc0, ahi, blo);
-                    mma_f16(acc0, ahi, bhi);
+                const uint4* ap = Ahi + mt * KT * 32 + lane;
+                const uint4* alp = Alo + mt * KT * 32 + lane;
+                const uint4* w0p = Wf + n0 * KT * 32 + lane;
+                const uint4* w1p = w0p + KT * 32;
+#pragma unroll 4
+                for (int kk = 0; kk < KT; ++kk) {
+                    const uint4 ah = ap[32 * kk], al = alp[32 * kk], b0 = w0p[32 * kk];
+                    const uint32_t ahv[4] = {ah.x, ah.y, ah.z, ah.w}, alv[4] = {al.x, al.y, al.z, al.w};
+                    const uint32_t bh0[2] = {b0.x, b0.y}, bl0[2] = {b0.z, b0.w};
+                    mma_f16(acc0, alv, bh0);
+                    mma_f16(acc0, ahv, bl0);
+                    mma_f16(acc0, ahv, bh0);
                     if (two) {
-                        const uint32_t chi[2] = {Whi[w1off + ko], Whi[w1off + ko + 4]};
-                        const uint32_t clo[2] = {Wlo[w1off + ko], Wlo[w1off + ko + 4]};
-                        mma_f16(acc1, alo, chi);
-                        mma_f16(acc1, ahi, clo);
-                        mma_f16(acc1, ahi, chi);
+                        const uint4 b1 = w1p[32 * kk];
+                        const uint32_t bh1[2] = {b1.x, b1.y}, bl1[2] = {b1.z, b1.w};
+                        mma_f16(acc1, alv, bh1);
+                        mma_f16(acc1, ahv, bl1);
+                        mma_f16(acc1, ahv, bh1);
                     }
                 }
-                auto store = [&](const float* acc, int nt) {
-                    const int n = 8 * nt + 2 * c4;
-                    const float b0 = B[n], b1 = B[n + 1];
-                    float v[4] = {acc[0] + b0, acc[1] + b1, acc[2] + b0, acc[3] + b1};
-                    if (last) {  // f32 logits for the owner threads
-                        float* lg = reinterpret_cast<float*>(smem + S.logits);
-                        *reinterpret_cast<float2*>(lg + ar * kLStride + n) = make_float2(v[0], v[1]);
-                        *reinterpret_cast<float2*>(lg + (ar + 8) * kLStride + n) = make_float2(v[2], v[3]);
-                        return;
+                // bias, activation; output columns n0*8 + 2c (+1) and (n0 + 1)*8 + 2c (+1)
+                const int na = 8 * n0 + 2 * c4, nb = na + 8;
+                float v[8] = {acc0[0] + B[na], acc0[1] + B[na + 1], acc0[2] + B[na], acc0[3] + B[na + 1],
+                              acc1[0] + B[nb], acc1[1] + B[nb + 1], acc1[2] + B[nb], acc1[3] + B[nb + 1]};
+                if (last) {  // f32 logits for the owner threads
+                    float* lg = reinterpret_cast<float*>(smem + S.logits);
+                    *reinterpret_cast<float2*>(lg + ar * kLStride + na) = make_float2(v[0], v[1]);
+                    *reinterpret_cast<float2*>(lg + (ar + 8) * kLStride + na) = make_float2(v[2], v[3]);
+                    if (two) {
+                        *reinterpret_cast<float2*>(lg + ar * kLStride + nb) = make_float2(v[4], v[5]);
+                        *reinterpret_cast<float2*>(lg + (ar + 8) * kLStride + nb) = make_float2(v[6], v[7]);
                     }
+                } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) v[j] = a.act == 0 ? tanh_mufu(v[j]) : fmaxf(v[j], 0.0f);
-                    uint32_t* Ohi = reinterpret_cast<uint32_t*>(smem + S.hhi[l & 1]);
-                    uint32_t* Olo = reinterpret_cast<uint32_t*>(smem + S.hlo[l & 1]);
-                    const int o2 = n / 2;
-                    split_f16x2(v[0], v[1], Ohi[ar * (hs / 2) + o2], Olo[ar * (hs / 2) + o2]);
-                    split_f16x2(v[2], v[3], Ohi[(ar + 8) * (hs / 2) + o2], Olo[(ar + 8) * (hs / 2) + o2]);
-                };
-                store(acc0, nt0);
-                if (two) store(acc1, nt0 + 4);
+                    for (int j = 0; j < 8; ++j) v[j] = a.act == 0 ? tanh_mufu(v[j]) : fmaxf(v[j], 0.0f);
+                    if (!two) v[4] = v[5] = v[6] = v[7] = 0.0f;
+                    // the two accumulator fragments = the next layer's A fragment of k-step jw
+                    uint4 hi, lo;
+                    split_f16x2(v[0], v[1], hi.x, lo.x);
+                    split_f16x2(v[2], v[3], hi.y, lo.y);
+                    split_f16x2(v[4], v[5], hi.z, lo.z);
+                    split_f16x2(v[6], v[7], hi.w, lo.w);
+                    const int KTn = pad16(out) / 16;
+                    reinterpret_cast<uint4*>(smem + S.hhi[l & 1])[(mt * KTn + jw) * 32 + lane] = hi;
+                    reinterpret_cast<uint4*>(smem + S.hlo[l & 1])[(mt * KTn + jw) * 32 + lane] = lo;
+                }
             }
             __syncthreads();
         }

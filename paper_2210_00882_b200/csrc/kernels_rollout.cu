@@ -50,7 +50,7 @@ __host__ __device__ inline uint32_t wfrag_bytes(int in, int out) {
 __host__ __device__ inline uint32_t afrag_bytes(int k) { return static_cast<uint32_t>(kMT * (pad16(k) / 16) * 32 * 16); }
 
 struct RolloutSmem {
-    uint32_t w0, xhi, xlo, hhi[2], hlo[2], logits, total;  // weights: layers back to back from w0
+    uint32_t w0, xhi, xlo, hhi[2], hlo[2], logits, sb, total;  // weights: layers back to back from w0
 };
 
 __host__ __device__ inline RolloutSmem rollout_carve(const FastRolloutArgs& a) {
@@ -72,6 +72,8 @@ __host__ __device__ inline RolloutSmem rollout_carve(const FastRolloutArgs& a) {
     }
     s.logits = off;
     off += kEnvsPerCta * kLStride * 4;
+    s.sb = off;  // synth17x6 action table B[a][i] (double)
+    off += 16 * kSynthObs * 8;
     s.total = off;
     return s;
 }
@@ -133,6 +135,9 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             off += static_cast<uint32_t>(pad16(out) * 4);
         }
     }
+    if (ENV == 1)
+        for (int i = t; i < a.A * kSynthObs; i += kThreads)
+            reinterpret_cast<double*>(smem + S.sb)[i] = a.env.synth_b[i];
     // zero the activation images once: padded input columns must read as 0
     for (uint32_t i = t; i < (S.logits - S.xhi) / 4; i += kThreads) reinterpret_cast<uint32_t*>(smem + S.xhi)[i] = 0u;
     __syncthreads();
@@ -176,6 +181,11 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
 #ifdef FLW_LEARN_TRACE
         if (step - a.step0 < 8) tr0[step - a.step0] = clock64();
 #endif
+        // the owner's action draw (integer hashing) issues ahead of the MLP and overlaps it
+        double u = 0.0;
+        if (owner)
+            u = rng_uniform(
+                rng_key(a.seed, kActionStream, ep, static_cast<uint64_t>(step), static_cast<uint64_t>(a.env_lo + e)));
         uint32_t woff = S.w0;
         for (int l = 0; l < a.L; ++l) {
             const int in = a.dims[l], out = a.dims[l + 1], KT = pad16(in) / 16, NT = pad8(out) / 8;
@@ -257,8 +267,6 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             }
             const float rden = 1.0f / den;
             for (int c = 0; c < A; ++c) p[c] *= rden;
-            const double u = rng_uniform(
-                rng_key(a.seed, kActionStream, ep, static_cast<uint64_t>(step), static_cast<uint64_t>(a.env_lo + e)));
             double cum = 0.0;
             int chosen = A - 1;
             for (int c = 0; c < A; ++c) {
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                         d = true;
                     }
                 } else {  // synth17x6 (oracle/refx/env_ext.cpp)
-                    const double* tb = a.env.synth_b + chosen * kSynthObs;
+                    const double* tb = reinterpret_cast<const double*>(smem + S.sb) + chosen * kSynthObs;
                     double old[kSynthObs], sq = 0.0, m = 0.0;
 #pragma unroll
                     for (int i = 0; i < kSynthObs; ++i) old[i] = st[i];

@@ -588,8 +588,49 @@ void Engine::enq_rollout_fast(int64_t step0, int64_t nsteps) {
     fast_rollout(stream_, b.ctx, a);
 }
 
+// MAPPO, fast numerics: the fused episode rollout (tensor-core MLP, one launch) when the shape
+// fits (n <= 16 agents, widths <= 64); false: the exact per-step rollout is used.
+bool Engine::enq_rollout_fast_mappo(int64_t step0, int64_t nsteps) {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    FastRolloutArgs a{};
+    a.params = b.params;
+    a.L = s.L;
+    for (int l = 0; l <= s.L; ++l) a.dims[l] = s.pdims[l];
+    for (int l = 0; l < s.L; ++l) {
+        a.woff[l] = s.woff[0][l];
+        a.boff[l] = s.boff[0][l];
+    }
+    a.act = act_of(cfg_);
+    a.est = b.est;
+    a.done = b.done;
+    a.stepc = b.stepc;
+    a.states = b.states;  // the policy rows prows[T+1][n*E][S]
+    a.actions = b.actions;
+    a.logp = b.logp;
+    a.reward = b.rew;
+    a.done_f = b.done_f;
+    a.reward_d = b.rew_d;
+    a.E = E_;
+    a.env_lo = lo_;
+    a.env_total = etot_;
+    a.step0 = step0;
+    a.nsteps = nsteps;
+    a.S = s.obs_dim;
+    a.A = s.n_actions;
+    a.seed = seed_;
+    a.env = env_params(cfg_, shape_, b.synth_b);
+    a.joint = b.joint;
+    a.cin = b.cin;
+    static const bool off = std::getenv("FLW_MAPPO_EXACT_ROLLOUT") != nullptr;  // A/B only
+    if (off || !fast_rollout_mappo_ok(a)) return false;
+    fast_rollout_mappo(stream_, b.ctx, a);
+    return true;
+}
+
 void Engine::enq_step(int64_t st) {
     if (numerics_ == Numerics::Fast && !mappo_) return enq_rollout_fast(st, 1);
+    if (numerics_ == Numerics::Fast && mappo_ && enq_rollout_fast_mappo(st, 1)) return;
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions;
@@ -1058,8 +1099,8 @@ void Engine::build_graph() {
     probe_begin("rollout");
     if (numerics_ == Numerics::Fast && !mappo_)
         enq_rollout_fast(0, T_);
-    else  // exact rollout (also fast MAPPO: the multi-agent rollout is the exact one)
-        for (int64_t st = 0; st < T_; ++st) enq_step(st);
+    else if (!(numerics_ == Numerics::Fast && mappo_ && enq_rollout_fast_mappo(0, T_)))
+        for (int64_t st = 0; st < T_; ++st) enq_step(st);  // exact rollout
     probe_end();
     if (nrep_ > 1 && numerics_ == Numerics::Exact) enq_permute_replicas();
     FLW_CUDA(cudaEventRecord(ev_fork_, stream_));

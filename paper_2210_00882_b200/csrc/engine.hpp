@@ -119,6 +119,7 @@ class Engine {
     void enq_reset();
     void enq_step(int64_t st);
     void enq_rollout_fast(int64_t step0, int64_t nsteps);
+    bool enq_rollout_fast_mappo(int64_t step0, int64_t nsteps);
     void enq_learn_fast();
     void enq_learn_grads();
     void enq_grad_sync_and_adam();

@@ -143,10 +143,16 @@ struct FastRolloutArgs {     // whole-episode rollout, all T steps in one launch
     int S, A;
     uint64_t seed;
     EnvParams env;
+    // MAPPO (spread_lite): agent-major rows a*E + e; the step-block layouts of kernels_mappo.cu
+    int64_t env_total;
+    float *joint, *cin;      // cin: null with the compact critic
 };
 
 struct DeviceCtx;
 size_t fast_rollout_smem_bytes(const FastRolloutArgs& a);
 void fast_rollout(cudaStream_t s, const DeviceCtx* ctx, const FastRolloutArgs& a);
+// MAPPO fused fast rollout (n <= 16 agents, hidden <= 64); false: shape not supported
+bool fast_rollout_mappo_ok(const FastRolloutArgs& a);
+void fast_rollout_mappo(cudaStream_t s, const DeviceCtx* ctx, const FastRolloutArgs& a);
 
 }  // namespace flw

@@ -353,6 +353,296 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// MAPPO on spread_lite, fast numerics: the whole episode in one launch, the same fragment-major
+// 3-term F16 MLP over the CTA's agent-major rows r = a * EPC + le (EPC envs per CTA, n agents;
+// 16-row MMA tiles, the last one zero padded), then per step
+//   PolicyApply  one thread per row: f32 softmax, the reference's draw
+//                U(key(seed, 0x616374, ep, step, a*env_total + env_lo + e)) and inverse-CDF walk
+//   EnvStep      one thread per env: the exact spread_lite moves / rewards / done in double
+//                (envs.cpp:111-150, same arithmetic as k_rollout_mappo), state in shared memory
+//   emit         one thread per row: the agent observation (envs.cpp:96-109) -> next MLP input and
+//                the trajectory layouts the learn phase reads (joint, prows, cin)
+struct MappoSmem {
+    uint32_t w0, xhi, xlo, hhi[2], hlo[2], logits, st, act, total;
+};
+
+__host__ __device__ inline MappoSmem mappo_carve(const FastRolloutArgs& a, int EPC) {
+    MappoSmem s{};
+    const int n = a.env.n_agents, MT = (n * EPC + 15) / 16;
+    uint32_t off = 0;
+    s.w0 = off;
+    for (int l = 0; l < a.L; ++l) off += wfrag_bytes(a.dims[l], a.dims[l + 1]) + static_cast<uint32_t>(pad16(a.dims[l + 1]) * 4);
+    const uint32_t xb = static_cast<uint32_t>(MT * (pad16(a.dims[0]) / 16) * 512);
+    s.xhi = off;
+    off += xb;
+    s.xlo = off;
+    off += xb;
+    int hmax = 16;
+    for (int l = 1; l < a.L; ++l) hmax = a.dims[l] > hmax ? a.dims[l] : hmax;
+    const uint32_t hb = static_cast<uint32_t>(MT * (pad16(hmax) / 16) * 512);
+    for (int i = 0; i < 2; ++i) {
+        s.hhi[i] = off;
+        off += hb;
+        s.hlo[i] = off;
+        off += hb;
+    }
+    s.logits = off;
+    off += static_cast<uint32_t>(MT * 16 * kLStride * 4);
+    s.st = off;  // env state, [4n][EPC] doubles
+    off += static_cast<uint32_t>(4 * n * EPC * 8);
+    s.act = off;
+    off += static_cast<uint32_t>(MT * 16 * 4);
+    s.total = off;
+    return s;
+}
+
+template <int EPC>
+__global__ void __launch_bounds__(256, 1) k_rollout_mappo_fast(const DeviceCtx* __restrict__ ctx, FastRolloutArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const MappoSmem S = mappo_carve(a, EPC);
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int n = a.env.n_agents, A = a.A, Sd = 2 + 2 * n, W = n * Sd, C = W + n;
+    const int rows = n * EPC, MT = (rows + 15) / 16;
+    const int64_t E = a.E, e0 = static_cast<int64_t>(blockIdx.x) * EPC, R = static_cast<int64_t>(n) * E;
+    const int KT0 = pad16(a.dims[0]) / 16;
+    {  // weights, as k_rollout_episode
+        uint32_t off = S.w0;
+        for (int l = 0; l < a.L; ++l) {
+            const int in = a.dims[l], out = a.dims[l + 1], NT = pad8(out) / 8, KT = pad16(in) / 16;
+            uint32_t* Wf = reinterpret_cast<uint32_t*>(smem + off);
+            for (int i = t; i < NT * KT * 32 * 2; i += blockDim.x) {
+                const int r = i & 1, ln = (i >> 1) & 31, kk = (i >> 6) % KT, nt = (i >> 6) / KT;
+                const int nn = 8 * nt + (ln >> 2), k = 16 * kk + 8 * r + 2 * (ln & 3);
+                float w[2];
+                for (int h = 0; h < 2; ++h)
+                    w[h] = (nn < out && k + h < in) ? a.params[a.woff[l] + static_cast<int64_t>(k + h) * out + nn] : 0.0f;
+                uint32_t hi, lo;
+                split_f16x2(w[0], w[1], hi, lo);
+                Wf[4 * ((nt * KT + kk) * 32 + ln) + r] = hi;
+                Wf[4 * ((nt * KT + kk) * 32 + ln) + 2 + r] = lo;
+            }
+            off += wfrag_bytes(in, out);
+            float* B = reinterpret_cast<float*>(smem + off);
+            for (int o = t; o < pad16(out); o += blockDim.x) B[o] = o < out ? a.params[a.boff[l] + o] : 0.0f;
+            off += static_cast<uint32_t>(pad16(out) * 4);
+        }
+    }
+    for (uint32_t i = t; i < (S.logits - S.xhi) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem + S.xhi)[i] = 0u;
+    double* sts = reinterpret_cast<double*>(smem + S.st);
+    int* acts = reinterpret_cast<int*>(smem + S.act);
+    // env threads: t < EPC; row threads: t < rows (agent ra, local env rle)
+    const bool envt = t < EPC && e0 + t < E;
+    const int ra = t / EPC, rle = t % EPC;
+    const int64_t re = e0 + rle;
+    const bool rowt = t < rows && re < E;
+    bool done = false;
+    int32_t stepc = 0;
+    if (envt) {
+        for (int i = 0; i < 4 * n; ++i) sts[i * EPC + t] = a.est[i * E + e0 + t];
+        done = a.done[e0 + t] != 0;
+        stepc = a.stepc[e0 + t];
+    }
+    __syncthreads();
+    __half* xhi = reinterpret_cast<__half*>(smem + S.xhi);
+    __half* xlo = reinterpret_cast<__half*>(smem + S.xlo);
+    // observation of row (ra, rle) from the state (envs.cpp:96-109): next MLP input, and the step
+    // block `blk` of the trajectory layouts when blk >= 0
+    auto emit = [&](int64_t blk) {
+        const double xa = sts[(2 * ra) * EPC + rle], ya = sts[(2 * ra + 1) * EPC + rle];
+        float* pr = blk >= 0 ? a.states + (blk * R + static_cast<int64_t>(ra) * E + re) * Sd : nullptr;
+        float* jr = blk >= 0 ? a.joint + (blk * E + re) * W + ra * Sd : nullptr;
+        for (int j = 0; j < Sd; ++j) {
+            float o;
+            if (j < 2) {
+                o = static_cast<float>(j == 0 ? xa : ya);
+            } else {
+                const int lm = (j - 2) >> 1;
+                o = static_cast<float>((j & 1) == 0 ? __dsub_rn(sts[(2 * n + 2 * lm) * EPC + rle], xa)
+                                                   : __dsub_rn(sts[(2 * n + 2 * lm + 1) * EPC + rle], ya));
+            }
+            const int rr = t & 15, kc = j & 15;
+            const int ln = 4 * (rr & 7) + ((kc & 7) >> 1), reg = 2 * (kc >> 3) + (rr >> 3);
+            const int el = 2 * (4 * (((t >> 4) * KT0 + (j >> 4)) * 32 + ln) + reg) + (kc & 1);
+            const __half h = __float2half_rn(o);
+            xhi[el] = h;
+            xlo[el] = __float2half_rn(o - __half2float(h));
+            if (pr) {
+                pr[j] = o;
+                jr[j] = o;
+            }
+        }
+        if (blk >= 0 && a.cin) {  // [joint(t, e) | one-hot(a)] (programs.cpp:390-402)
+            float* cr = a.cin + (blk * R + static_cast<int64_t>(ra) * E + re) * C;
+            for (int b = 0; b < n; ++b) {
+                const double xb = sts[(2 * b) * EPC + rle], yb = sts[(2 * b + 1) * EPC + rle];
+                cr[b * Sd] = static_cast<float>(xb);
+                cr[b * Sd + 1] = static_cast<float>(yb);
+                for (int lm = 0; lm < n; ++lm) {
+                    cr[b * Sd + 2 + 2 * lm] = static_cast<float>(__dsub_rn(sts[(2 * n + 2 * lm) * EPC + rle], xb));
+                    cr[b * Sd + 3 + 2 * lm] = static_cast<float>(__dsub_rn(sts[(2 * n + 2 * lm + 1) * EPC + rle], yb));
+                }
+            }
+            for (int j = 0; j < n; ++j) cr[W + j] = j == ra ? 1.0f : 0.0f;
+        }
+    };
+    if (rowt) emit(-1);  // step0's rows are in the trajectory already (reset or previous call)
+    __syncthreads();
+    const uint64_t ep = static_cast<uint64_t>(ctx->episode);
+    const int g8 = lane >> 2, c4 = lane & 3;
+    for (int64_t step = a.step0; step < a.step0 + a.nsteps; ++step) {
+        double u = 0.0;
+        if (rowt)
+            u = rng_uniform(rng_key(a.seed, kActionStream, ep, static_cast<uint64_t>(step),
+                                    static_cast<uint64_t>(ra * a.env_total + a.env_lo + re)));
+        uint32_t woff = S.w0;
+        for (int l = 0; l < a.L; ++l) {
+            const int in = a.dims[l], out = a.dims[l + 1], KT = pad16(in) / 16, NT = pad8(out) / 8;
+            const bool last = l + 1 == a.L;
+            const uint4* Ahi = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xhi : S.hhi[(l - 1) & 1]));
+            const uint4* Alo = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xlo : S.hlo[(l - 1) & 1]));
+            const uint4* Wf = reinterpret_cast<const uint4*>(smem + woff);
+            const float* B = reinterpret_cast<const float*>(smem + woff + wfrag_bytes(in, out));
+            woff += wfrag_bytes(in, out) + static_cast<uint32_t>(pad16(out) * 4);
+            const int KTn = pad16(out) / 16;
+            for (int pi = warp; pi < MT * 4; pi += 8) {
+                const int mt = pi % MT, jw = pi / MT, n0 = 2 * jw;
+                if (n0 >= NT) continue;
+                const bool two = n0 + 1 < NT;
+                float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
+                const uint4* ap = Ahi + mt * KT * 32 + lane;
+                const uint4* alp = Alo + mt * KT * 32 + lane;
+                const uint4* w0p = Wf + n0 * KT * 32 + lane;
+                const uint4* w1p = w0p + KT * 32;
+                for (int kk = 0; kk < KT; ++kk) {
+                    const uint4 ah = ap[32 * kk], al = alp[32 * kk], b0 = w0p[32 * kk];
+                    const uint32_t ahv[4] = {ah.x, ah.y, ah.z, ah.w}, alv[4] = {al.x, al.y, al.z, al.w};
+                    const uint32_t bh0[2] = {b0.x, b0.y}, bl0[2] = {b0.z, b0.w};
+                    mma_f16(acc0, alv, bh0);
+                    mma_f16(acc0, ahv, bl0);
+                    mma_f16(acc0, ahv, bh0);
+                    if (two) {
+                        const uint4 b1 = w1p[32 * kk];
+                        const uint32_t bh1[2] = {b1.x, b1.y}, bl1[2] = {b1.z, b1.w};
+                        mma_f16(acc1, alv, bh1);
+                        mma_f16(acc1, ahv, bl1);
+                        mma_f16(acc1, ahv, bh1);
+                    }
+                }
+                const int na = 8 * n0 + 2 * c4, nb = na + 8, ar = 16 * mt + g8;
+                float v[8] = {acc0[0] + B[na], acc0[1] + B[na + 1], acc0[2] + B[na], acc0[3] + B[na + 1],
+                              acc1[0] + B[nb], acc1[1] + B[nb + 1], acc1[2] + B[nb], acc1[3] + B[nb + 1]};
+                if (last) {
+                    float* lg = reinterpret_cast<float*>(smem + S.logits);
+                    *reinterpret_cast<float2*>(lg + ar * kLStride + na) = make_float2(v[0], v[1]);
+                    *reinterpret_cast<float2*>(lg + (ar + 8) * kLStride + na) = make_float2(v[2], v[3]);
+                    if (two) {
+                        *reinterpret_cast<float2*>(lg + ar * kLStride + nb) = make_float2(v[4], v[5]);
+                        *reinterpret_cast<float2*>(lg + (ar + 8) * kLStride + nb) = make_float2(v[6], v[7]);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) v[j] = a.act == 0 ? tanh_mufu(v[j]) : fmaxf(v[j], 0.0f);
+                    if (!two) v[4] = v[5] = v[6] = v[7] = 0.0f;
+                    uint4 hi, lo;
+                    split_f16x2(v[0], v[1], hi.x, lo.x);
+                    split_f16x2(v[2], v[3], hi.y, lo.y);
+                    split_f16x2(v[4], v[5], hi.z, lo.z);
+                    split_f16x2(v[6], v[7], hi.w, lo.w);
+                    reinterpret_cast<uint4*>(smem + S.hhi[l & 1])[(mt * KTn + jw) * 32 + lane] = hi;
+                    reinterpret_cast<uint4*>(smem + S.hlo[l & 1])[(mt * KTn + jw) * 32 + lane] = lo;
+                }
+            }
+            __syncthreads();
+        }
+        // ---- PolicyApply: one thread per row (f32 softmax, the reference's draw and walk)
+        if (rowt) {
+            const float* lg = reinterpret_cast<const float*>(smem + S.logits) + t * kLStride;
+            float p[16];
+            float mx = lg[0];
+            for (int c = 1; c < A; ++c) mx = fmaxf(mx, lg[c]);
+            float den = 0.0f;
+            for (int c = 0; c < A; ++c) {
+                p[c] = __expf(lg[c] - mx);
+                den += p[c];
+            }
+            const float rden = 1.0f / den;
+            double cum = 0.0;
+            int chosen = A - 1;
+            for (int c = 0; c < A; ++c) {
+                p[c] *= rden;
+                cum = __dadd_rn(cum, static_cast<double>(p[c]));
+                if (u < cum) {
+                    chosen = c;
+                    break;
+                }
+            }
+            acts[t] = chosen;
+            const int64_t row = static_cast<int64_t>(ra) * E + re;
+            a.actions[step * R + row] = chosen;
+            a.logp[step * R + row] = __logf(fmaxf(p[chosen], 1e-30f));
+        }
+        __syncthreads();
+        // ---- EnvStep: one thread per env (envs.cpp:111-150; absorbing after done, interp.cpp:239-245)
+        if (envt) {
+            const int le = t;
+            const int64_t e = e0 + le;
+            double total = 0.0;
+            bool d;
+            if (done) {
+                for (int ag = 0; ag < n; ++ag) a.reward[step * R + static_cast<int64_t>(ag) * E + e] = 0.0f;
+                d = true;
+            } else {
+                for (int ag = 0; ag < n; ++ag) {  // moves (envs.cpp:114-126)
+                    double dx = 0.0, dy = 0.0;
+                    switch (acts[ag * EPC + le]) {
+                        case 1: dx = 0.1; break;
+                        case 2: dx = -0.1; break;
+                        case 3: dy = 0.1; break;
+                        case 4: dy = -0.1; break;
+                        default: break;
+                    }
+                    sts[(2 * ag) * EPC + le] = __dadd_rn(sts[(2 * ag) * EPC + le], dx);
+                    sts[(2 * ag + 1) * EPC + le] = __dadd_rn(sts[(2 * ag + 1) * EPC + le], dy);
+                }
+                for (int ag = 0; ag < n; ++ag) {  // rewards (envs.cpp:128-144)
+                    const double xa = sts[(2 * ag) * EPC + le], ya = sts[(2 * ag + 1) * EPC + le];
+                    double best = 1e18;
+                    for (int lm = 0; lm < n; ++lm) {
+                        const double dx = __dsub_rn(sts[(2 * n + 2 * lm) * EPC + le], xa);
+                        const double dy = __dsub_rn(sts[(2 * n + 2 * lm + 1) * EPC + le], ya);
+                        const double dist = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+                        best = dist < best ? dist : best;
+                    }
+                    double r = -best;
+                    for (int b = 0; b < n; ++b) {
+                        if (b == ag) continue;
+                        const double dx = __dsub_rn(sts[(2 * b) * EPC + le], xa);
+                        const double dy = __dsub_rn(sts[(2 * b + 1) * EPC + le], ya);
+                        if (__dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy))) < 0.1) r = __dsub_rn(r, 0.5);
+                    }
+                    total = __dadd_rn(total, r);
+                    a.reward[step * R + static_cast<int64_t>(ag) * E + e] = static_cast<float>(r);
+                }
+                d = a.env.max_steps > 0 && stepc + 1 >= a.env.max_steps;
+                stepc += 1;
+            }
+            done = d;
+            a.reward_d[step * E + e] = total;
+            for (int ag = 0; ag < n; ++ag) a.done_f[step * R + static_cast<int64_t>(ag) * E + e] = d ? 1.0f : 0.0f;
+        }
+        __syncthreads();
+        if (rowt) emit(step + 1);
+        __syncthreads();
+    }
+    if (envt) {
+        for (int i = 0; i < 4 * n; ++i) a.est[i * E + e0 + t] = sts[i * EPC + t];
+        a.done[e0 + t] = done ? 1 : 0;
+        a.stepc[e0 + t] = stepc;
+    }
+}
+
 }  // namespace
 
 size_t fast_rollout_smem_bytes(const FastRolloutArgs& a) { return rollout_carve(a).total; }
@@ -368,6 +658,36 @@ void fast_rollout(cudaStream_t s, const DeviceCtx* ctx, const FastRolloutArgs& a
         FLW_CUDA(cudaFuncSetAttribute(k_rollout_episode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
         k_rollout_episode<1><<<grid, kThreads, smem, s>>>(ctx, a);
+    }
+}
+
+}  // namespace flw
+
+namespace flw {
+namespace {
+inline int mappo_epc(int n) { return n <= 8 ? 16 : 8; }
+}  // namespace
+
+bool fast_rollout_mappo_ok(const FastRolloutArgs& a) {
+    const int n = a.env.n_agents;
+    if (a.env.kind != 2 || n < 1 || n > 16 || a.A > 16 || a.dims[0] > 64) return false;
+    for (int l = 1; l < a.L; ++l)
+        if (a.dims[l] > 64) return false;
+    return mappo_carve(a, mappo_epc(n)).total <= 227u * 1024u;
+}
+
+void fast_rollout_mappo(cudaStream_t s, const DeviceCtx* ctx, const FastRolloutArgs& a) {
+    const int epc = mappo_epc(a.env.n_agents);
+    const size_t smem = mappo_carve(a, epc).total;
+    const unsigned grid = static_cast<unsigned>((a.E + epc - 1) / epc);
+    if (epc == 16) {
+        FLW_CUDA(cudaFuncSetAttribute(k_rollout_mappo_fast<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        k_rollout_mappo_fast<16><<<grid, 256, smem, s>>>(ctx, a);
+    } else {
+        FLW_CUDA(cudaFuncSetAttribute(k_rollout_mappo_fast<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        k_rollout_mappo_fast<8><<<grid, 256, smem, s>>>(ctx, a);
     }
 }
 

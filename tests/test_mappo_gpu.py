@@ -77,10 +77,10 @@ def test_mappo_episodes_match_oracle(n_agents):
 
 @pytest.mark.parametrize("n_agents", [3, 4])
 def test_fast_mappo_tracks_exact(n_agents):
-    """Fast numerics for MAPPO (n <= 4, critic input 2n^2+3n <= 64): the exact multi-agent
-    rollout + the tensor-core learn kernels over [joint | one-hot] rows. The first episode's
-    rollout is bit-exact (same parameters, exact rollout); afterwards the bf16 learn keeps the
-    trained parameters close to the exact run."""
+    """Fast numerics for MAPPO (n <= 4, critic input 2n^2+3n <= 64): the fused tensor-core
+    rollout (test_fast_mappo_rollout_matches_exact) + the tensor-core learn kernels over
+    [joint | one-hot] rows keep the episode rewards and trained parameters close to the exact
+    run."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2210_00882_b200 import DpdEngine
@@ -92,8 +92,8 @@ def test_fast_mappo_tracks_exact(n_agents):
     fa = DpdEngine(algo, seed=5, numerics="fast")
     r_ex = [ex.run_episode(ep)[0] for ep in range(4)]
     r_fa = [fa.run_episode(ep)[0] for ep in range(4)]
-    # identical rollout before any learning (the reward sum itself is a parallel sum in fast mode)
-    assert r_fa[0] == pytest.approx(r_ex[0], rel=1e-12)
+    # first episode: same parameters, rollouts differ only by near-tie action draws
+    assert r_fa[0] == pytest.approx(r_ex[0], rel=2e-2)
     np.testing.assert_allclose(r_fa, r_ex, rtol=5e-2)
     p_ex, p_fa = np.asarray(ex.params()), np.asarray(fa.params())
     rel = np.linalg.norm(p_fa - p_ex) / np.linalg.norm(p_ex)
@@ -117,8 +117,42 @@ def test_fast_mappo_compact_critic_tracks_exact(n_agents):
     fa = DpdEngine(algo, seed=5, numerics="fast")
     r_ex = [ex.run_episode(ep)[0] for ep in range(4)]
     r_fa = [fa.run_episode(ep)[0] for ep in range(4)]
-    assert r_fa[0] == pytest.approx(r_ex[0], rel=1e-12)
+    assert r_fa[0] == pytest.approx(r_ex[0], rel=2e-2)
     np.testing.assert_allclose(r_fa, r_ex, rtol=5e-2)
     p_ex, p_fa = np.asarray(ex.params()), np.asarray(fa.params())
     rel = np.linalg.norm(p_fa - p_ex) / np.linalg.norm(p_ex)
     assert rel < 2e-2, rel
+
+
+@pytest.mark.parametrize("n_agents", [3, 10])
+def test_fast_mappo_rollout_matches_exact(n_agents):
+    """The fused fast MAPPO rollout (3-term F16 tensor-core MLP over the agent rows, f32 softmax,
+    the reference's draws, exact spread_lite dynamics in double) against the exact per-step
+    rollout from the same reset: step 0's actions agree except near-tie draws and their logp to
+    1e-5; over the episode the draws agree for >= 98% of the agent rows (a flip changes that
+    env's later trajectory)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2210_00882_b200 import DpdEngine
+
+    T = 16
+    algo = {"algorithm": "mappo", "agent": {"num": n_agents},
+            "env": {"type": "spread_lite", "num": 96, "params": {"accel": 1}},
+            "policy_net": {"hidden": [64] * 6}, "loop": {"episodes": 1, "steps_per_episode": T}}
+    ex = DpdEngine(algo, seed=11, numerics="exact")
+    fa = DpdEngine(algo, seed=11, numerics="fast")
+    ex.reset(0)
+    fa.reset(0)
+    np.testing.assert_array_equal(fa.get("state_in"), ex.get("state_in"))
+    same_all = total = 0
+    for st in range(T):
+        ex.step(0, st)
+        fa.step(0, st)
+        pe, pf = ex.get("pa").reshape(-1, 2), fa.get("pa").reshape(-1, 2)
+        same = pe[:, 0] == pf[:, 0]
+        if st == 0:
+            assert same.mean() >= 0.99, same.mean()
+            np.testing.assert_allclose(pf[same, 1], pe[same, 1], rtol=1e-5, atol=1e-6)
+        same_all += int(same.sum())
+        total += same.size
+    assert same_all >= 0.98 * total, (same_all, total)

@@ -47,7 +47,7 @@ def ours_point(n: int, envs: int, episodes: int, seed: int, numerics: str = "exa
     csv, _ = prog.run_local(seed=seed)
     ms = statistics.median(float(l.split(",")[1]) for l in csv.strip().split("\n")[1:])
     arm = ("ours dp-d fused, 1 x B200, numerics=exact (compact critic)" if numerics == "exact" else
-           "ours dp-d fused, 1 x B200, numerics=fast (exact rollout, tensor-core learn"
+           "ours dp-d fused, 1 x B200, numerics=fast (fused tensor-core rollout, tensor-core learn"
            + (", compact critic: TF32 joint GEMM)" if 2 * n * n + 3 * n > 64 else ")"))
     return {"arm": arm, "agents": n, "envs": envs,
             "episode_ms": ms, "env_steps_per_s": envs * 32 / (ms * 1e-3)}

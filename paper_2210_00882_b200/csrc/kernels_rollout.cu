@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
 //   emit         one thread per row: the agent observation (envs.cpp:96-109) -> next MLP input and
 //                the trajectory layouts the learn phase reads (joint, prows, cin)
 struct MappoSmem {
-    uint32_t w0, xhi, xlo, hhi[2], hlo[2], logits, st, act, total;
+    uint32_t w0, xhi, xlo, hhi[2], hlo[2], logits, st, act, rew, dn, total;
 };
 
 __host__ __device__ inline MappoSmem mappo_carve(const FastRolloutArgs& a, int EPC) {
@@ -394,6 +394,10 @@ __host__ __device__ inline MappoSmem mappo_carve(const FastRolloutArgs& a, int E
     off += static_cast<uint32_t>(4 * n * EPC * 8);
     s.act = off;
     off += static_cast<uint32_t>(MT * 16 * 4);
+    s.rew = off;  // per-row reward of the step (double)
+    off += static_cast<uint32_t>(MT * 16 * 8);
+    s.dn = off;  // per-env done flag
+    off += static_cast<uint32_t>(EPC * 4);
     s.total = off;
     return s;
 }
@@ -432,6 +436,8 @@ __global__ void __launch_bounds__(256, 1) k_rollout_mappo_fast(const DeviceCtx* 
     for (uint32_t i = t; i < (S.logits - S.xhi) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem + S.xhi)[i] = 0u;
     double* sts = reinterpret_cast<double*>(smem + S.st);
     int* acts = reinterpret_cast<int*>(smem + S.act);
+    double* rews = reinterpret_cast<double*>(smem + S.rew);
+    int* dns = reinterpret_cast<int*>(smem + S.dn);
     // env threads: t < EPC; row threads: t < rows (agent ra, local env rle)
     const bool envt = t < EPC && e0 + t < E;
     const int ra = t / EPC, rle = t % EPC;
@@ -443,6 +449,7 @@ __global__ void __launch_bounds__(256, 1) k_rollout_mappo_fast(const DeviceCtx* 
         for (int i = 0; i < 4 * n; ++i) sts[i * EPC + t] = a.est[i * E + e0 + t];
         done = a.done[e0 + t] != 0;
         stepc = a.stepc[e0 + t];
+        dns[t] = done ? 1 : 0;
     }
     __syncthreads();
     __half* xhi = reinterpret_cast<__half*>(smem + S.xhi);
@@ -584,51 +591,57 @@ __global__ void __launch_bounds__(256, 1) k_rollout_mappo_fast(const DeviceCtx* 
             a.logp[step * R + row] = __logf(fmaxf(p[chosen], 1e-30f));
         }
         __syncthreads();
-        // ---- EnvStep: one thread per env (envs.cpp:111-150; absorbing after done, interp.cpp:239-245)
+        // ---- EnvStep (envs.cpp:111-150; absorbing after done, interp.cpp:239-245): each row
+        // thread moves its own agent, then scores it against the moved positions; the env thread
+        // adds the agents' rewards in agent order and advances done / the step counter
+        const bool live_row = rowt && !dns[rle];
+        if (live_row) {  // moves (envs.cpp:114-126)
+            double dx = 0.0, dy = 0.0;
+            switch (acts[t]) {
+                case 1: dx = 0.1; break;
+                case 2: dx = -0.1; break;
+                case 3: dy = 0.1; break;
+                case 4: dy = -0.1; break;
+                default: break;
+            }
+            sts[(2 * ra) * EPC + rle] = __dadd_rn(sts[(2 * ra) * EPC + rle], dx);
+            sts[(2 * ra + 1) * EPC + rle] = __dadd_rn(sts[(2 * ra + 1) * EPC + rle], dy);
+        }
+        __syncthreads();
+        if (rowt) {  // rewards (envs.cpp:128-144)
+            double r = 0.0;
+            if (live_row) {
+                const double xa = sts[(2 * ra) * EPC + rle], ya = sts[(2 * ra + 1) * EPC + rle];
+                double best = 1e18;
+                for (int lm = 0; lm < n; ++lm) {
+                    const double dx = __dsub_rn(sts[(2 * n + 2 * lm) * EPC + rle], xa);
+                    const double dy = __dsub_rn(sts[(2 * n + 2 * lm + 1) * EPC + rle], ya);
+                    const double dist = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+                    best = dist < best ? dist : best;
+                }
+                r = -best;
+                for (int b = 0; b < n; ++b) {
+                    if (b == ra) continue;
+                    const double dx = __dsub_rn(sts[(2 * b) * EPC + rle], xa);
+                    const double dy = __dsub_rn(sts[(2 * b + 1) * EPC + rle], ya);
+                    if (__dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy))) < 0.1) r = __dsub_rn(r, 0.5);
+                }
+            }
+            rews[t] = r;
+            a.reward[step * R + static_cast<int64_t>(ra) * E + re] = static_cast<float>(r);
+        }
+        __syncthreads();
         if (envt) {
-            const int le = t;
-            const int64_t e = e0 + le;
+            const int64_t e = e0 + t;
             double total = 0.0;
-            bool d;
-            if (done) {
-                for (int ag = 0; ag < n; ++ag) a.reward[step * R + static_cast<int64_t>(ag) * E + e] = 0.0f;
-                d = true;
-            } else {
-                for (int ag = 0; ag < n; ++ag) {  // moves (envs.cpp:114-126)
-                    double dx = 0.0, dy = 0.0;
-                    switch (acts[ag * EPC + le]) {
-                        case 1: dx = 0.1; break;
-                        case 2: dx = -0.1; break;
-                        case 3: dy = 0.1; break;
-                        case 4: dy = -0.1; break;
-                        default: break;
-                    }
-                    sts[(2 * ag) * EPC + le] = __dadd_rn(sts[(2 * ag) * EPC + le], dx);
-                    sts[(2 * ag + 1) * EPC + le] = __dadd_rn(sts[(2 * ag + 1) * EPC + le], dy);
-                }
-                for (int ag = 0; ag < n; ++ag) {  // rewards (envs.cpp:128-144)
-                    const double xa = sts[(2 * ag) * EPC + le], ya = sts[(2 * ag + 1) * EPC + le];
-                    double best = 1e18;
-                    for (int lm = 0; lm < n; ++lm) {
-                        const double dx = __dsub_rn(sts[(2 * n + 2 * lm) * EPC + le], xa);
-                        const double dy = __dsub_rn(sts[(2 * n + 2 * lm + 1) * EPC + le], ya);
-                        const double dist = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
-                        best = dist < best ? dist : best;
-                    }
-                    double r = -best;
-                    for (int b = 0; b < n; ++b) {
-                        if (b == ag) continue;
-                        const double dx = __dsub_rn(sts[(2 * b) * EPC + le], xa);
-                        const double dy = __dsub_rn(sts[(2 * b + 1) * EPC + le], ya);
-                        if (__dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy))) < 0.1) r = __dsub_rn(r, 0.5);
-                    }
-                    total = __dadd_rn(total, r);
-                    a.reward[step * R + static_cast<int64_t>(ag) * E + e] = static_cast<float>(r);
-                }
+            bool d = true;
+            if (!done) {
+                for (int ag = 0; ag < n; ++ag) total = __dadd_rn(total, rews[ag * EPC + t]);
                 d = a.env.max_steps > 0 && stepc + 1 >= a.env.max_steps;
                 stepc += 1;
             }
             done = d;
+            dns[t] = d ? 1 : 0;
             a.reward_d[step * E + e] = total;
             for (int ag = 0; ag < n; ++ag) a.done_f[step * R + static_cast<int64_t>(ag) * E + e] = d ? 1.0f : 0.0f;
         }

@@ -372,8 +372,9 @@ void Engine::alloc() {
         int sms = 0;
         FLW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         b.grid = static_cast<int>(std::min<int64_t>(sms, (TR_ + 127) / 128));
-        b.part_p = b.alloc<float>(static_cast<int64_t>(b.grid) * s.P_policy);
-        b.part_c = b.alloc<float>(static_cast<int64_t>(b.grid) * (s.P - s.P_policy));
+        // rows padded to 4 floats: the fused update reads them as float4
+        b.part_p = b.alloc<float>(static_cast<int64_t>(b.grid) * ((s.P_policy + 3) / 4 * 4));
+        b.part_c = b.alloc<float>(static_cast<int64_t>(b.grid) * ((s.P - s.P_policy + 3) / 4 * 4));
         b.loss_parts = b.alloc<float>(2 * 3 * b.grid);
         b.wimg_p = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.pol) / 2));
         b.wimg_c = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.crit) / 2));
@@ -775,7 +776,10 @@ void Engine::enq_learn_fast() {
     f.hload = 0;
     f.kind = ppo ? kNetPolicyPpo : kNetPolicyA3c;
     f.partials = b.part_p;
-    f.part_stride = s.P_policy;
+    // one GPU, one unit, no exchange: the reduction is fused with Adam (enq_grad_sync_and_adam)
+    // and reads 16-byte aligned partial rows
+    fused_pending_ = fuse_ok_ && !p2p_enabled() && !(comm_ && comm_->nranks() > 1) && !cfast_ && nrep_ == 1;
+    f.part_stride = fused_pending_ ? (s.P_policy + 3) / 4 * 4 : s.P_policy;
     f.loss_partials = b.loss_parts;
     // The policy and critic learn kernels run CONCURRENTLY on disjoint SMs (two streams), the
     // SMs split in proportion to their per-tile cost (the critic skips its forward), so both
@@ -804,7 +808,7 @@ void Engine::enq_learn_fast() {
     fc.partials = b.part_c;
     // compact critic: the fused kernel owns layers 1.. (and reports dZ wrt its input rows)
     const int64_t c_off = cfast_ ? static_cast<int64_t>(J + s.n_agents) * H0 + H0 : 0;
-    fc.part_stride = s.P - s.P_policy - c_off;
+    fc.part_stride = fused_pending_ ? (s.P - s.P_policy + 3) / 4 * 4 : s.P - s.P_policy - c_off;
     fc.dx_out = cfast_ ? b.dz0 : nullptr;
     fc.loss_partials = b.loss_parts + 3 * gp;
     if (concurrent) {
@@ -818,8 +822,6 @@ void Engine::enq_learn_fast() {
     }
     b.lgrid_p = gp;
     b.lgrid_c = gc;
-    // one GPU, one unit, no exchange: the reduction is fused with Adam (enq_grad_sync_and_adam)
-    fused_pending_ = fuse_ok_ && !p2p_enabled() && !(comm_ && comm_->nranks() > 1) && !cfast_ && nrep_ == 1;
     if (!p2p_enabled() && !fused_pending_) {  // with peer-memory exchange the reduction is fused into the exchange
         probe_begin("reduce");
         fast_reduce_partials(stream_, b.part_p, b.part_c, gp, gc, s.P_policy, s.P - s.P_policy - c_off, b.grads,

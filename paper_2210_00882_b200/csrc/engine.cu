@@ -779,7 +779,8 @@ void Engine::enq_learn_fast() {
     // one GPU, one unit, no exchange: the reduction is fused with Adam (enq_grad_sync_and_adam)
     // and reads 16-byte aligned partial rows
     fused_pending_ = fuse_ok_ && !p2p_enabled() && !(comm_ && comm_->nranks() > 1) && !cfast_ && nrep_ == 1;
-    f.part_stride = fused_pending_ ? (s.P_policy + 3) / 4 * 4 : s.P_policy;
+    const bool padded = fused_pending_ || (p2p_enabled() && !cfast_);  // float4 partial rows
+    f.part_stride = padded ? (s.P_policy + 3) / 4 * 4 : s.P_policy;
     f.loss_partials = b.loss_parts;
     // The policy and critic learn kernels run CONCURRENTLY on disjoint SMs (two streams), the
     // SMs split in proportion to their per-tile cost (the critic skips its forward), so both
@@ -808,7 +809,7 @@ void Engine::enq_learn_fast() {
     fc.partials = b.part_c;
     // compact critic: the fused kernel owns layers 1.. (and reports dZ wrt its input rows)
     const int64_t c_off = cfast_ ? static_cast<int64_t>(J + s.n_agents) * H0 + H0 : 0;
-    fc.part_stride = fused_pending_ ? (s.P - s.P_policy + 3) / 4 * 4 : s.P - s.P_policy - c_off;
+    fc.part_stride = padded ? (s.P - s.P_policy + 3) / 4 * 4 : s.P - s.P_policy - c_off;
     fc.dx_out = cfast_ ? b.dz0 : nullptr;
     fc.loss_partials = b.loss_parts + 3 * gp;
     if (concurrent) {

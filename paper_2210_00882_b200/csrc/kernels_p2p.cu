@@ -1,12 +1,14 @@
 // Gradient all-reduce over NVLink peer memory, fused with the producing reduction and with
 // Adam (fast numerics, k GPUs). Replaces  k_reduce_partials -> ncclAllReduce -> k_adam:
 //
-//   k_reduce_push  one block per 32-parameter chunk reduces the per-CTA dW partials (fixed
-//                  order) and its warp r stores the chunk straight into rank r's inbox[rank]
-//                  over NVLink, then releases flag[chunk][rank] on rank r (system scope). The
-//                  exchange of a chunk overlaps the reduction of the others; it never waits.
-//   k_sum_adam     one warp per chunk acquires the k flags, sums inbox[0..k-1] in rank order
-//                  (every rank computes the identical mean, deterministic) and applies Adam.
+//   k_reduce_push  one block per 128-parameter chunk reduces the per-CTA dW partials (fixed
+//                  order, float4 rows) and stores the chunk straight into every rank's
+//                  inbox[rank] over NVLink, then releases flag[chunk][rank] on each rank (system
+//                  scope). The exchange of a chunk overlaps the reduction of the others; it
+//                  never waits.
+//   k_sum_adam     one block per chunk acquires the k flags, sums inbox[0..k-1] in rank order
+//                  (every rank computes the identical mean, deterministic), applies Adam and
+//                  refreshes the bf16 weight images.
 //                  It waits only on k_reduce_push kernels, so no residency requirement.
 //
 // Flags are monotonically increasing epochs (DeviceCtx::coll_seq), never reset. Region layout
@@ -36,56 +38,78 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 
 __global__ void k_coll_tick(DeviceCtx* ctx) { ++ctx->coll_seq; }
 
-// A: reduce the per-CTA dW partials of one 32-parameter chunk (fixed order) and push the chunk
+// Chunks of 128 parameters in the padded index space [policy rows padded to 4][critic rows
+// padded to 4] (the learn kernels write 16-byte aligned partial rows), so a lane's float4 never
+// straddles the two nets. pad_to_flat maps a padded index to the flat parameter index (-1: pad).
+__device__ __forceinline__ int64_t pad_to_flat(const P2pArgs& a, int64_t ip) {
+    const int64_t Pps = (a.Pp + 3) / 4 * 4, Pcs = (a.Pc + 3) / 4 * 4;
+    if (ip < Pps) return ip < a.Pp ? ip : -1;
+    const int64_t c = ip - Pps;
+    return c < a.Pc && ip < Pps + Pcs ? a.Pp + c : -1;
+}
+
+// A: reduce the per-CTA dW partials of one 128-parameter chunk (fixed order: warp w sums
+// partials w, w+8, ... as float4 rows, then the 8 warp sums in warp order) and push the chunk
 // into EVERY rank's inbox[rank] over NVLink; then release flag[chunk][rank] on every rank.
 // Never waits, so any grid size is safe.
 __global__ void __launch_bounds__(256) k_reduce_push(P2pArgs a) {
-    __shared__ float ws[8][32];
+    __shared__ float4 ws[8][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x;
     const uint64_t epoch = a.ctx->coll_seq;
     const int64_t P = a.Pp + a.Pc;
-    const int64_t i = 32LL * c + lane;
-    const bool ok = i < P;
-    const float* src = !ok ? a.part_p : (i < a.Pp ? a.part_p + i : a.part_c + (i - a.Pp));
-    const int64_t stride = i < a.Pp ? a.Pp : a.Pc;
-    const int nparts = i < a.Pp ? a.np : a.nc;
-    float s = 0.0f;
-    if (ok) {
-#pragma unroll 8
-        for (int p = w; p < nparts; p += 8) s += src[p * stride];  // loads hoisted, adds in order
+    const int64_t Pps = (a.Pp + 3) / 4 * 4, Pcs = (a.Pc + 3) / 4 * 4;
+    const int64_t q0 = 128LL * c + 4 * lane;
+    float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q0 < Pps + Pcs) {
+        const bool pol = q0 < Pps;
+        const float* base = pol ? a.part_p + q0 : a.part_c + (q0 - Pps);
+        const int64_t stride = pol ? Pps : Pcs;
+        const int nparts = pol ? a.np : a.nc;
+#pragma unroll 4
+        for (int p = w; p < nparts; p += 8) {  // loads hoisted, adds in order
+            const float4 v = *reinterpret_cast<const float4*>(base + p * stride);
+            s4.x += v.x;
+            s4.y += v.y;
+            s4.z += v.z;
+            s4.w += v.w;
+        }
     }
-    ws[w][lane] = s;
+    ws[w][lane] = s4;
     __syncthreads();
-    float t = 0.0f;
+    if (threadIdx.x < 128) {
+        const int64_t i = pad_to_flat(a, 128LL * c + threadIdx.x);
+        if (i >= 0) {
+            float t = 0.0f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += ws[k][lane];
-    for (int r = w; r < a.k; r += 8) {  // warp w pushes the chunk to ranks w, w+8, ...
-        // inbox[epoch & 1]: rank r may still be reading the previous exchange's buffer
-        float* inbox = reinterpret_cast<float*>(a.peers[r] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
-        if (ok) inbox[static_cast<int64_t>(a.rank) * P + i] = t;
-        __syncwarp();
-        if (lane == 0)  // release: this warp's chunk stores are ordered before the flag
-            st_release_sys(reinterpret_cast<uint64_t*>(a.peers[r] + a.off_sflag) +
-                               static_cast<int64_t>(c) * a.k + a.rank,
-                           epoch);
+            for (int k = 0; k < 8; ++k) t += reinterpret_cast<const float*>(&ws[k][threadIdx.x >> 2])[threadIdx.x & 3];
+            for (int r = 0; r < a.k; ++r) {
+                // inbox[epoch & 1]: rank r may still be reading the previous exchange's buffer
+                float* inbox = reinterpret_cast<float*>(a.peers[r] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
+                inbox[static_cast<int64_t>(a.rank) * P + i] = t;
+            }
+        }
     }
+    __syncthreads();
+    if (threadIdx.x < a.k)  // release: the block's chunk stores are ordered before the flag
+        st_release_sys(reinterpret_cast<uint64_t*>(a.peers[threadIdx.x] + a.off_sflag) +
+                           static_cast<int64_t>(c) * a.k + a.rank,
+                       epoch);
 }
 
 // B: wait for the k ranks' copies of the chunk, sum them in rank order (every rank computes
 // the identical mean) and apply Adam (adam_step, mlp.cpp:480-495; 1/k folded into the step).
 // Waits only on A kernels, which never wait: no residency requirement.
-__global__ void __launch_bounds__(32) k_sum_adam(P2pArgs a) {
-    const int lane = threadIdx.x;
+__global__ void __launch_bounds__(128) k_sum_adam(P2pArgs a) {
     const int c = blockIdx.x;
     const uint64_t epoch = a.ctx->coll_seq;
     const int64_t P = a.Pp + a.Pc;
     const uint64_t* flag = reinterpret_cast<const uint64_t*>(a.peers[a.rank] + a.off_sflag) + static_cast<int64_t>(c) * a.k;
-    for (int r = lane; r < a.k; r += 32)
+    for (int r = threadIdx.x; r < a.k; r += blockDim.x)
         while (ld_acquire_sys(flag + r) < epoch) __nanosleep(32);
-    __syncwarp();
-    const int64_t i = 32LL * c + lane;
-    if (i >= P) return;
+    __syncthreads();
+    const int64_t i = pad_to_flat(a, 128LL * c + threadIdx.x);
+    if (i < 0) return;
     const float* inbox =
         reinterpret_cast<const float*>(a.peers[a.rank] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
     float gs = 0.0f;
@@ -124,9 +148,10 @@ P2pLayout p2p_layout(int k, int64_t P) {
 void coll_tick(cudaStream_t s, DeviceCtx* ctx) { k_coll_tick<<<1, 1, 0, s>>>(ctx); }
 
 void reduce_allreduce_adam(cudaStream_t s, const P2pArgs& a) {
-    const unsigned nchunks = static_cast<unsigned>((a.Pp + a.Pc + 31) / 32);
+    const int64_t padded = (a.Pp + 3) / 4 * 4 + (a.Pc + 3) / 4 * 4;
+    const unsigned nchunks = static_cast<unsigned>((padded + 127) / 128);  // <= the layout's flag rows
     k_reduce_push<<<nchunks, 256, 0, s>>>(a);
-    k_sum_adam<<<nchunks, 32, 0, s>>>(a);
+    k_sum_adam<<<nchunks, 128, 0, s>>>(a);
 }
 
 }  // namespace flw

@@ -788,7 +788,7 @@ void Engine::enq_learn_fast() {
     int gp = lgrid, gc = lgrid;
     const bool concurrent = hreuse && lgrid >= 8;  // the critic reads hsave, not hscratch
     if (concurrent) {
-        static const double split = std::getenv("FLW_LEARN_SPLIT") ? std::atof(std::getenv("FLW_LEARN_SPLIT")) : 0.6;
+        static const double split = std::getenv("FLW_LEARN_SPLIT") ? std::atof(std::getenv("FLW_LEARN_SPLIT")) : 0.7;
         gp = std::max(1, std::min(lgrid - 1, static_cast<int>(lgrid * split + 0.5)));
         gc = std::max(1, lgrid - gp);
         FLW_CUDA(cudaEventRecord(ev_lfork_, stream_));

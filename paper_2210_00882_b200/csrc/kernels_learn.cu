@@ -38,7 +38,7 @@ constexpr int kRows = 128;
 constexpr int kMaxW = 64;
 constexpr int kGroups = 3;  // tiles in flight per CTA (one epilogue group of 4 warps each)
 constexpr int kEpiWarps = 4 * kGroups;
-constexpr int kThreads = 32 * (kEpiWarps + 1);
+constexpr int kThreads = 32 * (kEpiWarps + 2);  // + producer + loader (learn-reuse mode)
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
 constexpr int kXPre = 32;                      // input columns prefetched in registers
 #ifndef FLW_TANH_MUFU_PAIRS
@@ -303,15 +303,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #endif
                         } else {  // ---- backward layer m: dH_m = dZ_m W_m and dW_m = H_{m-1}^T dZ_m
                             const int m = L - 1 - (j - nfwd);
-                            if (j == nfwd) {
-                                if (fwd) {  // the forward's bulk stores are in global memory
-                                    if (lane == 0) umma::bulk_wait_all();
-                                    __syncwarp();
+                            if (!reuse) {  // (learn-reuse: the loader warp issues these copies)
+                                if (j == nfwd) {
+                                    if (fwd) {  // the forward's bulk stores are in global memory
+                                        if (lane == 0) umma::bulk_wait_all();
+                                        __syncwarp();
+                                    }
+                                    if (!resident(m - 1)) load_h(g, tl[g], m - 1);
                                 }
-                                if (!resident(m - 1)) load_h(g, tl[g], m - 1);
+                                // prefetch H_{m-2} into the slot H_m freed (its readers were stage m + 1)
+                                if (m - 2 >= -1 && !resident(m - 2)) load_h(g, tl[g], m - 2);
                             }
-                            // prefetch H_{m-2} into the slot H_m freed (its readers were stage m + 1)
-                            if (m - 2 >= -1 && !resident(m - 2)) load_h(g, tl[g], m - 2);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
 #endif
@@ -339,6 +341,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             }
             if (lane == 0) umma::bulk_wait_all();  // values pass: saved activations written, slots read
             __syncwarp();
+        }
+    } else if (w == kEpiWarps + 1) {
+        // ================================================================ loader (learn-reuse)
+        // The critic learn pass streams every tile it reads from the values pass's save area; a
+        // second issuing warp follows the producer's stage sequence (same epi_done hand-offs) and
+        // issues those TMA copies, so the producer only issues MMAs (it waits the ldbar
+        // barriers). The copy into the slot of H_m happens once stage m + 1's epilogue (its last
+        // reader, after stage m + 1's MMAs completed) handed off.
+        if constexpr (reuse) {
+            uint32_t ph_epi[kGroups] = {};
+            auto hsrc = [&](int64_t tile) -> uint8_t* { return a.hsave + static_cast<size_t>(tile) * C.hbytes; };
+            auto load_h = [&](int g, int64_t tile, int k) {  // H_k (k = -1: X) -> ring slot k & 1
+                if (lane == 0) {
+                    const uint32_t bytes = static_cast<uint32_t>(kRows * hwidth(k) * 2);
+                    umma::mbar_expect_tx(&ldbar[g][k & 1], bytes);
+                    umma::bulk_g2s_hint(smem + C.ring[g][k & 1], hsrc(tile) + C.hoff[k + 1], bytes, &ldbar[g][k & 1],
+                                        umma::policy_evict_first());
+                }
+                __syncwarp();
+            };
+            for (int64_t it = 0;; ++it) {
+                int64_t tl[kGroups];
+                bool has[kGroups], any = false;
+                for (int g = 0; g < kGroups; ++g) {
+                    tl[g] = it * kGroups * G + kGroups * static_cast<int64_t>(blockIdx.x) + g;
+                    has[g] = tl[g] < ntiles;
+                    any = any || has[g];
+                }
+                if (!any) break;
+                for (int j = 0; j < njobs; ++j) {
+                    for (int g = 0; g < kGroups; ++g) {
+                        if (!has[g]) continue;
+                        umma::mbar_wait(&epi_done[g], ph_epi[g]);
+                        ph_epi[g] ^= 1;
+                        const int m = L - 1 - j;
+                        if (j == 0) load_h(g, tl[g], m - 1);
+                        if (m - 2 >= -1) load_h(g, tl[g], m - 2);
+                    }
+                }
+            }
         }
     } else {
         // ================================================================ epilogue groups

@@ -157,7 +157,7 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 template <int MODE, int ACT>
 __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar;
+    __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], st_done[kGroups], wbar;
     __shared__ uint32_t tslot;
     __shared__ Carve C;  // offsets live in shared memory, not in 40 registers per thread
 #ifdef FLW_LEARN_TRACE
@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             umma::mbar_init(&epi_done[g], 4);
             umma::mbar_init(&ldbar[g][0], 1);
             umma::mbar_init(&ldbar[g][1], 1);
+            umma::mbar_init(&st_done[g], 1);
         }
         umma::mbar_init(&wbar, 1);
         umma::fence_barrier_init();
@@ -222,15 +223,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             auto hsrc = [&](int g, int64_t tile) -> uint8_t* {
                 return reuse ? a.hsave + static_cast<size_t>(tile) * C.hbytes
                              : a.hscratch + static_cast<size_t>(kGroups * blockIdx.x + g) * C.hbytes;
-            };
-            auto load_h = [&](int g, int64_t tile, int k) {  // H_k (k = -1: X) -> ring slot k & 1
-                if (umma::elect_one()) {
-                    const uint32_t bytes = static_cast<uint32_t>(kRows * hwidth(k) * 2);
-                    umma::mbar_expect_tx(&ldbar[g][k & 1], bytes);
-                    umma::bulk_g2s_hint(smem + C.ring[g][k & 1], hsrc(g, tile) + C.hoff[k + 1], bytes,
-                                        &ldbar[g][k & 1], umma::policy_evict_first());  // read once
-                }
-                __syncwarp();
             };
             auto issue_dw = [&](int g, int l, uint32_t hin) {  // dW_l += H_{l-1}^T dZ_l  (M = din_l)
                 const int di = n.din[l], dout = n.dout[l];
@@ -303,16 +295,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #endif
                         } else {  // ---- backward layer m: dH_m = dZ_m W_m and dW_m = H_{m-1}^T dZ_m
                             const int m = L - 1 - (j - nfwd);
-                            if (!reuse) {  // (learn-reuse: the loader warp issues these copies)
-                                if (j == nfwd) {
-                                    if (fwd) {  // the forward's bulk stores are in global memory
-                                        if (lane == 0) umma::bulk_wait_all();
-                                        __syncwarp();
-                                    }
-                                    if (!resident(m - 1)) load_h(g, tl[g], m - 1);
+                            // (the loader warp issues the backward's TMA copies)
+                            if (j == nfwd && fwd) {  // the forward's bulk stores are in global memory
+                                if (lane == 0) {
+                                    umma::bulk_wait_all();
+                                    mbar_arrive(&st_done[g]);  // the loader may read them back
                                 }
-                                // prefetch H_{m-2} into the slot H_m freed (its readers were stage m + 1)
-                                if (m - 2 >= -1 && !resident(m - 2)) load_h(g, tl[g], m - 2);
+                                __syncwarp();
                             }
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
@@ -343,21 +332,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             __syncwarp();
         }
     } else if (w == kEpiWarps + 1) {
-        // ================================================================ loader (learn-reuse)
-        // The critic learn pass streams every tile it reads from the values pass's save area; a
-        // second issuing warp follows the producer's stage sequence (same epi_done hand-offs) and
-        // issues those TMA copies, so the producer only issues MMAs (it waits the ldbar
-        // barriers). The copy into the slot of H_m happens once stage m + 1's epilogue (its last
-        // reader, after stage m + 1's MMAs completed) handed off.
-        if constexpr (reuse) {
-            uint32_t ph_epi[kGroups] = {};
-            auto hsrc = [&](int64_t tile) -> uint8_t* { return a.hsave + static_cast<size_t>(tile) * C.hbytes; };
+        // ================================================================ loader (learn modes)
+        // The backward streams the activation tiles it does not keep resident back from global
+        // memory (learn: this CTA's scratch, written by the producer's bulk stores during the
+        // forward; learn-reuse: the values pass's save area). A second issuing warp follows the
+        // producer's stage sequence (same epi_done hand-offs) and issues those TMA copies, so the
+        // producer only issues MMAs (it waits the ldbar barriers). The copy into the slot of H_m
+        // happens once stage m + 1's epilogue (its last reader, after stage m + 1's MMAs
+        // completed) handed off; in learn mode the first one after the producer flushed its stores.
+        if constexpr (learn) {
+            uint32_t ph_epi[kGroups] = {}, ph_st[kGroups] = {};
+            auto hsrc = [&](int g, int64_t tile) -> uint8_t* {
+                return reuse ? a.hsave + static_cast<size_t>(tile) * C.hbytes
+                             : a.hscratch + static_cast<size_t>(kGroups * blockIdx.x + g) * C.hbytes;
+            };
             auto load_h = [&](int g, int64_t tile, int k) {  // H_k (k = -1: X) -> ring slot k & 1
                 if (lane == 0) {
                     const uint32_t bytes = static_cast<uint32_t>(kRows * hwidth(k) * 2);
                     umma::mbar_expect_tx(&ldbar[g][k & 1], bytes);
-                    umma::bulk_g2s_hint(smem + C.ring[g][k & 1], hsrc(tile) + C.hoff[k + 1], bytes, &ldbar[g][k & 1],
-                                        umma::policy_evict_first());
+                    umma::bulk_g2s_hint(smem + C.ring[g][k & 1], hsrc(g, tile) + C.hoff[k + 1], bytes,
+                                        &ldbar[g][k & 1], umma::policy_evict_first());
                 }
                 __syncwarp();
             };
@@ -375,9 +369,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                         if (!has[g]) continue;
                         umma::mbar_wait(&epi_done[g], ph_epi[g]);
                         ph_epi[g] ^= 1;
-                        const int m = L - 1 - j;
-                        if (j == 0) load_h(g, tl[g], m - 1);
-                        if (m - 2 >= -1) load_h(g, tl[g], m - 2);
+                        if (j < nfwd) continue;  // forward stages: nothing to stream
+                        const int m = L - 1 - (j - nfwd);
+                        if (j == nfwd && fwd) {  // the producer's stores of this tile are flushed
+                            umma::mbar_wait(&st_done[g], ph_st[g]);
+                            ph_st[g] ^= 1;
+                            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                        }
+                        if (j == nfwd && !resident(m - 1)) load_h(g, tl[g], m - 1);
+                        if (m - 2 >= -1 && !resident(m - 2)) load_h(g, tl[g], m - 2);
                     }
                 }
             }

@@ -95,6 +95,17 @@ __host__ __device__ inline Carve carve_learn(const FastNet& n) {
 __device__ __forceinline__ uint32_t uni(uint32_t x) { return __shfl_sync(0xffffffffu, x, 0); }
 __device__ __forceinline__ int uni(int x) { return __shfl_sync(0xffffffffu, x, 0); }
 
+// Monotonic shared-memory hand-off counters (the loader may trail the epilogue by several
+// stages, which a parity-tracked mbarrier cannot tell apart).
+__device__ __forceinline__ void cnt_add_release(uint32_t* c) {
+    asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;\n" ::"r"(umma::smem_u32(c)) : "memory");
+}
+__device__ __forceinline__ uint32_t cnt_acquire(const uint32_t* c) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n" : "=r"(v) : "r"(umma::smem_u32(c)) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_u32(bar)) : "memory");
 }
@@ -157,8 +168,11 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 template <int MODE, int ACT>
 __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], st_done[kGroups], wbar;
+    __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar;
     __shared__ uint32_t tslot;
+    __shared__ uint32_t epi_cnt[kGroups];  // epilogue hand-offs per group (4 per stage), for the loader
+    __shared__ uint32_t rd_cnt[kGroups];   // loader: bulk stores whose smem read completed (producer)
+    __shared__ uint32_t xf_cnt[kGroups];   // loader, values pass: last saved tile read (epilogue)
     __shared__ Carve C;  // offsets live in shared memory, not in 40 registers per thread
 #ifdef FLW_LEARN_TRACE
     __shared__ long long tr_p[4][64], tr_e[3][64], tr_f[5][16];
@@ -183,6 +197,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     // stay resident there (never reloaded)
     auto resident = [&](int k) { return fwd && (k == L - 2 || k == L - 3); };
     auto hwidth = [&](int k) { return k < 0 ? n.din[0] : n.dout[k]; };
+    // where the forward saves H_k of a tile (k = -1: X): this group's scratch (learn, the tiles
+    // the backward does not keep resident) or the values pass's save area; null: not saved
+    auto save_dst = [&](int g, int64_t tile, int k) -> uint8_t* {
+        if (learn) return resident(k) ? nullptr : a.hscratch + static_cast<size_t>(kGroups * blockIdx.x + g) * C.hbytes;
+        return (a.hsave && tile < a.save_tiles) ? a.hsave + static_cast<size_t>(tile) * C.hbytes : nullptr;
+    };
 
     // ---- setup
     if (t == 0) {
@@ -191,9 +211,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             umma::mbar_init(&epi_done[g], 4);
             umma::mbar_init(&ldbar[g][0], 1);
             umma::mbar_init(&ldbar[g][1], 1);
-            umma::mbar_init(&st_done[g], 1);
+
         }
         umma::mbar_init(&wbar, 1);
+        for (int g = 0; g < kGroups; ++g) epi_cnt[g] = rd_cnt[g] = xf_cnt[g] = 0;
         umma::fence_barrier_init();
     }
     for (int l = 0; l < L; ++l)
@@ -214,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             if (umma::elect_one()) bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
             __syncwarp();
             umma::mbar_wait(&wbar, 0);
-            uint32_t ph_epi[kGroups] = {}, ph_ld[kGroups][2] = {};
+            uint32_t ph_epi[kGroups] = {}, ph_ld[kGroups][2] = {}, need_rd[kGroups] = {};
             bool dw_init[kMaxLayers];
             for (int l = 0; l < kMaxLayers; ++l) dw_init[l] = false;
             auto dw_tmem = [&](int l) {
@@ -258,27 +279,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
 #endif
-                            {  // H_{l-1} (X for l = 0) is complete in its ring slot: save it (TMA bulk store)
-                                const int hk = l - 1;
-                                uint8_t* gdst = nullptr;
-                                if (learn) {
-                                    if (!resident(hk))
-                                        gdst = a.hscratch + static_cast<size_t>(kGroups * blockIdx.x + g) * C.hbytes;
-                                } else if (a.hsave && tl[g] < a.save_tiles) {
-                                    gdst = a.hsave + static_cast<size_t>(tl[g]) * C.hbytes;
-                                }
-                                if (lane == 0) {
-                                    if (gdst) {  // the critic learn re-reads the values pass's tiles: keep in L2
-                                        umma::bulk_s2g_hint(gdst + C.hoff[hk + 1], smem + C.ring[g][hk & 1],
-                                                            static_cast<uint32_t>(kRows * hwidth(hk) * 2),
-                                                            learn ? umma::policy_evict_first() : umma::policy_evict_last());
-                                        umma::bulk_commit();
-                                    }
-                                    // every older store has read its slot: the epilogue may overwrite
-                                    // the slot of H_{l-2} once this job's MMAs commit
-                                    umma::bulk_wait_read1();
-                                }
-                                __syncwarp();
+                            // the epilogue of this job overwrites the slot of H_{l-2}: the loader's
+                            // bulk store of it must have read the slot
+                            if (l >= 1 && save_dst(g, tl[g], l - 2)) {
+                                ++need_rd[g];
+                                while (cnt_acquire(&rd_cnt[g]) < need_rd[g]) __nanosleep(20);
                             }
                             const uint32_t in = uni(sbase + C.ring[g][(l - 1) & 1]);
                             const uint32_t wl = uni(sbase + C.wt[l]);
@@ -295,14 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 #endif
                         } else {  // ---- backward layer m: dH_m = dZ_m W_m and dW_m = H_{m-1}^T dZ_m
                             const int m = L - 1 - (j - nfwd);
-                            // (the loader warp issues the backward's TMA copies)
-                            if (j == nfwd && fwd) {  // the forward's bulk stores are in global memory
-                                if (lane == 0) {
-                                    umma::bulk_wait_all();
-                                    mbar_arrive(&st_done[g]);  // the loader may read them back
-                                }
-                                __syncwarp();
-                            }
+                            // (the loader warp issues the activation tiles' TMA copies)
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
 #endif
@@ -328,8 +326,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     }
                 }
             }
-            if (lane == 0) umma::bulk_wait_all();  // values pass: saved activations written, slots read
-            __syncwarp();
         }
     } else if (w == kEpiWarps + 1) {
         // ================================================================ loader (learn modes)
@@ -340,8 +336,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
         // producer only issues MMAs (it waits the ldbar barriers). The copy into the slot of H_m
         // happens once stage m + 1's epilogue (its last reader, after stage m + 1's MMAs
         // completed) handed off; in learn mode the first one after the producer flushed its stores.
-        if constexpr (learn) {
-            uint32_t ph_epi[kGroups] = {}, ph_st[kGroups] = {};
+        {
+            uint32_t seen[kGroups] = {};  // hand-offs consumed per group
+            // the last bulk store whose smem read is not yet released (g * 2 + (values-pass last
+            // tile ? 1 : 0), -1: none): released when the next store is issued (wait_group.read 1)
+            // or before the loader would block waiting for a hand-off
+            int pend = -1;
+            auto release = [&](int e) { cnt_add_release((e & 1) ? &xf_cnt[e >> 1] : &rd_cnt[e >> 1]); };
+            auto flush = [&]() {
+                if (pend >= 0) {
+                    if (lane == 0) {
+                        umma::bulk_wait_read();
+                        release(pend);
+                    }
+                    __syncwarp();
+                    pend = -1;
+                }
+            };
             auto hsrc = [&](int g, int64_t tile) -> uint8_t* {
                 return reuse ? a.hsave + static_cast<size_t>(tile) * C.hbytes
                              : a.hscratch + static_cast<size_t>(kGroups * blockIdx.x + g) * C.hbytes;
@@ -367,13 +378,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                 for (int j = 0; j < njobs; ++j) {
                     for (int g = 0; g < kGroups; ++g) {
                         if (!has[g]) continue;
-                        umma::mbar_wait(&epi_done[g], ph_epi[g]);
-                        ph_epi[g] ^= 1;
-                        if (j < nfwd) continue;  // forward stages: nothing to stream
+                        ++seen[g];
+                        if (cnt_acquire(&epi_cnt[g]) < 4u * seen[g]) {
+                            flush();
+                            while (cnt_acquire(&epi_cnt[g]) < 4u * seen[g]) __nanosleep(20);
+                        }
+                        if (j < nfwd) {  // forward job l: H_{l-1} (X for l = 0) is complete, save it
+                            const int hk = j - 1;
+                            uint8_t* gdst = save_dst(g, tl[g], hk);
+                            if (gdst) {
+                                if (lane == 0) {  // the critic learn re-reads the values pass's tiles
+                                    umma::bulk_s2g_hint(gdst + C.hoff[hk + 1], smem + C.ring[g][hk & 1],
+                                                        static_cast<uint32_t>(kRows * hwidth(hk) * 2),
+                                                        learn ? umma::policy_evict_first() : umma::policy_evict_last());
+                                    umma::bulk_commit();
+                                    if (pend >= 0) {  // every older store has read its slot
+                                        umma::bulk_wait_read1();
+                                        release(pend);
+                                    }
+                                }
+                                __syncwarp();
+                                // values pass: the last saved tile shares its slot with the next
+                                // tile's X, which the epilogue writes (not an MMA)
+                                pend = 2 * g + (!learn && hk == L - 2 ? 1 : 0);
+                            }
+                            continue;
+                        }
                         const int m = L - 1 - (j - nfwd);
-                        if (j == nfwd && fwd) {  // the producer's stores of this tile are flushed
-                            umma::mbar_wait(&st_done[g], ph_st[g]);
-                            ph_st[g] ^= 1;
+                        if (j == nfwd && fwd) {  // this tile's stores are in global memory
+                            flush();
+                            if (lane == 0) umma::bulk_wait_all();
+                            __syncwarp();
                             asm volatile("fence.proxy.async.global;\n" ::: "memory");
                         }
                         if (j == nfwd && !resident(m - 1)) load_h(g, tl[g], m - 1);
@@ -381,6 +416,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
                     }
                 }
             }
+            flush();
+            if (lane == 0) umma::bulk_wait_all();  // values pass: the saved tiles are written
+            __syncwarp();
         }
     } else {
         // ================================================================ epilogue groups
@@ -388,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
         const int r = 32 * q + lane;  // tile row == TMEM lane
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
         const uint32_t zt = tmem + lane_base + 64u * static_cast<uint32_t>(g);
-        uint32_t ph_mma = 0, ph_ld[2] = {0, 0};
+        uint32_t ph_mma = 0, ph_ld[2] = {0, 0}, need_xf = 0;
         float pl_acc = 0.0f, vl_acc = 0.0f, en_acc = 0.0f;
         float* mydb = dbacc + w * kMaxLayers * kMaxW;
         const int din0 = n.din[0];
@@ -409,7 +447,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             umma::fence_async_smem();
             umma::fence_before_sync();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&epi_done[g]);
+            if (lane == 0) {
+                mbar_arrive(&epi_done[g]);
+                cnt_add_release(&epi_cnt[g]);
+            }
 #ifdef FLW_LEARN_TRACE
             if (t == 0 && ne_ev > 0 && ne_ev <= 64) tr_e[2][ne_ev - 1] = clock64();
 #endif
@@ -447,6 +488,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
             const bool valid = row < a.rows;
             // previous tile's last MMAs (dW_0) released X and dZ (dx mode: waited by its epilogue)
             if (learn && !first && !dx) wait_mma();
+            if (!learn && !first && save_dst(g, tile - kGroups * G, L - 2)) {  // values pass: see the loader
+                ++need_xf;
+                while (cnt_acquire(&xf_cnt[g]) < need_xf) __nanosleep(20);
+            }
             first = false;
             // ---- input tile (f32 -> bf16); learn-reuse: X comes from the values pass's save area
             if (!fwd) {

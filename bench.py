@@ -334,11 +334,13 @@ def bench_ours(args, world, rank, local):
     roofline = roofline_for(dom, sum(probes_dom) / len(probes_dom), ENVS_PER_GPU, peaks) if dom else None
     line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if args.envs_total else "weak", "vs_baseline": None,
             "dtype": "f32-storage/f64-accumulate" if args.numerics == "exact" else "bf16-mma/f32-accumulate",
             "data": "synthetic (synth17x6 env, seeded)",
-            "config": {"workload": f"C2: PPO synth17x6, 4096 envs/GPU, 7-layer MLP (hidden 6x{HIDDEN[0]}), T=32, "
-                                   "train_iters=4, dp-d fused loop", "envs_total": total, "envs_per_gpu":
+            "config": {"workload": (f"C4: PPO synth17x6, {total} envs over {world} learners" if args.envs_total else
+                                    "C2: PPO synth17x6, 4096 envs/GPU") +
+                                   f", 7-layer MLP (hidden 6x{HIDDEN[0]}), T=32, train_iters=4, dp-d fused loop",
+                       "envs_total": total, "envs_per_gpu":
                        ENVS_PER_GPU, "numerics": args.numerics, "parallelism": f"dp{world}",
                        "exchange": (args.exchange if args.numerics == "fast" else "nccl") if world > 1 else None,
                        "l2": "per-episode working set (activations, ~0.9 GB) exceeds the 126 MB L2"},
@@ -369,12 +371,18 @@ def main():
     ap.add_argument("--hidden", type=int, default=64,
                     help="hidden width H of the 7-layer MLP (SURVEY §8: H=64, also report H=256; fast numerics "
                          "supports H <= 64)")
+    ap.add_argument("--envs-total", type=int, default=0,
+                    help="strong scaling: this many envs split over the N GPUs (C4: 16384); default 4096 per GPU")
     ap.add_argument("--no-microbench", action="store_true",
                     help="skip the scaled HBM kernel sweeps (profiling runs: the launch list then holds episodes only)")
     args = ap.parse_args()
-    global HIDDEN
+    global HIDDEN, ENVS_PER_GPU
     HIDDEN = [args.hidden] * 6
     world, rank, local = dist_setup()
+    if args.envs_total:  # strong scaling (BASELINE configs[3]: 16384 envs over N learners)
+        if args.envs_total % world:
+            raise SystemExit("--envs-total must be a multiple of the GPU count")
+        ENVS_PER_GPU = args.envs_total // world
     if args.impl == "reference":
         bench_reference(args, world, rank)
     else:

@@ -96,6 +96,11 @@ __device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hi, ui
     lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
+// named barrier of env tile mt's four warps (ids 1.. ; 0 is __syncthreads)
+__device__ __forceinline__ void tile_sync(int mt) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + mt), "r"(128) : "memory");
+}
+
 __device__ __forceinline__ void mma_f16(float* d, const uint32_t* a, const uint32_t* b) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -141,9 +146,12 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     // zero the activation images once: padded input columns must read as 0
     for (uint32_t i = t; i < (S.logits - S.xhi) / 4; i += kThreads) reinterpret_cast<uint32_t*>(smem + S.xhi)[i] = 0u;
     __syncthreads();
-    // ---- env owner threads (warp 0): env state in registers
-    const bool owner = t < kEnvsPerCta;
-    const int64_t e = e0 + t;  // env of an owner thread
+    // ---- env owner threads: lanes 0-15 of warp mt own the 16 envs of env tile mt (state in
+    // registers). The env tiles are independent pipelines (MLP -> owner -> MLP ...) that sync on
+    // their own named barriers, so one tile's owner phase overlaps another tile's MLP.
+    const int le = 16 * warp + lane;  // local env of an owner thread
+    const bool owner = warp < kMT && lane < 16;
+    const int64_t e = e0 + le;  // env of an owner thread
     const bool live = owner && e < E;
     constexpr int SW = ENV == 0 ? 2 : kSynthObs;
     double st[SW];
@@ -154,9 +162,9 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     __half* xhi = reinterpret_cast<__half*>(smem + S.xhi);
     __half* xlo = reinterpret_cast<__half*>(smem + S.xlo);
     auto put_obs = [&](int j, float o) {  // next layer-0 input element (row t, column j), split
-        const int rr = t & 15, kc = j & 15;
+        const int rr = le & 15, kc = j & 15;
         const int ln = 4 * (rr & 7) + ((kc & 7) >> 1), reg = 2 * (kc >> 3) + (rr >> 3);
-        const int el = 2 * (4 * (((t >> 4) * KT0 + (j >> 4)) * 32 + ln) + reg) + (kc & 1);
+        const int el = 2 * (4 * (((le >> 4) * KT0 + (j >> 4)) * 32 + ln) + reg) + (kc & 1);
         const __half h = __float2half_rn(o);
         xhi[el] = h;
         xlo[el] = __float2half_rn(o - __half2float(h));
@@ -246,7 +254,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                     reinterpret_cast<uint4*>(smem + S.hlo[l & 1])[(mt * KTn + jw) * 32 + lane] = lo;
                 }
             }
-            __syncthreads();
+            tile_sync(mt);
         }
 #ifdef FLW_LEARN_TRACE
         if (step - a.step0 < 8) tr1[step - a.step0] = clock64();
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             // softmax in f32 (the reference's is double, rounded to f32: the probabilities differ
             // by <= ~1 f32 ulp, far below the f32-logit deviation the fast path already has);
             // the draw and the inverse-CDF walk are the reference's (double u, double cumsum)
-            const float* logits = reinterpret_cast<const float*>(smem + S.logits) + t * kLStride;
+            const float* logits = reinterpret_cast<const float*>(smem + S.logits) + le * kLStride;
             float p[16];
             float mx = logits[0];
             for (int c = 1; c < A; ++c) mx = fmaxf(mx, logits[c]);
@@ -336,7 +344,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             }
             done = done || d;
         }
-        __syncthreads();
+        tile_sync(mt);
 #ifdef FLW_LEARN_TRACE
         if (step - a.step0 < 8) tr2[step - a.step0] = clock64();
 #endif

@@ -749,7 +749,7 @@ void Engine::enq_learn_fast() {
     auto launch = [&](int grid) { fast_learn(stream_, f, grid); };
     f.hscratch = b.hscratch;
     probe_begin("critic_fwd");
-    const int64_t grp = fast_learn_groups();
+    const int64_t grp = fast_values_groups();
     launch(static_cast<int>(std::min<int64_t>(lgrid, ((f.rows + 127) / 128 + grp - 1) / grp)));
     probe_end();
     f.split_rows = -1;

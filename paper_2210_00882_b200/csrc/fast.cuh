@@ -73,7 +73,8 @@ void fast_build_wimg(cudaStream_t s, const float* params, const FastNet& n0, __n
 void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid);
 size_t fast_learn_smem_bytes(const FastNet& n);
 size_t fast_learn_scratch_bytes(const FastNet& n);  // hidden bytes of one 128-row tile
-int fast_learn_groups();  // tiles in flight per k_learn CTA
+int fast_learn_groups();   // tiles in flight per k_learn CTA (learn modes)
+int fast_values_groups();  // ... in the values pass (forward only)
 // fixed-order sums of the per-CTA partial slots: np policy slots, nc critic slots
 // Element index of flat parameter p (absolute, params layout) in its net's bf16 weight-tile image
 // (W_l^T as [dout x din] K-major core-matrix tiles at 128-byte aligned per-layer offsets, the

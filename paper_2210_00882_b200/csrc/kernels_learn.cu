@@ -36,9 +36,12 @@ namespace {
 
 constexpr int kRows = 128;
 constexpr int kMaxW = 64;
-constexpr int kGroups = 3;  // tiles in flight per CTA (one epilogue group of 4 warps each)
-constexpr int kEpiWarps = 4 * kGroups;
-constexpr int kThreads = 32 * (kEpiWarps + 2);  // + producer + loader (learn-reuse mode)
+// tiles in flight per CTA (one epilogue group of 4 warps each): 3 in the learn modes (TMEM /
+// shared memory hold their dZ slots and dW accumulators), 4 in the values pass (forward only)
+__host__ __device__ constexpr int groups_for(int mode) { return mode == 0 ? 4 : 3; }
+constexpr int kGroupsMax = 4;
+constexpr int kGroups = groups_for(1);
+__host__ __device__ constexpr int threads_for(int mode) { return 32 * (4 * groups_for(mode) + 2); }  // + producer + loader
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
 constexpr int kXPre = 32;                      // input columns prefetched in registers
 #ifndef FLW_TANH_MUFU_PAIRS
@@ -48,14 +51,14 @@ constexpr int kMufuPairs = FLW_TANH_MUFU_PAIRS;  // of each 8-column chunk's 4 p
 
 struct Carve {
     uint32_t wt[kMaxLayers], wbytes;
-    uint32_t ring[kGroups][2], dz[kGroups];  // ring slot 1 also holds the input tile X
+    uint32_t ring[kGroupsMax][2], dz[kGroupsMax];  // ring slot 1 also holds the input tile X
     uint32_t bias, dbacc, loss, total;
     uint32_t hoff[kMaxLayers + 1], hbytes;  // saved tile images: hoff[k + 1] = H_k, hoff[0] = X
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ inline Carve carve_learn(const FastNet& n) {
+__host__ __device__ inline Carve carve_learn(const FastNet& n, int groups, bool learn) {
     Carve c{};
     uint32_t off = 0;
     for (int l = 0; l < n.L; ++l) {  // identical to the weight image built by k_build_wimg
@@ -64,20 +67,22 @@ __host__ __device__ inline Carve carve_learn(const FastNet& n) {
     }
     c.wbytes = off;
     off = align_up(off, 1024);
-    for (int g = 0; g < kGroups; ++g) {
+    for (int g = 0; g < groups; ++g) {
         for (int s = 0; s < 2; ++s) {
             c.ring[g][s] = off;
             off += kSlot;
         }
-        c.dz[g] = off;
-        off += kSlot;
+        if (learn) {
+            c.dz[g] = off;
+            off += kSlot;
+        }
     }
     c.bias = off;
     off += kMaxLayers * kMaxW * 4;
     c.dbacc = off;
-    off += kEpiWarps * kMaxLayers * kMaxW * 4;
+    if (learn) off += 4 * groups * kMaxLayers * kMaxW * 4;
     c.loss = off;
-    off += kEpiWarps * 3 * 4;
+    off += 4 * groups * 3 * 4;
     c.total = off + 2048;  // slack: M=64 MN-major reads of narrow tiles run past their end
     uint32_t h = static_cast<uint32_t>(kRows * n.din[0] * 2);  // X first
     c.hoff[0] = 0;
@@ -166,7 +171,10 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
 // Compile-time modes keep each instantiation's code small (the stage loops are instruction-
 // cache sensitive) and branch-free per activation chunk.
 template <int MODE, int ACT>
-__global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
+__global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a) {
+    constexpr int kGroups = groups_for(MODE);
+    constexpr int kEpiWarps = 4 * kGroups;
+    constexpr int kThreads = threads_for(MODE);
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar;
     __shared__ uint32_t tslot;
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     int np_ev = 0, ne_ev = 0, nf_ev = 0;
 #endif
     const FastNet& n = a.net;
-    if (threadIdx.x == 0) C = carve_learn(n);
+    if (threadIdx.x == 0) C = carve_learn(n, kGroups, MODE != 0);
     __syncthreads();
     const int t = threadIdx.x, w = uni(static_cast<int>(t >> 5)), lane = t & 31;
     const int L = n.L;
@@ -219,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
     }
     for (int l = 0; l < L; ++l)
         for (int o = t; o < kMaxW; o += kThreads) bias[l * kMaxW + o] = o < n.rout[l] ? a.params[n.boff[l] + o] : 0.0f;
-    for (int i = t; i < kEpiWarps * kMaxLayers * kMaxW; i += kThreads) dbacc[i] = 0.0f;
+    if (learn)
+        for (int i = t; i < kEpiWarps * kMaxLayers * kMaxW; i += kThreads) dbacc[i] = 0.0f;
     if (w == 0) umma::tmem_alloc<512>(&tslot);
     umma::fence_before_sync();
     __syncthreads();
@@ -844,18 +853,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_learn(FastLearnArgs a) {
 
 }  // namespace
 
-size_t fast_learn_smem_bytes(const FastNet& n) { return carve_learn(n).total; }
-size_t fast_learn_scratch_bytes(const FastNet& n) { return carve_learn(n).hbytes; }
+size_t fast_learn_smem_bytes(const FastNet& n) { return carve_learn(n, kGroups, true).total; }
+size_t fast_learn_scratch_bytes(const FastNet& n) { return carve_learn(n, kGroups, true).hbytes; }
 int fast_learn_groups() { return kGroups; }
+int fast_values_groups() { return groups_for(0); }
 
 void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid) {
-    const size_t smem = carve_learn(a.net).total;
-    if (smem > 227u * 1024u) throw Error(Errc::Config, "fast numerics: network too wide/deep for one SM's shared memory");
     const int mode = a.mode != 1 ? 0 : (a.hload && a.net.L > 1 ? 2 : 1);
+    const size_t smem = carve_learn(a.net, groups_for(mode), mode != 0).total;
+    if (smem > 227u * 1024u) throw Error(Errc::Config, "fast numerics: network too wide/deep for one SM's shared memory");
     auto go = [&](auto kern) {
         // per-device attribute: set on every launch (cheap, and legal inside stream capture)
         FLW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<grid, kThreads, smem, s>>>(a);
+        kern<<<grid, threads_for(mode), smem, s>>>(a);
     };
     if (a.act == 0) {
         if (mode == 0) go(k_learn<0, 0>);

@@ -26,6 +26,9 @@
 // mma_done[g]; the epilogue waits mma_done[g], reads the accumulator, writes the next operand.
 #include <cuda_runtime.h>
 
+// MODE 0 instantiations end each tile with `continue` before the learn-only stages
+#pragma nv_diag_suppress 128
+
 #include "common.cuh"
 #include "fast.cuh"
 #include "umma.cuh"

@@ -354,7 +354,8 @@ void Engine::alloc() {
         if (L > kMaxLayers) fail(Errc::Config, "fast numerics supports at most 8 layers");
         b.pol = make_net(0);
         if (cfast_) {
-            if (L < 2 || s.cdims[1] > 64) fail(Errc::Config, "compact fast critic needs >= 2 layers, hidden <= 64");
+            if (L < 2 || s.cdims[1] > 64 || s.cdims[1] % 4 != 0)
+                fail(Errc::Config, "compact fast critic needs >= 2 layers, hidden <= 64 and a multiple of 4");
             b.crit = make_net(1, 1);  // the critic without its layer 0
             const int H0 = s.cdims[1];
             b.h0 = b.alloc<float>((T_ + 1) * R_ * H0);

@@ -445,58 +445,77 @@ __global__ void __launch_bounds__(1024) k_gae_scan32(const float* __restrict__ r
 // over [joint(t,e) | onehot(a)] is P[t,e] = joint . W_J (a cuBLAS TF32 GEMM, once per env)
 // plus the row W[J+a]; its gradients come back from the input-gradient stage of k_learn.
 template <int ACT>
-__global__ void k_mappo_h0(const float* __restrict__ P, const float* __restrict__ W0, const float* __restrict__ b0,
-                           int64_t blocks, int64_t E, int n, int J, int H, float* __restrict__ h0) {
-    const int64_t total = blocks * n * E * H;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(i % H);
-        const int64_t row = i / H, blk = row / (n * E), rem = row % (n * E), a = rem / E, e = rem % E;
-        float z = P[(blk * E + e) * H + c] + W0[(J + a) * H + c] + b0[c];
-        if (ACT == 0) z = tanhf(z);
-        if (ACT == 1) z = fmaxf(z, 0.0f);
-        h0[i] = z;
+__global__ void __launch_bounds__(256) k_mappo_h0(const float* __restrict__ P, const float* __restrict__ W0,
+                                                  const float* __restrict__ b0, int64_t blocks, int64_t E, int n, int J,
+                                                  int H, float* __restrict__ h0) {
+    // thread = (row, 4 columns): float4 traffic, 32-bit index math once per row (the row count
+    // blocks * n * E and H are far below 2^31)
+    const uint32_t H4 = static_cast<uint32_t>(H) / 4, nE = static_cast<uint32_t>(n * E), E32 = static_cast<uint32_t>(E);
+    const uint32_t total = static_cast<uint32_t>(blocks) * nE * H4;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t c4 = i % H4, row = i / H4, blk = row / nE, rem = row % nE, a = rem / E32, e = rem % E32;
+        const float4 p = reinterpret_cast<const float4*>(P + (static_cast<int64_t>(blk) * E + e) * H)[c4];
+        // W0 / b0 live inside the flat parameter vector: not 16-byte aligned in general
+        const float* w = W0 + static_cast<int64_t>(J + a) * H + 4 * c4;
+        const float* b = b0 + 4 * c4;
+        float z[4] = {p.x + w[0] + b[0], p.y + w[1] + b[1], p.z + w[2] + b[2], p.w + w[3] + b[3]};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (ACT == 0) asm("tanh.approx.f32 %0, %1;" : "=f"(z[j]) : "f"(z[j]));
+            if (ACT == 1) z[j] = fmaxf(z[j], 0.0f);
+        }
+        reinterpret_cast<float4*>(h0)[i] = make_float4(z[0], z[1], z[2], z[3]);
     }
 }
 
-// S[t,e] = sum_a dz0[t,a,e] (the joint rows' gradient, fixed agent order)
-__global__ void k_mappo_sum_agents(const float* __restrict__ dz0, int64_t T, int64_t E, int n, int H, float* S) {
-    const int64_t total = T * E * H;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(i % H);
-        const int64_t te = i / H, t = te / E, e = te % E;
-        float acc = 0.0f;
-        for (int a = 0; a < n; ++a) acc += dz0[((t * n + a) * E + e) * H + c];
-        S[i] = acc;
+// S[t,e] = sum_a dz0[t,a,e] (the joint rows' gradient, fixed agent order); thread = (t, e, 4 columns)
+__global__ void __launch_bounds__(256) k_mappo_sum_agents(const float* __restrict__ dz0, int64_t T, int64_t E, int n,
+                                                          int H, float* S) {
+    const uint32_t H4 = static_cast<uint32_t>(H) / 4, E32 = static_cast<uint32_t>(E);
+    const uint32_t total = static_cast<uint32_t>(T * E) * H4;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t c4 = i % H4, te = i / H4, t = te / E32, e = te % E32;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int a = 0; a < n; ++a) {
+            const float4 v = reinterpret_cast<const float4*>(dz0 + ((static_cast<int64_t>(t) * n + a) * E + e) * H)[c4];
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        reinterpret_cast<float4*>(S)[i] = acc;
     }
 }
 
 // dW_onehot[a][c] = sum_{t,e} dz0[t,a,e][c], in two fixed-order passes: block (t, a) sums its
-// E rows (8 warps stride e, lane = column, combined in warp order) into part[t][a][c], then the
-// T partials are added in order
+// E rows (16 row phases x 16 float4 column chunks; the phases combined in order) into
+// part[t][a][c], then the T partials are added in order
 __global__ void __launch_bounds__(256) k_mappo_onehot_part(const float* __restrict__ dz0, int64_t E, int n, int H,
                                                            float* part) {
-    __shared__ float ws[8][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ float4 ws[16][16];
+    const int ch = threadIdx.x & 15, ph = threadIdx.x >> 4;
     const int64_t t = blockIdx.x;
     const int a = blockIdx.y;
+    const int H4 = H / 4;
     const float* base = dz0 + ((t * n + a) * E) * H;
-    for (int c0 = 0; c0 < H; c0 += 32) {
-        const int c = c0 + lane;
-        float s = 0.0f;
-        if (c < H) {
-#pragma unroll 8
-            for (int64_t e = w; e < E; e += 8) s += base[e * H + c];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ch < H4) {
+#pragma unroll 4
+        for (int64_t e = ph; e < E; e += 16) {
+            const float4 v = reinterpret_cast<const float4*>(base + e * H)[ch];
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
         }
-        ws[w][lane] = s;
-        __syncthreads();
-        if (w == 0 && c < H) {
-            float tsum = 0.0f;
-            for (int k = 0; k < 8; ++k) tsum += ws[k][lane];
-            part[(t * n + a) * H + c] = tsum;
-        }
-        __syncthreads();
+    }
+    ws[ph][ch] = acc;
+    __syncthreads();
+    if (threadIdx.x < H) {
+        const int c = threadIdx.x;
+        float tsum = 0.0f;
+        for (int k = 0; k < 16; ++k) tsum += reinterpret_cast<const float*>(&ws[k][c >> 2])[c & 3];
+        part[(t * n + a) * H + c] = tsum;
     }
 }
 

@@ -46,7 +46,7 @@ constexpr int kGroupsMax = 4;
 constexpr int kGroups = groups_for(1);
 __host__ __device__ constexpr int threads_for(int mode) { return 32 * (4 * groups_for(mode) + 2); }  // + producer + loader
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
-constexpr int kXPre = 32;                      // input columns prefetched in registers
+constexpr int kXPre = 24;                      // input columns prefetched in registers (12 packed regs)
 #ifndef FLW_TANH_MUFU_PAIRS
 #define FLW_TANH_MUFU_PAIRS 4
 #endif
@@ -522,6 +522,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                     if (c0 < din0)
                         *reinterpret_cast<uint4*>(xs + umma::tile_offset(r, c0, din0)) =
                             make_uint4(xnext[c0 / 2], xnext[c0 / 2 + 1], xnext[c0 / 2 + 2], xnext[c0 / 2 + 3]);
+                for (int c0 = kXPre; c0 < din0; c0 += 8)  // padded input columns: zeros
+                    *reinterpret_cast<uint4*>(xs + umma::tile_offset(r, c0, din0)) = make_uint4(0u, 0u, 0u, 0u);
                 fetch_x(tile + kGroups * G);
             }
             int act_r = 0;

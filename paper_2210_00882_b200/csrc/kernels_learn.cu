@@ -169,6 +169,34 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
     return v[0];
 }
 
+// The same reduce-scatter for a 32-wide slice held as 16 packed bf16 pairs (pair j = columns
+// 2j | 2j+1, low half first): the first level exchanges whole pairs (8 shuffles instead of 16)
+// and the sums, orders and results are those of warp_colsum32 on the unpacked values.
+__device__ __forceinline__ float warp_colsum32_bf16(const uint32_t* pk, int lane) {
+    const bool up = (lane & 16) != 0;
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t keep = up ? pk[j + 8] : pk[j];
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, up ? pk[j] : pk[j + 8], 16);
+        v[2 * j] = __uint_as_float(keep << 16) + __uint_as_float(recv << 16);
+        v[2 * j + 1] = __uint_as_float(keep & 0xFFFF0000u) + __uint_as_float(recv & 0xFFFF0000u);
+    }
+#pragma unroll
+    for (int w = 8, off = 8; off > 0; w >>= 1, off >>= 1) {
+        const bool hi = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (i < w) {
+                const float keep = hi ? v[i + w] : v[i];
+                const float send = hi ? v[i] : v[i + w];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        }
+    }
+    return v[0];
+}
+
 // MODE 0: values pass (critic forward, saves activations); 1: learn (forward + backward);
 // 2: learn reusing the values pass's activations (backward only). ACT 0: tanh, 1: relu.
 // Compile-time modes keep each instantiation's code small (the stage loops are instruction-
@@ -708,6 +736,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 uint8_t* dst = smem + C.dz[g];
                 auto half = [&]<bool FULL, int h0>() {
                     float gv[32];
+                    uint32_t pkc[16];  // the bf16 dZ pairs of these 32 columns (what dW and db see)
                     umma::tmem_ld16(zt + h0, gv);
                     if (FULL || h0 + 16 < di) umma::tmem_ld16(zt + h0 + 16, gv + 16);
                     umma::tmem_ld_wait();
@@ -729,19 +758,17 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                                     d = make_float2(yy.x > 0.0f ? gg.x : 0.0f, yy.y > 0.0f ? gg.y : 0.0f);
                                 }
                                 pk[i] = umma::pack_bf16x2(d.x, d.y);
-                                // db sums exactly the bf16 operand dW sees
-                                gv[c + 2 * i] = __uint_as_float(pk[i] << 16);
-                                gv[c + 2 * i + 1] = __uint_as_float(pk[i] & 0xFFFF0000u);
+                                pkc[c / 2 + i] = pk[i];  // db sums exactly the bf16 operand dW sees
                             }
                             *reinterpret_cast<uint4*>(dst + umma::tile_offset(r, h0 + c, di)) =
                                 make_uint4(pk[0], pk[1], pk[2], pk[3]);
                         } else {
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) gv[c + i] = 0.0f;
+                            for (int i = 0; i < 4; ++i) pkc[c / 2 + i] = 0u;
                         }
                     }
                     if (h0 + 32 >= di) signal();  // dZ_{m-1} complete: hand it to the producer
-                    mydb[(m - 1) * kMaxW + h0 + lane] += warp_colsum32(gv, lane);
+                    mydb[(m - 1) * kMaxW + h0 + lane] += warp_colsum32_bf16(pkc, lane);
                 };
                 if (di == kMaxW) {
                     half.template operator()<true, 0>();

@@ -169,6 +169,28 @@ __device__ __forceinline__ float warp_colsum32(float* v, int lane) {
     return v[0];
 }
 
+// Column sums of an (at most) 8-wide row slice: three reduce-scatter levels (4 + 2 + 1
+// shuffles) leave column (lane >> 2) & 7 summed over 8 lanes, two all-reduce levels finish it;
+// every lane of the quad (lane >> 2) holds that column's sum.
+__device__ __forceinline__ float warp_colsum8(float* v, int lane) {
+#pragma unroll
+    for (int w = 4, off = 16; off >= 4; w >>= 1, off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (i < w) {
+                const float keep = up ? v[i + w] : v[i];
+                const float send = up ? v[i] : v[i + w];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        }
+    }
+    float s = v[0];
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    return s;
+}
+
 // The same reduce-scatter for a 32-wide slice held as 16 packed bf16 pairs (pair j = columns
 // 2j | 2j+1, low half first): the first level exchanges whole pairs (8 shuffles instead of 16)
 // and the sums, orders and results are those of warp_colsum32 on the unpacked values.
@@ -517,8 +539,13 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
 #pragma unroll
             for (int c = 0; c < 32; ++c)
                 if (c0 + c >= width) v[c] = 0.0f;
-            const float sum = warp_colsum32(v, lane);
-            mydb[layer * kMaxW + c0 + lane] += sum;
+            if (width - c0 <= 8) {  // the output layer (A or 1 columns)
+                const float sum = warp_colsum8(v, lane);
+                if ((lane & 3) == 0) mydb[layer * kMaxW + c0 + (lane >> 2)] += sum;
+            } else {
+                const float sum = warp_colsum32(v, lane);
+                mydb[layer * kMaxW + c0 + lane] += sum;
+            }
         };
         bool first = true;
         uint8_t* const xs = smem + C.ring[g][1];  // the input tile X lives in ring slot 1

@@ -201,19 +201,33 @@ __device__ __forceinline__ float warp_colsum32_bf16(const uint32_t* pk, int lane
     for (int j = 0; j < 8; ++j) {
         const uint32_t keep = up ? pk[j + 8] : pk[j];
         const uint32_t recv = __shfl_xor_sync(0xffffffffu, up ? pk[j] : pk[j + 8], 16);
-        v[2 * j] = __uint_as_float(keep << 16) + __uint_as_float(recv << 16);
-        v[2 * j + 1] = __uint_as_float(keep & 0xFFFF0000u) + __uint_as_float(recv & 0xFFFF0000u);
+        const float2 s2 = __fadd2_rn(make_float2(__uint_as_float(keep << 16), __uint_as_float(keep & 0xFFFF0000u)),
+                                     make_float2(__uint_as_float(recv << 16), __uint_as_float(recv & 0xFFFF0000u)));
+        v[2 * j] = s2.x;
+        v[2 * j + 1] = s2.y;
     }
 #pragma unroll
     for (int w = 8, off = 8; off > 0; w >>= 1, off >>= 1) {
         const bool hi = (lane & off) != 0;
+        float k[8], rv[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             if (i < w) {
-                const float keep = hi ? v[i + w] : v[i];
-                const float send = hi ? v[i] : v[i + w];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                k[i] = hi ? v[i + w] : v[i];
+                rv[i] = __shfl_xor_sync(0xffffffffu, hi ? v[i] : v[i + w], off);
             }
+        }
+        if (w >= 2) {  // the level's adds as packed f32x2 adds (same per-element rounding)
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+                if (i < w) {
+                    const float2 s2 = __fadd2_rn(make_float2(k[i], k[i + 1]), make_float2(rv[i], rv[i + 1]));
+                    v[i] = s2.x;
+                    v[i + 1] = s2.y;
+                }
+            }
+        } else {
+            v[0] = k[0] + rv[0];
         }
     }
     return v[0];
@@ -618,8 +632,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                                     uint32_t p[4];
 #pragma unroll
                                     for (int i = 0; i < 4; ++i) {
-                                        const float z0 = z[c + 2 * i] + bb[2 * i];
-                                        const float z1 = z[c + 2 * i + 1] + bb[2 * i + 1];
+                                        // bias add as one packed f32x2 add (same rounding as two)
+                                        const float2 zz = __fadd2_rn(make_float2(z[c + 2 * i], z[c + 2 * i + 1]),
+                                                                     make_float2(bb[2 * i], bb[2 * i + 1]));
+                                        const float z0 = zz.x, z1 = zz.y;
                                         if constexpr (ACT != 0) {
                                             p[i] = umma::pack_bf16x2(fmaxf(z0, 0.0f), fmaxf(z1, 0.0f));
                                         } else if (i < kMufuPairs) {

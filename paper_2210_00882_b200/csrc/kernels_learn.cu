@@ -44,7 +44,8 @@ constexpr int kMaxW = 64;
 __host__ __device__ constexpr int groups_for(int mode) { return mode == 0 ? 4 : 3; }
 constexpr int kGroupsMax = 4;
 constexpr int kGroups = groups_for(1);
-__host__ __device__ constexpr int threads_for(int mode) { return 32 * (4 * groups_for(mode) + 2); }  // + producer + loader
+// + two MMA producers (groups split by parity) + loader
+__host__ __device__ constexpr int threads_for(int mode) { return 32 * (4 * groups_for(mode) + 3); }
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
 constexpr int kXPre = 24;                      // input columns prefetched in registers (12 packed regs)
 #ifndef FLW_TANH_MUFU_PAIRS
@@ -243,8 +244,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
     constexpr int kEpiWarps = 4 * kGroups;
     constexpr int kThreads = threads_for(MODE);
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar;
+    __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar, zbar;
     __shared__ uint32_t tslot;
+    __shared__ uint32_t dwtok[kMaxLayers];  // dW_l MMAs issued so far, in (tile round, group) order
     __shared__ uint32_t epi_cnt[kGroups];  // epilogue hand-offs per group (4 per stage), for the loader
     __shared__ uint32_t rd_cnt[kGroups];   // loader: bulk stores whose smem read completed (producer)
     __shared__ uint32_t xf_cnt[kGroups];   // loader, values pass: last saved tile read (epilogue)
@@ -289,13 +291,20 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
 
         }
         umma::mbar_init(&wbar, 1);
+        umma::mbar_init(&zbar, 1);
         for (int g = 0; g < kGroups; ++g) epi_cnt[g] = rd_cnt[g] = xf_cnt[g] = 0;
+        for (int l = 0; l < kMaxLayers; ++l) dwtok[l] = 0;
         umma::fence_barrier_init();
     }
     for (int l = 0; l < L; ++l)
         for (int o = t; o < kMaxW; o += kThreads) bias[l * kMaxW + o] = o < n.rout[l] ? a.params[n.boff[l] + o] : 0.0f;
     if (learn)
         for (int i = t; i < kEpiWarps * kMaxLayers * kMaxW; i += kThreads) dbacc[i] = 0.0f;
+    if (learn) {  // dz slot of group 0 zeroed: the operand of the dW accumulators' zero-init MMAs
+        for (uint32_t i = t; i < kSlot / 16; i += kThreads)
+            reinterpret_cast<uint4*>(smem + C.dz[0])[i] = make_uint4(0u, 0u, 0u, 0u);
+        umma::fence_async_smem();
+    }
     if (w == 0) umma::tmem_alloc<512>(&tslot);
     umma::fence_before_sync();
     __syncthreads();
@@ -303,17 +312,21 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
     const uint32_t tmem = uni(tslot);
     const uint32_t sbase = umma::smem_u32(smem);
 
-    if (w == kEpiWarps) {
+    if (w == kEpiWarps || w == kEpiWarps + 2) {
         // ================================================================ producer (whole warp)
         // The warp runs the issue loop converged (warp-uniform control flow and operands); one
         // elected lane issues each tcgen05.mma / commit / bulk copy (umma::mma_bf16_warp).
         {
-            if (umma::elect_one()) bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
+            // two producer warps: groups of parity `pidx` each; the dW accumulators are shared,
+            // so producer 0 zeroes them with one accumulate=0 MMA per layer on a zero operand
+            // before either producer issues a stage, and every dW MMA accumulates
+            const int pidx = w == kEpiWarps ? 0 : 1;
+            if (pidx == 0 && umma::elect_one()) bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
             __syncwarp();
             umma::mbar_wait(&wbar, 0);
             uint32_t ph_epi[kGroups] = {}, ph_ld[kGroups][2] = {}, need_rd[kGroups] = {};
             bool dw_init[kMaxLayers];
-            for (int l = 0; l < kMaxLayers; ++l) dw_init[l] = false;
+            for (int l = 0; l < kMaxLayers; ++l) dw_init[l] = true;
             auto dw_tmem = [&](int l) {
                 return tmem + 64u * kGroups + 64u * static_cast<uint32_t>(l >> 1) + ((l & 1) ? (16u << 16) : 0u);
             };
@@ -331,6 +344,18 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 }
                 dw_init[l] = true;
             };
+            if (learn) {
+                if (pidx == 0) {
+                    const uint32_t zs = uni(sbase + C.dz[0]);
+                    for (int l = 0; l < L; ++l)
+                        umma::mma_bf16_warp(dw_tmem(l), umma::desc_mnmajor(zs, n.din[l], 0),
+                                            umma::desc_mnmajor(zs, n.dout[l], 0),
+                                            umma::idesc_bf16(64, n.dout[l], true, true), false);
+                    umma::commit_warp(&zbar);
+                }
+                umma::mbar_wait(&zbar, 0);
+                umma::fence_after_sync();
+            }
             for (int64_t it = 0;; ++it) {
                 int64_t tl[kGroups];
                 bool has[kGroups], any = false;
@@ -341,7 +366,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 }
                 if (!any) break;
                 for (int j = 0; j < njobs; ++j) {
-                    for (int g = 0; g < kGroups; ++g) {
+                    for (int g = pidx; g < kGroups; g += 2) {
                         if (!has[g]) continue;
                         umma::mbar_wait(&epi_done[g], ph_epi[g]);
                         ph_epi[g] ^= 1;
@@ -393,7 +418,16 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                                     umma::mma_bf16_warp(zt, umma::desc_kmajor(dzt, dout, kb),
                                                         umma::desc_mnmajor(wm, di, kb), id, kb > 0);
                             }
+                            // the shared dW_m accumulator takes its MMAs in the single-issuer order
+                            // ((tile round, group) ascending), so the sums stay deterministic
+                            const uint32_t want = static_cast<uint32_t>(it * kGroups + g);
+                            while (cnt_acquire(&dwtok[m]) != want) {
+                            }
+                            umma::fence_after_sync();
                             issue_dw(g, m, uni(sbase + C.ring[g][sh]));
+                            umma::fence_before_sync();
+                            __syncwarp();
+                            if (lane == 0) cnt_add_release(&dwtok[m]);
                             umma::commit_warp(&mma_done[g]);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
@@ -498,6 +532,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
         }
     } else {
         // ================================================================ epilogue groups
+        // the dW zero-init MMAs read group 0's dz slot: no dZ store before they completed
+        // (learn-reuse writes dZ_{L-1} before any MMA of its own)
+        if (learn) umma::mbar_wait(&zbar, 0);
         const int g = w >> 2, q = w & 3;
         const int r = 32 * q + lane;  // tile row == TMEM lane
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;

@@ -10,6 +10,9 @@
 //   warp  8    producer: lane 0 issues every tcgen05.mma / commit and every TMA bulk copy, in a
 //              FIXED alternating order (group 0 job j, group 1 job j, ...), so the dW
 //              accumulation order - and therefore the result - is deterministic.
+//   (current layout: 4 epilogue warps per group x kGroups, then producer 0 (even groups),
+//    the loader warp, producer 1 (odd groups); the shared dW accumulators take their MMA
+//    batches in the single-producer order through the per-layer dwtok token)
 //
 // Shared memory holds, per group, the input tile, a 2-slot ring for hidden activations and a
 // 2-slot dZ ring; the forward streams every hidden tile H_l out to global scratch (L2-resident,

@@ -101,6 +101,14 @@ int flw_dpd_p2p_export(flw_dpd* e, int nranks, char* out_handle, int64_t cap);
 int flw_dpd_p2p_import(flw_dpd* e, const char* handles, int64_t len, int rank, int nranks);
 /* Back to the NCCL exchange (every rank of the group must make the same choice). */
 int flw_dpd_p2p_disable(flw_dpd* e);
+/* Bounded group waits (the reference's receive timeouts, local_run.cpp:543-546 / fraglow.h:36):
+ * a unit in a gradient group fails its episode / learn call with Timeout (code 3) once it has
+ * waited timeout_ms (<= 0: 30 s) for its peers, and aborts the group (NCCL communicator abort +
+ * the peer-memory exchange's abort word). flw_dpd_abort aborts the group from the caller
+ * (a peer failed); the unit's next waits fail with PeerFailure. Either leaves the unit unusable
+ * for further grouped episodes: destroy it. */
+int flw_dpd_set_timeout(flw_dpd* e, int64_t timeout_ms);
+int flw_dpd_abort(flw_dpd* e);
 
 /* One whole episode (Reset, T x Step, I x Learn) as a replayed CUDA graph. reward_sum is the
  * episode's summed env reward over this unit's envs (interp.cpp:257); device_ms the graph time. */

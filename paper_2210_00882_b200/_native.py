@@ -61,6 +61,8 @@ def lib():
         "flw_dpd_p2p_export": (ci, [vp, ci, C.c_char_p, i64]),
         "flw_dpd_p2p_import": (ci, [vp, C.c_char_p, i64, ci, ci]),
         "flw_dpd_p2p_disable": (ci, [vp]),
+        "flw_dpd_set_timeout": (ci, [vp, i64]),
+        "flw_dpd_abort": (ci, [vp]),
         "flw_dpd_destroy": (ci, [vp]),
         "flw_dpd_comm_unique_id": (ci, [C.c_char_p, i64]),
         "flw_dpd_comm_init": (ci, [vp, C.c_char_p, i64, ci, ci]),

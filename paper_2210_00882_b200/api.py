@@ -122,6 +122,14 @@ class DpdEngine:
         blob = b"".join(handles)
         N.check(N.lib().flw_dpd_p2p_import(self._h, blob, len(blob), rank, len(handles)))
 
+    def set_timeout(self, timeout_ms: int):
+        """Bound on a grouped unit's waits for its peers (0: 30 s); past it the call raises Timeout."""
+        N.check(N.lib().flw_dpd_set_timeout(self._h, timeout_ms))
+
+    def abort(self):
+        """Abort this unit's gradient group (its waits fail with PeerFailure)."""
+        N.check(N.lib().flw_dpd_abort(self._h))
+
     def p2p_disable(self):
         N.check(N.lib().flw_dpd_p2p_disable(self._h))
 

@@ -3,6 +3,7 @@
 // guarded() maps exceptions to codes, thread-local last error, malloc'd out strings.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <barrier>
 #include <chrono>
 #include <cmath>
@@ -208,6 +209,7 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
     } else {
         for (auto& e : p.engines) e->reinit(seed);
     }
+    for (auto& e : p.engines) e->set_timeout_ms(opts ? opts->timeout_ms : 0);  // 0: 30 s (fraglow.h:36)
     eps.assign(static_cast<size_t>(episodes), {});
     // reward sum of every unit and episode, folded in unit order below (local_run.cpp:560-570)
     std::vector<std::vector<double>> rsum(static_cast<size_t>(k), std::vector<double>(episodes, 0.0));
@@ -215,7 +217,8 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
     // Reference byte accounting of the GradSync channel: k(k-1) legs x learn iters x (14 + 8P).
     const int64_t per_ep_bytes = k > 1 ? static_cast<int64_t>(k) * (k - 1) * s.learn_iters * (14 + 8 * s.P) : 0;
     std::mutex err_mu;
-    std::string first_error;
+    std::string first_error;          // guarded by err_mu
+    std::atomic<bool> failed{false};  // lock-free "a unit failed" for the worker fast path
     auto run_one = [&](int g, int64_t ep) {
         p.engines[g]->run_episode(ep);
         const std::vector<double> v = p.engines[g]->replica_reward_sums();
@@ -239,13 +242,14 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
                     gate.arrive_and_wait();  // raise_gate(ep)
                     try {
                         flw_trace(("engine " + std::to_string(g) + " episode " + std::to_string(ep)).c_str());
-                        if (first_error.empty()) run_one(g, ep);
+                        if (!failed.load(std::memory_order_acquire)) run_one(g, ep);
                     } catch (const std::exception& e) {
                         std::lock_guard<std::mutex> lk2(err_mu);
                         if (first_error.empty()) first_error = "unit " + std::to_string(g * R) + ": " + e.what();
-                        // peers may be blocked inside a collective waiting for this unit
-                        for (auto& en : p.engines)
-                            if (en->comm()) en->comm()->abort();
+                        failed.store(true, std::memory_order_release);
+                        // peers may be blocked inside a collective or a peer-memory flag wait
+                        // for this unit: abort the whole group (local_run.cpp:79-86)
+                        for (auto& en : p.engines) en->abort_group();
                     }
                     gate.arrive_and_wait();  // on_episode_done
                 }
@@ -258,7 +262,7 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
             eps[static_cast<size_t>(ep)].wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         }
         for (auto& t : threads) t.join();
-        if (!first_error.empty()) {
+        if (failed.load()) {
             p.engines.clear();  // aborted communicators: rebuild on the next run
             fail(Errc::PeerFailure, first_error);
         }
@@ -428,6 +432,20 @@ int flw_dpd_p2p_import(flw_dpd* e, const char* handles, int64_t len, int rank, i
             regions[static_cast<size_t>(r)] = ptr;
         }
         en.set_p2p_peers(rank, nranks, regions);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_set_timeout(flw_dpd* e, int64_t timeout_ms) {
+    return guarded([&] {
+        eng(e).set_timeout_ms(timeout_ms);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_abort(flw_dpd* e) {
+    return guarded([&] {
+        eng(e).abort_group();
         return FLW_OK;
     });
 }

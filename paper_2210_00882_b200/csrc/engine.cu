@@ -23,6 +23,9 @@
 #include "common.cuh"
 #include "fast.cuh"
 #include "p2p.cuh"
+
+#include <chrono>
+#include <thread>
 #include "kernels.cuh"
 
 namespace flw {
@@ -170,6 +173,11 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     FLW_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreate(&ev_t0_));
     FLW_CUDA(cudaEventCreate(&ev_t1_));
+    // group abort word in host-mapped memory: the host sets it (deadline passed, a peer failed)
+    // and the peer-memory exchange's flag waits give up (kernels_p2p.cu)
+    FLW_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&abort_h_), sizeof(unsigned), cudaHostAllocMapped | cudaHostAllocPortable));
+    *abort_h_ = 0;
+    FLW_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&abort_d_), abort_h_, 0));
     alloc();
     init_params();
 }
@@ -187,6 +195,46 @@ Engine::~Engine() {
     if (side_) cudaStreamDestroy(side_);
     if (side2_) cudaStreamDestroy(side2_);
     if (stream_) cudaStreamDestroy(stream_);
+    if (abort_h_) cudaFreeHost(abort_h_);
+}
+
+void Engine::abort_group() {
+    if (abort_h_) *reinterpret_cast<volatile unsigned*>(abort_h_) = 1u;
+    if (comm_) comm_->abort();
+}
+
+bool Engine::grouped() const { return p2p_enabled() || (comm_ && comm_->nranks() > 1); }
+
+// Waits for the engine stream. A unit in a gradient group can block on its peers (flag waits of
+// the peer-memory exchange, NCCL collectives), so its wait is bounded like the reference's
+// channel receives (local_run.cpp:543-546): past timeout_ms the group is aborted and the call
+// fails with Timeout. A unit without a group cannot block on anything: plain synchronize.
+void Engine::wait_stream(const char* what) {
+    if (!grouped()) {
+        FLW_CUDA(cudaStreamSynchronize(stream_));
+        return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        const cudaError_t st = cudaStreamQuery(stream_);
+        if (st == cudaSuccess) break;
+        if (st != cudaErrorNotReady) FLW_CUDA(st);
+        if (*reinterpret_cast<volatile unsigned*>(abort_h_)) {
+            FLW_CUDA(cudaStreamSynchronize(stream_));  // the exchange gives up on the abort word
+            fail(Errc::PeerFailure, std::string(what) + ": the gradient group was aborted (a peer failed)");
+        }
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > static_cast<double>(timeout_ms_)) {
+            abort_group();
+            FLW_CUDA(cudaStreamSynchronize(stream_));
+            fail(Errc::Timeout, std::string(what) + ": no progress from the gradient group within " +
+                                    std::to_string(timeout_ms_) + " ms (a peer did not reach the exchange)");
+        }
+        if (spin < 2000)
+            std::this_thread::yield();
+        else
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
 }
 
 void Engine::destroy_graph() {
@@ -251,7 +299,7 @@ void Engine::alloc() {
     const int S = s.obs_dim, A = s.n_actions, L = s.L;
     b.ctx = b.alloc<DeviceCtx>(1);
     // Adam bias-correction table 1 - beta^t computed with the host libm pow, the reference's
-    // arithmetic (mlp.cpp:485-486), for every step this run can take (+ slack).
+    // arithmetic (mlp.cpp:151-152), for every step this run can take (+ slack).
     b.bc_len = std::max<int64_t>(4096, (cfg_.episodes + 16) * s.learn_iters);
     {
         std::vector<double2> tab(static_cast<size_t>(b.bc_len));
@@ -963,6 +1011,7 @@ void Engine::enq_grad_sync_and_adam() {
         a.off_sflag = Lo.off_sflag;
         a.off_dflag = Lo.off_dflag;
         a.ctx = b.ctx;
+        a.abort_flag = abort_d_;
         a.params = b.params;
         a.m = b.m;
         a.v = b.v;
@@ -1087,7 +1136,7 @@ void Engine::learn(int64_t ep, int64_t k) {
     fuse_ok_ = false;
     if (numerics_ == Numerics::Exact) exact_loss_reduce(stream_, b_->terms, TR_, cfg_.entropy_coef, b_->loss);
     enq_grad_sync_and_adam();
-    FLW_CUDA(cudaStreamSynchronize(stream_));
+    wait_stream("learn");
 }
 
 // ------------------------------------------------------------------------ episode graph
@@ -1220,7 +1269,7 @@ double Engine::run_episode(int64_t ep, float* device_ms) {
     launch_graph();
     FLW_CUDA(cudaEventRecord(ev_t1_, stream_));
     flw_trace("run_episode: launched");
-    FLW_CUDA(cudaStreamSynchronize(stream_));
+    wait_stream("run_episode");
     flw_trace("run_episode: synced");
     steps_ += T_ * nrep_;
     cur_step_ = T_;
@@ -1278,6 +1327,7 @@ int64_t Engine::tensor_size(const std::string& n) const {
     if (n == "loss") return 1;
     if (n == "grads") return shape_.P;
     if (n == "env_state") return E_ * shape_.env_state_w;
+    if (n == "env_full") return E_ * (shape_.env_state_w + 2);  // [env state | done | step count]
     return -1;
 }
 
@@ -1415,11 +1465,18 @@ void Engine::read_tensor(const std::string& n, double* out) {
         }
         return;
     }
-    if (n == "env_state") {
-        auto est = d2h(b.est, E_ * shape_.env_state_w);
-        for (int64_t e = 0; e < E_; ++e)
-            for (int64_t j = 0; j < shape_.env_state_w; ++j)
-                out[e * shape_.env_state_w + j] = est[static_cast<size_t>(j * E_ + e)];
+    if (n == "env_state" || n == "env_full") {
+        const int64_t sw = shape_.env_state_w, w = n == "env_full" ? sw + 2 : sw;
+        auto est = d2h(b.est, E_ * sw);
+        auto dn = d2h(b.done, E_);
+        auto sc = d2h(b.stepc, E_);
+        for (int64_t e = 0; e < E_; ++e) {
+            for (int64_t j = 0; j < sw; ++j) out[e * w + j] = est[static_cast<size_t>(j * E_ + e)];
+            if (w > sw) {
+                out[e * w + sw] = dn[static_cast<size_t>(e)];
+                out[e * w + sw + 1] = sc[static_cast<size_t>(e)];
+            }
+        }
         return;
     }
     fail(Errc::Config, "unknown tensor '" + n + "'");
@@ -1438,6 +1495,21 @@ void Engine::write_tensor(const std::string& n, const double* in, int64_t cnt) {
         return v;
     };
     if (n == "state_in") return h2d(b.states + cur_step_ * E_ * S, f(0, E_ * S));
+    if (n == "env_full") {  // teacher forcing of the env state (SoA on the device)
+        const int64_t sw = shape_.env_state_w, w = sw + 2;
+        std::vector<double> est(static_cast<size_t>(E_ * sw));
+        std::vector<uint8_t> dn(static_cast<size_t>(E_));
+        std::vector<int32_t> sc(static_cast<size_t>(E_));
+        for (int64_t e = 0; e < E_; ++e) {
+            for (int64_t j = 0; j < sw; ++j) est[static_cast<size_t>(j * E_ + e)] = in[e * w + j];
+            dn[static_cast<size_t>(e)] = static_cast<uint8_t>(in[e * w + sw] != 0.0);
+            sc[static_cast<size_t>(e)] = static_cast<int32_t>(in[e * w + sw + 1]);
+        }
+        h2d(b.est, est);
+        h2d(b.done, dn);
+        h2d(b.stepc, sc);
+        return;
+    }
     if (n == "sample") {  // teacher forcing of the learn batch
         const int64_t W = 2 * S + 4;
         std::vector<float> st(static_cast<size_t>((T_ + 1) * E_ * S)), rw(TR_), dn(TR_), lp(TR_);

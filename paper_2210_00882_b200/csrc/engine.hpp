@@ -63,6 +63,13 @@ class Engine {
         p2p_k_ = 0;
     }
     void set_eager_collectives(bool on);
+    // Bounded waits (reference: channel receive timeouts, local_run.cpp:543-546): a grouped
+    // unit's episode / learn call fails with Timeout after timeout_ms and aborts its group.
+    void set_timeout_ms(int64_t ms) { timeout_ms_ = ms > 0 ? ms : 30000; }
+    int64_t timeout_ms() const { return timeout_ms_; }
+    // Sets the group abort word (peer-memory flag waits give up) and aborts the NCCL group.
+    void abort_group();
+    bool grouped() const;
     void prepare();  // captures the episode graph now (before any peer launches its own)
 
     // Phase-level API (each enqueues on the engine stream and synchronises before returning).
@@ -126,6 +133,10 @@ class Engine {
     void enq_reward_sum();
     void enq_mlp_forward(int net, const float* X, int64_t M, float* const* H, int first_layer = 0);
     void build_graph();
+    void wait_stream(const char* what);
+    unsigned* abort_h_ = nullptr;  // host-mapped group abort word (host view)
+    unsigned* abort_d_ = nullptr;  // ... device view
+    int64_t timeout_ms_ = 30000;
 
     AlgoConfig cfg_;
     ProgramShape shape_;

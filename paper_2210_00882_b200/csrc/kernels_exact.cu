@@ -443,7 +443,7 @@ __global__ void k_adam_tick(DeviceCtx* ctx, const double2* __restrict__ table, i
     }
 }
 
-// adam_step (mlp.cpp:480-495): double moments, f32 params.
+// adam_step (mlp.cpp:146-161): double moments, f32 params.
 __global__ void k_adam(const DeviceCtx* __restrict__ ctx, float* params, const float* __restrict__ g32,
                        const double* __restrict__ g64, double* m, double* v, int64_t P, double lr, double b1,
                        double b2, double eps, double gscale) {

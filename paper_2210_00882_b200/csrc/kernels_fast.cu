@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
 
 // One train iteration's parameter update fused into a single launch (1 GPU, no exchange): the
 // fixed-order reduction of the per-CTA dW partials (as k_reduce_partials), Adam with double
-// moments (mlp.cpp:480-495, as k_adam) and the bf16 weight-image entry of every weight (as
+// moments (mlp.cpp:146-161, as k_adam) and the bf16 weight-image entry of every weight (as
 // k_build_wimg), so the next train iteration's learn kernels read the updated image without a
 // build launch. The Adam step counter and its bias corrections (as k_adam_tick) are advanced by
 // the last block to finish (every block has read the old counter by then).

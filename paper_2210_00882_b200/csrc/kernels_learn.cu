@@ -981,6 +981,7 @@ void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid) {
         // per-device attribute: set on every launch (cheap, and legal inside stream capture)
         FLW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<grid, threads_for(mode), smem, s>>>(a);
+        FLW_CUDA(cudaGetLastError());
     };
     if (a.act == 0) {
         if (mode == 0) go(k_learn<0, 0>);

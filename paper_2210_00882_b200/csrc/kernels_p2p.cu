@@ -98,18 +98,27 @@ __global__ void __launch_bounds__(256) k_reduce_push(P2pArgs a) {
 }
 
 // B: wait for the k ranks' copies of the chunk, sum them in rank order (every rank computes
-// the identical mean) and apply Adam (adam_step, mlp.cpp:480-495; 1/k folded into the step).
+// the identical mean) and apply Adam (adam_step, mlp.cpp:146-161; 1/k folded into the step).
 // Waits only on A kernels, which never wait: no residency requirement.
 __global__ void __launch_bounds__(128) k_sum_adam(P2pArgs a) {
     const int c = blockIdx.x;
     const uint64_t epoch = a.ctx->coll_seq;
     const int64_t P = a.Pp + a.Pc;
     const uint64_t* flag = reinterpret_cast<const uint64_t*>(a.peers[a.rank] + a.off_sflag) + static_cast<int64_t>(c) * a.k;
+    __shared__ int gave_up;
+    if (threadIdx.x == 0) gave_up = 0;
+    __syncthreads();
     for (int r = threadIdx.x; r < a.k; r += blockDim.x)
-        while (ld_acquire_sys(flag + r) < epoch) __nanosleep(32);
+        while (ld_acquire_sys(flag + r) < epoch) {
+            if (*a.abort_flag) {  // the host aborted the group: leave the state untouched
+                gave_up = 1;
+                break;
+            }
+            __nanosleep(64);
+        }
     __syncthreads();
     const int64_t i = pad_to_flat(a, 128LL * c + threadIdx.x);
-    if (i < 0) return;
+    if (i < 0 || gave_up) return;
     const float* inbox =
         reinterpret_cast<const float*>(a.peers[a.rank] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
     float gs = 0.0f;

@@ -26,6 +26,9 @@ struct P2pArgs {
     uint8_t* const* peers;  // device array [k]: every rank's exchange region, mapped here
     int64_t off_inbox, off_grads, off_sflag, off_dflag;
     const DeviceCtx* ctx;   // coll_seq (epoch), Adam bias corrections
+    // host-mapped abort word: nonzero makes every flag wait give up (a peer failed or the host's
+    // deadline passed); the update is then skipped and the host reports Timeout / PeerFailure
+    const volatile unsigned* abort_flag;
     float* params;
     double *m, *v;
     double lr, b1, b2, eps, gscale;

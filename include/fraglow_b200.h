@@ -152,6 +152,13 @@ int flw_dpd_probe_times(flw_dpd* e, char** json);
  * b_mn=0: B is stored [N,K]; b_mn=1: B is [K,N]. lane_off = TMEM lane offset of D (M=64 only). */
 int flw_selftest_umma(int M, int N, int K, int a_mn, int b_mn, int lane_off, const float* A, const float* B, float* D);
 
+/* Diagnostic (tests only): D[M,N] = op(A) op(B) through the generic TMA + tcgen05 GEMM of the
+ * layer-wise learn path (kernels_tgemm.cu), K split `splits` ways (partials summed on the host).
+ * a_mn: A given as [K,M] (else [M,K]); b_mn: B given as [K,N] (else [N,K]); tf32: kind::tf32 on
+ * the f32 values, else kind::f16 on their bf16 roundings; bn: N tile (64, 128 or 256). */
+int flw_selftest_tgemm(int64_t M, int64_t N, int64_t K, int a_mn, int b_mn, int tf32, int splits, int bn,
+                       const float* A, const float* B, float* D);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,458 @@
+// Generic warp-specialised tcgen05 GEMM (interface and operand conventions: tgemm.cuh).
+//
+// One CTA per SM, persistent over work items (128-row tile, BN-column tile, K split):
+//   warp 0      TMA producer: one elected lane streams the A / B k-blocks (128-byte rows,
+//               SWIZZLE_128B) into an S-stage shared-memory ring (full / empty mbarriers)
+//   warp 1      MMA issuer: per k-block BK/UK tcgen05.mma (M=128, N=BN) into one of two TMEM
+//               accumulators (double-buffered, so the epilogue of item i overlaps item i+1's
+//               MMAs); tcgen05.commit releases the ring slot / hands the accumulator over
+//   warps 2-5   epilogue: one accumulator row per thread (TMEM lane quarter = warp % 4),
+//               tcgen05.ld in 32-column chunks, fused bias / activation / act' / stores
+//
+// Shared-memory operand layouts are the canonical UMMA SWIZZLE_128B ones the TMA unit writes
+// (cute/atom/mma_traits_sm100.hpp make_umma_desc):
+//   K-major : 8-row x 128-byte atoms, atoms along M/N at SBO = 1024 B; the k-th UK-slice of a
+//             k-block starts 32 B further (the swizzle is applied on the absolute address bits,
+//             so the tiles are 1024-byte aligned)
+//   MN-major: 64 bf16 / 32 f32 MN-contiguous elements x 8 K-rows per atom; K-row groups at
+//             SBO = 1024 B, MN atoms at LBO = one TMA box (BK rows x 128 B)
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "tgemm.cuh"
+#include "umma.cuh"
+
+namespace flw {
+
+namespace {
+
+struct TgArgs {
+    int64_t M, N;
+    int kblocks, mtiles, ntiles, splits;
+    TgEpilogue epi;
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(umma::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(umma::smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// SWIZZLE_128B shared-memory descriptor (layout type 2 at bits [61,64), version 1).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
+// kind::f16 (bf16) / kind::tf32 instruction descriptor, f32 accumulate, M = 128.
+__host__ __device__ constexpr uint32_t idesc_tg(int N, bool tf32, bool a_mn, bool b_mn) {
+    const uint32_t fmt = tf32 ? 2u : 1u;
+    return (1u << 4) | (fmt << 7) | (fmt << 10) | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u) |
+           (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+}
+
+template <bool TF32>
+__device__ __forceinline__ void mma_tg(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, bool acc) {
+    if constexpr (TF32) {
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc ? 1u : 0u));
+    } else {
+        umma::mma_bf16_warp(tmem_d, adesc, bdesc, idesc, acc);
+    }
+}
+
+__device__ __forceinline__ float act_fwd(float z, int act) { return act == 0 ? tanhf(z) : fmaxf(z, 0.0f); }
+
+constexpr int kTgThreads = 192;
+
+template <int BN>
+__host__ __device__ constexpr int tg_stages() {
+    return BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+}
+template <int BN>
+__host__ __device__ constexpr uint32_t tg_stage_bytes() {
+    return 128u * 128u + static_cast<uint32_t>(BN) * 128u;
+}
+
+template <int BN, bool TF32, bool AMN, bool BMN>
+__global__ void __launch_bounds__(kTgThreads, 1)
+    k_tgemm(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, const TgArgs a) {
+    constexpr int S = tg_stages<BN>();
+    constexpr uint32_t kStage = tg_stage_bytes<BN>();
+    constexpr uint32_t kABytes = 128u * 128u;
+    constexpr int esz = TF32 ? 4 : 2;
+    constexpr int BK = 128 / esz;  // K elements per k-block (one 128-byte row)
+    constexpr int UK = 32 / esz;   // K elements per MMA
+    constexpr int kAtom = 128 / esz;
+    constexpr uint32_t kCols = 2 * BN;  // two accumulators
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[S], empty[S], tfull[2], tempty[2];
+    __shared__ uint32_t tslot;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t items = static_cast<int64_t>(a.mtiles) * a.ntiles * a.splits;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            umma::mbar_init(&full[i], 1);
+            umma::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            umma::mbar_init(&tfull[i], 1);
+            umma::mbar_init(&tempty[i], 4);
+        }
+        umma::fence_barrier_init();
+        prefetch_map(&ma);
+        prefetch_map(&mb);
+    }
+    if (w == 1) umma::tmem_alloc<kCols>(&tslot);
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = tslot;
+
+    auto decode = [&](int64_t wi, int& mt, int& nt, int& kb0, int& kb1) {
+        const int s = static_cast<int>(wi % a.splits);
+        const int64_t r = wi / a.splits;
+        nt = static_cast<int>(r % a.ntiles);
+        mt = static_cast<int>(r / a.ntiles);
+        kb0 = static_cast<int>((static_cast<int64_t>(s) * a.kblocks) / a.splits);
+        kb1 = static_cast<int>((static_cast<int64_t>(s + 1) * a.kblocks) / a.splits);
+        return s;
+    };
+
+    if (w == 0) {
+        // ------------------------------------------------------------------ TMA producer
+        if (umma::elect_one()) {
+            int stage = 0;
+            uint32_t ph = 0;
+            for (int64_t wi = blockIdx.x; wi < items; wi += gridDim.x) {
+                int mt, nt, kb0, kb1;
+                decode(wi, mt, nt, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    umma::mbar_wait(&empty[stage], ph ^ 1);
+                    uint8_t* sa = smem + stage * kStage;
+                    uint8_t* sb = sa + kABytes;
+                    umma::mbar_expect_tx(&full[stage], kStage);
+                    if constexpr (!AMN) {
+                        tma_load_2d(sa, &ma, kb * BK, mt * 128, &full[stage]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 128 / kAtom; ++j)
+                            tma_load_2d(sa + j * (BK * 128), &ma, mt * 128 + j * kAtom, kb * BK, &full[stage]);
+                    }
+                    if constexpr (!BMN) {
+                        tma_load_2d(sb, &mb, kb * BK, nt * BN, &full[stage]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BN / kAtom; ++j)
+                            tma_load_2d(sb + j * (BK * 128), &mb, nt * BN + j * kAtom, kb * BK, &full[stage]);
+                    }
+                    if (++stage == S) {
+                        stage = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (w == 1) {
+        // ------------------------------------------------------------------ MMA issuer
+        constexpr uint32_t idesc = idesc_tg(BN, TF32, AMN, BMN);
+        int stage = 0;
+        uint32_t ph = 0, tph[2] = {0, 0};
+        int acc = 0;
+        const uint32_t sbase = umma::smem_u32(smem);
+        for (int64_t wi = blockIdx.x; wi < items; wi += gridDim.x) {
+            int mt, nt, kb0, kb1;
+            decode(wi, mt, nt, kb0, kb1);
+            umma::mbar_wait(&tempty[acc], tph[acc] ^ 1);
+            tph[acc] ^= 1;
+            umma::fence_after_sync();
+            const uint32_t dt = tmem + static_cast<uint32_t>(acc * BN);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                umma::mbar_wait(&full[stage], ph);
+                umma::fence_after_sync();
+                const uint32_t sa = sbase + stage * kStage, sb = sa + kABytes;
+#pragma unroll
+                for (int k = 0; k < BK / UK; ++k) {
+                    const uint64_t ad = AMN ? desc_sw128(sa + k * (UK * 128), BK * 128, 1024)
+                                            : desc_sw128(sa + k * 32, 16, 1024);
+                    const uint64_t bd = BMN ? desc_sw128(sb + k * (UK * 128), BK * 128, 1024)
+                                            : desc_sw128(sb + k * 32, 16, 1024);
+                    mma_tg<TF32>(dt, ad, bd, idesc, kb > kb0 || k > 0);
+                }
+                umma::commit_warp(&empty[stage]);  // the slot is free once these MMAs read it
+                if (++stage == S) {
+                    stage = 0;
+                    ph ^= 1;
+                }
+            }
+            umma::commit_warp(&tfull[acc]);
+            acc ^= 1;
+        }
+    } else {
+        // ------------------------------------------------------------------ epilogue
+        const int q = w & 3;
+        const TgEpilogue& e = a.epi;
+        const int64_t m_store = e.m_store >= 0 ? e.m_store : a.M;
+        const int64_t n_store = e.n_store >= 0 ? e.n_store : a.N;
+        uint32_t tph[2] = {0, 0};
+        int acc = 0;
+        for (int64_t wi = blockIdx.x; wi < items; wi += gridDim.x) {
+            int mt, nt, kb0, kb1;
+            const int s = decode(wi, mt, nt, kb0, kb1);
+            umma::mbar_wait(&tfull[acc], tph[acc]);
+            tph[acc] ^= 1;
+            umma::fence_after_sync();
+            const int64_t m = static_cast<int64_t>(mt) * 128 + 32 * q + lane;
+            const int64_t n0 = static_cast<int64_t>(nt) * BN;
+            const uint32_t dt = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * BN);
+            const bool mok = m < m_store;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                if (n0 + c0 >= n_store) break;  // warp-uniform
+                float v[32];
+                umma::tmem_ld16(dt + c0, v);
+                umma::tmem_ld16(dt + c0 + 16, v + 16);
+                umma::tmem_ld_wait();
+                if (!mok) continue;
+                const int64_t nb = n0 + c0;
+                const int nv = n_store - nb < 32 ? static_cast<int>(n_store - nb) : 32;
+                if (e.mode == kTgStoreF32 || e.mode == kTgBias) {
+                    float* dst = e.c32 + static_cast<int64_t>(s) * e.split_stride + m * e.ldc32 + nb;
+                    if (e.mode == kTgBias)
+                        for (int j = 0; j < nv; ++j) v[j] += e.bias[nb + j];
+                    if (nv == 32 && (e.ldc32 & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    } else {
+                        for (int j = 0; j < nv; ++j) dst[j] = v[j];
+                    }
+                } else {
+                    if (e.mode == kTgBiasAct) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float z = v[j] + (j < nv ? e.bias[nb + j] : 0.0f);
+                            v[j] = act_fwd(z, e.act);
+                        }
+                        if (e.c32) {
+                            float* d32 = e.c32 + m * e.ldc32 + nb;
+                            for (int j = 0; j < nv; ++j) d32[j] = v[j];
+                        }
+                    } else {  // kTgActGrad: acc * act'(h), h = the activation output (bf16)
+                        const __nv_bfloat16* hr = e.h + m * e.ldh + nb;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            float y[8];
+                            if (j + 8 <= nv && (e.ldh & 7) == 0) {
+                                const uint4 u = *reinterpret_cast<const uint4*>(hr + j);
+                                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const float2 f = __bfloat1622float2(h2[i]);
+                                    y[2 * i] = f.x;
+                                    y[2 * i + 1] = f.y;
+                                }
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) y[i] = j + i < nv ? __bfloat162float(hr[j + i]) : 0.0f;
+                            }
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                v[j + i] = e.act == 0 ? v[j + i] * (1.0f - y[i] * y[i]) : (y[i] > 0.0f ? v[j + i] : 0.0f);
+                        }
+                    }
+                    __nv_bfloat16* d16 = e.c16 + m * e.ldc16 + nb;
+                    if (nv == 32 && (e.ldc16 & 7) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8)
+                            *reinterpret_cast<uint4*>(d16 + j) =
+                                make_uint4(umma::pack_bf16x2(v[j], v[j + 1]), umma::pack_bf16x2(v[j + 2], v[j + 3]),
+                                           umma::pack_bf16x2(v[j + 4], v[j + 5]), umma::pack_bf16x2(v[j + 6], v[j + 7]));
+                    } else {
+                        for (int j = 0; j < nv; ++j) d16[j] = __float2bfloat16(v[j]);
+                    }
+                }
+            }
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_u32(&tempty[acc])) : "memory");
+            acc ^= 1;
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (w == 1) umma::tmem_free<kCols>(tmem);
+}
+
+// ---------------------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        FLW_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw Error(Errc::Runtime, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+CUtensorMap make_map(const TgOperand& o, uint32_t box_inner, uint32_t box_outer) {
+    const int esz = o.f32 ? 4 : 2;
+    if ((reinterpret_cast<uintptr_t>(o.ptr) & 15) != 0 || (o.ld * esz) % 16 != 0)
+        throw Error(Errc::Config, "tgemm: operand base / row stride must be 16-byte aligned");
+    CUtensorMap m;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(o.cols), static_cast<cuuint64_t>(o.rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(o.ld * esz)};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, o.f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                   const_cast<void*>(o.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(Errc::Runtime, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return m;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        FLW_CUDA(cudaGetDevice(&dev));
+        FLW_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
+template <int BN, bool TF32, bool AMN, bool BMN>
+void launch_tg(cudaStream_t s, const TgOperand& A, const TgOperand& B, const TgArgs& a, int grid_cap) {
+    constexpr int esz = TF32 ? 4 : 2;
+    constexpr uint32_t BK = 128 / esz, atom = 128 / esz;
+    const CUtensorMap ma = AMN ? make_map(A, atom, BK) : make_map(A, BK, 128);
+    const CUtensorMap mb = BMN ? make_map(B, atom, BK) : make_map(B, BK, BN);
+    const size_t smem = static_cast<size_t>(tg_stages<BN>()) * tg_stage_bytes<BN>() + 1024;
+    auto kern = k_tgemm<BN, TF32, AMN, BMN>;
+    FLW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const int64_t items = static_cast<int64_t>(a.mtiles) * a.ntiles * a.splits;
+    const int cap = grid_cap > 0 ? grid_cap : sm_count();
+    const int grid = static_cast<int>(std::min<int64_t>(items, cap));
+    kern<<<grid, kTgThreads, smem, s>>>(ma, mb, a);
+    FLW_CUDA(cudaGetLastError());
+}
+
+template <int BN, bool TF32>
+void dispatch_major(cudaStream_t s, const TgOperand& A, bool a_mn, const TgOperand& B, bool b_mn, const TgArgs& a,
+                    int cap) {
+    if (!a_mn && !b_mn) launch_tg<BN, TF32, false, false>(s, A, B, a, cap);
+    else if (!a_mn && b_mn) launch_tg<BN, TF32, false, true>(s, A, B, a, cap);
+    else if (a_mn && !b_mn) launch_tg<BN, TF32, true, false>(s, A, B, a, cap);
+    else launch_tg<BN, TF32, true, true>(s, A, B, a, cap);
+}
+
+}  // namespace
+
+void tgemm(cudaStream_t s, const TgOperand& A, bool a_mn, const TgOperand& B, bool b_mn, int64_t M, int64_t N,
+           int64_t K, int splits, const TgEpilogue& epi, int bn, int grid_cap) {
+    if (A.f32 != B.f32) throw Error(Errc::Config, "tgemm: A and B must share the element type");
+    // 32-bit MN-major operands need the SWIZZLE_128B_BASE32B canonical layout, not this one
+    if (A.f32 && (a_mn || b_mn)) throw Error(Errc::Config, "tgemm: tf32 operands must both be K-major");
+    if (bn != 64 && bn != 128 && bn != 256) throw Error(Errc::Config, "tgemm: bn must be 64, 128 or 256");
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    const int BK = A.f32 ? 32 : 64;
+    TgArgs a{};
+    a.M = M;
+    a.N = N;
+    a.kblocks = static_cast<int>((K + BK - 1) / BK);
+    a.mtiles = static_cast<int>((M + 127) / 128);
+    a.ntiles = static_cast<int>((N + bn - 1) / bn);
+    a.splits = std::max(1, std::min(splits, a.kblocks));
+    if (a.splits > 1 && epi.mode != kTgStoreF32) throw Error(Errc::Config, "tgemm: split-K needs the f32 partial epilogue");
+    a.epi = epi;
+    const bool tf = A.f32;
+    if (bn == 64) tf ? dispatch_major<64, true>(s, A, a_mn, B, b_mn, a, grid_cap) : dispatch_major<64, false>(s, A, a_mn, B, b_mn, a, grid_cap);
+    else if (bn == 128) tf ? dispatch_major<128, true>(s, A, a_mn, B, b_mn, a, grid_cap) : dispatch_major<128, false>(s, A, a_mn, B, b_mn, a, grid_cap);
+    else tf ? dispatch_major<256, true>(s, A, a_mn, B, b_mn, a, grid_cap) : dispatch_major<256, false>(s, A, a_mn, B, b_mn, a, grid_cap);
+}
+
+}  // namespace flw
+
+// ---------------------------------------------------------------------------- self-test (C-ABI)
+// D = op(A) op(B) through tgemm with the f32 partial epilogue; the K splits are summed here.
+// a_mn: A given as [K, M] (else [M, K]); b_mn: B given as [K, N] (else [N, K]). tf32: operands
+// stay f32 (kind::tf32), else they are rounded to bf16 (kind::f16).
+extern "C" int flw_selftest_tgemm(int64_t M, int64_t N, int64_t K, int a_mn, int b_mn, int tf32, int splits, int bn,
+                                  const float* A, const float* B, float* D) {
+    using namespace flw;
+    try {
+        const int64_t ar = a_mn ? K : M, ac = a_mn ? M : K, br = b_mn ? K : N, bc = b_mn ? N : K;
+        const int esz = tf32 ? 4 : 2;
+        const int64_t ald = (ac * esz + 15) / 16 * 16 / esz, bld = (bc * esz + 15) / 16 * 16 / esz;
+        std::vector<uint8_t> ha(static_cast<size_t>(ar * ald * esz), 0), hb(static_cast<size_t>(br * bld * esz), 0);
+        for (int64_t r = 0; r < ar; ++r)
+            for (int64_t c = 0; c < ac; ++c) {
+                if (tf32) reinterpret_cast<float*>(ha.data())[r * ald + c] = A[r * ac + c];
+                else reinterpret_cast<__nv_bfloat16*>(ha.data())[r * ald + c] = __float2bfloat16(A[r * ac + c]);
+            }
+        for (int64_t r = 0; r < br; ++r)
+            for (int64_t c = 0; c < bc; ++c) {
+                if (tf32) reinterpret_cast<float*>(hb.data())[r * bld + c] = B[r * bc + c];
+                else reinterpret_cast<__nv_bfloat16*>(hb.data())[r * bld + c] = __float2bfloat16(B[r * bc + c]);
+            }
+        void *da = nullptr, *db = nullptr;
+        float* dd = nullptr;
+        const int BK = tf32 ? 32 : 64;
+        const int sp = std::max(1, std::min<int>(splits, static_cast<int>((K + BK - 1) / BK)));
+        FLW_CUDA(cudaMalloc(&da, ha.size()));
+        FLW_CUDA(cudaMalloc(&db, hb.size()));
+        FLW_CUDA(cudaMalloc(&dd, static_cast<size_t>(sp * M * N) * sizeof(float)));
+        FLW_CUDA(cudaMemcpy(da, ha.data(), ha.size(), cudaMemcpyHostToDevice));
+        FLW_CUDA(cudaMemcpy(db, hb.data(), hb.size(), cudaMemcpyHostToDevice));
+        FLW_CUDA(cudaMemset(dd, 0, static_cast<size_t>(sp * M * N) * sizeof(float)));
+        TgEpilogue e;
+        e.mode = kTgStoreF32;
+        e.c32 = dd;
+        e.ldc32 = N;
+        e.split_stride = M * N;
+        tgemm(nullptr, TgOperand{da, ar, ac, ald, tf32 != 0}, a_mn != 0, TgOperand{db, br, bc, bld, tf32 != 0}, b_mn != 0,
+              M, N, K, sp, e, bn);
+        std::vector<float> part(static_cast<size_t>(sp * M * N));
+        FLW_CUDA(cudaDeviceSynchronize());
+        FLW_CUDA(cudaMemcpy(part.data(), dd, part.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < M * N; ++i) {
+            float t = 0.0f;
+            for (int s2 = 0; s2 < sp; ++s2) t += part[static_cast<size_t>(s2 * M * N + i)];
+            D[i] = t;
+        }
+        cudaFree(da);
+        cudaFree(db);
+        cudaFree(dd);
+        return 0;
+    } catch (const std::exception& ex) {
+        fprintf(stderr, "flw_selftest_tgemm: %s\n", ex.what());
+        return 3;
+    }
+}

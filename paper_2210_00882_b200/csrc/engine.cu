@@ -23,6 +23,8 @@
 #include "common.cuh"
 #include "fast.cuh"
 #include "p2p.cuh"
+#include "tgemm.cuh"
+#include "wide.cuh"
 
 #include <chrono>
 #include <thread>
@@ -87,6 +89,18 @@ struct Engine::Bufs {
     double* prew_d = nullptr;
     float* gslots = nullptr;
     float* rep_w = nullptr;
+    // layer-wise learn path (fast numerics, an MLP wider than the fused kernel's 64 columns):
+    // bf16 weight copies, the input rows and every hidden activation as bf16 in HBM, dZ ping-pong
+    WideNet wpol{}, wcrit{};
+    __nv_bfloat16 *wb_p = nullptr, *wb_c = nullptr;
+    __nv_bfloat16* xb = nullptr;
+    int64_t xld = 0;
+    std::vector<__nv_bfloat16*> hw_p, hw_c;
+    std::vector<int64_t> hld_p, hld_c;
+    float* wlogits = nullptr;
+    __nv_bfloat16 *wdz0 = nullptr, *wdz1 = nullptr;
+    int64_t dzld = 0;
+    int wsplits = 0;
     std::vector<void*> owned;
 
     template <typename T>
@@ -145,6 +159,13 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     if (mappo_ && shape_.n_agents > 64) fail(Errc::Config, "at most 64 agents");
     if (!mappo_ && shape_.env == EnvKind::SpreadLite)
         fail(Errc::PolicyInapplicable, "PPO/A3C need a single-agent env (spread_lite is multi-agent)");
+    {  // fast numerics with a layer wider than the fused kernel's 64 columns: layer-wise GEMMs
+        int maxw = 0;
+        for (int l = 1; l < shape_.L; ++l) maxw = std::max({maxw, shape_.pdims[l], shape_.cdims[l]});
+        wide_ = numerics == Numerics::Fast && !mappo_ && (maxw > 64 || shape_.obs_dim > 64);
+        if (wide_ && replicas > 1)
+            fail(Errc::Config, "the layer-wise fast path (hidden > 64) runs one replica per engine");
+    }
     if (env_hi <= env_lo || env_lo < 0 || env_hi > env_total) fail(Errc::Config, "bad env range");
     if (shape_.n_actions > 16) fail(Errc::Config, "at most 16 discrete actions are supported");
     E_ = env_hi - env_lo;
@@ -252,7 +273,7 @@ void Engine::set_eager_collectives(bool on) {
 int64_t Engine::p2p_region_bytes() const { return p2p_layout(p2p_k_ > 0 ? p2p_k_ : 1, shape_.P).bytes; }
 
 void* Engine::p2p_region() {
-    if (numerics_ != Numerics::Fast || nrep_ > 1 || cfast_)
+    if (numerics_ != Numerics::Fast || nrep_ > 1 || cfast_ || wide_)
         fail(Errc::Config, "the peer-memory exchange serves fast numerics with one unit per GPU");
     if (!p2p_region_ptr_) fail(Errc::Config, "call set_p2p_group first (region size depends on k)");
     return p2p_region_ptr_;
@@ -271,7 +292,7 @@ void Engine::set_p2p_peers(int rank, int k, const std::vector<void*>& regions) {
 
 void Engine::alloc_p2p_region(int k) {
     FLW_CUDA(cudaSetDevice(device_));
-    if (numerics_ != Numerics::Fast || nrep_ > 1 || cfast_)
+    if (numerics_ != Numerics::Fast || nrep_ > 1 || cfast_ || wide_)
         fail(Errc::Config, "the peer-memory exchange serves fast numerics with one unit per GPU");
     const P2pLayout L = p2p_layout(k, shape_.P);
     if (!p2p_region_ptr_) {
@@ -379,6 +400,10 @@ void Engine::alloc() {
             b.rep_w = b.alloc<float>(nrep_);
             FLW_CUDA(cudaMemcpy(b.rep_w, w.data(), w.size() * sizeof(float), cudaMemcpyHostToDevice));
         }
+    }
+    if (numerics_ == Numerics::Fast && wide_) {
+        alloc_wide();
+        return;
     }
     if (numerics_ == Numerics::Fast) {
         // Fused tensor-core learn kernels: per-CTA dW partials replace the per-layer activations.
@@ -679,7 +704,7 @@ bool Engine::enq_rollout_fast_mappo(int64_t step0, int64_t nsteps) {
 }
 
 void Engine::enq_step(int64_t st) {
-    if (numerics_ == Numerics::Fast && !mappo_) return enq_rollout_fast(st, 1);
+    if (numerics_ == Numerics::Fast && !mappo_ && !wide_) return enq_rollout_fast(st, 1);
     if (numerics_ == Numerics::Fast && mappo_ && enq_rollout_fast_mappo(st, 1)) return;
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
@@ -892,8 +917,169 @@ void Engine::enq_learn_fast() {
     // the scalar loss is not an input of anything downstream: reduced on demand (read_tensor)
 }
 
+void Engine::alloc_wide() {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    const int L = s.L;
+    if (L > kMaxLayers) fail(Errc::Config, "fast numerics supports at most 8 layers");
+    auto pad8 = [](int64_t x) { return (x + 7) / 8 * 8; };
+    auto make = [&](int net, WideNet& n) {
+        const auto& d = net == 0 ? s.pdims : s.cdims;
+        n.L = L;
+        int64_t off = 0;
+        for (int l = 0; l < L; ++l) {
+            n.din[l] = d[l];
+            n.dout[l] = d[l + 1];
+            n.woff[l] = s.woff[net][l];
+            n.boff[l] = s.boff[net][l];
+            n.wofs[l] = off;
+            n.wld[l] = pad8(d[l + 1]);
+            off += (static_cast<int64_t>(d[l]) * n.wld[l] + 7) / 8 * 8;  // 16-byte aligned layers
+        }
+        n.wbytes = off;
+    };
+    make(0, b.wpol);
+    make(1, b.wcrit);
+    b.wb_p = b.alloc<__nv_bfloat16>(b.wpol.wbytes);
+    b.wb_c = b.alloc<__nv_bfloat16>(b.wcrit.wbytes);
+    const int64_t Rc = TR_ + R_;
+    b.xld = pad8(s.obs_dim);
+    b.xb = b.alloc<__nv_bfloat16>(Rc * b.xld);
+    int maxw = 1;
+    for (int l = 0; l + 1 < L; ++l) {
+        b.hld_p.push_back(pad8(s.pdims[l + 1]));
+        b.hld_c.push_back(pad8(s.cdims[l + 1]));
+        b.hw_p.push_back(b.alloc<__nv_bfloat16>(TR_ * b.hld_p.back()));
+        b.hw_c.push_back(b.alloc<__nv_bfloat16>(Rc * b.hld_c.back()));
+    }
+    for (int l = 0; l <= L; ++l) maxw = std::max({maxw, s.pdims[l], s.cdims[l]});
+    b.dzld = pad8(maxw);
+    b.wdz0 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
+    b.wdz1 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
+    b.wlogits = b.alloc<float>(TR_ * s.n_actions);
+    b.values = b.alloc<float>(Rc);  // values | last_value: one critic forward over all rows
+    b.last_value = b.values + TR_;
+    b.wsplits = static_cast<int>(std::min<int64_t>(64, (TR_ + 63) / 64));  // = tgemm's clamp
+    b.grid = b.wsplits;
+    b.part_p = b.alloc<float>(static_cast<int64_t>(b.wsplits) * s.P_policy);
+    b.part_c = b.alloc<float>(static_cast<int64_t>(b.wsplits) * (s.P - s.P_policy));
+    b.loss_parts = b.alloc<float>(2 * 3 * wide_loss_blocks(TR_));
+    b.block_sums = b.alloc<double>(2 * ((R_ + 31) / 32));
+    b.gae_counter = b.alloc<unsigned>(1);
+    b.upd_counter = b.alloc<unsigned>(1);
+    b.rsum_scratch = b.alloc<double>(256);
+}
+
+// Fast numerics, widths > 64: one train iteration as layer-wise tcgen05 GEMMs (kernels_tgemm.cu)
+// with bf16 activations in HBM: critic forward (values | last_value) -> GAE -> policy forward ->
+// losses (dZ of the output layers) -> per layer dW (split-K partials) + db + dZ of the layer
+// below -> fixed-order reduction of the partials. Same operand precision as the fused kernel
+// (bf16 operands, f32 accumulation, bf16 activations and adjoints).
+void Engine::enq_learn_wide() {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    const bool ppo = s.algo != Algo::A3c;
+    const int L = s.L;
+    const int64_t Rc = TR_ + R_;
+    const int act = act_of(cfg_);
+    wide_build_weights(stream_, b.params, b.wpol, b.wb_p, b.wcrit, b.wb_c);
+    wide_to_bf16(stream_, b.states, Rc, s.obs_dim, b.xb, b.xld);  // states blocks 0..T (last_next)
+    auto bn_for = [](int64_t n) { return n > 128 ? 256 : (n > 64 ? 128 : 64); };
+    auto forward = [&](const WideNet& n, const __nv_bfloat16* wb, const std::vector<__nv_bfloat16*>& H,
+                       const std::vector<int64_t>& ld, int64_t rows, float* out) {
+        for (int l = 0; l < L; ++l) {
+            const TgOperand A{l == 0 ? b.xb : H[l - 1], rows, n.din[l], l == 0 ? b.xld : ld[l - 1], false};
+            const TgOperand B{wb + n.wofs[l], n.din[l], n.dout[l], n.wld[l], false};
+            TgEpilogue e;
+            e.bias = b.params + n.boff[l];
+            if (l + 1 < L) {
+                e.mode = kTgBiasAct;
+                e.act = act;
+                e.c16 = H[l];
+                e.ldc16 = ld[l];
+            } else {
+                e.mode = kTgBias;
+                e.c32 = out;
+                e.ldc32 = n.dout[l];
+            }
+            tgemm(stream_, A, false, B, true, rows, n.dout[l], n.din[l], 1, e, bn_for(n.dout[l]));
+        }
+    };
+    const int splits = b.wsplits;
+    auto backward = [&](const WideNet& n, const __nv_bfloat16* wb, const std::vector<__nv_bfloat16*>& H,
+                        const std::vector<int64_t>& ld, float* part, int64_t pstride) {
+        __nv_bfloat16 *dz = b.wdz0, *other = b.wdz1;
+        for (int m = L - 1; m >= 0; --m) {
+            const int din = n.din[m], dout = n.dout[m];
+            // dW_m = H_{m-1}^T dZ_m (K = rows split `splits` ways) -> partial slots
+            const TgOperand Hin{m == 0 ? b.xb : H[m - 1], TR_, din, m == 0 ? b.xld : ld[m - 1], false};
+            const TgOperand Dz{dz, TR_, dout, b.dzld, false};
+            TgEpilogue e;
+            e.mode = kTgStoreF32;
+            e.c32 = part + (n.woff[m] - n.woff[0]);
+            e.ldc32 = dout;
+            e.split_stride = pstride;
+            tgemm(stream_, Hin, true, Dz, true, din, dout, TR_, splits, e, bn_for(dout));
+            wide_colsum(stream_, dz, TR_, dout, b.dzld, splits, part + (n.boff[m] - n.woff[0]), pstride);
+            if (m == 0) break;
+            // dZ_{m-1} = (dZ_m W_m^T) * act'(H_{m-1})
+            const TgOperand Wk{wb + n.wofs[m], din, dout, n.wld[m], false};
+            TgEpilogue g;
+            g.mode = kTgActGrad;
+            g.act = act;
+            g.h = H[m - 1];
+            g.ldh = ld[m - 1];
+            g.c16 = other;
+            g.ldc16 = b.dzld;
+            tgemm(stream_, Dz, false, Wk, false, TR_, din, dout, 1, g, bn_for(din));
+            std::swap(dz, other);
+        }
+    };
+    probe_begin("critic_fwd");
+    forward(b.wcrit, b.wb_c, b.hw_c, b.hld_c, Rc, b.values);
+    probe_end();
+    probe_begin("gae");
+    fast_gae(stream_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
+             b.block_sums, b.stats, b.gae_counter);
+    probe_end();
+    probe_begin("learn_policy");
+    forward(b.wpol, b.wb_p, b.hw_p, b.hld_p, TR_, b.wlogits);
+    const int nlb = wide_loss_blocks(TR_);
+    WideLossArgs la{};
+    la.rows = TR_;
+    la.actions = b.actions;
+    la.logp_old = b.logp;
+    la.adv = b.adv;
+    la.ret = b.ret;
+    la.values_in = b.values;
+    la.adv_stats = (ppo && cfg_.normalize_adv) ? b.stats : nullptr;
+    la.inv_n = 1.0 / static_cast<double>(TR_);
+    la.value_coef = cfg_.value_coef;
+    la.entropy_coef = cfg_.entropy_coef;
+    la.clip_eps = static_cast<float>(cfg_.clip_eps);
+    la.ld = b.dzld;
+    la.kind = ppo ? kNetPolicyPpo : kNetPolicyA3c;
+    la.out = b.wlogits;
+    la.A = s.n_actions;
+    la.width = s.n_actions;
+    la.dz = b.wdz0;
+    la.loss_partials = b.loss_parts;
+    wide_loss(stream_, la);
+    backward(b.wpol, b.wb_p, b.hw_p, b.hld_p, b.part_p, s.P_policy);
+    la.kind = kNetCritic;
+    la.out = b.values;
+    la.A = 1;
+    la.width = 1;
+    la.loss_partials = b.loss_parts + 3 * nlb;
+    wide_loss(stream_, la);
+    backward(b.wcrit, b.wb_c, b.hw_c, b.hld_c, b.part_c, s.P - s.P_policy);
+    b.lgrid_p = b.lgrid_c = nlb;
+    fast_reduce_partials(stream_, b.part_p, b.part_c, splits, splits, s.P_policy, s.P - s.P_policy, b.grads, 0);
+    probe_end();
+}
+
 void Engine::enq_learn_grads() {
-    if (numerics_ == Numerics::Fast) return enq_learn_fast();
+    if (numerics_ == Numerics::Fast) return wide_ ? enq_learn_wide() : enq_learn_fast();
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions, L = s.L;
@@ -1153,7 +1339,7 @@ void Engine::build_graph() {
     enq_reset();
     trace_capture("reset");
     probe_begin("rollout");
-    if (numerics_ == Numerics::Fast && !mappo_)
+    if (numerics_ == Numerics::Fast && !mappo_ && !wide_)
         enq_rollout_fast(0, T_);
     else if (!(numerics_ == Numerics::Fast && mappo_ && enq_rollout_fast_mappo(0, T_)))
         for (int64_t st = 0; st < T_; ++st) enq_step(st);  // exact rollout

@@ -57,7 +57,7 @@ class Engine {
     void adopt_ipc_mapping(void* p) { p2p_ipc_opened_.push_back(p); }  // closed by the destructor
     void set_p2p_peers(int rank, int k, const std::vector<void*>& regions);
     bool p2p_enabled() const { return p2p_k_ > 1; }
-    bool p2p_capable() const { return numerics_ == Numerics::Fast && nrep_ == 1 && !cfast_; }
+    bool p2p_capable() const { return numerics_ == Numerics::Fast && nrep_ == 1 && !cfast_ && !wide_; }
     void disable_p2p() {  // back to the NCCL exchange (the group must agree; see bench.py)
         destroy_graph();
         p2p_k_ = 0;
@@ -128,6 +128,8 @@ class Engine {
     void enq_rollout_fast(int64_t step0, int64_t nsteps);
     bool enq_rollout_fast_mappo(int64_t step0, int64_t nsteps);
     void enq_learn_fast();
+    void alloc_wide();
+    void enq_learn_wide();
     void enq_learn_grads();
     void enq_grad_sync_and_adam();
     void enq_reward_sum();
@@ -145,6 +147,7 @@ class Engine {
     int64_t lo_, hi_, etot_, E_, R_, T_, TR_;
     bool mappo_ = false;   // agent-major rows R = n*E, critic on [joint obs | agent one-hot]
     bool cfast_ = false;   // fast MAPPO with the compact critic (critic input > 64 wide)
+    bool wide_ = false;    // fast numerics, a layer > 64 wide: layer-wise tcgen05 GEMM learn path
     int p2p_rank_ = 0, p2p_k_ = 0;
     void* p2p_region_ptr_ = nullptr;
     int p2p_alloc_k_ = 0;

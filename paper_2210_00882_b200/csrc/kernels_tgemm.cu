@@ -82,7 +82,12 @@ __device__ __forceinline__ void mma_tg(uint32_t tmem_d, uint64_t adesc, uint64_t
     }
 }
 
-__device__ __forceinline__ float act_fwd(float z, int act) { return act == 0 ? tanhf(z) : fmaxf(z, 0.0f); }
+// MUFU tanh (max rel. error ~2^-11, below the bf16 rounding of the stored activation)
+__device__ __forceinline__ float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 constexpr int kTgThreads = 192;
 
@@ -110,6 +115,7 @@ __global__ void __launch_bounds__(kTgThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t full[S], empty[S], tfull[2], tempty[2];
     __shared__ uint32_t tslot;
+    __shared__ __align__(16) float sbias[BN];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t items = static_cast<int64_t>(a.mtiles) * a.ntiles * a.splits;
 
@@ -214,19 +220,26 @@ __global__ void __launch_bounds__(kTgThreads, 1)
     } else {
         // ------------------------------------------------------------------ epilogue
         const int q = w & 3;
+        const int et = threadIdx.x - 64;  // 0..127 over the four epilogue warps
         const TgEpilogue& e = a.epi;
         const int64_t m_store = e.m_store >= 0 ? e.m_store : a.M;
         const int64_t n_store = e.n_store >= 0 ? e.n_store : a.N;
+        const bool use_bias = e.mode == kTgBias || e.mode == kTgBiasAct;
         uint32_t tph[2] = {0, 0};
         int acc = 0;
         for (int64_t wi = blockIdx.x; wi < items; wi += gridDim.x) {
             int mt, nt, kb0, kb1;
             const int s = decode(wi, mt, nt, kb0, kb1);
+            const int64_t n0 = static_cast<int64_t>(nt) * BN;
+            if (use_bias) {  // this item's bias slice, staged once (named barrier: epilogue warps)
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                for (int i = et; i < BN; i += 128) sbias[i] = n0 + i < n_store ? e.bias[n0 + i] : 0.0f;
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+            }
             umma::mbar_wait(&tfull[acc], tph[acc]);
             tph[acc] ^= 1;
             umma::fence_after_sync();
             const int64_t m = static_cast<int64_t>(mt) * 128 + 32 * q + lane;
-            const int64_t n0 = static_cast<int64_t>(nt) * BN;
             const uint32_t dt = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * BN);
             const bool mok = m < m_store;
 #pragma unroll 1
@@ -235,65 +248,97 @@ __global__ void __launch_bounds__(kTgThreads, 1)
                 float v[32];
                 umma::tmem_ld16(dt + c0, v);
                 umma::tmem_ld16(dt + c0 + 16, v + 16);
-                umma::tmem_ld_wait();
-                if (!mok) continue;
                 const int64_t nb = n0 + c0;
                 const int nv = n_store - nb < 32 ? static_cast<int>(n_store - nb) : 32;
+                uint4 hv[4];  // act' input row slice, loaded while the TMEM load is in flight
+                if (e.mode == kTgActGrad && mok) {
+                    const __nv_bfloat16* hr = e.h + m * e.ldh + nb;
+                    if (nv == 32 && (e.ldh & 7) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) hv[j] = __ldg(reinterpret_cast<const uint4*>(hr + 8 * j));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint32_t w4[4];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const int c = 8 * j + 2 * i;
+                                const float x0 = c < nv ? __bfloat162float(hr[c]) : 0.0f;
+                                const float x1 = c + 1 < nv ? __bfloat162float(hr[c + 1]) : 0.0f;
+                                w4[i] = umma::pack_bf16x2(x0, x1);
+                            }
+                            hv[j] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                        }
+                    }
+                }
+                umma::tmem_ld_wait();
+                if (!mok) continue;
+                if (use_bias) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 b4 = *reinterpret_cast<const float4*>(sbias + c0 + j);
+                        v[j] += b4.x;
+                        v[j + 1] += b4.y;
+                        v[j + 2] += b4.z;
+                        v[j + 3] += b4.w;
+                    }
+                }
                 if (e.mode == kTgStoreF32 || e.mode == kTgBias) {
                     float* dst = e.c32 + static_cast<int64_t>(s) * e.split_stride + m * e.ldc32 + nb;
-                    if (e.mode == kTgBias)
-                        for (int j = 0; j < nv; ++j) v[j] += e.bias[nb + j];
                     if (nv == 32 && (e.ldc32 & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
                         for (int j = 0; j < 32; j += 4)
                             *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                    } else {
-                        for (int j = 0; j < nv; ++j) dst[j] = v[j];
+                    } else {  // (static indices keep v[] in registers)
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (j < nv) dst[j] = v[j];
                     }
-                } else {
-                    if (e.mode == kTgBiasAct) {
+                    continue;
+                }
+                if (e.mode == kTgBiasAct) {
+                    if (e.act == 0) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float z = v[j] + (j < nv ? e.bias[nb + j] : 0.0f);
-                            v[j] = act_fwd(z, e.act);
-                        }
-                        if (e.c32) {
-                            float* d32 = e.c32 + m * e.ldc32 + nb;
-                            for (int j = 0; j < nv; ++j) d32[j] = v[j];
-                        }
-                    } else {  // kTgActGrad: acc * act'(h), h = the activation output (bf16)
-                        const __nv_bfloat16* hr = e.h + m * e.ldh + nb;
+                        for (int j = 0; j < 32; ++j) v[j] = tanh_approx(v[j]);
+                    } else {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            float y[8];
-                            if (j + 8 <= nv && (e.ldh & 7) == 0) {
-                                const uint4 u = *reinterpret_cast<const uint4*>(hr + j);
-                                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                        for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+                    }
+                    if (e.c32) {
+                        float* d32 = e.c32 + m * e.ldc32 + nb;
 #pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    const float2 f = __bfloat1622float2(h2[i]);
-                                    y[2 * i] = f.x;
-                                    y[2 * i + 1] = f.y;
-                                }
+                        for (int j = 0; j < 32; ++j)
+                            if (j < nv) d32[j] = v[j];
+                    }
+                } else {  // kTgActGrad: acc * act'(h), h = the activation output (bf16)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hv[j]);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float2 y = __bfloat1622float2(h2[i]);
+                            const int c = 8 * j + 2 * i;
+                            if (e.act == 0) {
+                                v[c] *= 1.0f - y.x * y.x;
+                                v[c + 1] *= 1.0f - y.y * y.y;
                             } else {
-#pragma unroll
-                                for (int i = 0; i < 8; ++i) y[i] = j + i < nv ? __bfloat162float(hr[j + i]) : 0.0f;
+                                v[c] = y.x > 0.0f ? v[c] : 0.0f;
+                                v[c + 1] = y.y > 0.0f ? v[c + 1] : 0.0f;
                             }
-#pragma unroll
-                            for (int i = 0; i < 8; ++i)
-                                v[j + i] = e.act == 0 ? v[j + i] * (1.0f - y[i] * y[i]) : (y[i] > 0.0f ? v[j + i] : 0.0f);
                         }
                     }
-                    __nv_bfloat16* d16 = e.c16 + m * e.ldc16 + nb;
-                    if (nv == 32 && (e.ldc16 & 7) == 0) {
+                }
+                __nv_bfloat16* d16 = e.c16 + m * e.ldc16 + nb;
+                if (nv == 32 && (e.ldc16 & 7) == 0) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8)
-                            *reinterpret_cast<uint4*>(d16 + j) =
-                                make_uint4(umma::pack_bf16x2(v[j], v[j + 1]), umma::pack_bf16x2(v[j + 2], v[j + 3]),
-                                           umma::pack_bf16x2(v[j + 4], v[j + 5]), umma::pack_bf16x2(v[j + 6], v[j + 7]));
-                    } else {
-                        for (int j = 0; j < nv; ++j) d16[j] = __float2bfloat16(v[j]);
-                    }
+                    for (int j = 0; j < 32; j += 8)
+                        *reinterpret_cast<uint4*>(d16 + j) =
+                            make_uint4(umma::pack_bf16x2(v[j], v[j + 1]), umma::pack_bf16x2(v[j + 2], v[j + 3]),
+                                       umma::pack_bf16x2(v[j + 4], v[j + 5]), umma::pack_bf16x2(v[j + 6], v[j + 7]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < nv) d16[j] = __float2bfloat16(v[j]);
                 }
             }
             umma::fence_before_sync();

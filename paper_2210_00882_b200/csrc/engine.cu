@@ -25,6 +25,7 @@
 #include "p2p.cuh"
 #include "tgemm.cuh"
 #include "wide.cuh"
+#include <cuda_fp16.h>
 
 #include <chrono>
 #include <thread>
@@ -101,6 +102,9 @@ struct Engine::Bufs {
     __nv_bfloat16 *wdz0 = nullptr, *wdz1 = nullptr;
     int64_t dzld = 0;
     int wsplits = 0;
+    // f32-accurate rollout of wide policies: split f16 operands (hi | lo | hi), f16 weight image
+    __half *wr_x = nullptr, *wr_h0 = nullptr, *wr_h1 = nullptr, *wr_w = nullptr;
+    int64_t wr_ldx = 0, wr_ldh = 0;
     std::vector<void*> owned;
 
     template <typename T>
@@ -705,6 +709,7 @@ bool Engine::enq_rollout_fast_mappo(int64_t step0, int64_t nsteps) {
 
 void Engine::enq_step(int64_t st) {
     if (numerics_ == Numerics::Fast && !mappo_ && !wide_) return enq_rollout_fast(st, 1);
+    if (numerics_ == Numerics::Fast && wide_) return enq_step_wide(st);
     if (numerics_ == Numerics::Fast && mappo_ && enq_rollout_fast_mappo(st, 1)) return;
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
@@ -742,6 +747,14 @@ void Engine::enq_step(int64_t st) {
         mappo_rollout(stream_, b.ctx, m);
         return;
     }
+    enq_step_env(st);
+}
+
+// PolicyApply + env step of one rollout step on the f32 logits in b.logits (PPO / A3C).
+void Engine::enq_step_env(int64_t st) {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    const int S = s.obs_dim, A = s.n_actions;
     RolloutArgs a{};
     a.logits = b.logits;
     a.est = b.est;
@@ -917,6 +930,47 @@ void Engine::enq_learn_fast() {
     // the scalar loss is not an input of anything downstream: reduced on demand (read_tensor)
 }
 
+// Fast numerics, wide policy: one rollout step. The policy MLP runs as f32-accurate split
+// GEMMs on the tensor cores (x = hi + lo, W = hi + lo in f16; x.W ~ hi.hi + lo.hi + hi.lo with
+// f32 accumulation, one GEMM with K = 3 segments per layer; tanh in f32), then the reference's
+// PolicyApply + env step (the exact step kernel on the f32 logits).
+void Engine::enq_step_wide(int64_t st) {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    const int L = s.L, S = s.obs_dim;
+    const WideNet& n = b.wpol;
+    if (st == 0 || !capturing_) wide_build_split_weights(stream_, b.params, n, b.wr_w);
+    wide_split_input(stream_, b.states + st * R_ * S, R_, S, b.wr_x, n.dp[0]);
+    auto bn_for = [](int64_t x) { return x > 128 ? 256 : (x > 64 ? 128 : 64); };
+    const __half* in = b.wr_x;
+    int64_t inld = b.wr_ldx;
+    __half* outs[2] = {b.wr_h0, b.wr_h1};
+    for (int l = 0; l < L; ++l) {
+        const TgOperand A{in, R_, 3 * n.dp[l], inld, kTgF16};
+        const TgOperand B{b.wr_w + n.sofs[l], 3 * n.dp[l], n.dout[l], n.wld[l], kTgF16};
+        TgEpilogue e;
+        e.bias = b.params + n.boff[l];
+        if (l + 1 < L) {
+            e.mode = kTgSplit3;
+            e.act = act_of(cfg_);
+            e.c16h = outs[l & 1];
+            e.ldc16 = 3 * n.dp[l + 1];
+            e.seg = n.dp[l + 1];
+        } else {
+            e.mode = kTgBias;
+            e.c32 = b.logits;
+            e.ldc32 = n.dout[l];
+        }
+        // few rows per step: narrow N tiles spread the layer over more SMs
+        tgemm(stream_, A, false, B, true, R_, n.dout[l], 3 * n.dp[l], 1, e, R_ <= 16384 ? 64 : bn_for(n.dout[l]));
+        if (l + 1 < L) {
+            in = outs[l & 1];
+            inld = 3 * n.dp[l + 1];
+        }
+    }
+    enq_step_env(st);
+}
+
 void Engine::alloc_wide() {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
@@ -937,6 +991,13 @@ void Engine::alloc_wide() {
             off += (static_cast<int64_t>(d[l]) * n.wld[l] + 7) / 8 * 8;  // 16-byte aligned layers
         }
         n.wbytes = off;
+        int64_t so = 0;
+        for (int l = 0; l < L; ++l) {
+            n.dp[l] = (d[l] + 63) / 64 * 64;
+            n.sofs[l] = so;
+            so += 3 * n.dp[l] * n.wld[l];
+        }
+        n.sbytes = so;
     };
     make(0, b.wpol);
     make(1, b.wcrit);
@@ -957,6 +1018,16 @@ void Engine::alloc_wide() {
     b.wdz0 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
     b.wdz1 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
     b.wlogits = b.alloc<float>(TR_ * s.n_actions);
+    {  // rollout: split operands of R_ rows (pad columns stay zero)
+        int64_t maxh = 64;
+        for (int l = 1; l < L; ++l) maxh = std::max<int64_t>(maxh, (s.pdims[l] + 63) / 64 * 64);
+        b.wr_ldx = 3 * b.wpol.dp[0];
+        b.wr_ldh = 3 * maxh;
+        b.wr_x = b.alloc<__half>(R_ * b.wr_ldx);
+        b.wr_h0 = b.alloc<__half>(R_ * b.wr_ldh);
+        b.wr_h1 = b.alloc<__half>(R_ * b.wr_ldh);
+        b.wr_w = b.alloc<__half>(b.wpol.sbytes);
+    }
     b.values = b.alloc<float>(Rc);  // values | last_value: one critic forward over all rows
     b.last_value = b.values + TR_;
     b.wsplits = static_cast<int>(std::min<int64_t>(64, (TR_ + 63) / 64));  // = tgemm's clamp
@@ -988,8 +1059,8 @@ void Engine::enq_learn_wide() {
     auto forward = [&](const WideNet& n, const __nv_bfloat16* wb, const std::vector<__nv_bfloat16*>& H,
                        const std::vector<int64_t>& ld, int64_t rows, float* out) {
         for (int l = 0; l < L; ++l) {
-            const TgOperand A{l == 0 ? b.xb : H[l - 1], rows, n.din[l], l == 0 ? b.xld : ld[l - 1], false};
-            const TgOperand B{wb + n.wofs[l], n.din[l], n.dout[l], n.wld[l], false};
+            const TgOperand A{l == 0 ? b.xb : H[l - 1], rows, n.din[l], l == 0 ? b.xld : ld[l - 1], kTgBF16};
+            const TgOperand B{wb + n.wofs[l], n.din[l], n.dout[l], n.wld[l], kTgBF16};
             TgEpilogue e;
             e.bias = b.params + n.boff[l];
             if (l + 1 < L) {
@@ -1012,8 +1083,8 @@ void Engine::enq_learn_wide() {
         for (int m = L - 1; m >= 0; --m) {
             const int din = n.din[m], dout = n.dout[m];
             // dW_m = H_{m-1}^T dZ_m (K = rows split `splits` ways) -> partial slots
-            const TgOperand Hin{m == 0 ? b.xb : H[m - 1], TR_, din, m == 0 ? b.xld : ld[m - 1], false};
-            const TgOperand Dz{dz, TR_, dout, b.dzld, false};
+            const TgOperand Hin{m == 0 ? b.xb : H[m - 1], TR_, din, m == 0 ? b.xld : ld[m - 1], kTgBF16};
+            const TgOperand Dz{dz, TR_, dout, b.dzld, kTgBF16};
             TgEpilogue e;
             e.mode = kTgStoreF32;
             e.c32 = part + (n.woff[m] - n.woff[0]);
@@ -1023,7 +1094,7 @@ void Engine::enq_learn_wide() {
             wide_colsum(stream_, dz, TR_, dout, b.dzld, splits, part + (n.boff[m] - n.woff[0]), pstride);
             if (m == 0) break;
             // dZ_{m-1} = (dZ_m W_m^T) * act'(H_{m-1})
-            const TgOperand Wk{wb + n.wofs[m], din, dout, n.wld[m], false};
+            const TgOperand Wk{wb + n.wofs[m], din, dout, n.wld[m], kTgBF16};
             TgEpilogue g;
             g.mode = kTgActGrad;
             g.act = act;

@@ -129,6 +129,8 @@ class Engine {
     bool enq_rollout_fast_mappo(int64_t step0, int64_t nsteps);
     void enq_learn_fast();
     void alloc_wide();
+    void enq_step_wide(int64_t st);
+    void enq_step_env(int64_t st);
     void enq_learn_wide();
     void enq_learn_grads();
     void enq_grad_sync_and_adam();

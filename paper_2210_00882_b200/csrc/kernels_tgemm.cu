@@ -17,10 +17,12 @@
 //   MN-major: 64 bf16 / 32 f32 MN-contiguous elements x 8 K-rows per atom; K-row groups at
 //             SBO = 1024 B, MN atoms at LBO = one TMA box (BK rows x 128 B)
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <mutex>
 #include <vector>
 
@@ -61,16 +63,16 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uin
     return d;
 }
 
-// kind::f16 (bf16) / kind::tf32 instruction descriptor, f32 accumulate, M = 128.
-__host__ __device__ constexpr uint32_t idesc_tg(int N, bool tf32, bool a_mn, bool b_mn) {
-    const uint32_t fmt = tf32 ? 2u : 1u;
+// kind::f16 (bf16 / f16) / kind::tf32 instruction descriptor, f32 accumulate, M = 128.
+__host__ __device__ constexpr uint32_t idesc_tg(int N, int dt, bool a_mn, bool b_mn) {
+    const uint32_t fmt = dt == kTgF32 ? 2u : (dt == kTgF16 ? 0u : 1u);
     return (1u << 4) | (fmt << 7) | (fmt << 10) | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u) |
            (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
 }
 
-template <bool TF32>
+template <int DT>
 __device__ __forceinline__ void mma_tg(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, bool acc) {
-    if constexpr (TF32) {
+    if constexpr (DT == kTgF32) {
         asm volatile(
             "{\n\t.reg .pred p, e;\n\t"
             "elect.sync _|e, 0xffffffff;\n\t"
@@ -100,13 +102,13 @@ __host__ __device__ constexpr uint32_t tg_stage_bytes() {
     return 128u * 128u + static_cast<uint32_t>(BN) * 128u;
 }
 
-template <int BN, bool TF32, bool AMN, bool BMN>
+template <int BN, int DT, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kTgThreads, 1)
     k_tgemm(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, const TgArgs a) {
     constexpr int S = tg_stages<BN>();
     constexpr uint32_t kStage = tg_stage_bytes<BN>();
     constexpr uint32_t kABytes = 128u * 128u;
-    constexpr int esz = TF32 ? 4 : 2;
+    constexpr int esz = DT == kTgF32 ? 4 : 2;
     constexpr int BK = 128 / esz;  // K elements per k-block (one 128-byte row)
     constexpr int UK = 32 / esz;   // K elements per MMA
     constexpr int kAtom = 128 / esz;
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(kTgThreads, 1)
         }
     } else if (w == 1) {
         // ------------------------------------------------------------------ MMA issuer
-        constexpr uint32_t idesc = idesc_tg(BN, TF32, AMN, BMN);
+        constexpr uint32_t idesc = idesc_tg(BN, DT, AMN, BMN);
         int stage = 0;
         uint32_t ph = 0, tph[2] = {0, 0};
         int acc = 0;
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(kTgThreads, 1)
                                             : desc_sw128(sa + k * 32, 16, 1024);
                     const uint64_t bd = BMN ? desc_sw128(sb + k * (UK * 128), BK * 128, 1024)
                                             : desc_sw128(sb + k * 32, 16, 1024);
-                    mma_tg<TF32>(dt, ad, bd, idesc, kb > kb0 || k > 0);
+                    mma_tg<DT>(dt, ad, bd, idesc, kb > kb0 || k > 0);
                 }
                 umma::commit_warp(&empty[stage]);  // the slot is free once these MMAs read it
                 if (++stage == S) {
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kTgThreads, 1)
         const TgEpilogue& e = a.epi;
         const int64_t m_store = e.m_store >= 0 ? e.m_store : a.M;
         const int64_t n_store = e.n_store >= 0 ? e.n_store : a.N;
-        const bool use_bias = e.mode == kTgBias || e.mode == kTgBiasAct;
+        const bool use_bias = e.mode == kTgBias || e.mode == kTgBiasAct || e.mode == kTgSplit3;
         uint32_t tph[2] = {0, 0};
         int acc = 0;
         for (int64_t wi = blockIdx.x; wi < items; wi += gridDim.x) {
@@ -293,6 +295,44 @@ __global__ void __launch_bounds__(kTgThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
                             if (j < nv) dst[j] = v[j];
+                    }
+                    continue;
+                }
+                if (e.mode == kTgSplit3) {  // f32-accurate activation, split into f16 hi + lo
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) {
+                        const float y0 = e.act == 0 ? tanhf(v[j]) : fmaxf(v[j], 0.0f);
+                        const float y1 = e.act == 0 ? tanhf(v[j + 1]) : fmaxf(v[j + 1], 0.0f);
+                        const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
+                        const __half l0 = __float2half_rn(y0 - __half2float(h0));
+                        const __half l1 = __float2half_rn(y1 - __half2float(h1));
+                        hi[j / 2] = static_cast<uint32_t>(__half_as_ushort(h0)) |
+                                    (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+                        lo[j / 2] = static_cast<uint32_t>(__half_as_ushort(l0)) |
+                                    (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+                    }
+                    __half* d = e.c16h + m * e.ldc16 + nb;
+                    if (nv == 32 && (e.ldc16 & 7) == 0 && (e.seg & 7) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint4 h4 = make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
+                            *reinterpret_cast<uint4*>(d + 8 * j) = h4;
+                            *reinterpret_cast<uint4*>(d + e.seg + 8 * j) =
+                                make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
+                            *reinterpret_cast<uint4*>(d + 2 * e.seg + 8 * j) = h4;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            if (j < nv) {
+                                const unsigned short hs = static_cast<unsigned short>(hi[j / 2] >> (16 * (j & 1)));
+                                const unsigned short ls = static_cast<unsigned short>(lo[j / 2] >> (16 * (j & 1)));
+                                d[j] = __ushort_as_half(hs);
+                                d[e.seg + j] = __ushort_as_half(ls);
+                                d[2 * e.seg + j] = __ushort_as_half(hs);
+                            }
+                        }
                     }
                     continue;
                 }
@@ -367,7 +407,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 CUtensorMap make_map(const TgOperand& o, uint32_t box_inner, uint32_t box_outer) {
-    const int esz = o.f32 ? 4 : 2;
+    const int esz = o.dt == kTgF32 ? 4 : 2;
     if ((reinterpret_cast<uintptr_t>(o.ptr) & 15) != 0 || (o.ld * esz) % 16 != 0)
         throw Error(Errc::Config, "tgemm: operand base / row stride must be 16-byte aligned");
     CUtensorMap m;
@@ -375,7 +415,9 @@ CUtensorMap make_map(const TgOperand& o, uint32_t box_inner, uint32_t box_outer)
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(o.ld * esz)};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
-    const CUresult r = encode_fn()(&m, o.f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+    const CUtensorMapDataType ty = o.dt == kTgF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                   : (o.dt == kTgF16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
+    const CUresult r = encode_fn()(&m, ty, 2,
                                    const_cast<void*>(o.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -393,14 +435,14 @@ int sm_count() {
     return n;
 }
 
-template <int BN, bool TF32, bool AMN, bool BMN>
+template <int BN, int DT, bool AMN, bool BMN>
 void launch_tg(cudaStream_t s, const TgOperand& A, const TgOperand& B, const TgArgs& a, int grid_cap) {
-    constexpr int esz = TF32 ? 4 : 2;
+    constexpr int esz = DT == kTgF32 ? 4 : 2;
     constexpr uint32_t BK = 128 / esz, atom = 128 / esz;
     const CUtensorMap ma = AMN ? make_map(A, atom, BK) : make_map(A, BK, 128);
     const CUtensorMap mb = BMN ? make_map(B, atom, BK) : make_map(B, BK, BN);
     const size_t smem = static_cast<size_t>(tg_stages<BN>()) * tg_stage_bytes<BN>() + 1024;
-    auto kern = k_tgemm<BN, TF32, AMN, BMN>;
+    auto kern = k_tgemm<BN, DT, AMN, BMN>;
     FLW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const int64_t items = static_cast<int64_t>(a.mtiles) * a.ntiles * a.splits;
     const int cap = grid_cap > 0 ? grid_cap : sm_count();
@@ -409,25 +451,25 @@ void launch_tg(cudaStream_t s, const TgOperand& A, const TgOperand& B, const TgA
     FLW_CUDA(cudaGetLastError());
 }
 
-template <int BN, bool TF32>
+template <int BN, int DT>
 void dispatch_major(cudaStream_t s, const TgOperand& A, bool a_mn, const TgOperand& B, bool b_mn, const TgArgs& a,
                     int cap) {
-    if (!a_mn && !b_mn) launch_tg<BN, TF32, false, false>(s, A, B, a, cap);
-    else if (!a_mn && b_mn) launch_tg<BN, TF32, false, true>(s, A, B, a, cap);
-    else if (a_mn && !b_mn) launch_tg<BN, TF32, true, false>(s, A, B, a, cap);
-    else launch_tg<BN, TF32, true, true>(s, A, B, a, cap);
+    if (!a_mn && !b_mn) launch_tg<BN, DT, false, false>(s, A, B, a, cap);
+    else if (!a_mn && b_mn) launch_tg<BN, DT, false, true>(s, A, B, a, cap);
+    else if (a_mn && !b_mn) launch_tg<BN, DT, true, false>(s, A, B, a, cap);
+    else launch_tg<BN, DT, true, true>(s, A, B, a, cap);
 }
 
 }  // namespace
 
 void tgemm(cudaStream_t s, const TgOperand& A, bool a_mn, const TgOperand& B, bool b_mn, int64_t M, int64_t N,
            int64_t K, int splits, const TgEpilogue& epi, int bn, int grid_cap) {
-    if (A.f32 != B.f32) throw Error(Errc::Config, "tgemm: A and B must share the element type");
+    if (A.dt != B.dt) throw Error(Errc::Config, "tgemm: A and B must share the element type");
     // 32-bit MN-major operands need the SWIZZLE_128B_BASE32B canonical layout, not this one
-    if (A.f32 && (a_mn || b_mn)) throw Error(Errc::Config, "tgemm: tf32 operands must both be K-major");
+    if (A.dt == kTgF32 && (a_mn || b_mn)) throw Error(Errc::Config, "tgemm: tf32 operands must both be K-major");
     if (bn != 64 && bn != 128 && bn != 256) throw Error(Errc::Config, "tgemm: bn must be 64, 128 or 256");
     if (M <= 0 || N <= 0 || K <= 0) return;
-    const int BK = A.f32 ? 32 : 64;
+    const int BK = A.dt == kTgF32 ? 32 : 64;
     TgArgs a{};
     a.M = M;
     a.N = N;
@@ -437,39 +479,47 @@ void tgemm(cudaStream_t s, const TgOperand& A, bool a_mn, const TgOperand& B, bo
     a.splits = std::max(1, std::min(splits, a.kblocks));
     if (a.splits > 1 && epi.mode != kTgStoreF32) throw Error(Errc::Config, "tgemm: split-K needs the f32 partial epilogue");
     a.epi = epi;
-    const bool tf = A.f32;
-    if (bn == 64) tf ? dispatch_major<64, true>(s, A, a_mn, B, b_mn, a, grid_cap) : dispatch_major<64, false>(s, A, a_mn, B, b_mn, a, grid_cap);
-    else if (bn == 128) tf ? dispatch_major<128, true>(s, A, a_mn, B, b_mn, a, grid_cap) : dispatch_major<128, false>(s, A, a_mn, B, b_mn, a, grid_cap);
-    else tf ? dispatch_major<256, true>(s, A, a_mn, B, b_mn, a, grid_cap) : dispatch_major<256, false>(s, A, a_mn, B, b_mn, a, grid_cap);
+    auto go = [&](auto bnc) {
+        constexpr int BNc = decltype(bnc)::value;
+        if (A.dt == kTgF32) dispatch_major<BNc, kTgF32>(s, A, a_mn, B, b_mn, a, grid_cap);
+        else if (A.dt == kTgF16) dispatch_major<BNc, kTgF16>(s, A, a_mn, B, b_mn, a, grid_cap);
+        else dispatch_major<BNc, kTgBF16>(s, A, a_mn, B, b_mn, a, grid_cap);
+    };
+    if (bn == 64) go(std::integral_constant<int, 64>{});
+    else if (bn == 128) go(std::integral_constant<int, 128>{});
+    else go(std::integral_constant<int, 256>{});
 }
 
 }  // namespace flw
 
 // ---------------------------------------------------------------------------- self-test (C-ABI)
 // D = op(A) op(B) through tgemm with the f32 partial epilogue; the K splits are summed here.
-// a_mn: A given as [K, M] (else [M, K]); b_mn: B given as [K, N] (else [N, K]). tf32: operands
-// stay f32 (kind::tf32), else they are rounded to bf16 (kind::f16).
+// a_mn: A given as [K, M] (else [M, K]); b_mn: B given as [K, N] (else [N, K]). tf32: 1 operands
+// stay f32 (kind::tf32), 2 rounded to f16, 0 rounded to bf16 (kind::f16).
 extern "C" int flw_selftest_tgemm(int64_t M, int64_t N, int64_t K, int a_mn, int b_mn, int tf32, int splits, int bn,
                                   const float* A, const float* B, float* D) {
     using namespace flw;
     try {
         const int64_t ar = a_mn ? K : M, ac = a_mn ? M : K, br = b_mn ? K : N, bc = b_mn ? N : K;
-        const int esz = tf32 ? 4 : 2;
+        const int dt = tf32 == 1 ? kTgF32 : (tf32 == 2 ? kTgF16 : kTgBF16);
+        const int esz = dt == kTgF32 ? 4 : 2;
         const int64_t ald = (ac * esz + 15) / 16 * 16 / esz, bld = (bc * esz + 15) / 16 * 16 / esz;
         std::vector<uint8_t> ha(static_cast<size_t>(ar * ald * esz), 0), hb(static_cast<size_t>(br * bld * esz), 0);
         for (int64_t r = 0; r < ar; ++r)
             for (int64_t c = 0; c < ac; ++c) {
-                if (tf32) reinterpret_cast<float*>(ha.data())[r * ald + c] = A[r * ac + c];
+                if (dt == kTgF32) reinterpret_cast<float*>(ha.data())[r * ald + c] = A[r * ac + c];
+                else if (dt == kTgF16) reinterpret_cast<__half*>(ha.data())[r * ald + c] = __float2half_rn(A[r * ac + c]);
                 else reinterpret_cast<__nv_bfloat16*>(ha.data())[r * ald + c] = __float2bfloat16(A[r * ac + c]);
             }
         for (int64_t r = 0; r < br; ++r)
             for (int64_t c = 0; c < bc; ++c) {
-                if (tf32) reinterpret_cast<float*>(hb.data())[r * bld + c] = B[r * bc + c];
+                if (dt == kTgF32) reinterpret_cast<float*>(hb.data())[r * bld + c] = B[r * bc + c];
+                else if (dt == kTgF16) reinterpret_cast<__half*>(hb.data())[r * bld + c] = __float2half_rn(B[r * bc + c]);
                 else reinterpret_cast<__nv_bfloat16*>(hb.data())[r * bld + c] = __float2bfloat16(B[r * bc + c]);
             }
         void *da = nullptr, *db = nullptr;
         float* dd = nullptr;
-        const int BK = tf32 ? 32 : 64;
+        const int BK = dt == kTgF32 ? 32 : 64;
         const int sp = std::max(1, std::min<int>(splits, static_cast<int>((K + BK - 1) / BK)));
         FLW_CUDA(cudaMalloc(&da, ha.size()));
         FLW_CUDA(cudaMalloc(&db, hb.size()));
@@ -482,7 +532,7 @@ extern "C" int flw_selftest_tgemm(int64_t M, int64_t N, int64_t K, int a_mn, int
         e.c32 = dd;
         e.ldc32 = N;
         e.split_stride = M * N;
-        tgemm(nullptr, TgOperand{da, ar, ac, ald, tf32 != 0}, a_mn != 0, TgOperand{db, br, bc, bld, tf32 != 0}, b_mn != 0,
+        tgemm(nullptr, TgOperand{da, ar, ac, ald, dt}, a_mn != 0, TgOperand{db, br, bc, bld, dt}, b_mn != 0,
               M, N, K, sp, e, bn);
         std::vector<float> part(static_cast<size_t>(sp * M * N));
         FLW_CUDA(cudaDeviceSynchronize());

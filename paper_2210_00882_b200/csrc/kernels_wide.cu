@@ -42,6 +42,36 @@ __global__ void k_wide_to_bf16(const float* __restrict__ x, int64_t rows, int co
     }
 }
 
+__global__ void k_wide_split_input(const float* __restrict__ x, int64_t rows, int cols, __half* out, int64_t seg) {
+    const int64_t n = rows * cols;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / cols, c = i % cols;
+        const float v = x[i];
+        const __half hi = __float2half_rn(v);
+        __half* o = out + r * 3 * seg + c;
+        o[0] = hi;
+        o[seg] = __float2half_rn(v - __half2float(hi));
+        o[2 * seg] = hi;
+    }
+}
+
+__global__ void k_wide_split_weights(const float* __restrict__ params, WideNet n, __half* ws) {
+    for (int l = 0; l < n.L; ++l) {
+        const int64_t cnt = static_cast<int64_t>(n.din[l]) * n.dout[l];
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < cnt;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int64_t r = i / n.dout[l], c = i % n.dout[l];
+            const float w = params[n.woff[l] + i];
+            const __half hi = __float2half_rn(w);
+            __half* o = ws + n.sofs[l] + r * n.wld[l] + c;
+            o[0] = hi;                                                        // x_hi . W_hi
+            o[n.dp[l] * n.wld[l]] = hi;                                       // x_lo . W_hi
+            o[2 * n.dp[l] * n.wld[l]] = __float2half_rn(w - __half2float(hi));  // x_hi . W_lo
+        }
+    }
+}
+
 // One row per thread: the loss terms of rl.cpp:137-202 in f32 (the fused kernel's loss epilogue)
 // and dZ_{L-1} rounded to the bf16 operand the backward GEMMs read. Per-block sums of the
 // policy / value / entropy terms in a fixed order (block-local tree), one slot per block.
@@ -194,6 +224,16 @@ void wide_to_bf16(cudaStream_t s, const float* x, int64_t rows, int cols, __nv_b
     const int64_t n = rows * cols;
     const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
     k_wide_to_bf16<<<blocks, 256, 0, s>>>(x, rows, cols, out, ld);
+}
+
+void wide_split_input(cudaStream_t s, const float* x, int64_t rows, int cols, __half* out, int64_t seg) {
+    const int64_t n = rows * cols;
+    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+    k_wide_split_input<<<blocks, 256, 0, s>>>(x, rows, cols, out, seg);
+}
+
+void wide_build_split_weights(cudaStream_t s, const float* params, const WideNet& n, __half* ws) {
+    k_wide_split_weights<<<64, 256, 0, s>>>(params, n, ws);
 }
 
 int wide_loss_blocks(int64_t rows) { return static_cast<int>(std::min<int64_t>(74, (rows + 255) / 256)); }

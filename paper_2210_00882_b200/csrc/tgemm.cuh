@@ -16,22 +16,27 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace flw {
+
+enum TgType : int { kTgBF16 = 0, kTgF16 = 1, kTgF32 = 2 };  // f32 operands are read as tf32
 
 enum TgEpi : int {
     kTgStoreF32 = 0,    // C32[m, n] = acc (split s at C32 + s * split_stride): split-K partials
     kTgBiasAct = 1,     // C16[m, n] = bf16(act(acc + bias[n])) (and C32 if set)
     kTgBias = 2,        // C32[m, n] = acc + bias[n]
     kTgActGrad = 3,     // C16[m, n] = bf16(acc * act'(H[m, n])), H bf16 (act' from the output)
+    kTgSplit3 = 4,      // y = act(acc + bias[n]) (accurate tanhf), written as f16 hi | lo | hi
+                        // (y = hi + lo): the next layer's A operand of the split f32-accurate GEMM
 };
 
 struct TgOperand {
     const void* ptr;
     int64_t rows, cols, ld;  // storage [rows, cols] row-major, ld in elements (ld * esz % 16 == 0)
-    bool f32;                // f32 (tf32 MMA) or bf16
+    int dt;                  // TgType
 };
 
 struct TgEpilogue {
@@ -46,6 +51,8 @@ struct TgEpilogue {
     const __nv_bfloat16* h = nullptr;   // kTgActGrad: activation whose derivative scales acc
     int64_t ldh = 0;
     int64_t m_store = -1, n_store = -1; // stored extent (default M, N)
+    __half* c16h = nullptr;             // kTgSplit3: [m, seg*k + n] for the segments hi, lo, hi
+    int64_t seg = 0;
 };
 
 // D = op(A) op(B) with K split `splits` ways (kTgStoreF32 only for splits > 1). bn: 64, 128 or

@@ -34,9 +34,12 @@ def _run(M, N, K, a_mn, b_mn, tf32, splits, bn, seed=0):
     assert rc == 0
     Am = A.T if a_mn else A
     Bm = B if b_mn else B.T
-    if tf32:
+    if tf32 == 1:
         want = Am.astype(np.float64) @ Bm.astype(np.float64)
         tol = 2e-3  # tf32 operands (10-bit mantissa)
+    elif tf32 == 2:
+        want = Am.astype(np.float16).astype(np.float64) @ Bm.astype(np.float16).astype(np.float64)
+        tol = 1e-5  # exact f16 products, f32 accumulation
     else:
         want = _bf16(Am) @ _bf16(Bm)
         tol = 1e-5  # exact bf16 products, f32 accumulation
@@ -51,10 +54,10 @@ def _need_gpu():
 
 @pytest.mark.parametrize("a_mn", [0, 1])
 @pytest.mark.parametrize("b_mn", [0, 1])
-@pytest.mark.parametrize("tf32", [0, 1])
+@pytest.mark.parametrize("tf32", [0, 1, 2])  # bf16, tf32, f16
 def test_tgemm_majors(a_mn, b_mn, tf32):
     _need_gpu()
-    if tf32 and (a_mn or b_mn):
+    if tf32 == 1 and (a_mn or b_mn):
         pytest.skip("tf32 operands are K-major only (32-bit MN-major needs the BASE32B swizzle)")
     for (M, N, K, bn, splits) in [(128, 64, 64, 64, 1), (256, 128, 192, 128, 1), (300, 200, 130, 256, 1),
                                   (130, 70, 1000, 64, 3)]:

@@ -92,3 +92,35 @@ def test_wide_episodes_deterministic_and_learn():
     np.testing.assert_array_equal(a.params(), b.params())
     np.testing.assert_array_equal(a.params(), c.params())
     assert np.abs(a.params() - p0).max() > 1e-4
+
+
+def test_wide_rollout_teacher_forced():
+    """The wide policy's rollout (f32-accurate split-f16 GEMMs, K = hi | lo | hi) against the
+    exact one at H=256 on the C2 shape, the exact engine's state fed in before every step:
+    logp within 1e-5 relative where the sampled action agrees, flips <= 1e-3, env outputs equal."""
+    _need_gpu()
+    from paper_2210_00882_b200 import DpdEngine
+
+    algo = _algo(4096, 256)
+    ex = DpdEngine(algo, seed=5, numerics="exact")
+    fa = DpdEngine(algo, seed=5, numerics="fast")
+    ex.reset(0)
+    fa.reset(0)
+    flips = total = 0
+    worst = 0.0
+    for st in range(32):
+        fa.set("state_in", ex.get("state_in"))
+        fa.set("env_full", ex.get("env_full"))
+        ex.step(0, st)
+        fa.step(0, st)
+        pe, pf = ex.get("pa").reshape(-1, 2), fa.get("pa").reshape(-1, 2)
+        same = pe[:, 0] == pf[:, 0]
+        flips += int((~same).sum())
+        total += same.size
+        rel = np.abs(pf[same, 1] - pe[same, 1]) / np.maximum(np.abs(pe[same, 1]), 1e-6)
+        worst = max(worst, float(rel.max()))
+        ee, ef = ex.get("envstep").reshape(pe.shape[0], -1), fa.get("envstep").reshape(pe.shape[0], -1)
+        np.testing.assert_array_equal(ef[same], ee[same])
+    print(f"wide rollout H=256: flips {flips}/{total}, worst logp rel {worst:.2e}")
+    assert worst <= 1e-5
+    assert flips <= 1e-3 * total

@@ -10,7 +10,6 @@
 //   params  f32 [P], m/v f64 [P], grads f32 [P]   flat, reference parameter order
 #include "engine.hpp"
 
-#include <cublas_v2.h>
 
 #include <cmath>
 #include <cstddef>
@@ -67,8 +66,10 @@ struct Engine::Bufs {
     double* cprefix = nullptr;  // MAPPO compact critic: joint prefix chains [(T+1)*E, H0]
     // fast MAPPO compact critic (n > 4): joint GEMM, layer-0 rows, input gradients, per-env sums
     float *h0 = nullptr, *cP = nullptr, *dz0 = nullptr, *cS = nullptr, *cpart = nullptr;
-    cublasHandle_t blas = nullptr;
-    uint8_t* blas_ws = nullptr;
+    __nv_bfloat16 *jb = nullptr, *wjb = nullptr, *Sb = nullptr;  // bf16 joint rows, W_J, S
+    float* jpart = nullptr;                                        // dW_J split-K partials
+    int64_t jld = 0, hld0 = 0;
+    int jsplits = 1;
     // fast numerics
     FastNet pol{}, crit{};
     int grid = 0;                       // persistent CTAs of the fused learn kernel
@@ -116,17 +117,9 @@ struct Engine::Bufs {
         return static_cast<T*>(p);
     }
     ~Bufs() {
-        if (blas) cublasDestroy(blas);
         for (void* p : owned) cudaFree(p);
     }
 };
-
-#define FLW_CUBLAS(x)                                                                          \
-    do {                                                                                       \
-        cublasStatus_t st_ = (x);                                                              \
-        if (st_ != CUBLAS_STATUS_SUCCESS)                                                      \
-            throw ::flw::Error(::flw::Errc::Runtime, "cuBLAS error " + std::to_string(st_));  \
-    } while (0)
 
 namespace {
 
@@ -155,8 +148,13 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     mappo_ = shape_.algo == Algo::Mappo;
     if (mappo_ && shape_.env != EnvKind::SpreadLite)
         fail(Errc::PolicyInapplicable, "MAPPO runs on spread_lite (the reference's multi-agent env)");
-    if (mappo_ && numerics == Numerics::Fast && shape_.obs_dim > 64)
-        fail(Errc::Config, "fast MAPPO needs per-agent observations <= 64 wide (n <= 31); use numerics=exact");
+    // fast MAPPO with a policy wider than the fused kernel (per-agent observation 2 + 2n > 64,
+    // i.e. n > 31 agents, or hidden > 64): the policy learns on the layer-wise GEMM path
+    if (mappo_ && numerics == Numerics::Fast) {
+        bool w = shape_.obs_dim > 64;
+        for (int l = 1; l < shape_.L; ++l) w = w || shape_.pdims[l] > 64;
+        pwide_ = w;
+    }
     // fast MAPPO with a critic input wider than the fused kernel's 64 columns (n > 4): the
     // compact critic - layer 0 as a joint GEMM once per env + W[J+a], the rest fused
     cfast_ = mappo_ && numerics == Numerics::Fast && shape_.crit_in > 64;
@@ -406,6 +404,7 @@ void Engine::alloc() {
         }
     }
     if (numerics_ == Numerics::Fast && wide_) {
+        gemm_roll_ = true;
         alloc_wide();
         return;
     }
@@ -429,7 +428,19 @@ void Engine::alloc() {
             return n;
         };
         if (L > kMaxLayers) fail(Errc::Config, "fast numerics supports at most 8 layers");
-        b.pol = make_net(0);
+        {  // MAPPO policies the fused rollout kernel cannot hold roll out on split GEMMs
+            FastRolloutArgs ra{};
+            ra.L = L;
+            for (int l = 0; l <= L; ++l) ra.dims[l] = s.pdims[l];
+            ra.S = S;
+            ra.A = A;
+            ra.env = env_params(cfg_, shape_, nullptr);
+            gemm_roll_ = mappo_ && !fast_rollout_mappo_ok(ra);
+        }
+        if (gemm_roll_ || pwide_) setup_wide_net(0, b.wpol);
+        if (gemm_roll_) alloc_split_rollout();
+        if (pwide_) alloc_wide_policy(TR_, 1);
+        b.pol = pwide_ ? FastNet{} : make_net(0);
         if (cfast_) {
             if (L < 2 || s.cdims[1] > 64 || s.cdims[1] % 4 != 0)
                 fail(Errc::Config, "compact fast critic needs >= 2 layers, hidden <= 64 and a multiple of 4");
@@ -440,10 +451,17 @@ void Engine::alloc() {
             b.dz0 = b.alloc<float>(TR_ * H0);
             b.cS = b.alloc<float>(T_ * E_ * H0);
             b.cpart = b.alloc<float>(T_ * s.n_agents * H0);
-            FLW_CUBLAS(cublasCreate(&b.blas));
-            FLW_CUBLAS(cublasSetMathMode(b.blas, CUBLAS_TF32_TENSOR_OP_MATH));
-            b.blas_ws = b.alloc<uint8_t>(32 << 20);
-            FLW_CUBLAS(cublasSetWorkspace(b.blas, b.blas_ws, 32 << 20));
+            // the joint GEMMs (P = joint . W_J, dW_J = joint^T . S) on tcgen05 (kernels_tgemm.cu):
+            // bf16 copies of the joint rows, W_J and S, split-K partials of dW_J
+            const int J = s.state_w;
+            b.jld = (J + 7) / 8 * 8;
+            b.hld0 = (H0 + 7) / 8 * 8;
+            b.jb = b.alloc<__nv_bfloat16>((T_ + 1) * E_ * b.jld);
+            b.wjb = b.alloc<__nv_bfloat16>(static_cast<int64_t>(J) * b.hld0);
+            b.Sb = b.alloc<__nv_bfloat16>(T_ * E_ * b.hld0);
+            const int64_t mt = (J + 127) / 128, kb = (T_ * E_ + 63) / 64;
+            b.jsplits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kb, 148 / mt)));
+            b.jpart = b.alloc<float>(static_cast<int64_t>(b.jsplits) * J * H0);
         } else {
             b.crit = make_net(1);
         }
@@ -451,9 +469,9 @@ void Engine::alloc() {
         FLW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
         b.grid = static_cast<int>(std::min<int64_t>(sms, (TR_ + 127) / 128));
         // rows padded to 4 floats: the fused update reads them as float4
-        b.part_p = b.alloc<float>(static_cast<int64_t>(b.grid) * ((s.P_policy + 3) / 4 * 4));
+        b.part_p = b.alloc<float>(static_cast<int64_t>(std::max(b.grid, b.wsplits)) * ((s.P_policy + 3) / 4 * 4));
         b.part_c = b.alloc<float>(static_cast<int64_t>(b.grid) * ((s.P - s.P_policy + 3) / 4 * 4));
-        b.loss_parts = b.alloc<float>(2 * 3 * b.grid);
+        b.loss_parts = b.alloc<float>(3 * (2 * b.grid + wide_loss_blocks(TR_)));
         b.wimg_p = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.pol) / 2));
         b.wimg_c = b.alloc<__nv_bfloat16>(static_cast<int64_t>(fast_wimg_bytes(b.crit) / 2));
         b.hsave = b.alloc<uint8_t>(static_cast<int64_t>(fast_hsave_bytes(b.crit)) * ((TR_ + 127) / 128));
@@ -709,18 +727,21 @@ bool Engine::enq_rollout_fast_mappo(int64_t step0, int64_t nsteps) {
 
 void Engine::enq_step(int64_t st) {
     if (numerics_ == Numerics::Fast && !mappo_ && !wide_) return enq_rollout_fast(st, 1);
-    if (numerics_ == Numerics::Fast && wide_) return enq_step_wide(st);
-    if (numerics_ == Numerics::Fast && mappo_ && enq_rollout_fast_mappo(st, 1)) return;
+    if (numerics_ == Numerics::Fast && mappo_ && !gemm_roll_ && enq_rollout_fast_mappo(st, 1)) return;
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions;
-    const float* in = b.states + st * R_ * S;
-    float* bufs[2] = {b.act0, b.act1};
-    for (int l = 0; l < s.L; ++l) {
-        float* out = l + 1 == s.L ? b.logits : bufs[l & 1];
-        exact_layer_fwd(stream_, in, b.params + s.woff[0][l], b.params + s.boff[0][l], out, R_, s.pdims[l],
-                        s.pdims[l + 1], l + 1 < s.L ? act_of(cfg_) : kNone);
-        in = out;
+    if (gemm_roll_) {
+        enq_policy_fwd_split(st);  // f32-accurate tensor-core policy forward -> b.logits
+    } else {
+        const float* in = b.states + st * R_ * S;
+        float* bufs[2] = {b.act0, b.act1};
+        for (int l = 0; l < s.L; ++l) {
+            float* out = l + 1 == s.L ? b.logits : bufs[l & 1];
+            exact_layer_fwd(stream_, in, b.params + s.woff[0][l], b.params + s.boff[0][l], out, R_, s.pdims[l],
+                            s.pdims[l + 1], l + 1 < s.L ? act_of(cfg_) : kNone);
+            in = out;
+        }
     }
     if (mappo_) {
         MappoStepArgs m{};
@@ -807,11 +828,15 @@ void Engine::enq_learn_fast() {
     // the compact critic's layer-0 activations (MAPPO, n > 4)
     const int H0 = s.cdims[1], J = s.state_w;
     if (cfast_) {
-        // P[(T+1)*E, H0] = joint . W_J  (row-major; cuBLAS column-major: P^T = W_J^T . joint^T)
-        const float one = 1.0f, zero = 0.0f;
-        FLW_CUBLAS(cublasSetStream(b.blas, stream_));
-        FLW_CUBLAS(cublasSgemm(b.blas, CUBLAS_OP_N, CUBLAS_OP_N, H0, static_cast<int>((T_ + 1) * E_), J, &one,
-                               b.params + s.woff[1][0], H0, b.joint, J, &zero, b.cP, H0));
+        // P[(T+1)*E, H0] = joint . W_J on the tensor cores (bf16 operands, f32 accumulation)
+        wide_to_bf16(stream_, b.joint, (T_ + 1) * E_, J, b.jb, b.jld);
+        wide_to_bf16(stream_, b.params + s.woff[1][0], J, H0, b.wjb, b.hld0);
+        TgEpilogue pe;
+        pe.mode = kTgStoreF32;
+        pe.c32 = b.cP;
+        pe.ldc32 = H0;
+        tgemm(stream_, TgOperand{b.jb, (T_ + 1) * E_, J, b.jld, kTgBF16}, false, TgOperand{b.wjb, J, H0, b.hld0, kTgBF16},
+              true, (T_ + 1) * E_, H0, J, 1, pe, 64);
         mappo_fast_h0(stream_, b.cP, b.params + s.woff[1][0], b.params + s.boff[1][0], T_ + 1, E_, s.n_agents, J, H0,
                       act_of(cfg_), b.h0);
     }
@@ -873,7 +898,8 @@ void Engine::enq_learn_fast() {
     // SMs split in proportion to their per-tile cost (the critic skips its forward), so both
     // finish together instead of each paying its own tail.
     int gp = lgrid, gc = lgrid;
-    const bool concurrent = hreuse && lgrid >= 8;  // the critic reads hsave, not hscratch
+    // (a layer-wise policy runs after the critic on the whole GPU)
+    const bool concurrent = hreuse && lgrid >= 8 && !pwide_;  // the critic reads hsave, not hscratch
     if (concurrent) {
         // measured: 70/30 for PPO / MAPPO with the direct critic; the compact critic's extra
         // input-gradient stage makes its kernel heavier: 60/40
@@ -885,9 +911,12 @@ void Engine::enq_learn_fast() {
         FLW_CUDA(cudaStreamWaitEvent(side2_, ev_lfork_, 0));
     }
     f.loss_partials = b.loss_parts;
-    probe_begin("learn_policy");
-    launch(gp);
-    probe_end();
+    const int np_loss = pwide_ ? wide_loss_blocks(TR_) : gp;  // policy loss-partial slots
+    if (!pwide_) {
+        probe_begin("learn_policy");
+        launch(gp);
+        probe_end();
+    }
     FastLearnArgs fc = f;
     fc.X = Xc;
     fc.in_cols = Cin;
@@ -901,7 +930,7 @@ void Engine::enq_learn_fast() {
     const int64_t c_off = cfast_ ? static_cast<int64_t>(J + s.n_agents) * H0 + H0 : 0;
     fc.part_stride = padded ? (s.P - s.P_policy + 3) / 4 * 4 : s.P - s.P_policy - c_off;
     fc.dx_out = cfast_ ? b.dz0 : nullptr;
-    fc.loss_partials = b.loss_parts + 3 * gp;
+    fc.loss_partials = b.loss_parts + 3 * np_loss;
     if (concurrent) {
         fast_learn(side2_, fc, gc);
         FLW_CUDA(cudaEventRecord(ev_ljoin_, side2_));
@@ -911,30 +940,43 @@ void Engine::enq_learn_fast() {
         fast_learn(stream_, fc, gc);
         probe_end();
     }
-    b.lgrid_p = gp;
+    if (pwide_) {
+        probe_begin("learn_policy");
+        enq_learn_policy_wide(b.loss_parts);
+        probe_end();
+    }
+    b.lgrid_p = pwide_ ? np_loss : gp;
     b.lgrid_c = gc;
     if (!p2p_enabled() && !fused_pending_) {  // with peer-memory exchange the reduction is fused into the exchange
         probe_begin("reduce");
-        fast_reduce_partials(stream_, b.part_p, b.part_c, gp, gc, s.P_policy, s.P - s.P_policy - c_off, b.grads,
-                             c_off);
+        fast_reduce_partials(stream_, b.part_p, b.part_c, pwide_ ? b.wsplits : gp, gc, s.P_policy,
+                             s.P - s.P_policy - c_off, b.grads, c_off);
         probe_end();
     }
-    if (cfast_) {  // critic layer-0 gradients: one-hot rows, bias, and dW_J = joint^T . S (cuBLAS)
+    if (cfast_) {  // critic layer-0 gradients: one-hot rows, bias, and dW_J = joint^T . S
         float* g0 = b.grads + s.woff[1][0];
         mappo_fast_layer0_grads(stream_, b.dz0, T_, E_, s.n_agents, H0, b.cS, b.cpart,
                                 g0 + static_cast<int64_t>(J) * H0, b.grads + s.boff[1][0]);
-        const float one = 1.0f, zero = 0.0f;
-        FLW_CUBLAS(cublasSgemm(b.blas, CUBLAS_OP_N, CUBLAS_OP_T, H0, J, static_cast<int>(T_ * E_), &one, b.cS, H0,
-                               b.joint, J, &zero, g0, H0));
+        // dW_J = joint^T . S over the T*E trajectory envs: split-K tcgen05 GEMM + fixed-order sum
+        wide_to_bf16(stream_, b.cS, T_ * E_, H0, b.Sb, b.hld0);
+        TgEpilogue we;
+        we.mode = kTgStoreF32;
+        we.c32 = b.jpart;
+        we.ldc32 = H0;
+        we.split_stride = static_cast<int64_t>(J) * H0;
+        tgemm(stream_, TgOperand{b.jb, T_ * E_, J, b.jld, kTgBF16}, true, TgOperand{b.Sb, T_ * E_, H0, b.hld0, kTgBF16},
+              true, J, H0, T_ * E_, b.jsplits, we, 64);
+        wide_sum_partials(stream_, b.jpart, b.jsplits, static_cast<int64_t>(J) * H0, g0);
     }
     // the scalar loss is not an input of anything downstream: reduced on demand (read_tensor)
 }
 
-// Fast numerics, wide policy: one rollout step. The policy MLP runs as f32-accurate split
-// GEMMs on the tensor cores (x = hi + lo, W = hi + lo in f16; x.W ~ hi.hi + lo.hi + hi.lo with
-// f32 accumulation, one GEMM with K = 3 segments per layer; tanh in f32), then the reference's
-// PolicyApply + env step (the exact step kernel on the f32 logits).
-void Engine::enq_step_wide(int64_t st) {
+// Fast numerics, policy forward of one rollout step as f32-accurate split GEMMs on the tensor
+// cores (x = hi + lo, W = hi + lo in f16; x.W ~ hi.hi + lo.hi + hi.lo with f32 accumulation, one
+// GEMM with K = 3 segments per layer; tanh in f32) into the f32 logits b.logits; the reference's
+// PolicyApply + env step follow (enq_step). Used when the fused rollout kernel does not fit the
+// policy (hidden > 64, or MAPPO with n > 16 agents).
+void Engine::enq_policy_fwd_split(int64_t st) {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int L = s.L, S = s.obs_dim;
@@ -968,69 +1010,87 @@ void Engine::enq_step_wide(int64_t st) {
             inld = 3 * n.dp[l + 1];
         }
     }
-    enq_step_env(st);
+}
+
+void Engine::setup_wide_net(int net, WideNet& n) const {
+    const ProgramShape& s = shape_;
+    const auto& d = net == 0 ? s.pdims : s.cdims;
+    const int L = s.L;
+    if (L > kMaxLayers) fail(Errc::Config, "fast numerics supports at most 8 layers");
+    auto pad8 = [](int64_t x) { return (x + 7) / 8 * 8; };
+    n = WideNet{};
+    n.L = L;
+    int64_t off = 0, so = 0;
+    for (int l = 0; l < L; ++l) {
+        n.din[l] = d[l];
+        n.dout[l] = d[l + 1];
+        n.woff[l] = s.woff[net][l];
+        n.boff[l] = s.boff[net][l];
+        n.wofs[l] = off;
+        n.wld[l] = pad8(d[l + 1]);
+        off += (static_cast<int64_t>(d[l]) * n.wld[l] + 7) / 8 * 8;  // 16-byte aligned layers
+        n.dp[l] = (d[l] + 63) / 64 * 64;
+        n.sofs[l] = so;
+        so += 3 * n.dp[l] * n.wld[l];
+    }
+    n.wbytes = off;
+    n.sbytes = so;
+}
+
+// split-GEMM rollout buffers of the policy (R_ rows per step; pad columns stay zero)
+void Engine::alloc_split_rollout() {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    int64_t maxh = 64;
+    for (int l = 1; l < s.L; ++l) maxh = std::max<int64_t>(maxh, (s.pdims[l] + 63) / 64 * 64);
+    b.wr_ldx = 3 * b.wpol.dp[0];
+    b.wr_ldh = 3 * maxh;
+    b.wr_x = b.alloc<__half>(R_ * b.wr_ldx);
+    b.wr_h0 = b.alloc<__half>(R_ * b.wr_ldh);
+    b.wr_h1 = b.alloc<__half>(R_ * b.wr_ldh);
+    b.wr_w = b.alloc<__half>(b.wpol.sbytes);
+}
+
+// layer-wise learn buffers of the policy: bf16 weights, input rows, hidden activations, dZ
+// ping-pong (sized for `maxw` columns), outputs, split-K partial slots
+void Engine::alloc_wide_policy(int64_t xrows, int maxw) {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    auto pad8 = [](int64_t x) { return (x + 7) / 8 * 8; };
+    b.wb_p = b.alloc<__nv_bfloat16>(b.wpol.wbytes);
+    b.xld = pad8(s.obs_dim);
+    b.xb = b.alloc<__nv_bfloat16>(xrows * b.xld);
+    for (int l = 0; l + 1 < s.L; ++l) {
+        b.hld_p.push_back(pad8(s.pdims[l + 1]));
+        b.hw_p.push_back(b.alloc<__nv_bfloat16>(TR_ * b.hld_p.back()));
+    }
+    for (int l = 0; l <= s.L; ++l) maxw = std::max(maxw, s.pdims[l]);
+    b.dzld = pad8(maxw);
+    b.wdz0 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
+    b.wdz1 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
+    b.wlogits = b.alloc<float>(TR_ * s.n_actions);
+    b.wsplits = static_cast<int>(std::min<int64_t>(64, (TR_ + 63) / 64));  // = tgemm's clamp
 }
 
 void Engine::alloc_wide() {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const int L = s.L;
-    if (L > kMaxLayers) fail(Errc::Config, "fast numerics supports at most 8 layers");
     auto pad8 = [](int64_t x) { return (x + 7) / 8 * 8; };
-    auto make = [&](int net, WideNet& n) {
-        const auto& d = net == 0 ? s.pdims : s.cdims;
-        n.L = L;
-        int64_t off = 0;
-        for (int l = 0; l < L; ++l) {
-            n.din[l] = d[l];
-            n.dout[l] = d[l + 1];
-            n.woff[l] = s.woff[net][l];
-            n.boff[l] = s.boff[net][l];
-            n.wofs[l] = off;
-            n.wld[l] = pad8(d[l + 1]);
-            off += (static_cast<int64_t>(d[l]) * n.wld[l] + 7) / 8 * 8;  // 16-byte aligned layers
-        }
-        n.wbytes = off;
-        int64_t so = 0;
-        for (int l = 0; l < L; ++l) {
-            n.dp[l] = (d[l] + 63) / 64 * 64;
-            n.sofs[l] = so;
-            so += 3 * n.dp[l] * n.wld[l];
-        }
-        n.sbytes = so;
-    };
-    make(0, b.wpol);
-    make(1, b.wcrit);
-    b.wb_p = b.alloc<__nv_bfloat16>(b.wpol.wbytes);
-    b.wb_c = b.alloc<__nv_bfloat16>(b.wcrit.wbytes);
+    setup_wide_net(0, b.wpol);
+    setup_wide_net(1, b.wcrit);
     const int64_t Rc = TR_ + R_;
-    b.xld = pad8(s.obs_dim);
-    b.xb = b.alloc<__nv_bfloat16>(Rc * b.xld);
     int maxw = 1;
+    for (int l = 0; l <= L; ++l) maxw = std::max(maxw, s.cdims[l]);
+    alloc_wide_policy(Rc, maxw);  // the critic reads the same input rows (+ last_next)
+    b.wb_c = b.alloc<__nv_bfloat16>(b.wcrit.wbytes);
     for (int l = 0; l + 1 < L; ++l) {
-        b.hld_p.push_back(pad8(s.pdims[l + 1]));
         b.hld_c.push_back(pad8(s.cdims[l + 1]));
-        b.hw_p.push_back(b.alloc<__nv_bfloat16>(TR_ * b.hld_p.back()));
         b.hw_c.push_back(b.alloc<__nv_bfloat16>(Rc * b.hld_c.back()));
     }
-    for (int l = 0; l <= L; ++l) maxw = std::max({maxw, s.pdims[l], s.cdims[l]});
-    b.dzld = pad8(maxw);
-    b.wdz0 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
-    b.wdz1 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
-    b.wlogits = b.alloc<float>(TR_ * s.n_actions);
-    {  // rollout: split operands of R_ rows (pad columns stay zero)
-        int64_t maxh = 64;
-        for (int l = 1; l < L; ++l) maxh = std::max<int64_t>(maxh, (s.pdims[l] + 63) / 64 * 64);
-        b.wr_ldx = 3 * b.wpol.dp[0];
-        b.wr_ldh = 3 * maxh;
-        b.wr_x = b.alloc<__half>(R_ * b.wr_ldx);
-        b.wr_h0 = b.alloc<__half>(R_ * b.wr_ldh);
-        b.wr_h1 = b.alloc<__half>(R_ * b.wr_ldh);
-        b.wr_w = b.alloc<__half>(b.wpol.sbytes);
-    }
+    alloc_split_rollout();
     b.values = b.alloc<float>(Rc);  // values | last_value: one critic forward over all rows
     b.last_value = b.values + TR_;
-    b.wsplits = static_cast<int>(std::min<int64_t>(64, (TR_ + 63) / 64));  // = tgemm's clamp
     b.grid = b.wsplits;
     b.part_p = b.alloc<float>(static_cast<int64_t>(b.wsplits) * s.P_policy);
     b.part_c = b.alloc<float>(static_cast<int64_t>(b.wsplits) * (s.P - s.P_policy));
@@ -1039,6 +1099,103 @@ void Engine::alloc_wide() {
     b.gae_counter = b.alloc<unsigned>(1);
     b.upd_counter = b.alloc<unsigned>(1);
     b.rsum_scratch = b.alloc<double>(256);
+}
+
+// Layer-wise forward of one net over `rows` rows of b.xb: hidden activations to H (bf16), the
+// output layer to `out` (f32).
+void Engine::wide_forward(const WideNet& n, const __nv_bfloat16* wb, const std::vector<__nv_bfloat16*>& H,
+                          const std::vector<int64_t>& ld, int64_t rows, float* out) {
+    Bufs& b = *b_;
+    auto bn_for = [](int64_t x) { return x > 128 ? 256 : (x > 64 ? 128 : 64); };
+    for (int l = 0; l < n.L; ++l) {
+        const TgOperand A{l == 0 ? b.xb : H[l - 1], rows, n.din[l], l == 0 ? b.xld : ld[l - 1], kTgBF16};
+        const TgOperand B{wb + n.wofs[l], n.din[l], n.dout[l], n.wld[l], kTgBF16};
+        TgEpilogue e;
+        e.bias = b.params + n.boff[l];
+        if (l + 1 < n.L) {
+            e.mode = kTgBiasAct;
+            e.act = act_of(cfg_);
+            e.c16 = H[l];
+            e.ldc16 = ld[l];
+        } else {
+            e.mode = kTgBias;
+            e.c32 = out;
+            e.ldc32 = n.dout[l];
+        }
+        tgemm(stream_, A, false, B, true, rows, n.dout[l], n.din[l], 1, e, bn_for(n.dout[l]));
+    }
+}
+
+// Layer-wise backward over the TR_ trajectory rows from dZ_{L-1} in b.wdz0: per layer dW_m
+// (split-K partial slots, stride pstride) and db_m, then dZ_{m-1} = (dZ_m W_m^T) * act'(H_{m-1}).
+void Engine::wide_backward(const WideNet& n, const __nv_bfloat16* wb, const std::vector<__nv_bfloat16*>& H,
+                           const std::vector<int64_t>& ld, float* part, int64_t pstride) {
+    Bufs& b = *b_;
+    auto bn_for = [](int64_t x) { return x > 128 ? 256 : (x > 64 ? 128 : 64); };
+    const int splits = b.wsplits;
+    __nv_bfloat16 *dz = b.wdz0, *other = b.wdz1;
+    for (int m = n.L - 1; m >= 0; --m) {
+        const int din = n.din[m], dout = n.dout[m];
+        // dW_m = H_{m-1}^T dZ_m (K = rows split `splits` ways) -> partial slots
+        const TgOperand Hin{m == 0 ? b.xb : H[m - 1], TR_, din, m == 0 ? b.xld : ld[m - 1], kTgBF16};
+        const TgOperand Dz{dz, TR_, dout, b.dzld, kTgBF16};
+        TgEpilogue e;
+        e.mode = kTgStoreF32;
+        e.c32 = part + (n.woff[m] - n.woff[0]);
+        e.ldc32 = dout;
+        e.split_stride = pstride;
+        tgemm(stream_, Hin, true, Dz, true, din, dout, TR_, splits, e, bn_for(dout));
+        wide_colsum(stream_, dz, TR_, dout, b.dzld, splits, part + (n.boff[m] - n.woff[0]), pstride);
+        if (m == 0) break;
+        const TgOperand Wk{wb + n.wofs[m], din, dout, n.wld[m], kTgBF16};
+        TgEpilogue g;
+        g.mode = kTgActGrad;
+        g.act = act_of(cfg_);
+        g.h = H[m - 1];
+        g.ldh = ld[m - 1];
+        g.c16 = other;
+        g.ldc16 = b.dzld;
+        tgemm(stream_, Dz, false, Wk, false, TR_, din, dout, 1, g, bn_for(din));
+        std::swap(dz, other);
+    }
+}
+
+// PPO / A3C loss rows over the output layer (rl.cpp:137-202) -> dZ_{L-1} in b.wdz0
+void Engine::wide_loss_rows(int kind, const float* out, int A, float* loss_partials) {
+    Bufs& b = *b_;
+    WideLossArgs la{};
+    la.rows = TR_;
+    la.actions = b.actions;
+    la.logp_old = b.logp;
+    la.adv = b.adv;
+    la.ret = b.ret;
+    la.values_in = b.values;
+    la.adv_stats = (shape_.algo != Algo::A3c && cfg_.normalize_adv) ? b.stats : nullptr;
+    la.inv_n = 1.0 / static_cast<double>(TR_);
+    la.value_coef = cfg_.value_coef;
+    la.entropy_coef = cfg_.entropy_coef;
+    la.clip_eps = static_cast<float>(cfg_.clip_eps);
+    la.ld = b.dzld;
+    la.kind = kind;
+    la.out = out;
+    la.A = A;
+    la.width = A;
+    la.dz = b.wdz0;
+    la.loss_partials = loss_partials;
+    wide_loss(stream_, la);
+}
+
+// MAPPO with a policy wider than the fused kernel (n > 31 agents: per-agent observation
+// 2 + 2n > 64): the policy's train iteration on the layer-wise path, into part_p
+void Engine::enq_learn_policy_wide(float* loss_partials) {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    WideNet none{};
+    wide_build_weights(stream_, b.params, b.wpol, b.wb_p, none, nullptr);
+    wide_to_bf16(stream_, b.states, TR_, s.obs_dim, b.xb, b.xld);
+    wide_forward(b.wpol, b.wb_p, b.hw_p, b.hld_p, TR_, b.wlogits);
+    wide_loss_rows(s.algo != Algo::A3c ? kNetPolicyPpo : kNetPolicyA3c, b.wlogits, s.n_actions, loss_partials);
+    wide_backward(b.wpol, b.wb_p, b.hw_p, b.hld_p, b.part_p, s.P_policy);
 }
 
 // Fast numerics, widths > 64: one train iteration as layer-wise tcgen05 GEMMs (kernels_tgemm.cu)
@@ -1050,102 +1207,25 @@ void Engine::enq_learn_wide() {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     const bool ppo = s.algo != Algo::A3c;
-    const int L = s.L;
     const int64_t Rc = TR_ + R_;
-    const int act = act_of(cfg_);
     wide_build_weights(stream_, b.params, b.wpol, b.wb_p, b.wcrit, b.wb_c);
     wide_to_bf16(stream_, b.states, Rc, s.obs_dim, b.xb, b.xld);  // states blocks 0..T (last_next)
-    auto bn_for = [](int64_t n) { return n > 128 ? 256 : (n > 64 ? 128 : 64); };
-    auto forward = [&](const WideNet& n, const __nv_bfloat16* wb, const std::vector<__nv_bfloat16*>& H,
-                       const std::vector<int64_t>& ld, int64_t rows, float* out) {
-        for (int l = 0; l < L; ++l) {
-            const TgOperand A{l == 0 ? b.xb : H[l - 1], rows, n.din[l], l == 0 ? b.xld : ld[l - 1], kTgBF16};
-            const TgOperand B{wb + n.wofs[l], n.din[l], n.dout[l], n.wld[l], kTgBF16};
-            TgEpilogue e;
-            e.bias = b.params + n.boff[l];
-            if (l + 1 < L) {
-                e.mode = kTgBiasAct;
-                e.act = act;
-                e.c16 = H[l];
-                e.ldc16 = ld[l];
-            } else {
-                e.mode = kTgBias;
-                e.c32 = out;
-                e.ldc32 = n.dout[l];
-            }
-            tgemm(stream_, A, false, B, true, rows, n.dout[l], n.din[l], 1, e, bn_for(n.dout[l]));
-        }
-    };
-    const int splits = b.wsplits;
-    auto backward = [&](const WideNet& n, const __nv_bfloat16* wb, const std::vector<__nv_bfloat16*>& H,
-                        const std::vector<int64_t>& ld, float* part, int64_t pstride) {
-        __nv_bfloat16 *dz = b.wdz0, *other = b.wdz1;
-        for (int m = L - 1; m >= 0; --m) {
-            const int din = n.din[m], dout = n.dout[m];
-            // dW_m = H_{m-1}^T dZ_m (K = rows split `splits` ways) -> partial slots
-            const TgOperand Hin{m == 0 ? b.xb : H[m - 1], TR_, din, m == 0 ? b.xld : ld[m - 1], kTgBF16};
-            const TgOperand Dz{dz, TR_, dout, b.dzld, kTgBF16};
-            TgEpilogue e;
-            e.mode = kTgStoreF32;
-            e.c32 = part + (n.woff[m] - n.woff[0]);
-            e.ldc32 = dout;
-            e.split_stride = pstride;
-            tgemm(stream_, Hin, true, Dz, true, din, dout, TR_, splits, e, bn_for(dout));
-            wide_colsum(stream_, dz, TR_, dout, b.dzld, splits, part + (n.boff[m] - n.woff[0]), pstride);
-            if (m == 0) break;
-            // dZ_{m-1} = (dZ_m W_m^T) * act'(H_{m-1})
-            const TgOperand Wk{wb + n.wofs[m], din, dout, n.wld[m], kTgBF16};
-            TgEpilogue g;
-            g.mode = kTgActGrad;
-            g.act = act;
-            g.h = H[m - 1];
-            g.ldh = ld[m - 1];
-            g.c16 = other;
-            g.ldc16 = b.dzld;
-            tgemm(stream_, Dz, false, Wk, false, TR_, din, dout, 1, g, bn_for(din));
-            std::swap(dz, other);
-        }
-    };
     probe_begin("critic_fwd");
-    forward(b.wcrit, b.wb_c, b.hw_c, b.hld_c, Rc, b.values);
+    wide_forward(b.wcrit, b.wb_c, b.hw_c, b.hld_c, Rc, b.values);
     probe_end();
     probe_begin("gae");
     fast_gae(stream_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
              b.block_sums, b.stats, b.gae_counter);
     probe_end();
     probe_begin("learn_policy");
-    forward(b.wpol, b.wb_p, b.hw_p, b.hld_p, TR_, b.wlogits);
+    wide_forward(b.wpol, b.wb_p, b.hw_p, b.hld_p, TR_, b.wlogits);
     const int nlb = wide_loss_blocks(TR_);
-    WideLossArgs la{};
-    la.rows = TR_;
-    la.actions = b.actions;
-    la.logp_old = b.logp;
-    la.adv = b.adv;
-    la.ret = b.ret;
-    la.values_in = b.values;
-    la.adv_stats = (ppo && cfg_.normalize_adv) ? b.stats : nullptr;
-    la.inv_n = 1.0 / static_cast<double>(TR_);
-    la.value_coef = cfg_.value_coef;
-    la.entropy_coef = cfg_.entropy_coef;
-    la.clip_eps = static_cast<float>(cfg_.clip_eps);
-    la.ld = b.dzld;
-    la.kind = ppo ? kNetPolicyPpo : kNetPolicyA3c;
-    la.out = b.wlogits;
-    la.A = s.n_actions;
-    la.width = s.n_actions;
-    la.dz = b.wdz0;
-    la.loss_partials = b.loss_parts;
-    wide_loss(stream_, la);
-    backward(b.wpol, b.wb_p, b.hw_p, b.hld_p, b.part_p, s.P_policy);
-    la.kind = kNetCritic;
-    la.out = b.values;
-    la.A = 1;
-    la.width = 1;
-    la.loss_partials = b.loss_parts + 3 * nlb;
-    wide_loss(stream_, la);
-    backward(b.wcrit, b.wb_c, b.hw_c, b.hld_c, b.part_c, s.P - s.P_policy);
+    wide_loss_rows(ppo ? kNetPolicyPpo : kNetPolicyA3c, b.wlogits, s.n_actions, b.loss_parts);
+    wide_backward(b.wpol, b.wb_p, b.hw_p, b.hld_p, b.part_p, s.P_policy);
+    wide_loss_rows(kNetCritic, b.values, 1, b.loss_parts + 3 * nlb);
+    wide_backward(b.wcrit, b.wb_c, b.hw_c, b.hld_c, b.part_c, s.P - s.P_policy);
     b.lgrid_p = b.lgrid_c = nlb;
-    fast_reduce_partials(stream_, b.part_p, b.part_c, splits, splits, s.P_policy, s.P - s.P_policy, b.grads, 0);
+    fast_reduce_partials(stream_, b.part_p, b.part_c, b.wsplits, b.wsplits, s.P_policy, s.P - s.P_policy, b.grads, 0);
     probe_end();
 }
 
@@ -1412,8 +1492,8 @@ void Engine::build_graph() {
     probe_begin("rollout");
     if (numerics_ == Numerics::Fast && !mappo_ && !wide_)
         enq_rollout_fast(0, T_);
-    else if (!(numerics_ == Numerics::Fast && mappo_ && enq_rollout_fast_mappo(0, T_)))
-        for (int64_t st = 0; st < T_; ++st) enq_step(st);  // exact rollout
+    else if (!(numerics_ == Numerics::Fast && mappo_ && !gemm_roll_ && enq_rollout_fast_mappo(0, T_)))
+        for (int64_t st = 0; st < T_; ++st) enq_step(st);  // per-step rollout (exact or split GEMMs)
     probe_end();
     if (nrep_ > 1 && numerics_ == Numerics::Exact) enq_permute_replicas();
     FLW_CUDA(cudaEventRecord(ev_fork_, stream_));

@@ -5,6 +5,7 @@
 // reads back per-episode scalars.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -32,6 +33,7 @@ struct DeviceCtx {      // device-resident episode context (read by kernels insi
 };
 
 class Comm;  // NCCL gradient group (comm.hpp)
+struct WideNet;  // layer-wise learn path net description (wide.cuh)
 
 class Engine {
   public:
@@ -129,8 +131,17 @@ class Engine {
     bool enq_rollout_fast_mappo(int64_t step0, int64_t nsteps);
     void enq_learn_fast();
     void alloc_wide();
-    void enq_step_wide(int64_t st);
+    void setup_wide_net(int net, WideNet& n) const;
+    void alloc_split_rollout();
+    void alloc_wide_policy(int64_t xrows, int maxw);
+    void enq_policy_fwd_split(int64_t st);
     void enq_step_env(int64_t st);
+    void wide_forward(const WideNet& n, const __nv_bfloat16* wb, const std::vector<__nv_bfloat16*>& H,
+                      const std::vector<int64_t>& ld, int64_t rows, float* out);
+    void wide_backward(const WideNet& n, const __nv_bfloat16* wb, const std::vector<__nv_bfloat16*>& H,
+                       const std::vector<int64_t>& ld, float* part, int64_t pstride);
+    void wide_loss_rows(int kind, const float* out, int A, float* loss_partials);
+    void enq_learn_policy_wide(float* loss_partials);
     void enq_learn_wide();
     void enq_learn_grads();
     void enq_grad_sync_and_adam();
@@ -150,6 +161,8 @@ class Engine {
     bool mappo_ = false;   // agent-major rows R = n*E, critic on [joint obs | agent one-hot]
     bool cfast_ = false;   // fast MAPPO with the compact critic (critic input > 64 wide)
     bool wide_ = false;    // fast numerics, a layer > 64 wide: layer-wise tcgen05 GEMM learn path
+    bool pwide_ = false;   // fast MAPPO, policy wider than the fused kernel: layer-wise policy learn
+    bool gemm_roll_ = false;  // fast numerics: rollout policy forward as split-f16 GEMMs
     int p2p_rank_ = 0, p2p_k_ = 0;
     void* p2p_region_ptr_ = nullptr;
     int p2p_alloc_k_ = 0;

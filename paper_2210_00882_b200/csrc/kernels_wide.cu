@@ -213,7 +213,21 @@ __global__ void __launch_bounds__(256) k_wide_colsum(const __nv_bfloat16* __rest
     }
 }
 
+__global__ void k_wide_sum_partials(const float* __restrict__ part, int splits, int64_t count, float* out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float t = 0.0f;
+        for (int s = 0; s < splits; ++s) t += part[s * count + i];  // split order: deterministic
+        out[i] = t;
+    }
+}
+
 }  // namespace
+
+void wide_sum_partials(cudaStream_t s, const float* part, int splits, int64_t count, float* out) {
+    const int blocks = static_cast<int>(std::min<int64_t>((count + 255) / 256, 148 * 8));
+    k_wide_sum_partials<<<blocks, 256, 0, s>>>(part, splits, count, out);
+}
 
 void wide_build_weights(cudaStream_t s, const float* params, const WideNet& n0, __nv_bfloat16* w0, const WideNet& n1,
                         __nv_bfloat16* w1) {

@@ -48,6 +48,7 @@ void wide_split_input(cudaStream_t s, const float* x, int64_t rows, int cols, __
 // per layer [W_hi; W_hi; W_lo] f16 (the split B operand)
 void wide_build_split_weights(cudaStream_t s, const float* params, const WideNet& n, __half* ws);
 void wide_loss(cudaStream_t s, const WideLossArgs& a);
+void wide_sum_partials(cudaStream_t s, const float* part, int splits, int64_t count, float* out);  // fixed order
 void wide_colsum(cudaStream_t s, const __nv_bfloat16* dz, int64_t rows, int cols, int64_t ld, int splits, float* part,
                  int64_t stride);
 

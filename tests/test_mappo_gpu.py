@@ -103,9 +103,9 @@ def test_fast_mappo_tracks_exact(n_agents):
 @pytest.mark.parametrize("n_agents", [6, 10])
 def test_fast_mappo_compact_critic_tracks_exact(n_agents):
     """n > 4: the critic input [joint | one-hot] (2n^2+3n) is wider than the fused kernel, so
-    its layer 0 runs compact - a TF32 joint GEMM once per env plus W[J+a] - and its gradients
-    come from the fused kernel's input-gradient stage (dW_J = joint^T . sum_a dZ0, one-hot rows,
-    bias). Same checks as the direct path."""
+    its layer 0 runs compact - a tcgen05 joint GEMM once per env (kernels_tgemm.cu) plus W[J+a] -
+    and its gradients come from the fused kernel's input-gradient stage (dW_J = joint^T . sum_a
+    dZ0 as a split-K tcgen05 GEMM, one-hot rows, bias). Same checks as the direct path."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2210_00882_b200 import DpdEngine
@@ -124,9 +124,10 @@ def test_fast_mappo_compact_critic_tracks_exact(n_agents):
     assert rel < 2e-2, rel
 
 
-@pytest.mark.parametrize("n_agents", [3, 10])
+@pytest.mark.parametrize("n_agents", [3, 10, 24, 40])
 def test_fast_mappo_rollout_matches_exact(n_agents):
-    """The fused fast MAPPO rollout (3-term F16 tensor-core MLP over the agent rows, f32 softmax,
+    """The fused fast MAPPO rollout (n <= 16; n = 24, 40: the policy forward as f32-accurate
+    split-f16 tcgen05 GEMMs) (3-term F16 tensor-core MLP over the agent rows, f32 softmax,
     the reference's draws, exact spread_lite dynamics in double) against the exact per-step
     rollout from the same reset: step 0's actions agree except near-tie draws and their logp to
     1e-5; over the episode the draws agree for >= 98% of the agent rows (a flip changes that
@@ -156,3 +157,51 @@ def test_fast_mappo_rollout_matches_exact(n_agents):
         same_all += int(same.sum())
         total += same.size
     assert same_all >= 0.98 * total, (same_all, total)
+
+
+@pytest.mark.parametrize("n_agents", [32, 64])
+def test_fast_mappo_wide_tracks_exact(n_agents):
+    """n = 32, 64 (C3's upper end; joint observation 2112 / 8320 wide, per-agent observation
+    66 / 130 > the fused kernel's 64): split-GEMM rollout, layer-wise policy learn, compact
+    critic on tcgen05 GEMMs, against the exact (reference-arithmetic) engine.
+      1. episode 0's rollout (same initial params): sampled actions identical but for near-ties;
+      2. the first train iteration on that (identical) trajectory: gradient cosine / rel-L2;
+      3. three free-running episodes: rewards within 5%, params within 5% (Adam's sign-like
+         steps amplify tiny gradient differences along the trajectory)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2210_00882_b200 import DpdEngine
+
+    algo = {"algorithm": "mappo", "agent": {"num": n_agents},
+            "env": {"type": "spread_lite", "num": 32, "params": {"accel": 1}},
+            "policy_net": {"hidden": [64] * 6}, "loop": {"episodes": 3, "steps_per_episode": 16}}
+    ex = DpdEngine(algo, seed=5, numerics="exact")
+    fa = DpdEngine(algo, seed=5, numerics="fast")
+    ex.reset(0)
+    fa.reset(0)
+    same = total = 0
+    for st in range(16):
+        ex.step(0, st)
+        fa.step(0, st)
+        pe, pf = ex.get("pa").reshape(-1, 2), fa.get("pa").reshape(-1, 2)
+        same += int((pe[:, 0] == pf[:, 0]).sum())
+        total += pe.shape[0]
+    assert same >= 0.999 * total, (same, total)
+    ex.learn_grads(0, 0)
+    fa.learn_grads(0, 0)
+    g_e, g_f = ex.get("grads"), fa.get("grads")
+    cos = float(g_e @ g_f / (np.linalg.norm(g_e) * np.linalg.norm(g_f)))
+    rel = float(np.linalg.norm(g_f - g_e) / np.linalg.norm(g_e))
+    print(f"n={n_agents}: actions same {same}/{total}, grads cos {cos:.6f} rel {rel:.2e}")
+    if same == total:
+        assert cos >= 0.9999 and rel <= 2e-2, (cos, rel)
+    ex = DpdEngine(algo, seed=5, numerics="exact")
+    fa = DpdEngine(algo, seed=5, numerics="fast")
+    r_ex = [ex.run_episode(ep)[0] for ep in range(3)]
+    r_fa = [fa.run_episode(ep)[0] for ep in range(3)]
+    assert r_fa[0] == pytest.approx(r_ex[0], rel=2e-2)
+    np.testing.assert_allclose(r_fa, r_ex, rtol=5e-2)
+    p_ex, p_fa = np.asarray(ex.params()), np.asarray(fa.params())
+    prel = np.linalg.norm(p_fa - p_ex) / np.linalg.norm(p_ex)
+    print(f"n={n_agents}: rewards {r_ex} vs {r_fa}, params rel {prel:.3g}")
+    assert prel < 5e-2, prel

@@ -10,8 +10,8 @@ N>1 (torchrun): one unit per GPU, 4096 envs each (weak scaling; 16384 total at N
 gradients averaged every train iteration over NVLink (the DP-C == replicated DP-D exchange).
 
 --impl reference times the reference's own CPU implementation (oracle/_ref/ref_tool: the
-unmodified reference compiled from its sources) on this host's cores: DP-D with one replica per
-core over a bounded sample of the same workload, rank 0 only.
+unmodified reference compiled from its sources) on this host's cores on the same workload
+(4096 envs per GPU of the run), DP-D with one replica thread per core, rank 0 only.
 """
 from __future__ import annotations
 
@@ -233,32 +233,57 @@ def cpu_baseline(target_s: float = 12.0) -> dict:
     r1 = run_reference(e1, 1, episodes=1)
     ms1 = sum(e["wall_ms"] for e in r1["episodes"])
     return {"value": envs * T_STEPS * len(r["episodes"]) / (ms / 1e3), "unit": "env-steps/s", "cores": cores,
-            "kind": "reference",
+            "kind": "reference", "cpu_model": cpu_model(),
             "sample": f"1 episode of C2 at {envs} envs (dp-d, {k} replica threads), {ms / 1e3:.1f} s",
             "single_core": {"value": e1 * T_STEPS / (ms1 / 1e3), "unit": "env-steps/s", "cores": 1,
                             "sample": f"1 episode of C2 at {e1} envs (dp-d, 1 unit), {ms1 / 1e3:.1f} s"}}
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def bench_reference(args, world, rank):
+    """The reference's own CPU implementation of the path (oracle/_ref/ref_tool = the unmodified
+    reference compiled from its sources) on this host's cores, on OUR arm's config: C2 at 4096
+    envs (ENVS_PER_GPU x world when N > 1, timed on rank 0's host only), DP-D with one replica
+    thread per core. One ref_tool process runs W + K episodes; the reference's own per-episode
+    wall_ms (local_run.cpp:540-551) of the last K are the steps."""
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    envs, k = reference_sample(cores, 4.0)
-    times = []
-    for i in range(args.warmup + args.steps):
-        r = run_reference(envs, k, episodes=1, seed=7 + i)
-        if i >= args.warmup:
-            times.append(sum(e["wall_ms"] for e in r["episodes"]))
+    envs = ENVS_PER_GPU * world
+    k = min(cores, envs)
+    # N > 1: the whole job's envs on one host; the episode count shrinks by the same factor
+    # (>= 1 warm-up + 1 timed) so the CPU arm stays within minutes
+    warm, steps = args.warmup, args.steps
+    if world > 1:
+        warm = 1
+        steps = max(1, round(args.steps / world))
+    r = run_reference(envs, k, episodes=warm + steps)
+    times = [e["wall_ms"] for e in r["episodes"]][warm:]
     ms = sum(times) / len(times)
     value = envs * T_STEPS / (ms / 1e3)
     line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32-storage/f64-accumulate", "data": "synthetic (synth17x6 env)",
+            "vs_baseline": None, "dtype": "f32-storage/f64-accumulate", "data": "synthetic (synth17x6 env, seeded)",
             "impl": "reference",
-            "config": {"workload": f"C2 sample: PPO synth17x6, {envs} envs, 7-layer MLP (hidden 6x{HIDDEN[0]}), T=32, "
-                                   f"train_iters=4, dp-d with {k} CPU replicas", "envs": envs, "replicas": k},
-            "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": cores, "kind": "reference",
-                             "sample": f"{envs} envs per episode, {k} replica threads"},
+            "config": {"workload": f"C2: PPO synth17x6, {envs} envs, 7-layer MLP (hidden 6x{HIDDEN[0]}), T=32, "
+                                   f"train_iters=4, dp-d with {k} CPU replica threads",
+                       "envs_total": envs, "envs_per_gpu": ENVS_PER_GPU, "replicas": k, "numerics": "reference",
+                       "cpu_model": cpu_model()},
+            "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": k, "kind": "reference",
+                             "cpu_model": cpu_model(),
+                             "sample": f"{steps} timed episodes (after {warm} warm-up) of the full "
+                                       f"workload, {envs} envs, {k} replica threads"},
             "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

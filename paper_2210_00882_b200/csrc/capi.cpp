@@ -80,8 +80,17 @@ struct EpisodeMetrics {
 };
 
 // capi.cpp:74-113 summary schema.
+// The bytes the GPU gradient exchange really moves (all ranks, NVLink), next to the reference's
+// message accounting in bytes_total: kind "p2p" (each rank stores its f32 gradient
+// into every peer's inbox), "nccl_allreduce" (ring: 2(k-1)/k of the vector per rank) or
+// "nccl_allgather" (exact numerics: every rank receives the other ranks' R unit gradients).
+struct DeviceExchange {
+    std::string kind = "none";
+    int64_t bytes_per_episode = 0;
+};
+
 std::string summarize(const std::vector<EpisodeMetrics>& eps, int64_t steps, const std::vector<double>& params,
-                      int64_t grad_bytes_total, const flw_run_options* opts) {
+                      int64_t grad_bytes_total, const flw_run_options* opts, const DeviceExchange& dx) {
     nlohmann::ordered_json j;
     j["episodes"] = eps.size();
     j["steps"] = steps;
@@ -94,6 +103,11 @@ std::string summarize(const std::vector<EpisodeMetrics>& eps, int64_t steps, con
     nlohmann::ordered_json per = nlohmann::ordered_json::object();
     if (grad_bytes_total > 0) per["0"] = grad_bytes_total;
     j["bytes_per_channel"] = per;
+    nlohmann::ordered_json dev;
+    dev["kind"] = dx.kind;
+    dev["bytes_per_episode"] = dx.bytes_per_episode;
+    dev["bytes_total"] = dx.bytes_per_episode * static_cast<int64_t>(eps.size());
+    j["device_exchange"] = dev;
     double sum = 0.0, sumsq = 0.0;
     for (double v : params) {
         sum += v;
@@ -128,7 +142,7 @@ std::string to_csv(const std::vector<EpisodeMetrics>& eps) {  // local_run.cpp:5
 // run_plan_local (local_run.cpp:512-581) for a DP-D plan: one host thread per unit, each unit
 // on its own GPU, an episode lockstep gate driven by this thread, wall_ms per episode.
 void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeMetrics>& eps, int64_t& steps,
-               std::vector<double>& final_params, int64_t& grad_bytes) {
+               std::vector<double>& final_params, int64_t& grad_bytes, DeviceExchange& dx) {
     std::lock_guard<std::mutex> lk(p.mu);
     const uint64_t seed = opts ? opts->seed : 0;
     const int64_t episodes = opts && opts->episodes > 0 ? opts->episodes : p.algo.episodes;
@@ -278,6 +292,21 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
     final_params.assign(static_cast<size_t>(s.P), 0.0);
     p.engines[0]->get_params(final_params.data());
     grad_bytes = per_ep_bytes * episodes;
+    dx = DeviceExchange{};
+    if (ng > 1) {
+        const int64_t P4 = 4 * s.P, I = s.learn_iters;
+        const Engine& e0 = *p.engines[0];
+        if (e0.numerics() == Numerics::Exact) {
+            dx.kind = "nccl_allgather";
+            dx.bytes_per_episode = I * static_cast<int64_t>(ng) * (ng - 1) * R * P4;
+        } else if (e0.p2p_enabled()) {
+            dx.kind = "p2p";
+            dx.bytes_per_episode = I * static_cast<int64_t>(ng) * (ng - 1) * P4;
+        } else {
+            dx.kind = "nccl_allreduce";
+            dx.bytes_per_episode = I * 2 * static_cast<int64_t>(ng - 1) * P4;
+        }
+    }
 }
 
 Engine& eng(flw_dpd* e) {
@@ -336,9 +365,10 @@ int flw_run_local(const flw_program* p, const flw_run_options* opts, char** metr
         std::vector<EpisodeMetrics> eps;
         int64_t steps = 0, bytes = 0;
         std::vector<double> params;
-        run_local(*const_cast<flw_program*>(p), opts, eps, steps, params, bytes);
+        DeviceExchange dx;
+        run_local(*const_cast<flw_program*>(p), opts, eps, steps, params, bytes, dx);
         if (metrics_csv) *metrics_csv = dup_string(to_csv(eps));
-        if (summary_json) *summary_json = dup_string(summarize(eps, steps, params, bytes, opts));
+        if (summary_json) *summary_json = dup_string(summarize(eps, steps, params, bytes, opts, dx));
         return FLW_OK;
     });
 }

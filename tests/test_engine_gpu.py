@@ -155,8 +155,9 @@ def test_run_local_summary_schema():
     assert lines[0] == "episode,wall_ms,reward,bytes_total" and len(lines) == 4
     for key in ("episodes", "steps", "grad_messages", "final_reward", "total_wall_ms", "bytes_total",
                 "bytes_per_channel", "param_count", "param_checksum", "param_l2", "reward_threshold",
-                "time_to_threshold_ms"):
+                "time_to_threshold_ms", "device_exchange"):
         assert key in s
+    assert s["device_exchange"] == {"kind": "none", "bytes_per_episode": 0, "bytes_total": 0}  # one unit
     rew, par, _ = pyoracle.run(algo, 17, 1, episodes=3)
     close("final_reward", s["final_reward"], rew[-1])
     assert s["param_count"] == par.size

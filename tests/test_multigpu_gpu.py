@@ -29,6 +29,12 @@ def test_k_units_on_k_gpus_match_reference(name):
     np.testing.assert_allclose(rewards, z["rewards"], rtol=1e-5)
     assert s["steps"] == int(z["steps"])
     assert s["bytes_total"] == int(np.sum(z["bytes_total"]))
+    # the NCCL bytes really moved, next to the reference's message accounting:
+    # every rank receives the other k-1 ranks' f32 gradients each train iteration
+    P, eps = s["param_count"], s["episodes"]
+    it = s["bytes_total"] // (eps * k * (k - 1) * (14 + 8 * P))  # train iterations (reference accounting)
+    assert s["device_exchange"]["kind"] == "nccl_allgather"
+    assert s["device_exchange"]["bytes_total"] == eps * it * k * (k - 1) * 4 * P
     # final params: the summary's checksum/l2 over the f32 params equal the reference's
     par = z["final_params"]
     assert s["param_count"] == par.size
@@ -68,6 +74,11 @@ def test_fast_peer_memory_exchange_matches_nccl(gpus):
         csv, s = prog.run_local(seed=3)
         out[ex] = (csv, s)
     sp, sn = out["p2p"][1], out["nccl"][1]
+    P = sp["param_count"]
+    assert sp["device_exchange"]["kind"] == "p2p"
+    assert sp["device_exchange"]["bytes_per_episode"] == 4 * gpus * (gpus - 1) * 4 * P
+    assert sn["device_exchange"]["kind"] == "nccl_allreduce"
+    assert sn["device_exchange"]["bytes_per_episode"] == 4 * 2 * (gpus - 1) * 4 * P
     if gpus == 2:
         assert sp["param_checksum"] == sn["param_checksum"]
         assert sp["param_l2"] == sn["param_l2"]

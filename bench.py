@@ -209,12 +209,23 @@ def roofline_for(tag: str, ms: float, envs: int, peaks: dict) -> dict:
 
 
 def hbm_microbenchmarks(peaks: dict) -> dict:
-    """Env step / GAE / Adam at scaled sizes (inputs >> 126 MB L2), SURVEY §8(d)."""
+    """The HBM-bound kernels the episodes launch, at scaled sizes (at C2 they move
+    < 20 MB and are launch/L2 bound), with the survey's algorithmic bytes per unit:
+      rollout_env   k_rollout (PolicyApply + env step of the per-step rollouts), 2^21 envs, 173 B/env-step
+      gae_scan32    k_gae_scan32 (the episode's GAE), its largest size 2^21 rows, 4 rotating sets > L2, 17 B/row
+      gae_streams   k_fast_gae<8,4> (GAE when R > 65536 streams, e.g. MAPPO n >= 32), 2^26 rows, 17 B/row
+      reduce_adam   k_reduce_adam (the fused per-iteration update, 1 GPU), 2^26 params, 8 partial slots:
+                    44 B/param (Adam, f64 moments) + 4 B/param per slot
+      exchange_adam k_reduce_push + k_sum_adam (the k-GPU peer-memory update, k = 1), same
+    In the C2 fast episode the env step is fused into k_rollout_episode (MMA-latency bound: see
+    kernel_shares / rollout_only)."""
     from paper_2210_00882_b200.api import microbench
 
     out = {}
-    for name, n in (("env_step", 1 << 21), ("gae", 1 << 26), ("adam", 1 << 27)):
-        ms, nbytes = microbench(name, n, 10)
+    for name, kern, n in (("rollout_env", "rollout_env", 1 << 21), ("gae_scan32", "gae_scan32", 1 << 21),
+                          ("gae_streams", "gae", 1 << 26), ("reduce_adam", "reduce_adam", 1 << 26),
+                          ("exchange_adam", "exchange_adam", 1 << 26)):
+        ms, nbytes = microbench(kern, n, 10)
         gbs = nbytes / (ms * 1e-3) / 1e9
         out[name] = {"n": n, "ms": ms, "bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peaks["hbm_gbs"]}
     return out

@@ -17,6 +17,8 @@
 // lane offsets 0 and 16.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "engine.hpp"
 #include "fast.cuh"
@@ -102,63 +104,65 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
 // k_build_wimg), so the next train iteration's learn kernels read the updated image without a
 // build launch. The Adam step counter and its bias corrections (as k_adam_tick) are advanced by
 // the last block to finish (every block has read the old counter by then).
-__global__ void __launch_bounds__(256) k_reduce_adam(FastUpdateArgs a) {
-    // 128 parameters per block: lane -> 4 consecutive parameters (float4 rows, 512 B per warp
-    // load); warp w sums partials w, w+8, ... in order, then the 8 warp sums are added in warp
-    // order (the k_reduce_partials tree, per parameter); Adam then runs one parameter per thread
+__global__ void __launch_bounds__(256) k_reduce_adam(FastUpdateArgs a, int nchunks) {
+    // 128 parameters per chunk (grid-stride): lane -> 4 consecutive parameters (float4 rows, 512 B
+    // per warp load); warp w sums partials w, w+8, ... in order, then the 8 warp sums are added in
+    // warp order (the k_reduce_partials tree, per parameter); Adam then runs one parameter per thread
     __shared__ float4 ws[8][32];
     __shared__ bool last;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // padded index space: [policy rows padded to Pps][critic rows padded to Pcs], so a lane's
     // float4 never straddles the two nets
     const int64_t Pps = (a.Pp + 3) / 4 * 4, Pcs = (a.Pc + 3) / 4 * 4;
-    const int64_t q0 = blockIdx.x * 128LL + 4 * lane;  // first of this lane's 4 padded indices
-    float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (q0 < Pps + Pcs) {
-        const bool pol = q0 < Pps;
-        const float* base = pol ? a.pp + q0 : a.pc + (q0 - Pps);
-        const int64_t stride = pol ? Pps : Pcs;
-        const int nparts = pol ? a.np : a.nc;
-#pragma unroll 4
-        for (int p = w; p < nparts; p += 8) {
-            const float4 v = *reinterpret_cast<const float4*>(base + p * stride);
-            s4.x += v.x;
-            s4.y += v.y;
-            s4.z += v.z;
-            s4.w += v.w;
-        }
-    }
-    ws[w][lane] = s4;
     const int64_t t = a.ctx->adam_t + 1;
     const double bc1 = t <= a.bc_len ? a.bc_table[t - 1].x : 1.0 - pow(0.9, static_cast<double>(t));
     const double bc2 = t <= a.bc_len ? a.bc_table[t - 1].y : 1.0 - pow(0.999, static_cast<double>(t));
-    __syncthreads();
-    if (threadIdx.x < 128) {
-        const int ln = threadIdx.x >> 2, j = threadIdx.x & 3;
-        const int64_t ipad = blockIdx.x * 128LL + threadIdx.x;
-        const bool inpol = ipad < Pps;
-        const int64_t i = inpol ? ipad : a.Pp + (ipad - Pps);  // flat parameter index
-        if (inpol ? ipad < a.Pp : (ipad - Pps < a.Pc && ipad < Pps + Pcs)) {
-            float gsum = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) gsum += reinterpret_cast<const float*>(&ws[k][ln])[j];
-            a.grads[i] = gsum;
-            const double g = static_cast<double>(gsum);
-            const double mi = __dadd_rn(__dmul_rn(a.b1, a.m[i]), __dmul_rn(__dsub_rn(1.0, a.b1), g));
-            const double vi = __dadd_rn(__dmul_rn(a.b2, a.v[i]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, a.b2), g), g));
-            a.m[i] = mi;
-            a.v[i] = vi;
-            const double mhat = __ddiv_rn(mi, bc1), vhat = __ddiv_rn(vi, bc2);
-            const float next = static_cast<float>(__dsub_rn(
-                static_cast<double>(a.params[i]), __ddiv_rn(__dmul_rn(a.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), a.eps))));
-            a.params[i] = next;
-            // weight-image entry (biases are read from params by the learn kernels)
-            const bool ip = i < a.Pp;
-            const int64_t e = wimg_elem(ip ? a.pol : a.crit, i);
-            if (e >= 0) (ip ? a.img_p : a.img_c)[e] = __float2bfloat16(next);
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const int64_t q0 = c * 128LL + 4 * lane;  // first of this lane's 4 padded indices
+        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q0 < Pps + Pcs) {
+            const bool pol = q0 < Pps;
+            const float* base = pol ? a.pp + q0 : a.pc + (q0 - Pps);
+            const int64_t stride = pol ? Pps : Pcs;
+            const int nparts = pol ? a.np : a.nc;
+#pragma unroll 4
+            for (int p = w; p < nparts; p += 8) {
+                const float4 v = *reinterpret_cast<const float4*>(base + p * stride);
+                s4.x += v.x;
+                s4.y += v.y;
+                s4.z += v.z;
+                s4.w += v.w;
+            }
         }
+        ws[w][lane] = s4;
+        __syncthreads();
+        if (threadIdx.x < 128) {
+            const int ln = threadIdx.x >> 2, j = threadIdx.x & 3;
+            const int64_t ipad = c * 128LL + threadIdx.x;
+            const bool inpol = ipad < Pps;
+            const int64_t i = inpol ? ipad : a.Pp + (ipad - Pps);  // flat parameter index
+            if (inpol ? ipad < a.Pp : (ipad - Pps < a.Pc && ipad < Pps + Pcs)) {
+                float gsum = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) gsum += reinterpret_cast<const float*>(&ws[k][ln])[j];
+                a.grads[i] = gsum;
+                const double g = static_cast<double>(gsum);
+                const double mi = __dadd_rn(__dmul_rn(a.b1, a.m[i]), __dmul_rn(__dsub_rn(1.0, a.b1), g));
+                const double vi = __dadd_rn(__dmul_rn(a.b2, a.v[i]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, a.b2), g), g));
+                a.m[i] = mi;
+                a.v[i] = vi;
+                const double mhat = __ddiv_rn(mi, bc1), vhat = __ddiv_rn(vi, bc2);
+                const float next = static_cast<float>(__dsub_rn(
+                    static_cast<double>(a.params[i]), __ddiv_rn(__dmul_rn(a.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), a.eps))));
+                a.params[i] = next;
+                // weight-image entry (biases are read from params by the learn kernels)
+                const bool ip = i < a.Pp;
+                const int64_t e = wimg_elem(ip ? a.pol : a.crit, i);
+                if (e >= 0) (ip ? a.img_p : a.img_c)[e] = __float2bfloat16(next);
+            }
+        }
+        __syncthreads();  // ws is rewritten by the next chunk
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
@@ -632,7 +636,8 @@ void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part
 
 void fast_reduce_adam(cudaStream_t s, const FastUpdateArgs& a) {
     const int64_t padded = (a.Pp + 3) / 4 * 4 + (a.Pc + 3) / 4 * 4;
-    k_reduce_adam<<<static_cast<unsigned>((padded + 127) / 128), 256, 0, s>>>(a);
+    const int nchunks = static_cast<int>((padded + 127) / 128);
+    k_reduce_adam<<<static_cast<unsigned>(std::min(nchunks, 148 * 8)), 256, 0, s>>>(a, nchunks);
 }
 
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss) {

@@ -1,13 +1,23 @@
-// Scaled-size HBM microbenchmarks of the DP-D element-wise kernels (at C2 these
-// move < 20 MB and are launch/L2 bound, so their roofline is reported on scaled sizes):
-//   env_step : batched synth17x6 step over E envs, SoA double state in/out, f32 obs/reward,
-//              u8 done, i32 action                      -> 8*17*2 + 4 + 4*17 + 4 + 1 = 349 B/env
-//   gae      : GAE + returns over T*E rows (T = 32)     -> r, V, done (f32) in; adv, ret out = 20 B/row
-//   adam     : Adam with f64 moments over P params      -> g,p (f32) + m,v (f64) in; p,m,v out = 44 B/param
-// Inputs are device-resident and larger than L2 at the sizes bench.py uses; each launch is
-// timed with CUDA events on the launching stream, after warm-up.
+// Scaled-size HBM microbenchmarks of the DP-D element-wise kernels the episodes launch (SURVEY
+// §8(d): at C2 these move < 20 MB and are launch/L2 bound, so their roofline is reported on
+// scaled sizes). Algorithmic bytes are the survey's per-unit figures:
+//   rollout_env : k_rollout (PolicyApply + synth17x6 step, the per-step env kernel of the exact,
+//                 layer-wise and split-GEMM rollouts) over E envs: (8S+9) B/env-step (state in/out,
+//                 action, reward, done) + 4A logits in + 4 logp out = 173 B (the kernel keeps the
+//                 env state in f64, so it moves more than this)
+//   gae_scan32  : k_gae_scan32 (the episode's GAE + returns + advantage statistics, T = 32) at its
+//                 largest size, R = 65536 streams, four rotating buffer sets (> L2): 17 B/row + 4 B/stream
+//   gae         : k_fast_gae<8,4> (fast_gae's kernel when R > 65536, e.g. MAPPO n >= 32) at T*R rows
+//   reduce_adam : k_reduce_adam (the fused per-iteration update: partial reduction + Adam with f64
+//                 moments) over P params and 8 partial slots: 44 B/param (g in, p, m, v in/out) + 4 B
+//                 per partial slot
+//   exchange_adam: k_reduce_push + k_sum_adam (the k-GPU peer-memory update) with k = 1: same bytes
+//   env_step / adam: the standalone microbenchmark kernels of round 1 (kept for comparison)
+// Each launch is timed with CUDA events on the launching stream, after warm-up.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -16,6 +26,7 @@
 #include "envs.cuh"
 #include "fast.cuh"
 #include "kernels.cuh"
+#include "p2p.cuh"
 
 namespace flw {
 
@@ -138,7 +149,8 @@ void microbench(const std::string& which, int64_t n, int iters, double* ms, doub
         FLW_CUDA(cudaGetLastError());
         *ms = time_launches([&] { fast_gae(0, r, v, dn, lv, T * R, R, 0.99, 0.95, adv, ret, true, bs, st, cnt); },
                             iters);
-        *bytes = static_cast<double>(T * R) * 20.0 + static_cast<double>(R) * 4.0;
+        // algorithmic 17 B/row (done as one byte); the kernel reads done as f32 (20 B)
+        *bytes = static_cast<double>(T * R) * 17.0 + static_cast<double>(R) * 4.0;
     } else if (which == "adam") {
         float* p = d.get<float>(n);
         float* gr = d.get<float>(n);
@@ -157,6 +169,160 @@ void microbench(const std::string& which, int64_t n, int iters, double* ms, doub
         FLW_CUDA(cudaGetLastError());
         *ms = time_launches([&] { exact_adam(0, ctx, p, gr, nullptr, m, v, n, 3e-3, 0.9, 0.999, 1e-8); }, iters);
         *bytes = static_cast<double>(n) * 44.0;
+    } else if (which == "rollout_env") {  // k_rollout: PolicyApply + env step, E = n envs
+        const int S = kSynthObs, A = kSynthAct;
+        float* logits = d.get<float>(A * n);
+        double* est = d.get<double>(S * n);
+        uint8_t* done = d.get<uint8_t>(n);
+        int32_t* stepc = d.get<int32_t>(n);
+        int32_t* act = d.get<int32_t>(n);
+        float* lp = d.get<float>(n);
+        float* rw = d.get<float>(n);
+        double* rwd = d.get<double>(n);
+        float* dnf = d.get<float>(n);
+        float* obs = d.get<float>(S * n);
+        double* tab = d.get<double>(A * S);
+        DeviceCtx* ctx = d.get<DeviceCtx>(1);
+        FLW_CUDA(cudaMemset(ctx, 0, sizeof(DeviceCtx)));
+        FLW_CUDA(cudaMemset(done, 0, n));
+        FLW_CUDA(cudaMemset(stepc, 0, n * sizeof(int32_t)));
+        k_init_f32<<<g, blk>>>(logits, A * n, 1, -1.f, 1.f);
+        k_init_u64<<<g, blk>>>(est, S * n, 2, -0.1, 0.1);
+        k_init_u64<<<g, blk>>>(tab, A * S, 3, -1.0, 1.0);
+        FLW_CUDA(cudaGetLastError());
+        RolloutArgs a{};
+        a.logits = logits;
+        a.est = est;
+        a.done = done;
+        a.stepc = stepc;
+        a.actions = act;
+        a.logp = lp;
+        a.reward = rw;
+        a.reward_d = rwd;
+        a.done_f = dnf;
+        a.next_obs = obs;
+        a.E = n;
+        a.S = S;
+        a.A = A;
+        a.seed = 7;
+        a.env.kind = static_cast<int>(EnvKind::Synth17x6);
+        a.env.synth_b = tab;
+        *ms = time_launches([&] { exact_rollout(0, ctx, a); }, iters);
+        *bytes = static_cast<double>(n) * (8.0 * S + 9 + 4.0 * A + 4);
+    } else if (which == "gae_scan32") {  // the episode's GAE kernel at R = n / 32 <= 65536 streams
+        const int64_t T = 32, R = std::min<int64_t>(n / T, 65536);
+        constexpr int kSets = 4;  // 4 x 42 MB > L2: every launch reads from HBM
+        float *r[kSets], *v[kSets], *dn[kSets], *lv[kSets], *adv[kSets], *ret[kSets];
+        for (int k = 0; k < kSets; ++k) {
+            r[k] = d.get<float>(T * R);
+            v[k] = d.get<float>(T * R);
+            dn[k] = d.get<float>(T * R);
+            lv[k] = d.get<float>(R);
+            adv[k] = d.get<float>(T * R);
+            ret[k] = d.get<float>(T * R);
+            k_init_f32<<<g, blk>>>(r[k], T * R, 1 + k, -1.f, 1.f);
+            k_init_f32<<<g, blk>>>(v[k], T * R, 11 + k, -1.f, 1.f);
+            k_init_f32<<<g, blk>>>(dn[k], T * R, 21 + k, -18.f, 1.f);
+            k_init_f32<<<g, blk>>>(lv[k], R, 31 + k, -1.f, 1.f);
+        }
+        double* bs = d.get<double>(2 * ((R + 31) / 32));
+        double* st = d.get<double>(2);
+        unsigned* cnt = d.get<unsigned>(1);
+        FLW_CUDA(cudaMemset(cnt, 0, sizeof(unsigned)));
+        FLW_CUDA(cudaGetLastError());
+        int it = 0;
+        *ms = time_launches([&] {
+            const int k = it++ % kSets;
+            fast_gae(0, r[k], v[k], dn[k], lv[k], T * R, R, 0.99, 0.95, adv[k], ret[k], true, bs, st, cnt);
+        }, iters);
+        *bytes = static_cast<double>(T * R) * 17.0 + static_cast<double>(R) * 4.0;
+    } else if (which == "reduce_adam" || which == "exchange_adam") {  // the fused update kernels, P = n
+        constexpr int kParts = 8;  // partial slots (the episode's learn kernels write 44-148)
+        const int64_t npad = (n + 3) / 4 * 4;
+        float* part = d.get<float>(kParts * npad);
+        float* p = d.get<float>(n);
+        float* gr = d.get<float>(n);
+        double* m = d.get<double>(n);
+        double* v = d.get<double>(n);
+        DeviceCtx* ctx = d.get<DeviceCtx>(1);
+        constexpr int kBc = 256;  // the engine's host-computed bias-correction table (t <= kBc here)
+        double2* bct = d.get<double2>(kBc);
+        unsigned* cnt = d.get<unsigned>(1);
+        {
+            std::vector<double2> tab(kBc);
+            for (int t = 1; t <= kBc; ++t) tab[t - 1] = double2{1.0 - std::pow(0.9, t), 1.0 - std::pow(0.999, t)};
+            FLW_CUDA(cudaMemcpy(bct, tab.data(), kBc * sizeof(double2), cudaMemcpyHostToDevice));
+        }
+        DeviceCtx c{};
+        c.bc1 = 0.1;
+        c.bc2 = 0.001;
+        FLW_CUDA(cudaMemcpy(ctx, &c, sizeof(c), cudaMemcpyHostToDevice));
+        FLW_CUDA(cudaMemset(cnt, 0, sizeof(unsigned)));
+        k_init_f32<<<g, blk>>>(p, n, 1, -0.1f, 0.1f);
+        k_init_f32<<<g, blk>>>(part, kParts * npad, 2, -1e-3f, 1e-3f);
+        FLW_CUDA(cudaMemset(m, 0, n * sizeof(double)));
+        FLW_CUDA(cudaMemset(v, 0, n * sizeof(double)));
+        FLW_CUDA(cudaGetLastError());
+        if (which == "reduce_adam") {
+            FastUpdateArgs u{};
+            u.pp = part;
+            u.pc = part;
+            u.np = kParts;
+            u.nc = 0;
+            u.Pp = n;
+            u.Pc = 0;
+            u.ctx = ctx;
+            u.bc_table = bct;
+            u.bc_len = kBc;
+            u.params = p;
+            u.grads = gr;
+            u.m = m;
+            u.v = v;
+            u.lr = 3e-3;
+            u.b1 = 0.9;
+            u.b2 = 0.999;
+            u.eps = 1e-8;
+            u.counter = cnt;  // pol / crit: L = 0 (no weight-image entries)
+            *ms = time_launches([&] { fast_reduce_adam(0, u); }, iters);
+        } else {
+            const P2pLayout L = p2p_layout(1, n);
+            uint8_t* region = d.get<uint8_t>(L.bytes);
+            FLW_CUDA(cudaMemset(region, 0, L.bytes));
+            uint8_t** peers = d.get<uint8_t*>(1);
+            FLW_CUDA(cudaMemcpy(peers, &region, sizeof(region), cudaMemcpyHostToDevice));
+            unsigned* abort_word = d.get<unsigned>(1);
+            FLW_CUDA(cudaMemset(abort_word, 0, sizeof(unsigned)));
+            P2pArgs a{};
+            a.part_p = part;
+            a.part_c = part;
+            a.np = kParts;
+            a.nc = 0;
+            a.Pp = n;
+            a.Pc = 0;
+            a.rank = 0;
+            a.k = 1;
+            a.peers = peers;
+            a.off_inbox = L.off_inbox;
+            a.off_grads = L.off_grads;
+            a.off_sflag = L.off_sflag;
+            a.off_dflag = L.off_dflag;
+            a.ctx = ctx;
+            a.abort_flag = abort_word;
+            a.params = p;
+            a.m = m;
+            a.v = v;
+            a.lr = 3e-3;
+            a.b1 = 0.9;
+            a.b2 = 0.999;
+            a.eps = 1e-8;
+            a.gscale = 1.0;
+            *ms = time_launches([&] {
+                coll_tick(0, ctx);
+                reduce_allreduce_adam(0, a);
+            }, iters);
+        }
+        // survey: 44 B/param of Adam with f64 moments + 4 B per partial slot of the reduction
+        *bytes = static_cast<double>(n) * (44.0 + 4.0 * kParts);
     } else {
         fail(Errc::Config, "unknown microbenchmark '" + which + "'");
     }

@@ -901,10 +901,9 @@ void Engine::enq_learn_fast() {
     // (a layer-wise policy runs after the critic on the whole GPU)
     const bool concurrent = hreuse && lgrid >= 8 && !pwide_;  // the critic reads hsave, not hscratch
     if (concurrent) {
-        // measured: 70/30 for PPO / MAPPO with the direct critic; the compact critic's extra
-        // input-gradient stage makes its kernel heavier: 60/40
+        // measured (C2 sweep 0.58-0.70, profiles/r02_learn_split.txt): 60/40
         static const char* env_split = std::getenv("FLW_LEARN_SPLIT");
-        const double split = env_split ? std::atof(env_split) : (cfast_ ? 0.6 : 0.7);
+        const double split = env_split ? std::atof(env_split) : 0.6;
         gp = std::max(1, std::min(lgrid - 1, static_cast<int>(lgrid * split + 0.5)));
         gc = std::max(1, lgrid - gp);
         FLW_CUDA(cudaEventRecord(ev_lfork_, stream_));
@@ -1611,7 +1610,11 @@ double Engine::run_episode(int64_t ep, float* device_ms) {
     steps_ += T_ * nrep_;
     cur_step_ = T_;
     if (device_ms) FLW_CUDA(cudaEventElapsedTime(device_ms, ev_t0_, ev_t1_));
-    return last_reward_sum();
+    const double r = last_reward_sum();
+    if (std::isnan(r) && numerics_ == Numerics::Fast)
+        fail(Errc::Runtime, "fast numerics: an observation left the f16 range (|x| >= 65504) of the rollout's "
+                            "split tensor-core MLP; use numerics=exact");
+    return r;
 }
 
 // --------------------------------------------------------------------------- params

@@ -1,14 +1,17 @@
 // Fast-numerics rollout: the whole episode's T steps in ONE launch. Each CTA owns 32 envs for
 // the whole episode; per step it runs
 //   policy MLP   on the tensor cores with f32 accuracy: mma.sync m16n8k16 F16 in a 3-term split
-//                (x = hi + lo, hi = f16(x), lo = f16(x - hi), carrying ~22 significant bits;
-//                x.w ~ lo.hi + hi.lo + hi.hi with f32 accumulation). Weights are split once per
+//                (x = hi + lo, hi = f16(x), lo = f16(x - hi); x.w ~ lo.hi + hi.lo + hi.hi with f32
+//                accumulation). The pair carries ~22 significant bits for |x| >= 2^-3; below
+//                that lo is an f16 subnormal (|lo| < 2^-14) with absolute precision 2^-24, e.g.
+//                ~18 bits at |x| ~ 1e-2 (measured logp error at C2: 4.4e-6 relative). Weights are split once per
 //                launch and activations when they are produced, and both live in shared memory
 //                in FRAGMENT-MAJOR order ([tile][k-step][lane] x 16 B): every MMA operand is one
 //                conflict-free 128-bit load. Warp w owns env rows [16(w%2), +16) and the output
 //                tiles 2(w/2), 2(w/2)+1 of every layer, so its two accumulator fragments ARE the
 //                next layer's A fragment for k-step w/2 (one 128-bit store each for hi and lo).
-//                Valid for |activations|, |obs|, |weights| < 65504 (f16).
+//                Valid for |activations|, |obs|, |weights| < 65504 (f16): an observation outside
+//                that range poisons the step's reward (NaN) and the episode call fails loudly.
 //   PolicyApply  one thread per env (warp 0): the reference's double-precision softmax /
 //                inverse-CDF sampling on the f32 logits (interp.cpp:175-203)
 //   EnvStep      same thread, env state in its registers, bit-exact double dynamics (envs.cuh)
@@ -161,10 +164,12 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
     int32_t stepc = 0;
     __half* xhi = reinterpret_cast<__half*>(smem + S.xhi);
     __half* xlo = reinterpret_cast<__half*>(smem + S.xlo);
+    bool f16_oob = false;  // an observation left the f16 range of the split MLP
     auto put_obs = [&](int j, float o) {  // next layer-0 input element (row t, column j), split
         const int rr = le & 15, kc = j & 15;
         const int ln = 4 * (rr & 7) + ((kc & 7) >> 1), reg = 2 * (kc >> 3) + (rr >> 3);
         const int el = 2 * (4 * (((le >> 4) * KT0 + (j >> 4)) * 32 + ln) + reg) + (kc & 1);
+        f16_oob = f16_oob || !(fabsf(o) < 65504.0f);
         const __half h = __float2half_rn(o);
         xhi[el] = h;
         xlo[el] = __float2half_rn(o - __half2float(h));
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                 a.actions[ti] = chosen;
                 a.logp[ti] = __logf(fmaxf(p[chosen], 1e-30f));
                 a.reward[ti] = done ? 0.0f : static_cast<float>(rew);
-                a.reward_d[ti] = done ? 0.0 : rew;
+                a.reward_d[ti] = f16_oob ? __longlong_as_double(0x7ff8000000000000LL) : (done ? 0.0 : rew);
                 a.done_f[ti] = (done || d) ? 1.0f : 0.0f;
                 float* nt = a.states + ((step + 1) * E + e) * S_;
                 if (ENV == 0) {

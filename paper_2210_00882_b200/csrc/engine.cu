@@ -436,6 +436,10 @@ void Engine::alloc() {
             ra.A = A;
             ra.env = env_params(cfg_, shape_, nullptr);
             gemm_roll_ = mappo_ && !fast_rollout_mappo_ok(ra);
+            // A/B: FLW_ROLLOUT=tcgen05 runs the PPO / A3C rollout's policy MLP as the split-f16
+            // tcgen05 GEMMs (per layer, TMA + TMEM) instead of the fused mma.sync kernel
+            static const char* rv = std::getenv("FLW_ROLLOUT");
+            if (rv && std::string(rv) == "tcgen05") gemm_roll_ = true;
         }
         if (gemm_roll_ || pwide_) setup_wide_net(0, b.wpol);
         if (gemm_roll_) alloc_split_rollout();
@@ -726,7 +730,7 @@ bool Engine::enq_rollout_fast_mappo(int64_t step0, int64_t nsteps) {
 }
 
 void Engine::enq_step(int64_t st) {
-    if (numerics_ == Numerics::Fast && !mappo_ && !wide_) return enq_rollout_fast(st, 1);
+    if (numerics_ == Numerics::Fast && !mappo_ && !wide_ && !gemm_roll_) return enq_rollout_fast(st, 1);
     if (numerics_ == Numerics::Fast && mappo_ && !gemm_roll_ && enq_rollout_fast_mappo(st, 1)) return;
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
@@ -1489,7 +1493,7 @@ void Engine::build_graph() {
     enq_reset();
     trace_capture("reset");
     probe_begin("rollout");
-    if (numerics_ == Numerics::Fast && !mappo_ && !wide_)
+    if (numerics_ == Numerics::Fast && !mappo_ && !wide_ && !gemm_roll_)
         enq_rollout_fast(0, T_);
     else if (!(numerics_ == Numerics::Fast && mappo_ && !gemm_roll_ && enq_rollout_fast_mappo(0, T_)))
         for (int64_t st = 0; st < T_; ++st) enq_step(st);  // per-step rollout (exact or split GEMMs)

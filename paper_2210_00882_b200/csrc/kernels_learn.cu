@@ -246,6 +246,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
     constexpr int kGroups = groups_for(MODE);
     constexpr int kEpiWarps = 4 * kGroups;
     constexpr int kThreads = threads_for(MODE);
+#ifndef FLW_LEARN_ZPRE  // forward epilogue: one TMEM round trip for all 64 columns (1: all modes)
+#define FLW_LEARN_ZPRE 0
+#endif
+    constexpr bool kZPre = MODE == 0 || FLW_LEARN_ZPRE;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar, zbar;
     __shared__ uint32_t tslot;
@@ -658,11 +662,14 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                         // (the producer bulk-stores the finished tile for the backward / critic learn)
                         // 32 columns of H_l = act(Z + b); FULL: no per-chunk guards, so the
                         // compiler interleaves the four 8-column chains
-                        auto half = [&]<bool FULL>(int h0) {
-                            float z[32];
-                            umma::tmem_ld16(zt + h0, z);
-                            if (FULL || h0 + 16 < dout) umma::tmem_ld16(zt + h0 + 16, z + 16);
-                            umma::tmem_ld_wait();
+                        auto half = [&]<bool FULL, bool LOADED>(int h0, float* zin) {
+                            float zl[32];
+                            float* z = LOADED ? zin : zl;
+                            if constexpr (!LOADED) {
+                                umma::tmem_ld16(zt + h0, zl);
+                                if (FULL || h0 + 16 < dout) umma::tmem_ld16(zt + h0 + 16, zl + 16);
+                                umma::tmem_ld_wait();
+                            }
 #pragma unroll
                             for (int c = 0; c < 32; c += 8) {
                                 if (FULL || h0 + c < dout) {
@@ -695,14 +702,24 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                         const bool trf = learn && g == 0 && t == 0 && nf_ev < 16;
                         if (trf) tr_f[0][nf_ev] = clock64();
 #endif
-                        if (dout == kMaxW) {
-                            half.template operator()<true>(0);
+                        if (dout == kMaxW && kZPre) {
+                            // all 64 accumulator columns in one TMEM round trip
+                            float z0[32], z1[32];
+                            umma::tmem_ld16(zt, z0);
+                            umma::tmem_ld16(zt + 16, z0 + 16);
+                            umma::tmem_ld16(zt + 32, z1);
+                            umma::tmem_ld16(zt + 48, z1 + 16);
+                            umma::tmem_ld_wait();
+                            half.template operator()<true, true>(0, z0);
+                            half.template operator()<true, true>(32, z1);
+                        } else if (dout == kMaxW) {
+                            half.template operator()<true, false>(0, nullptr);
 #ifdef FLW_LEARN_TRACE
                             if (trf) tr_f[1][nf_ev] = clock64();
 #endif
-                            half.template operator()<true>(32);
+                            half.template operator()<true, false>(32, nullptr);
                         } else {
-                            for (int h0 = 0; h0 < dout; h0 += 32) half.template operator()<false>(h0);
+                            for (int h0 = 0; h0 < dout; h0 += 32) half.template operator()<false, false>(h0, nullptr);
                         }
 #ifdef FLW_LEARN_TRACE
                         if (trf) tr_f[2][nf_ev] = clock64();

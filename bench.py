@@ -212,8 +212,8 @@ def hbm_microbenchmarks(peaks: dict) -> dict:
     """The HBM-bound kernels the episodes launch, at scaled sizes (at C2 they move
     < 20 MB and are launch/L2 bound), with the survey's algorithmic bytes per unit:
       rollout_env   k_rollout (PolicyApply + env step of the per-step rollouts), 2^21 envs, 173 B/env-step
-      gae_scan32    k_gae_scan32 (the episode's GAE), its largest size 2^21 rows, 4 rotating sets > L2, 17 B/row
-      gae_streams   k_fast_gae<8,4> (GAE when R > 65536 streams, e.g. MAPPO n >= 32), 2^26 rows, 17 B/row
+      gae_scan32    k_gae_scan32 (the episodes' GAE, T = 32), 2^26 rows, 17 B/row
+      gae_streams   k_fast_gae<8,4> (the GAE kernel for T != 32), 2^26 rows, 17 B/row
       reduce_adam   k_reduce_adam (the fused per-iteration update, 1 GPU), 2^26 params, 8 partial slots:
                     44 B/param (Adam, f64 moments) + 4 B/param per slot
       exchange_adam k_reduce_push + k_sum_adam (the k-GPU peer-memory update, k = 1), same
@@ -222,7 +222,7 @@ def hbm_microbenchmarks(peaks: dict) -> dict:
     from paper_2210_00882_b200.api import microbench
 
     out = {}
-    for name, kern, n in (("rollout_env", "rollout_env", 1 << 21), ("gae_scan32", "gae_scan32", 1 << 21),
+    for name, kern, n in (("rollout_env", "rollout_env", 1 << 21), ("gae_scan32", "gae_scan32", 1 << 26),
                           ("gae_streams", "gae", 1 << 26), ("reduce_adam", "reduce_adam", 1 << 26),
                           ("exchange_adam", "exchange_adam", 1 << 26)):
         ms, nbytes = microbench(kern, n, 10)

@@ -122,6 +122,10 @@ void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, d
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
               double* block_sums, double* stats, unsigned* done_counter = nullptr);  // counter: fused stats
+// k_gae_scan32 for any stream count (T = 32), persistent over 32-stream tiles (microbenchmarks)
+void fast_gae_scan32(cudaStream_t s, const float* rew, const float* values, const float* done_f,
+                     const float* last_value, int64_t R, double gamma, double lam, float* adv, float* ret,
+                     bool with_adv, double* block_sums, double* stats, unsigned* done_counter);
 void fast_sum(cudaStream_t s, const double* x, int64_t n, double* scratch, double* out);
 void fast_rep_adv_stats(cudaStream_t s, const float* adv, int64_t T, int64_t E, const int64_t* rep_off,
                         const int64_t* rep_n, int R, double* stats);

@@ -344,38 +344,64 @@ __global__ void __launch_bounds__(1024) k_gae_scan32(const float* __restrict__ r
                                                      const float* __restrict__ last_value, int64_t R, double gamma,
                                                      double lam, float* adv, float* ret, bool with_adv,
                                                      double* block_sums, double* stats, unsigned* done_counter) {
+    // Persistent over tiles of 32 streams x 32 steps (grid-stride); the next tile's inputs are
+    // loaded into registers while the current one is scanned, so the loads of consecutive tiles
+    // overlap (bandwidth regime) and a single tile per block is the latency regime of C2.
     __shared__ float sr[32][33], sv[32][33], sd[32][33];
     __shared__ double w1[32], w2[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * 32;
-    {  // coalesced staging: warp w loads step t = w of the block's 32 streams
+    const int64_t ntile = (R + 31) / 32;
+    float pr = 0.0f, pv = 0.0f, pd = 1.0f, plv = 0.0f;
+    auto fetch = [&](int64_t tile) {  // coalesced: warp w loads step t = w of the tile's 32 streams
+        const int64_t s0 = tile * 32;
         const int64_t i = static_cast<int64_t>(w) * R + s0 + lane;
         const bool ok = s0 + lane < R;
-        sr[w][lane] = ok ? rew[i] : 0.0f;
-        sv[w][lane] = ok ? values[i] : 0.0f;
-        sd[w][lane] = ok ? done_f[i] : 1.0f;
+        pr = ok ? rew[i] : 0.0f;
+        pv = ok ? values[i] : 0.0f;
+        pd = ok ? done_f[i] : 1.0f;
+        plv = s0 + w < R ? last_value[s0 + w] : 0.0f;  // this warp's stream (broadcast)
+    };
+    double a1 = 0.0, a2 = 0.0;  // this lane's advantage sums, tiles in order
+    if (blockIdx.x < ntile) fetch(blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const int64_t s0 = tile * 32;
+        __syncthreads();  // the previous tile's transposed outputs were read
+        sr[w][lane] = pr;
+        sv[w][lane] = pv;
+        sd[w][lane] = pd;
+        const float lvf = plv;
+        __syncthreads();
+        if (tile + gridDim.x < ntile) fetch(tile + gridDim.x);  // prefetch the next tile
+        const int64_t st = s0 + w;  // this warp's stream; lane = step t
+        const bool live = st < R;
+        const int t = lane;
+        const bool done = sd[t][w] > 0.5f;
+        const double r = sr[t][w], v = sv[t][w];
+        const double lv = live ? static_cast<double>(lvf) : 0.0;
+        const double vnext = t == 31 ? lv : static_cast<double>(sv[t + 1][w]);
+        // GAE: acc_t = delta_t + (done_t ? 0 : gamma lambda) acc_{t+1}, acc_32 = 0
+        double a = done ? 0.0 : gamma * lam;
+        double b = (r + gamma * (done ? 0.0 : vnext)) - v;
+        rscan_affine(a, b, lane);
+        const double acc = b;  // + a * 0
+        // returns: run_t = r_t + (done_t ? 0 : gamma) run_{t+1}, run_32 = last_value
+        double ar = done ? 0.0 : gamma, br = r;
+        rscan_affine(ar, br, lane);
+        const double run = br + ar * lv;
+        __syncthreads();
+        sr[t][w] = static_cast<float>(run);  // reuse the tiles for the transposed stores
+        sv[t][w] = static_cast<float>(acc);
+        if (live && with_adv) {
+            a1 += acc;
+            a2 += acc * acc;
+        }
+        __syncthreads();
+        const int64_t i = static_cast<int64_t>(w) * R + s0 + lane;
+        if (s0 + lane < R) {
+            ret[i] = sr[w][lane];
+            if (with_adv) adv[i] = sv[w][lane];
+        }
     }
-    __syncthreads();
-    const int64_t st = s0 + w;  // this warp's stream; lane = step t
-    const bool live = st < R;
-    const int t = lane;
-    const bool done = sd[t][w] > 0.5f;
-    const double r = sr[t][w], v = sv[t][w];
-    const double lv = live ? static_cast<double>(last_value[st]) : 0.0;
-    const double vnext = t == 31 ? lv : static_cast<double>(sv[t + 1][w]);
-    // GAE: acc_t = delta_t + (done_t ? 0 : gamma lambda) acc_{t+1}, acc_32 = 0
-    double a = done ? 0.0 : gamma * lam;
-    double b = (r + gamma * (done ? 0.0 : vnext)) - v;
-    rscan_affine(a, b, lane);
-    const double acc = b;  // + a * 0
-    // returns: run_t = r_t + (done_t ? 0 : gamma) run_{t+1}, run_32 = last_value
-    double ar = done ? 0.0 : gamma, br = r;
-    rscan_affine(ar, br, lane);
-    const double run = br + ar * lv;
-    __syncthreads();
-    sr[t][w] = static_cast<float>(run);  // reuse the tiles for the transposed stores
-    sv[t][w] = static_cast<float>(acc);
-    double a1 = (live && with_adv) ? acc : 0.0, a2 = a1 * a1;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         a1 += __shfl_xor_sync(0xffffffffu, a1, off);
@@ -386,13 +412,6 @@ __global__ void __launch_bounds__(1024) k_gae_scan32(const float* __restrict__ r
         w2[w] = a2;
     }
     __syncthreads();
-    {
-        const int64_t i = static_cast<int64_t>(w) * R + s0 + lane;
-        if (s0 + lane < R) {
-            ret[i] = sr[w][lane];
-            if (with_adv) adv[i] = sv[w][lane];
-        }
-    }
     if (w == 0) {  // block sums in warp order, then the last block combines them (fixed order)
         double b1 = w1[lane], b2 = w2[lane];
 #pragma unroll
@@ -650,8 +669,11 @@ void fast_gae(cudaStream_t s, const float* rew, const float* values, const float
     // T = 32 with few streams (the episode: latency-bound): warp-shuffle reverse scan, lane = step.
     // Many streams (bandwidth-bound sweeps): the chunked thread-per-stream recurrence, which needs
     // no shuffles (the scan's 40 shuffles per stream would cap it at ~20% of HBM bandwidth).
+    // T = 32 and up to 65536 streams (the C2 / C3 / C5 episodes): the warp-shuffle scan, one
+    // 32-stream tile per block (latency regime). Many streams: the thread-per-stream recurrence
+    // streams HBM faster (2^26 rows: 5.1 vs 1.8 TB/s, bench.py hbm_kernels).
     if (TR == 32 * R && done_counter && R <= 65536) {
-        const int nb32 = static_cast<int>((R + 31) / 32);
+        const int nb32 = static_cast<int>(std::min<int64_t>((R + 31) / 32, 2 * 148));
         k_gae_scan32<<<nb32, 1024, 0, s>>>(rew, values, done_f, last_value, R, gamma, lam, adv, ret, with_adv,
                                            block_sums, stats, done_counter);
         return;
@@ -666,6 +688,14 @@ void fast_gae(cudaStream_t s, const float* rew, const float* values, const float
         k_fast_gae<8, 4><<<nb, 256, 0, s>>>(rew, values, done_f, last_value, TR / R, R, gamma, lam, adv, ret,
                                             with_adv, block_sums, stats, done_counter);
     if (with_adv && !done_counter) k_adv_stats<<<1, 256, 0, s>>>(block_sums, nb, TR, stats);
+}
+
+void fast_gae_scan32(cudaStream_t s, const float* rew, const float* values, const float* done_f,
+                     const float* last_value, int64_t R, double gamma, double lam, float* adv, float* ret,
+                     bool with_adv, double* block_sums, double* stats, unsigned* done_counter) {
+    const int nb32 = static_cast<int>(std::min<int64_t>((R + 31) / 32, 2 * 148));
+    k_gae_scan32<<<nb32, 1024, 0, s>>>(rew, values, done_f, last_value, R, gamma, lam, adv, ret, with_adv,
+                                       block_sums, stats, done_counter);
 }
 
 void fast_rep_adv_stats(cudaStream_t s, const float* adv, int64_t T, int64_t E, const int64_t* rep_off,

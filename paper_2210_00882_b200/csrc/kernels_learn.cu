@@ -246,10 +246,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
     constexpr int kGroups = groups_for(MODE);
     constexpr int kEpiWarps = 4 * kGroups;
     constexpr int kThreads = threads_for(MODE);
-#ifndef FLW_LEARN_ZPRE  // forward epilogue: one TMEM round trip for all 64 columns (1: all modes)
-#define FLW_LEARN_ZPRE 0
+#ifndef FLW_LEARN_ZPRE  // forward epilogue: one TMEM round trip for all 64 columns (A/B: no gain,
+#define FLW_LEARN_ZPRE 0  // values pass 0.1445 -> 0.1457 ms per episode)
 #endif
-    constexpr bool kZPre = MODE == 0 || FLW_LEARN_ZPRE;
+    constexpr bool kZPre = FLW_LEARN_ZPRE;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar, zbar;
     __shared__ uint32_t tslot;

@@ -5,9 +5,9 @@
 //                 layer-wise and split-GEMM rollouts) over E envs: (8S+9) B/env-step (state in/out,
 //                 action, reward, done) + 4A logits in + 4 logp out = 173 B (the kernel keeps the
 //                 env state in f64, so it moves more than this)
-//   gae_scan32  : k_gae_scan32 (the episode's GAE + returns + advantage statistics, T = 32) at its
-//                 largest size, R = 65536 streams, four rotating buffer sets (> L2): 17 B/row + 4 B/stream
-//   gae         : k_fast_gae<8,4> (fast_gae's kernel when R > 65536, e.g. MAPPO n >= 32) at T*R rows
+//   gae_scan32  : k_gae_scan32 (the episode's GAE + returns + advantage statistics, T = 32) at
+//                 T*R rows (>= 2^22 rows: inputs > L2; smaller: four rotating sets): 17 B/row + 4 B/stream
+//   gae         : k_fast_gae<8,4> (fast_gae's kernel for T != 32) at T*R rows
 //   reduce_adam : k_reduce_adam (the fused per-iteration update: partial reduction + Adam with f64
 //                 moments) over P params and 8 partial slots: 44 B/param (g in, p, m, v in/out) + 4 B
 //                 per partial slot
@@ -209,10 +209,10 @@ void microbench(const std::string& which, int64_t n, int iters, double* ms, doub
         a.env.synth_b = tab;
         *ms = time_launches([&] { exact_rollout(0, ctx, a); }, iters);
         *bytes = static_cast<double>(n) * (8.0 * S + 9 + 4.0 * A + 4);
-    } else if (which == "gae_scan32") {  // the episode's GAE kernel at R = n / 32 <= 65536 streams
-        const int64_t T = 32, R = std::min<int64_t>(n / T, 65536);
-        constexpr int kSets = 4;  // 4 x 42 MB > L2: every launch reads from HBM
-        float *r[kSets], *v[kSets], *dn[kSets], *lv[kSets], *adv[kSets], *ret[kSets];
+    } else if (which == "gae_scan32") {  // the episode's GAE kernel (T = 32) at R = n / 32 streams
+        const int64_t T = 32, R = n / T;
+        const int kSets = n <= (1 << 22) ? 4 : 1;  // small sizes: 4 rotating sets > L2
+        float *r[4], *v[4], *dn[4], *lv[4], *adv[4], *ret[4];
         for (int k = 0; k < kSets; ++k) {
             r[k] = d.get<float>(T * R);
             v[k] = d.get<float>(T * R);
@@ -230,10 +230,10 @@ void microbench(const std::string& which, int64_t n, int iters, double* ms, doub
         unsigned* cnt = d.get<unsigned>(1);
         FLW_CUDA(cudaMemset(cnt, 0, sizeof(unsigned)));
         FLW_CUDA(cudaGetLastError());
-        int it = 0;
+        int it = 0;  // k_gae_scan32 directly (fast_gae routes R > 65536 to the thread-per-stream kernel)
         *ms = time_launches([&] {
             const int k = it++ % kSets;
-            fast_gae(0, r[k], v[k], dn[k], lv[k], T * R, R, 0.99, 0.95, adv[k], ret[k], true, bs, st, cnt);
+            fast_gae_scan32(0, r[k], v[k], dn[k], lv[k], R, 0.99, 0.95, adv[k], ret[k], true, bs, st, cnt);
         }, iters);
         *bytes = static_cast<double>(T * R) * 17.0 + static_cast<double>(R) * 4.0;
     } else if (which == "reduce_adam" || which == "exchange_adam") {  // the fused update kernels, P = n

@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(128) k_sum_adam(P2pArgs a, int nchunks) {
         if (threadIdx.x == 0) gave_up = 0;
         __syncthreads();
         for (int r = threadIdx.x; r < a.k; r += blockDim.x)
-            while (ld_acquire_sys(flag + r) < epoch) {
-                if (*a.abort_flag) {  // the host aborted the group: leave the state untouched
+            for (uint32_t spin = 1; ld_acquire_sys(flag + r) < epoch; ++spin) {
+                // the abort word lives in host memory (a PCIe read): polled every 512 spins only
+                if ((spin & 511u) == 0 && *a.abort_flag) {  // the host aborted the group
                     gave_up = 1;
                     break;
                 }

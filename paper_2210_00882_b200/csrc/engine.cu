@@ -833,7 +833,8 @@ void Engine::enq_learn_fast() {
     const int H0 = s.cdims[1], J = s.state_w;
     if (cfast_) {
         // P[(T+1)*E, H0] = joint . W_J on the tensor cores (bf16 operands, f32 accumulation)
-        wide_to_bf16(stream_, b.joint, (T_ + 1) * E_, J, b.jb, b.jld);
+        if (learn_iter_ == 0)  // the joint rows change once per episode (the rollout)
+            wide_to_bf16(stream_, b.joint, (T_ + 1) * E_, J, b.jb, b.jld);
         wide_to_bf16(stream_, b.params + s.woff[1][0], J, H0, b.wjb, b.hld0);
         TgEpilogue pe;
         pe.mode = kTgStoreF32;
@@ -1061,12 +1062,17 @@ void Engine::alloc_wide_policy(int64_t xrows, int maxw) {
     const ProgramShape& s = shape_;
     auto pad8 = [](int64_t x) { return (x + 7) / 8 * 8; };
     b.wb_p = b.alloc<__nv_bfloat16>(b.wpol.wbytes);
-    b.xld = pad8(s.obs_dim);
+    // activation buffers carry a column of ones after the data (the bias-gradient row of the
+    // weight-gradient GEMM)
+    b.xld = pad8(s.obs_dim + 1);
     b.xb = b.alloc<__nv_bfloat16>(xrows * b.xld);
     for (int l = 0; l + 1 < s.L; ++l) {
-        b.hld_p.push_back(pad8(s.pdims[l + 1]));
+        b.hld_p.push_back(pad8(s.pdims[l + 1] + 1));
         b.hw_p.push_back(b.alloc<__nv_bfloat16>(TR_ * b.hld_p.back()));
     }
+    FLW_CUDA(cudaDeviceSynchronize());  // the allocations' memsets before the fills on stream_
+    wide_fill_col(stream_, b.xb, xrows, b.xld, s.obs_dim, 1.0f);
+    for (int l = 0; l + 1 < s.L; ++l) wide_fill_col(stream_, b.hw_p[l], TR_, b.hld_p[l], s.pdims[l + 1], 1.0f);
     for (int l = 0; l <= s.L; ++l) maxw = std::max(maxw, s.pdims[l]);
     b.dzld = pad8(maxw);
     b.wdz0 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
@@ -1088,9 +1094,11 @@ void Engine::alloc_wide() {
     alloc_wide_policy(Rc, maxw);  // the critic reads the same input rows (+ last_next)
     b.wb_c = b.alloc<__nv_bfloat16>(b.wcrit.wbytes);
     for (int l = 0; l + 1 < L; ++l) {
-        b.hld_c.push_back(pad8(s.cdims[l + 1]));
+        b.hld_c.push_back(pad8(s.cdims[l + 1] + 1));
         b.hw_c.push_back(b.alloc<__nv_bfloat16>(Rc * b.hld_c.back()));
     }
+    FLW_CUDA(cudaDeviceSynchronize());
+    for (int l = 0; l + 1 < L; ++l) wide_fill_col(stream_, b.hw_c[l], Rc, b.hld_c[l], s.cdims[l + 1], 1.0f);
     alloc_split_rollout();
     b.values = b.alloc<float>(Rc);  // values | last_value: one critic forward over all rows
     b.last_value = b.values + TR_;
@@ -1140,15 +1148,17 @@ void Engine::wide_backward(const WideNet& n, const __nv_bfloat16* wb, const std:
     for (int m = n.L - 1; m >= 0; --m) {
         const int din = n.din[m], dout = n.dout[m];
         // dW_m = H_{m-1}^T dZ_m (K = rows split `splits` ways) -> partial slots
-        const TgOperand Hin{m == 0 ? b.xb : H[m - 1], TR_, din, m == 0 ? b.xld : ld[m - 1], kTgBF16};
+        // [dW_m ; db_m] = [H_{m-1} | 1]^T dZ_m (K = rows split `splits` ways) -> partial slots:
+        // column din of every activation buffer holds ones, so output row din is the bias
+        // gradient (the column sums of dZ_m), landing at boff = woff + din*dout
+        const TgOperand Hin{m == 0 ? b.xb : H[m - 1], TR_, din + 1, m == 0 ? b.xld : ld[m - 1], kTgBF16};
         const TgOperand Dz{dz, TR_, dout, b.dzld, kTgBF16};
         TgEpilogue e;
         e.mode = kTgStoreF32;
         e.c32 = part + (n.woff[m] - n.woff[0]);
         e.ldc32 = dout;
         e.split_stride = pstride;
-        tgemm(stream_, Hin, true, Dz, true, din, dout, TR_, splits, e, bn_for(dout));
-        wide_colsum(stream_, dz, TR_, dout, b.dzld, splits, part + (n.boff[m] - n.woff[0]), pstride);
+        tgemm(stream_, Hin, true, Dz, true, din + 1, dout, TR_, splits, e, bn_for(dout));
         if (m == 0) break;
         const TgOperand Wk{wb + n.wofs[m], din, dout, n.wld[m], kTgBF16};
         TgEpilogue g;
@@ -1195,7 +1205,7 @@ void Engine::enq_learn_policy_wide(float* loss_partials) {
     const ProgramShape& s = shape_;
     WideNet none{};
     wide_build_weights(stream_, b.params, b.wpol, b.wb_p, none, nullptr);
-    wide_to_bf16(stream_, b.states, TR_, s.obs_dim, b.xb, b.xld);
+    if (learn_iter_ == 0) wide_to_bf16(stream_, b.states, TR_, s.obs_dim, b.xb, b.xld);  // once per episode
     wide_forward(b.wpol, b.wb_p, b.hw_p, b.hld_p, TR_, b.wlogits);
     wide_loss_rows(s.algo != Algo::A3c ? kNetPolicyPpo : kNetPolicyA3c, b.wlogits, s.n_actions, loss_partials);
     wide_backward(b.wpol, b.wb_p, b.hw_p, b.hld_p, b.part_p, s.P_policy);
@@ -1212,7 +1222,8 @@ void Engine::enq_learn_wide() {
     const bool ppo = s.algo != Algo::A3c;
     const int64_t Rc = TR_ + R_;
     wide_build_weights(stream_, b.params, b.wpol, b.wb_p, b.wcrit, b.wb_c);
-    wide_to_bf16(stream_, b.states, Rc, s.obs_dim, b.xb, b.xld);  // states blocks 0..T (last_next)
+    if (learn_iter_ == 0)  // states blocks 0..T (last_next): once per episode
+        wide_to_bf16(stream_, b.states, Rc, s.obs_dim, b.xb, b.xld);
     probe_begin("critic_fwd");
     wide_forward(b.wcrit, b.wb_c, b.hw_c, b.hld_c, Rc, b.values);
     probe_end();

@@ -33,13 +33,34 @@ __global__ void k_wide_weights(const float* __restrict__ params, WideNet n0, __n
     }
 }
 
+// row-major f32 [rows, cols] -> bf16 [rows, ld]: one warp per row, consecutive lanes on
+// consecutive columns (coalesced both ways, no per-element division)
 __global__ void k_wide_to_bf16(const float* __restrict__ x, int64_t rows, int cols, __nv_bfloat16* out, int64_t ld) {
-    const int64_t n = rows * cols;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t r = i / cols, c = i % cols;
-        out[r * ld + c] = __float2bfloat16(x[i]);
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+        const float* xr = x + r * cols;
+        __nv_bfloat16* orow = out + r * ld;
+        for (int c = 2 * lane; c < cols; c += 64) {
+            if (c + 1 < cols) {
+                const float2 v = make_float2(__ldg(xr + c), __ldg(xr + c + 1));
+                if ((ld & 1) == 0)
+                    *reinterpret_cast<__nv_bfloat162*>(orow + c) = __floats2bfloat162_rn(v.x, v.y);
+                else {
+                    orow[c] = __float2bfloat16(v.x);
+                    orow[c + 1] = __float2bfloat16(v.y);
+                }
+            } else {
+                orow[c] = __float2bfloat16(__ldg(xr + c));
+            }
+        }
     }
+}
+
+__global__ void k_wide_fill_col(__nv_bfloat16* p, int64_t rows, int64_t ld, int64_t col, float v) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[r * ld + col] = __float2bfloat16(v);
 }
 
 __global__ void k_wide_split_input(const float* __restrict__ x, int64_t rows, int cols, __half* out, int64_t seg) {
@@ -235,9 +256,13 @@ void wide_build_weights(cudaStream_t s, const float* params, const WideNet& n0, 
 }
 
 void wide_to_bf16(cudaStream_t s, const float* x, int64_t rows, int cols, __nv_bfloat16* out, int64_t ld) {
-    const int64_t n = rows * cols;
-    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+    const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, 148 * 16));
     k_wide_to_bf16<<<blocks, 256, 0, s>>>(x, rows, cols, out, ld);
+}
+
+void wide_fill_col(cudaStream_t s, __nv_bfloat16* p, int64_t rows, int64_t ld, int64_t col, float v) {
+    const int blocks = static_cast<int>(std::min<int64_t>((rows + 255) / 256, 148 * 8));
+    k_wide_fill_col<<<blocks, 256, 0, s>>>(p, rows, ld, col, v);
 }
 
 void wide_split_input(cudaStream_t s, const float* x, int64_t rows, int cols, __half* out, int64_t seg) {

@@ -42,6 +42,7 @@ struct WideLossArgs {
 void wide_build_weights(cudaStream_t s, const float* params, const WideNet& n0, __nv_bfloat16* w0, const WideNet& n1,
                         __nv_bfloat16* w1);
 void wide_to_bf16(cudaStream_t s, const float* x, int64_t rows, int cols, __nv_bfloat16* out, int64_t ld);
+void wide_fill_col(cudaStream_t s, __nv_bfloat16* p, int64_t rows, int64_t ld, int64_t col, float v);
 int wide_loss_blocks(int64_t rows);
 // f32 -> f16 hi | lo | hi segments of width seg (x = hi + lo to ~2^-22): the split A operand
 void wide_split_input(cudaStream_t s, const float* x, int64_t rows, int cols, __half* out, int64_t seg);

@@ -59,7 +59,7 @@ def test_mappo_matches_reference_trace():
             _close(p + "params", eng.params(), tr[p + "params"])
 
 
-@pytest.mark.parametrize("n_agents", [2, 4])
+@pytest.mark.parametrize("n_agents", [2, 4, 6, 9])  # n > 4: the block-per-env step kernel
 def test_mappo_episodes_match_oracle(n_agents):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")

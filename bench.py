@@ -345,15 +345,32 @@ def bench_ours(args, world, rank, local):
     value = total * T_STEPS * args.steps / (dev_ms / 1e3)
     stats = eng.stats()
 
-    # e2e through the public per-unit C-ABI with host round trips every step: the episode index
-    # goes host->device and the episode reward sum comes back device->host each episode.
+    # e2e through the reference's public API (flw_run_local, fraglow.h:55) on one GPU: a dp-d
+    # program runs K episodes with the host episode gate - per episode the episode index goes
+    # host->device and the reward sum device->host; per run the initial params go in and the
+    # final params come out. N > 1 (one process per GPU): the per-unit seam flw_dpd_run_episode
+    # with the same per-episode round trips (flw_run_local drives in-process GPUs only).
     barrier(world)
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        eng.run_episode(args.warmup + args.steps + i)
-    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    e2e = {"value": total * T_STEPS * args.steps / e2e_s, "unit": "env-steps/s", "h2d_bytes_per_step": 8,
-           "d2h_bytes_per_step": 8}
+    P = eng.param_count
+    if world == 1:
+        prog = Program(algo_config(total, episodes=args.steps),
+                       {"workers": ["local"], "slots_per_worker": {"cpu": 1, "accel": 1},
+                        "distribution_policy": "dp-d", "numerics": args.numerics})
+        prog.run_local(seed=args.seed, episodes=2)  # engine build + graph capture (untimed)
+        t0 = time.perf_counter()
+        _, summ = prog.run_local(seed=args.seed, episodes=args.steps)
+        e2e_s = time.perf_counter() - t0
+        assert summ["episodes"] == args.steps
+        e2e = {"value": total * T_STEPS * args.steps / e2e_s, "unit": "env-steps/s", "api": "flw_run_local",
+               "h2d_bytes_per_step": 8 + 4 * P / args.steps, "d2h_bytes_per_step": 8 + 4 * P / args.steps}
+        prog.close()
+    else:
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            eng.run_episode(args.warmup + args.steps + i)
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+        e2e = {"value": total * T_STEPS * args.steps / e2e_s, "unit": "env-steps/s", "api": "flw_dpd_run_episode",
+               "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 8}
 
     # per-kernel shares (roofline, kernel_shares): a separately captured graph with CUDA-event
     # probes around the main kernels (external event-record nodes), outside the timed regions

@@ -1078,7 +1078,11 @@ void Engine::alloc_wide_policy(int64_t xrows, int maxw) {
     b.wdz0 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
     b.wdz1 = b.alloc<__nv_bfloat16>(TR_ * b.dzld);
     b.wlogits = b.alloc<float>(TR_ * s.n_actions);
-    b.wsplits = static_cast<int>(std::min<int64_t>(64, (TR_ + 63) / 64));  // = tgemm's clamp
+    // partial slots of the weight-gradient GEMMs (<= tgemm's clamp of one k-block per split):
+    // 128 for nets of <= 200 k parameters (one 148-CTA wave for 64-wide layers), 64 above (the
+    // reduction reads every slot)
+    const int64_t pmax = std::max<int64_t>(s.P_policy, s.P - s.P_policy);
+    b.wsplits = static_cast<int>(std::min<int64_t>(pmax <= 200000 ? 128 : 64, (TR_ + 63) / 64));
 }
 
 void Engine::alloc_wide() {
@@ -1158,7 +1162,11 @@ void Engine::wide_backward(const WideNet& n, const __nv_bfloat16* wb, const std:
         e.c32 = part + (n.woff[m] - n.woff[0]);
         e.ldc32 = dout;
         e.split_stride = pstride;
-        tgemm(stream_, Hin, true, Dz, true, din + 1, dout, TR_, splits, e, bn_for(dout));
+        // one wave: this layer's K split so that (M tiles x N tiles x splits) <= 148; rows of
+        // the partial buffer beyond its split count are never written (stay zero)
+        const int64_t tiles = ((din + 1 + 127) / 128) * ((dout + bn_for(dout) - 1) / bn_for(dout));
+        const int lsplits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(splits, 148 / tiles)));
+        tgemm(stream_, Hin, true, Dz, true, din + 1, dout, TR_, lsplits, e, bn_for(dout));
         if (m == 0) break;
         const TgOperand Wk{wb + n.wofs[m], din, dout, n.wld[m], kTgBF16};
         TgEpilogue g;

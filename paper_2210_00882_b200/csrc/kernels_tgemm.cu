@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <mutex>
 #include <vector>
@@ -37,8 +38,25 @@ namespace {
 struct TgArgs {
     int64_t M, N;
     int kblocks, mtiles, ntiles, splits;
+    int tma_store;  // bf16 outputs leave through shared memory + TMA stores (map mc)
+    // B resident (one N tile, no split-K, B small): the whole B loads once per CTA at shared
+    // offset 0 and the ring streams A only
+    int bres;
+    int nstages;           // ring stages
+    uint32_t stage_bytes;  // per stage (A, or A + B)
+    uint32_t off_ring;     // first stage
+    uint32_t off_stg;      // epilogue output staging
     TgEpilogue epi;
 };
+
+constexpr int kTgMaxStages = 8;
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(umma::smem_u32(src))
+                 : "memory");
+}
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
     asm volatile(
@@ -104,18 +122,21 @@ __host__ __device__ constexpr uint32_t tg_stage_bytes() {
 
 template <int BN, int DT, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kTgThreads, 1)
-    k_tgemm(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, const TgArgs a) {
-    constexpr int S = tg_stages<BN>();
-    constexpr uint32_t kStage = tg_stage_bytes<BN>();
+    k_tgemm(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
+            const __grid_constant__ CUtensorMap mc, const TgArgs a) {
+    const int S = a.nstages;
+    const uint32_t kStage = a.stage_bytes;
     constexpr uint32_t kABytes = 128u * 128u;
+    constexpr uint32_t kBBlock = static_cast<uint32_t>(BN) * 128u;  // one k-block of B
     constexpr int esz = DT == kTgF32 ? 4 : 2;
     constexpr int BK = 128 / esz;  // K elements per k-block (one 128-byte row)
     constexpr int UK = 32 / esz;   // K elements per MMA
     constexpr int kAtom = 128 / esz;
     constexpr uint32_t kCols = 2 * BN;  // two accumulators
+    const uint32_t kStageOff = a.off_stg;  // epilogue output staging: [4 warps][2][32 x 64 B]
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t full[S], empty[S], tfull[2], tempty[2];
+    __shared__ uint64_t full[kTgMaxStages], empty[kTgMaxStages], tfull[2], tempty[2], bfull;
     __shared__ uint32_t tslot;
     __shared__ __align__(16) float sbias[BN];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -130,6 +151,7 @@ __global__ void __launch_bounds__(kTgThreads, 1)
             umma::mbar_init(&tfull[i], 1);
             umma::mbar_init(&tempty[i], 4);
         }
+        umma::mbar_init(&bfull, 1);
         umma::fence_barrier_init();
         prefetch_map(&ma);
         prefetch_map(&mb);
@@ -155,12 +177,24 @@ __global__ void __launch_bounds__(kTgThreads, 1)
         if (umma::elect_one()) {
             int stage = 0;
             uint32_t ph = 0;
+            if (a.bres && blockIdx.x < items) {  // the whole B (one N tile), once
+                umma::mbar_expect_tx(&bfull, kBBlock * static_cast<uint32_t>(a.kblocks));
+                for (int kb = 0; kb < a.kblocks; ++kb) {
+                    uint8_t* sb = smem + kb * kBBlock;
+                    if constexpr (!BMN) {
+                        tma_load_2d(sb, &mb, kb * BK, 0, &bfull);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BN / kAtom; ++j) tma_load_2d(sb + j * (BK * 128), &mb, j * kAtom, kb * BK, &bfull);
+                    }
+                }
+            }
             for (int64_t wi = blockIdx.x; wi < items; wi += gridDim.x) {
                 int mt, nt, kb0, kb1;
                 decode(wi, mt, nt, kb0, kb1);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     umma::mbar_wait(&empty[stage], ph ^ 1);
-                    uint8_t* sa = smem + stage * kStage;
+                    uint8_t* sa = smem + a.off_ring + stage * kStage;
                     uint8_t* sb = sa + kABytes;
                     umma::mbar_expect_tx(&full[stage], kStage);
                     if constexpr (!AMN) {
@@ -170,7 +204,8 @@ __global__ void __launch_bounds__(kTgThreads, 1)
                         for (int j = 0; j < 128 / kAtom; ++j)
                             tma_load_2d(sa + j * (BK * 128), &ma, mt * 128 + j * kAtom, kb * BK, &full[stage]);
                     }
-                    if constexpr (!BMN) {
+                    if (a.bres) {
+                    } else if constexpr (!BMN) {
                         tma_load_2d(sb, &mb, kb * BK, nt * BN, &full[stage]);
                     } else {
 #pragma unroll
@@ -191,6 +226,7 @@ __global__ void __launch_bounds__(kTgThreads, 1)
         uint32_t ph = 0, tph[2] = {0, 0};
         int acc = 0;
         const uint32_t sbase = umma::smem_u32(smem);
+        if (a.bres && blockIdx.x < items) umma::mbar_wait(&bfull, 0);
         for (int64_t wi = blockIdx.x; wi < items; wi += gridDim.x) {
             int mt, nt, kb0, kb1;
             decode(wi, mt, nt, kb0, kb1);
@@ -201,7 +237,8 @@ __global__ void __launch_bounds__(kTgThreads, 1)
             for (int kb = kb0; kb < kb1; ++kb) {
                 umma::mbar_wait(&full[stage], ph);
                 umma::fence_after_sync();
-                const uint32_t sa = sbase + stage * kStage, sb = sa + kABytes;
+                const uint32_t sa = sbase + a.off_ring + stage * kStage;
+                const uint32_t sb = a.bres ? sbase + kb * kBBlock : sa + kABytes;
 #pragma unroll
                 for (int k = 0; k < BK / UK; ++k) {
                     const uint64_t ad = AMN ? desc_sw128(sa + k * (UK * 128), BK * 128, 1024)
@@ -274,7 +311,8 @@ __global__ void __launch_bounds__(kTgThreads, 1)
                     }
                 }
                 umma::tmem_ld_wait();
-                if (!mok) continue;
+                // (TMA-stored chunks keep every lane: the store clips rows beyond m_store)
+                if (!mok && !(a.tma_store && (e.mode == kTgBiasAct || e.mode == kTgActGrad))) continue;
                 if (use_bias) {
 #pragma unroll
                     for (int j = 0; j < 32; j += 4) {
@@ -368,6 +406,28 @@ __global__ void __launch_bounds__(kTgThreads, 1)
                         }
                     }
                 }
+                if (a.tma_store) {
+                    // this warp's 32 rows x 32 columns (64 B per row) into its staging buffer in
+                    // the SWIZZLE_64B layout (16-byte chunk k of row r at k ^ ((r >> 1) & 3)),
+                    // then one TMA store; the other buffer's store may still be reading
+                    uint8_t* stg = smem + kStageOff + (q * 2 + (c0 >> 5 & 1)) * 2048;
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        *reinterpret_cast<uint4*>(stg + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) =
+                            make_uint4(umma::pack_bf16x2(v[8 * k], v[8 * k + 1]),
+                                       umma::pack_bf16x2(v[8 * k + 2], v[8 * k + 3]),
+                                       umma::pack_bf16x2(v[8 * k + 4], v[8 * k + 5]),
+                                       umma::pack_bf16x2(v[8 * k + 6], v[8 * k + 7]));
+                    umma::fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&mc, static_cast<int>(nb), static_cast<int>(mt * 128 + 32 * q), stg);
+                        umma::bulk_commit();
+                    }
+                    continue;
+                }
                 __nv_bfloat16* d16 = e.c16 + m * e.ldc16 + nb;
                 if (nv == 32 && (e.ldc16 & 7) == 0) {
 #pragma unroll
@@ -386,6 +446,8 @@ __global__ void __launch_bounds__(kTgThreads, 1)
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_u32(&tempty[acc])) : "memory");
             acc ^= 1;
         }
+        if (a.tma_store && lane == 0) umma::bulk_wait_all();  // the staged outputs are written
+        __syncwarp();
     }
     umma::fence_before_sync();
     __syncthreads();
@@ -406,7 +468,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-CUtensorMap make_map(const TgOperand& o, uint32_t box_inner, uint32_t box_outer) {
+CUtensorMap make_map(const TgOperand& o, uint32_t box_inner, uint32_t box_outer,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     const int esz = o.dt == kTgF32 ? 4 : 2;
     if ((reinterpret_cast<uintptr_t>(o.ptr) & 15) != 0 || (o.ld * esz) % 16 != 0)
         throw Error(Errc::Config, "tgemm: operand base / row stride must be 16-byte aligned");
@@ -419,7 +482,7 @@ CUtensorMap make_map(const TgOperand& o, uint32_t box_inner, uint32_t box_outer)
                                    : (o.dt == kTgF16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
     const CUresult r = encode_fn()(&m, ty, 2,
                                    const_cast<void*>(o.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(Errc::Runtime, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
     return m;
@@ -436,18 +499,45 @@ int sm_count() {
 }
 
 template <int BN, int DT, bool AMN, bool BMN>
-void launch_tg(cudaStream_t s, const TgOperand& A, const TgOperand& B, const TgArgs& a, int grid_cap) {
+void launch_tg(cudaStream_t s, const TgOperand& A, const TgOperand& B, TgArgs a, int grid_cap) {
     constexpr int esz = DT == kTgF32 ? 4 : 2;
     constexpr uint32_t BK = 128 / esz, atom = 128 / esz;
     const CUtensorMap ma = AMN ? make_map(A, atom, BK) : make_map(A, BK, 128);
     const CUtensorMap mb = BMN ? make_map(B, atom, BK) : make_map(B, BK, BN);
-    const size_t smem = static_cast<size_t>(tg_stages<BN>()) * tg_stage_bytes<BN>() + 1024;
+    // A/B option (FLW_TG_TMA_STORE=1): bf16 outputs leave through shared memory and TMA stores
+    // (32 x 32 boxes, SWIZZLE_64B). Measured: H = 256 layer-wise learn slower (forward GEMM 42 ->
+    // 50 us), MAPPO n = 64 2% faster - off by default.
+    static const bool tma_store_on = std::getenv("FLW_TG_TMA_STORE") != nullptr;
+    const TgEpilogue& e = a.epi;
+    CUtensorMap mc = ma;
+    a.tma_store = 0;
+    if (tma_store_on && (e.mode == kTgBiasAct || e.mode == kTgActGrad) && !e.c32 && e.c16 &&
+        (reinterpret_cast<uintptr_t>(e.c16) & 15) == 0 && (e.ldc16 * 2) % 16 == 0) {
+        const int64_t ms = e.m_store >= 0 ? e.m_store : a.M, ns = e.n_store >= 0 ? e.n_store : a.N;
+        mc = make_map(TgOperand{e.c16, ms, ns, e.ldc16, kTgBF16}, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        a.tma_store = 1;
+    }
+    constexpr uint32_t kBBlock = static_cast<uint32_t>(BN) * 128u, kAB = 128u * 128u;
+    constexpr uint32_t kBudget = 227u * 1024u - 4096u;  // dynamic shared memory (static: barriers, bias)
+    const uint32_t bbytes = kBBlock * static_cast<uint32_t>(a.kblocks);
+    a.bres = a.ntiles == 1 && a.splits == 1 && a.mtiles > sm_count() && bbytes <= 128u * 1024u;
+    if (a.bres) {
+        a.off_ring = (bbytes + 1023u) / 1024u * 1024u;
+        a.stage_bytes = kAB;
+        a.nstages = static_cast<int>(std::min<uint32_t>(kTgMaxStages, (kBudget - a.off_ring - 16384u - 1024u) / kAB));
+    } else {
+        a.off_ring = 0;
+        a.stage_bytes = tg_stage_bytes<BN>();
+        a.nstages = tg_stages<BN>();
+    }
+    a.off_stg = a.off_ring + static_cast<uint32_t>(a.nstages) * a.stage_bytes;
+    const size_t smem = static_cast<size_t>(a.off_stg) + 16384 + 1024;
     auto kern = k_tgemm<BN, DT, AMN, BMN>;
     FLW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const int64_t items = static_cast<int64_t>(a.mtiles) * a.ntiles * a.splits;
     const int cap = grid_cap > 0 ? grid_cap : sm_count();
     const int grid = static_cast<int>(std::min<int64_t>(items, cap));
-    kern<<<grid, kTgThreads, smem, s>>>(ma, mb, a);
+    kern<<<grid, kTgThreads, smem, s>>>(ma, mb, mc, a);
     FLW_CUDA(cudaGetLastError());
 }
 

@@ -275,7 +275,7 @@ void wide_build_split_weights(cudaStream_t s, const float* params, const WideNet
     k_wide_split_weights<<<64, 256, 0, s>>>(params, n, ws);
 }
 
-int wide_loss_blocks(int64_t rows) { return static_cast<int>(std::min<int64_t>(74, (rows + 255) / 256)); }
+int wide_loss_blocks(int64_t rows) { return static_cast<int>(std::min<int64_t>(148 * 4, (rows + 255) / 256)); }
 
 void wide_loss(cudaStream_t s, const WideLossArgs& a) {
     k_wide_loss<<<wide_loss_blocks(a.rows), 256, 0, s>>>(a);

@@ -182,3 +182,42 @@ def test_learning_gridline_reaches_goal():
                           "numerics": "exact"})
     csv, s = prog.run_local(seed=1, reward_threshold=0.9)
     assert s["time_to_threshold_ms"] >= 0, csv
+
+
+def test_degenerate_advantages_skip_normalisation():
+    """normalize_advantages' `std < 1e-8` branch (rl.cpp:104): T = 1 step, no env reaches the
+    goal (rewards 0), the critic outputs the constant 0.5 (zero weights, last bias 0.5), so every
+    advantage is (gamma - 1) * 0.5 and their std is 0 -> left unnormalised (normalising would
+    give 0). The exact engine matches the oracle bit-for-bit (grads, loss, adv); the fast engine
+    keeps the unnormalised advantages too."""
+    _need_gpu()
+    from paper_2210_00882_b200 import DpdEngine
+
+    algo = {"algorithm": "ppo", "env": {"type": "gridline", "num": 32, "params": {"length": 16}},
+            "learner": {"params": {"gamma": 0.9}}, "policy_net": {"hidden": [16, 16]},
+            "loop": {"episodes": 1, "steps_per_episode": 1}}
+    ex = DpdEngine(algo, seed=4, numerics="exact")
+    u = pyoracle.Unit(algo, 4)
+    p = u.params()
+    dims_c = [1, 16, 16, 1]
+    pc = sum(i * o + o for i, o in zip(dims_c[:-1], dims_c[1:]))
+    p[-pc:] = 0.0
+    p[-1] = 0.5  # critic output bias
+    ex.set_params(p)
+    u.set_params(p)
+    fa = DpdEngine(algo, seed=4, numerics="fast")
+    fa.set_params(p)
+    for e in (ex, fa):
+        e.reset(0)
+        e.step(0, 0)
+    u.reset(0)
+    u.step(0, 0)
+    g_o = u.learn_grads(0, 0)
+    ex.learn_grads(0, 0)
+    fa.learn_grads(0, 0)
+    want_adv = (0.9 - 1.0) * 0.5
+    np.testing.assert_allclose(u.get("adv"), want_adv, rtol=1e-6)  # (f32-rounded terms)
+    np.testing.assert_array_equal(ex.get("adv"), u.get("adv"))
+    np.testing.assert_array_equal(ex.get("grads"), g_o)
+    np.testing.assert_array_equal(ex.get("loss"), u.get("loss"))
+    np.testing.assert_allclose(fa.get("adv"), want_adv, rtol=1e-6)

@@ -70,3 +70,12 @@ def test_tgemm_weight_grad_shape():
     _need_gpu()
     err, tol = _run(256, 256, 16384, 1, 1, 0, 16, 256)
     assert err <= tol, err
+
+
+@pytest.mark.parametrize("a_mn,b_mn,bn", [(0, 1, 256), (0, 0, 128), (0, 1, 64)])
+def test_tgemm_b_resident(a_mn, b_mn, bn):
+    """More 128-row tiles than SMs, one N tile, no split-K: B loads once per CTA into shared
+    memory and the ring streams A only (the layer-wise forward / dH GEMMs)."""
+    _need_gpu()
+    err, tol = _run(128 * 160 + 5, bn if bn < 256 else 200, 256, a_mn, b_mn, 0, 1, bn, seed=3)
+    assert err <= tol, err

@@ -70,6 +70,11 @@ struct Engine::Bufs {
     float* jpart = nullptr;                                        // dW_J split-K partials
     int64_t jld = 0, hld0 = 0;
     int jsplits = 1;
+    // fast MAPPO compact policy (n > 31): layer 0 on tcgen05 GEMMs around the fused kernel
+    __nv_bfloat16 *w0b = nullptr, *pdz0b = nullptr;
+    float *ph0 = nullptr, *pdz0 = nullptr, *ppart0 = nullptr;
+    int64_t hld0p = 0;
+    int psplits = 1;
     // fast numerics
     FastNet pol{}, crit{};
     int grid = 0;                       // persistent CTAs of the fused learn kernel
@@ -151,9 +156,12 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     // fast MAPPO with a policy wider than the fused kernel (per-agent observation 2 + 2n > 64,
     // i.e. n > 31 agents, or hidden > 64): the policy learns on the layer-wise GEMM path
     if (mappo_ && numerics == Numerics::Fast) {
-        bool w = shape_.obs_dim > 64;
-        for (int l = 1; l < shape_.L; ++l) w = w || shape_.pdims[l] > 64;
-        pwide_ = w;
+        bool hw = false;
+        for (int l = 1; l < shape_.L; ++l) hw = hw || shape_.pdims[l] > 64;
+        pwide_ = hw;  // hidden > 64: the whole policy on the layer-wise path
+        // per-agent observation > 64 (n > 31) with hidden <= 64: layer 0 as tcgen05 GEMMs, the
+        // rest in the fused learn kernel (the compact critic's split, for the policy)
+        pcompact_ = !hw && shape_.obs_dim > 64 && shape_.L >= 2;
     }
     // fast MAPPO with a critic input wider than the fused kernel's 64 columns (n > 4): the
     // compact critic - layer 0 as a joint GEMM once per env + W[J+a], the rest fused
@@ -444,7 +452,23 @@ void Engine::alloc() {
         if (gemm_roll_ || pwide_) setup_wide_net(0, b.wpol);
         if (gemm_roll_) alloc_split_rollout();
         if (pwide_) alloc_wide_policy(TR_, 1);
-        b.pol = pwide_ ? FastNet{} : make_net(0);
+        b.pol = pwide_ ? FastNet{} : make_net(0, pcompact_ ? 1 : 0);
+        if (pcompact_) {  // compact policy: layer-0 GEMM operands and products
+            const int H0 = s.pdims[1];
+            auto pad8 = [](int64_t x) { return (x + 7) / 8 * 8; };
+            b.xld = pad8(S + 1);  // + a column of ones: the bias-gradient row of dW0
+            b.xb = b.alloc<__nv_bfloat16>(TR_ * b.xld);
+            b.w0b = b.alloc<__nv_bfloat16>(static_cast<int64_t>(S) * pad8(H0));
+            b.ph0 = b.alloc<float>(TR_ * H0);
+            b.pdz0 = b.alloc<float>(TR_ * H0);
+            b.hld0p = pad8(H0);
+            b.pdz0b = b.alloc<__nv_bfloat16>(TR_ * b.hld0p);
+            const int64_t mt = (S + 1 + 127) / 128, kb = (TR_ + 63) / 64;
+            b.psplits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kb, 148 / mt)));
+            b.ppart0 = b.alloc<float>(static_cast<int64_t>(b.psplits) * (S + 1) * H0);
+            FLW_CUDA(cudaDeviceSynchronize());
+            wide_fill_col(stream_, b.xb, TR_, b.xld, S, 1.0f);
+        }
         if (cfast_) {
             if (L < 2 || s.cdims[1] > 64 || s.cdims[1] % 4 != 0)
                 fail(Errc::Config, "compact fast critic needs >= 2 layers, hidden <= 64 and a multiple of 4");
@@ -914,6 +938,26 @@ void Engine::enq_learn_fast() {
         FLW_CUDA(cudaEventRecord(ev_lfork_, stream_));
         FLW_CUDA(cudaStreamWaitEvent(side2_, ev_lfork_, 0));
     }
+    int64_t p_off = 0;  // compact policy: the fused kernel owns layers 1.., its partials start there
+    if (pcompact_) {
+        // layer 0: h0 = act(X W0 + b0) as one tcgen05 GEMM over the policy rows (bf16 operands)
+        const int H0 = s.pdims[1];
+        p_off = static_cast<int64_t>(S) * H0 + H0;
+        if (learn_iter_ == 0) wide_to_bf16(stream_, b.states, TR_, S, b.xb, b.xld);  // once per episode
+        wide_to_bf16(stream_, b.params + s.woff[0][0], S, H0, b.w0b, b.hld0p);
+        TgEpilogue he;
+        he.mode = kTgBiasAct;
+        he.act = act_of(cfg_);
+        he.bias = b.params + s.boff[0][0];
+        he.c32 = b.ph0;
+        he.ldc32 = H0;
+        tgemm(stream_, TgOperand{b.xb, TR_, S, b.xld, kTgBF16}, false, TgOperand{b.w0b, S, H0, b.hld0p, kTgBF16}, true,
+              TR_, H0, S, 1, he, 64);
+        f.X = b.ph0;
+        f.in_cols = H0;
+        f.dx_out = b.pdz0;  // dZ0 = dH0 * act'(h0) from the kernel's input-gradient stage
+        f.part_stride = s.P_policy - p_off;
+    }
     f.loss_partials = b.loss_parts;
     const int np_loss = pwide_ ? wide_loss_blocks(TR_) : gp;  // policy loss-partial slots
     if (!pwide_) {
@@ -949,12 +993,25 @@ void Engine::enq_learn_fast() {
         enq_learn_policy_wide(b.loss_parts);
         probe_end();
     }
+    if (pcompact_) {  // [dW0 ; db0] = [X | 1]^T dZ0: split-K tcgen05 GEMM + fixed-order sum
+        const int H0 = s.pdims[1];
+        wide_to_bf16(stream_, b.pdz0, TR_, H0, b.pdz0b, b.hld0p);
+        TgEpilogue we;
+        we.mode = kTgStoreF32;
+        we.c32 = b.ppart0;
+        we.ldc32 = H0;
+        we.split_stride = static_cast<int64_t>(S + 1) * H0;
+        tgemm(stream_, TgOperand{b.xb, TR_, S + 1, b.xld, kTgBF16}, true, TgOperand{b.pdz0b, TR_, H0, b.hld0p, kTgBF16},
+              true, S + 1, H0, TR_, b.psplits, we, 64);
+        wide_sum_partials(stream_, b.ppart0, b.psplits, static_cast<int64_t>(S + 1) * H0, b.grads + s.woff[0][0]);
+    }
     b.lgrid_p = pwide_ ? np_loss : gp;
     b.lgrid_c = gc;
     if (!p2p_enabled() && !fused_pending_) {  // with peer-memory exchange the reduction is fused into the exchange
         probe_begin("reduce");
-        fast_reduce_partials(stream_, b.part_p, b.part_c, pwide_ ? b.wsplits : gp, gc, s.P_policy,
-                             s.P - s.P_policy - c_off, b.grads, c_off);
+        // (compact policy: partial index i is parameter p_off + i; the critic's offset is unchanged)
+        fast_reduce_partials(stream_, b.part_p, b.part_c, pwide_ ? b.wsplits : gp, gc, s.P_policy - p_off,
+                             s.P - s.P_policy - c_off, b.grads + p_off, c_off);
         probe_end();
     }
     if (cfast_) {  // critic layer-0 gradients: one-hot rows, bias, and dW_J = joint^T . S

@@ -161,7 +161,8 @@ class Engine {
     bool mappo_ = false;   // agent-major rows R = n*E, critic on [joint obs | agent one-hot]
     bool cfast_ = false;   // fast MAPPO with the compact critic (critic input > 64 wide)
     bool wide_ = false;    // fast numerics, a layer > 64 wide: layer-wise tcgen05 GEMM learn path
-    bool pwide_ = false;   // fast MAPPO, policy wider than the fused kernel: layer-wise policy learn
+    bool pwide_ = false;   // fast MAPPO, policy hidden > 64: layer-wise policy learn
+    bool pcompact_ = false;  // fast MAPPO, observation > 64, hidden <= 64: layer 0 on GEMMs
     bool gemm_roll_ = false;  // fast numerics: rollout policy forward as split-f16 GEMMs
     int p2p_rank_ = 0, p2p_k_ = 0;
     void* p2p_region_ptr_ = nullptr;

@@ -384,10 +384,17 @@ __global__ void __launch_bounds__(kTgThreads, 1)
                     }
                     if (e.c32) {
                         float* d32 = e.c32 + m * e.ldc32 + nb;
+                        if (nv == 32 && (e.ldc32 & 3) == 0) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (j < nv) d32[j] = v[j];
+                            for (int j = 0; j < 32; j += 4)
+                                *reinterpret_cast<float4*>(d32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (j < nv) d32[j] = v[j];
+                        }
                     }
+                    if (!e.c16) continue;  // f32 output only
                 } else {  // kTgActGrad: acc * act'(h), h = the activation output (bf16)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {

@@ -159,6 +159,10 @@ int flw_selftest_umma(int M, int N, int K, int a_mn, int b_mn, int lane_off, con
 int flw_selftest_tgemm(int64_t M, int64_t N, int64_t K, int a_mn, int b_mn, int tf32, int splits, int bn,
                        const float* A, const float* B, float* D);
 
+/* Diagnostic: mean ms per launch of that GEMM for one shape and epilogue (synthetic operands).
+ * dt: 0 bf16, 1 f16, 2 f32/tf32; mode: 0 f32 store, 1 bias + tanh -> bf16, 4 f16 hi|lo|hi. */
+int flw_bench_tgemm(int64_t M, int64_t N, int64_t K, int dt, int mode, int bn, int iters, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,7 @@ def lib():
         "flw_dpd_write": (ci, [vp, cs, P(d), i64]),
         "flw_selftest_umma": (ci, [ci, ci, ci, ci, ci, ci, P(C.c_float), P(C.c_float), P(C.c_float)]),
         "flw_selftest_tgemm": (ci, [i64, i64, i64, ci, ci, ci, ci, ci, P(C.c_float), P(C.c_float), P(C.c_float)]),
+        "flw_bench_tgemm": (ci, [i64, i64, i64, ci, ci, ci, ci, P(d)]),
         "flw_microbench": (ci, [cs, i64, ci, P(d), P(d)]),
         "flw_dpd_enable_probes": (ci, [vp, ci]),
         "flw_dpd_probe_times": (ci, [vp, P(vp)]),

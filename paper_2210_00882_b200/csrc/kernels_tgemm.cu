@@ -102,6 +102,25 @@ __device__ __forceinline__ void mma_tg(uint32_t tmem_d, uint64_t adesc, uint64_t
     }
 }
 
+// f32-accurate tanh for the split (rollout) epilogue: an odd minimax polynomial below 0.6,
+// 1 - 2 / (exp(2|x|) + 1) above; max relative error ~2e-7 (libdevice tanhf: ~1.2e-7), at a
+// third of tanhf's instructions.
+__device__ __forceinline__ float tanh_acc(float x) {
+    const float ax = fabsf(x);
+    if (ax < 0.6f) {
+        const float t = x * x;
+        float p = -0.00589968f;
+        p = fmaf(p, t, 0.020798558f);
+        p = fmaf(p, t, -0.053783875f);
+        p = fmaf(p, t, 0.13331906f);
+        p = fmaf(p, t, -0.33333296f);
+        p = fmaf(p, t, 1.0f);
+        return x * p;
+    }
+    const float r = 1.0f - __fdividef(2.0f, __expf(2.0f * ax) + 1.0f);
+    return copysignf(r, x);
+}
+
 // MUFU tanh (max rel. error ~2^-11, below the bf16 rounding of the stored activation)
 __device__ __forceinline__ float tanh_approx(float x) {
     float y;
@@ -109,7 +128,8 @@ __device__ __forceinline__ float tanh_approx(float x) {
     return y;
 }
 
-constexpr int kTgThreads = 192;
+constexpr int kTgEpiWarps = 8;  // two per TMEM lane quarter, each owning half of the N tile
+constexpr int kTgThreads = 32 * (2 + kTgEpiWarps);
 
 template <int BN>
 __host__ __device__ constexpr int tg_stages() {
@@ -149,7 +169,7 @@ __global__ void __launch_bounds__(kTgThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             umma::mbar_init(&tfull[i], 1);
-            umma::mbar_init(&tempty[i], 4);
+            umma::mbar_init(&tempty[i], kTgEpiWarps);
         }
         umma::mbar_init(&bfull, 1);
         umma::fence_barrier_init();
@@ -258,8 +278,9 @@ __global__ void __launch_bounds__(kTgThreads, 1)
         }
     } else {
         // ------------------------------------------------------------------ epilogue
-        const int q = w & 3;
-        const int et = threadIdx.x - 64;  // 0..127 over the four epilogue warps
+        const int q = w & 3;              // TMEM lane quarter
+        const int hn = (w - 2) >> 2;      // which half of the N tile
+        const int et = threadIdx.x - 64;  // 0..255 over the eight epilogue warps
         const TgEpilogue& e = a.epi;
         const int64_t m_store = e.m_store >= 0 ? e.m_store : a.M;
         const int64_t n_store = e.n_store >= 0 ? e.n_store : a.N;
@@ -271,9 +292,9 @@ __global__ void __launch_bounds__(kTgThreads, 1)
             const int s = decode(wi, mt, nt, kb0, kb1);
             const int64_t n0 = static_cast<int64_t>(nt) * BN;
             if (use_bias) {  // this item's bias slice, staged once (named barrier: epilogue warps)
-                asm volatile("bar.sync 1, 128;\n" ::: "memory");
-                for (int i = et; i < BN; i += 128) sbias[i] = n0 + i < n_store ? e.bias[n0 + i] : 0.0f;
-                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                asm volatile("bar.sync 1, 256;\n" ::: "memory");
+                for (int i = et; i < BN; i += 256) sbias[i] = n0 + i < n_store ? e.bias[n0 + i] : 0.0f;
+                asm volatile("bar.sync 1, 256;\n" ::: "memory");
             }
             umma::mbar_wait(&tfull[acc], tph[acc]);
             tph[acc] ^= 1;
@@ -282,7 +303,7 @@ __global__ void __launch_bounds__(kTgThreads, 1)
             const uint32_t dt = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * BN);
             const bool mok = m < m_store;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int c0 = hn * (BN / 2); c0 < (hn + 1) * (BN / 2); c0 += 32) {
                 if (n0 + c0 >= n_store) break;  // warp-uniform
                 float v[32];
                 umma::tmem_ld16(dt + c0, v);
@@ -340,8 +361,8 @@ __global__ void __launch_bounds__(kTgThreads, 1)
                     uint32_t hi[16], lo[16];
 #pragma unroll
                     for (int j = 0; j < 32; j += 2) {
-                        const float y0 = e.act == 0 ? tanhf(v[j]) : fmaxf(v[j], 0.0f);
-                        const float y1 = e.act == 0 ? tanhf(v[j + 1]) : fmaxf(v[j + 1], 0.0f);
+                        const float y0 = e.act == 0 ? tanh_acc(v[j]) : fmaxf(v[j], 0.0f);
+                        const float y1 = e.act == 0 ? tanh_acc(v[j + 1]) : fmaxf(v[j + 1], 0.0f);
                         const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
                         const __half l0 = __float2half_rn(y0 - __half2float(h0));
                         const __half l1 = __float2half_rn(y1 - __half2float(h1));
@@ -417,7 +438,7 @@ __global__ void __launch_bounds__(kTgThreads, 1)
                     // this warp's 32 rows x 32 columns (64 B per row) into its staging buffer in
                     // the SWIZZLE_64B layout (16-byte chunk k of row r at k ^ ((r >> 1) & 3)),
                     // then one TMA store; the other buffer's store may still be reading
-                    uint8_t* stg = smem + kStageOff + (q * 2 + (c0 >> 5 & 1)) * 2048;
+                    uint8_t* stg = smem + kStageOff + ((w - 2) * 2 + (c0 >> 5 & 1)) * 2048;
                     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
                     __syncwarp();
 #pragma unroll
@@ -531,14 +552,16 @@ void launch_tg(cudaStream_t s, const TgOperand& A, const TgOperand& B, TgArgs a,
     if (a.bres) {
         a.off_ring = (bbytes + 1023u) / 1024u * 1024u;
         a.stage_bytes = kAB;
-        a.nstages = static_cast<int>(std::min<uint32_t>(kTgMaxStages, (kBudget - a.off_ring - 16384u - 1024u) / kAB));
+        a.nstages = static_cast<int>(
+            std::min<uint32_t>(kTgMaxStages, (kBudget - a.off_ring - (a.tma_store ? 32768u : 0u) - 1024u) / kAB));
     } else {
         a.off_ring = 0;
         a.stage_bytes = tg_stage_bytes<BN>();
         a.nstages = tg_stages<BN>();
     }
     a.off_stg = a.off_ring + static_cast<uint32_t>(a.nstages) * a.stage_bytes;
-    const size_t smem = static_cast<size_t>(a.off_stg) + 16384 + 1024;
+    const uint32_t stg = a.tma_store ? 2048u * 2 * kTgEpiWarps : 0u;  // [warp][2][32 x 64 B]
+    const size_t smem = static_cast<size_t>(a.off_stg) + stg + 1024;
     auto kern = k_tgemm<BN, DT, AMN, BMN>;
     FLW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const int64_t items = static_cast<int64_t>(a.mtiles) * a.ntiles * a.splits;
@@ -645,6 +668,64 @@ extern "C" int flw_selftest_tgemm(int64_t M, int64_t N, int64_t K, int a_mn, int
         return 0;
     } catch (const std::exception& ex) {
         fprintf(stderr, "flw_selftest_tgemm: %s\n", ex.what());
+        return 3;
+    }
+}
+
+// Diagnostic: mean ms per tgemm launch for one shape / epilogue (synthetic operands, CUDA events
+// after warm-up). mode: kTgStoreF32, kTgBiasAct (bf16 out), kTgSplit3 (f16 hi|lo|hi out).
+extern "C" int flw_bench_tgemm(int64_t M, int64_t N, int64_t K, int dt, int mode, int bn, int iters, double* ms) {
+    using namespace flw;
+    try {
+        const int esz = dt == kTgF32 ? 4 : 2;
+        const int64_t lda = (K * esz + 15) / 16 * 16 / esz, ldb = (N * esz + 15) / 16 * 16 / esz;
+        void *da = nullptr, *db = nullptr, *dc = nullptr;
+        float* bias = nullptr;
+        FLW_CUDA(cudaMalloc(&da, static_cast<size_t>(M * lda * esz)));
+        FLW_CUDA(cudaMalloc(&db, static_cast<size_t>(K * ldb * esz)));
+        FLW_CUDA(cudaMalloc(&dc, static_cast<size_t>(M * 3 * ((N + 63) / 64 * 64)) * 4));
+        FLW_CUDA(cudaMalloc(&bias, static_cast<size_t>(N) * 4));
+        FLW_CUDA(cudaMemset(da, 0, static_cast<size_t>(M * lda * esz)));
+        FLW_CUDA(cudaMemset(db, 0, static_cast<size_t>(K * ldb * esz)));
+        FLW_CUDA(cudaMemset(bias, 0, static_cast<size_t>(N) * 4));
+        TgEpilogue e;
+        e.mode = mode;
+        e.bias = bias;
+        if (mode == kTgStoreF32) {
+            e.c32 = static_cast<float*>(dc);
+            e.ldc32 = N;
+        } else if (mode == kTgSplit3) {
+            e.c16h = static_cast<__half*>(dc);
+            e.seg = (N + 63) / 64 * 64;
+            e.ldc16 = 3 * e.seg;
+        } else {
+            e.c16 = static_cast<__nv_bfloat16*>(dc);
+            e.ldc16 = (N + 7) / 8 * 8;
+        }
+        auto run = [&] {
+            tgemm(nullptr, TgOperand{da, M, K, lda, dt}, false, TgOperand{db, K, N, ldb, dt}, dt != kTgF32, M, N, K, 1, e,
+                  bn);
+        };
+        for (int i = 0; i < 3; ++i) run();
+        cudaEvent_t a, b;
+        FLW_CUDA(cudaEventCreate(&a));
+        FLW_CUDA(cudaEventCreate(&b));
+        FLW_CUDA(cudaEventRecord(a, nullptr));
+        for (int i = 0; i < iters; ++i) run();
+        FLW_CUDA(cudaEventRecord(b, nullptr));
+        FLW_CUDA(cudaEventSynchronize(b));
+        float t = 0.0f;
+        FLW_CUDA(cudaEventElapsedTime(&t, a, b));
+        *ms = t / iters;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaFree(da);
+        cudaFree(db);
+        cudaFree(dc);
+        cudaFree(bias);
+        return 0;
+    } catch (const std::exception& ex) {
+        fprintf(stderr, "flw_bench_tgemm: %s\n", ex.what());
         return 3;
     }
 }

@@ -641,20 +641,27 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
             }
             int act_r = 0;
             float lpo_r = 0.0f, adv_r = 0.0f, ret_r = 0.0f, val_r = 0.0f;
-            if (learn && valid) {
-                if (a.kind != kNetPolicyPpo) ret_r = a.ret[row];
-                if (a.kind != kNetCritic) act_r = a.actions[row];
-                if (a.kind == kNetPolicyPpo) {
-                    lpo_r = a.logp_old[row];
-                    adv_r = a.adv[row];
+            // the loss epilogue's per-row inputs: issued two forward stages ahead of their use
+            // (not at the tile start), so they are neither held across the whole forward nor
+            // waited for at the loss stage
+            auto load_rows = [&]() {
+                if (learn && valid) {
+                    if (a.kind != kNetPolicyPpo) ret_r = a.ret[row];
+                    if (a.kind != kNetCritic) act_r = a.actions[row];
+                    if (a.kind == kNetPolicyPpo) {
+                        lpo_r = a.logp_old[row];
+                        adv_r = a.adv[row];
+                    }
+                    if (a.kind == kNetPolicyA3c || reuse) val_r = a.values_in[row];
                 }
-                if (a.kind == kNetPolicyA3c || reuse) val_r = a.values_in[row];
-            }
+            };
+            if (!fwd) load_rows();
             float out[16];
             if (fwd) {
                 signal();  // X ready
                 for (int l = 0; l < L; ++l) {
                     const int dout = n.dout[l];
+                    if (l == (L > 2 ? L - 2 : 0)) load_rows();
                     wait_mma();
                     const float* bl = bias + l * kMaxW;
                     if (l + 1 < L) {
@@ -751,10 +758,12 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 continue;
             }
             // ---- loss epilogue (rl.cpp:137-202 semantics, f32) -> dZ_{L-1}
+            // Static loop bounds only (predicated on the action count) and the probabilities
+            // recomputed per use instead of held in arrays: out[] and dz[] stay in registers.
             {
-                float dz[32];  // output layer width <= 16 (the loss epilogue owns the whole row)
+                float dz[16];  // output layer width <= 16 (the loss epilogue owns the whole row)
 #pragma unroll
-                for (int j = 0; j < 32; ++j) dz[j] = 0.0f;
+                for (int j = 0; j < 16; ++j) dz[j] = 0.0f;
                 if (valid) {
                     float inv_n = static_cast<float>(a.inv_n);
                     const double* ast = a.adv_stats;
@@ -770,21 +779,23 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                     } else {  // policy: clipped surrogate (PPO) or A3C policy gradient, + entropy bonus
                         const int A = n.rout[L - 1];
                         float mx = out[0];
-                        for (int j = 1; j < A; ++j) mx = fmaxf(mx, out[j]);
-                        float den = 0.0f;
-                        for (int j = 0; j < A; ++j) den += __expf(out[j] - mx);
-                        const float lden = __logf(den);
-                        float p[16], lp[16], H = 0.0f;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            lp[j] = out[j] - mx - lden;
-                            p[j] = j < A ? __expf(lp[j]) : 0.0f;
-                            if (j < A) H -= p[j] * lp[j];
-                        }
-                        float lpa = 0.0f;
+                        for (int j = 1; j < 16; ++j)
+                            if (j < A) mx = fmaxf(mx, out[j]);
+                        float den = 0.0f;
 #pragma unroll
                         for (int j = 0; j < 16; ++j)
-                            if (j == act_r) lpa = lp[j];
+                            if (j < A) den += __expf(out[j] - mx);
+                        const float lden = __logf(den);
+                        float H = 0.0f, lpa = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            if (j < A) {
+                                const float lp = out[j] - mx - lden;
+                                H -= __expf(lp) * lp;
+                                if (j == act_r) lpa = lp;
+                            }
+                        }
                         float coef;
                         if (a.kind == kNetPolicyPpo) {
                             float adv = adv_r;
@@ -805,8 +816,12 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                         en_acc += H * inv_n;
                         const float eci = static_cast<float>(a.entropy_coef) * inv_n;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (j < A) dz[j] = coef * ((j == act_r ? 1.0f : 0.0f) - p[j]) + eci * p[j] * (lp[j] + H);
+                        for (int j = 0; j < 16; ++j) {
+                            if (j < A) {
+                                const float lp = out[j] - mx - lden, pj = __expf(lp);
+                                dz[j] = coef * ((j == act_r ? 1.0f : 0.0f) - pj) + eci * pj * (lp + H);
+                            }
+                        }
                     }
                 }
                 const int wo = n.dout[L - 1];
@@ -821,7 +836,17 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                     }
                 }
                 signal();  // dZ_{L-1} ready
-                colsum32(dz, 0, wo, L - 1);
+                // bias gradient of the output layer: columns >= rout are zero
+                const int ro = n.rout[L - 1];
+                if (ro <= 8) {
+                    const float sum = warp_colsum8(dz, lane);
+                    if ((lane & 3) == 0) mydb[(L - 1) * kMaxW + (lane >> 2)] += sum;
+                } else {
+                    float v32[32];
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) v32[c] = c < 16 ? dz[c] : 0.0f;
+                    colsum32(v32, 0, wo, L - 1);
+                }
             }
             // ---- backward epilogues: dZ_{m-1} = dH_m * act'(H_{m-1})
             for (int m = L - 1; m >= 1; --m) {
@@ -969,7 +994,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
     if (blockIdx.x == 0 && t == 0 && MODE != 0) {
         const long long t0 = tr_p[0][0];
         for (int i = 0; i < ne_ev; ++i)
-            printf("E %2d wait %7lld got %7lld signal %7lld\n", i, tr_e[0][i] - t0, tr_e[1][i] - t0, tr_e[2][i] - t0);
+            printf("E%d %2d wait %7lld got %7lld signal %7lld\n", MODE, i, tr_e[0][i] - t0, tr_e[1][i] - t0, tr_e[2][i] - t0);
         for (int i = 0; i < nf_ev; ++i)
             printf("F %2d start %7lld half0 %7lld stores %7lld signaled %7lld bulk %7lld\n", i, tr_f[0][i] - t0,
                    tr_f[1][i] - t0, tr_f[2][i] - t0, tr_f[3][i] - t0, tr_f[4][i] - t0);
@@ -977,7 +1002,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
     if (blockIdx.x == 0 && t == 32 * kEpiWarps && MODE != 0) {
         const long long t0 = tr_p[0][0];
         for (int i = 0; i < np_ev; ++i)
-            printf("P %2d epi %7lld a %7lld b %7lld commit %7lld\n", i, tr_p[0][i] - t0, tr_p[2][i] - t0,
+            printf("P%d %2d epi %7lld a %7lld b %7lld commit %7lld\n", MODE, i, tr_p[0][i] - t0, tr_p[2][i] - t0,
                    tr_p[3][i] - t0, tr_p[1][i] - t0);
     }
 #endif

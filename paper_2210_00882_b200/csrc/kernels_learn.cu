@@ -241,7 +241,7 @@ __device__ __forceinline__ float warp_colsum32_bf16(const uint32_t* pk, int lane
 // 2: learn reusing the values pass's activations (backward only). ACT 0: tanh, 1: relu.
 // Compile-time modes keep each instantiation's code small (the stage loops are instruction-
 // cache sensitive) and branch-free per activation chunk.
-template <int MODE, int ACT>
+template <int MODE, int ACT, int NA>  // NA: output columns held by the loss epilogue (8 or 16)
 __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a) {
     constexpr int kGroups = groups_for(MODE);
     constexpr int kEpiWarps = 4 * kGroups;
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 }
             };
             if (!fwd) load_rows();
-            float out[16];
+            float out[NA];
             if (fwd) {
                 signal();  // X ready
                 for (int l = 0; l < L; ++l) {
@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                         float z[32];
                         ld_acc32(z, 0, 16);
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) out[j] = z[j] + bl[j];
+                        for (int j = 0; j < NA; ++j) out[j] = z[j] + bl[j];
                     }
                 }
             } else {
@@ -761,9 +761,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
             // Static loop bounds only (predicated on the action count) and the probabilities
             // recomputed per use instead of held in arrays: out[] and dz[] stay in registers.
             {
-                float dz[16];  // output layer width <= 16 (the loss epilogue owns the whole row)
+                float dz[NA];  // output layer width <= NA (the loss epilogue owns the whole row)
 #pragma unroll
-                for (int j = 0; j < 16; ++j) dz[j] = 0.0f;
+                for (int j = 0; j < NA; ++j) dz[j] = 0.0f;
                 if (valid) {
                     float inv_n = static_cast<float>(a.inv_n);
                     const double* ast = a.adv_stats;
@@ -780,16 +780,16 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                         const int A = n.rout[L - 1];
                         float mx = out[0];
 #pragma unroll
-                        for (int j = 1; j < 16; ++j)
+                        for (int j = 1; j < NA; ++j)
                             if (j < A) mx = fmaxf(mx, out[j]);
                         float den = 0.0f;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
+                        for (int j = 0; j < NA; ++j)
                             if (j < A) den += __expf(out[j] - mx);
                         const float lden = __logf(den);
                         float H = 0.0f, lpa = 0.0f;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
+                        for (int j = 0; j < NA; ++j) {
                             if (j < A) {
                                 const float lp = out[j] - mx - lden;
                                 H -= __expf(lp) * lp;
@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                         en_acc += H * inv_n;
                         const float eci = static_cast<float>(a.entropy_coef) * inv_n;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
+                        for (int j = 0; j < NA; ++j) {
                             if (j < A) {
                                 const float lp = out[j] - mx - lden, pj = __expf(lp);
                                 dz[j] = coef * ((j == act_r ? 1.0f : 0.0f) - pj) + eci * pj * (lp + H);
@@ -829,10 +829,14 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
 #pragma unroll
                 for (int c0 = 0; c0 < 16; c0 += 8) {
                     if (c0 < wo) {
-                        // round to the bf16 operand first so db sums exactly what dW sees
+                        if (c0 < NA) {
+                            // round to the bf16 operand first so db sums exactly what dW sees
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) dz[c0 + i] = __bfloat162float(__float2bfloat16(dz[c0 + i]));
-                        umma::st_row8(dst, wo, r, c0, dz + c0);
+                            for (int i = 0; i < 8; ++i) dz[c0 + i] = __bfloat162float(__float2bfloat16(dz[c0 + i]));
+                            umma::st_row8(dst, wo, r, c0, dz + c0);
+                        } else {  // padding columns of the output layer
+                            *reinterpret_cast<uint4*>(dst + umma::tile_offset(r, c0, wo)) = make_uint4(0u, 0u, 0u, 0u);
+                        }
                     }
                 }
                 signal();  // dZ_{L-1} ready
@@ -844,7 +848,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 } else {
                     float v32[32];
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) v32[c] = c < 16 ? dz[c] : 0.0f;
+                    for (int c = 0; c < 32; ++c) v32[c] = c < NA ? dz[c] : 0.0f;
                     colsum32(v32, 0, wo, L - 1);
                 }
             }
@@ -1025,14 +1029,15 @@ void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid) {
         kern<<<grid, threads_for(mode), smem, s>>>(a);
         FLW_CUDA(cudaGetLastError());
     };
+    const bool na8 = a.net.rout[a.net.L - 1] <= 8;
     if (a.act == 0) {
-        if (mode == 0) go(k_learn<0, 0>);
-        else if (mode == 1) go(k_learn<1, 0>);
-        else go(k_learn<2, 0>);
+        if (mode == 0) na8 ? go(k_learn<0, 0, 8>) : go(k_learn<0, 0, 16>);
+        else if (mode == 1) na8 ? go(k_learn<1, 0, 8>) : go(k_learn<1, 0, 16>);
+        else na8 ? go(k_learn<2, 0, 8>) : go(k_learn<2, 0, 16>);
     } else {
-        if (mode == 0) go(k_learn<0, 1>);
-        else if (mode == 1) go(k_learn<1, 1>);
-        else go(k_learn<2, 1>);
+        if (mode == 0) na8 ? go(k_learn<0, 1, 8>) : go(k_learn<0, 1, 16>);
+        else if (mode == 1) na8 ? go(k_learn<1, 1, 8>) : go(k_learn<1, 1, 16>);
+        else na8 ? go(k_learn<2, 1, 8>) : go(k_learn<2, 1, 16>);
     }
 }
 

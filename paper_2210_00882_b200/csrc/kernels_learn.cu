@@ -50,7 +50,7 @@ constexpr int kGroups = groups_for(1);
 // + two MMA producers (groups split by parity) + loader
 __host__ __device__ constexpr int threads_for(int mode) { return 32 * (4 * groups_for(mode) + 3); }
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
-constexpr int kXPre = 24;                      // input columns prefetched in registers (12 packed regs)
+constexpr int kXPre = 18;                      // input columns prefetched in registers (9 packed regs)
 #ifndef FLW_TANH_MUFU_PAIRS
 #define FLW_TANH_MUFU_PAIRS 4
 #endif
@@ -631,11 +631,15 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 }
             } else {
 #pragma unroll
-                for (int c0 = 0; c0 < kXPre; c0 += 8)
-                    if (c0 < din0)
+                for (int c0 = 0; c0 < 24; c0 += 8)  // 8-column chunks; pairs beyond kXPre are zero
+                    if (c0 < din0) {
+                        uint32_t q4[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) q4[i] = c0 / 2 + i < kXPre / 2 ? xnext[c0 / 2 + i] : 0u;
                         *reinterpret_cast<uint4*>(xs + umma::tile_offset(r, c0, din0)) =
-                            make_uint4(xnext[c0 / 2], xnext[c0 / 2 + 1], xnext[c0 / 2 + 2], xnext[c0 / 2 + 3]);
-                for (int c0 = kXPre; c0 < din0; c0 += 8)  // padded input columns: zeros
+                            make_uint4(q4[0], q4[1], q4[2], q4[3]);
+                    }
+                for (int c0 = 24; c0 < din0; c0 += 8)  // padded input columns: zeros
                     *reinterpret_cast<uint4*>(xs + umma::tile_offset(r, c0, din0)) = make_uint4(0u, 0u, 0u, 0u);
                 fetch_x(tile + kGroups * G);
             }

@@ -331,9 +331,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
             if (pidx == 0 && umma::elect_one()) bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
             __syncwarp();
             umma::mbar_wait(&wbar, 0);
-            uint32_t ph_epi[kGroups] = {}, ph_ld[kGroups][2] = {}, need_rd[kGroups] = {};
-            bool dw_init[kMaxLayers];
-            for (int l = 0; l < kMaxLayers; ++l) dw_init[l] = true;
+            // per-producer state of its own groups g = pidx + 2 gi, indexed by the compile-time gi
+            // (runtime-indexed arrays would live in local memory): hand-off phases, the ldbar
+            // phases as a bit mask (bit s: slot s), bulk-store reads required before a forward
+            constexpr int kMine = (kGroups + 1) / 2;
+            uint32_t ph_epi[kMine] = {}, ph_ld[kMine] = {}, need_rd[kMine] = {};
             auto dw_tmem = [&](int l) {
                 return tmem + 64u * kGroups + 64u * static_cast<uint32_t>(l >> 1) + ((l & 1) ? (16u << 16) : 0u);
             };
@@ -345,11 +347,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 const int di = n.din[l], dout = n.dout[l];
                 const uint32_t dzt = uni(sbase + C.dz[g]);
                 const uint32_t id = umma::idesc_bf16(64, dout, true, true);
-                for (int kb = 0; kb < kRows / 16; ++kb) {
+                for (int kb = 0; kb < kRows / 16; ++kb)  // accumulators zeroed once below
                     umma::mma_bf16_warp(dw_tmem(l), umma::desc_mnmajor(hin, di, kb), umma::desc_mnmajor(dzt, dout, kb),
-                                        id, dw_init[l] || kb > 0);
-                }
-                dw_init[l] = true;
+                                        id, true);
             };
             if (learn) {
                 if (pidx == 0) {
@@ -364,19 +364,20 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 umma::fence_after_sync();
             }
             for (int64_t it = 0;; ++it) {
-                int64_t tl[kGroups];
-                bool has[kGroups], any = false;
-                for (int g = 0; g < kGroups; ++g) {
-                    tl[g] = it * kGroups * G + kGroups * static_cast<int64_t>(blockIdx.x) + g;
-                    has[g] = tl[g] < ntiles;
-                    any = any || has[g];
-                }
-                if (!any) break;
+                // tiles are dealt to groups in ascending order: this producer's groups with a
+                // tile this round are its first nmine (the groups past the end hold none)
+                const int64_t t0 = it * kGroups * G + kGroups * static_cast<int64_t>(blockIdx.x);
+                if (t0 + pidx >= ntiles) break;
+                const int64_t avail = (ntiles - t0 - pidx + 1) / 2;
+                const int nmine = avail < kMine ? static_cast<int>(avail) : kMine;
                 for (int j = 0; j < njobs; ++j) {
-                    for (int g = pidx; g < kGroups; g += 2) {
-                        if (!has[g]) continue;
-                        umma::mbar_wait(&epi_done[g], ph_epi[g]);
-                        ph_epi[g] ^= 1;
+#pragma unroll
+                    for (int gi = 0; gi < kMine; ++gi) {
+                        const int g = pidx + 2 * gi;
+                        if (gi >= nmine || g >= kGroups) continue;
+                        const int64_t tlg = t0 + g;
+                        umma::mbar_wait(&epi_done[g], ph_epi[gi]);
+                        ph_epi[gi] ^= 1;
 #ifdef FLW_LEARN_TRACE
                         if (g == 0 && np_ev < 64) tr_p[0][np_ev] = clock64();
 #endif
@@ -389,9 +390,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
 #endif
                             // the epilogue of this job overwrites the slot of H_{l-2}: the loader's
                             // bulk store of it must have read the slot
-                            if (l >= 1 && save_dst(g, tl[g], l - 2)) {
-                                ++need_rd[g];
-                                while (cnt_acquire(&rd_cnt[g]) < need_rd[g]) __nanosleep(20);
+                            if (l >= 1 && save_dst(g, tlg, l - 2)) {
+                                ++need_rd[gi];
+                                while (cnt_acquire(&rd_cnt[g]) < need_rd[gi]) __nanosleep(20);
                             }
                             const uint32_t in = uni(sbase + C.ring[g][(l - 1) & 1]);
                             const uint32_t wl = uni(sbase + C.wt[l]);
@@ -414,8 +415,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
 #endif
                             const int sh = (m - 1) & 1;
                             if (!resident(m - 1)) {
-                                umma::mbar_wait(&ldbar[g][sh], ph_ld[g][sh]);
-                                ph_ld[g][sh] ^= 1;
+                                umma::mbar_wait(&ldbar[g][sh], (ph_ld[gi] >> sh) & 1u);
+                                ph_ld[gi] ^= 1u << sh;
                             }
                             if (m >= 1 || dx) {  // dH_m (m = 0: gradient wrt the input, dx mode)
                                 const int di = n.din[m], dout = n.dout[m];
@@ -486,6 +487,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
             for (int64_t it = 0;; ++it) {
                 int64_t tl[kGroups];
                 bool has[kGroups], any = false;
+#pragma unroll
                 for (int g = 0; g < kGroups; ++g) {
                     tl[g] = it * kGroups * G + kGroups * static_cast<int64_t>(blockIdx.x) + g;
                     has[g] = tl[g] < ntiles;
@@ -493,6 +495,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 }
                 if (!any) break;
                 for (int j = 0; j < njobs; ++j) {
+#pragma unroll
                     for (int g = 0; g < kGroups; ++g) {
                         if (!has[g]) continue;
                         ++seen[g];
@@ -546,7 +549,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
         const int r = 32 * q + lane;  // tile row == TMEM lane
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
         const uint32_t zt = tmem + lane_base + 64u * static_cast<uint32_t>(g);
-        uint32_t ph_mma = 0, ph_ld[2] = {0, 0}, need_xf = 0;
+        uint32_t ph_mma = 0, ph_ld = 0, need_xf = 0;  // ph_ld: bit s = phase of ldbar slot s
         float pl_acc = 0.0f, vl_acc = 0.0f, en_acc = 0.0f;
         float* mydb = dbacc + w * kMaxLayers * kMaxW;
         const int din0 = n.din[0];
@@ -862,8 +865,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 wait_mma();
                 const int s = (m - 1) & 1;
                 if (!resident(m - 1)) {
-                    umma::mbar_wait(&ldbar[g][s], ph_ld[s]);
-                    ph_ld[s] ^= 1;
+                    umma::mbar_wait(&ldbar[g][s], (ph_ld >> s) & 1u);
+                    ph_ld ^= 1u << s;
                 }
                 const uint8_t* hs = smem + C.ring[g][s];
                 uint8_t* dst = smem + C.dz[g];
@@ -912,12 +915,12 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 }
 
             }
-            if (!resident(-1) && !dx) ph_ld[1] ^= 1;  // X's reload (stage 0): consumed by the producer only
+            if (!resident(-1) && !dx) ph_ld ^= 2u;  // X's reload (stage 0): consumed by the producer only
             if (dx) {  // dZ wrt the input pre-activation: dH_0 * act'(X), X = the input tile (bf16)
                 wait_mma();
                 if (!resident(-1)) {
-                    umma::mbar_wait(&ldbar[g][1], ph_ld[1]);
-                    ph_ld[1] ^= 1;
+                    umma::mbar_wait(&ldbar[g][1], (ph_ld >> 1) & 1u);
+                    ph_ld ^= 2u;
                 }
                 const int di = n.din[0];
                 for (int h0 = 0; h0 < di; h0 += 32) {

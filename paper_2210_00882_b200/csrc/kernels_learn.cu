@@ -961,16 +961,24 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
     __syncthreads();
     umma::fence_after_sync();
 
-    // ---- per-CTA partials: dW from TMEM, db and loss terms from shared memory (fixed order)
+    // ---- per-CTA partials: dW from TMEM, db and loss terms from shared memory (fixed order).
+    // The slot is assembled in the (now idle) activation slots and leaves as one bulk copy: the
+    // TMEM lane layout puts one dW row per lane, so direct stores would be 4-byte writes
+    // strided by a row (partial-sector L2 writes, ~9% of the kernel in ncu r02e).
+    const bool any = kGroups * static_cast<int64_t>(blockIdx.x) < ntiles;
+    float* part = learn ? a.partials + static_cast<int64_t>(blockIdx.x) * a.part_stride : nullptr;
+    const bool staged = learn && any && static_cast<uint64_t>(a.part_stride) * 4u <= C.bias - C.ring[0][0];
+    float* stage = reinterpret_cast<float*>(smem + C.ring[0][0]);
+    float* dst = staged ? stage : part;
     if (learn && w < kEpiWarps) {
         const int q = w & 3, half = w >> 2;
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
-        const bool any = kGroups * static_cast<int64_t>(blockIdx.x) < ntiles;
-        float* part = a.partials + static_cast<int64_t>(blockIdx.x) * a.part_stride;
         for (int l = 0; l < L; ++l) {
             const int dout = n.dout[l], ri = n.rin[l], ro = n.rout[l];
             const int lo = (l & 1) ? 16 : 0;
             const uint32_t col = 64u * kGroups + 64u * static_cast<uint32_t>(l >> 1);
+            const int64_t base = n.woff[l] - n.woff[0];
+            const bool vec = staged && ((base | ro) & 3) == 0;
             for (int c0 = 16 * half; c0 < dout; c0 += 16 * kGroups) {
                 float v[16];
                 umma::tmem_ld16(tmem + lane_base + col + c0, v);
@@ -978,15 +986,25 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
                 const int mrow = lane - lo;  // dW row (input index) held by this lane
                 if (any && mrow >= 0 && mrow < 16) {
                     const int i = mrow + 16 * q;
-                    if (i < ri)
-                        for (int j = 0; j < 16; ++j)
-                            if (c0 + j < ro) part[n.woff[l] - n.woff[0] + i * ro + c0 + j] = v[j];
+                    if (i < ri) {
+                        float* rowp = dst + base + static_cast<int64_t>(i) * ro + c0;
+                        if (vec) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4)
+                                if (c0 + j < ro)
+                                    *reinterpret_cast<float4*>(rowp + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (c0 + j < ro) rowp[j] = v[j];
+                        }
+                    }
                 }
             }
             for (int o = t; o < ro; o += 32 * kEpiWarps) {
                 float s = 0.0f;
                 for (int k = 0; k < kEpiWarps; ++k) s += dbacc[(k * kMaxLayers + l) * kMaxW + o];
-                part[n.boff[l] - n.woff[0] + o] = s;
+                dst[n.boff[l] - n.woff[0] + o] = s;
             }
         }
         if (t < 3) {
@@ -997,6 +1015,20 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
         }
         if (!any)
             for (int64_t i = t; i < a.part_stride; i += 32 * kEpiWarps) part[i] = 0.0f;
+    }
+    if (staged) {
+        umma::fence_async_smem();  // the generic stores above -> the bulk copy's async proxy
+        __syncthreads();
+        const uint64_t bytes = static_cast<uint64_t>(a.part_stride) * 4u;
+        if ((reinterpret_cast<uintptr_t>(part) & 15u) == 0 && (bytes & 15u) == 0) {
+            if (t == 0) {
+                umma::bulk_s2g(part, stage, static_cast<uint32_t>(bytes));
+                umma::bulk_commit();
+                umma::bulk_wait_all();
+            }
+        } else {
+            for (int64_t i = t; i < a.part_stride; i += kThreads) part[i] = stage[i];
+        }
     }
     umma::fence_before_sync();
     __syncthreads();

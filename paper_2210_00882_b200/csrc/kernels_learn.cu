@@ -242,7 +242,7 @@ __device__ __forceinline__ float warp_colsum32_bf16(const uint32_t* pk, int lane
 // Compile-time modes keep each instantiation's code small (the stage loops are instruction-
 // cache sensitive) and branch-free per activation chunk.
 template <int MODE, int ACT, int NA>  // NA: output columns held by the loss epilogue (8 or 16)
-__global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a) {
+__global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a, const __grid_constant__ Carve C) {
     constexpr int kGroups = groups_for(MODE);
     constexpr int kEpiWarps = 4 * kGroups;
     constexpr int kThreads = threads_for(MODE);
@@ -257,14 +257,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
     __shared__ uint32_t epi_cnt[kGroups];  // epilogue hand-offs per group (4 per stage), for the loader
     __shared__ uint32_t rd_cnt[kGroups];   // loader: bulk stores whose smem read completed (producer)
     __shared__ uint32_t xf_cnt[kGroups];   // loader, values pass: last saved tile read (epilogue)
-    __shared__ Carve C;  // offsets live in shared memory, not in 40 registers per thread
 #ifdef FLW_LEARN_TRACE
     __shared__ long long tr_p[4][64], tr_e[3][64], tr_f[5][16];
     int np_ev = 0, ne_ev = 0, nf_ev = 0;
 #endif
     const FastNet& n = a.net;
-    if (threadIdx.x == 0) C = carve_learn(n, kGroups, MODE != 0);
-    __syncthreads();
     const int t = threadIdx.x, w = uni(static_cast<int>(t >> 5)), lane = t & 31;
     const int L = n.L;
     const int64_t ntiles = (a.rows + kRows - 1) / kRows;
@@ -302,11 +299,16 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
         for (int g = 0; g < kGroups; ++g) epi_cnt[g] = rd_cnt[g] = xf_cnt[g] = 0;
         for (int l = 0; l < kMaxLayers; ++l) dwtok[l] = 0;
         umma::fence_barrier_init();
+        // the weight image's copy starts first: it overlaps the rest of the setup
+        bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
     }
-    for (int l = 0; l < L; ++l)
-        for (int o = t; o < kMaxW; o += kThreads) bias[l * kMaxW + o] = o < n.rout[l] ? a.params[n.boff[l] + o] : 0.0f;
+    for (int i = t; i < L * kMaxW; i += kThreads) {  // one global load per thread, all in flight
+        const int l = i / kMaxW, o = i % kMaxW;
+        bias[i] = o < n.rout[l] ? a.params[n.boff[l] + o] : 0.0f;
+    }
     if (learn)
-        for (int i = t; i < kEpiWarps * kMaxLayers * kMaxW; i += kThreads) dbacc[i] = 0.0f;
+        for (int i = t; i < kEpiWarps * kMaxLayers * kMaxW / 4; i += kThreads)
+            reinterpret_cast<float4*>(dbacc)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     if (learn) {  // dz slot of group 0 zeroed: the operand of the dW accumulators' zero-init MMAs
         for (uint32_t i = t; i < kSlot / 16; i += kThreads)
             reinterpret_cast<uint4*>(smem + C.dz[0])[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -328,8 +330,6 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a)
             // so producer 0 zeroes them with one accumulate=0 MMA per layer on a zero operand
             // before either producer issues a stage, and every dW MMA accumulates
             const int pidx = w == kEpiWarps ? 0 : 1;
-            if (pidx == 0 && umma::elect_one()) bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
-            __syncwarp();
             umma::mbar_wait(&wbar, 0);
             // per-producer state of its own groups g = pidx + 2 gi, indexed by the compile-time gi
             // (runtime-indexed arrays would live in local memory): hand-off phases, the ldbar
@@ -1060,12 +1060,13 @@ int fast_values_groups() { return groups_for(0); }
 
 void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid) {
     const int mode = a.mode != 1 ? 0 : (a.hload && a.net.L > 1 ? 2 : 1);
-    const size_t smem = carve_learn(a.net, groups_for(mode), mode != 0).total;
+    const Carve carve = carve_learn(a.net, groups_for(mode), mode != 0);  // smem offsets: a kernel argument
+    const size_t smem = carve.total;
     if (smem > 227u * 1024u) throw Error(Errc::Config, "fast numerics: network too wide/deep for one SM's shared memory");
     auto go = [&](auto kern) {
         // per-device attribute: set on every launch (cheap, and legal inside stream capture)
         FLW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<grid, threads_for(mode), smem, s>>>(a);
+        kern<<<grid, threads_for(mode), smem, s>>>(a, carve);
         FLW_CUDA(cudaGetLastError());
     };
     const bool na8 = a.net.rout[a.net.L - 1] <= 8;

@@ -27,6 +27,9 @@
 // Stage protocol per group: the producer waits epi_done[g] (all 4 epilogue warps stored their
 // operand tile and fenced it to the async proxy), issues the stage's MMAs and commits to
 // mma_done[g]; the epilogue waits mma_done[g], reads the accumulator, writes the next operand.
+// A backward stage commits twice: dH_m to mma_done[g] (the epilogue starts on it) and dW_m, which
+// still reads dZ_m from the dz slot, to dw_done[g]; the epilogue waits dw_done[g] just before it
+// overwrites that slot with dZ_{m-1} (the next tile's first stores wait the last one).
 #include <cuda_runtime.h>
 
 // MODE 0 instantiations end each tile with `continue` before the learn-only stages
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
 #endif
     constexpr bool kZPre = FLW_LEARN_ZPRE;
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t mma_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar, zbar;
+    __shared__ uint64_t mma_done[kGroups], dw_done[kGroups], epi_done[kGroups], ldbar[kGroups][2], wbar, zbar;
     __shared__ uint32_t tslot;
     __shared__ uint32_t dwtok[kMaxLayers];  // dW_l MMAs issued so far, in (tile round, group) order
     __shared__ uint32_t epi_cnt[kGroups];  // epilogue hand-offs per group (4 per stage), for the loader
@@ -289,6 +292,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
     if (t == 0) {
         for (int g = 0; g < kGroups; ++g) {
             umma::mbar_init(&mma_done[g], 1);
+            umma::mbar_init(&dw_done[g], 1);
             umma::mbar_init(&epi_done[g], 4);
             umma::mbar_init(&ldbar[g][0], 1);
             umma::mbar_init(&ldbar[g][1], 1);
@@ -414,17 +418,19 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                             if (g == 0 && np_ev < 64) tr_p[2][np_ev] = clock64();
 #endif
                             const int sh = (m - 1) & 1;
-                            if (!resident(m - 1)) {
-                                umma::mbar_wait(&ldbar[g][sh], (ph_ld[gi] >> sh) & 1u);
-                                ph_ld[gi] ^= 1u << sh;
-                            }
-                            if (m >= 1 || dx) {  // dH_m (m = 0: gradient wrt the input, dx mode)
+                            const bool has_dh = m >= 1 || dx;
+                            if (has_dh) {  // dH_m (m = 0: gradient wrt the input, dx mode)
                                 const int di = n.din[m], dout = n.dout[m];
                                 const uint32_t id = umma::idesc_bf16(128, di, false, true);
                                 const uint32_t dzt = uni(sbase + C.dz[g]), wm = uni(sbase + C.wt[m]);
                                 for (int kb = 0; kb < dout / 16; ++kb)
                                     umma::mma_bf16_warp(zt, umma::desc_kmajor(dzt, dout, kb),
                                                         umma::desc_mnmajor(wm, di, kb), id, kb > 0);
+                                umma::commit_warp(&mma_done[g]);  // the epilogue starts on dH_m
+                            }
+                            if (!resident(m - 1)) {  // H_{m-1}: only dW_m reads it
+                                umma::mbar_wait(&ldbar[g][sh], (ph_ld[gi] >> sh) & 1u);
+                                ph_ld[gi] ^= 1u << sh;
                             }
                             // the shared dW_m accumulator takes its MMAs in the single-issuer order
                             // ((tile round, group) ascending), so the sums stay deterministic
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                             umma::fence_before_sync();
                             __syncwarp();
                             if (lane == 0) cnt_add_release(&dwtok[m]);
-                            umma::commit_warp(&mma_done[g]);
+                            umma::commit_warp(has_dh ? &dw_done[g] : &mma_done[g]);
 #ifdef FLW_LEARN_TRACE
                             if (g == 0 && np_ev < 64) tr_p[1][np_ev++] = clock64();
 #endif
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
         const int r = 32 * q + lane;  // tile row == TMEM lane
         const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
         const uint32_t zt = tmem + lane_base + 64u * static_cast<uint32_t>(g);
-        uint32_t ph_mma = 0, ph_ld = 0, need_xf = 0;  // ph_ld: bit s = phase of ldbar slot s
+        uint32_t ph_mma = 0, ph_dw = 0, ph_ld = 0, need_xf = 0;  // ph_ld: bit s = phase of ldbar slot s
         float pl_acc = 0.0f, vl_acc = 0.0f, en_acc = 0.0f;
         float* mydb = dbacc + w * kMaxLayers * kMaxW;
         const int din0 = n.din[0];
@@ -589,6 +595,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
             if (t == 0 && ne_ev < 64) tr_e[1][ne_ev++] = clock64();
 #endif
         };
+        auto wait_dw = [&]() {  // this group's last dW MMAs completed: the dz slot is free
+            umma::mbar_wait(&dw_done[g], ph_dw);
+            ph_dw ^= 1;
+            umma::fence_after_sync();
+        };
         // loads accumulator columns [c0, c0 + 32) of this thread's row (those below `width`)
         auto ld_acc32 = [&](float* v, int c0, int width) {
             umma::tmem_ld16(zt + c0, v);
@@ -614,8 +625,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
         for (int64_t tile = kGroups * static_cast<int64_t>(blockIdx.x) + g; tile < ntiles; tile += kGroups * G) {
             const int64_t row = tile * kRows + r;
             const bool valid = row < a.rows;
-            // previous tile's last MMAs (dW_0) released X and dZ (dx mode: waited by its epilogue)
-            if (learn && !first && !dx) wait_mma();
+            // previous tile's last MMAs (dW_0) released X and dZ
+            if (learn && !first) dx ? wait_dw() : wait_mma();
             if (!learn && !first && save_dst(g, tile - kGroups * G, L - 2)) {  // values pass: see the loader
                 ++need_xf;
                 while (cnt_acquire(&xf_cnt[g]) < need_xf) __nanosleep(20);
@@ -876,6 +887,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                     umma::tmem_ld16(zt + h0, gv);
                     if (FULL || h0 + 16 < di) umma::tmem_ld16(zt + h0 + 16, gv + 16);
                     umma::tmem_ld_wait();
+                    if (h0 == 0) wait_dw();  // dW_m has read dZ_m: the slot takes dZ_{m-1}
 #pragma unroll
                     for (int c = 0; c < 32; c += 8) {
                         if (FULL || h0 + c < di) {
@@ -943,7 +955,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                 }
             }
         }
-        if (learn && !first && !dx) wait_mma();  // the last tile's dW_0
+        if (learn && !first) dx ? wait_dw() : wait_mma();  // the last tile's dW_0
         // ---- loss partials of this warp
         for (int off = 16; off > 0; off >>= 1) {
             pl_acc += __shfl_xor_sync(0xffffffffu, pl_acc, off);

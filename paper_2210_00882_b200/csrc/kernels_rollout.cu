@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
 
 #ifdef FLW_LEARN_TRACE
     long long tr0[8], tr1[8], tr2[8];
+    long long trl[3][8];  // step 2, per layer: MMA loop done, epilogue stored, tile barrier passed
 #endif
     for (int64_t step = a.step0; step < a.step0 + a.nsteps; ++step) {
 #ifdef FLW_LEARN_TRACE
@@ -211,6 +212,9 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             const int n0 = 2 * jw;
             if (n0 < NT) {
                 const bool two = n0 + 1 < NT;
+#ifdef FLW_LEARN_TRACE
+                const bool trl_on = step == a.step0 + 2 && l < 8;
+#endif
                 float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
                 const uint4* ap = Ahi + mt * KT * 32 + lane;
                 const uint4* alp = Alo + mt * KT * 32 + lane;
@@ -232,6 +236,9 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                         mma_f16(acc1, ahv, bh1);
                     }
                 }
+#ifdef FLW_LEARN_TRACE
+                if (trl_on) trl[0][l] = clock64();
+#endif
                 // bias, activation; output columns n0*8 + 2c (+1) and (n0 + 1)*8 + 2c (+1)
                 const int na = 8 * n0 + 2 * c4, nb = na + 8;
                 float v[8] = {acc0[0] + B[na], acc0[1] + B[na + 1], acc0[2] + B[na], acc0[3] + B[na + 1],
@@ -258,8 +265,14 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                     reinterpret_cast<uint4*>(smem + S.hhi[l & 1])[(mt * KTn + jw) * 32 + lane] = hi;
                     reinterpret_cast<uint4*>(smem + S.hlo[l & 1])[(mt * KTn + jw) * 32 + lane] = lo;
                 }
+#ifdef FLW_LEARN_TRACE
+                if (trl_on) trl[1][l] = clock64();
+#endif
             }
             tile_sync(mt);
+#ifdef FLW_LEARN_TRACE
+            if (step == a.step0 + 2 && l < 8) trl[2][l] = clock64();
+#endif
         }
 #ifdef FLW_LEARN_TRACE
         if (step - a.step0 < 8) tr1[step - a.step0] = clock64();
@@ -357,6 +370,10 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
 #ifdef FLW_LEARN_TRACE
     if (blockIdx.x == 0 && t == 0)
         for (int i = 0; i < 8; ++i) printf("R step %d mlp %lld owner %lld\n", i, tr1[i] - tr0[i], tr2[i] - tr1[i]);
+    if (blockIdx.x == 0 && t == 0)
+        for (int l = 0; l < a.L && l < 8; ++l)
+            printf("RL layer %d mma %lld epi %lld sync %lld\n", l, trl[0][l] - (l ? trl[2][l - 1] : tr0[2]),
+                   trl[1][l] - trl[0][l], trl[2][l] - trl[1][l]);
 #endif
     if (live) {
 #pragma unroll

@@ -198,46 +198,48 @@ __device__ __forceinline__ float warp_colsum8(float* v, int lane) {
     return s;
 }
 
-// The same reduce-scatter for a 32-wide slice held as 16 packed bf16 pairs (pair j = columns
-// 2j | 2j+1, low half first): the first level exchanges whole pairs (8 shuffles instead of 16)
-// and the sums, orders and results are those of warp_colsum32 on the unpacked values.
-__device__ __forceinline__ float warp_colsum32_bf16(const uint32_t* pk, int lane) {
-    const bool up = (lane & 16) != 0;
-    float v[16];
+// Column sums of the 32 rows [32 q, 32 q + 32) of a bf16 operand tile in shared memory (core-
+// matrix layout, width C <= 64), added to acc[0, C): lane (k = lane & 7, s = lane >> 3) sums
+// the 8-column chunk k over the 8 rows of core block 4q + s, reading them in the order rotated
+// by k (the eight chunks of one read hit disjoint banks), then a two-level reduce-scatter over
+// s (6 shuffles) leaves columns 8k + 4 s0 + 2 s1 + {0, 1} on the lane. Fixed order throughout.
+__device__ __forceinline__ void warp_colsum_tile(const uint8_t* tile, int C, int q, int lane, float* acc) {
+    const int k = lane & 7, s = lane >> 3;
+    float v[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const uint32_t keep = up ? pk[j + 8] : pk[j];
-        const uint32_t recv = __shfl_xor_sync(0xffffffffu, up ? pk[j] : pk[j + 8], 16);
-        const float2 s2 = __fadd2_rn(make_float2(__uint_as_float(keep << 16), __uint_as_float(keep & 0xFFFF0000u)),
-                                     make_float2(__uint_as_float(recv << 16), __uint_as_float(recv & 0xFFFF0000u)));
-        v[2 * j] = s2.x;
-        v[2 * j + 1] = s2.y;
-    }
-#pragma unroll
-    for (int w = 8, off = 8; off > 0; w >>= 1, off >>= 1) {
-        const bool hi = (lane & off) != 0;
-        float k[8], rv[8];
+    for (int j = 0; j < 8; ++j) v[j] = 0.0f;
+    if (8 * k < C) {
+        const uint8_t* base = tile + (4 * q + s) * (C * 16) + k * 128;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            if (i < w) {
-                k[i] = hi ? v[i + w] : v[i];
-                rv[i] = __shfl_xor_sync(0xffffffffu, hi ? v[i] : v[i + w], off);
-            }
-        }
-        if (w >= 2) {  // the level's adds as packed f32x2 adds (same per-element rounding)
+            const uint4 w = *reinterpret_cast<const uint4*>(base + ((i + k) & 7) * 16);
+            const uint32_t p[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-            for (int i = 0; i < 8; i += 2) {
-                if (i < w) {
-                    const float2 s2 = __fadd2_rn(make_float2(k[i], k[i + 1]), make_float2(rv[i], rv[i + 1]));
-                    v[i] = s2.x;
-                    v[i + 1] = s2.y;
-                }
+            for (int j = 0; j < 4; ++j) {
+                const float2 s2 = __fadd2_rn(make_float2(v[2 * j], v[2 * j + 1]),
+                                             make_float2(__uint_as_float(p[j] << 16), __uint_as_float(p[j] & 0xFFFF0000u)));
+                v[2 * j] = s2.x;
+                v[2 * j + 1] = s2.y;
             }
-        } else {
-            v[0] = k[0] + rv[0];
         }
     }
-    return v[0];
+    const bool up8 = (lane & 8) != 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float keep = up8 ? v[4 + i] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, up8 ? v[i] : v[4 + i], 8);
+    }
+    const bool up16 = (lane & 16) != 0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float keep = up16 ? v[2 + i] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, up16 ? v[i] : v[2 + i], 16);
+    }
+    if (8 * k < C) {
+        float2* a2 = reinterpret_cast<float2*>(acc + 8 * k + (up8 ? 4 : 0) + (up16 ? 2 : 0));
+        const float2 o = *a2;
+        *a2 = make_float2(o.x + v[0], o.y + v[1]);
+    }
 }
 
 // MODE 0: values pass (critic forward, saves activations); 1: learn (forward + backward);
@@ -260,9 +262,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
     __shared__ uint32_t epi_cnt[kGroups];  // epilogue hand-offs per group (4 per stage), for the loader
     __shared__ uint32_t rd_cnt[kGroups];   // loader: bulk stores whose smem read completed (producer)
     __shared__ uint32_t xf_cnt[kGroups];   // loader, values pass: last saved tile read (epilogue)
+    __shared__ double s_adv[2];            // advantage {mean, sd} (one unit: uniform over the rows)
+    __shared__ int s_adv_on;
 #ifdef FLW_LEARN_TRACE
-    __shared__ long long tr_p[4][64], tr_e[3][64], tr_f[5][16];
-    int np_ev = 0, ne_ev = 0, nf_ev = 0;
+    __shared__ long long tr_p[4][64], tr_e[3][64], tr_f[5][16], tr_b[4][32], tr_l[6][8];
+    int np_ev = 0, ne_ev = 0, nf_ev = 0, nb_ev = 0, nl_ev = 0;
 #endif
     const FastNet& n = a.net;
     const int t = threadIdx.x, w = uni(static_cast<int>(t >> 5)), lane = t & 31;
@@ -302,6 +306,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
         umma::mbar_init(&zbar, 1);
         for (int g = 0; g < kGroups; ++g) epi_cnt[g] = rd_cnt[g] = xf_cnt[g] = 0;
         for (int l = 0; l < kMaxLayers; ++l) dwtok[l] = 0;
+        s_adv_on = a.adv_stats && !a.rep_of_env;
+        s_adv[0] = s_adv_on ? a.adv_stats[0] : 0.0;
+        s_adv[1] = s_adv_on ? a.adv_stats[1] : 0.0;
         umma::fence_barrier_init();
         // the weight image's copy starts first: it overlaps the rest of the setup
         bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
@@ -657,8 +664,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                     *reinterpret_cast<uint4*>(xs + umma::tile_offset(r, c0, din0)) = make_uint4(0u, 0u, 0u, 0u);
                 fetch_x(tile + kGroups * G);
             }
-            int act_r = 0;
-            float lpo_r = 0.0f, adv_r = 0.0f, ret_r = 0.0f, val_r = 0.0f;
+            int act_r = 0, rep_r = 0;
+            float lpo_r = 0.0f, adv_r = 0.0f, ret_r = 0.0f, val_r = 0.0f, inv_n_r = 0.0f;
             // the loss epilogue's per-row inputs: issued two forward stages ahead of their use
             // (not at the tile start), so they are neither held across the whole forward nor
             // waited for at the loss stage
@@ -671,15 +678,38 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                         adv_r = a.adv[row];
                     }
                     if (a.kind == kNetPolicyA3c || reuse) val_r = a.values_in[row];
+                    if (a.rep_of_env) rep_r = a.rep_of_env[row % a.rep_E];
                 }
             };
-            if (!fwd) load_rows();
+            // the row's loss weight and normalised advantage, computed while the last forward
+            // MMA runs (the statistics' loads and the double division are off the loss stage)
+            auto prep_rows = [&]() {
+                if (!(learn && valid)) return;
+                inv_n_r = static_cast<float>(a.inv_n);
+                double am = s_adv[0], asd = s_adv[1];
+                bool norm = s_adv_on != 0;
+                if (a.rep_of_env) {  // folded replicas: this row's unit weight and statistics
+                    inv_n_r = a.rep_w[rep_r];
+                    if (a.adv_stats) {
+                        am = a.adv_stats[2 * rep_r];
+                        asd = a.adv_stats[2 * rep_r + 1];
+                        norm = true;
+                    }
+                }
+                if (a.kind == kNetPolicyPpo && norm && !(asd < 1e-8))
+                    adv_r = static_cast<float>((adv_r - am) / (asd + 1e-8));
+            };
+            if (!fwd) {
+                load_rows();
+                prep_rows();
+            }
             float out[NA];
             if (fwd) {
                 signal();  // X ready
                 for (int l = 0; l < L; ++l) {
                     const int dout = n.dout[l];
                     if (l == (L > 2 ? L - 2 : 0)) load_rows();
+                    if (l == L - 1) prep_rows();
                     wait_mma();
                     const float* bl = bias + l * kMaxW;
                     if (l + 1 < L) {
@@ -776,6 +806,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                 continue;
             }
             // ---- loss epilogue (rl.cpp:137-202 semantics, f32) -> dZ_{L-1}
+#ifdef FLW_LEARN_TRACE
+            const bool trl = g == 0 && t == 0 && nl_ev < 8;
+            if (trl) tr_l[0][nl_ev] = clock64();
+#endif
             // Static loop bounds only (predicated on the action count) and the probabilities
             // recomputed per use instead of held in arrays: out[] and dz[] stay in registers.
             {
@@ -783,13 +817,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
 #pragma unroll
                 for (int j = 0; j < NA; ++j) dz[j] = 0.0f;
                 if (valid) {
-                    float inv_n = static_cast<float>(a.inv_n);
-                    const double* ast = a.adv_stats;
-                    if (a.rep_of_env) {  // folded replicas: this row's unit weight and statistics
-                        const int rr = a.rep_of_env[row % a.rep_E];
-                        inv_n = a.rep_w[rr];
-                        if (ast) ast += 2 * rr;
-                    }
+                    const float inv_n = inv_n_r;
                     if (a.kind == kNetCritic) {  // value MSE: dV = 2 c_v (V - R) / N
                         const float verr = out[0] - ret_r;
                         dz[0] = static_cast<float>(2.0 * a.value_coef) * inv_n * verr;
@@ -800,27 +828,32 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
 #pragma unroll
                         for (int j = 1; j < NA; ++j)
                             if (j < A) mx = fmaxf(mx, out[j]);
-                        float den = 0.0f;
+                        // the exponentials once (the MUFU pipe is shared with the other groups'
+                        // tanh epilogues: every dependent MUFU stage here queues behind them)
+                        float pr[NA], den = 0.0f;
 #pragma unroll
-                        for (int j = 0; j < NA; ++j)
-                            if (j < A) den += __expf(out[j] - mx);
-                        const float lden = __logf(den);
+                        for (int j = 0; j < NA; ++j) {
+                            pr[j] = j < A ? __expf(out[j] - mx) : 0.0f;
+                            den += pr[j];
+                        }
+                        const float lden = __logf(den), rden = __fdividef(1.0f, den);
+#pragma unroll
+                        for (int j = 0; j < NA; ++j) pr[j] *= rden;  // probabilities
+#ifdef FLW_LEARN_TRACE
+                        if (trl) tr_l[3][nl_ev] = clock64();
+#endif
                         float H = 0.0f, lpa = 0.0f;
 #pragma unroll
                         for (int j = 0; j < NA; ++j) {
                             if (j < A) {
                                 const float lp = out[j] - mx - lden;
-                                H -= __expf(lp) * lp;
+                                H -= pr[j] * lp;
                                 if (j == act_r) lpa = lp;
                             }
                         }
                         float coef;
                         if (a.kind == kNetPolicyPpo) {
-                            float adv = adv_r;
-                            if (ast) {
-                                const double sd = ast[1];
-                                if (!(sd < 1e-8)) adv = static_cast<float>((adv - ast[0]) / (sd + 1e-8));
-                            }
+                            const float adv = adv_r;  // normalised by prep_rows
                             const float ratio = __expf(lpa - lpo_r);
                             const float clipped = fminf(fmaxf(ratio, 1.0f - a.clip_eps), 1.0f + a.clip_eps);
                             const float s1 = ratio * adv, s2 = clipped * adv;
@@ -832,11 +865,14 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                             coef = -inv_n * adv;
                         }
                         en_acc += H * inv_n;
+#ifdef FLW_LEARN_TRACE
+                        if (trl) tr_l[4][nl_ev] = clock64();
+#endif
                         const float eci = static_cast<float>(a.entropy_coef) * inv_n;
 #pragma unroll
                         for (int j = 0; j < NA; ++j) {
                             if (j < A) {
-                                const float lp = out[j] - mx - lden, pj = __expf(lp);
+                                const float lp = out[j] - mx - lden, pj = pr[j];
                                 dz[j] = coef * ((j == act_r ? 1.0f : 0.0f) - pj) + eci * pj * (lp + H);
                             }
                         }
@@ -857,7 +893,13 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                         }
                     }
                 }
+#ifdef FLW_LEARN_TRACE
+                if (trl) tr_l[5][nl_ev] = clock64();
+#endif
                 signal();  // dZ_{L-1} ready
+#ifdef FLW_LEARN_TRACE
+                if (trl) tr_l[1][nl_ev] = clock64();
+#endif
                 // bias gradient of the output layer: columns >= rout are zero
                 const int ro = n.rout[L - 1];
                 if (ro <= 8) {
@@ -870,6 +912,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                     colsum32(v32, 0, wo, L - 1);
                 }
             }
+#ifdef FLW_LEARN_TRACE
+            if (trl) tr_l[2][nl_ev++] = clock64();
+#endif
             // ---- backward epilogues: dZ_{m-1} = dH_m * act'(H_{m-1})
             for (int m = L - 1; m >= 1; --m) {
                 const int di = n.din[m];
@@ -881,9 +926,12 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                 }
                 const uint8_t* hs = smem + C.ring[g][s];
                 uint8_t* dst = smem + C.dz[g];
+#ifdef FLW_LEARN_TRACE
+                const bool trb = g == 0 && t == 0 && nb_ev < 32;
+                if (trb) tr_b[0][nb_ev] = clock64();
+#endif
                 auto half = [&]<bool FULL, int h0>() {
                     float gv[32];
-                    uint32_t pkc[16];  // the bf16 dZ pairs of these 32 columns (what dW and db see)
                     umma::tmem_ld16(zt + h0, gv);
                     if (FULL || h0 + 16 < di) umma::tmem_ld16(zt + h0 + 16, gv + 16);
                     umma::tmem_ld_wait();
@@ -906,25 +954,32 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                                     d = make_float2(yy.x > 0.0f ? gg.x : 0.0f, yy.y > 0.0f ? gg.y : 0.0f);
                                 }
                                 pk[i] = umma::pack_bf16x2(d.x, d.y);
-                                pkc[c / 2 + i] = pk[i];  // db sums exactly the bf16 operand dW sees
                             }
                             *reinterpret_cast<uint4*>(dst + umma::tile_offset(r, h0 + c, di)) =
                                 make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) pkc[c / 2 + i] = 0u;
                         }
                     }
-                    if (h0 + 32 >= di) signal();  // dZ_{m-1} complete: hand it to the producer
-                    mydb[(m - 1) * kMaxW + h0 + lane] += warp_colsum32_bf16(pkc, lane);
                 };
                 if (di == kMaxW) {
                     half.template operator()<true, 0>();
+#ifdef FLW_LEARN_TRACE
+                    if (trb) tr_b[1][nb_ev] = clock64();
+#endif
                     half.template operator()<true, 32>();
                 } else {
                     half.template operator()<false, 0>();
                     if (32 < di) half.template operator()<false, 32>();
                 }
+                signal();  // dZ_{m-1} complete: hand it to the producer
+#ifdef FLW_LEARN_TRACE
+                if (trb) tr_b[2][nb_ev] = clock64();
+#endif
+                // bias gradient off the hand-off path: column sums of this warp's 32 rows of the
+                // bf16 dZ_{m-1} just stored (exactly the operand dW sees), read back from the slot
+                warp_colsum_tile(dst, di, q, lane, mydb + (m - 1) * kMaxW);
+#ifdef FLW_LEARN_TRACE
+                if (trb) tr_b[3][nb_ev++] = clock64();
+#endif
 
             }
             if (!resident(-1) && !dx) ph_ld ^= 2u;  // X's reload (stage 0): consumed by the producer only
@@ -1050,6 +1105,12 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
         const long long t0 = tr_p[0][0];
         for (int i = 0; i < ne_ev; ++i)
             printf("E%d %2d wait %7lld got %7lld signal %7lld\n", MODE, i, tr_e[0][i] - t0, tr_e[1][i] - t0, tr_e[2][i] - t0);
+        for (int i = 0; i < nb_ev; ++i)
+            printf("B %2d got %7lld half0 %7lld signaled %7lld end %7lld\n", i, tr_b[0][i] - t0, tr_b[1][i] - t0,
+                   tr_b[2][i] - t0, tr_b[3][i] - t0);
+        for (int i = 0; i < nl_ev; ++i)
+            printf("L %2d start %7lld softmax %7lld coef %7lld stored %7lld signaled %7lld end %7lld\n", i, tr_l[0][i] - t0,
+                   tr_l[3][i] - t0, tr_l[4][i] - t0, tr_l[5][i] - t0, tr_l[1][i] - t0, tr_l[2][i] - t0);
         for (int i = 0; i < nf_ev; ++i)
             printf("F %2d start %7lld half0 %7lld stores %7lld signaled %7lld bulk %7lld\n", i, tr_f[0][i] - t0,
                    tr_f[1][i] - t0, tr_f[2][i] - t0, tr_f[3][i] - t0, tr_f[4][i] - t0);

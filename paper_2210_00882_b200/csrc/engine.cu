@@ -298,6 +298,18 @@ void Engine::set_p2p_peers(int rank, int k, const std::vector<void*>& regions) {
     FLW_CUDA(cudaMemcpy(p2p_peers_dev_, regions.data(), sizeof(void*) * regions.size(), cudaMemcpyHostToDevice));
     p2p_rank_ = rank;
     p2p_k_ = k;
+    // the fused exchange kernel's blocks wait for the other ranks' blocks: only safe when no two
+    // ranks share a GPU (FLW_P2P_FUSED=0 forces the two-kernel form, A/B)
+    static const char* fz = std::getenv("FLW_P2P_FUSED");
+    p2p_fused_ = !(fz && fz[0] == '0');
+    for (int r = 0; r < k && p2p_fused_; ++r) {
+        if (r == rank) continue;
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, regions[static_cast<size_t>(r)]) != cudaSuccess || at.device == device_) {
+            cudaGetLastError();
+            p2p_fused_ = false;
+        }
+    }
 }
 
 void Engine::alloc_p2p_region(int k) {
@@ -1445,7 +1457,7 @@ void Engine::enq_grad_sync_and_adam() {
         }
         coll_tick(stream_, b.ctx);
         probe_begin("exchange_adam");
-        reduce_allreduce_adam(stream_, a);
+        reduce_allreduce_adam(stream_, a, p2p_fused_);
         probe_end();
         return;
     }

@@ -165,6 +165,7 @@ class Engine {
     bool pcompact_ = false;  // fast MAPPO, observation > 64, hidden <= 64: layer 0 on GEMMs
     bool gemm_roll_ = false;  // fast numerics: rollout policy forward as split-f16 GEMMs
     int p2p_rank_ = 0, p2p_k_ = 0;
+    bool p2p_fused_ = false;  // every peer region on another GPU: the one-kernel exchange
     void* p2p_region_ptr_ = nullptr;
     int p2p_alloc_k_ = 0;
     std::vector<void*> p2p_ipc_opened_;

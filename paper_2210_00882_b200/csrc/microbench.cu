@@ -318,7 +318,7 @@ void microbench(const std::string& which, int64_t n, int iters, double* ms, doub
             a.gscale = 1.0;
             *ms = time_launches([&] {
                 coll_tick(0, ctx);
-                reduce_allreduce_adam(0, a);
+                reduce_allreduce_adam(0, a, true);  // k = 1: waits on its own push only
             }, iters);
         }
         // survey: 44 B/param of Adam with f64 moments + 4 B per partial slot of the reduction

@@ -38,6 +38,8 @@ struct P2pArgs {
 };
 
 void coll_tick(cudaStream_t s, DeviceCtx* ctx);  // ++ctx->coll_seq (one per exchange)
-void reduce_allreduce_adam(cudaStream_t s, const P2pArgs& a);
+// fused: one kernel (reduce + push + wait + Adam per chunk); only when every peer region lives
+// on another GPU (blocks of co-located ranks could fill the device and wait on each other)
+void reduce_allreduce_adam(cudaStream_t s, const P2pArgs& a, bool fused);
 
 }  // namespace flw

@@ -300,8 +300,8 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
             dx.kind = "nccl_allgather";
             dx.bytes_per_episode = I * static_cast<int64_t>(ng) * (ng - 1) * R * P4;
         } else if (e0.p2p_enabled()) {
-            dx.kind = "p2p";
-            dx.bytes_per_episode = I * static_cast<int64_t>(ng) * (ng - 1) * P4;
+            dx.kind = "p2p";  // one 8-byte {value, epoch} word per parameter and peer
+            dx.bytes_per_episode = I * static_cast<int64_t>(ng) * (ng - 1) * 2 * P4;
         } else {
             dx.kind = "nccl_allreduce";
             dx.bytes_per_episode = I * 2 * static_cast<int64_t>(ng - 1) * P4;

@@ -76,7 +76,7 @@ def test_fast_peer_memory_exchange_matches_nccl(gpus):
     sp, sn = out["p2p"][1], out["nccl"][1]
     P = sp["param_count"]
     assert sp["device_exchange"]["kind"] == "p2p"
-    assert sp["device_exchange"]["bytes_per_episode"] == 4 * gpus * (gpus - 1) * 4 * P
+    assert sp["device_exchange"]["bytes_per_episode"] == 4 * gpus * (gpus - 1) * 8 * P  # {value, epoch} words
     assert sn["device_exchange"]["kind"] == "nccl_allreduce"
     assert sn["device_exchange"]["bytes_per_episode"] == 4 * 2 * (gpus - 1) * 4 * P
     if gpus == 2:

@@ -51,7 +51,12 @@ __host__ __device__ constexpr int groups_for(int mode) { return mode == 0 ? 4 : 
 constexpr int kGroupsMax = 4;
 constexpr int kGroups = groups_for(1);
 // + two MMA producers (groups split by parity) + loader
-__host__ __device__ constexpr int threads_for(int mode) { return 32 * (4 * groups_for(mode) + 3); }
+// (learn modes: + one idle warp, so the non-epilogue warps form a whole warpgroup for setmaxnreg)
+__host__ __device__ constexpr int threads_for(int mode) { return 32 * (4 * groups_for(mode) + (mode != 0 ? 4 : 3)); }
+// learn modes: registers per thread after the role split (3 x 128 x 152 + 128 x 56 = 65536): the
+// epilogue warps hold a row's accumulators, activations and loss inputs; the producers and the
+// loader only issue
+constexpr int kRegEpi = 152, kRegSide = 56;
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
 constexpr int kXPre = 18;                      // input columns prefetched in registers (9 packed regs)
 #ifndef FLW_TANH_MUFU_PAIRS
@@ -332,7 +337,13 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
     const uint32_t tmem = uni(tslot);
     const uint32_t sbase = umma::smem_u32(smem);
 
+    // learn modes: the register file is rebalanced between the roles (per warpgroup: the
+    // producers, the loader and the idle warp form the last one)
+    auto regs_side = [&]() {
+        if constexpr (MODE != 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegSide));
+    };
     if (w == kEpiWarps || w == kEpiWarps + 2) {
+        regs_side();
         // ================================================================ producer (whole warp)
         // The warp runs the issue loop converged (warp-uniform control flow and operands); one
         // elected lane issues each tcgen05.mma / commit / bulk copy (umma::mma_bf16_warp).
@@ -459,6 +470,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
             }
         }
     } else if (w == kEpiWarps + 1) {
+        regs_side();
         // ================================================================ loader (learn modes)
         // The backward streams the activation tiles it does not keep resident back from global
         // memory (learn: this CTA's scratch, written by the producer's bulk stores during the
@@ -553,7 +565,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
             if (lane == 0) umma::bulk_wait_all();  // values pass: the saved tiles are written
             __syncwarp();
         }
-    } else {
+    } else if (w < kEpiWarps) {
+        if constexpr (MODE != 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegEpi));
         // ================================================================ epilogue groups
         // the dW zero-init MMAs read group 0's dz slot: no dZ store before they completed
         // (learn-reuse writes dZ_{L-1} before any MMA of its own)
@@ -1023,6 +1036,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
             ls[w * 3 + 1] = vl_acc;
             ls[w * 3 + 2] = en_acc;
         }
+    } else {
+        regs_side();  // the idle warp (learn modes)
     }
     umma::fence_before_sync();
     __syncthreads();

@@ -203,6 +203,12 @@ __device__ __forceinline__ float warp_colsum8(float* v, int lane) {
     return s;
 }
 
+// acc + x for a bf16 x, rounded once to f32 (mixed-precision add: the bf16 half is read in place)
+__device__ __forceinline__ float add_f32_bf16(float acc, uint16_t x) {
+    asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(acc) : "h"(x));
+    return acc;
+}
+
 // Column sums of the 32 rows [32 q, 32 q + 32) of a bf16 operand tile in shared memory (core-
 // matrix layout, width C <= 64), added to acc[0, C): lane (k = lane & 7, s = lane >> 3) sums
 // the 8-column chunk k over the 8 rows of core block 4q + s, reading them in the order rotated
@@ -220,11 +226,9 @@ __device__ __forceinline__ void warp_colsum_tile(const uint8_t* tile, int C, int
             const uint4 w = *reinterpret_cast<const uint4*>(base + ((i + k) & 7) * 16);
             const uint32_t p[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float2 s2 = __fadd2_rn(make_float2(v[2 * j], v[2 * j + 1]),
-                                             make_float2(__uint_as_float(p[j] << 16), __uint_as_float(p[j] & 0xFFFF0000u)));
-                v[2 * j] = s2.x;
-                v[2 * j + 1] = s2.y;
+            for (int j = 0; j < 4; ++j) {  // f32 += bf16 (FHADD.BF16: no unpacking; exact widening)
+                v[2 * j] = add_f32_bf16(v[2 * j], static_cast<uint16_t>(p[j] & 0xFFFFu));
+                v[2 * j + 1] = add_f32_bf16(v[2 * j + 1], static_cast<uint16_t>(p[j] >> 16));
             }
         }
     }

@@ -204,8 +204,8 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
         for (int l = 0; l < a.L; ++l) {
             const int in = a.dims[l], out = a.dims[l + 1], KT = pad16(in) / 16, NT = pad8(out) / 8;
             const bool last = l + 1 == a.L;
-            const uint4* Ahi = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xhi : S.hhi[(l - 1) & 1]));
-            const uint4* Alo = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xlo : S.hlo[(l - 1) & 1]));
+            const uint4* Ahi = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xhi : ((l - 1) & 1) ? S.hhi[1] : S.hhi[0]));
+            const uint4* Alo = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xlo : ((l - 1) & 1) ? S.hlo[1] : S.hlo[0]));
             const uint4* Wf = reinterpret_cast<const uint4*>(smem + woff);
             const float* B = reinterpret_cast<const float*>(smem + woff + wfrag_bytes(in, out));
             woff += wfrag_bytes(in, out) + static_cast<uint32_t>(pad16(out) * 4);
@@ -262,8 +262,8 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
                     split_f16x2(v[4], v[5], hi.z, lo.z);
                     split_f16x2(v[6], v[7], hi.w, lo.w);
                     const int KTn = pad16(out) / 16;
-                    reinterpret_cast<uint4*>(smem + S.hhi[l & 1])[(mt * KTn + jw) * 32 + lane] = hi;
-                    reinterpret_cast<uint4*>(smem + S.hlo[l & 1])[(mt * KTn + jw) * 32 + lane] = lo;
+                    reinterpret_cast<uint4*>(smem + ((l & 1) ? S.hhi[1] : S.hhi[0]))[(mt * KTn + jw) * 32 + lane] = hi;
+                    reinterpret_cast<uint4*>(smem + ((l & 1) ? S.hlo[1] : S.hlo[0]))[(mt * KTn + jw) * 32 + lane] = lo;
                 }
 #ifdef FLW_LEARN_TRACE
                 if (trl_on) trl[1][l] = clock64();
@@ -283,25 +283,38 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             // by <= ~1 f32 ulp, far below the f32-logit deviation the fast path already has);
             // the draw and the inverse-CDF walk are the reference's (double u, double cumsum)
             const float* logits = reinterpret_cast<const float*>(smem + S.logits) + le * kLStride;
+            // static loop bounds (predicated on A <= 16): p[] stays in registers
             float p[16];
             float mx = logits[0];
-            for (int c = 1; c < A; ++c) mx = fmaxf(mx, logits[c]);
+#pragma unroll
+            for (int c = 1; c < 16; ++c)
+                if (c < A) mx = fmaxf(mx, logits[c]);
             float den = 0.0f;
-            for (int c = 0; c < A; ++c) {
-                p[c] = __expf(logits[c] - mx);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                p[c] = c < A ? __expf(logits[c] - mx) : 0.0f;
                 den += p[c];
             }
             const float rden = 1.0f / den;
-            for (int c = 0; c < A; ++c) p[c] *= rden;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) p[c] *= rden;
             double cum = 0.0;
             int chosen = A - 1;
-            for (int c = 0; c < A; ++c) {
-                cum = __dadd_rn(cum, static_cast<double>(p[c]));
-                if (u < cum) {
-                    chosen = c;
-                    break;
+            float pch = 0.0f;  // p[chosen]
+            bool found = false;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {  // the first c with u < cumsum (interp.cpp:175-203)
+                if (c < A && !found) {
+                    cum = __dadd_rn(cum, static_cast<double>(p[c]));
+                    if (u < cum) {
+                        chosen = c;
+                        found = true;
+                    }
                 }
             }
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (c == chosen) pch = p[c];
             double rew = 0.0;
             bool d = done;
             if (!done) {
@@ -342,7 +355,7 @@ __global__ void __launch_bounds__(kThreads) k_rollout_episode(const DeviceCtx* _
             if (live) {
                 const int64_t ti = step * E + e;
                 a.actions[ti] = chosen;
-                a.logp[ti] = __logf(fmaxf(p[chosen], 1e-30f));
+                a.logp[ti] = __logf(fmaxf(pch, 1e-30f));
                 a.reward[ti] = done ? 0.0f : static_cast<float>(rew);
                 a.reward_d[ti] = f16_oob ? __longlong_as_double(0x7ff8000000000000LL) : (done ? 0.0 : rew);
                 a.done_f[ti] = (done || d) ? 1.0f : 0.0f;
@@ -537,8 +550,8 @@ __global__ void __launch_bounds__(256, 1) k_rollout_mappo_fast(const DeviceCtx* 
         for (int l = 0; l < a.L; ++l) {
             const int in = a.dims[l], out = a.dims[l + 1], KT = pad16(in) / 16, NT = pad8(out) / 8;
             const bool last = l + 1 == a.L;
-            const uint4* Ahi = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xhi : S.hhi[(l - 1) & 1]));
-            const uint4* Alo = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xlo : S.hlo[(l - 1) & 1]));
+            const uint4* Ahi = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xhi : ((l - 1) & 1) ? S.hhi[1] : S.hhi[0]));
+            const uint4* Alo = reinterpret_cast<const uint4*>(smem + (l == 0 ? S.xlo : ((l - 1) & 1) ? S.hlo[1] : S.hlo[0]));
             const uint4* Wf = reinterpret_cast<const uint4*>(smem + woff);
             const float* B = reinterpret_cast<const float*>(smem + woff + wfrag_bytes(in, out));
             woff += wfrag_bytes(in, out) + static_cast<uint32_t>(pad16(out) * 4);
@@ -587,8 +600,8 @@ __global__ void __launch_bounds__(256, 1) k_rollout_mappo_fast(const DeviceCtx* 
                     split_f16x2(v[2], v[3], hi.y, lo.y);
                     split_f16x2(v[4], v[5], hi.z, lo.z);
                     split_f16x2(v[6], v[7], hi.w, lo.w);
-                    reinterpret_cast<uint4*>(smem + S.hhi[l & 1])[(mt * KTn + jw) * 32 + lane] = hi;
-                    reinterpret_cast<uint4*>(smem + S.hlo[l & 1])[(mt * KTn + jw) * 32 + lane] = lo;
+                    reinterpret_cast<uint4*>(smem + ((l & 1) ? S.hhi[1] : S.hhi[0]))[(mt * KTn + jw) * 32 + lane] = hi;
+                    reinterpret_cast<uint4*>(smem + ((l & 1) ? S.hlo[1] : S.hlo[0]))[(mt * KTn + jw) * 32 + lane] = lo;
                 }
             }
             __syncthreads();
@@ -596,29 +609,41 @@ __global__ void __launch_bounds__(256, 1) k_rollout_mappo_fast(const DeviceCtx* 
         // ---- PolicyApply: one thread per row (f32 softmax, the reference's draw and walk)
         if (rowt) {
             const float* lg = reinterpret_cast<const float*>(smem + S.logits) + t * kLStride;
+            // static loop bounds (predicated on A <= 16): p[] stays in registers
             float p[16];
             float mx = lg[0];
-            for (int c = 1; c < A; ++c) mx = fmaxf(mx, lg[c]);
+#pragma unroll
+            for (int c = 1; c < 16; ++c)
+                if (c < A) mx = fmaxf(mx, lg[c]);
             float den = 0.0f;
-            for (int c = 0; c < A; ++c) {
-                p[c] = __expf(lg[c] - mx);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                p[c] = c < A ? __expf(lg[c] - mx) : 0.0f;
                 den += p[c];
             }
             const float rden = 1.0f / den;
             double cum = 0.0;
             int chosen = A - 1;
-            for (int c = 0; c < A; ++c) {
+            bool found = false;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
                 p[c] *= rden;
-                cum = __dadd_rn(cum, static_cast<double>(p[c]));
-                if (u < cum) {
-                    chosen = c;
-                    break;
+                if (c < A && !found) {
+                    cum = __dadd_rn(cum, static_cast<double>(p[c]));
+                    if (u < cum) {
+                        chosen = c;
+                        found = true;
+                    }
                 }
             }
+            float pch = 0.0f;  // p[chosen]
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (c == chosen) pch = p[c];
             acts[t] = chosen;
             const int64_t row = static_cast<int64_t>(ra) * E + re;
             a.actions[step * R + row] = chosen;
-            a.logp[step * R + row] = __logf(fmaxf(p[chosen], 1e-30f));
+            a.logp[step * R + row] = __logf(fmaxf(pch, 1e-30f));
         }
         __syncthreads();
         // ---- EnvStep (envs.cpp:111-150; absorbing after done, interp.cpp:239-245): each row

@@ -70,6 +70,14 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def wait_ready(self, timeout_s: float = 5.0):
+        """nvidia-smi's start-up (driver init) must not land in the timed region: it can stall
+        this process's CUDA launches for milliseconds, and at N > 1 the other ranks then wait
+        for it inside the gradient exchange."""
+        t0 = time.perf_counter()
+        while self.proc and not self.samples and time.perf_counter() - t0 < timeout_s:
+            time.sleep(0.02)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
@@ -335,11 +343,12 @@ def bench_ours(args, world, rank, local):
     # warm-up (also captures the episode graph; no instrumentation in the timed graph)
     eng.enable_probes(False)
     eng.run_episodes(0, args.warmup)
-    barrier(world)
-    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        clk.wait_ready()
+        barrier(world)
+        torch.cuda.synchronize()
         dev_ms = eng.run_episodes(args.warmup, args.steps)
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
     barrier(world)
     dev_ms = max_over_ranks(dev_ms, world)
     value = total * T_STEPS * args.steps / (dev_ms / 1e3)
@@ -375,7 +384,10 @@ def bench_ours(args, world, rank, local):
     # per-kernel shares (roofline, kernel_shares): a separately captured graph with CUDA-event
     # probes around the main kernels (external event-record nodes), outside the timed regions
     eng.enable_probes(True)
-    eng.run_episodes(args.warmup + 2 * args.steps, 2)
+    eng.run_episodes(args.warmup + 2 * args.steps, 1)  # captures the probed graph (per-rank delay)
+    torch.cuda.synchronize()
+    barrier(world)  # ranks aligned again: the exchange probes must not absorb the capture skew
+    eng.run_episodes(args.warmup + 2 * args.steps + 1, 2)
     torch.cuda.synchronize()
     probes = eng.probe_times()  # per-kernel ms of the last probed episode
     eng.enable_probes(False)

@@ -94,27 +94,49 @@ __device__ __forceinline__ void reduce_push_chunk(const P2pArgs& a, int c, uint6
     }
 }
 
-// Wait for the k ranks' copies of this thread's parameter (threads [0, 128) of the block), sum
-// them in rank order (every rank computes the identical mean) and apply Adam (adam_step,
-// mlp.cpp:146-161; 1/k folded into the step). false: the host aborted the group.
-__device__ __forceinline__ bool sum_adam_chunk(const P2pArgs& a, int c, uint64_t epoch) {
+// Wait (the whole block) until the k ranks' copies of chunk c carry this exchange's epoch tag.
+// One warp polls: lane l checks the chunk's words l, l+32, ... of every rank, resuming at the
+// first word it has not seen tagged yet; lane 0 alone reads the host-mapped abort word (a PCIe
+// read), every 64 rounds - one poller per block keeps a long wait off the PCIe bus. false: the
+// host aborted the group.
+__device__ __forceinline__ bool wait_chunk(const P2pArgs& a, int c, uint64_t epoch, int* s_abort) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int64_t P = a.Pp + a.Pc;
+        const uint2* inbox =
+            reinterpret_cast<const uint2*>(a.peers[a.rank] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
+        const uint32_t tag = static_cast<uint32_t>(epoch);
+        int pos = 0;  // next (rank, word) of this lane to check: rank = pos / 4, word = lane + 32 (pos % 4)
+        int ab = 0;
+        for (uint32_t round = 1;; ++round) {
+            for (; pos < 4 * a.k; ++pos) {
+                const int64_t i = pad_to_flat(a, 128LL * c + lane + 32 * (pos & 3));
+                if (i >= 0 && ld_tagged(inbox + static_cast<int64_t>(pos >> 2) * P + i).y != tag) break;
+            }
+            if (__all_sync(0xffffffffu, pos == 4 * a.k)) break;
+            if ((round & 63u) == 0) {
+                ab = __shfl_sync(0xffffffffu, lane == 0 ? static_cast<int>(*a.abort_flag) : 0, 0);
+                if (ab) break;
+            }
+            __nanosleep(100);
+        }
+        if (lane == 0) *s_abort = ab;
+    }
+    __syncthreads();
+    return *s_abort == 0;
+}
+
+// Sum the k copies of this thread's parameter (threads [0, 128) of the block; wait_chunk saw
+// them tagged) in rank order - every rank computes the identical mean - and apply Adam
+// (adam_step, mlp.cpp:146-161; 1/k folded into the step).
+__device__ __forceinline__ void sum_adam_chunk(const P2pArgs& a, int c, uint64_t epoch) {
     const int64_t P = a.Pp + a.Pc;
     const int64_t i = threadIdx.x < 128 ? pad_to_flat(a, 128LL * c + threadIdx.x) : -1;
-    if (i < 0) return true;
+    if (i < 0) return;
     const uint2* inbox =
         reinterpret_cast<const uint2*>(a.peers[a.rank] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
-    const uint32_t tag = static_cast<uint32_t>(epoch);
     float gs = 0.0f;
-    for (int r = 0; r < a.k; ++r) {
-        uint2 w = ld_tagged(inbox + static_cast<int64_t>(r) * P + i);
-        for (uint32_t spin = 1; w.y != tag; ++spin) {
-            // the abort word lives in host memory (a PCIe read): polled every 512 spins only
-            if ((spin & 511u) == 0 && *a.abort_flag) return false;  // the host aborted the group
-            __nanosleep(32);
-            w = ld_tagged(inbox + static_cast<int64_t>(r) * P + i);
-        }
-        gs += __uint_as_float(w.x);
-    }
+    for (int r = 0; r < a.k; ++r) gs += __uint_as_float(ld_tagged(inbox + static_cast<int64_t>(r) * P + i).x);
     const double g = __dmul_rn(static_cast<double>(gs), a.gscale);
     const double bc1 = a.ctx->bc1, bc2 = a.ctx->bc2;
     const double mi = __dadd_rn(__dmul_rn(a.b1, a.m[i]), __dmul_rn(__dsub_rn(1.0, a.b1), g));
@@ -130,7 +152,6 @@ __device__ __forceinline__ bool sum_adam_chunk(const P2pArgs& a, int c, uint64_t
         const int64_t e = wimg_elem(pol ? a.pol : a.crit, i);
         if (e >= 0) (pol ? a.img_p : a.img_c)[e] = __float2bfloat16(static_cast<float>(next));
     }
-    return true;
 }
 
 // A (two-kernel form): reduce + push of every chunk; never waits, so any grid size is safe.
@@ -146,9 +167,13 @@ __global__ void __launch_bounds__(256) k_reduce_push(P2pArgs a, int nchunks) {
 // B (two-kernel form): per chunk, wait for the k copies, sum, Adam. Waits only on A kernels,
 // which never wait: no residency requirement.
 __global__ void __launch_bounds__(256) k_sum_adam(P2pArgs a, int nchunks) {
+    __shared__ int s_abort;
     const uint64_t epoch = a.ctx->coll_seq;
-    for (int c = blockIdx.x; c < nchunks; c += gridDim.x)
-        if (!sum_adam_chunk(a, c, epoch)) return;
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        if (!wait_chunk(a, c, epoch, &s_abort)) return;
+        sum_adam_chunk(a, c, epoch);
+        __syncthreads();  // s_abort is rewritten by the next chunk
+    }
 }
 
 // Fused form (peers on distinct GPUs): each block reduces and pushes its chunk, then waits for
@@ -158,11 +183,13 @@ __global__ void __launch_bounds__(256) k_sum_adam(P2pArgs a, int nchunks) {
 // capacity, checked by the host): every block is eventually resident, no cyclic wait.
 __global__ void __launch_bounds__(256) k_exchange_adam(P2pArgs a, int nchunks) {
     __shared__ float4 ws[8][32];
+    __shared__ int s_abort;
     const uint64_t epoch = a.ctx->coll_seq;
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
         reduce_push_chunk(a, c, epoch, ws);
-        if (!sum_adam_chunk(a, c, epoch)) return;
-        __syncthreads();  // ws is rewritten by the next chunk
+        if (!wait_chunk(a, c, epoch, &s_abort)) return;
+        sum_adam_chunk(a, c, epoch);
+        __syncthreads();  // ws / s_abort are rewritten by the next chunk
     }
 }
 

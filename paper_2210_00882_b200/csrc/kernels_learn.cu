@@ -59,18 +59,10 @@ __host__ __device__ constexpr int threads_for(int mode) { return 32 * (4 * group
 constexpr int kRegEpi = 152, kRegSide = 56;
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
 constexpr int kXPre = 18;                      // input columns prefetched in registers (9 packed regs)
-// Of each 8-column chunk's 4 tanh pairs, how many go to MUFU (the rest: the FMA-pipe
-// polynomial). The values pass (four groups of forward-only epilogues) saturates MUFU: 3:1
-// there (0.1249 -> 0.1206 ms per episode); the learn kernels measured best all-MUFU.
-#ifndef FLW_TANH_MUFU_PAIRS_VALUES
-#define FLW_TANH_MUFU_PAIRS_VALUES 3
-#endif
 #ifndef FLW_TANH_MUFU_PAIRS
 #define FLW_TANH_MUFU_PAIRS 4
 #endif
-__host__ __device__ constexpr int mufu_pairs_for(int mode) {
-    return mode == 0 ? FLW_TANH_MUFU_PAIRS_VALUES : FLW_TANH_MUFU_PAIRS;
-}
+constexpr int kMufuPairs = FLW_TANH_MUFU_PAIRS;  // of each 8-column chunk's 4 pairs: MUFU, rest poly
 
 struct Carve {
     uint32_t wt[kMaxLayers], wbytes;
@@ -765,7 +757,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
                                         const float z0 = zz.x, z1 = zz.y;
                                         if constexpr (ACT != 0) {
                                             p[i] = umma::pack_bf16x2(fmaxf(z0, 0.0f), fmaxf(z1, 0.0f));
-                                        } else if (i < mufu_pairs_for(MODE)) {
+                                        } else if (i < kMufuPairs) {
                                             p[i] = umma::pack_bf16x2(tanh_fast(z0), tanh_fast(z1));
                                         } else {
                                             const float2 y2 = tanh_poly2(make_float2(z0, z1));

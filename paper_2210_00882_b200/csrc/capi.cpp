@@ -239,11 +239,24 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
         for (int r = 0; r < R; ++r) rsum[static_cast<size_t>(g * R + r)][static_cast<size_t>(ep)] = v[static_cast<size_t>(r)];
     };
     if (ng == 1) {
-        for (int64_t ep = 0; ep < episodes; ++ep) {
-            auto t0 = std::chrono::steady_clock::now();
-            run_one(0, ep);
-            auto t1 = std::chrono::steady_clock::now();
-            eps[static_cast<size_t>(ep)].wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        // One GPU, no gradient group: the episode gate is pipelined - episode ep + 1 is already
+        // enqueued while the host waits for episode ep and records its reward (same episode
+        // order and results; wall_ms = time between consecutive episode completions).
+        Engine& e0 = *p.engines[0];
+        try {
+            auto t_prev = std::chrono::steady_clock::now();
+            if (episodes > 0) e0.launch_episode(0);
+            for (int64_t ep = 0; ep < episodes; ++ep) {
+                if (ep + 1 < episodes) e0.launch_episode(ep + 1);
+                const std::vector<double> v = e0.finish_episode();
+                for (int r = 0; r < R; ++r) rsum[static_cast<size_t>(r)][static_cast<size_t>(ep)] = v[static_cast<size_t>(r)];
+                const auto t1 = std::chrono::steady_clock::now();
+                eps[static_cast<size_t>(ep)].wall_ms = std::chrono::duration<double, std::milli>(t1 - t_prev).count();
+                t_prev = t1;
+            }
+        } catch (...) {
+            e0.drain_episodes();
+            throw;
         }
     } else {
         // Every engine's episode graph segments are captured before any engine launches.

@@ -223,6 +223,9 @@ Engine::~Engine() {
     b_.reset();
     for (cudaEvent_t e : {ev_fork_, ev_join_, ev_t0_, ev_t1_, ev_lfork_, ev_ljoin_})
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_done_)
+        if (e) cudaEventDestroy(e);
+    if (rs_pinned_) cudaFreeHost(rs_pinned_);
     if (side_) cudaStreamDestroy(side_);
     if (side2_) cudaStreamDestroy(side2_);
     if (stream_) cudaStreamDestroy(stream_);
@@ -1707,6 +1710,50 @@ double Engine::run_episode(int64_t ep, float* device_ms) {
         fail(Errc::Runtime, "fast numerics: an observation left the f16 range (|x| >= 65504) of the rollout's "
                             "split tensor-core MLP; use numerics=exact");
     return r;
+}
+
+void Engine::launch_episode(int64_t ep) {
+    FLW_CUDA(cudaSetDevice(device_));
+    if (grouped()) fail(Errc::Config, "pipelined episodes serve units without a gradient group");
+    if (fl_head_ - fl_tail_ >= kInFlight) fail(Errc::Config, "launch_episode: too many episodes in flight");
+    if (!graph_) build_graph();
+    if (!rs_pinned_) {
+        FLW_CUDA(cudaMallocHost(&rs_pinned_, sizeof(double) * static_cast<size_t>(kInFlight * nrep_)));
+        for (cudaEvent_t& e : ev_done_) FLW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int slot = static_cast<int>(fl_head_ % kInFlight);
+    FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, &ep, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+    launch_graph();
+    const int n = numerics_ == Numerics::Exact ? nrep_ : 1;  // (fast: the total in slot 0)
+    FLW_CUDA(cudaMemcpyAsync(rs_pinned_ + static_cast<size_t>(slot) * nrep_, b_->rsum, sizeof(double) * n,
+                             cudaMemcpyDeviceToHost, stream_));
+    FLW_CUDA(cudaEventRecord(ev_done_[slot], stream_));
+    ++fl_head_;
+}
+
+std::vector<double> Engine::finish_episode() {
+    FLW_CUDA(cudaSetDevice(device_));
+    if (fl_tail_ == fl_head_) fail(Errc::Config, "finish_episode: no episode in flight");
+    const int slot = static_cast<int>(fl_tail_ % kInFlight);
+    FLW_CUDA(cudaEventSynchronize(ev_done_[slot]));
+    ++fl_tail_;
+    steps_ += T_ * nrep_;
+    cur_step_ = T_;
+    const int n = numerics_ == Numerics::Exact ? nrep_ : 1;
+    std::vector<double> r(static_cast<size_t>(nrep_), 0.0);
+    for (int i = 0; i < n; ++i) r[static_cast<size_t>(i)] = rs_pinned_[static_cast<size_t>(slot) * nrep_ + i];
+    double total = 0.0;
+    for (double v : r) total += v;
+    if (std::isnan(total) && numerics_ == Numerics::Fast)
+        fail(Errc::Runtime, "fast numerics: an observation left the f16 range (|x| >= 65504) of the rollout's "
+                            "split tensor-core MLP; use numerics=exact");
+    return r;
+}
+
+void Engine::drain_episodes() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    fl_tail_ = fl_head_;
 }
 
 // --------------------------------------------------------------------------- params

@@ -84,6 +84,15 @@ class Engine {
     // Whole episode: Reset, T x Step, I x Learn as one captured CUDA graph. Returns the
     // episode reward sum (sum over this unit's envs, interp.cpp:257) and the device time.
     double run_episode(int64_t ep, float* device_ms = nullptr);
+    // Pipelined episodes of an ungrouped unit (flw_run_local on one GPU): launch_episode
+    // enqueues episode ep (its index, the episode graph, an async copy of its reward sums into a
+    // pinned slot); finish_episode waits for the oldest enqueued episode and returns its
+    // per-replica reward sums. At most kInFlight are enqueued, so the host's per-episode gate
+    // (wait, read the reward, record the episode) overlaps the next episode on the GPU.
+    static constexpr int kInFlight = 2;
+    void launch_episode(int64_t ep);
+    std::vector<double> finish_episode();
+    void drain_episodes();  // after a failure: wait for and discard the in-flight episodes
     // Enqueue `count` episodes starting at `first` back to back (no host sync in between).
     void enqueue_episodes(int64_t first, int64_t count);
     double last_reward_sum();
@@ -176,6 +185,9 @@ class Engine {
     Numerics numerics_;
     cudaStream_t stream_ = nullptr, side_ = nullptr, side2_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_t0_ = nullptr, ev_t1_ = nullptr;
+    double* rs_pinned_ = nullptr;                  // [kInFlight][nrep_] reward sums of in-flight episodes
+    cudaEvent_t ev_done_[kInFlight] = {};          // per slot: the episode and its reward copy finished
+    int64_t fl_head_ = 0, fl_tail_ = 0;            // pipelined episodes launched / finished
     cudaEvent_t ev_lfork_ = nullptr, ev_ljoin_ = nullptr;  // policy || critic learn fork/join
     std::unique_ptr<Bufs> b_;
     std::unique_ptr<Comm> comm_;

@@ -374,11 +374,16 @@ def bench_ours(args, world, rank, local):
                "h2d_bytes_per_step": 8 + 4 * P / args.steps, "d2h_bytes_per_step": 8 + 4 * P / args.steps}
         prog.close()
     else:
+        # (pipelined: episode i + 1 enqueued before the host waits for episode i's reward)
         t0 = time.perf_counter()
+        base = args.warmup + args.steps
+        eng.launch_episode(base)
         for i in range(args.steps):
-            eng.run_episode(args.warmup + args.steps + i)
+            if i + 1 < args.steps:
+                eng.launch_episode(base + i + 1)
+            eng.finish_episode()
         e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-        e2e = {"value": total * T_STEPS * args.steps / e2e_s, "unit": "env-steps/s", "api": "flw_dpd_run_episode",
+        e2e = {"value": total * T_STEPS * args.steps / e2e_s, "unit": "env-steps/s", "api": "flw_dpd_launch_episode/flw_dpd_finish_episode",
                "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 8}
 
     # per-kernel shares (roofline, kernel_shares): a separately captured graph with CUDA-event

@@ -113,6 +113,12 @@ int flw_dpd_abort(flw_dpd* e);
 /* One whole episode (Reset, T x Step, I x Learn) as a replayed CUDA graph. reward_sum is the
  * episode's summed env reward over this unit's envs (interp.cpp:257); device_ms the graph time. */
 int flw_dpd_run_episode(flw_dpd* e, int64_t episode, double* reward_sum, float* device_ms);
+/* Pipelined episodes: launch_episode enqueues an episode (at most 2 in flight) and returns;
+ * finish_episode waits (bounded like run_episode for a unit in a gradient group) for the oldest
+ * enqueued one and returns its reward sum. Launching episode e+1 before finishing e overlaps the
+ * host's per-episode gate with the GPU (flw_run_local does this on one GPU). */
+int flw_dpd_launch_episode(flw_dpd* e, int64_t episode);
+int flw_dpd_finish_episode(flw_dpd* e, double* reward_sum);
 /* Back-to-back episodes without host synchronisation in between (throughput timing). */
 int flw_dpd_run_episodes(flw_dpd* e, int64_t first_episode, int64_t count, float* device_ms);
 int flw_dpd_reinit(flw_dpd* e, uint64_t seed);

@@ -68,6 +68,8 @@ def lib():
         "flw_dpd_comm_init": (ci, [vp, C.c_char_p, i64, ci, ci]),
         "flw_dpd_run_episode": (ci, [vp, i64, P(d), P(C.c_float)]),
         "flw_dpd_run_episodes": (ci, [vp, i64, i64, P(C.c_float)]),
+        "flw_dpd_launch_episode": (ci, [vp, i64]),
+        "flw_dpd_finish_episode": (ci, [vp, P(d)]),
         "flw_dpd_reinit": (ci, [vp, u64]),
         "flw_dpd_param_count": (ci, [vp, P(i64)]),
         "flw_dpd_get_params": (ci, [vp, P(d), i64]),

@@ -142,6 +142,15 @@ class DpdEngine:
         N.check(N.lib().flw_dpd_run_episode(self._h, episode, C.byref(r), C.byref(ms)))
         return r.value, ms.value
 
+    def launch_episode(self, episode: int):
+        """Enqueue one episode (at most two in flight); finish_episode() returns the oldest's reward."""
+        N.check(N.lib().flw_dpd_launch_episode(self._h, episode))
+
+    def finish_episode(self) -> float:
+        r = C.c_double()
+        N.check(N.lib().flw_dpd_finish_episode(self._h, C.byref(r)))
+        return r.value
+
     def run_episodes(self, first: int, count: int) -> float:
         ms = C.c_float()
         N.check(N.lib().flw_dpd_run_episodes(self._h, first, count, C.byref(ms)))

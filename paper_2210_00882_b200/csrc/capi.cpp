@@ -516,6 +516,22 @@ int flw_dpd_run_episode(flw_dpd* e, int64_t episode, double* reward_sum, float* 
     });
 }
 
+int flw_dpd_launch_episode(flw_dpd* e, int64_t episode) {
+    return guarded([&] {
+        eng(e).launch_episode(episode);
+        return FLW_OK;
+    });
+}
+
+int flw_dpd_finish_episode(flw_dpd* e, double* reward_sum) {
+    return guarded([&] {
+        double total = 0.0;
+        for (double v : eng(e).finish_episode()) total += v;
+        if (reward_sum) *reward_sum = total;
+        return FLW_OK;
+    });
+}
+
 int flw_dpd_run_episodes(flw_dpd* e, int64_t first_episode, int64_t count, float* device_ms) {
     return guarded([&] {
         Engine& en = eng(e);

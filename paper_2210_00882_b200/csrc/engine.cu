@@ -243,14 +243,20 @@ bool Engine::grouped() const { return p2p_enabled() || (comm_ && comm_->nranks()
 // the peer-memory exchange, NCCL collectives), so its wait is bounded like the reference's
 // channel receives (local_run.cpp:543-546): past timeout_ms the group is aborted and the call
 // fails with Timeout. A unit without a group cannot block on anything: plain synchronize.
-void Engine::wait_stream(const char* what) {
+void Engine::wait_stream(const char* what) { wait_event(nullptr, what); }
+
+// (ev null: the whole stream)
+void Engine::wait_event(cudaEvent_t ev, const char* what) {
     if (!grouped()) {
-        FLW_CUDA(cudaStreamSynchronize(stream_));
+        if (ev)
+            FLW_CUDA(cudaEventSynchronize(ev));
+        else
+            FLW_CUDA(cudaStreamSynchronize(stream_));
         return;
     }
     const auto t0 = std::chrono::steady_clock::now();
     for (int spin = 0;; ++spin) {
-        const cudaError_t st = cudaStreamQuery(stream_);
+        const cudaError_t st = ev ? cudaEventQuery(ev) : cudaStreamQuery(stream_);
         if (st == cudaSuccess) break;
         if (st != cudaErrorNotReady) FLW_CUDA(st);
         if (*reinterpret_cast<volatile unsigned*>(abort_h_)) {
@@ -1714,7 +1720,6 @@ double Engine::run_episode(int64_t ep, float* device_ms) {
 
 void Engine::launch_episode(int64_t ep) {
     FLW_CUDA(cudaSetDevice(device_));
-    if (grouped()) fail(Errc::Config, "pipelined episodes serve units without a gradient group");
     if (fl_head_ - fl_tail_ >= kInFlight) fail(Errc::Config, "launch_episode: too many episodes in flight");
     if (!graph_) build_graph();
     if (!rs_pinned_) {
@@ -1735,7 +1740,7 @@ std::vector<double> Engine::finish_episode() {
     FLW_CUDA(cudaSetDevice(device_));
     if (fl_tail_ == fl_head_) fail(Errc::Config, "finish_episode: no episode in flight");
     const int slot = static_cast<int>(fl_tail_ % kInFlight);
-    FLW_CUDA(cudaEventSynchronize(ev_done_[slot]));
+    wait_event(ev_done_[slot], "finish_episode");
     ++fl_tail_;
     steps_ += T_ * nrep_;
     cur_step_ = T_;

@@ -84,7 +84,7 @@ class Engine {
     // Whole episode: Reset, T x Step, I x Learn as one captured CUDA graph. Returns the
     // episode reward sum (sum over this unit's envs, interp.cpp:257) and the device time.
     double run_episode(int64_t ep, float* device_ms = nullptr);
-    // Pipelined episodes of an ungrouped unit (flw_run_local on one GPU): launch_episode
+    // Pipelined episodes (flw_run_local on one GPU, flw_dpd_launch/finish_episode): launch_episode
     // enqueues episode ep (its index, the episode graph, an async copy of its reward sums into a
     // pinned slot); finish_episode waits for the oldest enqueued episode and returns its
     // per-replica reward sums. At most kInFlight are enqueued, so the host's per-episode gate
@@ -158,6 +158,7 @@ class Engine {
     void enq_mlp_forward(int net, const float* X, int64_t M, float* const* H, int first_layer = 0);
     void build_graph();
     void wait_stream(const char* what);
+    void wait_event(cudaEvent_t ev, const char* what);  // bounded like wait_stream (grouped units)
     unsigned* abort_h_ = nullptr;  // host-mapped group abort word (host view)
     unsigned* abort_d_ = nullptr;  // ... device view
     int64_t timeout_ms_ = 30000;

@@ -143,6 +143,29 @@ def test_phase_api_equals_graph():
         np.testing.assert_array_equal(a.params(), b.params())
 
 
+@pytest.mark.parametrize("numerics", ["exact", "fast"])
+def test_pipelined_episodes_equal_synchronous(numerics):
+    """launch_episode / finish_episode (two episodes in flight) are the same computation as
+    run_episode: identical rewards per episode and identical final params."""
+    _need_gpu()
+    from paper_2210_00882_b200 import DpdEngine
+
+    algo = CASES["ppo_synth_h64"]
+    a = DpdEngine(algo, seed=5, numerics=numerics)
+    b = DpdEngine(algo, seed=5, numerics=numerics)
+    ra = [a.run_episode(ep)[0] for ep in range(4)]
+    b.launch_episode(0)
+    rb = []
+    for ep in range(4):
+        if ep + 1 < 4:
+            b.launch_episode(ep + 1)
+        rb.append(b.finish_episode())
+    assert ra == rb
+    np.testing.assert_array_equal(a.params(), b.params())
+    with pytest.raises(Exception):
+        b.finish_episode()  # nothing in flight
+
+
 def test_run_local_summary_schema():
     _need_gpu()
     from paper_2210_00882_b200 import Program

@@ -1002,6 +1002,7 @@ void Engine::enq_learn_fast() {
     fc.loss_partials = b.loss_parts + 3 * np_loss;
     if (concurrent) {
         fast_learn(side2_, fc, gc);
+        if (split_update_ok()) enq_critic_update(side2_, gc);
         FLW_CUDA(cudaEventRecord(ev_ljoin_, side2_));
         FLW_CUDA(cudaStreamWaitEvent(stream_, ev_ljoin_, 0));
     } else {
@@ -1395,75 +1396,140 @@ void Engine::enq_permute_replicas() {
     permute_rows_f64(stream_, b.rew_d, b.prew_d, T_, E_, m);
 }
 
+FastUpdateArgs Engine::update_args() const {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    FastUpdateArgs u{};
+    u.pp = b.part_p;
+    u.pc = b.part_c;
+    u.np = b.lgrid_p;
+    u.nc = b.lgrid_c;
+    u.Pp = s.P_policy;
+    u.Pc = s.P - s.P_policy;
+    u.ctx = b.ctx;
+    u.bc_table = b.bc_table;
+    u.bc_len = b.bc_len;
+    u.params = b.params;
+    u.grads = b.grads;
+    u.m = b.m;
+    u.v = b.v;
+    u.lr = cfg_.lr;
+    u.b1 = 0.9;
+    u.b2 = 0.999;
+    u.eps = 1e-8;
+    u.pol = b.pol;
+    u.crit = b.crit;
+    u.img_p = b.wimg_p;
+    u.img_c = b.wimg_c;
+    u.counter = b.upd_counter;
+    return u;
+}
+
+P2pArgs Engine::p2p_args() const {
+    Bufs& b = *b_;
+    const ProgramShape& s = shape_;
+    const P2pLayout Lo = p2p_layout(p2p_k_, s.P);
+    P2pArgs a{};
+    a.part_p = b.part_p;
+    a.part_c = b.part_c;
+    a.np = b.lgrid_p;
+    a.nc = b.lgrid_c;
+    a.Pp = s.P_policy;
+    a.Pc = s.P - s.P_policy;
+    a.rank = p2p_rank_;
+    a.k = p2p_k_;
+    a.peers = p2p_peers_dev_;
+    a.off_inbox = Lo.off_inbox;
+    a.off_grads = Lo.off_grads;
+    a.off_sflag = Lo.off_sflag;
+    a.off_dflag = Lo.off_dflag;
+    a.ctx = b.ctx;
+    a.abort_flag = abort_d_;
+    a.params = b.params;
+    a.m = b.m;
+    a.v = b.v;
+    a.lr = cfg_.lr;
+    a.b1 = 0.9;
+    a.b2 = 0.999;
+    a.eps = 1e-8;
+    a.gscale = 1.0 / static_cast<double>(p2p_k_);
+    a.Ptot = s.P;
+    if (!cfast_) {  // the exchange's Adam also refreshes the weight images
+        a.pol = b.pol;
+        a.crit = b.crit;
+        a.img_p = b.wimg_p;
+        a.img_c = b.wimg_c;
+    }
+    return a;
+}
+
+// The critic's half of the update, enqueued on the critic learn's stream right after it (the
+// policy learn is still running on the other SMs): its partials reduced (and exchanged over
+// peer memory with k GPUs) and Adam applied to the critic parameters. The policy half follows
+// the join in enq_grad_sync_and_adam. Same arithmetic per parameter as the one-launch update.
+bool Engine::split_update_ok() const {
+    // (fuse_ok_: the update follows this learn; peer exchange only between distinct GPUs - a
+    // co-located rank's waiting exchange could hold the SMs its peer's critic learn needs)
+    return fuse_ok_ && !cfast_ && !pcompact_ && !pwide_ && nrep_ == 1 && numerics_ == Numerics::Fast &&
+           (fused_pending_ || (p2p_enabled() && p2p_fused_));
+}
+
+void Engine::enq_critic_update(cudaStream_t st, int ncrit) {
+    const ProgramShape& s = shape_;
+    split_done_ = true;
+    if (fused_pending_) {
+        FastUpdateArgs u = update_args();
+        u.pp = b_->part_c;
+        u.np = ncrit;
+        u.Pp = s.P - s.P_policy;
+        u.Pc = 0;
+        u.nc = 0;
+        u.off = s.P_policy;
+        u.critic_only = true;
+        u.advance = false;  // the policy launch (the iteration's last) advances the step counter
+        fast_reduce_adam(st, u);
+        return;
+    }
+    adam_tick(st, b_->ctx, b_->bc_table, b_->bc_len);  // once per iteration: before both halves
+    P2pArgs a = p2p_args();
+    a.part_p = b_->part_c;
+    a.np = ncrit;
+    a.Pp = s.P - s.P_policy;
+    a.Pc = 0;
+    a.nc = 0;
+    a.off = s.P_policy;
+    a.critic_only = true;
+    coll_tick(st, b_->ctx);
+    reduce_allreduce_adam(st, a, p2p_fused_);
+}
+
 void Engine::enq_grad_sync_and_adam() {
     Bufs& b = *b_;
     const ProgramShape& s = shape_;
     prev_fused_ = fused_pending_;
+    const bool split = split_done_;
+    split_done_ = false;
     if (fused_pending_) {  // partial reduction + Adam + weight images, one launch
         fused_pending_ = false;
-        FastUpdateArgs u{};
-        u.pp = b.part_p;
-        u.pc = b.part_c;
-        u.np = b.lgrid_p;
-        u.nc = b.lgrid_c;
-        u.Pp = s.P_policy;
-        u.Pc = s.P - s.P_policy;
-        u.ctx = b.ctx;
-        u.bc_table = b.bc_table;
-        u.bc_len = b.bc_len;
-        u.params = b.params;
-        u.grads = b.grads;
-        u.m = b.m;
-        u.v = b.v;
-        u.lr = cfg_.lr;
-        u.b1 = 0.9;
-        u.b2 = 0.999;
-        u.eps = 1e-8;
-        u.pol = b.pol;
-        u.crit = b.crit;
-        u.img_p = b.wimg_p;
-        u.img_c = b.wimg_c;
-        u.counter = b.upd_counter;
+        FastUpdateArgs u = update_args();
+        if (split) {  // the critic's half already ran after the critic learn
+            u.Pc = 0;
+            u.nc = 0;
+        }
         probe_begin("reduce");
         fast_reduce_adam(stream_, u);
         probe_end();
         return;
     }
-    adam_tick(stream_, b.ctx, b.bc_table, b.bc_len);
+    if (!split) adam_tick(stream_, b.ctx, b.bc_table, b.bc_len);
     if (p2p_enabled() && numerics_ == Numerics::Fast) {
         // reduce the CTA partials + all-reduce over NVLink peer memory + Adam: one kernel
-        const P2pLayout Lo = p2p_layout(p2p_k_, s.P);
-        P2pArgs a{};
-        a.part_p = b.part_p;
-        a.part_c = b.part_c;
-        a.np = b.lgrid_p;
-        a.nc = b.lgrid_c;
-        a.Pp = s.P_policy;
-        a.Pc = s.P - s.P_policy;
-        a.rank = p2p_rank_;
-        a.k = p2p_k_;
-        a.peers = p2p_peers_dev_;
-        a.off_inbox = Lo.off_inbox;
-        a.off_grads = Lo.off_grads;
-        a.off_sflag = Lo.off_sflag;
-        a.off_dflag = Lo.off_dflag;
-        a.ctx = b.ctx;
-        a.abort_flag = abort_d_;
-        a.params = b.params;
-        a.m = b.m;
-        a.v = b.v;
-        a.lr = cfg_.lr;
-        a.b1 = 0.9;
-        a.b2 = 0.999;
-        a.eps = 1e-8;
-        a.gscale = 1.0 / static_cast<double>(p2p_k_);
-        if (!cfast_) {  // the exchange's Adam also refreshes the weight images
-            a.pol = b.pol;
-            a.crit = b.crit;
-            a.img_p = b.wimg_p;
-            a.img_c = b.wimg_c;
-            prev_fused_ = true;
+        P2pArgs a = p2p_args();
+        if (split) {
+            a.Pc = 0;
+            a.nc = 0;
         }
+        if (!cfast_) prev_fused_ = true;
         coll_tick(stream_, b.ctx);
         probe_begin("exchange_adam");
         reduce_allreduce_adam(stream_, a, p2p_fused_);

@@ -19,6 +19,9 @@
 
 namespace flw {
 
+struct FastUpdateArgs;  // fast.cuh
+struct P2pArgs;         // p2p.cuh
+
 enum class Numerics : int {
     Exact = 0,  // FP64-accumulate CUDA-core path, bit-exact with the reference's per-op f32 rounding
     Fast = 1,   // tensor-core (tcgen05) path, fp32 accumulate, tolerance-checked
@@ -218,6 +221,11 @@ class Engine {
     bool fuse_ok_ = false;        // enq_grad_sync_and_adam follows the learn being enqueued
     bool fused_pending_ = false;  // the learn left its partials for k_reduce_adam
     bool prev_fused_ = false;     // the last update also refreshed the weight images
+    bool split_done_ = false;     // this iteration's critic update already ran (enq_critic_update)
+    FastUpdateArgs update_args() const;
+    P2pArgs p2p_args() const;
+    bool split_update_ok() const;
+    void enq_critic_update(cudaStream_t st, int ncrit);
     std::vector<Probe> probes_;
     int open_probe_ = -1;
     void probe_begin(const char* tag);

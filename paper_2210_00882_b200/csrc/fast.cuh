@@ -108,6 +108,13 @@ struct FastUpdateArgs {      // k_reduce_adam: partial reduction + Adam + weight
     FastNet pol, crit;
     __nv_bfloat16 *img_p, *img_c;
     unsigned* counter;       // zero between launches
+    // split update (the critic's update runs as soon as the critic learn finishes, while the
+    // policy learn still runs): a launch over one net only - off = its first flat parameter,
+    // critic_only = the rows are critic parameters; advance = this launch advances the Adam
+    // step counter (the iteration's last launch)
+    int64_t off = 0;
+    bool critic_only = false;
+    bool advance = true;
 };
 void fast_reduce_adam(cudaStream_t s, const FastUpdateArgs& a);
 void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int np, int nc, int64_t Pp,

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) k_reduce_adam(FastUpdateArgs a, int nchun
             const int ln = threadIdx.x >> 2, j = threadIdx.x & 3;
             const int64_t ipad = c * 128LL + threadIdx.x;
             const bool inpol = ipad < Pps;
-            const int64_t i = inpol ? ipad : a.Pp + (ipad - Pps);  // flat parameter index
+            const int64_t i = a.off + (inpol ? ipad : a.Pp + (ipad - Pps));  // flat parameter index
             if (inpol ? ipad < a.Pp : (ipad - Pps < a.Pc && ipad < Pps + Pcs)) {
                 float gsum = 0.0f;
 #pragma unroll
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) k_reduce_adam(FastUpdateArgs a, int nchun
                     static_cast<double>(a.params[i]), __ddiv_rn(__dmul_rn(a.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), a.eps))));
                 a.params[i] = next;
                 // weight-image entry (biases are read from params by the learn kernels)
-                const bool ip = i < a.Pp;
+                const bool ip = !a.critic_only && i < a.Pp;
                 const int64_t e = wimg_elem(ip ? a.pol : a.crit, i);
                 if (e >= 0) (ip ? a.img_p : a.img_c)[e] = __float2bfloat16(next);
             }
@@ -169,9 +169,11 @@ __global__ void __launch_bounds__(256) k_reduce_adam(FastUpdateArgs a, int nchun
     }
     __syncthreads();
     if (last && threadIdx.x == 0) {
-        a.ctx->adam_t = t;
-        a.ctx->bc1 = bc1;
-        a.ctx->bc2 = bc2;
+        if (a.advance) {
+            a.ctx->adam_t = t;
+            a.ctx->bc1 = bc1;
+            a.ctx->bc2 = bc2;
+        }
         *a.counter = 0u;
     }
 }

@@ -18,7 +18,7 @@
 // same chunk from the other ranks) when every peer is another GPU, else k_reduce_push +
 // k_sum_adam (the first never waits, so co-located ranks cannot fill a device with waiting
 // blocks). Region layout (identical on every rank, one cudaMalloc, CUDA-IPC exported for one-
-// process-per-GPU runs): inbox u32x2 [2][k][P] | grads f32 [P] (unused) | flag u64 (unused).
+// process-per-GPU runs): inbox u32x2 [2][k][Ptot] | grads f32 [P] (unused) | flag u64 (unused).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -87,8 +87,10 @@ __device__ __forceinline__ void reduce_push_chunk(const P2pArgs& a, int c, uint6
             for (int k = 0; k < 8; ++k) t += reinterpret_cast<const float*>(&ws[k][threadIdx.x >> 2])[threadIdx.x & 3];
             for (int r = 0; r < a.k; ++r) {
                 // inbox[epoch & 1]: rank r may still be reading the previous exchange's buffer
-                uint2* inbox = reinterpret_cast<uint2*>(a.peers[r] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
-                st_tagged(inbox + static_cast<int64_t>(a.rank) * P + i, t, static_cast<uint32_t>(epoch));
+                // (the inbox is laid out over ALL parameters: a launch over one net writes its
+                // own columns [off, off + P), never another launch's)
+                uint2* inbox = reinterpret_cast<uint2*>(a.peers[r] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * a.Ptot;
+                st_tagged(inbox + static_cast<int64_t>(a.rank) * a.Ptot + a.off + i, t, static_cast<uint32_t>(epoch));
             }
         }
     }
@@ -103,15 +105,15 @@ __device__ __forceinline__ bool wait_chunk(const P2pArgs& a, int c, uint64_t epo
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         const int64_t P = a.Pp + a.Pc;
-        const uint2* inbox =
-            reinterpret_cast<const uint2*>(a.peers[a.rank] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
+        const uint2* inbox = reinterpret_cast<const uint2*>(a.peers[a.rank] + a.off_inbox) +
+                             static_cast<int64_t>(epoch & 1) * a.k * a.Ptot + a.off;
         const uint32_t tag = static_cast<uint32_t>(epoch);
         int pos = 0;  // next (rank, word) of this lane to check: rank = pos / 4, word = lane + 32 (pos % 4)
         int ab = 0;
         for (uint32_t round = 1;; ++round) {
             for (; pos < 4 * a.k; ++pos) {
                 const int64_t i = pad_to_flat(a, 128LL * c + lane + 32 * (pos & 3));
-                if (i >= 0 && ld_tagged(inbox + static_cast<int64_t>(pos >> 2) * P + i).y != tag) break;
+                if (i >= 0 && ld_tagged(inbox + static_cast<int64_t>(pos >> 2) * a.Ptot + i).y != tag) break;
             }
             if (__all_sync(0xffffffffu, pos == 4 * a.k)) break;
             if ((round & 63u) == 0) {
@@ -131,12 +133,13 @@ __device__ __forceinline__ bool wait_chunk(const P2pArgs& a, int c, uint64_t epo
 // (adam_step, mlp.cpp:146-161; 1/k folded into the step).
 __device__ __forceinline__ void sum_adam_chunk(const P2pArgs& a, int c, uint64_t epoch) {
     const int64_t P = a.Pp + a.Pc;
-    const int64_t i = threadIdx.x < 128 ? pad_to_flat(a, 128LL * c + threadIdx.x) : -1;
-    if (i < 0) return;
-    const uint2* inbox =
-        reinterpret_cast<const uint2*>(a.peers[a.rank] + a.off_inbox) + static_cast<int64_t>(epoch & 1) * a.k * P;
+    const int64_t il = threadIdx.x < 128 ? pad_to_flat(a, 128LL * c + threadIdx.x) : -1;  // this launch's index
+    if (il < 0) return;
+    const int64_t i = a.off + il;  // flat parameter index
+    const uint2* inbox = reinterpret_cast<const uint2*>(a.peers[a.rank] + a.off_inbox) +
+                         static_cast<int64_t>(epoch & 1) * a.k * a.Ptot + a.off;
     float gs = 0.0f;
-    for (int r = 0; r < a.k; ++r) gs += __uint_as_float(ld_tagged(inbox + static_cast<int64_t>(r) * P + i).x);
+    for (int r = 0; r < a.k; ++r) gs += __uint_as_float(ld_tagged(inbox + static_cast<int64_t>(r) * a.Ptot + il).x);
     const double g = __dmul_rn(static_cast<double>(gs), a.gscale);
     const double bc1 = a.ctx->bc1, bc2 = a.ctx->bc2;
     const double mi = __dadd_rn(__dmul_rn(a.b1, a.m[i]), __dmul_rn(__dsub_rn(1.0, a.b1), g));
@@ -148,7 +151,7 @@ __device__ __forceinline__ void sum_adam_chunk(const P2pArgs& a, int c, uint64_t
                                   __ddiv_rn(__dmul_rn(a.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), a.eps)));
     a.params[i] = static_cast<float>(next);
     if (a.img_p) {  // weight-image entry for the next train iteration's learn kernels
-        const bool pol = i < a.Pp;
+        const bool pol = !a.critic_only && il < a.Pp;
         const int64_t e = wimg_elem(pol ? a.pol : a.crit, i);
         if (e >= 0) (pol ? a.img_p : a.img_c)[e] = __float2bfloat16(static_cast<float>(next));
     }

@@ -316,6 +316,7 @@ void microbench(const std::string& which, int64_t n, int iters, double* ms, doub
             a.b2 = 0.999;
             a.eps = 1e-8;
             a.gscale = 1.0;
+            a.Ptot = n;
             *ms = time_launches([&] {
                 coll_tick(0, ctx);
                 reduce_allreduce_adam(0, a, true);  // k = 1: waits on its own push only

@@ -35,6 +35,10 @@ struct P2pArgs {
     // optional: also refresh the bf16 weight-tile images (null: the next learn rebuilds them)
     FastNet pol, crit;
     __nv_bfloat16 *img_p, *img_c;
+    // one net only (see FastUpdateArgs): flat offset of its first parameter, critic rows;
+    // Ptot = all parameters (the inbox layout, identical for every launch)
+    int64_t off = 0, Ptot = 0;
+    bool critic_only = false;
 };
 
 void coll_tick(cudaStream_t s, DeviceCtx* ctx);  // ++ctx->coll_seq (one per exchange)

@@ -2,27 +2,28 @@
 // per 128-row tile on the 5th-gen tensor cores (forward -> loss -> backward -> dW in TMEM).
 //
 // Every stage of a tile is a dependency chain (MMA -> TMEM load -> activation -> shared store ->
-// next MMA), so a single tile per SM leaves the tensor pipe idle most of the time. Here each CTA
-// (one per SM) runs TWO tiles at once, ping-ponging on the tensor core:
+// proxy fence -> hand-off -> next MMA), so one tile per SM leaves the tensor pipe idle most of
+// the time. Each CTA (one per SM, persistent over its tiles) keeps several tiles in flight:
 //
-//   warps 0-3  epilogue group 0   (tile rows = TMEM lanes, one full row per thread)
-//   warps 4-7  epilogue group 1
-//   warp  8    producer: lane 0 issues every tcgen05.mma / commit and every TMA bulk copy, in a
-//              FIXED alternating order (group 0 job j, group 1 job j, ...), so the dW
-//              accumulation order - and therefore the result - is deterministic.
-//   (current layout: 4 epilogue warps per group x kGroups, then producer 0 (even groups),
-//    the loader warp, producer 1 (odd groups); the shared dW accumulators take their MMA
-//    batches in the single-producer order through the per-layer dwtok token)
+//   warps [4g, 4g + 4)   epilogue group g (g < kGroups: 3 in the learn modes, 4 in the values
+//                        pass): tile rows = TMEM lanes, one full row per thread
+//   warp 4 kGroups       MMA producer 0 (even groups)   - one elected lane issues each
+//   warp 4 kGroups + 1   loader (every TMA bulk copy: the forward's activation-tile stores,
+//                        the backward's reloads)
+//   warp 4 kGroups + 2   MMA producer 1 (odd groups)
+//   warp 4 kGroups + 3   idle (learn modes: completes the warpgroup for setmaxnreg, which moves
+//                        registers from these warps to the epilogue warps)
 //
-// Shared memory holds, per group, the input tile, a 2-slot ring for hidden activations and a
-// 2-slot dZ ring; the forward streams every hidden tile H_l out to global scratch (L2-resident,
-// cp.async.bulk) and the backward streams H_{l-1} back in one stage ahead, so two tiles fit in
-// the 227 KB of one SM. The critic learn pass skips its forward entirely: its activations were
-// saved by the values pass (same parameters) and are streamed from there.
+// Shared memory holds the bf16 weight image, per group a 2-slot activation ring (slot 1 also
+// holds the input tile X) and one dZ slot, the bias rows and per-warp bias-gradient
+// accumulators. The forward streams every hidden tile not kept resident out to global scratch
+// and the backward streams it back one stage ahead. The critic learn pass skips its forward:
+// its activations were saved by the values pass (same parameters) and are streamed from there.
 //
 // TMEM (512 columns): Z/dH accumulator of group g at columns [64g, 64g+64) (M=128); dW_l
-// accumulators (M=64, half-sub-partition layout) for the layer pair (2j, 2j+1) at columns
-// [128+64j, 192+64j), lane offsets 0 / 16 - shared by both groups, accumulated across all tiles.
+// accumulators (M=64, half-sub-partition layout) of the layer pair (2j, 2j+1) after them, lane
+// offsets 0 / 16 - shared by the groups and both producers, accumulated across all tiles in the
+// single-issuer order (tile round, group) through the per-layer token dwtok: deterministic.
 //
 // Stage protocol per group: the producer waits epi_done[g] (all 4 epilogue warps stored their
 // operand tile and fenced it to the async proxy), issues the stage's MMAs and commits to

@@ -224,7 +224,7 @@ def hbm_microbenchmarks(peaks: dict) -> dict:
       gae_streams   k_fast_gae<8,4> (the GAE kernel for T != 32), 2^26 rows, 17 B/row
       reduce_adam   k_reduce_adam (the fused per-iteration update, 1 GPU), 2^26 params, 8 partial slots:
                     44 B/param (Adam, f64 moments) + 4 B/param per slot
-      exchange_adam k_reduce_push + k_sum_adam (the k-GPU peer-memory update, k = 1), same
+      exchange_adam k_exchange_adam (the k-GPU peer-memory update, k = 1), same
     In the C2 fast episode the env step is fused into k_rollout_episode (MMA-latency bound: see
     kernel_shares / rollout_only)."""
     from paper_2210_00882_b200.api import microbench

@@ -11,7 +11,7 @@
 //   reduce_adam : k_reduce_adam (the fused per-iteration update: partial reduction + Adam with f64
 //                 moments) over P params and 8 partial slots: 44 B/param (g in, p, m, v in/out) + 4 B
 //                 per partial slot
-//   exchange_adam: k_reduce_push + k_sum_adam (the k-GPU peer-memory update) with k = 1: same bytes
+//   exchange_adam: k_exchange_adam (the k-GPU peer-memory update) with k = 1: same bytes
 //   env_step / adam: the standalone microbenchmark kernels of round 1 (kept for comparison)
 // Each launch is timed with CUDA events on the launching stream, after warm-up.
 #include <cuda_runtime.h>

@@ -200,6 +200,8 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     FLW_CUDA(cudaStreamCreateWithFlags(&side2_, cudaStreamNonBlocking));
     FLW_CUDA(cudaEventCreateWithFlags(&ev_lfork_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreateWithFlags(&ev_ljoin_, cudaEventDisableTiming));
+    FLW_CUDA(cudaEventCreateWithFlags(&ev_plearn_, cudaEventDisableTiming));
+    FLW_CUDA(cudaEventCreateWithFlags(&ev_gae_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreate(&ev_t0_));
@@ -221,7 +223,7 @@ Engine::~Engine() {
     for (void* q : p2p_ipc_opened_) cudaIpcCloseMemHandle(q);
     if (p2p_region_ptr_) cudaFree(p2p_region_ptr_);
     b_.reset();
-    for (cudaEvent_t e : {ev_fork_, ev_join_, ev_t0_, ev_t1_, ev_lfork_, ev_ljoin_})
+    for (cudaEvent_t e : {ev_fork_, ev_join_, ev_t0_, ev_t1_, ev_lfork_, ev_ljoin_, ev_plearn_, ev_gae_})
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_done_)
         if (e) cudaEventDestroy(e);
@@ -910,17 +912,25 @@ void Engine::enq_learn_fast() {
     const int lgrid = b.grid2;
     auto launch = [&](int grid) { fast_learn(stream_, f, grid); };
     f.hscratch = b.hscratch;
-    probe_begin("critic_fwd");
     const int64_t grp = fast_values_groups();
-    launch(static_cast<int>(std::min<int64_t>(lgrid, ((f.rows + 127) / 128 + grp - 1) / grp)));
-    probe_end();
+    const int vgrid = static_cast<int>(std::min<int64_t>(lgrid, ((f.rows + 127) / 128 + grp - 1) / grp));
+    const FastLearnArgs fv = f;  // the values pass (kept for the next iteration's, see below)
+    if (vg_ready_) {
+        // the previous iteration enqueued this one's values pass + GAE on side2_ (pipelined)
+        vg_ready_ = false;
+        FLW_CUDA(cudaStreamWaitEvent(stream_, ev_gae_, 0));
+    } else {
+        probe_begin("critic_fwd");
+        launch(vgrid);
+        probe_end();
+        probe_begin("gae");
+        fast_gae(stream_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
+                 b.block_sums, b.stats, b.gae_counter);
+        if (nrep_ > 1 && ppo && cfg_.normalize_adv)  // each folded unit normalises over its own rows
+            fast_rep_adv_stats(stream_, b.adv, T_, E_, b.rep_off, b.rep_n, nrep_, b.stats);
+        probe_end();
+    }
     f.split_rows = -1;
-    probe_begin("gae");
-    fast_gae(stream_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
-             b.block_sums, b.stats, b.gae_counter);
-    if (nrep_ > 1 && ppo && cfg_.normalize_adv)  // each folded unit normalises over its own rows
-        fast_rep_adv_stats(stream_, b.adv, T_, E_, b.rep_off, b.rep_n, nrep_, b.stats);
-    probe_end();
     // learn: policy then critic, each a persistent fused kernel
     f.mode = 1;
     f.X = b.states;
@@ -986,6 +996,7 @@ void Engine::enq_learn_fast() {
         launch(gp);
         probe_end();
     }
+    if (concurrent) FLW_CUDA(cudaEventRecord(ev_plearn_, stream_));  // the policy learn read adv
     FastLearnArgs fc = f;
     fc.X = Xc;
     fc.in_cols = Cin;
@@ -1005,6 +1016,18 @@ void Engine::enq_learn_fast() {
         if (split_update_ok()) enq_critic_update(side2_, gc);
         FLW_CUDA(cudaEventRecord(ev_ljoin_, side2_));
         FLW_CUDA(cudaStreamWaitEvent(stream_, ev_ljoin_, 0));
+        // Train-iteration pipelining: the next iteration's values pass needs only the updated
+        // critic, so it starts here on the critic's stream - on the SMs the critic learn freed -
+        // while the policy learn and the policy update still run; its GAE waits for the policy
+        // learn (which reads adv). PPO only (an A3C policy reads the values).
+        if (pipe_next_ok_ && split_done_ && ppo && nrep_ == 1 && !eager_coll_ && hreuse) {
+            fast_learn(side2_, fv, vgrid);
+            FLW_CUDA(cudaStreamWaitEvent(side2_, ev_plearn_, 0));
+            fast_gae(side2_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
+                     b.block_sums, b.stats, b.gae_counter);
+            FLW_CUDA(cudaEventRecord(ev_gae_, side2_));
+            vg_ready_ = true;
+        }
     } else {
         probe_begin("learn_critic");
         fast_learn(stream_, fc, gc);
@@ -1673,7 +1696,9 @@ void Engine::build_graph() {
         if (numerics_ == Numerics::Exact) probe_begin("learn_grads");
         learn_iter_ = k;
         fuse_ok_ = true;  // the update follows right away
+        pipe_next_ok_ = k + 1 < shape_.learn_iters;
         enq_learn_grads();
+        pipe_next_ok_ = false;
         fuse_ok_ = false;
         trace_capture("learn_grads");
         if (numerics_ == Numerics::Exact) probe_end();

@@ -222,6 +222,10 @@ class Engine {
     bool fused_pending_ = false;  // the learn left its partials for k_reduce_adam
     bool prev_fused_ = false;     // the last update also refreshed the weight images
     bool split_done_ = false;     // this iteration's critic update already ran (enq_critic_update)
+    // Train-iteration pipelining (graph build only): another iteration follows this one, and
+    // the next iteration's values pass + GAE are already enqueued on side2_ (ev_gae_)
+    bool pipe_next_ok_ = false, vg_ready_ = false;
+    cudaEvent_t ev_plearn_ = nullptr, ev_gae_ = nullptr;
     FastUpdateArgs update_args() const;
     P2pArgs p2p_args() const;
     bool split_update_ok() const;

@@ -1522,6 +1522,7 @@ void Engine::enq_critic_update(cudaStream_t st, int ncrit) {
     a.nc = 0;
     a.off = s.P_policy;
     a.critic_only = true;
+    a.flag0 = static_cast<int>(((s.P_policy + 3) / 4 * 4 + 127) / 128);  // after the policy launch's hint rows
     coll_tick(st, b_->ctx);
     reduce_allreduce_adam(st, a, p2p_fused_);
 }

@@ -36,6 +36,15 @@ __device__ __forceinline__ void st_tagged(uint2* p, float v, uint32_t epoch) {
                  : "memory");
 }
 
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint2 ld_tagged(const uint2* p) {
     uint2 v;
     asm volatile("ld.relaxed.sys.global.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
@@ -94,6 +103,14 @@ __device__ __forceinline__ void reduce_push_chunk(const P2pArgs& a, int c, uint6
             }
         }
     }
+    // a per-(chunk, rank) hint word after the chunk's data: the readers poll this one word
+    // instead of the chunk's 128 x k tagged words (which they still check afterwards - the
+    // hint carries no ordering, so no fence is needed here)
+    __syncthreads();
+    if (threadIdx.x < a.k)
+        st_relaxed_u64(reinterpret_cast<uint64_t*>(a.peers[threadIdx.x] + a.off_sflag) +
+                           (static_cast<int64_t>(a.flag0) + c) * a.k + a.rank,
+                       epoch);
 }
 
 // Wait (the whole block) until the k ranks' copies of chunk c carry this exchange's epoch tag.
@@ -108,9 +125,25 @@ __device__ __forceinline__ bool wait_chunk(const P2pArgs& a, int c, uint64_t epo
         const uint2* inbox = reinterpret_cast<const uint2*>(a.peers[a.rank] + a.off_inbox) +
                              static_cast<int64_t>(epoch & 1) * a.k * a.Ptot + a.off;
         const uint32_t tag = static_cast<uint32_t>(epoch);
-        int pos = 0;  // next (rank, word) of this lane to check: rank = pos / 4, word = lane + 32 (pos % 4)
         int ab = 0;
+        // phase 1: the k hint words of this chunk (lane r: rank r), with a growing back-off -
+        // a long wait must not flood this GPU's L2 (the peers' NVLink stores land there)
+        const uint64_t* hint = reinterpret_cast<const uint64_t*>(a.peers[a.rank] + a.off_sflag) +
+                               (static_cast<int64_t>(a.flag0) + c) * a.k;
+        uint32_t ns = 32;
         for (uint32_t round = 1;; ++round) {
+            const bool here = lane >= a.k || ld_relaxed_u64(hint + lane) >= epoch;
+            if (__all_sync(0xffffffffu, here)) break;
+            if ((round & 255u) == 0) {
+                ab = __shfl_sync(0xffffffffu, lane == 0 ? static_cast<int>(*a.abort_flag) : 0, 0);
+                if (ab) break;
+            }
+            __nanosleep(ns);
+            ns = ns < 1024u ? 2u * ns : 1024u;
+        }
+        // phase 2: every word of the chunk carries the epoch's tag (normally already true)
+        int pos = 0;  // next (rank, word) of this lane to check: rank = pos / 4, word = lane + 32 (pos % 4)
+        for (uint32_t round = 1; !ab; ++round) {
             for (; pos < 4 * a.k; ++pos) {
                 const int64_t i = pad_to_flat(a, 128LL * c + lane + 32 * (pos & 3));
                 if (i >= 0 && ld_tagged(inbox + static_cast<int64_t>(pos >> 2) * a.Ptot + i).y != tag) break;

@@ -38,6 +38,7 @@ struct P2pArgs {
     // one net only (see FastUpdateArgs): flat offset of its first parameter, critic rows;
     // Ptot = all parameters (the inbox layout, identical for every launch)
     int64_t off = 0, Ptot = 0;
+    int flag0 = 0;  // first hint-word row of this launch's chunks (launches of one net: disjoint rows)
     bool critic_only = false;
 };
 

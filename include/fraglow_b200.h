@@ -97,6 +97,8 @@ int flw_dpd_comm_init(flw_dpd* e, const char* id, int64_t id_len, int rank, int 
  * (reduce of the per-CTA partials + all-reduce + Adam in one kernel). Every rank exports the
  * CUDA IPC handle (64 bytes) of its exchange region, the caller gathers the k handles in rank
  * order and every rank imports them. */
+/* exchange handle: the region's CUDA IPC handle + the exporting GPU's UUID */
+#define FLW_P2P_HANDLE_BYTES 80
 int flw_dpd_p2p_export(flw_dpd* e, int nranks, char* out_handle, int64_t cap);
 int flw_dpd_p2p_import(flw_dpd* e, const char* handles, int64_t len, int rank, int nranks);
 /* Back to the NCCL exchange (every rank of the group must make the same choice). */

@@ -112,8 +112,8 @@ class DpdEngine:
 
     def p2p_export(self, nranks: int) -> bytes:
         """CUDA IPC handle of this unit's peer-memory exchange region (fast numerics)."""
-        buf = C.create_string_buffer(64)
-        N.check(N.lib().flw_dpd_p2p_export(self._h, nranks, buf, 64))
+        buf = C.create_string_buffer(80)  # FLW_P2P_HANDLE_BYTES: IPC handle + GPU UUID
+        N.check(N.lib().flw_dpd_p2p_export(self._h, nranks, buf, 80))
         return buf.raw
 
     def p2p_import(self, handles: list, rank: int):

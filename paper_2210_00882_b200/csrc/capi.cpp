@@ -216,7 +216,7 @@ void run_local(flw_program& p, const flw_run_options* opts, std::vector<EpisodeM
                             else
                                 FLW_CUDA(err);
                         }
-                    p.engines[g]->set_p2p_peers(g, ng, regions);
+                    p.engines[g]->set_p2p_peers(g, ng, regions, true);  // one engine per GPU
                 }
             }
         }
@@ -441,15 +441,27 @@ int flw_dpd_comm_unique_id(char* out_id, int64_t cap) {
     });
 }
 
+// The exported handle: the region's CUDA IPC handle followed by the exporting GPU's UUID (so an
+// importer can tell co-located ranks from ranks on other GPUs).
+constexpr int64_t kP2pHandleBytes = static_cast<int64_t>(sizeof(cudaIpcMemHandle_t)) + 16;
+static_assert(kP2pHandleBytes == FLW_P2P_HANDLE_BYTES, "fraglow_b200.h FLW_P2P_HANDLE_BYTES");
+
+static void device_uuid(int dev, char* out16) {
+    cudaDeviceProp pr{};
+    FLW_CUDA(cudaGetDeviceProperties(&pr, dev));
+    std::memcpy(out16, &pr.uuid, 16);
+}
+
 int flw_dpd_p2p_export(flw_dpd* e, int nranks, char* out_handle, int64_t cap) {
     return guarded([&] {
         Engine& en = eng(e);
-        if (cap < static_cast<int64_t>(sizeof(cudaIpcMemHandle_t))) fail(Errc::Config, "handle buffer too small");
+        if (cap < kP2pHandleBytes) fail(Errc::Config, "handle buffer too small (FLW_P2P_HANDLE_BYTES)");
         en.alloc_p2p_region(nranks);
         FLW_CUDA(cudaSetDevice(en.device()));
         cudaIpcMemHandle_t h;
         FLW_CUDA(cudaIpcGetMemHandle(&h, en.p2p_region()));
         std::memcpy(out_handle, &h, sizeof(h));
+        device_uuid(en.device(), out_handle + sizeof(h));
         return FLW_OK;
     });
 }
@@ -457,16 +469,20 @@ int flw_dpd_p2p_export(flw_dpd* e, int nranks, char* out_handle, int64_t cap) {
 int flw_dpd_p2p_import(flw_dpd* e, const char* handles, int64_t len, int rank, int nranks) {
     return guarded([&] {
         Engine& en = eng(e);
-        const int64_t hb = static_cast<int64_t>(sizeof(cudaIpcMemHandle_t));
-        if (len != hb * nranks) fail(Errc::Config, "expected nranks IPC handles");
+        const int64_t hb = kP2pHandleBytes;
+        if (len != hb * nranks) fail(Errc::Config, "expected nranks exchange handles (FLW_P2P_HANDLE_BYTES each)");
         en.alloc_p2p_region(nranks);
         FLW_CUDA(cudaSetDevice(en.device()));
+        char mine[16];
+        device_uuid(en.device(), mine);
+        bool elsewhere = true;
         std::vector<void*> regions(static_cast<size_t>(nranks), nullptr);
         for (int r = 0; r < nranks; ++r) {
             if (r == rank) {
                 regions[static_cast<size_t>(r)] = en.p2p_region();
                 continue;
             }
+            if (std::memcmp(handles + hb * r + sizeof(cudaIpcMemHandle_t), mine, 16) == 0) elsewhere = false;
             cudaIpcMemHandle_t h;
             std::memcpy(&h, handles + hb * r, sizeof(h));
             void* ptr = nullptr;
@@ -474,7 +490,7 @@ int flw_dpd_p2p_import(flw_dpd* e, const char* handles, int64_t len, int rank, i
             en.adopt_ipc_mapping(ptr);
             regions[static_cast<size_t>(r)] = ptr;
         }
-        en.set_p2p_peers(rank, nranks, regions);
+        en.set_p2p_peers(rank, nranks, regions, elsewhere);
         return FLW_OK;
     });
 }

@@ -300,7 +300,7 @@ void* Engine::p2p_region() {
     return p2p_region_ptr_;
 }
 
-void Engine::set_p2p_peers(int rank, int k, const std::vector<void*>& regions) {
+void Engine::set_p2p_peers(int rank, int k, const std::vector<void*>& regions, bool peers_elsewhere) {
     FLW_CUDA(cudaSetDevice(device_));
     if (static_cast<int>(regions.size()) != k || rank < 0 || rank >= k) fail(Errc::Config, "bad p2p group");
     destroy_graph();
@@ -312,15 +312,7 @@ void Engine::set_p2p_peers(int rank, int k, const std::vector<void*>& regions) {
     // the fused exchange kernel's blocks wait for the other ranks' blocks: only safe when no two
     // ranks share a GPU (FLW_P2P_FUSED=0 forces the two-kernel form, A/B)
     static const char* fz = std::getenv("FLW_P2P_FUSED");
-    p2p_fused_ = !(fz && fz[0] == '0');
-    for (int r = 0; r < k && p2p_fused_; ++r) {
-        if (r == rank) continue;
-        cudaPointerAttributes at{};
-        if (cudaPointerGetAttributes(&at, regions[static_cast<size_t>(r)]) != cudaSuccess || at.device == device_) {
-            cudaGetLastError();
-            p2p_fused_ = false;
-        }
-    }
+    p2p_fused_ = peers_elsewhere && !(fz && fz[0] == '0');
 }
 
 void Engine::alloc_p2p_region(int k) {

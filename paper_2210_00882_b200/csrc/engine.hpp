@@ -60,7 +60,9 @@ class Engine {
     int64_t p2p_region_bytes() const;
     void alloc_p2p_region(int k);  // before p2p_region(): the layout depends on k
     void adopt_ipc_mapping(void* p) { p2p_ipc_opened_.push_back(p); }  // closed by the destructor
-    void set_p2p_peers(int rank, int k, const std::vector<void*>& regions);
+    // peers_elsewhere: every other rank's region lives on another GPU (the one-kernel exchange
+    // and the split update are then allowed; co-located ranks use the two-kernel form)
+    void set_p2p_peers(int rank, int k, const std::vector<void*>& regions, bool peers_elsewhere);
     bool p2p_enabled() const { return p2p_k_ > 1; }
     bool p2p_capable() const { return numerics_ == Numerics::Fast && nrep_ == 1 && !cfast_ && !wide_; }
     void disable_p2p() {  // back to the NCCL exchange (the group must agree; see bench.py)

@@ -1806,12 +1806,16 @@ void Engine::launch_episode(int64_t ep) {
     FLW_CUDA(cudaSetDevice(device_));
     if (fl_head_ - fl_tail_ >= kInFlight) fail(Errc::Config, "launch_episode: too many episodes in flight");
     if (!graph_) build_graph();
-    if (!rs_pinned_) {
-        FLW_CUDA(cudaMallocHost(&rs_pinned_, sizeof(double) * static_cast<size_t>(kInFlight * nrep_)));
+    if (!rs_pinned_) {  // [kInFlight][nrep_] reward sums, then [kInFlight] episode indices
+        FLW_CUDA(cudaMallocHost(&rs_pinned_, sizeof(double) * static_cast<size_t>(kInFlight * (nrep_ + 1))));
         for (cudaEvent_t& e : ev_done_) FLW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     const int slot = static_cast<int>(fl_head_ % kInFlight);
-    FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, &ep, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+    // the episode index from a pinned slot: a truly asynchronous copy (the slot is reused only
+    // after finish_episode has waited for this episode)
+    int64_t* ep_pinned = reinterpret_cast<int64_t*>(rs_pinned_ + static_cast<size_t>(kInFlight) * nrep_) + slot;
+    *ep_pinned = ep;
+    FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, ep_pinned, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
     launch_graph();
     const int n = numerics_ == Numerics::Exact ? nrep_ : 1;  // (fast: the total in slot 0)
     FLW_CUDA(cudaMemcpyAsync(rs_pinned_ + static_cast<size_t>(slot) * nrep_, b_->rsum, sizeof(double) * n,

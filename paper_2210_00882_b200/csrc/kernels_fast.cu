@@ -16,6 +16,7 @@
 // dW accumulators (M=64, "half sub-partition" layout) share columns [64+64j, 128+64j) at
 // lane offsets 0 and 16.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <algorithm>
 
@@ -23,6 +24,7 @@
 #include "engine.hpp"
 #include "fast.cuh"
 #include "umma.cuh"
+#include "update.cuh"
 
 namespace flw {
 
@@ -105,77 +107,13 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
 // build launch. The Adam step counter and its bias corrections (as k_adam_tick) are advanced by
 // the last block to finish (every block has read the old counter by then).
 __global__ void __launch_bounds__(256) k_reduce_adam(FastUpdateArgs a, int nchunks) {
-    // 128 parameters per chunk (grid-stride): lane -> 4 consecutive parameters (float4 rows, 512 B
-    // per warp load); warp w sums partials w, w+8, ... in order, then the 8 warp sums are added in
-    // warp order (the k_reduce_partials tree, per parameter); Adam then runs one parameter per thread
     __shared__ float4 ws[8][32];
-    __shared__ bool last;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // padded index space: [policy rows padded to Pps][critic rows padded to Pcs], so a lane's
-    // float4 never straddles the two nets
-    const int64_t Pps = (a.Pp + 3) / 4 * 4, Pcs = (a.Pc + 3) / 4 * 4;
-    const int64_t t = a.ctx->adam_t + 1;
-    const double bc1 = t <= a.bc_len ? a.bc_table[t - 1].x : 1.0 - pow(0.9, static_cast<double>(t));
-    const double bc2 = t <= a.bc_len ? a.bc_table[t - 1].y : 1.0 - pow(0.999, static_cast<double>(t));
-    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const int64_t q0 = c * 128LL + 4 * lane;  // first of this lane's 4 padded indices
-        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (q0 < Pps + Pcs) {
-            const bool pol = q0 < Pps;
-            const float* base = pol ? a.pp + q0 : a.pc + (q0 - Pps);
-            const int64_t stride = pol ? Pps : Pcs;
-            const int nparts = pol ? a.np : a.nc;
-#pragma unroll 4
-            for (int p = w; p < nparts; p += 8) {
-                const float4 v = *reinterpret_cast<const float4*>(base + p * stride);
-                s4.x += v.x;
-                s4.y += v.y;
-                s4.z += v.z;
-                s4.w += v.w;
-            }
-        }
-        ws[w][lane] = s4;
-        __syncthreads();
-        if (threadIdx.x < 128) {
-            const int ln = threadIdx.x >> 2, j = threadIdx.x & 3;
-            const int64_t ipad = c * 128LL + threadIdx.x;
-            const bool inpol = ipad < Pps;
-            const int64_t i = a.off + (inpol ? ipad : a.Pp + (ipad - Pps));  // flat parameter index
-            if (inpol ? ipad < a.Pp : (ipad - Pps < a.Pc && ipad < Pps + Pcs)) {
-                float gsum = 0.0f;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) gsum += reinterpret_cast<const float*>(&ws[k][ln])[j];
-                a.grads[i] = gsum;
-                const double g = static_cast<double>(gsum);
-                const double mi = __dadd_rn(__dmul_rn(a.b1, a.m[i]), __dmul_rn(__dsub_rn(1.0, a.b1), g));
-                const double vi = __dadd_rn(__dmul_rn(a.b2, a.v[i]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, a.b2), g), g));
-                a.m[i] = mi;
-                a.v[i] = vi;
-                const double mhat = __ddiv_rn(mi, bc1), vhat = __ddiv_rn(vi, bc2);
-                const float next = static_cast<float>(__dsub_rn(
-                    static_cast<double>(a.params[i]), __ddiv_rn(__dmul_rn(a.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), a.eps))));
-                a.params[i] = next;
-                // weight-image entry (biases are read from params by the learn kernels)
-                const bool ip = !a.critic_only && i < a.Pp;
-                const int64_t e = wimg_elem(ip ? a.pol : a.crit, i);
-                if (e >= 0) (ip ? a.img_p : a.img_c)[e] = __float2bfloat16(next);
-            }
-        }
-        __syncthreads();  // ws is rewritten by the next chunk
-    }
-    if (threadIdx.x == 0) {
-        __threadfence();
-        last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (last && threadIdx.x == 0) {
-        if (a.advance) {
-            a.ctx->adam_t = t;
-            a.ctx->bc1 = bc1;
-            a.ctx->bc2 = bc2;
-        }
-        *a.counter = 0u;
-    }
+    int64_t t;
+    double bc1, bc2;
+    adam_step_consts(a, t, bc1, bc2);
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x)
+        update_chunk(a, c, threadIdx.x, ws, bc1, bc2, [] { __syncthreads(); });
+    if (threadIdx.x == 0) update_arrive(a, t, bc1, bc2, gridDim.x);
 }
 
 __global__ void k_reduce_loss(const float* __restrict__ lp, int np, int nc, double ec, float* loss) {

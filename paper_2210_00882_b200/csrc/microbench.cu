@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -237,7 +238,8 @@ void microbench(const std::string& which, int64_t n, int iters, double* ms, doub
         }, iters);
         *bytes = static_cast<double>(T * R) * 17.0 + static_cast<double>(R) * 4.0;
     } else if (which == "reduce_adam" || which == "exchange_adam") {  // the fused update kernels, P = n
-        constexpr int kParts = 8;  // partial slots (the episode's learn kernels write 44-148)
+        // partial slots (the episode's learn kernels write 59-148; FLW_MB_PARTS overrides the 8)
+        const int kParts = std::getenv("FLW_MB_PARTS") ? std::atoi(std::getenv("FLW_MB_PARTS")) : 8;
         const int64_t npad = (n + 3) / 4 * 4;
         float* part = d.get<float>(kParts * npad);
         float* p = d.get<float>(n);

@@ -204,6 +204,7 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     FLW_CUDA(cudaEventCreateWithFlags(&ev_gae_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    FLW_CUDA(cudaEventCreateWithFlags(&ev_wimg_, cudaEventDisableTiming));
     FLW_CUDA(cudaEventCreate(&ev_t0_));
     FLW_CUDA(cudaEventCreate(&ev_t1_));
     // group abort word in host-mapped memory: the host sets it (deadline passed, a peer failed)
@@ -223,7 +224,7 @@ Engine::~Engine() {
     for (void* q : p2p_ipc_opened_) cudaIpcCloseMemHandle(q);
     if (p2p_region_ptr_) cudaFree(p2p_region_ptr_);
     b_.reset();
-    for (cudaEvent_t e : {ev_fork_, ev_join_, ev_t0_, ev_t1_, ev_lfork_, ev_ljoin_, ev_plearn_, ev_gae_})
+    for (cudaEvent_t e : {ev_fork_, ev_join_, ev_wimg_, ev_t0_, ev_t1_, ev_lfork_, ev_ljoin_, ev_plearn_, ev_gae_})
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_done_)
         if (e) cudaEventDestroy(e);
@@ -859,9 +860,11 @@ void Engine::enq_learn_fast() {
     f.rep_of_env = nrep_ > 1 ? b.rep_of_env : nullptr;
     f.rep_w = b.rep_w;
     f.rep_E = E_;
-    // the weight images: built at the first train iteration of an episode; later iterations use
-    // the images the previous iteration's fused update (k_reduce_adam) wrote
-    if (learn_iter_ == 0 || !prev_fused_) fast_build_wimg(stream_, b.params, b.crit, b.wimg_c, b.pol, b.wimg_p);
+    // the weight images: built at the first train iteration of an episode (in the episode graph:
+    // on the side stream during the rollout, build_graph); later iterations use the images the
+    // previous iteration's fused update (k_reduce_adam) wrote
+    if (learn_iter_ == 0 ? !wimg_early_ : !prev_fused_)
+        fast_build_wimg(stream_, b.params, b.crit, b.wimg_c, b.pol, b.wimg_p);
     // values = critic(states), last_value = critic(last_next)
     f.net = b.crit;
     f.wimg = b.wimg_c;
@@ -1669,6 +1672,15 @@ void Engine::build_graph() {
     capturing_ = true;
     begin_episode(stream_, b_->ctx);
     trace_capture("begin");
+    // The first train iteration's weight images depend only on the params the previous episode
+    // left: built on the side stream while the episode resets and rolls out (fast k_learn path)
+    wimg_early_ = numerics_ == Numerics::Fast && !mappo_ && !wide_ && !gemm_roll_ && !eager_coll_;
+    if (wimg_early_) {
+        FLW_CUDA(cudaEventRecord(ev_wimg_, stream_));
+        FLW_CUDA(cudaStreamWaitEvent(side_, ev_wimg_, 0));
+        fast_build_wimg(side_, b_->params, b_->crit, b_->wimg_c, b_->pol, b_->wimg_p);
+        FLW_CUDA(cudaEventRecord(ev_wimg_, side_));
+    }
     enq_reset();
     trace_capture("reset");
     probe_begin("rollout");
@@ -1682,6 +1694,7 @@ void Engine::build_graph() {
     FLW_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
     enq_reward_sum();
     FLW_CUDA(cudaEventRecord(ev_join_, side_));
+    if (wimg_early_) FLW_CUDA(cudaStreamWaitEvent(stream_, ev_wimg_, 0));
     // a capture segment cannot end with the side stream still forked
     if (eager_coll_) FLW_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
     trace_capture("rollout+reward");
@@ -1699,6 +1712,7 @@ void Engine::build_graph() {
         trace_capture("sync+adam");
     }
     learn_iter_ = 0;
+    wimg_early_ = false;
     if (!eager_coll_) FLW_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
     end_segment();
     graph_ = segs_.front();

@@ -191,6 +191,8 @@ class Engine {
     Numerics numerics_;
     cudaStream_t stream_ = nullptr, side_ = nullptr, side2_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_t0_ = nullptr, ev_t1_ = nullptr;
+    cudaEvent_t ev_wimg_ = nullptr;  // the episode's first weight images, built on side_ (build_graph)
+    bool wimg_early_ = false;        // ... so the first train iteration does not build them
     double* rs_pinned_ = nullptr;                  // [kInFlight][nrep_] reward sums of in-flight episodes
     cudaEvent_t ev_done_[kInFlight] = {};          // per slot: the episode and its reward copy finished
     int64_t fl_head_ = 0, fl_tail_ = 0;            // pipelined episodes launched / finished

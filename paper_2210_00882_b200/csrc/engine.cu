@@ -1485,6 +1485,13 @@ P2pArgs Engine::p2p_args() const {
 // policy learn is still running on the other SMs): its partials reduced (and exchanged over
 // peer memory with k GPUs) and Adam applied to the critic parameters. The policy half follows
 // the join in enq_grad_sync_and_adam. Same arithmetic per parameter as the one-launch update.
+// The fused update as a programmatic dependent launch of the learn kernel before it (k_learn
+// triggers its dependents once its tiles are done). FLW_NO_PDL: plain launches (A/B only).
+bool Engine::pdl_ok() const {
+    static const bool off = std::getenv("FLW_NO_PDL") != nullptr;
+    return !off && !cfast_ && !pcompact_ && !pwide_;
+}
+
 bool Engine::split_update_ok() const {
     // (fuse_ok_: the update follows this learn; peer exchange only between distinct GPUs - a
     // co-located rank's waiting exchange could hold the SMs its peer's critic learn needs)
@@ -1505,7 +1512,7 @@ void Engine::enq_critic_update(cudaStream_t st, int ncrit) {
         u.off = s.P_policy;
         u.critic_only = true;
         u.advance = false;  // the policy launch (the iteration's last) advances the step counter
-        fast_reduce_adam(st, u);
+        fast_reduce_adam(st, u, pdl_ok());
         return;
     }
     adam_tick(st, b_->ctx, b_->bc_table, b_->bc_len);  // once per iteration: before both halves
@@ -1536,7 +1543,7 @@ void Engine::enq_grad_sync_and_adam() {
             u.nc = 0;
         }
         probe_begin("reduce");
-        fast_reduce_adam(stream_, u);
+        fast_reduce_adam(stream_, u, pdl_ok() && !probes_on_);
         probe_end();
         return;
     }

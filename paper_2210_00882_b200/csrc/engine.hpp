@@ -233,6 +233,7 @@ class Engine {
     FastUpdateArgs update_args() const;
     P2pArgs p2p_args() const;
     bool split_update_ok() const;
+    bool pdl_ok() const;
     void enq_critic_update(cudaStream_t st, int ncrit);
     std::vector<Probe> probes_;
     int open_probe_ = -1;

@@ -116,7 +116,8 @@ struct FastUpdateArgs {      // k_reduce_adam: partial reduction + Adam + weight
     bool critic_only = false;
     bool advance = true;
 };
-void fast_reduce_adam(cudaStream_t s, const FastUpdateArgs& a);
+// pdl: a programmatic dependent launch of the preceding learn kernel (same stream)
+void fast_reduce_adam(cudaStream_t s, const FastUpdateArgs& a, bool pdl = false);
 void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part_c, int np, int nc, int64_t Pp,
                           int64_t Pc, float* grads, int64_t c_off = 0);  // critic slots land at Pp + c_off
 // MAPPO compact critic (fast numerics, n > 4): layer-0 rows from the joint GEMM P, and the

@@ -106,13 +106,18 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
 // k_build_wimg), so the next train iteration's learn kernels read the updated image without a
 // build launch. The Adam step counter and its bias corrections (as k_adam_tick) are advanced by
 // the last block to finish (every block has read the old counter by then).
+// kPdl: launched as a programmatic dependent of the learn kernel (k_learn triggers its
+// dependents when its tiles are done): the Adam operands are fetched before the wait.
+template <bool kPdl>
 __global__ void __launch_bounds__(256) k_reduce_adam(FastUpdateArgs a, int nchunks) {
     __shared__ float4 ws[8][32];
     int64_t t;
     double bc1, bc2;
     adam_step_consts(a, t, bc1, bc2);
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x)
-        update_chunk(a, c, threadIdx.x, ws, bc1, bc2, [] { __syncthreads(); });
+        update_chunk<12, kPdl>(a, c, threadIdx.x, ws, bc1, bc2, [] { __syncthreads(); });
+    if constexpr (kPdl)
+        if (blockIdx.x >= nchunks) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) update_arrive(a, t, bc1, bc2, gridDim.x);
 }
 
@@ -593,10 +598,24 @@ void fast_reduce_partials(cudaStream_t s, const float* part_p, const float* part
                                                                                  c_off, grads);
 }
 
-void fast_reduce_adam(cudaStream_t s, const FastUpdateArgs& a) {
+void fast_reduce_adam(cudaStream_t s, const FastUpdateArgs& a, bool pdl) {
     const int64_t padded = (a.Pp + 3) / 4 * 4 + (a.Pc + 3) / 4 * 4;
     const int nchunks = static_cast<int>((padded + 127) / 128);
-    k_reduce_adam<<<static_cast<unsigned>(std::min(nchunks, 148 * 8)), 256, 0, s>>>(a, nchunks);
+    const unsigned grid = static_cast<unsigned>(std::min(nchunks, 148 * 8));
+    if (!pdl) {
+        k_reduce_adam<false><<<grid, 256, 0, s>>>(a, nchunks);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FLW_CUDA(cudaLaunchKernelEx(&cfg, k_reduce_adam<true>, a, nchunks));
 }
 
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss) {

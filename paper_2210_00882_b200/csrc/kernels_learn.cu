@@ -1048,6 +1048,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
     __syncthreads();
     umma::fence_after_sync();
 
+    // a programmatic dependent (the update kernel) may launch once every CTA is here: its
+    // prologue overlaps this CTA's partial-slot store
+    if constexpr (learn) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // ---- per-CTA partials: dW from TMEM, db and loss terms from shared memory (fixed order).
     // The slot is assembled in the (now idle) activation slots and leaves as one bulk copy: the
     // TMEM lane layout puts one dW row per lane, so direct stores would be 4-byte writes

@@ -25,7 +25,7 @@ __device__ __forceinline__ void adam_step_consts(const FastUpdateArgs& a, int64_
 // then runs one parameter per thread (tid < 128). The Adam operands and the weight-image index
 // are fetched before the sums, and each warp issues up to kBatch partial loads before its first
 // add (the chunk is a chain of memory round trips, not a bandwidth problem at C2 sizes).
-template <int kBatch = 12, class Sync>
+template <int kBatch = 12, bool kPdl = false, class Sync>
 __device__ __forceinline__ void update_chunk(const FastUpdateArgs& a, int64_t c, int tid, float4 (*ws)[32],
                                              double bc1, double bc2, Sync sync) {
     const int lane = tid & 31, w = tid >> 5;
@@ -46,6 +46,9 @@ __device__ __forceinline__ void update_chunk(const FastUpdateArgs& a, int64_t c,
         ip = !a.critic_only && i < a.Pp;
         e = wimg_elem(ip ? a.pol : a.crit, i);
     }
+    // programmatic dependent launch: everything above is the previous iteration's state; the
+    // partial slots below are the learn kernel's output
+    if constexpr (kPdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t q0 = c * 128LL + 4 * lane;  // first of this lane's 4 padded indices
     float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
     if (q0 < Pps + Pcs) {

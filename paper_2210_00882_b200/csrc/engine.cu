@@ -610,6 +610,7 @@ void Engine::reinit(uint64_t seed) {
     FLW_CUDA(cudaMemset(b_->m, 0, static_cast<size_t>(shape_.P) * sizeof(double)));
     FLW_CUDA(cudaMemset(b_->v, 0, static_cast<size_t>(shape_.P) * sizeof(double)));
     FLW_CUDA(cudaMemset(b_->ctx, 0, offsetof(DeviceCtx, coll_seq)));  // keep the exchange epoch
+    next_ep_dev_ = -1;
     steps_ = 0;
     cur_step_ = 0;
 }
@@ -1671,6 +1672,12 @@ void Engine::learn(int64_t ep, int64_t k) {
 // ------------------------------------------------------------------------ episode graph
 void Engine::build_graph() {
     FLW_CUDA(cudaSetDevice(device_));
+    if (!rs_pinned_) {  // [kInFlight][nrep_] reward sums (mapped), then [kInFlight] episode indices
+        FLW_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&rs_pinned_),
+                               sizeof(double) * static_cast<size_t>(kInFlight * (nrep_ + 1)), cudaHostAllocMapped));
+        FLW_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&rs_ring_d_), rs_pinned_, 0));
+        for (cudaEvent_t& e : ev_done_) FLW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     flw_trace("build_graph: capture");
     destroy_graph();
     graph_kernels_ = 0;
@@ -1700,6 +1707,7 @@ void Engine::build_graph() {
     FLW_CUDA(cudaEventRecord(ev_fork_, stream_));
     FLW_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
     enq_reward_sum();
+    publish_rsum(side_, b_->ctx, b_->rsum, numerics_ == Numerics::Exact ? nrep_ : 1, rs_ring_d_, kInFlight);
     FLW_CUDA(cudaEventRecord(ev_join_, side_));
     if (wimg_early_) FLW_CUDA(cudaStreamWaitEvent(stream_, ev_wimg_, 0));
     // a capture segment cannot end with the side stream still forked
@@ -1767,6 +1775,7 @@ void Engine::launch_graph() {
         FLW_CUDA(cudaGraphLaunch(segs_[i], stream_));
         if (i < between_.size()) between_[i]();
     }
+    ++graph_runs_;
 }
 
 void Engine::prepare() {
@@ -1777,9 +1786,11 @@ void Engine::prepare() {
 
 void Engine::enqueue_episodes(int64_t first, int64_t count) {
     FLW_CUDA(cudaSetDevice(device_));
+    if (fl_head_ != fl_tail_) fail(Errc::Config, "enqueue_episodes: pipelined episodes still in flight");
     if (!graph_) build_graph();
     FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, &first, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
     for (int64_t i = 0; i < count; ++i) launch_graph();
+    next_ep_dev_ = first + count;
     steps_ += T_ * count * nrep_;
     cur_step_ = T_;
 }
@@ -1805,10 +1816,12 @@ void Engine::sync() {
 
 double Engine::run_episode(int64_t ep, float* device_ms) {
     FLW_CUDA(cudaSetDevice(device_));
+    if (fl_head_ != fl_tail_) fail(Errc::Config, "run_episode: pipelined episodes still in flight");
     if (!graph_) build_graph();
     FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, &ep, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
     FLW_CUDA(cudaEventRecord(ev_t0_, stream_));
     launch_graph();
+    next_ep_dev_ = ep + 1;
     FLW_CUDA(cudaEventRecord(ev_t1_, stream_));
     flw_trace("run_episode: launched");
     wait_stream("run_episode");
@@ -1827,20 +1840,20 @@ void Engine::launch_episode(int64_t ep) {
     FLW_CUDA(cudaSetDevice(device_));
     if (fl_head_ - fl_tail_ >= kInFlight) fail(Errc::Config, "launch_episode: too many episodes in flight");
     if (!graph_) build_graph();
-    if (!rs_pinned_) {  // [kInFlight][nrep_] reward sums, then [kInFlight] episode indices
-        FLW_CUDA(cudaMallocHost(&rs_pinned_, sizeof(double) * static_cast<size_t>(kInFlight * (nrep_ + 1))));
-        for (cudaEvent_t& e : ev_done_) FLW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
     const int slot = static_cast<int>(fl_head_ % kInFlight);
     // the episode index from a pinned slot: a truly asynchronous copy (the slot is reused only
     // after finish_episode has waited for this episode)
     int64_t* ep_pinned = reinterpret_cast<int64_t*>(rs_pinned_ + static_cast<size_t>(kInFlight) * nrep_) + slot;
     *ep_pinned = ep;
-    FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, ep_pinned, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+    // consecutive episodes: the previous graph's k_begin_episode already advanced the device
+    // counter to ep, so no copy sits between the two graphs
+    if (ep != next_ep_dev_)
+        FLW_CUDA(cudaMemcpyAsync(&b_->ctx->next_episode, ep_pinned, sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+    // the graph publishes its reward sums into ring slot graph_runs_ % kInFlight (k_publish_rsum):
+    // nothing but the completion event follows it on the stream
+    fl_slot_[slot] = graph_runs_ % kInFlight;
     launch_graph();
-    const int n = numerics_ == Numerics::Exact ? nrep_ : 1;  // (fast: the total in slot 0)
-    FLW_CUDA(cudaMemcpyAsync(rs_pinned_ + static_cast<size_t>(slot) * nrep_, b_->rsum, sizeof(double) * n,
-                             cudaMemcpyDeviceToHost, stream_));
+    next_ep_dev_ = ep + 1;
     FLW_CUDA(cudaEventRecord(ev_done_[slot], stream_));
     ++fl_head_;
 }
@@ -1853,9 +1866,10 @@ std::vector<double> Engine::finish_episode() {
     ++fl_tail_;
     steps_ += T_ * nrep_;
     cur_step_ = T_;
-    const int n = numerics_ == Numerics::Exact ? nrep_ : 1;
+    const int n = numerics_ == Numerics::Exact ? nrep_ : 1;  // (fast: the total in entry 0)
     std::vector<double> r(static_cast<size_t>(nrep_), 0.0);
-    for (int i = 0; i < n; ++i) r[static_cast<size_t>(i)] = rs_pinned_[static_cast<size_t>(slot) * nrep_ + i];
+    const double* ring = rs_pinned_ + static_cast<size_t>(fl_slot_[slot]) * n;
+    for (int i = 0; i < n; ++i) r[static_cast<size_t>(i)] = ring[i];
     double total = 0.0;
     for (double v : r) total += v;
     if (std::isnan(total) && numerics_ == Numerics::Fast)

@@ -33,6 +33,7 @@ struct DeviceCtx {      // device-resident episode context (read by kernels insi
     int64_t adam_t;
     double bc1, bc2;    // Adam bias corrections 1 - beta^t, from a host-computed table
     uint64_t coll_seq;  // peer-memory exchange epoch: monotonically increasing, never reset
+    uint64_t runs;      // episode graphs completed (k_publish_rsum's ring slot), never reset
 };
 
 class Comm;  // NCCL gradient group (comm.hpp)
@@ -196,6 +197,10 @@ class Engine {
     double* rs_pinned_ = nullptr;                  // [kInFlight][nrep_] reward sums of in-flight episodes
     cudaEvent_t ev_done_[kInFlight] = {};          // per slot: the episode and its reward copy finished
     int64_t fl_head_ = 0, fl_tail_ = 0;            // pipelined episodes launched / finished
+    int64_t next_ep_dev_ = -1;  // ctx->next_episode once the enqueued work has run (-1: unknown)
+    int64_t graph_runs_ = 0;    // episode graphs launched (= ctx->runs once they have run)
+    int64_t fl_slot_[kInFlight] = {};  // ring slot (graph_runs_ % kInFlight) of each in-flight episode
+    double* rs_ring_d_ = nullptr;      // device address of the mapped reward ring (rs_pinned_)
     cudaEvent_t ev_lfork_ = nullptr, ev_ljoin_ = nullptr;  // policy || critic learn fork/join
     std::unique_ptr<Bufs> b_;
     std::unique_ptr<Comm> comm_;

@@ -432,6 +432,16 @@ __global__ void k_grad_mean(const float* __restrict__ g, int k, int64_t P, doubl
 
 __global__ void k_begin_episode(DeviceCtx* ctx) { ctx->episode = ctx->next_episode++; }
 
+// The episode's reward sums into slot (runs % slots) of a host-mapped ring (zero-copy: no
+// device-to-host copy between two episode graphs); the host reads the slot after the episode's
+// completion event.
+__global__ void k_publish_rsum(DeviceCtx* ctx, const double* rsum, int n, double* ring, int slots) {
+    const uint64_t slot = ctx->runs % static_cast<uint64_t>(slots);
+    for (int i = 0; i < n; ++i) ring[slot * n + i] = rsum[i];
+    __threadfence_system();
+    ctx->runs += 1;
+}
+
 __global__ void k_adam_tick(DeviceCtx* ctx, const double2* __restrict__ table, int64_t len) {
     int64_t t = ++ctx->adam_t;
     if (t <= len) {
@@ -632,6 +642,9 @@ void exact_grad_mean(cudaStream_t s, const float* gathered, int k, int64_t P, do
 }
 
 void begin_episode(cudaStream_t s, DeviceCtx* ctx) { k_begin_episode<<<1, 1, 0, s>>>(ctx); }
+void publish_rsum(cudaStream_t s, DeviceCtx* ctx, const double* rsum, int n, double* ring, int slots) {
+    k_publish_rsum<<<1, 1, 0, s>>>(ctx, rsum, n, ring, slots);
+}
 
 void adam_tick(cudaStream_t s, DeviceCtx* ctx, const double2* bc_table, int64_t table_len) {
     k_adam_tick<<<1, 1, 0, s>>>(ctx, bc_table, table_len);

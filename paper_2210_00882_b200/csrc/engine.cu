@@ -213,6 +213,7 @@ Engine::Engine(const AlgoConfig& cfg, int device, uint64_t seed, int64_t env_lo,
     *abort_h_ = 0;
     FLW_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&abort_d_), abort_h_, 0));
     alloc();
+    FLW_CUDA(cudaDeviceSynchronize());  // alloc's zero-fills (legacy stream) before the stream's work
     init_params();
 }
 
@@ -584,21 +585,21 @@ void Engine::alloc() {
 // Xavier-uniform weights keyed by (seed, param stream, node id, i), zero biases, rounded to
 // f32 (interp.cpp:71-85); node ids follow make_mlp_params order (programs.cpp:42-54).
 void Engine::init_params() {
+    // Xavier-uniform weights, zero biases (interp.cpp init): one kernel per layer computing the
+    // same keyed draws as the host would (rng_uniform_range rounds every operation on both sides;
+    // the bound a is computed here), on the engine's stream - no host loop, no blocking copy
     const ProgramShape& s = shape_;
-    std::vector<float> p(static_cast<size_t>(s.P), 0.0f);
+    FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaMemsetAsync(b_->params, 0, static_cast<size_t>(s.P) * sizeof(float), stream_));
     for (int net = 0; net < 2; ++net) {
         const auto& d = net == 0 ? s.pdims : s.cdims;
         for (int l = 0; l < s.L; ++l) {
-            uint64_t node = static_cast<uint64_t>(net * 2 * s.L + 2 * l);
-            double a = std::sqrt(6.0 / (static_cast<double>(d[l]) + static_cast<double>(d[l + 1])));
-            int64_t n = static_cast<int64_t>(d[l]) * d[l + 1];
-            for (int64_t i = 0; i < n; ++i)
-                p[static_cast<size_t>(s.woff[net][l] + i)] = static_cast<float>(
-                    rng_uniform_range(rng_key(seed_, kParamStream, node, static_cast<uint64_t>(i)), -a, a));
+            const uint64_t node = static_cast<uint64_t>(net * 2 * s.L + 2 * l);
+            const double a = std::sqrt(6.0 / (static_cast<double>(d[l]) + static_cast<double>(d[l + 1])));
+            const int64_t n = static_cast<int64_t>(d[l]) * d[l + 1];
+            xavier_init(stream_, b_->params + s.woff[net][l], n, seed_, node, a);
         }
     }
-    FLW_CUDA(cudaSetDevice(device_));
-    FLW_CUDA(cudaMemcpy(b_->params, p.data(), p.size() * sizeof(float), cudaMemcpyHostToDevice));
 }
 
 void Engine::reinit(uint64_t seed) {
@@ -607,9 +608,9 @@ void Engine::reinit(uint64_t seed) {
     if (seed != seed_ && graph_) destroy_graph();  // the seed is baked into the captured kernel arguments
     seed_ = seed;
     init_params();
-    FLW_CUDA(cudaMemset(b_->m, 0, static_cast<size_t>(shape_.P) * sizeof(double)));
-    FLW_CUDA(cudaMemset(b_->v, 0, static_cast<size_t>(shape_.P) * sizeof(double)));
-    FLW_CUDA(cudaMemset(b_->ctx, 0, offsetof(DeviceCtx, coll_seq)));  // keep the exchange epoch
+    FLW_CUDA(cudaMemsetAsync(b_->m, 0, static_cast<size_t>(shape_.P) * sizeof(double), stream_));
+    FLW_CUDA(cudaMemsetAsync(b_->v, 0, static_cast<size_t>(shape_.P) * sizeof(double), stream_));
+    FLW_CUDA(cudaMemsetAsync(b_->ctx, 0, offsetof(DeviceCtx, coll_seq), stream_));  // keep the exchange epoch
     next_ep_dev_ = -1;
     steps_ = 0;
     cur_step_ = 0;
@@ -1887,6 +1888,7 @@ void Engine::drain_episodes() {
 // --------------------------------------------------------------------------- params
 void Engine::get_params(double* out) {
     FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));  // (params are written on the engine's stream)
     std::vector<float> p(static_cast<size_t>(shape_.P));
     FLW_CUDA(cudaMemcpy(p.data(), b_->params, p.size() * sizeof(float), cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < p.size(); ++i) out[i] = static_cast<double>(p[i]);
@@ -1894,6 +1896,7 @@ void Engine::get_params(double* out) {
 
 void Engine::set_params(const double* in) {
     FLW_CUDA(cudaSetDevice(device_));
+    FLW_CUDA(cudaStreamSynchronize(stream_));
     std::vector<float> p(static_cast<size_t>(shape_.P));
     for (size_t i = 0; i < p.size(); ++i) p[i] = static_cast<float>(in[i]);
     FLW_CUDA(cudaMemcpy(b_->params, p.data(), p.size() * sizeof(float), cudaMemcpyHostToDevice));

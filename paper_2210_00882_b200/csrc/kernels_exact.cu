@@ -642,6 +642,15 @@ void exact_grad_mean(cudaStream_t s, const float* gathered, int k, int64_t P, do
 }
 
 void begin_episode(cudaStream_t s, DeviceCtx* ctx) { k_begin_episode<<<1, 1, 0, s>>>(ctx); }
+
+__global__ void k_xavier(float* w, int64_t n, uint64_t seed, uint64_t node, double a) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        w[i] = static_cast<float>(rng_uniform_range(rng_key(seed, kParamStream, node, static_cast<uint64_t>(i)), -a, a));
+}
+void xavier_init(cudaStream_t s, float* w, int64_t n, uint64_t seed, uint64_t node, double a) {
+    if (n > 0) k_xavier<<<blocks_for(n, 256), 256, 0, s>>>(w, n, seed, node, a);
+}
 void publish_rsum(cudaStream_t s, DeviceCtx* ctx, const double* rsum, int n, double* ring, int slots) {
     k_publish_rsum<<<1, 1, 0, s>>>(ctx, rsum, n, ring, slots);
 }

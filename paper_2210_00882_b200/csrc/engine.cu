@@ -584,22 +584,25 @@ void Engine::alloc() {
 
 // Xavier-uniform weights keyed by (seed, param stream, node id, i), zero biases, rounded to
 // f32 (interp.cpp:71-85); node ids follow make_mlp_params order (programs.cpp:42-54).
-void Engine::init_params() {
-    // Xavier-uniform weights, zero biases (interp.cpp init): one kernel per layer computing the
-    // same keyed draws as the host would (rng_uniform_range rounds every operation on both sides;
-    // the bound a is computed here), on the engine's stream - no host loop, no blocking copy
+void Engine::init_params(bool moments) {
+    // Xavier-uniform weights, zero biases (interp.cpp init) in one kernel computing the same keyed
+    // draws as the host would (rng_uniform_range rounds every operation on both sides; the bounds
+    // are computed here), on the engine's stream - no host loop, no blocking copy
     const ProgramShape& s = shape_;
     FLW_CUDA(cudaSetDevice(device_));
-    FLW_CUDA(cudaMemsetAsync(b_->params, 0, static_cast<size_t>(s.P) * sizeof(float), stream_));
+    XavierTable t{};
     for (int net = 0; net < 2; ++net) {
         const auto& d = net == 0 ? s.pdims : s.cdims;
         for (int l = 0; l < s.L; ++l) {
-            const uint64_t node = static_cast<uint64_t>(net * 2 * s.L + 2 * l);
-            const double a = std::sqrt(6.0 / (static_cast<double>(d[l]) + static_cast<double>(d[l + 1])));
-            const int64_t n = static_cast<int64_t>(d[l]) * d[l + 1];
-            xavier_init(stream_, b_->params + s.woff[net][l], n, seed_, node, a);
+            if (t.count == 16) fail(Errc::Config, "more than 8 layers per net");
+            t.node[t.count] = static_cast<uint64_t>(net * 2 * s.L + 2 * l);
+            t.a[t.count] = std::sqrt(6.0 / (static_cast<double>(d[l]) + static_cast<double>(d[l + 1])));
+            t.n[t.count] = static_cast<int64_t>(d[l]) * d[l + 1];
+            t.woff[t.count] = s.woff[net][l];
+            ++t.count;
         }
     }
+    param_init(stream_, t, b_->params, s.P, moments ? b_->m : nullptr, moments ? b_->v : nullptr, seed_);
 }
 
 void Engine::reinit(uint64_t seed) {
@@ -607,9 +610,7 @@ void Engine::reinit(uint64_t seed) {
     FLW_CUDA(cudaStreamSynchronize(stream_));
     if (seed != seed_ && graph_) destroy_graph();  // the seed is baked into the captured kernel arguments
     seed_ = seed;
-    init_params();
-    FLW_CUDA(cudaMemsetAsync(b_->m, 0, static_cast<size_t>(shape_.P) * sizeof(double), stream_));
-    FLW_CUDA(cudaMemsetAsync(b_->v, 0, static_cast<size_t>(shape_.P) * sizeof(double), stream_));
+    init_params(true);  // (and the Adam moments)
     FLW_CUDA(cudaMemsetAsync(b_->ctx, 0, offsetof(DeviceCtx, coll_seq), stream_));  // keep the exchange epoch
     next_ep_dev_ = -1;
     steps_ = 0;

@@ -138,7 +138,7 @@ class Engine {
   private:
     struct Bufs;
     void alloc();
-    void init_params();
+    void init_params(bool moments = false);
     void set_episode(int64_t ep);
     void enq_reset();
     void enq_step(int64_t st);

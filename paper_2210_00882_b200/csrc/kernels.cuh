@@ -98,8 +98,16 @@ void permute_rows_i32(cudaStream_t s, const int32_t* src, int32_t* dst, int64_t 
 void permute_rows_f64(cudaStream_t s, const double* src, double* dst, int64_t T, int64_t E, const ReplicaMap& m);
 void exact_grad_mean(cudaStream_t s, const float* gathered, int k, int64_t P, double* mean);
 void begin_episode(cudaStream_t s, DeviceCtx* ctx);  // ctx->episode = ctx->next_episode++
-// w[i] = f32(U(-a, a) keyed (seed, kParamStream, node, i)), i < n (Engine::init_params)
-void xavier_init(cudaStream_t s, float* w, int64_t n, uint64_t seed, uint64_t node, double a);
+// Engine::init_params: params[woff[l] + i] = f32(U(-a[l], a[l]) keyed (seed, kParamStream,
+// node[l], i)) for i < n[l], every other parameter 0; m, v (if given) zeroed. One launch.
+struct XavierTable {
+    int count;
+    int64_t woff[16], n[16];
+    uint64_t node[16];
+    double a[16];
+};
+void param_init(cudaStream_t s, const XavierTable& t, float* params, int64_t P, double* m, double* v,
+                uint64_t seed);
 // rsum[0, n) -> ring[(ctx->runs % slots) * n, +n) (host-mapped), then ++ctx->runs
 void publish_rsum(cudaStream_t s, DeviceCtx* ctx, const double* rsum, int n, double* ring, int slots);
 void adam_tick(cudaStream_t s, DeviceCtx* ctx, const double2* bc_table, int64_t table_len);

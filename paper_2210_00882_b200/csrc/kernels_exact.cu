@@ -643,13 +643,29 @@ void exact_grad_mean(cudaStream_t s, const float* gathered, int k, int64_t P, do
 
 void begin_episode(cudaStream_t s, DeviceCtx* ctx) { k_begin_episode<<<1, 1, 0, s>>>(ctx); }
 
-__global__ void k_xavier(float* w, int64_t n, uint64_t seed, uint64_t node, double a) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        w[i] = static_cast<float>(rng_uniform_range(rng_key(seed, kParamStream, node, static_cast<uint64_t>(i)), -a, a));
+// All parameters in one launch: weights of layer l (woff[l], n[l] elements) Xavier-uniform with
+// bound a[l], everything else (biases) zero; optionally the Adam moments zeroed too.
+__global__ void k_param_init(XavierTable t, float* params, int64_t P, double* m, double* v, uint64_t seed) {
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < P;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float w = 0.0f;
+        for (int l = 0; l < t.count; ++l) {
+            const int64_t i = j - t.woff[l];
+            if (i >= 0 && i < t.n[l]) {
+                w = static_cast<float>(rng_uniform_range(rng_key(seed, kParamStream, t.node[l], static_cast<uint64_t>(i)),
+                                                         -t.a[l], t.a[l]));
+                break;
+            }
+        }
+        params[j] = w;
+        if (m) m[j] = 0.0;
+        if (v) v[j] = 0.0;
+    }
 }
-void xavier_init(cudaStream_t s, float* w, int64_t n, uint64_t seed, uint64_t node, double a) {
-    if (n > 0) k_xavier<<<blocks_for(n, 256), 256, 0, s>>>(w, n, seed, node, a);
+void param_init(cudaStream_t s, const XavierTable& t, float* params, int64_t P, double* m, double* v,
+                uint64_t seed) {
+    if (P > 0) k_param_init<<<static_cast<unsigned>(std::min<int64_t>(blocks_for(P, 256), 148 * 8)), 256, 0, s>>>(
+        t, params, P, m, v, seed);
 }
 void publish_rsum(cudaStream_t s, DeviceCtx* ctx, const double* rsum, int n, double* ring, int slots) {
     k_publish_rsum<<<1, 1, 0, s>>>(ctx, rsum, n, ring, slots);

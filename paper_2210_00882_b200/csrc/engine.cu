@@ -87,6 +87,7 @@ struct Engine::Bufs {
     double *block_sums = nullptr, *rsum_scratch = nullptr;
     unsigned* gae_counter = nullptr;  // last-block-done counter of the fused GAE statistics
     unsigned* upd_counter = nullptr;  // last-block-done counter of k_reduce_adam
+    unsigned* begin_counter = nullptr;  // last-block-done counter of the episode-begin reset
     // R > 1 replicas: env -> replica map, replica-major trajectory copies (exact), per-replica
     // gradient slots [R, P], advantage statistics [R, 2] and row weights (fast)
     int32_t* rep_of_env = nullptr;
@@ -346,6 +347,7 @@ void Engine::alloc() {
     const ProgramShape& s = shape_;
     const int S = s.obs_dim, A = s.n_actions, L = s.L;
     b.ctx = b.alloc<DeviceCtx>(1);
+    b.begin_counter = b.alloc<unsigned>(1);
     // Adam bias-correction table 1 - beta^t computed with the host libm pow, the reference's
     // arithmetic (mlp.cpp:151-152), for every step this run can take (+ slack).
     b.bc_len = std::max<int64_t>(4096, (cfg_.episodes + 16) * s.learn_iters);
@@ -680,13 +682,15 @@ void Engine::set_episode(int64_t ep) {
 }
 
 // ----------------------------------------------------------------------------- phases
-void Engine::enq_reset() {
+void Engine::enq_reset(bool begin) {
     Bufs& b = *b_;
-    if (mappo_)
+    if (mappo_) {
+        if (begin) begin_episode(stream_, b.ctx);
         mappo_reset(stream_, b.ctx, shape_.n_agents, b.est, b.done, b.stepc, b.joint, b.states, b.cin, E_, lo_, seed_);
-    else
+    } else {
         exact_reset(stream_, b.ctx, env_params(cfg_, shape_, b_->synth_b), b.est, b.done, b.stepc, b.states, E_, lo_,
-                    shape_.obs_dim, seed_);
+                    shape_.obs_dim, seed_, begin ? b.begin_counter : nullptr);
+    }
 }
 
 void Engine::enq_mlp_forward(int net, const float* X, int64_t M, float* const* H, int first_layer) {
@@ -1686,7 +1690,7 @@ void Engine::build_graph() {
     clear_probes();
     FLW_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     capturing_ = true;
-    begin_episode(stream_, b_->ctx);
+    // (the episode begin - ctx->episode = ctx->next_episode++ - runs inside the reset launch)
     trace_capture("begin");
     // The first train iteration's weight images depend only on the params the previous episode
     // left: built on the side stream while the episode resets and rolls out (fast k_learn path)
@@ -1697,7 +1701,7 @@ void Engine::build_graph() {
         fast_build_wimg(side_, b_->params, b_->crit, b_->wimg_c, b_->pol, b_->wimg_p);
         FLW_CUDA(cudaEventRecord(ev_wimg_, side_));
     }
-    enq_reset();
+    enq_reset(true);
     trace_capture("reset");
     probe_begin("rollout");
     if (numerics_ == Numerics::Fast && !mappo_ && !wide_ && !gemm_roll_)

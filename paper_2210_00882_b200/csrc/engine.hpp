@@ -140,7 +140,7 @@ class Engine {
     void alloc();
     void init_params(bool moments = false);
     void set_episode(int64_t ep);
-    void enq_reset();
+    void enq_reset(bool begin = false);
     void enq_step(int64_t st);
     void enq_rollout_fast(int64_t step0, int64_t nsteps);
     bool enq_rollout_fast_mappo(int64_t step0, int64_t nsteps);

@@ -64,8 +64,10 @@ struct DwTile {           // one 32(t) x 32(j) block of dW_l = H_{l-1}^T dZ_l (+
 };
 
 // ---------------------------------------------------------------- exact (FP64-accumulate) path
-void exact_reset(cudaStream_t s, const DeviceCtx* ctx, const EnvParams& env, double* est, uint8_t* done,
-                 int32_t* stepc, float* obs0, int64_t E, int64_t env_lo, int S, uint64_t seed);
+// begin != null (the episode graph): the reset also does begin_episode's counter update
+void exact_reset(cudaStream_t s, DeviceCtx* ctx, const EnvParams& env, double* est, uint8_t* done,
+                 int32_t* stepc, float* obs0, int64_t E, int64_t env_lo, int S, uint64_t seed,
+                 unsigned* begin = nullptr);
 void exact_layer_fwd(cudaStream_t s, const float* in, const float* W, const float* b, float* out, int64_t M, int K,
                      int N, int act);
 void exact_layer_dh(cudaStream_t s, const float* dz, const float* W, const float* hprev, float* dzprev, int64_t M,

@@ -24,16 +24,30 @@ __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : 
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 
 // --------------------------------------------------------------------------------- reset
-__global__ void k_reset(const DeviceCtx* __restrict__ ctx, EnvParams env, double* est, uint8_t* done,
-                        int32_t* stepc, float* obs0, int64_t E, int64_t env_lo, int S, uint64_t seed) {
-    int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (e >= E) return;
-    // env_seed = key(seed, kEnvStream, env_lo + e, episode)  (interp.cpp:214-215)
-    uint64_t es = rng_key(seed, kEnvStream, static_cast<uint64_t>(env_lo + e), static_cast<uint64_t>(ctx->episode));
-    env_reset_dev(env, es, est, E, e);
-    done[e] = 0;
-    stepc[e] = 0;
-    for (int j = 0; j < S; ++j) obs0[e * S + j] = static_cast<float>(env_obs1(env, est, E, e, j));
+// begin (the episode graph): also k_begin_episode's work - the episode is ctx->next_episode, and
+// the last block to finish stores it in ctx->episode and advances ctx->next_episode (every block
+// has read it by then; begin re-armed to 0)
+__global__ void k_reset(DeviceCtx* __restrict__ ctx, EnvParams env, double* est, uint8_t* done,
+                        int32_t* stepc, float* obs0, int64_t E, int64_t env_lo, int S, uint64_t seed,
+                        unsigned* begin) {
+    const int64_t ep = begin ? ctx->next_episode : ctx->episode;
+    const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (e < E) {
+        // env_seed = key(seed, kEnvStream, env_lo + e, episode)  (interp.cpp:214-215)
+        const uint64_t es = rng_key(seed, kEnvStream, static_cast<uint64_t>(env_lo + e), static_cast<uint64_t>(ep));
+        env_reset_dev(env, es, est, E, e);
+        done[e] = 0;
+        stepc[e] = 0;
+        for (int j = 0; j < S; ++j) obs0[e * S + j] = static_cast<float>(env_obs1(env, est, E, e, j));
+    }
+    if (begin) {
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(begin, 1u) == gridDim.x - 1) {
+            ctx->episode = ep;
+            ctx->next_episode = ep + 1;
+            *begin = 0u;
+        }
+    }
 }
 
 // ------------------------------------------------------------------------ dense layers
@@ -476,9 +490,9 @@ inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n +
 }  // namespace
 
 // ------------------------------------------------------------------------------ launchers
-void exact_reset(cudaStream_t s, const DeviceCtx* ctx, const EnvParams& env, double* est, uint8_t* done,
-                 int32_t* stepc, float* obs0, int64_t E, int64_t env_lo, int S, uint64_t seed) {
-    k_reset<<<blocks_for(E, 128), 128, 0, s>>>(ctx, env, est, done, stepc, obs0, E, env_lo, S, seed);
+void exact_reset(cudaStream_t s, DeviceCtx* ctx, const EnvParams& env, double* est, uint8_t* done,
+                 int32_t* stepc, float* obs0, int64_t E, int64_t env_lo, int S, uint64_t seed, unsigned* begin) {
+    k_reset<<<blocks_for(E, 128), 128, 0, s>>>(ctx, env, est, done, stepc, obs0, E, env_lo, S, seed, begin);
 }
 
 void exact_layer_fwd(cudaStream_t s, const float* in, const float* W, const float* b, float* out, int64_t M, int K,

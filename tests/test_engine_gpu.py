@@ -166,6 +166,33 @@ def test_pipelined_episodes_equal_synchronous(numerics):
         b.finish_episode()  # nothing in flight
 
 
+@pytest.mark.parametrize("numerics", ["exact", "fast"])
+def test_pipelined_episode_indices_and_reinit(numerics):
+    """The pipelined gate keeps the device episode counter when launches are consecutive and
+    copies the index otherwise (a jump, or after run_episode / reinit); the graph publishes the
+    reward sums into a host-mapped ring slot per graph run. Any index sequence, mixed with
+    run_episode and reinit, gives run_episode's rewards and params."""
+    _need_gpu()
+    from paper_2210_00882_b200 import DpdEngine
+
+    algo = CASES["ppo_synth_h64"]
+    seq = [0, 1, 5, 6, 2]
+    a = DpdEngine(algo, seed=9, numerics=numerics)
+    ra = [a.run_episode(ep)[0] for ep in seq]
+    b = DpdEngine(algo, seed=3, numerics=numerics)
+    b.launch_episode(4)  # a different run first: reinit must forget its counter and params
+    b.finish_episode()
+    b.reinit(9)
+    rb = [b.run_episode(seq[0])[0]]  # synchronous first (a graph run: the ring slot advances)
+    b.launch_episode(seq[1])
+    for i in range(1, len(seq)):
+        if i + 1 < len(seq):
+            b.launch_episode(seq[i + 1])
+        rb.append(b.finish_episode())
+    assert ra == rb
+    np.testing.assert_array_equal(a.params(), b.params())
+
+
 def test_run_local_summary_schema():
     _need_gpu()
     from paper_2210_00882_b200 import Program

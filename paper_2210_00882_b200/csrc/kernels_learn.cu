@@ -57,13 +57,7 @@ __host__ __device__ constexpr int threads_for(int mode) { return 32 * (4 * group
 // learn modes: registers per thread after the role split (3 x 128 x 152 + 128 x 56 = 65536): the
 // epilogue warps hold a row's accumulators, activations and loss inputs; the producers and the
 // loader only issue
-// (12 x 160 + 4 x 32 = 16 x 128, the launch's registers; A/B at C2: 144/80 0.737, 152/56 0.733,
-// 160/32 0.730-0.732 ms; no spills in any of them)
-#ifndef FLW_REG_EPI
-#define FLW_REG_EPI 160
-#define FLW_REG_SIDE 32
-#endif
-constexpr int kRegEpi = FLW_REG_EPI, kRegSide = FLW_REG_SIDE;
+constexpr int kRegEpi = 152, kRegSide = 56;
 constexpr uint32_t kSlot = kRows * kMaxW * 2;  // one 128 x 64 bf16 tile
 constexpr int kXPre = 18;                      // input columns prefetched in registers (9 packed regs)
 #ifndef FLW_TANH_MUFU_PAIRS

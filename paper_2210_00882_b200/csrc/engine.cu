@@ -916,6 +916,9 @@ void Engine::enq_learn_fast() {
     f.hscratch = b.hscratch;
     const int64_t grp = fast_values_groups();
     const int vgrid = static_cast<int>(std::min<int64_t>(lgrid, ((f.rows + 127) / 128 + grp - 1) / grp));
+    // the values pass and the policy learn start as programmatic dependents of the kernel before
+    // them on their stream (setup overlapped; griddepcontrol.wait before any input is read)
+    f.pdl = pdl_ok() && !probes_on_ ? 1 : 0;
     const FastLearnArgs fv = f;  // the values pass (kept for the next iteration's, see below)
     if (vg_ready_) {
         // the previous iteration enqueued this one's values pass + GAE on side2_ (pipelined)
@@ -1000,6 +1003,7 @@ void Engine::enq_learn_fast() {
     }
     if (concurrent) FLW_CUDA(cudaEventRecord(ev_plearn_, stream_));  // the policy learn read adv
     FastLearnArgs fc = f;
+    fc.pdl = 0;
     fc.X = Xc;
     fc.in_cols = Cin;
     fc.net = b.crit;

@@ -60,6 +60,9 @@ struct FastLearnArgs {
     float* partials;           // [grid, part_stride]
     int64_t part_stride;       // = parameter count of this net
     float* loss_partials;      // [grid, 3]
+    // launched as a programmatic dependent of the kernel before it on the stream (the update):
+    // the setup runs, then griddepcontrol.wait before the weight image and the biases are read
+    int pdl = 0;
 };
 
 size_t fast_wimg_bytes(const FastNet& n);  // bytes of the weight-tile image (smem prefix)

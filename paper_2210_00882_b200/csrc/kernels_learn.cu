@@ -316,16 +316,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
         umma::mbar_init(&zbar, 1);
         for (int g = 0; g < kGroups; ++g) epi_cnt[g] = rd_cnt[g] = xf_cnt[g] = 0;
         for (int l = 0; l < kMaxLayers; ++l) dwtok[l] = 0;
-        s_adv_on = a.adv_stats && !a.rep_of_env;
-        s_adv[0] = s_adv_on ? a.adv_stats[0] : 0.0;
-        s_adv[1] = s_adv_on ? a.adv_stats[1] : 0.0;
         umma::fence_barrier_init();
-        // the weight image's copy starts first: it overlaps the rest of the setup
-        bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
-    }
-    for (int i = t; i < L * kMaxW; i += kThreads) {  // one global load per thread, all in flight
-        const int l = i / kMaxW, o = i % kMaxW;
-        bias[i] = o < n.rout[l] ? a.params[n.boff[l] + o] : 0.0f;
     }
     if (learn)
         for (int i = t; i < kEpiWarps * kMaxLayers * kMaxW / 4; i += kThreads)
@@ -336,6 +327,19 @@ __global__ void __launch_bounds__(threads_for(MODE), 1) k_learn(FastLearnArgs a,
         umma::fence_async_smem();
     }
     if (w == 0) umma::tmem_alloc<512>(&tslot);
+    // programmatic dependent launch (a.pdl): the setup above overlaps the update kernel before
+    // this one; the weight image and the biases are that kernel's output
+    if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (t == 0) {
+        bulk_load(smem, reinterpret_cast<const uint8_t*>(a.wimg), C.wbytes, &wbar);
+        s_adv_on = a.adv_stats && !a.rep_of_env;  // (the GAE's output: possibly the kernel before)
+        s_adv[0] = s_adv_on ? a.adv_stats[0] : 0.0;
+        s_adv[1] = s_adv_on ? a.adv_stats[1] : 0.0;
+    }
+    for (int i = t; i < L * kMaxW; i += kThreads) {  // one global load per thread, all in flight
+        const int l = i / kMaxW, o = i % kMaxW;
+        bias[i] = o < n.rout[l] ? a.params[n.boff[l] + o] : 0.0f;
+    }
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
@@ -1162,8 +1166,22 @@ void fast_learn(cudaStream_t s, const FastLearnArgs& a, int grid) {
     auto go = [&](auto kern) {
         // per-device attribute: set on every launch (cheap, and legal inside stream capture)
         FLW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<grid, threads_for(mode), smem, s>>>(a, carve);
-        FLW_CUDA(cudaGetLastError());
+        if (!a.pdl) {
+            kern<<<grid, threads_for(mode), smem, s>>>(a, carve);
+            FLW_CUDA(cudaGetLastError());
+            return;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(static_cast<unsigned>(threads_for(mode)));
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        FLW_CUDA(cudaLaunchKernelEx(&cfg, kern, a, carve));
     };
     const bool na8 = a.net.rout[a.net.L - 1] <= 8;
     if (a.act == 0) {

@@ -930,7 +930,7 @@ void Engine::enq_learn_fast() {
         probe_end();
         probe_begin("gae");
         fast_gae(stream_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
-                 b.block_sums, b.stats, b.gae_counter);
+                 b.block_sums, b.stats, b.gae_counter, f.pdl != 0);
         if (nrep_ > 1 && ppo && cfg_.normalize_adv)  // each folded unit normalises over its own rows
             fast_rep_adv_stats(stream_, b.adv, T_, E_, b.rep_off, b.rep_n, nrep_, b.stats);
         probe_end();
@@ -1030,7 +1030,7 @@ void Engine::enq_learn_fast() {
             fast_learn(side2_, fv, vgrid);
             FLW_CUDA(cudaStreamWaitEvent(side2_, ev_plearn_, 0));
             fast_gae(side2_, b.rew, b.values, b.done_f, b.last_value, TR_, R_, cfg_.gamma, cfg_.lam, b.adv, b.ret, ppo,
-                     b.block_sums, b.stats, b.gae_counter);
+                     b.block_sums, b.stats, b.gae_counter, fv.pdl != 0);
             FLW_CUDA(cudaEventRecord(ev_gae_, side2_));
             vg_ready_ = true;
         }

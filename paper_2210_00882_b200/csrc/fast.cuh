@@ -132,7 +132,8 @@ void mappo_fast_layer0_grads(cudaStream_t s, const float* dz0, int64_t T, int64_
 void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, double entropy_coef, float* loss);
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
-              double* block_sums, double* stats, unsigned* done_counter = nullptr);  // counter: fused stats
+              double* block_sums, double* stats, unsigned* done_counter = nullptr,  // counter: fused stats
+              bool pdl = false);  // k_gae_scan32 as a programmatic dependent of the values pass
 // k_gae_scan32 for any stream count (T = 32), persistent over 32-stream tiles (microbenchmarks)
 void fast_gae_scan32(cudaStream_t s, const float* rew, const float* values, const float* done_f,
                      const float* last_value, int64_t R, double gamma, double lam, float* adv, float* ret,

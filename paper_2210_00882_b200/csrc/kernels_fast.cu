@@ -288,7 +288,9 @@ __global__ void __launch_bounds__(1024) k_gae_scan32(const float* __restrict__ r
                                                      const float* __restrict__ done_f,
                                                      const float* __restrict__ last_value, int64_t R, double gamma,
                                                      double lam, float* adv, float* ret, bool with_adv,
-                                                     double* block_sums, double* stats, unsigned* done_counter) {
+                                                     double* block_sums, double* stats, unsigned* done_counter,
+                                                     bool pdl) {
+    if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // the values pass's output
     // Persistent over tiles of 32 streams x 32 steps (grid-stride); the next tile's inputs are
     // loaded into registers while the current one is scanned, so the loads of consecutive tiles
     // overlap (bandwidth regime) and a single tile per block is the latency regime of C2.
@@ -624,7 +626,7 @@ void fast_reduce_loss(cudaStream_t s, const float* loss_parts, int np, int nc, d
 
 void fast_gae(cudaStream_t s, const float* rew, const float* values, const float* done_f, const float* last_value,
               int64_t TR, int64_t R, double gamma, double lam, float* adv, float* ret, bool with_adv,
-              double* block_sums, double* stats, unsigned* done_counter) {
+              double* block_sums, double* stats, unsigned* done_counter, bool pdl) {
     // T = 32 with few streams (the episode: latency-bound): warp-shuffle reverse scan, lane = step.
     // Many streams (bandwidth-bound sweeps): the chunked thread-per-stream recurrence, which needs
     // no shuffles (the scan's 40 shuffles per stream would cap it at ~20% of HBM bandwidth).
@@ -633,8 +635,22 @@ void fast_gae(cudaStream_t s, const float* rew, const float* values, const float
     // streams HBM faster (2^26 rows: 5.1 vs 1.8 TB/s, bench.py hbm_kernels).
     if (TR == 32 * R && done_counter && R <= 65536) {
         const int nb32 = static_cast<int>(std::min<int64_t>((R + 31) / 32, 2 * 148));
-        k_gae_scan32<<<nb32, 1024, 0, s>>>(rew, values, done_f, last_value, R, gamma, lam, adv, ret, with_adv,
-                                           block_sums, stats, done_counter);
+        if (!pdl) {
+            k_gae_scan32<<<nb32, 1024, 0, s>>>(rew, values, done_f, last_value, R, gamma, lam, adv, ret, with_adv,
+                                               block_sums, stats, done_counter, false);
+            return;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(nb32));
+        cfg.blockDim = dim3(1024);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        FLW_CUDA(cudaLaunchKernelEx(&cfg, k_gae_scan32, rew, values, done_f, last_value, R, gamma, lam, adv, ret,
+                                    with_adv, block_sums, stats, done_counter, true));
         return;
     }
     const int nb = static_cast<int>((R + 255) / 256);
@@ -654,7 +670,7 @@ void fast_gae_scan32(cudaStream_t s, const float* rew, const float* values, cons
                      bool with_adv, double* block_sums, double* stats, unsigned* done_counter) {
     const int nb32 = static_cast<int>(std::min<int64_t>((R + 31) / 32, 2 * 148));
     k_gae_scan32<<<nb32, 1024, 0, s>>>(rew, values, done_f, last_value, R, gamma, lam, adv, ret, with_adv,
-                                       block_sums, stats, done_counter);
+                                       block_sums, stats, done_counter, false);
 }
 
 void fast_rep_adv_stats(cudaStream_t s, const float* adv, int64_t T, int64_t E, const int64_t* rep_off,

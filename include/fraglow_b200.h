@@ -60,6 +60,11 @@ typedef struct {
 int flw_program_create(const char* algo_json, const char* deploy_json, flw_program** out);
 void flw_program_destroy(flw_program* p);                              /* fraglow.h:44 */
 int flw_program_dump(const flw_program* p, int what, char** out_text); /* fraglow.h:46 */
+/* The seam's graph input: the dataflow graph JSON a reference worker receives
+ * (dfg::dump_json, graph.cpp:468-507; coordinator.cpp:75-84) of a PPO / MAPPO standard program
+ * -> the equivalent algo JSON (free with flw_string_free). flw_dpd_create and
+ * flw_dpd_create_replicas accept either JSON directly. */
+int flw_algo_from_graph(const char* graph_json, char** out_algo_json);
 int flw_validate_plan(const flw_program* p, char** out_report, int* n_violations); /* fraglow.h:49 */
 /* Replaces fraglow.h:55 / capi.cpp:249-265: runs every unit on its own GPU (one host thread per
  * unit, local_run.cpp:532-535), same CSV schema (episode,wall_ms,reward,bytes_total) and summary

@@ -213,11 +213,29 @@ int plan_cmd(const std::string& algo_path, const std::string& deploy_path) {
     return 0;
 }
 
+// ref_tool dfg <algo.json>: the dataflow graph JSON the reference ships to its workers
+// (flw_program_dump(FLW_DUMP_DFG) = dfg::dump_json, graph.cpp:468-507).
+int dfg_cmd(const std::string& algo_path) {
+    std::string a = slurp(algo_path);
+    flw_program* p = nullptr;
+    if (flw_program_create(a.c_str(), nullptr, &p) != 0) {
+        std::cerr << flw_last_error() << "\n";
+        return 1;
+    }
+    char* g = nullptr;
+    flw_program_dump(p, FLW_DUMP_DFG, &g);
+    std::cout << g << "\n";
+    flw_string_free(g);
+    flw_program_destroy(p);
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     try {
         if (argc >= 4 && std::string(argv[1]) == "plan") return plan_cmd(argv[2], argv[3]);
+        if (argc >= 3 && std::string(argv[1]) == "dfg") return dfg_cmd(argv[2]);
         if (argc >= 5 && std::string(argv[1]) == "trace")
             return trace(argv[2], std::stoull(argv[3]), argv[4]);
         if (argc >= 5 && std::string(argv[1]) == "run") {

@@ -51,6 +51,7 @@ def lib():
         "flw_program_create": (ci, [cs, cs, P(vp)]),
         "flw_program_destroy": (None, [vp]),
         "flw_program_dump": (ci, [vp, ci, P(vp)]),
+        "flw_algo_from_graph": (ci, [C.c_char_p, P(vp)]),
         "flw_validate_plan": (ci, [vp, P(vp), P(ci)]),
         "flw_run_local": (ci, [vp, P(RunOptions), P(vp), P(vp)]),
         "flw_string_free": (None, [vp]),

@@ -58,6 +58,13 @@ class Program:
         return N.take_string(csv), json.loads(N.take_string(summ))
 
 
+def algo_from_graph(graph) -> dict:
+    """flw_algo_from_graph: the algo config of a PPO / MAPPO dataflow-graph JSON (dfg::dump_json)."""
+    out = C.c_void_p()
+    N.check(N.lib().flw_algo_from_graph(_json(graph), C.byref(out)))
+    return json.loads(N.take_string(out))
+
+
 def microbench(which: str, n: int, iters: int = 10) -> tuple[float, float]:
     """flw_microbench: (ms per launch, algorithmic bytes per launch) of an element-wise kernel."""
     ms, nbytes = C.c_double(), C.c_double()
@@ -75,7 +82,10 @@ class DpdEngine:
     def __init__(self, algo, device: int = 0, seed: int = 0, env_lo: int = 0, env_hi: int | None = None,
                  env_total: int | None = None, numerics: str = "exact", replicas: int = 1):
         a = json.loads(algo) if isinstance(algo, str) else algo
-        total = int(a.get("env", {}).get("num", 1)) if env_total is None else env_total
+        if "nodes" in a:  # the dataflow-graph JSON (the seam's graph input): its env count
+            total = int(algo_from_graph(a)["env"]["num"]) if env_total is None else env_total
+        else:
+            total = int(a.get("env", {}).get("num", 1)) if env_total is None else env_total
         hi = total if env_hi is None else env_hi
         num = {"exact": N.FLW_NUMERICS_EXACT, "fast": N.FLW_NUMERICS_FAST}[numerics]
         self._h = C.c_void_p()

@@ -353,6 +353,14 @@ int flw_program_create(const char* algo_json, const char* deploy_json, flw_progr
 
 void flw_program_destroy(flw_program* p) { delete p; }
 
+int flw_algo_from_graph(const char* graph_json, char** out_algo_json) {
+    return guarded([&] {
+        if (!out_algo_json) fail(Errc::Config, "null output pointer");
+        *out_algo_json = dup_string(algo_to_json(algo_from_graph(graph_json ? graph_json : "{}")));
+        return FLW_OK;
+    });
+}
+
 int flw_program_dump(const flw_program* p, int what, char** out_text) {
     return guarded([&] {
         if (what != FLW_DUMP_PLAN)
@@ -394,7 +402,7 @@ const char* flw_last_error(void) { return g_last_error.c_str(); }
 int flw_dpd_create(const char* algo_json, int device, uint64_t seed, int64_t env_lo, int64_t env_hi,
                    int64_t env_total, int numerics, flw_dpd** out) {
     return guarded([&] {
-        AlgoConfig a = parse_algo_config(algo_json ? algo_json : "{}");
+        AlgoConfig a = parse_algo_or_graph(algo_json ? algo_json : "{}");
         if (numerics != FLW_NUMERICS_EXACT && numerics != FLW_NUMERICS_FAST) fail(Errc::Config, "bad numerics");
         auto h = std::make_unique<flw_dpd>();
         h->engine = std::make_unique<Engine>(a, device, seed, env_lo, env_hi, env_total, static_cast<Numerics>(numerics));
@@ -406,7 +414,7 @@ int flw_dpd_create(const char* algo_json, int device, uint64_t seed, int64_t env
 int flw_dpd_create_replicas(const char* algo_json, int device, uint64_t seed, int64_t env_lo, int64_t env_hi,
                             int64_t env_total, int numerics, int replicas, flw_dpd** out) {
     return guarded([&] {
-        AlgoConfig a = parse_algo_config(algo_json ? algo_json : "{}");
+        AlgoConfig a = parse_algo_or_graph(algo_json ? algo_json : "{}");
         if (numerics != FLW_NUMERICS_EXACT && numerics != FLW_NUMERICS_FAST) fail(Errc::Config, "bad numerics");
         auto h = std::make_unique<flw_dpd>();
         h->engine = std::make_unique<Engine>(a, device, seed, env_lo, env_hi, env_total, static_cast<Numerics>(numerics),

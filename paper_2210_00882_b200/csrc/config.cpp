@@ -81,6 +81,97 @@ static json parse_or_fail(const std::string& text) {
     }
 }
 
+// The seam's other input: the dataflow graph JSON a reference worker receives
+// (dfg::dump_json, graph.cpp:468-507) of a PPO or MAPPO standard program (programs.cpp:204-272,
+// 349-454) - its node attributes carry every hyper-parameter: EnvReset {env, num, ep_*},
+// xavier Param {pgroup, fan_in, fan_out} (the MLP widths), Tanh / Relu, GaeAdv {gamma, lam,
+// normalize}, PpoLoss {clip_eps, value_coef, entropy_coef}, OptimStep {lr, train_iters},
+// PolicyApply {rows_n} (MAPPO agents) and loop {episodes, steps_per_episode}.
+AlgoConfig algo_from_graph(const std::string& text) {
+    json g = parse_or_fail(text);
+    if (!g.contains("nodes") || !g["nodes"].is_array()) fail(Errc::Config, "graph JSON has no nodes array");
+    AlgoConfig c;
+    c.hidden.clear();
+    bool env = false, loss = false, optim = false, gae = false;
+    std::vector<int64_t> pol;  // policy layer widths: fan_in of layer 0, then every fan_out
+    try {
+        for (const auto& n : g["nodes"]) {
+            const std::string kind = n.at("kind").get<std::string>();
+            const json& a = n.contains("attrs") ? n["attrs"] : json::object();
+            if (kind == "EnvReset") {
+                env = true;
+                c.env_name = a.at("env").get<std::string>();
+                c.envs = a.at("num").get<int64_t>();
+                for (auto it = a.begin(); it != a.end(); ++it)
+                    if (it.key().rfind("ep_", 0) == 0 && it.key() != "ep_n_agents")
+                        c.env_params[it.key().substr(3)] = it.value().get<double>();
+            } else if (kind == "Param" && a.value("init", "") == "xavier" && a.value("pgroup", "") == "policy") {
+                if (pol.empty()) pol.push_back(a.at("fan_in").get<int64_t>());
+                pol.push_back(a.at("fan_out").get<int64_t>());
+            } else if (kind == "Relu") {
+                c.activation = "relu";
+            } else if (kind == "GaeAdv") {
+                gae = true;
+                c.gamma = a.at("gamma").get<double>();
+                c.lam = a.at("lam").get<double>();
+                c.normalize_adv = a.value("normalize", int64_t{1}) != 0;
+            } else if (kind == "PpoLoss") {
+                loss = true;
+                c.clip_eps = a.at("clip_eps").get<double>();
+                c.value_coef = a.at("value_coef").get<double>();
+                c.entropy_coef = a.at("entropy_coef").get<double>();
+            } else if (kind == "A3cLoss") {
+                fail(Errc::Config, "graph JSON input covers the PPO and MAPPO standard programs; pass an A3C "
+                                   "program as its algo JSON");
+            } else if (kind == "OptimStep") {
+                optim = true;
+                c.lr = a.at("lr").get<double>();
+                c.train_iters = a.at("train_iters").get<int64_t>();
+            } else if (kind == "PolicyApply") {
+                c.agents = a.value("rows_n", int64_t{1});
+            }
+        }
+        if (g.contains("loop")) {
+            c.episodes = g["loop"].value("episodes", c.episodes);
+            c.steps_per_episode = g["loop"].value("steps_per_episode", c.steps_per_episode);
+        }
+    } catch (const json::exception& e) {
+        fail(Errc::Config, std::string("graph JSON: ") + e.what());
+    }
+    if (!env || !loss || !optim || !gae || pol.size() < 2)
+        fail(Errc::Config, "graph JSON is not a PPO / MAPPO standard program (EnvReset, xavier policy Params, "
+                           "GaeAdv, PpoLoss, OptimStep expected)");
+    c.algorithm = c.agents > 1 ? "mappo" : "ppo";
+    c.hidden.assign(pol.begin() + 1, pol.end() - 1);  // [obs, h1 .. hL-1, actions]
+    c.validate();
+    return c;
+}
+
+std::string algo_to_json(const AlgoConfig& c) {
+    nlohmann::ordered_json j;
+    j["algorithm"] = c.algorithm;
+    j["agent"] = {{"num", c.agents}};
+    j["actor"] = {{"num", c.actors}};
+    nlohmann::ordered_json e = {{"type", c.env_name}, {"num", c.envs}};
+    if (!c.env_params.empty()) e["params"] = c.env_params;
+    j["env"] = e;
+    j["learner"] = {{"params", {{"gamma", c.gamma}, {"lam", c.lam}, {"clip_eps", c.clip_eps}, {"lr", c.lr},
+                                {"train_iters", c.train_iters}, {"value_coef", c.value_coef},
+                                {"entropy_coef", c.entropy_coef}, {"normalize_adv", c.normalize_adv}}}};
+    j["policy_net"] = {{"hidden", c.hidden}, {"activation", c.activation}};
+    j["loop"] = {{"episodes", c.episodes}, {"steps_per_episode", c.steps_per_episode}};
+    return j.dump();
+}
+
+AlgoConfig parse_algo_or_graph(const std::string& text) {
+    const auto p = text.find_first_not_of(" \t\r\n");
+    if (p != std::string::npos && text[p] == '{' && text.find("\"nodes\"") != std::string::npos) {
+        json j = json::parse(text, nullptr, false);
+        if (!j.is_discarded() && j.is_object() && j.contains("nodes")) return algo_from_graph(text);
+    }
+    return parse_algo_config(text);
+}
+
 AlgoConfig parse_algo_config(const std::string& text) {  // config.cpp:24-63
     json j = parse_or_fail(text);
     AlgoConfig c;

@@ -48,6 +48,11 @@ struct AlgoConfig {
 };
 
 AlgoConfig parse_algo_config(const std::string& json_text);
+// the dataflow graph JSON of a PPO / MAPPO standard program (dfg::dump_json) -> its algo config
+AlgoConfig algo_from_graph(const std::string& graph_json);
+std::string algo_to_json(const AlgoConfig& c);
+// algo JSON, or graph JSON when the object has a "nodes" array (the seam accepts either)
+AlgoConfig parse_algo_or_graph(const std::string& text);
 
 struct DeployConfig {
     std::vector<std::string> workers = {"local"};

@@ -142,5 +142,45 @@ def main():
             print("run", name, r["units"], "units", r["steps"], "steps")
 
 
+# dataflow-graph JSON (flw_program_dump(FLW_DUMP_DFG) = dfg::dump_json) of standard programs, with
+# every algo field explicit: the seam's graph input (tests/test_capi_cpu.py test_algo_from_graph)
+def _full(algorithm, agents, env, envs, params, hidden, act, hyper, loop):
+    return {"algorithm": algorithm, "agent": {"num": agents}, "actor": {"num": 1},
+            "env": {"type": env, "num": envs, **({"params": params} if params else {})},
+            "learner": {"params": hyper}, "policy_net": {"hidden": hidden, "activation": act}, "loop": loop}
+
+
+DFG_CASES = {
+    "ppo_synth_c2": _full("ppo", 1, "synth17x6", 4096, None, [64] * 6, "tanh",
+                          {"gamma": 0.97, "lam": 0.95, "clip_eps": 0.2, "lr": 3e-3, "train_iters": 4,
+                           "value_coef": 0.5, "entropy_coef": 0.01, "normalize_adv": True},
+                          {"episodes": 10, "steps_per_episode": 32}),
+    "ppo_gridline_relu": _full("ppo", 1, "gridline", 40, {"length": 12.0}, [32, 16], "relu",
+                               {"gamma": 0.9, "lam": 0.8, "clip_eps": 0.3, "lr": 5e-3, "train_iters": 2,
+                                "value_coef": 0.25, "entropy_coef": 0.0, "normalize_adv": False},
+                               {"episodes": 3, "steps_per_episode": 16}),
+    "mappo_spread3": _full("mappo", 3, "spread_lite", 16, None, [32, 32], "tanh",
+                           {"gamma": 0.99, "lam": 0.9, "clip_eps": 0.1, "lr": 1e-3, "train_iters": 3,
+                            "value_coef": 1.0, "entropy_coef": 0.02, "normalize_adv": True},
+                           {"episodes": 2, "steps_per_episode": 8}),
+}
+
+
+def make_dfg():
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, algo in DFG_CASES.items():
+            ap = os.path.join(tmp, name + ".json")
+            json.dump(algo, open(ap, "w"))
+            g = subprocess.run([pyoracle.REF_TOOL, "dfg", ap], check=True, capture_output=True, text=True).stdout
+            out[name] = {"algo": algo, "graph": json.loads(g)}
+    json.dump(out, open(os.path.join(HERE, "dfg.json"), "w"))
+    print("dfg", len(out))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["dfg"]:
+        build_ref()
+        make_dfg()
+    else:
+        main()

@@ -104,3 +104,33 @@ def test_deploy_extension_keys_are_accepted_and_validated():
                        "numerics": "fast", "replicas_per_gpu": 2, "exchange": "nccl"})
     # the plan itself is the reference's (the extension keys only steer the engine)
     assert len(json.loads(p.dump())["instances"]) == 4
+
+
+def test_algo_from_graph_recovers_the_algo_config():
+    """The seam's graph input: the reference's own dataflow-graph JSON of a PPO / MAPPO
+    standard program (tests/golden/dfg.json, dumped by oracle/_ref via flw_program_dump(DFG))
+    translates back to exactly the algo config it was built from."""
+    from paper_2210_00882_b200.api import algo_from_graph
+
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "dfg.json")))
+    assert len(cases) == 3
+    for name, c in cases.items():
+        got, want = algo_from_graph(c["graph"]), c["algo"]
+        assert got["algorithm"] == want["algorithm"], name
+        assert got["agent"]["num"] == want["agent"]["num"], name
+        assert got["env"]["type"] == want["env"]["type"] and got["env"]["num"] == want["env"]["num"], name
+        assert got["env"].get("params", {}) == {k: float(v) for k, v in want["env"].get("params", {}).items()}, name
+        assert got["policy_net"] == want["policy_net"], name
+        assert got["learner"]["params"] == want["learner"]["params"], name
+        assert got["loop"] == want["loop"], name
+
+
+def test_algo_from_graph_refuses_what_it_cannot_read():
+    from paper_2210_00882_b200.api import algo_from_graph
+
+    with pytest.raises(FlwError, match="nodes"):
+        algo_from_graph({"edges": []})
+    with pytest.raises(FlwError, match="standard program"):
+        algo_from_graph({"nodes": [{"id": 0, "kind": "Input", "attrs": {}}]})
+    with pytest.raises(FlwError, match="A3C"):
+        algo_from_graph({"nodes": [{"id": 0, "kind": "A3cLoss", "attrs": {}}]})

@@ -271,3 +271,20 @@ def test_degenerate_advantages_skip_normalisation():
     np.testing.assert_array_equal(ex.get("grads"), g_o)
     np.testing.assert_array_equal(ex.get("loss"), u.get("loss"))
     np.testing.assert_allclose(fa.get("adv"), want_adv, rtol=1e-6)
+
+
+@pytest.mark.parametrize("case,numerics", [("ppo_gridline_relu", "exact"), ("ppo_gridline_relu", "fast"),
+                                           ("ppo_synth_c2", "fast")])
+def test_engine_from_graph_json_equals_algo_json(case, numerics):
+    """flw_dpd_create given the reference's dataflow-graph JSON (the bundle a worker receives,
+    SURVEY §8b) runs the same program as given the algo JSON: identical rewards and params."""
+    _need_gpu()
+    from paper_2210_00882_b200 import DpdEngine
+
+    c = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "dfg.json")))[case]
+    a = DpdEngine(c["algo"], seed=3, numerics=numerics)
+    b = DpdEngine(c["graph"], seed=3, numerics=numerics)
+    ra = [a.run_episode(ep)[0] for ep in range(2)]
+    rb = [b.run_episode(ep)[0] for ep in range(2)]
+    assert ra == rb
+    np.testing.assert_array_equal(a.params(), b.params())
